@@ -1,0 +1,224 @@
+/*
+ * heatfem.h -- C ABI of libheatfem.so, the B200 (sm_100a) hot path of arXiv 1905.07622,
+ * "assembly-free FEM for transient heat flow through heterogeneous material".
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (section / equation / algorithm noted);
+ * readings Rn = DESIGN.md section "Readings of the paper".
+ *
+ * Discretisation (§3.1, §3.2).  A structured voxel grid of ne[0] x ne[1] x ne[2]
+ * trilinear hexahedra (reading R1; the paper's 6-tet split is not used) with spacing h and min
+ * corner origin.  Each element e carries a conductivity k_e and a capacity c_e = (rho C)_e,
+ * constant over the element.  The library never assembles a matrix; every operator
+ * is applied element by element (Eq. (1)):
+ *      y = sum_e A_e^T ( aK k_e K_ref + aM c_e M_ref ) A_e u
+ * with (aK, aM) = (theta dt, 1) for A = M + theta dt K and (-(1-theta) dt, 1) for
+ * L = M - (1-theta) dt K (reading R8), (1, 0) for K and (0, 1) for M.
+ *
+ * Layout.  Node (i,j,k) -> i + (ne0+1) * (j + (ne1+1) * k) (x fastest);
+ * element (ex,ey,ez) -> ex + ne0 * (ey + ne1 * ez).  All vectors are fp64.
+ *
+ * Pointers.  Array arguments may be device pointers (on the context's device) or host
+ * pointers (pageable or pinned); host arrays are staged through context-owned device
+ * memory on the context stream.  Device arrays are borrowed for the duration of the call.
+ *
+ * Streams.  All device work is enqueued on the context stream (the one passed to
+ * hf_create, or a library-owned stream if NULL).  hf_apply*, hf_diag and hf_face_load are
+ * asynchronous when every array is on the device; calls that return host results
+ * (hf_cg, hf_simulate*, hf_get_*) synchronise the context stream.
+ *
+ * Errors.  Every call returns an hf_status; on failure hf_last_error() returns a
+ * thread-local message.  No C++ exception crosses this boundary.  Non-convergence is a
+ * reported status, never a crash.
+ */
+#ifndef HEATFEM_H
+#define HEATFEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t hf_status;
+#define HF_OK 0
+#define HF_E_ARG (-1)        /* bad argument (NULL, size, value, dtype)                        */
+#define HF_E_INDEX (-2)      /* index out of range                                              */
+#define HF_E_NOCONV (-3)     /* PCG hit max_iter; x holds the last iterate, info is filled       */
+#define HF_E_BREAKDOWN (-4)  /* d^T q <= 0 or non-finite (operator not SPD, or NaN input)         */
+#define HF_E_PARTITION (-5)  /* slab decomposition impossible (fewer than 2 node planes per rank) */
+#define HF_E_CUDA (-6)       /* CUDA runtime error (message has the CUDA error string)           */
+#define HF_E_NCCL (-7)       /* NCCL unavailable or failed                                       */
+#define HF_E_OOM (-8)        /* device allocation failed                                         */
+#define HF_E_STATE (-9)      /* call out of order (e.g. hf_cg before hf_set_coefficients)        */
+
+/* Grid: elements per axis, spacing (mm), min corner (mm).  (§4.1; Appendix C,
+ * vert_scale P:408-409.) */
+typedef struct {
+    int64_t ne[3];
+    double h[3];
+    double origin[3];
+} hf_grid;
+
+/* PCG options (Alg. 1).  rtol: stop when ||r||_2 <= rtol ||b_F||_2 (reading R4);
+ * max_iter: i_max (reading R10); replace_every: the "i divisible by 50" true-residual
+ * replacement period of Alg. 1 line 9 (reading R6; 0 disables). */
+typedef struct {
+    double rtol;          /* default 1e-12 */
+    int32_t max_iter;     /* default 10000 */
+    int32_t replace_every;/* default 50 */
+} hf_cg_opts;
+
+typedef struct {
+    int32_t iters;        /* PCG iterations performed                                          */
+    int32_t status;       /* HF_OK, HF_E_NOCONV or HF_E_BREAKDOWN                              */
+    double relres;        /* ||r||_2 / ||b_F||_2 of the recurrence residual (0 if b_F = 0)     */
+    double delta;         /* final delta = r^T P^{-1} r                                         */
+} hf_cg_info;
+
+typedef struct {
+    int32_t steps_done;     /* time steps completed                                            */
+    int32_t total_iters;    /* sum of PCG iterations over the steps                            */
+    int32_t max_iters_step; /* largest PCG iteration count of one step                         */
+    int32_t first_failed_step; /* -1 if every step converged                                  */
+    double ms_total;        /* device time of the call (CUDA events on the context stream)     */
+} hf_sim_stats;
+
+typedef struct hf_ctx hf_ctx;
+
+/* Library version string (static storage). */
+const char *hf_version(void);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char *hf_last_error(void);
+
+/* Create a context for grid g on CUDA device `device`.  cuda_stream: a cudaStream_t on that
+ * device, or NULL for a library-owned stream.  *out receives the context.
+ * Errors: HF_E_ARG (ne < 1, h <= 0, NULL out), HF_E_CUDA, HF_E_OOM. */
+hf_status hf_create(const hf_grid *g, int device, void *cuda_stream, hf_ctx **out);
+
+/* Destroy a context and free everything it owns (NULL is a no-op). */
+void hf_destroy(hf_ctx *ctx);
+
+/* Set the per-element coefficients (P:61, P:70 A_e = (rho C)_e M_e + theta dt k_e K_e).
+ * k_elem, c_elem: n_elements fp64 each (element layout above), copied into context memory.
+ * In slab mode the arrays cover the GLOBAL grid.  Errors: HF_E_ARG (NULL), HF_E_CUDA. */
+hf_status hf_set_coefficients(hf_ctx *ctx, const double *k_elem, const double *c_elem);
+
+/* Dirichlet faces (extension, reading R3).  face_bits bit f (f = 0..5 for -x,+x,-y,+y,-z,+z)
+ * marks face f as Dirichlet with value values[f] (values may be NULL = all 0).  A node on
+ * several flagged faces takes the value of the lowest-numbered one.  Affects hf_diag, hf_cg
+ * and hf_simulate*; hf_apply is always the unconstrained operator. */
+hf_status hf_set_dirichlet_faces(hf_ctx *ctx, uint32_t face_bits, const double values[6]);
+
+/* Flux load F_i = int_face f phi_i ds over face `face` (0..5) (P:44, P:50-52 boundary term):
+ * f = f_const + beam, beam(a,b) = P/(2 pi s^2) exp(-((a-ca)^2 + (b-cb)^2) / (2 s^2)) with
+ * beam = {P, s, ca, cb} (or NULL), (a, b) the face's in-plane coordinates in increasing axis
+ * order (reading R12).  2x2 Gauss quadrature per boundary quad.  F: n_nodes fp64, written
+ * entirely (zero off the face).  Errors: HF_E_ARG (face, NULL F). */
+hf_status hf_face_load(hf_ctx *ctx, int face, double f_const, const double beam[4], double *F);
+
+/* y = (aK K + aM M) u, the element-by-element apply of Eq. (1) (Impl. 3 role,
+ * P:210-245).  u, y: n_nodes fp64, must not alias.  Unconstrained (no Dirichlet rows). */
+hf_status hf_apply(hf_ctx *ctx, double aK, double aM, const double *u, double *y);
+
+/* y = c (aK K + aM M) u + b  (the paper's FGDbDMVM_C).  b may be NULL (= 0);
+ * b may alias y. */
+hf_status hf_apply_axpby(hf_ctx *ctx, double aK, double aM, double c, const double *u,
+                         const double *b, double *y);
+
+/* Jacobi diagonal diag_i = sum_{e ni i} (aK k_e K_ref[l,l] + aM c_e M_ref[l,l]) (P:117,
+ * Jacobi_A P:659-662); 1 on Dirichlet rows (reading R3).  diag: n_nodes fp64. */
+hf_status hf_diag(hf_ctx *ctx, double aK, double aM, double *diag);
+
+/* Solve (P_F A P_F + P_D) x = b by Jacobi PCG, Algorithm 1, A = aK K + aM M.
+ * b must already carry the Dirichlet lift (b_D = g_D); x: in initial guess, out solution
+ * (x_D is set to b_D).  opts NULL -> defaults.  info may be NULL.  Synchronises.
+ * Returns HF_OK, HF_E_NOCONV (x = last iterate) or HF_E_BREAKDOWN. */
+hf_status hf_cg(hf_ctx *ctx, double aK, double aM, const double *b, double *x,
+                const hf_cg_opts *opts, hf_cg_info *info);
+
+/* theta-scheme time loop: for n = 0..nsteps-1 solve
+ *   [M + theta dt K] u^{n+1} = [M - (1-theta) dt K] u^n + dt F   (readings R7, R8)
+ * with Dirichlet lift (R3) and guess x0 = u^0 at n = 0, else 2 u^n - u^{n-1} (u0_update,
+ * P:575-589, reading R9).  u: in u^0 (Dirichlet nodes are overwritten with g), out u^nsteps.
+ * F: n_nodes (the flux load, NOT pre-multiplied by dt) or NULL (= 0).
+ * snap: NULL, or nsteps x n_plane fp64 receiving plane z = snap_plane (0 = front face) of
+ * u^{n+1} after every step.  Synchronises once at the end.  Returns the first failing
+ * step's status (HF_E_NOCONV / HF_E_BREAKDOWN) with stats->first_failed_step set, u then
+ * holding that step's last iterate. */
+hf_status hf_simulate(hf_ctx *ctx, double theta, double dt, int32_t nsteps, const double *F,
+                      double *u, int64_t snap_plane, double *snap, const hf_cg_opts *opts,
+                      hf_sim_stats *stats);
+
+/* Checkpoint / resume of the time loop (the stepper state is (u^n, u^{n-1}, n)): same as
+ * hf_simulate without snapshots, but the guess of the first step is 2 u - u_prev when
+ * step0 > 0 (u_prev required then).  On return u = u^{n+nsteps} and, if u_prev is non-NULL,
+ * u_prev = u^{n+nsteps-1}, ready for the next call. */
+hf_status hf_simulate_resume(hf_ctx *ctx, double theta, double dt, int32_t nsteps, const double *F,
+                             double *u, double *u_prev, int64_t step0, const hf_cg_opts *opts,
+                             hf_sim_stats *stats);
+
+/* B independent forward simulations on the context's grid (P:345-365 inverse problem; the
+ * paper's "rapid successive solutions").  k_batch: B x n_elements; c_batch: B x n_elements
+ * or NULL (= the context's c for every system); F: n_nodes shared load; u_batch: B x n_nodes
+ * (in u^0, out u^nsteps); front_out: NULL or B x n_plane receiving plane snap_plane of
+ * u^nsteps per system; stats: B entries (may be NULL).  Systems are independent: each has
+ * its own PCG scalars and convergence.  Returns the first failing status (others run on). */
+hf_status hf_simulate_batched(hf_ctx *ctx, int32_t B, const double *k_batch,
+                              const double *c_batch, double theta, double dt, int32_t nsteps,
+                              const double *F, double *u_batch, int64_t snap_plane,
+                              double *front_out, const hf_cg_opts *opts, hf_sim_stats *stats);
+
+/* ---- multi-GPU z-slabs (§4.4, generalised to R ranks) ---------- */
+
+/* Owned node planes [z_lo, z_hi) of rank `rank` out of `nranks` for a grid with nz1 node
+ * planes: contiguous, sizes differ by at most one.  Pure host function (no device).
+ * Errors: HF_E_PARTITION if nz1 < 2 * nranks, HF_E_ARG otherwise-bad input. */
+hf_status hf_slab_plan(int64_t nz1, int32_t rank, int32_t nranks, int64_t *z_lo, int64_t *z_hi);
+
+/* 128-byte NCCL unique id for hf_create_slab (call on one rank, broadcast the bytes).
+ * Loads libnccl.so.2 at run time.  Errors: HF_E_NCCL. */
+hf_status hf_nccl_unique_id(uint8_t id[128]);
+
+/* Slab context of rank `rank` of `nranks` for the GLOBAL grid g.  Vectors passed to a slab
+ * context cover the rank's LOCAL planes: owned planes [z_lo, z_hi) plus one ghost plane on
+ * each interior side (hf_slab_range).  Ghost entries of outputs are kept consistent by the
+ * library; dot products run over owned nodes only.  transport: 0 = NCCL (one process
+ * per GPU, id from hf_nccl_unique_id), 1 = in-process (all ranks in one process, one thread
+ * each, possibly on one device; `id` must then be the same hf_local_group pointer cast to
+ * uint8_t*).  The call blocks until every rank has joined. */
+hf_status hf_create_slab(const hf_grid *g, int32_t rank, int32_t nranks, const uint8_t *id,
+                         int32_t transport, int device, void *cuda_stream, hf_ctx **out);
+
+/* In-process transport group for `nranks` ranks (transport 1 of hf_create_slab). */
+typedef struct hf_local_group hf_local_group;
+hf_status hf_local_group_create(int32_t nranks, hf_local_group **out);
+void hf_local_group_destroy(hf_local_group *grp);
+
+/* Global node planes [z_lo, z_hi) owned by this context, and the local plane count
+ * (owned + ghosts) and the global index of local plane 0. */
+hf_status hf_slab_range(const hf_ctx *ctx, int64_t *z_lo, int64_t *z_hi, int64_t *local_planes,
+                        int64_t *local_z0);
+
+/* ---- introspection used by tests and bench.py ----------------------------------------- */
+
+/* Number of this library's kernels launched on the context so far (device counter). */
+hf_status hf_get_launch_count(hf_ctx *ctx, int64_t *count);
+
+/* Per-kernel-class timing (CUDA events around each launch; slows the loop slightly).
+ * enable = 1 turns it on and clears totals.  Classes: 0 apply/stencil CG kernel A,
+ * 1 pointwise kernel B, 2 residual kernel, 3 rhs, 4 other.  ms[c] total ms, n[c] launches. */
+hf_status hf_profile(hf_ctx *ctx, int32_t enable);
+hf_status hf_profile_read(hf_ctx *ctx, double ms[5], int64_t n[5]);
+
+/* Loop driver: 0 = CUDA graph with device-side WHILE loop (default), 1 = host loop.
+ * Profiling (hf_profile) and the in-process slab transport always use the host loop. */
+hf_status hf_set_driver(hf_ctx *ctx, int32_t driver);
+
+/* Enqueue a 512 MiB memset on the context stream (evicts the 126 MB L2; bench timing rule). */
+hf_status hf_flush_l2(hf_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEATFEM_H */

@@ -1,0 +1,345 @@
+"""Python binding of libheatfem.so -- the B200 hot path of arXiv 1905.07622.
+
+Thin ctypes marshalling over the C ABI of ``include/heatfem.h`` with the SAME function
+names.  Every computation runs in the library's sm_100a kernels; this module only checks
+dtypes/sizes and passes pointers.  There is no CPU fallback: importing fails loudly when
+the shared library is missing (build it with ``python -m paper_1905_07622_b200._build``).
+
+Arrays may be torch tensors (CUDA or CPU) or numpy arrays, float64 and contiguous.  CUDA
+tensors are passed by device pointer on the current torch stream; host arrays are staged
+by the library itself.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libheatfem.so")
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"libheatfem.so not built ({_LIB_PATH}); run python -m paper_1905_07622_b200._build")
+
+HF_OK, HF_E_ARG, HF_E_INDEX, HF_E_NOCONV, HF_E_BREAKDOWN = 0, -1, -2, -3, -4
+HF_E_PARTITION, HF_E_CUDA, HF_E_NCCL, HF_E_OOM, HF_E_STATE = -5, -6, -7, -8, -9
+FACE_XM, FACE_XP, FACE_YM, FACE_YP, FACE_ZM, FACE_ZP = range(6)
+
+
+class HfError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"heatfem status {status}: {msg}")
+        self.status = status
+
+
+class hf_grid(C.Structure):
+    _fields_ = [("ne", C.c_int64 * 3), ("h", C.c_double * 3), ("origin", C.c_double * 3)]
+
+
+class hf_cg_opts(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int32), ("replace_every", C.c_int32)]
+
+
+class hf_cg_info(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("status", C.c_int32), ("relres", C.c_double), ("delta", C.c_double)]
+
+
+class hf_sim_stats(C.Structure):
+    _fields_ = [("steps_done", C.c_int32), ("total_iters", C.c_int32), ("max_iters_step", C.c_int32),
+                ("first_failed_step", C.c_int32), ("ms_total", C.c_double)]
+
+
+_lib = C.CDLL(_LIB_PATH)
+_vp, _dp, _i32, _i64, _d = C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_double
+_P = C.POINTER
+
+_SIGS = {
+    "hf_version": (C.c_char_p, []),
+    "hf_last_error": (C.c_char_p, []),
+    "hf_create": (_i32, [_P(hf_grid), C.c_int, _vp, _P(_vp)]),
+    "hf_destroy": (None, [_vp]),
+    "hf_set_coefficients": (_i32, [_vp, _dp, _dp]),
+    "hf_set_dirichlet_faces": (_i32, [_vp, C.c_uint32, _P(C.c_double * 6)]),
+    "hf_face_load": (_i32, [_vp, C.c_int, _d, _P(C.c_double * 4), _dp]),
+    "hf_apply": (_i32, [_vp, _d, _d, _dp, _dp]),
+    "hf_apply_axpby": (_i32, [_vp, _d, _d, _d, _dp, _dp, _dp]),
+    "hf_diag": (_i32, [_vp, _d, _d, _dp]),
+    "hf_cg": (_i32, [_vp, _d, _d, _dp, _dp, _P(hf_cg_opts), _P(hf_cg_info)]),
+    "hf_simulate": (_i32, [_vp, _d, _d, _i32, _dp, _dp, _i64, _dp, _P(hf_cg_opts), _P(hf_sim_stats)]),
+    "hf_simulate_resume": (_i32, [_vp, _d, _d, _i32, _dp, _dp, _dp, _i64, _P(hf_cg_opts), _P(hf_sim_stats)]),
+    "hf_simulate_batched": (_i32, [_vp, _i32, _dp, _dp, _d, _d, _i32, _dp, _dp, _i64, _dp, _P(hf_cg_opts),
+                                   _P(hf_sim_stats)]),
+    "hf_slab_plan": (_i32, [_i64, _i32, _i32, _P(_i64), _P(_i64)]),
+    "hf_nccl_unique_id": (_i32, [C.c_char_p]),
+    "hf_create_slab": (_i32, [_P(hf_grid), _i32, _i32, _vp, _i32, C.c_int, _vp, _P(_vp)]),
+    "hf_local_group_create": (_i32, [_i32, _P(_vp)]),
+    "hf_local_group_destroy": (None, [_vp]),
+    "hf_slab_range": (_i32, [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)]),
+    "hf_get_launch_count": (_i32, [_vp, _P(_i64)]),
+    "hf_profile": (_i32, [_vp, _i32]),
+    "hf_profile_read": (_i32, [_vp, _P(C.c_double * 5), _P(C.c_int64 * 5)]),
+    "hf_set_driver": (_i32, [_vp, _i32]),
+    "hf_flush_l2": (_i32, [_vp]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+ABI_FUNCTIONS = tuple(_SIGS)
+
+
+def _check(st: int):
+    if st != HF_OK:
+        raise HfError(st, _lib.hf_last_error().decode())
+
+
+def _ptr(a, n: Optional[int] = None, name: str = "array", allow_none: bool = False):
+    """Pointer of a float64 contiguous torch tensor / numpy array (size check only)."""
+    if a is None:
+        if allow_none:
+            return None
+        raise HfError(HF_E_ARG, f"{name} is None")
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.dtype != torch.float64 or not a.is_contiguous():
+                raise HfError(HF_E_ARG, f"{name}: need a contiguous float64 tensor")
+            if n is not None and a.numel() != n:
+                raise HfError(HF_E_ARG, f"{name}: {a.numel()} entries, expected {n}")
+            return a.data_ptr()
+    except ImportError:
+        pass
+    import numpy as np
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise HfError(HF_E_ARG, f"{name}: need a C-contiguous float64 array")
+        if n is not None and a.size != n:
+            raise HfError(HF_E_ARG, f"{name}: {a.size} entries, expected {n}")
+        return a.ctypes.data
+    raise HfError(HF_E_ARG, f"{name}: unsupported type {type(a)}")
+
+
+def _stream(stream, device: int):
+    if stream is not None:
+        return stream
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_stream(device).cuda_stream
+    except ImportError:
+        pass
+    return None
+
+
+def _opts(rtol, max_iter, replace_every):
+    return hf_cg_opts(rtol, max_iter, replace_every)
+
+
+def make_grid(grid) -> hf_grid:
+    """hf_grid from an object with ne/h/origin attributes, or a (ne, h[, origin]) tuple."""
+    if isinstance(grid, hf_grid):
+        return grid
+    if hasattr(grid, "ne"):
+        ne, h, origin = grid.ne, grid.h, getattr(grid, "origin", (0.0, 0.0, 0.0))
+    else:
+        ne, h = grid[0], grid[1]
+        origin = grid[2] if len(grid) > 2 else (0.0, 0.0, 0.0)
+    return hf_grid((C.c_int64 * 3)(*ne), (C.c_double * 3)(*h), (C.c_double * 3)(*origin))
+
+
+class Context:
+    """An hf_ctx* plus the sizes the binding checks against."""
+
+    def __init__(self, ptr, grid: hf_grid, device: int, local_planes: int):
+        self.ptr = C.c_void_p(ptr)
+        self.grid = grid
+        self.device = device
+        self.ne = tuple(grid.ne)
+        self.n_elems = self.ne[0] * self.ne[1] * self.ne[2]
+        self.n_plane = (self.ne[0] + 1) * (self.ne[1] + 1)
+        self.n_nodes = self.n_plane * local_planes   # local (slab) node count
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and self.ptr.value:
+            _lib.hf_destroy(self.ptr)
+            self.ptr = C.c_void_p(None)
+
+
+# ---- C ABI, same names ---------------------------------------------------------------------
+
+def hf_version() -> str:
+    return _lib.hf_version().decode()
+
+
+def hf_last_error() -> str:
+    return _lib.hf_last_error().decode()
+
+
+def hf_create(grid, device: int = 0, stream=None) -> Context:
+    g = make_grid(grid)
+    out = C.c_void_p()
+    _check(_lib.hf_create(C.byref(g), device, _stream(stream, device), C.byref(out)))
+    return Context(out.value, g, device, g.ne[2] + 1)
+
+
+def hf_destroy(ctx: Context):
+    if ctx.ptr.value:
+        _lib.hf_destroy(ctx.ptr)
+        ctx.ptr = C.c_void_p(None)
+
+
+def hf_set_coefficients(ctx: Context, k, c):
+    _check(_lib.hf_set_coefficients(ctx.ptr, _ptr(k, ctx.n_elems, "k"), _ptr(c, ctx.n_elems, "c")))
+
+
+def hf_set_dirichlet_faces(ctx: Context, face_bits: int, values: Optional[Sequence[float]] = None):
+    v = (C.c_double * 6)(*(values if values is not None else (0.0,) * 6))
+    _check(_lib.hf_set_dirichlet_faces(ctx.ptr, face_bits, C.byref(v)))
+
+
+def hf_face_load(ctx: Context, face: int, f_const: float, beam, F):
+    b = None if beam is None else C.byref((C.c_double * 4)(*beam))
+    _check(_lib.hf_face_load(ctx.ptr, face, f_const, b, _ptr(F, ctx.n_nodes, "F")))
+
+
+def hf_apply(ctx: Context, aK: float, aM: float, u, y):
+    _check(_lib.hf_apply(ctx.ptr, aK, aM, _ptr(u, ctx.n_nodes, "u"), _ptr(y, ctx.n_nodes, "y")))
+
+
+def hf_apply_axpby(ctx: Context, aK: float, aM: float, c: float, u, b, y):
+    _check(_lib.hf_apply_axpby(ctx.ptr, aK, aM, c, _ptr(u, ctx.n_nodes, "u"),
+                               _ptr(b, ctx.n_nodes, "b", allow_none=True), _ptr(y, ctx.n_nodes, "y")))
+
+
+def hf_diag(ctx: Context, aK: float, aM: float, diag):
+    _check(_lib.hf_diag(ctx.ptr, aK, aM, _ptr(diag, ctx.n_nodes, "diag")))
+
+
+def hf_cg(ctx: Context, aK: float, aM: float, b, x, rtol=1e-12, max_iter=10000, replace_every=50,
+          raise_on_noconv: bool = True) -> dict:
+    info = hf_cg_info()
+    o = _opts(rtol, max_iter, replace_every)
+    st = _lib.hf_cg(ctx.ptr, aK, aM, _ptr(b, ctx.n_nodes, "b"), _ptr(x, ctx.n_nodes, "x"), C.byref(o), C.byref(info))
+    res = {"iters": info.iters, "status": info.status, "relres": info.relres, "delta": info.delta}
+    if st != HF_OK and (raise_on_noconv or st not in (HF_E_NOCONV, HF_E_BREAKDOWN)):
+        _check(st)
+    res["rc"] = st
+    return res
+
+
+def _stats(s: hf_sim_stats) -> dict:
+    return {"steps_done": s.steps_done, "total_iters": s.total_iters, "max_iters_step": s.max_iters_step,
+            "first_failed_step": s.first_failed_step, "ms_total": s.ms_total}
+
+
+def hf_simulate(ctx: Context, theta: float, dt: float, nsteps: int, F, u, snap_plane: int = -1, snap=None,
+                rtol=1e-12, max_iter=10000, replace_every=50, raise_on_noconv: bool = True) -> dict:
+    s = hf_sim_stats()
+    o = _opts(rtol, max_iter, replace_every)
+    st = _lib.hf_simulate(ctx.ptr, theta, dt, nsteps, _ptr(F, ctx.n_nodes, "F", allow_none=True),
+                          _ptr(u, ctx.n_nodes, "u"), snap_plane,
+                          _ptr(snap, nsteps * ctx.n_plane, "snap", allow_none=True), C.byref(o), C.byref(s))
+    res = _stats(s)
+    if st != HF_OK and (raise_on_noconv or st not in (HF_E_NOCONV, HF_E_BREAKDOWN)):
+        _check(st)
+    res["rc"] = st
+    return res
+
+
+def hf_simulate_resume(ctx: Context, theta: float, dt: float, nsteps: int, F, u, u_prev, step0: int,
+                       rtol=1e-12, max_iter=10000, replace_every=50) -> dict:
+    s = hf_sim_stats()
+    o = _opts(rtol, max_iter, replace_every)
+    _check(_lib.hf_simulate_resume(ctx.ptr, theta, dt, nsteps, _ptr(F, ctx.n_nodes, "F", allow_none=True),
+                                   _ptr(u, ctx.n_nodes, "u"), _ptr(u_prev, ctx.n_nodes, "u_prev", allow_none=True),
+                                   step0, C.byref(o), C.byref(s)))
+    return _stats(s)
+
+
+def hf_simulate_batched(ctx: Context, B: int, k_batch, c_batch, theta: float, dt: float, nsteps: int, F, u_batch,
+                        snap_plane: int = -1, front_out=None, rtol=1e-12, max_iter=10000, replace_every=50) -> list:
+    stats = (hf_sim_stats * max(B, 1))()
+    o = _opts(rtol, max_iter, replace_every)
+    _check(_lib.hf_simulate_batched(ctx.ptr, B, _ptr(k_batch, B * ctx.n_elems, "k_batch"),
+                                    _ptr(c_batch, B * ctx.n_elems, "c_batch", allow_none=True), theta, dt, nsteps,
+                                    _ptr(F, ctx.n_nodes, "F", allow_none=True),
+                                    _ptr(u_batch, B * ctx.n_nodes, "u_batch"), snap_plane,
+                                    _ptr(front_out, B * ctx.n_plane, "front_out", allow_none=True), C.byref(o), stats))
+    return [_stats(stats[j]) for j in range(B)]
+
+
+def hf_slab_plan(nz1: int, rank: int, nranks: int):
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(_lib.hf_slab_plan(nz1, rank, nranks, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def hf_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.hf_nccl_unique_id(buf))
+    return buf.raw
+
+
+def hf_local_group_create(nranks: int):
+    out = C.c_void_p()
+    _check(_lib.hf_local_group_create(nranks, C.byref(out)))
+    return out
+
+
+def hf_local_group_destroy(grp):
+    _lib.hf_local_group_destroy(grp)
+
+
+def hf_create_slab(grid, rank: int, nranks: int, uid, transport: int = 0, device: int = 0, stream=None) -> Context:
+    """uid: 128 NCCL id bytes (transport 0) or the hf_local_group handle (transport 1)."""
+    g = make_grid(grid)
+    out = C.c_void_p()
+    keep = None
+    if transport == 0:
+        keep = C.create_string_buffer(bytes(uid), 128)
+        idp = C.cast(keep, C.c_void_p)
+    else:
+        idp = uid
+    _check(_lib.hf_create_slab(C.byref(g), rank, nranks, idp, transport, device, _stream(stream, device),
+                               C.byref(out)))
+    lo, hi, lp, z0 = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    _check(_lib.hf_slab_range(out, C.byref(lo), C.byref(hi), C.byref(lp), C.byref(z0)))
+    ctx = Context(out.value, g, device, lp.value)
+    ctx.slab = (lo.value, hi.value, lp.value, z0.value)
+    return ctx
+
+
+def hf_slab_range(ctx: Context):
+    lo, hi, lp, z0 = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    _check(_lib.hf_slab_range(ctx.ptr, C.byref(lo), C.byref(hi), C.byref(lp), C.byref(z0)))
+    return lo.value, hi.value, lp.value, z0.value
+
+
+def hf_get_launch_count(ctx: Context) -> int:
+    v = C.c_int64()
+    _check(_lib.hf_get_launch_count(ctx.ptr, C.byref(v)))
+    return v.value
+
+
+def hf_profile(ctx: Context, enable: bool):
+    _check(_lib.hf_profile(ctx.ptr, 1 if enable else 0))
+
+
+def hf_profile_read(ctx: Context):
+    ms = (C.c_double * 5)()
+    n = (C.c_int64 * 5)()
+    _check(_lib.hf_profile_read(ctx.ptr, C.byref(ms), C.byref(n)))
+    names = ["stencil_cg_a", "pointwise_cg_b", "residual", "rhs_apply", "other"]
+    return {nm: (ms[i], n[i]) for i, nm in enumerate(names)}
+
+
+def hf_set_driver(ctx: Context, driver: int):
+    _check(_lib.hf_set_driver(ctx.ptr, driver))
+
+
+def hf_flush_l2(ctx: Context):
+    _check(_lib.hf_flush_l2(ctx.ptr))
+
+
+LIB_PATH = _LIB_PATH

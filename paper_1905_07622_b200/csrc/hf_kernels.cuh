@@ -1,0 +1,726 @@
+// hf_kernels.cuh -- sm_100a kernels of libheatfem (the hot path of arXiv 1905.07622).
+//
+// Citations: P:n = PAPER.md line n.  Rn = reading n in DESIGN.md.
+//
+// The operator apply (Eq. (1)) is computed with the element matrices written in
+// their Walsh-Hadamard eigenbasis: for a trilinear voxel every K_ref and M_ref is a tensor
+// product of the 1D matrices (1/h)[[1,-1],[-1,1]] and (h/6)[[2,1],[1,2]], both diagonalised
+// by H = [[1,1],[1,-1]], so
+//      A_e = (1/8) H3 diag(aK k_e lamK + aM c_e lamM) H3,   H3 = H (x) H (x) H.
+// H3 is applied by sum factorisation ACROSS elements: the x butterfly of an edge, the y
+// butterfly of a face and the z butterfly of an element are each computed once and shared
+// by the neighbours that touch them.  ~58 fp64 ops per node.
+//
+// Thread mapping: a CTA owns a 31 x (NW*R - 1) tile of node columns and marches in z over a
+// chunk of node planes.  Lane l of warp w holds node column x = X0-1+l and node rows
+// y = Y0-1+w*R+r (r = 0..R); it computes the R elements whose lower corner is at its nodes.
+// x neighbours come by warp shuffle, the y seam between warps through shared memory,
+// z neighbours stay in registers.  No atomics: every output node is written by one thread,
+// so results are deterministic.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hf {
+
+constexpr int NPART = 4;      // partial sums per block
+constexpr int TILE_X = 31;    // owned node columns per CTA
+
+enum { LD_RAW = 0, LD_GT = 1, LD_CGD = 2, LD_X0 = 3 };
+enum { EP_APPLY = 0, EP_CGA = 1, EP_RESID = 2, EP_RESID_INIT = 3 };
+enum { ST_OK = 0, ST_NOCONV = -3, ST_BREAKDOWN = -4 };
+
+// PCG state of one system (Alg. 1 scalars, device resident; the paper keeps them in device
+// buffers too: delta/alpha/beta kernels P:507-573).
+struct CgState {
+    double delta, alpha, beta, rr, bb, thresh, dq, rtol2;
+    int iter, max_iter, replace_every;
+    int active, status, zero_x, replace;
+    int step;               // time-step counter (step-finalize kernel)
+    int first_failed;       // first failing step, -1 if none
+    int total_iters, max_iters_step, steps_done;
+};
+
+struct Geom {
+    int nx1, ny1, nzl;      // nodes in x, y; local node planes
+    int zg0, nz1g;          // global index of local plane 0; global node planes
+    int px, py;             // coefficient pitches (nx1 + 1, ny1 + 1)
+    long long plane;        // nx1 * ny1
+    unsigned dbits;         // Dirichlet face bits (R3)
+    double gval[6];
+};
+
+struct Lam {                // (1/8) aM lamM[s], (1/8) aK lamK[s], s = sx + 2 sy + 4 sz
+    double lm[8], lk[8];
+};
+
+struct Sync {               // per-system reduction plumbing
+    CgState *st;
+    double *partials;       // gridDim * NPART
+    unsigned *ticket;
+    unsigned long long *launches;
+    double *sums_out;       // non-null: write local sums here and let a finalize kernel run
+    cudaGraphConditionalHandle h_while, h_if;
+    int use_handles;
+};
+
+struct StencilArgs {
+    Geom g;
+    Lam lam;
+    const double2 *kc;      // (k, c) per element, padded layout (see coef_index)
+    const double *in0, *in1, *in2;
+    double *out0, *out1;
+    const double *bvec;
+    double c, s;
+    int z_out0, z_out1, zchunk;   // output planes (local) and planes per CTA
+    int zs0, zs1;                 // planes whose centre values are stored (LD-time stores)
+    int dmode;                    // EP_APPLY: 0 none, 1 identity rows, 2 set g on D rows
+    int first;                    // LD_X0: step 0 of the run (guess = u^0)
+    int rot_role;                 // time-step buffer rotation (ROT_*), resolved from st->step
+    double *rot[3];               // U^n, U^{n+1}, U^{n+2} ring (role-dependent use)
+    double *dbuf[2];              // PCG direction ping-pong, selected by iteration parity
+    Sync sy;
+};
+
+enum { ROT_NONE = 0, ROT_RHS = 1, ROT_INIT = 2, ROT_X = 3 };
+
+// Pointers a stencil launch actually uses, resolved once per launch from the device state.
+// Ring of three time-step buffers: step s reads U[s%3] (u^n) and U[(s+2)%3] (u^{n-1}) and
+// writes U[(s+1)%3] (u^{n+1}); one captured graph then serves every step.  PCG directions
+// ping-pong by iteration parity: d_old = dbuf[i&1], d_new = dbuf[(i&1)^1].
+struct Ptrs {
+    const double *in0, *in1, *in2;
+    double *out1;
+    int first;
+};
+
+__device__ __forceinline__ long long coef_index(const Geom &g, int ex, int ey, int L)
+{
+    // element (ex, ey) in [-1, nx1-1] x [-1, ny1-1], local layer L in [-1, nzl-1]
+    return ((long long)(L + 1) * g.py + (ey + 1)) * g.px + (ex + 1);
+}
+
+__device__ __forceinline__ bool is_dirichlet(const Geom &g, int x, int y, int zl, double &val)
+{
+    const unsigned b = g.dbits;
+    if (!b) return false;
+    const int zg = zl + g.zg0;
+    if ((b & 1u) && x == 0) { val = g.gval[0]; return true; }
+    if ((b & 2u) && x == g.nx1 - 1) { val = g.gval[1]; return true; }
+    if ((b & 4u) && y == 0) { val = g.gval[2]; return true; }
+    if ((b & 8u) && y == g.ny1 - 1) { val = g.gval[3]; return true; }
+    if ((b & 16u) && zg == 0) { val = g.gval[4]; return true; }
+    if ((b & 32u) && zg == g.nz1g - 1) { val = g.gval[5]; return true; }
+    return false;
+}
+
+template <int LD>
+__device__ __forceinline__ double load_node(const StencilArgs &a, const Ptrs &P, long long idx, int x, int y,
+                                            int zl, double beta)
+{
+    if (LD == LD_RAW) return __ldg(P.in0 + idx);
+    if (LD == LD_GT) { double v = 0.0; return is_dirichlet(a.g, x, y, zl, v) ? v : 0.0; }
+    if (LD == LD_CGD) {
+        // d_new = P^{-1} r + beta d_old  (Alg. 1 lines 15, 18; fused, never stored as s)
+        double v = __ldg(P.in0 + idx) * __ldg(P.in1 + idx);
+        if (beta != 0.0) v = fma(beta, __ldg(P.in2 + idx), v);
+        return v;
+    }
+    // LD_X0: guess of u0_update: x0 = 2 u^n - u^{n-1}, or u^0 at the first step
+    const double un = __ldg(P.in0 + idx);
+    return P.first ? un : 2.0 * un - __ldg(P.in1 + idx);
+}
+
+// ---- deterministic block reduction + last-block finalisation -----------------------------
+
+template <int NT>
+__device__ __forceinline__ void block_reduce_store(double (&acc)[NPART], double *partials, int blk)
+{
+    __shared__ double red[NT / 32][NPART];
+    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int j = 0; j < NPART; j++) {
+        double v = acc[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[wid][j] = v;
+    }
+    __syncthreads();
+    if (tid < NPART) {
+        double v = 0.0;
+        for (int w = 0; w < NT / 32; w++) v += red[w][tid];
+        partials[(long long)blk * NPART + tid] = v;
+    }
+}
+
+// Returns true in exactly one block (the last to finish); that block's threads then hold the
+// grid-wide sums in `sums` (fixed summation order: independent of which block was last).
+template <int NT>
+__device__ __forceinline__ bool last_block_sums(const Sync &sy, int nblocks, double (&sums)[NPART])
+{
+    __shared__ bool am_last;
+    __shared__ double red[NT / 32][NPART];
+    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        unsigned t = atomicAdd(sy.ticket, 1u);
+        am_last = (t == (unsigned)nblocks - 1u);
+    }
+    __syncthreads();
+    if (!am_last) return false;
+    __threadfence();
+    double acc[NPART];
+#pragma unroll
+    for (int j = 0; j < NPART; j++) acc[j] = 0.0;
+    for (int b = tid; b < nblocks; b += NT) {
+#pragma unroll
+        for (int j = 0; j < NPART; j++) acc[j] += __ldcg(sy.partials + (long long)b * NPART + j);
+    }
+    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int j = 0; j < NPART; j++) {
+        double v = acc[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[wid][j] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NPART; j++) {
+        double v = 0.0;
+        for (int w = 0; w < NT / 32; w++) v += red[w][j];
+        sums[j] = v;
+    }
+    if (tid == 0) *sy.ticket = 0u;
+    return true;
+}
+
+// ---- scalar updates of Alg. 1 (one thread) ---------------------------------------------
+
+__device__ __forceinline__ void set_while(const Sync &sy, int v)
+{
+    if (sy.use_handles) cudaGraphSetConditional(sy.h_while, (unsigned)v);
+}
+__device__ __forceinline__ void set_if(const Sync &sy, int v)
+{
+    if (sy.use_handles) cudaGraphSetConditional(sy.h_if, (unsigned)v);
+}
+
+// init: r = b - A x0, delta = r^T P^{-1} r, rr = r^T r, bb = b_F^T b_F  (Alg. 1 lines 2-4)
+__device__ __forceinline__ void fin_init(const Sync &sy, const double *s)
+{
+    CgState *st = sy.st;
+    st->delta = s[0]; st->rr = s[1]; st->bb = s[2];
+    st->thresh = st->rtol2 * s[2];
+    st->iter = 0; st->beta = 0.0; st->replace = 0; st->status = ST_OK;
+    if (s[2] == 0.0) {               // b_F = 0 -> x_F = 0, 0 iterations
+        st->zero_x = 1; st->active = 0;
+    } else {
+        st->zero_x = 0;
+        const bool need = s[1] > st->thresh;     // R4: ||r|| > tol ||b||
+        st->active = need && st->max_iter > 0;
+        if (need && st->max_iter <= 0) st->status = ST_NOCONV;
+    }
+    set_while(sy, st->active);
+}
+
+// after q = A d: alpha = delta / (d^T q)  (Alg. 1 line 8); breakdown if d^T q <= 0
+__device__ __forceinline__ void fin_cga(const Sync &sy, const double *s)
+{
+    CgState *st = sy.st;
+    const double dq = s[0];
+    st->dq = dq;
+    if (!(dq > 0.0) || !isfinite(dq) || !isfinite(st->delta)) {
+        st->status = ST_BREAKDOWN; st->active = 0;
+    } else {
+        st->alpha = st->delta / dq;
+    }
+}
+
+// after the residual update: delta_old <- delta, delta = r^T s, beta = delta/delta_old,
+// i <- i + 1, stop test (Alg. 1 lines 16-19, readings R4, R5)
+__device__ __forceinline__ void fin_iter(const Sync &sy, const double *s)
+{
+    CgState *st = sy.st;
+    const double delta_old = st->delta;
+    st->delta = s[0];
+    st->rr = s[1];
+    st->beta = s[0] / delta_old;
+    st->iter += 1;
+    const bool need = s[1] > st->thresh;
+    if (!isfinite(s[1])) { st->status = ST_BREAKDOWN; st->active = 0; }
+    else {
+        st->active = need && st->iter < st->max_iter;
+        if (need && st->iter >= st->max_iter) st->status = ST_NOCONV;
+    }
+    set_while(sy, st->active);
+}
+
+// ---- the stencil kernel (operator apply with fused prologue/epilogue) ---------------------
+//
+// Element-local WHT: channel ch = 2 sx + sy of a face; element wave number s = sx + 2 sy + 4 sz.
+
+template <int R, int NW, int LD, int EP, bool MASK>
+__global__ void __launch_bounds__(32 * NW)
+k_stencil(const StencilArgs a)
+{
+    constexpr int NT = 32 * NW;
+    const Geom &g = a.g;
+    const int lane = threadIdx.x, w = threadIdx.y;
+    const int blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int nblocks = gridDim.x * gridDim.y * gridDim.z;
+    if (blk == 0 && lane == 0 && w == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
+
+    double beta = 0.0;
+    Ptrs P{a.in0, a.in1, a.in2, a.out1, a.first};
+    if (a.sy.st) {
+        const CgState *st = a.sy.st;
+        if (st->first_failed >= 0) return;       // an earlier time step failed: stop the run
+        if (EP == EP_CGA || EP == EP_RESID) {
+            if (!st->active) return;             // converged / stopped: nothing to do
+            if (EP == EP_RESID && !st->replace) return;
+        }
+        if (LD == LD_CGD) {
+            beta = st->beta;
+            const int par = st->iter & 1;        // d_old = dbuf[par], d_new = dbuf[par ^ 1]
+            P.in2 = a.dbuf[par];
+            P.out1 = a.dbuf[par ^ 1];
+        }
+        if (a.rot_role != ROT_NONE) {
+            const int s = st->step % 3;
+            double *un = a.rot[s], *unext = a.rot[(s + 1) % 3], *uprev = a.rot[(s + 2) % 3];
+            if (a.rot_role == ROT_RHS) P.in0 = un;
+            else if (a.rot_role == ROT_INIT) { P.in0 = un; P.in1 = uprev; P.out1 = unext; P.first = a.first && st->step == 0; }
+            else P.in0 = unext;
+        }
+    }
+
+    const int X0 = blockIdx.x * TILE_X;
+    const int Y0 = blockIdx.y * (NW * R - 1);
+    const int xi = X0 - 1 + lane;
+    const int yb = Y0 - 1 + w * R;
+    const bool xin = xi >= 0 && xi < g.nx1;
+    const bool xin1 = (xi + 1) < g.nx1;            // lane 31's extra column
+    const bool xown = lane >= 1 && xin;
+    const int zb = a.z_out0 + blockIdx.z * a.zchunk;
+    const int ze = min(zb + a.zchunk, a.z_out1);
+
+    __shared__ double seam[2][NW][32];
+
+    // register state (z-marching)
+    double Fp[R][4];          // face transforms of the lower plane p-1
+    double Cy[R][4];          // face-space contributions carried from the layer below
+    double cen[R];            // raw centre values of plane p-1 (rows 0..R-1)
+    double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++) { Fp[r][ch] = 0.0; Cy[r][ch] = 0.0; }
+        cen[r] = 0.0;
+    }
+
+    int it = 0;
+    for (int p = zb - 1; p <= ze; ++p, ++it) {
+        // ---- load node plane p (rows 0..R), masked copy for the stencil ----------------
+        double vm[R + 1], nx[R + 1], craw[R];
+        const bool pin = p >= 0 && p < g.nzl;
+        // does this CTA store centre values of plane p (exactly one CTA per plane)?
+        const bool store_p = (p >= a.zs0 && p < a.zs1) &&
+                             ((p >= zb && p < ze) || (p == zb - 1 && zb == a.z_out0) ||
+                              (p == ze && ze == a.z_out1));
+#pragma unroll
+        for (int r = 0; r <= R; r++) {
+            const int yi = yb + r;
+            const bool in = pin && xin && yi >= 0 && yi < g.ny1;
+            const long long idx = (long long)p * g.plane + (long long)yi * g.nx1 + xi;
+            double v = in ? load_node<LD>(a, P, idx, xi, yi, p, beta) : 0.0;
+            if (r < R) craw[r] = v;
+            if (MASK && in) { double gv; if (is_dirichlet(g, xi, yi, p, gv)) v = 0.0; }
+            vm[r] = v;
+            // lane 31 loads its right neighbour column itself
+            const bool in1 = pin && lane == 31 && xin1 && xi + 1 >= 0 && yi >= 0 && yi < g.ny1;
+            double v1 = in1 ? load_node<LD>(a, P, idx + 1, xi + 1, yi, p, beta) : 0.0;
+            if (MASK && in1) { double gv; if (is_dirichlet(g, xi + 1, yi, p, gv)) v1 = 0.0; }
+            nx[r] = v1;
+            // d_new (CG kernel A) or the guess x0 (init) is stored once, raw, by its owner
+            if ((EP == EP_CGA || EP == EP_RESID_INIT) && r < R && store_p && in && xown && (w > 0 || r > 0))
+                P.out1[idx] = craw[r];
+        }
+        // ---- forward x butterfly (edges) -------------------------------------------------
+        double S[R + 1], D[R + 1];
+#pragma unroll
+        for (int r = 0; r <= R; r++) {
+            double un = __shfl_down_sync(0xffffffffu, vm[r], 1);
+            if (lane == 31) un = nx[r];
+            S[r] = vm[r] + un;
+            D[r] = vm[r] - un;
+        }
+        // ---- layer L = p-1: y butterfly (faces), z butterfly, scaling, backward z --------
+        // (skipped for the warm-up plane it == 0: it only primes Fp)
+        const int L = p - 1;
+        const bool Lin = it > 0 && L >= -1 && L < g.nzl;   // padded coefficient layers exist
+        double T[R][4];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            double Fc[4];
+            Fc[0] = S[r] + S[r + 1];   // sx=0, sy=0
+            Fc[1] = S[r] - S[r + 1];   // sx=0, sy=1
+            Fc[2] = D[r] + D[r + 1];   // sx=1, sy=0
+            Fc[3] = D[r] - D[r + 1];   // sx=1, sy=1
+            const int ey = yb + r;
+            double ke = 0.0, ce = 0.0;
+            if (Lin && xi < g.nx1 && ey < g.ny1) {
+                const double2 kc = __ldg(a.kc + coef_index(g, xi, ey, L));
+                ke = kc.x; ce = kc.y;
+            }
+#pragma unroll
+            for (int ch = 0; ch < 4; ch++) {
+                const int sx = ch >> 1, syb = ch & 1;
+                const int s0 = sx + 2 * syb, s1 = s0 + 4;
+                const double v0 = Fp[r][ch] + Fc[ch];     // sz = 0
+                const double v1 = Fp[r][ch] - Fc[ch];     // sz = 1
+                const double t0 = (s0 == 0) ? ce * a.lam.lm[0] : fma(ke, a.lam.lk[s0], ce * a.lam.lm[s0]);
+                const double t1 = fma(ke, a.lam.lk[s1], ce * a.lam.lm[s1]);
+                const double w0 = v0 * t0, w1 = v1 * t1;
+                T[r][ch] = Cy[r][ch] + (w0 + w1);        // bottom plane p-1 complete
+                Cy[r][ch] = w0 - w1;                     // top plane p, carried
+                Fp[r][ch] = Fc[ch];
+            }
+        }
+        // ---- backward y and x butterflies for plane p-1, seam exchange, epilogue ---------
+        const int pout = p - 1;
+        const bool out_plane = pout >= zb && pout < ze;   // uniform across the CTA
+        double yv[R + 1];
+#pragma unroll
+        for (int e = 0; e <= R; e++) {
+            double E0 = 0.0, E1 = 0.0;               // sx = 0, 1
+            if (e < R) { E0 += T[e][0] + T[e][1]; E1 += T[e][2] + T[e][3]; }
+            if (e > 0) { E0 += T[e - 1][0] - T[e - 1][1]; E1 += T[e - 1][2] - T[e - 1][3]; }
+            double left = __shfl_up_sync(0xffffffffu, E0 - E1, 1);
+            if (lane == 0) left = 0.0;
+            yv[e] = (E0 + E1) + left;
+        }
+        if (out_plane) {
+            seam[it & 1][w][lane] = yv[R];
+            __syncthreads();
+            if (w > 0) yv[0] += seam[it & 1][w - 1][lane];
+#pragma unroll
+            for (int e = 0; e < R; e++) {
+                const int yi = yb + e;
+                if (!(xown && (w > 0 || e > 0) && yi < g.ny1)) continue;
+                const long long idx = (long long)pout * g.plane + (long long)yi * g.nx1 + xi;
+                double gv = 0.0;
+                const bool isd = is_dirichlet(g, xi, yi, pout, gv);
+                if (EP == EP_APPLY) {
+                    double y = a.c * yv[e];
+                    if (a.dmode == 1 && isd) y = cen[e];
+                    if (a.bvec) y = fma(a.s, a.bvec[idx], y);
+                    if (a.dmode == 2 && isd) y = gv;
+                    a.out0[idx] = y;
+                } else if (EP == EP_CGA) {
+                    const double d = cen[e];
+                    const double q = isd ? d : yv[e];       // identity rows (R3)
+                    a.out0[idx] = q;
+                    acc[0] = fma(d, q, acc[0]);
+                } else {   // EP_RESID, EP_RESID_INIT: r = b - A x (identity rows on D)
+                    const double b = __ldg(a.bvec + idx);
+                    const double r = isd ? 0.0 : b - yv[e];
+                    a.out0[idx] = r;
+                    const double sv = r * __ldg(a.in2 + idx);  // in2 = P^{-1} diagonal
+                    acc[0] = fma(r, sv, acc[0]);
+                    acc[1] = fma(r, r, acc[1]);
+                    if (EP == EP_RESID_INIT && !isd) acc[2] = fma(b, b, acc[2]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) cen[r] = craw[r];
+    }
+
+    if (EP == EP_APPLY) return;
+    block_reduce_store<NT>(acc, a.sy.partials, blk);
+    double sums[NPART];
+    if (!last_block_sums<NT>(a.sy, nblocks, sums)) return;
+    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+    if (tid != 0) return;
+    if (a.sy.sums_out) {
+        for (int j = 0; j < NPART; j++) a.sy.sums_out[j] = sums[j];
+        return;
+    }
+    if (EP == EP_CGA) fin_cga(a.sy, sums);
+    else if (EP == EP_RESID_INIT) fin_init(a.sy, sums);
+    else fin_iter(a.sy, sums);
+}
+
+// ---- PCG kernel B: x += alpha d; r -= alpha q; s = P^{-1} r; r^T s, r^T r ---------------
+// (Alg. 1 lines 9, 13, 15, 16; the paper's knl_6, knl_7, knl_8, knl_9A-C, knl_10.)
+// x is updated on every local node (ghost planes included, so slab ghosts stay consistent);
+// r and the dot products only on owned nodes [own0, own1).  On a replacement iteration
+// (i > 0, i mod replace_every == 0, Alg. 1 line 10) only x is updated: the residual kernel
+// (EP_RESID) follows.
+
+struct BArgs {
+    double *x;
+    const double *q, *invd;
+    double *dbuf[2];        // d = dbuf[(iter & 1) ^ 1] (written by kernel A of this iteration)
+    double *r;
+    long long n, own0, own1;
+    double *rot[3];         // if rot[0]: x = rot[(step + 1) % 3]
+    Sync sy;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
+{
+    const int tid = threadIdx.x;
+    const int blk = blockIdx.x;
+    if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
+    CgState *st = a.sy.st;
+    if (!st->active) {
+        if (blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
+        return;
+    }
+    const int it = st->iter, re = st->replace_every;
+    const bool replace = it > 0 && re > 0 && (it % re) == 0;
+    const double alpha = st->alpha;
+    const double *dvec = a.dbuf[(it & 1) ^ 1];
+    double *xvec = a.rot[0] ? a.rot[(st->step + 1) % 3] : a.x;
+    double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
+    const long long stride = (long long)gridDim.x * NT * 2;
+    for (long long i = ((long long)blk * NT + tid) * 2; i < a.n; i += stride) {
+        if (i + 1 < a.n) {
+            double2 xv = *reinterpret_cast<const double2 *>(xvec + i);
+            const double2 dv = *reinterpret_cast<const double2 *>(dvec + i);
+            xv.x = fma(alpha, dv.x, xv.x);
+            xv.y = fma(alpha, dv.y, xv.y);
+            *reinterpret_cast<double2 *>(xvec + i) = xv;
+            if (!replace) {
+                double2 rv = *reinterpret_cast<const double2 *>(a.r + i);
+                const double2 qv = __ldg(reinterpret_cast<const double2 *>(a.q + i));
+                const double2 iv = __ldg(reinterpret_cast<const double2 *>(a.invd + i));
+                const bool o0 = i >= a.own0 && i < a.own1, o1 = i + 1 >= a.own0 && i + 1 < a.own1;
+                if (o0) { rv.x = fma(-alpha, qv.x, rv.x); const double sv = rv.x * iv.x;
+                          acc[0] = fma(rv.x, sv, acc[0]); acc[1] = fma(rv.x, rv.x, acc[1]); }
+                if (o1) { rv.y = fma(-alpha, qv.y, rv.y); const double sv = rv.y * iv.y;
+                          acc[0] = fma(rv.y, sv, acc[0]); acc[1] = fma(rv.y, rv.y, acc[1]); }
+                if (o0 || o1) *reinterpret_cast<double2 *>(a.r + i) = rv;
+            }
+        } else {
+            xvec[i] = fma(alpha, dvec[i], xvec[i]);
+            if (!replace && i >= a.own0 && i < a.own1) {
+                const double rv = fma(-alpha, a.q[i], a.r[i]);
+                a.r[i] = rv;
+                const double sv = rv * a.invd[i];
+                acc[0] = fma(rv, sv, acc[0]);
+                acc[1] = fma(rv, rv, acc[1]);
+            }
+        }
+    }
+    if (replace) {
+        if (blk == 0 && tid == 0) { st->replace = 1; set_if(a.sy, 1); }
+        return;
+    }
+    block_reduce_store<NT>(acc, a.sy.partials, blk);
+    double sums[NPART];
+    if (!last_block_sums<NT>(a.sy, gridDim.x, sums)) return;
+    if (tid != 0) return;
+    st->replace = 0;
+    set_if(a.sy, 0);
+    if (a.sy.sums_out) { for (int j = 0; j < NPART; j++) a.sy.sums_out[j] = sums[j]; return; }
+    fin_iter(a.sy, sums);
+}
+
+// Finalisation after a cross-rank allreduce of the local sums (slab mode).
+__global__ void k_finalize(Sync sy, int mode)
+{
+    if (sy.launches) atomicAdd(sy.launches, 1ull);
+    CgState *st = sy.st;
+    const double *s = sy.sums_out;
+    if (mode == EP_RESID_INIT) { if (st->first_failed < 0) fin_init(sy, s); }
+    else if (!st->active) return;
+    else if (mode == EP_CGA) fin_cga(sy, s);
+    else if (mode == EP_RESID) { if (st->replace) fin_iter(sy, s); }
+    else fin_iter(sy, s);   // kernel B
+}
+
+// ---- Jacobi diagonal (Jacobi_A P:659-662) -------------------------------------------
+// diag_i = sum over the 8 elements around node i of aK k_e Kd + aM c_e Md, with
+// Kd = K_ref[l][l], Md = M_ref[l][l] (the same for every l of a voxel); 1 on Dirichlet rows.
+
+__global__ void k_diag(Geom g, const double2 *kc, double aK, double aM, double Kd, double Md,
+                       double *diag, double *invd, unsigned long long *launches)
+{
+    const long long n = g.plane * g.nzl;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && launches) atomicAdd(launches, 1ull);
+    if (i >= n) return;
+    const int x = (int)(i % g.nx1), y = (int)((i / g.nx1) % g.ny1), z = (int)(i / g.plane);
+    double sk = 0.0, sc = 0.0;
+    for (int l = 0; l < 8; l++) {
+        const int ex = x - (l & 1), ey = y - ((l >> 1) & 1), ez = z - ((l >> 2) & 1);
+        const double2 v = kc[coef_index(g, ex, ey, ez)];
+        sk += v.x;
+        sc += v.y;
+    }
+    double d = aK * Kd * sk + aM * Md * sc;
+    double gv;
+    if (is_dirichlet(g, x, y, z, gv)) d = 1.0;
+    if (diag) diag[i] = d;
+    if (invd) invd[i] = 1.0 / d;
+}
+
+// ---- packing of the per-element coefficients into the padded (k, c) layout ----------------
+// padded entry (ex+1, ey+1, L+1) for ex in [-1, nx1-1], ey in [-1, ny1-1], L in [-1, nzl-1];
+// global element (ex, ey, zg0 + L) if it exists, else (0, 0).
+
+__global__ void k_pack(Geom g, int nx, int ny, int nz, const double *k, const double *c, double2 *kc,
+                       long long ntot, unsigned long long *launches)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && launches) atomicAdd(launches, 1ull);
+    if (i >= ntot) return;
+    const int ex = (int)(i % g.px) - 1, ey = (int)((i / g.px) % g.py) - 1;
+    const int L = (int)(i / ((long long)g.px * g.py)) - 1;
+    const int ez = g.zg0 + L;
+    double2 v = make_double2(0.0, 0.0);
+    if (ex >= 0 && ex < nx && ey >= 0 && ey < ny && ez >= 0 && ez < nz) {
+        const long long e = ex + (long long)nx * (ey + (long long)ny * ez);
+        v = make_double2(k[e], c[e]);
+    }
+    kc[i] = v;
+}
+
+// ---- flux load F_i = int_face f phi_i ds (reading R12) ----------------------------
+// one thread per node of the face plane; 2x2 Gauss points per adjacent boundary quad.
+
+struct FaceArgs {
+    Geom g;
+    int face, nd, ax, bx;     // normal axis, in-plane axes (increasing order)
+    int na, nb;               // nodes along ax, bx (global counts of that axis)
+    int plane_g;              // global index of the face along the normal axis
+    double ha, hb, oa, ob;    // spacing and origin of the in-plane axes
+    double f_const;
+    int has_beam;
+    double bP, bs, bca, bcb;
+    double *F;
+    unsigned long long *launches;
+};
+
+__device__ __forceinline__ double phi1(int b, double t, double h) { return b ? t / h : 1.0 - t / h; }
+
+__global__ void k_face_load(const FaceArgs a)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && a.launches) atomicAdd(a.launches, 1ull);
+    const long long nface = (long long)a.na * a.nb;
+    if (i >= nface) return;
+    const int ia = (int)(i % a.na), ib = (int)(i / a.na);
+    // local node coordinates
+    int idx3[3];
+    idx3[a.nd] = a.plane_g;
+    idx3[a.ax] = ia;
+    idx3[a.bx] = ib;
+    const int zl = idx3[2] - a.g.zg0;                  // local plane (slab)
+    if (zl < 0 || zl >= a.g.nzl) return;
+    const double gp0 = 0.5 * (1.0 - 0.57735026918962576451), gp1 = 0.5 * (1.0 + 0.57735026918962576451);
+    const double w = (a.ha * 0.5) * (a.hb * 0.5);
+    double sum = 0.0;
+    for (int cb = 0; cb < 2; cb++) {             // node is corner (ca, cb) of quad (ia-ca, ib-cb)
+        const int qb = ib - cb;
+        if (qb < 0 || qb >= a.nb - 1) continue;
+        for (int ca = 0; ca < 2; ca++) {
+            const int qa = ia - ca;
+            if (qa < 0 || qa >= a.na - 1) continue;
+            for (int gb = 0; gb < 2; gb++) {
+                const double tb = (gb ? gp1 : gp0) * a.hb;
+                for (int ga = 0; ga < 2; ga++) {
+                    const double ta = (ga ? gp1 : gp0) * a.ha;
+                    double f = a.f_const;
+                    if (a.has_beam) {
+                        const double xa = a.oa + qa * a.ha + ta - a.bca, xb = a.ob + qb * a.hb + tb - a.bcb;
+                        f += a.bP / (2.0 * 3.14159265358979323846 * a.bs * a.bs) *
+                             exp(-(xa * xa + xb * xb) / (2.0 * a.bs * a.bs));
+                    }
+                    sum += w * f * phi1(ca, ta, a.ha) * phi1(cb, tb, a.hb);
+                }
+            }
+        }
+    }
+    const long long node = (long long)zl * a.g.plane + (long long)idx3[1] * a.g.nx1 + idx3[0];
+    a.F[node] = sum;
+}
+
+// ---- small pointwise kernels ----------------------------------------------------------------
+
+// v_D <- src_D (src = NULL: the Dirichlet value g) on every local node.
+__global__ void k_set_dirichlet(Geom g, double *v, const double *src, unsigned long long *launches)
+{
+    const long long n = g.plane * g.nzl;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && launches) atomicAdd(launches, 1ull);
+    if (i >= n) return;
+    const int x = (int)(i % g.nx1), y = (int)((i / g.nx1) % g.ny1), z = (int)(i / g.plane);
+    double gv;
+    if (is_dirichlet(g, x, y, z, gv)) v[i] = src ? src[i] : gv;
+}
+
+// End of one solve / time step: x_F <- 0 if b_F = 0; per-step statistics;
+// snapshot of one plane of x; advance the step counter.  Last block does the bookkeeping.
+struct StepArgs {
+    Geom g;
+    double *x;
+    double *rot[3];         // if rot[0]: x = rot[(step + 1) % 3]
+    long long n;
+    double *snap;           // NULL or nsteps x plane
+    int snap_plane;         // local plane index, -1 none
+    int *iters_out;         // per-step iteration counts (may be NULL)
+    Sync sy;
+};
+
+__global__ void __launch_bounds__(256) k_step_end(const StepArgs a)
+{
+    const int tid = threadIdx.x, blk = blockIdx.x;
+    if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
+    CgState *st = a.sy.st;
+    if (st->first_failed >= 0) return;
+    const int step = st->step;
+    double *xv = a.rot[0] ? a.rot[(step + 1) % 3] : a.x;
+    if (st->zero_x) {
+        for (long long i = (long long)blk * 256 + tid; i < a.n; i += (long long)gridDim.x * 256) {
+            const int x = (int)(i % a.g.nx1), y = (int)((i / a.g.nx1) % a.g.ny1), z = (int)(i / a.g.plane);
+            double gv;
+            if (!is_dirichlet(a.g, x, y, z, gv)) xv[i] = 0.0;
+        }
+    }
+    if (a.snap && a.snap_plane >= 0) {
+        const double *src = xv + (long long)a.snap_plane * a.g.plane;
+        double *dst = a.snap + (long long)step * a.g.plane;
+        for (long long i = (long long)blk * 256 + tid; i < a.g.plane; i += (long long)gridDim.x * 256) {
+            // zero_x is rare; read after the zeroing above only matters for the same block
+            double v = src[i];
+            if (st->zero_x) {
+                const int x = (int)(i % a.g.nx1), y = (int)(i / a.g.nx1);
+                double gv;
+                if (!is_dirichlet(a.g, x, y, a.snap_plane, gv)) v = 0.0;
+            }
+            dst[i] = v;
+        }
+    }
+    __shared__ bool am_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) am_last = atomicAdd(a.sy.ticket, 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!am_last || tid != 0) return;
+    *a.sy.ticket = 0u;
+    if (a.iters_out) a.iters_out[step] = st->iter;
+    st->total_iters += st->iter;
+    if (st->iter > st->max_iters_step) st->max_iters_step = st->iter;
+    st->steps_done = step + 1;
+    if (st->status != ST_OK) st->first_failed = step;
+    st->step = step + 1;
+}
+
+}  // namespace hf

@@ -1,0 +1,1471 @@
+// hf_lib.cu -- libheatfem: the C ABI of include/heatfem.h on top of hf_kernels.cuh.
+//
+// Host runtime: contexts, workspaces, host-pointer staging, the PCG and time-loop drivers
+// (a CUDA graph with a device-side WHILE loop, or a host loop), batched simulations, z-slab
+// decomposition with NCCL (dlopen'ed) or an in-process transport.  Citations: P:n = PAPER.md.
+#include "heatfem.h"
+#include "hf_kernels.cuh"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace hf;
+
+// ============================================================================================
+// errors
+
+static thread_local std::string g_err;
+
+static hf_status fail(hf_status s, const std::string &msg)
+{
+    g_err = msg;
+    return s;
+}
+
+#define CUCK(call)                                                                           \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(e_ == cudaErrorMemoryAllocation ? HF_E_OOM : HF_E_CUDA,              \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                \
+    } while (0)
+
+#define HFCK(call)                                                                           \
+    do {                                                                                     \
+        hf_status s_ = (call);                                                               \
+        if (s_ != HF_OK) return s_;                                                          \
+    } while (0)
+
+// ============================================================================================
+// NCCL, loaded at run time (libnccl.so.2: torch's copy if torch is already loaded, else system)
+
+namespace nccl {
+typedef struct ncclComm *ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclFloat64 = 8, ncclSum = 0 };
+typedef ncclResult_t (*GetUniqueId_t)(ncclUniqueId *);
+typedef ncclResult_t (*CommInitRank_t)(ncclComm_t *, int, ncclUniqueId, int);
+typedef ncclResult_t (*CommDestroy_t)(ncclComm_t);
+typedef ncclResult_t (*AllReduce_t)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef ncclResult_t (*Send_t)(const void *, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef ncclResult_t (*Recv_t)(void *, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef ncclResult_t (*Group_t)(void);
+typedef const char *(*GetErrorString_t)(ncclResult_t);
+struct Api {
+    void *h = nullptr;
+    GetUniqueId_t getUniqueId;
+    CommInitRank_t commInitRank;
+    CommDestroy_t commDestroy;
+    AllReduce_t allReduce;
+    Send_t send;
+    Recv_t recv;
+    Group_t groupStart, groupEnd;
+    GetErrorString_t getErrorString;
+};
+static Api g_api;
+static std::mutex g_mu;
+
+static hf_status load()
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_api.h) return HF_OK;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return fail(HF_E_NCCL, std::string("dlopen libnccl.so.2: ") + dlerror());
+#define SYM(field, name, type)                                                               \
+    g_api.field = (type)dlsym(h, name);                                                      \
+    if (!g_api.field) return fail(HF_E_NCCL, std::string("dlsym ") + name);
+    SYM(getUniqueId, "ncclGetUniqueId", GetUniqueId_t)
+    SYM(commInitRank, "ncclCommInitRank", CommInitRank_t)
+    SYM(commDestroy, "ncclCommDestroy", CommDestroy_t)
+    SYM(allReduce, "ncclAllReduce", AllReduce_t)
+    SYM(send, "ncclSend", Send_t)
+    SYM(recv, "ncclRecv", Recv_t)
+    SYM(groupStart, "ncclGroupStart", Group_t)
+    SYM(groupEnd, "ncclGroupEnd", Group_t)
+    SYM(getErrorString, "ncclGetErrorString", GetErrorString_t)
+#undef SYM
+    g_api.h = h;
+    return HF_OK;
+}
+}  // namespace nccl
+
+#define NCCK(call)                                                                           \
+    do {                                                                                     \
+        nccl::ncclResult_t r_ = (call);                                                      \
+        if (r_ != 0) return fail(HF_E_NCCL, std::string(#call) + ": " + nccl::g_api.getErrorString(r_)); \
+    } while (0)
+
+// ============================================================================================
+// context
+
+struct SimKey {
+    double aK = 0, aM = 0, aKL = 0, aML = 0, rtol = 0;
+    int max_iter = 0, replace_every = 0, first = 0, snap_plane = -1, lift = 0;
+    const double *F = nullptr;
+    double *snap = nullptr, *ubase = nullptr;
+    double dt = 0;
+    bool operator==(const SimKey &o) const { return std::memcmp(this, &o, sizeof(SimKey)) == 0; }
+};
+
+struct Sys {                         // one system's PCG workspace (Table 3 buffers)
+    double2 *kc = nullptr;           // padded (k, c); owned if own_kc
+    bool own_kc = false;
+    double *U[3] = {nullptr, nullptr, nullptr};   // time-step ring
+    double *b = nullptr, *r = nullptr, *q = nullptr, *invd = nullptr;
+    double *dbuf[2] = {nullptr, nullptr};
+    CgState *st = nullptr;           // device
+    CgState *st_host = nullptr;      // pinned mirror
+    double *partials = nullptr, *sums = nullptr;
+    unsigned *ticket = nullptr;
+    int *iters = nullptr;
+    int iters_cap = 0;
+    cudaStream_t stream = nullptr;   // == ctx stream for the primary system
+    bool own_stream = false;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    SimKey key;
+    bool key_valid = false;
+};
+
+struct Comm {
+    virtual ~Comm() {}
+    // make ghost planes of `v` (local layout) equal to the neighbours' owned boundary planes
+    virtual hf_status exchange(hf_ctx *c, Sys &s, double *v) = 0;
+    // in-place sum of n doubles (device) across ranks
+    virtual hf_status allreduce(hf_ctx *c, Sys &s, double *v, int n) = 0;
+    virtual bool graph_capturable() const = 0;
+};
+
+struct hf_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int nsm = 148;
+    hf_grid g{};
+    int nx1 = 0, ny1 = 0, nz1g = 0;
+    int nzl = 0, zg0 = 0;            // local planes, global index of local plane 0
+    int own_lo = 0, own_hi = 0;      // owned local planes [own_lo, own_hi)
+    long long plane = 0, nloc = 0;
+    long long kc_elems = 0;
+    bool coef_set = false;
+    unsigned dbits = 0;
+    double gval[6] = {0, 0, 0, 0, 0, 0};
+    double Kd = 0, Md = 0;           // diagonal entry of K_ref, M_ref
+    Sys sys0;
+    std::vector<std::unique_ptr<Sys>> pool;
+    unsigned long long *launches = nullptr;
+    // host staging
+    std::vector<void *> scratch;
+    std::vector<size_t> scratch_cap;
+    double *flush = nullptr;
+    // config
+    int driver = 0;                  // 0 graph, 1 host loop
+    int tileR = 4;
+    int ctas_per_sm = 2;
+    int check_every = 8;
+    int tiles_x = 0, tiles_y = 0, max_blocks = 0;
+    // slab
+    int rank = 0, nranks = 1;
+    Comm *comm = nullptr;
+    // profiling
+    bool prof = false;
+    double prof_ms[5] = {0, 0, 0, 0, 0};
+    long long prof_n[5] = {0, 0, 0, 0, 0};
+};
+
+static const int NW = 8;             // warps per stencil CTA
+
+static bool is_device_ptr(const void *p)
+{
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static hf_status scratch_get(hf_ctx *c, int slot, size_t bytes, void **out)
+{
+    if ((int)c->scratch.size() <= slot) {
+        c->scratch.resize(slot + 1, nullptr);
+        c->scratch_cap.resize(slot + 1, 0);
+    }
+    if (c->scratch_cap[slot] < bytes) {
+        if (c->scratch[slot]) cudaFree(c->scratch[slot]);
+        c->scratch[slot] = nullptr;
+        c->scratch_cap[slot] = 0;
+        CUCK(cudaMalloc(&c->scratch[slot], bytes));
+        c->scratch_cap[slot] = bytes;
+    }
+    *out = c->scratch[slot];
+    return HF_OK;
+}
+
+// device view of an input array (host arrays are copied into scratch `slot`)
+static hf_status dev_in(hf_ctx *c, const double *p, size_t n, int slot, const double **out)
+{
+    if (!p) { *out = nullptr; return HF_OK; }
+    if (is_device_ptr(p)) { *out = p; return HF_OK; }
+    void *d;
+    HFCK(scratch_get(c, slot, n * sizeof(double), &d));
+    CUCK(cudaMemcpyAsync(d, p, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    *out = (const double *)d;
+    return HF_OK;
+}
+
+// device view of an output (or in/out) array; host arrays go through scratch `slot`
+static hf_status dev_out(hf_ctx *c, double *p, size_t n, int slot, bool copy_in, double **out)
+{
+    if (is_device_ptr(p)) { *out = p; return HF_OK; }
+    void *d;
+    HFCK(scratch_get(c, slot, n * sizeof(double), &d));
+    if (copy_in) CUCK(cudaMemcpyAsync(d, p, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    *out = (double *)d;
+    return HF_OK;
+}
+
+static hf_status dev_out_finish(hf_ctx *c, double *p, const double *d, size_t n)
+{
+    if (p == d) return HF_OK;
+    CUCK(cudaMemcpyAsync(p, d, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUCK(cudaStreamSynchronize(c->stream));
+    return HF_OK;
+}
+
+static Geom make_geom(const hf_ctx *c)
+{
+    Geom g;
+    g.nx1 = c->nx1; g.ny1 = c->ny1; g.nzl = c->nzl;
+    g.zg0 = c->zg0; g.nz1g = c->nz1g;
+    g.px = c->nx1 + 1; g.py = c->ny1 + 1;
+    g.plane = c->plane;
+    g.dbits = c->dbits;
+    for (int f = 0; f < 6; f++) g.gval[f] = c->gval[f];
+    return g;
+}
+
+// WHT eigenvalues of the voxel matrices (1/8 folded in): mu_d(0) = h/2, mu_d(1) = h/6 for
+// (h/6)[[2,1],[1,2]]; kappa_d(0) = 0, kappa_d(1) = 2/h for (1/h)[[1,-1],[-1,1]].
+static Lam make_lam(const double h[3], double aK, double aM)
+{
+    Lam L;
+    for (int s = 0; s < 8; s++) {
+        const int b[3] = {s & 1, (s >> 1) & 1, (s >> 2) & 1};
+        double mu[3], ka[3];
+        for (int d = 0; d < 3; d++) {
+            mu[d] = b[d] ? h[d] / 6.0 : h[d] / 2.0;
+            ka[d] = b[d] ? 2.0 / h[d] : 0.0;
+        }
+        const double lM = mu[0] * mu[1] * mu[2];
+        const double lK = ka[0] * mu[1] * mu[2] + mu[0] * ka[1] * mu[2] + mu[0] * mu[1] * ka[2];
+        L.lm[s] = aM * lM / 8.0;
+        L.lk[s] = aK * lK / 8.0;
+    }
+    return L;
+}
+
+// ============================================================================================
+// launches (one spec -> direct launch, or a graph kernel node)
+
+struct Launch {
+    const void *fn = nullptr;
+    dim3 grid, block;
+    std::vector<char> arg;
+    int cls = 4;
+    template <class T> void set(const T &v) { arg.resize(sizeof(T)); std::memcpy(arg.data(), &v, sizeof(T)); }
+};
+
+template <int LD, int EP, bool MASK> static const void *stencil_fn(int R)
+{
+    switch (R) {
+    case 4: return (const void *)k_stencil<4, NW, LD, EP, MASK>;
+    case 2: return (const void *)k_stencil<2, NW, LD, EP, MASK>;
+    default: return (const void *)k_stencil<1, NW, LD, EP, MASK>;
+    }
+}
+
+static const void *stencil_fn_dyn(int R, int LD, int EP, bool MASK)
+{
+    if (LD == LD_RAW && EP == EP_APPLY && !MASK) return stencil_fn<LD_RAW, EP_APPLY, false>(R);
+    if (LD == LD_GT && EP == EP_APPLY && !MASK) return stencil_fn<LD_GT, EP_APPLY, false>(R);
+    if (LD == LD_CGD && EP == EP_CGA && !MASK) return stencil_fn<LD_CGD, EP_CGA, false>(R);
+    if (LD == LD_X0 && EP == EP_RESID_INIT && MASK) return stencil_fn<LD_X0, EP_RESID_INIT, true>(R);
+    if (LD == LD_RAW && EP == EP_RESID_INIT && MASK) return stencil_fn<LD_RAW, EP_RESID_INIT, true>(R);
+    if (LD == LD_RAW && EP == EP_RESID && MASK) return stencil_fn<LD_RAW, EP_RESID, true>(R);
+    return nullptr;
+}
+
+static int rows_per_tile(int R) { return NW * R - 1; }
+
+// grid of the stencil over output planes [z0, z1)
+static void stencil_grid(const hf_ctx *c, int z0, int z1, dim3 *grid, int *zchunk)
+{
+    const int tx = (c->nx1 + TILE_X - 1) / TILE_X;
+    const int ty = (c->ny1 + rows_per_tile(c->tileR) - 1) / rows_per_tile(c->tileR);
+    const int planes = std::max(1, z1 - z0);
+    const long long cols = (long long)tx * ty;
+    const long long target = (long long)c->nsm * c->ctas_per_sm * 2;
+    long long nch = std::max(1LL, (target + cols - 1) / cols);
+    int chunk = (int)std::max(4LL, ((long long)planes + nch - 1) / nch);
+    chunk = std::min(chunk, planes);
+    nch = (planes + chunk - 1) / chunk;
+    *grid = dim3(tx, ty, (unsigned)nch);
+    *zchunk = chunk;
+}
+
+static Sync make_sync(hf_ctx *c, Sys &s)
+{
+    Sync y;
+    std::memset(&y, 0, sizeof(y));
+    y.st = s.st;
+    y.partials = s.partials;
+    y.ticket = s.ticket;
+    y.launches = c->launches;
+    y.sums_out = (c->nranks > 1) ? s.sums : nullptr;
+    y.use_handles = 0;
+    return y;
+}
+
+static StencilArgs base_args(hf_ctx *c, const double2 *kc, double aK, double aM)
+{
+    StencilArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.g = make_geom(c);
+    a.lam = make_lam(c->g.h, aK, aM);
+    a.kc = kc;
+    a.c = 1.0;
+    a.s = 0.0;
+    a.z_out0 = c->own_lo;
+    a.z_out1 = c->own_hi;
+    a.zs0 = c->own_lo;
+    a.zs1 = c->own_hi;
+    return a;
+}
+
+static Launch stencil_launch(hf_ctx *c, int LD, int EP, bool MASK, StencilArgs a, int cls)
+{
+    Launch L;
+    dim3 grid;
+    int chunk;
+    stencil_grid(c, a.z_out0, a.z_out1, &grid, &chunk);
+    a.zchunk = chunk;
+    L.fn = stencil_fn_dyn(c->tileR, LD, EP, MASK);
+    L.grid = grid;
+    L.block = dim3(32, NW, 1);
+    L.set(a);
+    L.cls = cls;
+    return L;
+}
+
+static int b_blocks(const hf_ctx *c) { return std::max(1, std::min((int)((c->nloc + 511) / 512), c->nsm * 4)); }
+
+static hf_status run(hf_ctx *c, const Launch &L, cudaStream_t s)
+{
+    void *args[1] = {(void *)L.arg.data()};
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->prof) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+    }
+    CUCK(cudaLaunchKernel(L.fn, L.grid, L.block, args, 0, s));
+    if (c->prof) {
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        c->prof_ms[L.cls] += ms;
+        c->prof_n[L.cls] += 1;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    return HF_OK;
+}
+
+static hf_status add_node(cudaGraph_t g, const Launch &L, cudaGraphNode_t *dep, cudaGraphNode_t *out)
+{
+    cudaKernelNodeParams p;
+    std::memset(&p, 0, sizeof(p));
+    void *args[1] = {(void *)L.arg.data()};
+    p.func = (void *)L.fn;
+    p.gridDim = L.grid;
+    p.blockDim = L.block;
+    p.kernelParams = args;
+    CUCK(cudaGraphAddKernelNode(out, g, dep, dep ? 1 : 0, &p));
+    return HF_OK;
+}
+
+// ============================================================================================
+// workspace
+
+static hf_status sys_alloc(hf_ctx *c, Sys &s, bool own_kc, cudaStream_t stream)
+{
+    const size_t vb = (size_t)c->nloc * sizeof(double);
+    for (int i = 0; i < 3; i++) CUCK(cudaMalloc(&s.U[i], vb));
+    CUCK(cudaMalloc(&s.b, vb));
+    CUCK(cudaMalloc(&s.r, vb));
+    CUCK(cudaMalloc(&s.q, vb));
+    CUCK(cudaMalloc(&s.invd, vb));
+    CUCK(cudaMalloc(&s.dbuf[0], vb));
+    CUCK(cudaMalloc(&s.dbuf[1], vb));
+    CUCK(cudaMemsetAsync(s.dbuf[0], 0, vb, stream));
+    CUCK(cudaMemsetAsync(s.dbuf[1], 0, vb, stream));
+    CUCK(cudaMalloc(&s.st, sizeof(CgState)));
+    CUCK(cudaMallocHost(&s.st_host, sizeof(CgState)));
+    CUCK(cudaMalloc(&s.partials, (size_t)c->max_blocks * NPART * sizeof(double)));
+    CUCK(cudaMalloc(&s.sums, NPART * sizeof(double)));
+    CUCK(cudaMalloc(&s.ticket, sizeof(unsigned)));
+    CUCK(cudaMemsetAsync(s.ticket, 0, sizeof(unsigned), stream));
+    CgState z;
+    std::memset(&z, 0, sizeof(z));
+    z.first_failed = -1;
+    CUCK(cudaMemcpyAsync(s.st, &z, sizeof(z), cudaMemcpyHostToDevice, stream));
+    if (own_kc) {
+        CUCK(cudaMalloc(&s.kc, (size_t)c->kc_elems * sizeof(double2)));
+        s.own_kc = true;
+    }
+    s.stream = stream;
+    CUCK(cudaStreamSynchronize(stream));
+    return HF_OK;
+}
+
+static void sys_free(Sys &s)
+{
+    for (int i = 0; i < 3; i++) cudaFree(s.U[i]);
+    cudaFree(s.b); cudaFree(s.r); cudaFree(s.q); cudaFree(s.invd);
+    cudaFree(s.dbuf[0]); cudaFree(s.dbuf[1]);
+    cudaFree(s.st); cudaFreeHost(s.st_host);
+    cudaFree(s.partials); cudaFree(s.sums); cudaFree(s.ticket); cudaFree(s.iters);
+    if (s.own_kc) cudaFree(s.kc);
+    if (s.gexec) cudaGraphExecDestroy(s.gexec);
+    if (s.graph) cudaGraphDestroy(s.graph);
+    if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
+    s = Sys();
+}
+
+static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream, int rank, int nranks)
+{
+    for (int d = 0; d < 3; d++)
+        if (g->ne[d] < 1 || !(g->h[d] > 0.0)) return fail(HF_E_ARG, "grid: ne must be >= 1 and h > 0");
+    c->g = *g;
+    c->device = device;
+    CUCK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUCK(cudaGetDeviceProperties(&prop, device));
+    c->nsm = prop.multiProcessorCount;
+    if (stream) c->stream = (cudaStream_t)stream;
+    else { CUCK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)); c->own_stream = true; }
+    c->nx1 = (int)g->ne[0] + 1;
+    c->ny1 = (int)g->ne[1] + 1;
+    c->nz1g = (int)g->ne[2] + 1;
+    c->rank = rank;
+    c->nranks = nranks;
+    int64_t lo = 0, hi = c->nz1g;
+    if (nranks > 1) HFCK(hf_slab_plan(c->nz1g, rank, nranks, &lo, &hi));
+    const int glo = (int)lo - (rank > 0 ? 1 : 0);
+    const int ghi = (int)hi + (rank < nranks - 1 ? 1 : 0);
+    c->zg0 = glo;
+    c->nzl = ghi - glo;
+    c->own_lo = (int)lo - glo;
+    c->own_hi = (int)hi - glo;
+    c->plane = (long long)c->nx1 * c->ny1;
+    c->nloc = c->plane * c->nzl;
+    c->kc_elems = (long long)(c->nx1 + 1) * (c->ny1 + 1) * (c->nzl + 1);
+    const double hx = g->h[0], hy = g->h[1], hz = g->h[2];
+    c->Kd = (hy * hz / hx + hx * hz / hy + hx * hy / hz) / 9.0;
+    c->Md = hx * hy * hz / 27.0;
+    if (const char *e = getenv("HF_TILE_R")) c->tileR = std::max(1, std::min(4, atoi(e)));
+    if (c->tileR == 3) c->tileR = 2;
+    if (const char *e = getenv("HF_CTAS_PER_SM")) c->ctas_per_sm = std::max(1, atoi(e));
+    if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e);
+    if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
+    dim3 grid;
+    int chunk;
+    stencil_grid(c, c->own_lo, c->own_hi, &grid, &chunk);
+    c->max_blocks = std::max((int)(grid.x * grid.y * grid.z), b_blocks(c));
+    c->max_blocks = std::max(c->max_blocks, c->nsm * 4);
+    CUCK(cudaMalloc(&c->launches, sizeof(unsigned long long)));
+    CUCK(cudaMemsetAsync(c->launches, 0, sizeof(unsigned long long), c->stream));
+    HFCK(sys_alloc(c, c->sys0, true, c->stream));
+    return HF_OK;
+}
+
+static void ctx_free(hf_ctx *c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    sys_free(c->sys0);
+    for (auto &p : c->pool) sys_free(*p);
+    c->pool.clear();
+    for (void *p : c->scratch) cudaFree(p);
+    cudaFree(c->launches);
+    cudaFree(c->flush);
+    delete c->comm;
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+}
+
+// ============================================================================================
+// building blocks
+
+static hf_status enqueue_pack(hf_ctx *c, Sys &s, const double *k, const double *cc)
+{
+    const long long n = c->kc_elems;
+    const int bs = 256;
+    k_pack<<<(unsigned)((n + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), (int)c->g.ne[0], (int)c->g.ne[1],
+                                                               (int)c->g.ne[2], k, cc, s.kc, n, c->launches);
+    CUCK(cudaGetLastError());
+    return HF_OK;
+}
+
+static hf_status enqueue_diag(hf_ctx *c, Sys &s, double aK, double aM, double *diag, double *invd)
+{
+    const int bs = 256;
+    k_diag<<<(unsigned)((c->nloc + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), s.kc, aK, aM, c->Kd, c->Md,
+                                                                     diag, invd, c->launches);
+    CUCK(cudaGetLastError());
+    return HF_OK;
+}
+
+static hf_status enqueue_set_dirichlet(hf_ctx *c, Sys &s, double *v, const double *src)
+{
+    if (!c->dbits) return HF_OK;
+    const int bs = 256;
+    k_set_dirichlet<<<(unsigned)((c->nloc + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), v, src, c->launches);
+    CUCK(cudaGetLastError());
+    return HF_OK;
+}
+
+// PCG kernels of one iteration for system s (operator lam), in order.
+struct CgLaunches {
+    Launch A, B, RES;
+};
+
+static CgLaunches cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x, bool rot)
+{
+    CgLaunches L;
+    Sync sy = make_sync(c, s);
+    // kernel A: d = P^{-1} r + beta d; q = A d; d^T q -> alpha   (Alg. 1 lines 7-8, 15, 18)
+    StencilArgs a = base_args(c, s.kc, aK, aM);
+    a.in0 = s.r;
+    a.in1 = s.invd;
+    a.dbuf[0] = s.dbuf[0];
+    a.dbuf[1] = s.dbuf[1];
+    a.out0 = s.q;
+    a.zs0 = c->own_lo - (c->own_lo > 0 ? 1 : 0);   // store d on ghost planes too (slab)
+    a.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
+    a.dmode = 1;
+    a.sy = sy;
+    L.A = stencil_launch(c, LD_CGD, EP_CGA, false, a, 0);
+    // kernel B: x += alpha d; r -= alpha q; s; r^T s, r^T r -> beta   (Alg. 1 lines 9-19)
+    BArgs b;
+    std::memset(&b, 0, sizeof(b));
+    b.x = x;
+    b.q = s.q;
+    b.invd = s.invd;
+    b.dbuf[0] = s.dbuf[0];
+    b.dbuf[1] = s.dbuf[1];
+    b.r = s.r;
+    b.n = c->nloc;
+    b.own0 = (long long)c->own_lo * c->plane;
+    b.own1 = (long long)c->own_hi * c->plane;
+    if (rot) for (int i = 0; i < 3; i++) b.rot[i] = s.U[i];
+    b.sy = sy;
+    L.B.fn = (const void *)k_cg_b<256>;
+    L.B.grid = dim3(b_blocks(c));
+    L.B.block = dim3(256);
+    L.B.set(b);
+    L.B.cls = 1;
+    // residual replacement r = b - A x every replace_every iterations (Alg. 1 lines 10-11)
+    StencilArgs rr = base_args(c, s.kc, aK, aM);
+    rr.in0 = x;
+    rr.in2 = s.invd;
+    rr.bvec = s.b;
+    rr.out0 = s.r;
+    rr.sy = sy;
+    if (rot) { rr.rot_role = ROT_X; for (int i = 0; i < 3; i++) rr.rot[i] = s.U[i]; }
+    L.RES = stencil_launch(c, LD_RAW, EP_RESID, true, rr, 2);
+    return L;
+}
+
+static hf_status comm_after(hf_ctx *c, Sys &s, int mode, bool exch_r)
+{
+    if (c->nranks <= 1) return HF_OK;
+    HFCK(c->comm->allreduce(c, s, s.sums, NPART));
+    Sync sy = make_sync(c, s);
+    k_finalize<<<1, 1, 0, s.stream>>>(sy, mode);
+    CUCK(cudaGetLastError());
+    if (exch_r) HFCK(c->comm->exchange(c, s, s.r));
+    return HF_OK;
+}
+
+static hf_status read_state(hf_ctx *c, Sys &s)
+{
+    CUCK(cudaMemcpyAsync(s.st_host, s.st, sizeof(CgState), cudaMemcpyDeviceToHost, s.stream));
+    CUCK(cudaStreamSynchronize(s.stream));
+    return HF_OK;
+}
+
+static hf_status set_solver_opts(hf_ctx *c, Sys &s, const hf_cg_opts *o, bool reset_steps)
+{
+    hf_cg_opts d = {1e-12, 10000, 50};
+    if (o) d = *o;
+    if (!(d.rtol >= 0.0) || d.max_iter < 0 || d.replace_every < 0) return fail(HF_E_ARG, "bad hf_cg_opts");
+    // write the option fields (and reset counters) with a tiny H2D of a prepared state image
+    CUCK(cudaMemcpyAsync(s.st_host, s.st, sizeof(CgState), cudaMemcpyDeviceToHost, s.stream));
+    CUCK(cudaStreamSynchronize(s.stream));
+    CgState h = *s.st_host;
+    h.rtol2 = d.rtol * d.rtol;
+    h.max_iter = d.max_iter;
+    h.replace_every = d.replace_every;
+    h.active = 0;
+    h.status = ST_OK;
+    if (reset_steps) {
+        h.step = 0;
+        h.first_failed = -1;
+        h.total_iters = 0;
+        h.max_iters_step = 0;
+        h.steps_done = 0;
+    }
+    *s.st_host = h;
+    CUCK(cudaMemcpyAsync(s.st, s.st_host, sizeof(CgState), cudaMemcpyHostToDevice, s.stream));
+    CUCK(cudaStreamSynchronize(s.stream));
+    return HF_OK;
+}
+
+static StepArgs step_args(hf_ctx *c, Sys &s, double *x, bool rot, double *snapdev, int snap_local)
+{
+    StepArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.g = make_geom(c);
+    a.x = x;
+    if (rot) for (int i = 0; i < 3; i++) a.rot[i] = s.U[i];
+    a.n = c->nloc;
+    a.snap = snapdev;
+    a.snap_plane = snap_local;
+    a.iters_out = s.iters;
+    a.sy = make_sync(c, s);
+    return a;
+}
+
+static Launch step_launch(hf_ctx *c, const StepArgs &a)
+{
+    Launch L;
+    L.fn = (const void *)k_step_end;
+    L.grid = dim3(std::max(1, std::min(c->nsm, (int)((c->nloc + 255) / 256))));
+    L.block = dim3(256);
+    L.set(a);
+    L.cls = 4;
+    return L;
+}
+
+// ---- host-loop PCG (profiling, slab transports) ------------------------------------------
+static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, int replace_every)
+{
+    HFCK(read_state(c, s));
+    if (!s.st_host->active) return HF_OK;
+    const bool slab = c->nranks > 1;
+    const int check = slab && !c->comm->graph_capturable() ? 1 : c->check_every;
+    for (int i = 0;; ) {
+        HFCK(run(c, L.A, s.stream));
+        HFCK(comm_after(c, s, EP_CGA, false));
+        const bool rep = i > 0 && replace_every > 0 && i % replace_every == 0;
+        HFCK(run(c, L.B, s.stream));
+        if (!rep) HFCK(comm_after(c, s, 100, true));
+        if (rep) {
+            HFCK(run(c, L.RES, s.stream));
+            HFCK(comm_after(c, s, EP_RESID, true));
+        }
+        i++;
+        if (i % check == 0 || i >= max_iter) {
+            HFCK(read_state(c, s));
+            if (!s.st_host->active) break;
+        }
+    }
+    return HF_OK;
+}
+
+// ---- graph with the device-side WHILE loop -------------------------------------------------
+// root: [pre...] -> init -> WHILE(active){ A -> B -> IF(replace){ RESID } } -> [post]
+static hf_status build_cg_graph(hf_ctx *c, Sys &s, std::vector<Launch> pre, Launch init, CgLaunches L,
+                                std::vector<Launch> post, cudaGraph_t *out)
+{
+    cudaGraph_t g;
+    CUCK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hw, hi;
+    CUCK(cudaGraphConditionalHandleCreate(&hw, g, 0, cudaGraphCondAssignDefault));
+    cudaGraphNode_t prev = nullptr, n;
+    for (auto &p : pre) { HFCK(add_node(g, p, prev ? &prev : nullptr, &n)); prev = n; }
+    // the init kernel and the loop body set the WHILE handle
+    StencilArgs ia;
+    std::memcpy(&ia, init.arg.data(), sizeof(ia));
+    ia.sy.h_while = hw;
+    ia.sy.use_handles = 1;
+    init.set(ia);
+    HFCK(add_node(g, init, prev ? &prev : nullptr, &n));
+    prev = n;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hw;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CUCK(cudaGraphAddNode(&wnode, g, &prev, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CUCK(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
+    {
+        StencilArgs aa;
+        std::memcpy(&aa, L.A.arg.data(), sizeof(aa));
+        aa.sy.h_while = hw; aa.sy.h_if = hi; aa.sy.use_handles = 1;
+        L.A.set(aa);
+        BArgs bb;
+        std::memcpy(&bb, L.B.arg.data(), sizeof(bb));
+        bb.sy.h_while = hw; bb.sy.h_if = hi; bb.sy.use_handles = 1;
+        L.B.set(bb);
+        StencilArgs ra;
+        std::memcpy(&ra, L.RES.arg.data(), sizeof(ra));
+        ra.sy.h_while = hw; ra.sy.h_if = hi; ra.sy.use_handles = 1;
+        L.RES.set(ra);
+    }
+    cudaGraphNode_t na, nb;
+    HFCK(add_node(body, L.A, nullptr, &na));
+    HFCK(add_node(body, L.B, &na, &nb));
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hi;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    CUCK(cudaGraphAddNode(&inode, body, &nb, 1, &ip));
+    cudaGraphNode_t nr;
+    HFCK(add_node(ip.conditional.phGraph_out[0], L.RES, nullptr, &nr));
+    prev = wnode;
+    for (auto &p : post) { HFCK(add_node(g, p, &prev, &n)); prev = n; }
+    *out = g;
+    return HF_OK;
+}
+
+// ============================================================================================
+// C ABI
+
+extern "C" {
+
+const char *hf_version(void) { return "heatfem-b200 0.1 (sm_100a)"; }
+
+const char *hf_last_error(void) { return g_err.c_str(); }
+
+hf_status hf_create(const hf_grid *g, int device, void *cuda_stream, hf_ctx **out)
+{
+    if (!g || !out) return fail(HF_E_ARG, "hf_create: NULL argument");
+    hf_ctx *c = new hf_ctx();
+    hf_status st = ctx_init(c, g, device, cuda_stream, 0, 1);
+    if (st != HF_OK) { ctx_free(c); delete c; return st; }
+    *out = c;
+    return HF_OK;
+}
+
+void hf_destroy(hf_ctx *c)
+{
+    if (!c) return;
+    ctx_free(c);
+    delete c;
+}
+
+hf_status hf_set_coefficients(hf_ctx *c, const double *k, const double *cc)
+{
+    if (!c || !k || !cc) return fail(HF_E_ARG, "hf_set_coefficients: NULL argument");
+    CUCK(cudaSetDevice(c->device));
+    const size_t ne = (size_t)(c->g.ne[0] * c->g.ne[1] * c->g.ne[2]);
+    const double *dk, *dc;
+    HFCK(dev_in(c, k, ne, 0, &dk));
+    HFCK(dev_in(c, cc, ne, 1, &dc));
+    HFCK(enqueue_pack(c, c->sys0, dk, dc));
+    CUCK(cudaStreamSynchronize(c->stream));
+    c->coef_set = true;
+    return HF_OK;
+}
+
+hf_status hf_set_dirichlet_faces(hf_ctx *c, uint32_t bits, const double values[6])
+{
+    if (!c || bits > 63u) return fail(HF_E_ARG, "hf_set_dirichlet_faces: bad argument");
+    c->dbits = bits;
+    for (int f = 0; f < 6; f++) c->gval[f] = values ? values[f] : 0.0;
+    c->sys0.key_valid = false;
+    for (auto &p : c->pool) p->key_valid = false;
+    return HF_OK;
+}
+
+hf_status hf_face_load(hf_ctx *c, int face, double f_const, const double beam[4], double *F)
+{
+    if (!c || !F || face < 0 || face > 5) return fail(HF_E_ARG, "hf_face_load: bad argument");
+    CUCK(cudaSetDevice(c->device));
+    double *dF;
+    HFCK(dev_out(c, F, c->nloc, 2, false, &dF));
+    CUCK(cudaMemsetAsync(dF, 0, c->nloc * sizeof(double), c->stream));
+    FaceArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.g = make_geom(c);
+    a.face = face;
+    a.nd = face / 2;
+    a.ax = a.nd == 0 ? 1 : 0;
+    a.bx = a.nd == 2 ? 1 : 2;
+    const int n1[3] = {c->nx1, c->ny1, c->nz1g};
+    a.na = n1[a.ax];
+    a.nb = n1[a.bx];
+    a.plane_g = (face & 1) ? (int)c->g.ne[a.nd] : 0;
+    a.ha = c->g.h[a.ax]; a.hb = c->g.h[a.bx];
+    a.oa = c->g.origin[a.ax]; a.ob = c->g.origin[a.bx];
+    a.f_const = f_const;
+    if (beam) { a.has_beam = 1; a.bP = beam[0]; a.bs = beam[1]; a.bca = beam[2]; a.bcb = beam[3]; }
+    if (beam && !(beam[1] > 0.0)) return fail(HF_E_ARG, "hf_face_load: beam sigma must be > 0");
+    a.F = dF;
+    a.launches = c->launches;
+    const long long n = (long long)a.na * a.nb;
+    k_face_load<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(a);
+    CUCK(cudaGetLastError());
+    return dev_out_finish(c, F, dF, c->nloc);
+}
+
+hf_status hf_apply_axpby(hf_ctx *c, double aK, double aM, double cc, const double *u, const double *b, double *y)
+{
+    if (!c || !u || !y) return fail(HF_E_ARG, "hf_apply: NULL argument");
+    if (!c->coef_set) return fail(HF_E_STATE, "hf_apply: coefficients not set");
+    if ((const double *)y == u) return fail(HF_E_ARG, "hf_apply: u and y must not alias");
+    CUCK(cudaSetDevice(c->device));
+    const double *du, *db = nullptr;
+    double *dy;
+    HFCK(dev_in(c, u, c->nloc, 3, &du));
+    if (b) HFCK(dev_in(c, b, c->nloc, 4, &db));
+    HFCK(dev_out(c, y, c->nloc, 5, false, &dy));
+    StencilArgs a = base_args(c, c->sys0.kc, aK, aM);
+    a.in0 = du;
+    a.out0 = dy;
+    a.bvec = db;
+    a.c = cc;
+    a.s = 1.0;
+    // every local plane is an output plane of a plain apply (ghost planes: partial sums)
+    Launch L = stencil_launch(c, LD_RAW, EP_APPLY, false, a, 3);
+    HFCK(run(c, L, c->stream));
+    return dev_out_finish(c, y, dy, c->nloc);
+}
+
+hf_status hf_apply(hf_ctx *c, double aK, double aM, const double *u, double *y)
+{
+    return hf_apply_axpby(c, aK, aM, 1.0, u, nullptr, y);
+}
+
+hf_status hf_diag(hf_ctx *c, double aK, double aM, double *diag)
+{
+    if (!c || !diag) return fail(HF_E_ARG, "hf_diag: NULL argument");
+    if (!c->coef_set) return fail(HF_E_STATE, "hf_diag: coefficients not set");
+    CUCK(cudaSetDevice(c->device));
+    double *dd;
+    HFCK(dev_out(c, diag, c->nloc, 5, false, &dd));
+    HFCK(enqueue_diag(c, c->sys0, aK, aM, dd, nullptr));
+    return dev_out_finish(c, diag, dd, c->nloc);
+}
+
+hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, const hf_cg_opts *opts,
+                hf_cg_info *info)
+{
+    if (!c || !b || !x) return fail(HF_E_ARG, "hf_cg: NULL argument");
+    if (!c->coef_set) return fail(HF_E_STATE, "hf_cg: coefficients not set");
+    CUCK(cudaSetDevice(c->device));
+    Sys &s = c->sys0;
+    hf_cg_opts o = {1e-12, 10000, 50};
+    if (opts) o = *opts;
+    HFCK(set_solver_opts(c, s, &o, true));
+    const double *db;
+    double *dx;
+    HFCK(dev_in(c, b, c->nloc, 4, &db));
+    HFCK(dev_out(c, x, c->nloc, 6, true, &dx));
+    CUCK(cudaMemcpyAsync(s.b, db, c->nloc * sizeof(double), cudaMemcpyDeviceToDevice, s.stream));
+    HFCK(enqueue_diag(c, s, aK, aM, nullptr, s.invd));
+    HFCK(enqueue_set_dirichlet(c, s, dx, s.b));           // x_D = b_D
+    if (c->nranks > 1) HFCK(c->comm->exchange(c, s, dx));
+    // init: r = b - A x0; s = P^{-1} r; delta; ||b_F||   (Alg. 1 lines 2-4)
+    StencilArgs ia = base_args(c, s.kc, aK, aM);
+    ia.in0 = dx;
+    ia.in2 = s.invd;
+    ia.bvec = s.b;
+    ia.out0 = s.r;
+    ia.out1 = dx;
+    ia.sy = make_sync(c, s);
+    Launch init = stencil_launch(c, LD_RAW, EP_RESID_INIT, true, ia, 2);
+    CgLaunches L = cg_launches(c, s, aK, aM, dx, false);
+    StepArgs sa = step_args(c, s, dx, false, nullptr, -1);
+    sa.iters_out = nullptr;
+    Launch post = step_launch(c, sa);
+    const bool use_graph = c->driver == 0 && c->nranks == 1 && !c->prof;
+    if (use_graph) {
+        cudaGraph_t g;
+        HFCK(build_cg_graph(c, s, {}, init, L, {post}, &g));
+        cudaGraphExec_t ge;
+        cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+        if (e != cudaSuccess) { cudaGraphDestroy(g); CUCK(e); }
+        e = cudaGraphLaunch(ge, s.stream);
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        CUCK(e);
+    } else {
+        HFCK(run(c, init, s.stream));
+        HFCK(comm_after(c, s, EP_RESID_INIT, true));
+        HFCK(host_cg_loop(c, s, L, o.max_iter, o.replace_every));
+        HFCK(run(c, post, s.stream));
+    }
+    HFCK(read_state(c, s));
+    HFCK(dev_out_finish(c, x, dx, c->nloc));
+    const CgState &h = *s.st_host;
+    if (info) {
+        info->iters = h.iter;
+        info->status = h.status;
+        info->relres = h.bb > 0 ? std::sqrt(h.rr / h.bb) : 0.0;
+        info->delta = h.delta;
+    }
+    if (h.status == ST_NOCONV) return fail(HF_E_NOCONV, "hf_cg: max_iter reached");
+    if (h.status == ST_BREAKDOWN) return fail(HF_E_BREAKDOWN, "hf_cg: breakdown (d^T q <= 0 or non-finite)");
+    return HF_OK;
+}
+
+// One system's time loop; U[0] holds u^0 (and U[2] u^{-1} when resuming) on entry.
+static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int nsteps, const double *dF,
+                              bool first, int snap_local, double *snapdev, const hf_cg_opts &o)
+{
+    const double aK = theta * dt, aM = 1.0;             // A = M + theta dt K
+    const double aKL = -(1.0 - theta) * dt, aML = 1.0;  // L = M - (1-theta) dt K   (R8)
+    HFCK(set_solver_opts(c, s, &o, true));
+    if (s.iters_cap < nsteps) {
+        cudaFree(s.iters);
+        s.iters = nullptr;
+        CUCK(cudaMalloc(&s.iters, (size_t)std::max(1, nsteps) * sizeof(int)));
+        s.iters_cap = nsteps;
+        s.key_valid = false;
+    }
+    HFCK(enqueue_diag(c, s, aK, aM, nullptr, s.invd));
+    HFCK(enqueue_set_dirichlet(c, s, s.U[0], nullptr));       // u^0_D = g
+    if (!first) HFCK(enqueue_set_dirichlet(c, s, s.U[2], nullptr));
+    bool lift = false;
+    for (int f = 0; f < 6; f++) if ((c->dbits >> f & 1u) && c->gval[f] != 0.0) lift = true;
+    if (nsteps <= 0) return HF_OK;
+
+    Sync sy = make_sync(c, s);
+    // b = L u^n + dt F  (knl_RHS_A/B P:678-681), b_D = g
+    StencilArgs ra = base_args(c, s.kc, aKL, aML);
+    ra.bvec = dF;
+    ra.s = dt;
+    ra.out0 = s.b;
+    ra.dmode = 2;
+    ra.rot_role = ROT_RHS;
+    for (int i = 0; i < 3; i++) ra.rot[i] = s.U[i];
+    ra.sy = sy;
+    ra.sy.partials = nullptr;
+    std::vector<Launch> pre;
+    pre.push_back(stencil_launch(c, LD_RAW, EP_APPLY, false, ra, 3));
+    if (lift) {  // b_F -= (A g~)_F  (Dirichlet lift, R3)
+        StencilArgs la = base_args(c, s.kc, aK, aM);
+        la.bvec = s.b;
+        la.s = 1.0;
+        la.c = -1.0;
+        la.out0 = s.b;
+        la.dmode = 2;
+        la.sy = sy;
+        pre.push_back(stencil_launch(c, LD_GT, EP_APPLY, false, la, 3));
+    }
+    // init with the extrapolated guess x0 = 2u^n - u^{n-1} (u0_update)
+    StencilArgs ia = base_args(c, s.kc, aK, aM);
+    ia.in2 = s.invd;
+    ia.bvec = s.b;
+    ia.out0 = s.r;
+    ia.first = first ? 1 : 0;
+    ia.rot_role = ROT_INIT;
+    for (int i = 0; i < 3; i++) ia.rot[i] = s.U[i];
+    ia.sy = sy;
+    ia.zs0 = c->own_lo - (c->own_lo > 0 ? 1 : 0);
+    ia.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
+    Launch init = stencil_launch(c, LD_X0, EP_RESID_INIT, true, ia, 2);
+    CgLaunches L = cg_launches(c, s, aK, aM, nullptr, true);
+    StepArgs sa = step_args(c, s, nullptr, true, snapdev, snap_local);
+    Launch post = step_launch(c, sa);
+
+    const bool use_graph = c->driver == 0 && c->nranks == 1 && !c->prof;
+    if (use_graph) {
+        SimKey key;
+        std::memset(&key, 0, sizeof(key));
+        key.aK = aK; key.aM = aM; key.aKL = aKL; key.aML = aML; key.rtol = o.rtol;
+        key.max_iter = o.max_iter; key.replace_every = o.replace_every; key.first = first;
+        key.snap_plane = snap_local; key.lift = lift; key.F = dF; key.snap = snapdev; key.dt = dt;
+        key.ubase = s.U[0];
+        if (!s.key_valid || !(s.key == key)) {
+            if (s.gexec) { cudaGraphExecDestroy(s.gexec); s.gexec = nullptr; }
+            if (s.graph) { cudaGraphDestroy(s.graph); s.graph = nullptr; }
+            HFCK(build_cg_graph(c, s, pre, init, L, {post}, &s.graph));
+            CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
+            s.key = key;
+            s.key_valid = true;
+        }
+        for (int n = 0; n < nsteps; n++) CUCK(cudaGraphLaunch(s.gexec, s.stream));
+    } else {
+        for (int n = 0; n < nsteps; n++) {
+            for (auto &p : pre) HFCK(run(c, p, s.stream));
+            if (c->nranks > 1) {
+                // ghost planes of b are never read; x0 ghosts are stored by the init kernel
+            }
+            HFCK(run(c, init, s.stream));
+            HFCK(comm_after(c, s, EP_RESID_INIT, true));
+            HFCK(host_cg_loop(c, s, L, o.max_iter, o.replace_every));
+            HFCK(run(c, post, s.stream));
+            if (c->nranks > 1) {
+                HFCK(read_state(c, s));
+                if (s.st_host->first_failed >= 0) break;
+            }
+        }
+    }
+    return HF_OK;
+}
+
+static hf_status finish_stats(hf_ctx *c, Sys &s, hf_sim_stats *stats, float ms)
+{
+    HFCK(read_state(c, s));
+    const CgState &h = *s.st_host;
+    if (stats) {
+        stats->steps_done = h.steps_done;
+        stats->total_iters = h.total_iters;
+        stats->max_iters_step = h.max_iters_step;
+        stats->first_failed_step = h.first_failed;
+        stats->ms_total = ms;
+    }
+    if (h.first_failed >= 0) {
+        if (h.status == ST_BREAKDOWN) return fail(HF_E_BREAKDOWN, "hf_simulate: PCG breakdown");
+        return fail(HF_E_NOCONV, "hf_simulate: PCG did not converge");
+    }
+    return HF_OK;
+}
+
+static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nsteps, const double *F, double *u,
+                                 const double *u_prev, int64_t step0, int64_t snap_plane, double *snap,
+                                 const hf_cg_opts *opts, hf_sim_stats *stats)
+{
+    if (!c || !u || nsteps < 0 || !(dt > 0.0) || !(theta >= 0.0 && theta <= 1.0))
+        return fail(HF_E_ARG, "hf_simulate: bad argument");
+    if (!c->coef_set) return fail(HF_E_STATE, "hf_simulate: coefficients not set");
+    if (snap && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "hf_simulate: snap_plane");
+    CUCK(cudaSetDevice(c->device));
+    Sys &s = c->sys0;
+    hf_cg_opts o = {1e-12, 10000, 50};
+    if (opts) o = *opts;
+    const double *dF = nullptr;
+    if (F) HFCK(dev_in(c, F, c->nloc, 7, &dF));
+    else {
+        void *z;
+        HFCK(scratch_get(c, 7, c->nloc * sizeof(double), &z));
+        CUCK(cudaMemsetAsync(z, 0, c->nloc * sizeof(double), c->stream));
+        dF = (const double *)z;
+    }
+    CUCK(cudaMemcpyAsync(s.U[0], u, c->nloc * sizeof(double), cudaMemcpyDefault, s.stream));
+    const bool first = step0 <= 0 || !u_prev;
+    if (!first) CUCK(cudaMemcpyAsync(s.U[2], u_prev, c->nloc * sizeof(double), cudaMemcpyDefault, s.stream));
+    if (c->nranks > 1) {          // make the ghost planes of the input state consistent
+        HFCK(c->comm->exchange(c, s, s.U[0]));
+        if (!first) HFCK(c->comm->exchange(c, s, s.U[2]));
+    }
+    int snap_local = -1;
+    double *snapdev = nullptr;
+    if (snap) {
+        snap_local = (int)(snap_plane - c->zg0);
+        if (snap_local < 0 || snap_local >= c->nzl) snap_local = -1;
+        void *z;
+        HFCK(scratch_get(c, 8, (size_t)std::max(1, nsteps) * c->plane * sizeof(double), &z));
+        snapdev = (double *)z;
+    }
+    cudaEvent_t e0, e1;
+    CUCK(cudaEventCreate(&e0));
+    CUCK(cudaEventCreate(&e1));
+    CUCK(cudaEventRecord(e0, s.stream));
+    hf_status st = simulate_sys(c, s, theta, dt, nsteps, dF, first, snap_local, snapdev, o);
+    CUCK(cudaEventRecord(e1, s.stream));
+    if (st != HF_OK) { cudaEventDestroy(e0); cudaEventDestroy(e1); return st; }
+    CUCK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    hf_status fs = finish_stats(c, s, stats, ms);
+    // the newest iterate sits in U[steps_done % 3] (or U[(failed+1) % 3])
+    const CgState &h = *s.st_host;
+    const int last = h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done;
+    CUCK(cudaMemcpyAsync(u, s.U[last % 3], c->nloc * sizeof(double), cudaMemcpyDefault, s.stream));
+    if (snap && snap_local >= 0)
+        CUCK(cudaMemcpyAsync(snap, snapdev, (size_t)nsteps * c->plane * sizeof(double), cudaMemcpyDefault, s.stream));
+    CUCK(cudaStreamSynchronize(s.stream));
+    return fs;
+}
+
+hf_status hf_simulate(hf_ctx *c, double theta, double dt, int32_t nsteps, const double *F, double *u,
+                      int64_t snap_plane, double *snap, const hf_cg_opts *opts, hf_sim_stats *stats)
+{
+    return simulate_common(c, theta, dt, nsteps, F, u, nullptr, 0, snap_plane, snap, opts, stats);
+}
+
+hf_status hf_simulate_resume(hf_ctx *c, double theta, double dt, int32_t nsteps, const double *F, double *u,
+                             double *u_prev, int64_t step0, const hf_cg_opts *opts, hf_sim_stats *stats)
+{
+    if (!c || !u) return fail(HF_E_ARG, "hf_simulate_resume: NULL argument");
+    if (step0 > 0 && !u_prev) return fail(HF_E_ARG, "hf_simulate_resume: u_prev needed for step0 > 0");
+    hf_status st = simulate_common(c, theta, dt, nsteps, F, u, u_prev, step0, -1, nullptr, opts, stats);
+    if (st != HF_OK && st != HF_E_NOCONV && st != HF_E_BREAKDOWN) return st;
+    // u_prev <- u^{n-1} of the new state (the ring slot before the newest)
+    if (u_prev && nsteps > 0) {
+        Sys &s = c->sys0;
+        const CgState &h = *s.st_host;
+        const int last = h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done;
+        CUCK(cudaMemcpyAsync(u_prev, s.U[(last + 2) % 3], c->nloc * sizeof(double), cudaMemcpyDefault, s.stream));
+        CUCK(cudaStreamSynchronize(s.stream));
+    }
+    return st;
+}
+
+hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const double *c_batch, double theta,
+                              double dt, int32_t nsteps, const double *F, double *u_batch, int64_t snap_plane,
+                              double *front_out, const hf_cg_opts *opts, hf_sim_stats *stats)
+{
+    if (!c || B < 0 || !k_batch || !u_batch || nsteps < 0 || !(dt > 0.0))
+        return fail(HF_E_ARG, "hf_simulate_batched: bad argument");
+    if (!c_batch && !c->coef_set) return fail(HF_E_STATE, "hf_simulate_batched: no capacity field");
+    if (c->nranks > 1) return fail(HF_E_ARG, "hf_simulate_batched: not available on slab contexts");
+    if (front_out && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "snap_plane");
+    CUCK(cudaSetDevice(c->device));
+    hf_cg_opts o = {1e-12, 10000, 50};
+    if (opts) o = *opts;
+    int nslots = 2;
+    if (const char *e = getenv("HF_BATCH_STREAMS")) nslots = std::max(1, atoi(e));
+    nslots = std::min(nslots, std::max(1, (int)B));
+    while ((int)c->pool.size() < nslots) {
+        std::unique_ptr<Sys> p(new Sys());
+        cudaStream_t st;
+        CUCK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        HFCK(sys_alloc(c, *p, true, st));
+        p->own_stream = true;
+        c->pool.push_back(std::move(p));
+    }
+    const size_t ne = (size_t)(c->g.ne[0] * c->g.ne[1] * c->g.ne[2]);
+    const size_t nn = (size_t)c->nloc;
+    const double *dF = nullptr;
+    if (F) HFCK(dev_in(c, F, nn, 7, &dF));
+    else {
+        void *z;
+        HFCK(scratch_get(c, 7, nn * sizeof(double), &z));
+        CUCK(cudaMemsetAsync(z, 0, nn * sizeof(double), c->stream));
+        dF = (const double *)z;
+    }
+    const bool kdev = is_device_ptr(k_batch), udev = is_device_ptr(u_batch);
+    const bool cdev = c_batch && is_device_ptr(c_batch);
+    // per-slot staging of the host inputs: k, c (per element) and u (per node)
+    std::vector<double *> kst(nslots, nullptr), cst(nslots, nullptr);
+    for (int i = 0; i < nslots; i++) {
+        void *p;
+        if (!kdev) { HFCK(scratch_get(c, 20 + i, ne * sizeof(double), &p)); kst[i] = (double *)p; }
+        if (c_batch && !cdev) { HFCK(scratch_get(c, 40 + i, ne * sizeof(double), &p)); cst[i] = (double *)p; }
+    }
+    CUCK(cudaStreamSynchronize(c->stream));
+    cudaEvent_t ready;
+    CUCK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CUCK(cudaEventRecord(ready, c->stream));
+    hf_status first_err = HF_OK;
+    std::vector<int> done_sys(nslots, -1);
+    auto collect = [&](int slot, int j) -> hf_status {
+        Sys &s = *c->pool[slot];
+        HFCK(read_state(c, s));
+        const CgState &h = *s.st_host;
+        const int last = h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done;
+        CUCK(cudaMemcpyAsync(u_batch + (size_t)j * nn, s.U[last % 3], nn * sizeof(double), cudaMemcpyDefault, s.stream));
+        if (front_out) {
+            const int sl = (int)(snap_plane - c->zg0);
+            CUCK(cudaMemcpyAsync(front_out + (size_t)j * c->plane, s.U[last % 3] + (size_t)sl * c->plane,
+                                 c->plane * sizeof(double), cudaMemcpyDefault, s.stream));
+        }
+        if (stats) {
+            stats[j].steps_done = h.steps_done;
+            stats[j].total_iters = h.total_iters;
+            stats[j].max_iters_step = h.max_iters_step;
+            stats[j].first_failed_step = h.first_failed;
+            stats[j].ms_total = 0;
+        }
+        if (h.first_failed >= 0 && first_err == HF_OK)
+            first_err = h.status == ST_BREAKDOWN ? HF_E_BREAKDOWN : HF_E_NOCONV;
+        return HF_OK;
+    };
+    for (int j = 0; j < B; j++) {
+        const int slot = j % nslots;
+        Sys &s = *c->pool[slot];
+        CUCK(cudaStreamWaitEvent(s.stream, ready, 0));
+        if (done_sys[slot] >= 0) { HFCK(collect(slot, done_sys[slot])); done_sys[slot] = -1; }
+        const double *kj = k_batch + (size_t)j * ne;
+        if (!kdev) { CUCK(cudaMemcpyAsync(kst[slot], kj, ne * sizeof(double), cudaMemcpyHostToDevice, s.stream)); kj = kst[slot]; }
+        const double *cj = nullptr;
+        if (c_batch) {
+            cj = c_batch + (size_t)j * ne;
+            if (!cdev) { CUCK(cudaMemcpyAsync(cst[slot], cj, ne * sizeof(double), cudaMemcpyHostToDevice, s.stream)); cj = cst[slot]; }
+        }
+        if (cj) HFCK(enqueue_pack(c, s, kj, cj));
+        else {
+            // shared capacity: k from this system, c copied from the context's packed array
+            HFCK(enqueue_pack(c, s, kj, kj));   // placeholder c lane, overwritten below
+            // copy the capacity lane of the context's packed array (strided y of double2)
+            CUCK(cudaMemcpy2DAsync((char *)s.kc + sizeof(double), sizeof(double2), (const char *)c->sys0.kc + sizeof(double),
+                                   sizeof(double2), sizeof(double), (size_t)c->kc_elems, cudaMemcpyDeviceToDevice, s.stream));
+        }
+        const double *uj = u_batch + (size_t)j * nn;
+        CUCK(cudaMemcpyAsync(s.U[0], uj, nn * sizeof(double), udev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s.stream));
+        HFCK(simulate_sys(c, s, theta, dt, nsteps, dF, true, -1, nullptr, o));
+        done_sys[slot] = j;
+    }
+    for (int i = 0; i < nslots; i++)
+        if (done_sys[i] >= 0) HFCK(collect(i, done_sys[i]));
+    for (int i = 0; i < nslots; i++) CUCK(cudaStreamSynchronize(c->pool[i]->stream));
+    cudaEventDestroy(ready);
+    if (first_err != HF_OK) return fail(first_err, "hf_simulate_batched: a system failed to converge");
+    return HF_OK;
+}
+
+// ============================================================================================
+// slabs
+
+hf_status hf_slab_plan(int64_t nz1, int32_t rank, int32_t nranks, int64_t *z_lo, int64_t *z_hi)
+{
+    if (nranks < 1 || rank < 0 || rank >= nranks || !z_lo || !z_hi) return fail(HF_E_ARG, "hf_slab_plan: bad argument");
+    if (nz1 < 2LL * nranks) return fail(HF_E_PARTITION, "hf_slab_plan: fewer than 2 node planes per rank");
+    const int64_t base = nz1 / nranks, rem = nz1 % nranks;
+    *z_lo = rank * base + std::min<int64_t>(rank, rem);
+    *z_hi = *z_lo + base + (rank < rem ? 1 : 0);
+    return HF_OK;
+}
+
+hf_status hf_nccl_unique_id(uint8_t id[128])
+{
+    if (!id) return fail(HF_E_ARG, "hf_nccl_unique_id: NULL");
+    HFCK(nccl::load());
+    nccl::ncclUniqueId u;
+    NCCK(nccl::g_api.getUniqueId(&u));
+    std::memcpy(id, u.internal, 128);
+    return HF_OK;
+}
+
+// ---- NCCL transport ------------------------------------------------------------------------
+struct NcclComm : Comm {
+    nccl::ncclComm_t comm = nullptr;
+    ~NcclComm() override { if (comm) nccl::g_api.commDestroy(comm); }
+    bool graph_capturable() const override { return true; }
+    hf_status exchange(hf_ctx *c, Sys &s, double *v) override
+    {
+        const size_t P = (size_t)c->plane;
+        NCCK(nccl::g_api.groupStart());
+        if (c->rank > 0) {
+            NCCK(nccl::g_api.send(v + (size_t)c->own_lo * P, P, nccl::ncclFloat64, c->rank - 1, comm, s.stream));
+            NCCK(nccl::g_api.recv(v + (size_t)(c->own_lo - 1) * P, P, nccl::ncclFloat64, c->rank - 1, comm, s.stream));
+        }
+        if (c->rank < c->nranks - 1) {
+            NCCK(nccl::g_api.send(v + (size_t)(c->own_hi - 1) * P, P, nccl::ncclFloat64, c->rank + 1, comm, s.stream));
+            NCCK(nccl::g_api.recv(v + (size_t)c->own_hi * P, P, nccl::ncclFloat64, c->rank + 1, comm, s.stream));
+        }
+        NCCK(nccl::g_api.groupEnd());
+        return HF_OK;
+    }
+    hf_status allreduce(hf_ctx *c, Sys &s, double *v, int n) override
+    {
+        NCCK(nccl::g_api.allReduce(v, v, (size_t)n, nccl::ncclFloat64, nccl::ncclSum, comm, s.stream));
+        return HF_OK;
+    }
+};
+
+// ---- in-process transport (all ranks in one process, one host thread each) -----------------
+}  // extern "C"
+
+struct hf_local_group {
+    int n = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long gen = 0;
+    std::vector<hf_ctx *> ctx;
+    std::vector<double *> vecs;   // vector each rank published for the current exchange
+    std::vector<double> slots;    // NPART partial sums per rank
+    void barrier()
+    {
+        std::unique_lock<std::mutex> lk(mu);
+        const long long g = gen;
+        if (++arrived == n) { arrived = 0; gen++; cv.notify_all(); }
+        else cv.wait(lk, [&] { return gen != g; });
+    }
+};
+
+struct LocalComm : Comm {
+    hf_local_group *grp = nullptr;
+    bool graph_capturable() const override { return false; }
+    hf_status exchange(hf_ctx *c, Sys &s, double *v) override
+    {
+        // publish v, wait until every rank's data is final, then pull the neighbours' owned
+        // boundary planes into our ghost planes (peer copies; same or different device)
+        CUCK(cudaStreamSynchronize(s.stream));
+        {
+            std::lock_guard<std::mutex> lk(grp->mu);
+            grp->vecs[c->rank] = v;
+        }
+        grp->barrier();
+        const size_t P = (size_t)c->plane;
+        if (c->rank > 0) {
+            hf_ctx *o = grp->ctx[c->rank - 1];
+            const double *ov = grp->vecs[c->rank - 1];
+            CUCK(cudaMemcpyPeerAsync(v + (size_t)(c->own_lo - 1) * P, c->device, ov + (size_t)(o->own_hi - 1) * P,
+                                     o->device, P * sizeof(double), s.stream));
+        }
+        if (c->rank < c->nranks - 1) {
+            hf_ctx *o = grp->ctx[c->rank + 1];
+            const double *ov = grp->vecs[c->rank + 1];
+            CUCK(cudaMemcpyPeerAsync(v + (size_t)c->own_hi * P, c->device, ov + (size_t)o->own_lo * P, o->device,
+                                     P * sizeof(double), s.stream));
+        }
+        CUCK(cudaStreamSynchronize(s.stream));
+        grp->barrier();
+        return HF_OK;
+    }
+    hf_status allreduce(hf_ctx *c, Sys &s, double *v, int n) override
+    {
+        double h[NPART];
+        CUCK(cudaMemcpyAsync(h, v, n * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+        CUCK(cudaStreamSynchronize(s.stream));
+        {
+            std::lock_guard<std::mutex> lk(grp->mu);
+            for (int j = 0; j < n; j++) grp->slots[(size_t)c->rank * NPART + j] = h[j];
+        }
+        grp->barrier();
+        double tot[NPART] = {0, 0, 0, 0};
+        for (int r = 0; r < grp->n; r++)       // fixed rank order: identical on every rank
+            for (int j = 0; j < n; j++) tot[j] += grp->slots[(size_t)r * NPART + j];
+        grp->barrier();
+        CUCK(cudaMemcpyAsync(v, tot, n * sizeof(double), cudaMemcpyHostToDevice, s.stream));
+        CUCK(cudaStreamSynchronize(s.stream));
+        return HF_OK;
+    }
+};
+
+extern "C" {
+
+hf_status hf_local_group_create(int32_t nranks, hf_local_group **out)
+{
+    if (nranks < 1 || !out) return fail(HF_E_ARG, "hf_local_group_create: bad argument");
+    hf_local_group *g = new hf_local_group();
+    g->n = nranks;
+    g->ctx.assign(nranks, nullptr);
+    g->vecs.assign(nranks, nullptr);
+    g->slots.assign((size_t)nranks * NPART, 0.0);
+    *out = g;
+    return HF_OK;
+}
+
+void hf_local_group_destroy(hf_local_group *g) { delete g; }
+
+hf_status hf_create_slab(const hf_grid *g, int32_t rank, int32_t nranks, const uint8_t *id, int32_t transport,
+                         int device, void *cuda_stream, hf_ctx **out)
+{
+    if (!g || !out || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(HF_E_ARG, "hf_create_slab: bad argument");
+    hf_ctx *c = new hf_ctx();
+    hf_status st = ctx_init(c, g, device, cuda_stream, rank, nranks);
+    if (st != HF_OK) { ctx_free(c); delete c; return st; }
+    if (transport == 0) {
+        st = nccl::load();
+        if (st == HF_OK) {
+            NcclComm *nc = new NcclComm();
+            nccl::ncclUniqueId u;
+            std::memcpy(u.internal, id, 128);
+            nccl::ncclResult_t r = nccl::g_api.commInitRank(&nc->comm, nranks, u, rank);
+            if (r != 0) { st = fail(HF_E_NCCL, std::string("ncclCommInitRank: ") + nccl::g_api.getErrorString(r)); delete nc; }
+            else c->comm = nc;
+        }
+    } else if (transport == 1) {
+        hf_local_group *grp = (hf_local_group *)id;
+        if (grp->n != nranks) st = fail(HF_E_ARG, "hf_create_slab: group size != nranks");
+        else {
+            LocalComm *lc = new LocalComm();
+            lc->grp = grp;
+            {
+                std::lock_guard<std::mutex> lk(grp->mu);
+                grp->ctx[rank] = c;
+            }
+            c->comm = lc;
+            grp->barrier();
+        }
+    } else st = fail(HF_E_ARG, "hf_create_slab: unknown transport");
+    if (st != HF_OK) { ctx_free(c); delete c; return st; }
+    *out = c;
+    return HF_OK;
+}
+
+hf_status hf_slab_range(const hf_ctx *c, int64_t *z_lo, int64_t *z_hi, int64_t *local_planes, int64_t *local_z0)
+{
+    if (!c) return fail(HF_E_ARG, "hf_slab_range: NULL");
+    if (z_lo) *z_lo = c->zg0 + c->own_lo;
+    if (z_hi) *z_hi = c->zg0 + c->own_hi;
+    if (local_planes) *local_planes = c->nzl;
+    if (local_z0) *local_z0 = c->zg0;
+    return HF_OK;
+}
+
+hf_status hf_get_launch_count(hf_ctx *c, int64_t *count)
+{
+    if (!c || !count) return fail(HF_E_ARG, "hf_get_launch_count: NULL");
+    unsigned long long v = 0;
+    CUCK(cudaMemcpyAsync(&v, c->launches, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+    CUCK(cudaStreamSynchronize(c->stream));
+    *count = (int64_t)v;
+    return HF_OK;
+}
+
+hf_status hf_profile(hf_ctx *c, int32_t enable)
+{
+    if (!c) return fail(HF_E_ARG, "hf_profile: NULL");
+    c->prof = enable != 0;
+    for (int i = 0; i < 5; i++) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
+    return HF_OK;
+}
+
+hf_status hf_profile_read(hf_ctx *c, double ms[5], int64_t n[5])
+{
+    if (!c) return fail(HF_E_ARG, "hf_profile_read: NULL");
+    for (int i = 0; i < 5; i++) {
+        if (ms) ms[i] = c->prof_ms[i];
+        if (n) n[i] = c->prof_n[i];
+    }
+    return HF_OK;
+}
+
+hf_status hf_set_driver(hf_ctx *c, int32_t driver)
+{
+    if (!c || driver < 0 || driver > 1) return fail(HF_E_ARG, "hf_set_driver: bad argument");
+    c->driver = driver;
+    return HF_OK;
+}
+
+hf_status hf_flush_l2(hf_ctx *c)
+{
+    if (!c) return fail(HF_E_ARG, "hf_flush_l2: NULL");
+    const size_t bytes = 512ull << 20;   // 4x the 126 MB L2
+    if (!c->flush) CUCK(cudaMalloc(&c->flush, bytes));
+    CUCK(cudaMemsetAsync(c->flush, c->launches ? 1 : 0, bytes, c->stream));
+    return HF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,419 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, element by element.
+
+Bars: operator apply / diagonal / load max-abs error <= 1e-12 of the
+output scale (rounding-order differences only); PCG and time-step solutions rel-L2 <= 1e-10
+(BASELINE.json north_star) at rtol 1e-12.
+"""
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1905_07622_b200 as hf  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def T(a):
+    return torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device=DEV)
+
+
+def N(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def maxerr(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def make_ctx(grid, k, c, tile_r=None):
+    if tile_r is not None:
+        os.environ["HF_TILE_R"] = str(tile_r)
+    try:
+        ctx = hf.hf_create(grid, 0)
+    finally:
+        os.environ.pop("HF_TILE_R", None)
+    hf.hf_set_coefficients(ctx, T(k), T(c))
+    return ctx
+
+
+GRIDS = {
+    "1x1x1": synth.Grid((1, 1, 1), (1.0, 1.0, 1.0)),
+    "c1": synth.Grid((8, 8, 8), (0.125, 0.125, 0.125)),
+    "c2bar": synth.Grid((64, 4, 4), (1 / 64, 1 / 64, 1 / 64)),
+    "ragged": synth.Grid((70, 40, 13), (0.3, 0.2, 0.7), (-1.0, 2.0, 0.5)),
+    "seams": synth.Grid((33, 65, 9), (0.2, 0.2, 0.2)),
+    "tall": synth.Grid((5, 3, 60), (0.1, 0.4, 0.05)),
+}
+
+
+# ---------------------------------------------------------------------------------------------
+# operator apply (Eq. (1))
+
+@pytest.mark.parametrize("tile_r", [1, 2, 4])
+@pytest.mark.parametrize("gname", list(GRIDS))
+def test_apply_matches_assembled(gname, tile_r):
+    g = GRIDS[gname]
+    k, c = synth.random_fields(g, seed=1)
+    o = oracle.Oracle(g, k, c)
+    ctx = make_ctx(g, k, c, tile_r)
+    u = synth.random_vector(g.n_nodes, seed=2)
+    ud = T(u)
+    y = torch.empty_like(ud)
+    for aK, aM in [(1.0, 0.0), (0.0, 1.0), (0.005, 1.0), (-0.005, 1.0)]:
+        hf.hf_apply(ctx, aK, aM, ud, y)
+        yo = o.spmv(aK, aM, u)
+        assert maxerr(N(y), yo) <= 1e-12, (gname, aK, aM)
+    # fused axpby (FGDbDMVM_C): y = c A u + b
+    b = synth.random_vector(g.n_nodes, seed=3)
+    hf.hf_apply_axpby(ctx, 0.01, 1.0, -1.0, ud, T(b), y)
+    assert maxerr(N(y), b - o.spmv(0.01, 1.0, u)) <= 1e-12
+
+
+def test_apply_host_buffers_and_determinism():
+    g = GRIDS["ragged"]
+    k, c = synth.random_fields(g, seed=4)
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_coefficients(ctx, k, c)            # host arrays, staged by the library
+    u = synth.random_vector(g.n_nodes, seed=5)
+    yh = np.empty_like(u)
+    hf.hf_apply(ctx, 0.3, 1.0, u, yh)
+    yd = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_apply(ctx, 0.3, 1.0, T(u), yd)
+    yd2 = torch.empty_like(yd)
+    hf.hf_apply(ctx, 0.3, 1.0, T(u), yd2)
+    assert np.array_equal(yh, N(yd)) and np.array_equal(N(yd), N(yd2))
+    o = oracle.Oracle(g, k, c)
+    assert maxerr(yh, o.spmv(0.3, 1.0, u)) <= 1e-12
+
+
+def test_apply_single_element_and_constant_field():
+    g = GRIDS["1x1x1"]
+    ctx = make_ctx(g, [2.0], [3.0])
+    Ke, Me = oracle.element_matrices(g.h)
+    for j in range(8):
+        e = np.zeros(8)
+        e[j] = 1.0
+        y = torch.empty(8, dtype=torch.float64, device=DEV)
+        hf.hf_apply(ctx, 0.25, 1.5, T(e), y)
+        assert np.allclose(N(y), 0.5 * Ke[:, j] + 4.5 * Me[:, j], rtol=0, atol=1e-15)
+    # K 1 = 0 on a heterogeneous grid
+    g = GRIDS["ragged"]
+    k, c = synth.random_fields(g, seed=6)
+    ctx = make_ctx(g, k, c)
+    y = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_apply(ctx, 1.0, 0.0, T(np.ones(g.n_nodes)), y)
+    assert np.abs(N(y)).max() <= 1e-12 * k.max() * max(g.h)
+
+
+# ---------------------------------------------------------------------------------------------
+# Jacobi diagonal and flux load
+
+@pytest.mark.parametrize("bits", [0, 0b000011, 0b110100])
+def test_diag_matches(bits):
+    g = GRIDS["ragged"]
+    k, c = synth.random_fields(g, seed=7)
+    o = oracle.Oracle(g, k, c)
+    ctx = make_ctx(g, k, c)
+    vals = (1.0, 2.0, 3.0, 4.0, 5.0, 6.0)
+    o.set_dirichlet(bits, vals)
+    hf.hf_set_dirichlet_faces(ctx, bits, vals)
+    d = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_diag(ctx, 0.02, 1.0, d)
+    assert maxerr(N(d), o.diag(0.02, 1.0)) <= 1e-13
+
+
+@pytest.mark.parametrize("face", range(6))
+def test_face_load_matches(face):
+    g = GRIDS["ragged"]
+    k, c = synth.random_fields(g, seed=8)
+    o = oracle.Oracle(g, k, c, assemble=False)
+    ctx = make_ctx(g, k, c)
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    for fc, beam in [(1.0, None), (0.0, (10.0, 2.0, 0.5, 3.0)), (0.3, (1.0, 0.7, -0.5, 4.0))]:
+        hf.hf_face_load(ctx, face, fc, beam, F)
+        Fo = o.face_load(face, fc, beam)
+        assert maxerr(N(F), Fo) <= 1e-13, (face, fc, beam)
+
+
+# ---------------------------------------------------------------------------------------------
+# PCG (Alg. 1)
+
+@pytest.mark.parametrize("driver", [0, 1])
+def test_cg_matches_oracle(driver):
+    p = synth.c1()
+    o, F = oracle.problem_oracle(p)
+    ctx = make_ctx(p.grid, p.k, p.c)
+    hf.hf_set_driver(ctx, driver)
+    b = synth.random_vector(p.grid.n_nodes, 9) * 1e5
+    x = torch.zeros(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    info = hf.hf_cg(ctx, 0.01, 1.0, T(b), x, rtol=1e-12)
+    xo, st, it, _ = o.pcg(0.01, 1.0, b, np.zeros_like(b), tol=1e-12)
+    assert info["status"] == 0 and st == 0
+    assert rel(N(x), xo) <= 1e-10
+    assert abs(info["iters"] - it) <= 3
+    assert info["relres"] <= 1e-12
+
+
+def test_cg_dirichlet_zero_rhs_and_breakdown():
+    g = GRIDS["ragged"]
+    k, c = synth.random_fields(g, seed=10)
+    o = oracle.Oracle(g, k, c)
+    ctx = make_ctx(g, k, c)
+    vals = (0.7, -0.3, 0.0, 0.0, 0.0, 0.0)
+    o.set_dirichlet(3, vals)
+    hf.hf_set_dirichlet_faces(ctx, 3, vals)
+    F = o.face_load(synth.FACE_ZM, 1.0)
+    b = o.rhs(0.5, 0.02, F, synth.random_vector(g.n_nodes, 11))
+    x = T(np.zeros(g.n_nodes))
+    info = hf.hf_cg(ctx, 0.01, 1.0, T(b), x)
+    xo, st, it, _ = o.pcg(0.01, 1.0, b, np.zeros(g.n_nodes))
+    assert info["status"] == 0 and rel(N(x), xo) <= 1e-10
+    # b = 0 (with g = 0) -> x = 0 in 0 iterations
+    hf.hf_set_dirichlet_faces(ctx, 0)
+    x = T(np.ones(g.n_nodes))
+    info = hf.hf_cg(ctx, 0.01, 1.0, T(np.zeros(g.n_nodes)), x)
+    assert info["iters"] == 0 and np.all(N(x) == 0.0)
+    # NaN input -> breakdown, reported not crashed
+    bn = b.copy()
+    bn[5] = np.nan
+    info = hf.hf_cg(ctx, 0.01, 1.0, T(bn), T(np.zeros(g.n_nodes)), raise_on_noconv=False)
+    assert info["rc"] in (hf.HF_E_BREAKDOWN, hf.HF_E_NOCONV)
+    # max_iter too small -> NOCONV with the last iterate
+    info = hf.hf_cg(ctx, 0.01, 1.0, T(b), T(np.zeros(g.n_nodes)), max_iter=3, raise_on_noconv=False)
+    assert info["rc"] == hf.HF_E_NOCONV and info["iters"] == 3
+
+
+# ---------------------------------------------------------------------------------------------
+# time stepping
+
+def _gpu_sim(p, driver=0, snap_plane=-1, tile_r=None):
+    ctx = make_ctx(p.grid, p.k, p.c, tile_r)
+    hf.hf_set_driver(ctx, driver)
+    if p.dirichlet_bits:
+        hf.hf_set_dirichlet_faces(ctx, p.dirichlet_bits, p.dirichlet_values)
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
+    u = T(p.u0)
+    snap = None
+    if snap_plane >= 0:
+        snap = torch.empty(p.nsteps * ctx.n_plane, dtype=torch.float64, device=DEV)
+    st = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, F, u, snap_plane, snap, rtol=p.rtol)
+    return N(u), st, (None if snap is None else N(snap)), ctx
+
+
+@pytest.mark.parametrize("tile_r", [1, 2, 4])
+def test_simulate_c1(tile_r):
+    p = synth.c1()
+    ug, st, _, _ = _gpu_sim(p, tile_r=tile_r)
+    o, F = oracle.problem_oracle(p)
+    uo, sto, it, _ = o.simulate(p.theta, p.dt, p.nsteps, F, p.u0, tol=p.rtol)
+    assert st["steps_done"] == p.nsteps and st["first_failed_step"] == -1
+    assert rel(ug, uo) <= 1e-10
+    assert abs(st["total_iters"] - int(it.sum())) <= 3 * p.nsteps
+
+
+def test_graph_and_host_drivers_bitwise_equal():
+    p = synth.c1()
+    ug, st0, s0, _ = _gpu_sim(p, driver=0, snap_plane=0)
+    uh, st1, s1, _ = _gpu_sim(p, driver=1, snap_plane=0)
+    assert np.array_equal(ug, uh) and np.array_equal(s0, s1)
+    assert st0["total_iters"] == st1["total_iters"]
+
+
+def test_simulate_c2_closed_form():
+    p = synth.c2()
+    ug, st, _, _ = _gpu_sim(p)
+    g = p.grid
+    h = g.h[0]
+    x, _, _ = g.node_coords()
+    lam = (6 / h ** 2) * (1 - np.cos(np.pi * h)) / (2 + np.cos(np.pi * h))
+    G = (1 - (1 - p.theta) * p.dt * lam) / (1 + p.theta * p.dt * lam)
+    ex = G ** p.nsteps * np.sin(np.pi * x.ravel())
+    ex[np.isclose(x.ravel(), 1.0)] = 0.0
+    assert rel(ug, ex) <= 1e-10
+    o, F = oracle.problem_oracle(p)
+    uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, F, p.u0, tol=p.rtol)
+    assert rel(ug, uo) <= 1e-10
+
+
+def test_simulate_nonzero_dirichlet_and_beam():
+    g = synth.Grid((20, 14, 9), (0.3, 0.3, 0.25), (-3.0, -2.0, 0.0))
+    k, c = synth.random_fields(g, seed=12)
+    p = synth.Problem("dir", g, k, c, synth.random_vector(g.n_nodes, 13), theta=0.5, dt=0.05, nsteps=8,
+                      beam=(10.0, 1.0, 0.0, 0.0), flux_const=0.2, dirichlet_bits=0b100001,
+                      dirichlet_values=(1.5, 0.0, 0.0, 0.0, 0.0, -0.5))
+    ug, st, snap, _ = _gpu_sim(p, snap_plane=0)
+    o, F = oracle.problem_oracle(p)
+    uo, sto, it, so = o.simulate(p.theta, p.dt, p.nsteps, F, p.u0, tol=p.rtol, snap_plane=0)
+    assert sto == 0 and rel(ug, uo) <= 1e-10
+    assert rel(snap, so.ravel()) <= 1e-10
+
+
+def test_resume_equals_one_run():
+    p = synth.c1()
+    ctx = make_ctx(p.grid, p.k, p.c)
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
+    u1 = T(p.u0)
+    hf.hf_simulate(ctx, p.theta, p.dt, 10, F, u1)
+    u2 = T(p.u0)
+    up = torch.empty_like(u2)
+    hf.hf_simulate_resume(ctx, p.theta, p.dt, 4, F, u2, up, 0)
+    hf.hf_simulate_resume(ctx, p.theta, p.dt, 6, F, u2, up, 4)
+    assert np.array_equal(N(u1), N(u2))
+
+
+def test_batched_matches_individual():
+    g = synth.Grid((12, 10, 9), (0.3, 0.3, 0.2))
+    B = 3
+    base_k, base_c = synth.random_fields(g, seed=14)
+    ks = np.stack([base_k * synth.lognormal_perturbation(g.n_elems, seed=20 + j) for j in range(B)])
+    cs = np.stack([base_c * (1.0 + 0.1 * j) for j in range(B)])
+    u0 = np.zeros((B, g.n_nodes))
+    for shared_c in (False, True):
+        ctx = make_ctx(g, base_k, base_c)
+        F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+        hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+        ub = T(u0.ravel())
+        front = torch.empty(B * ctx.n_plane, dtype=torch.float64, device=DEV)
+        stats = hf.hf_simulate_batched(ctx, B, T(ks.ravel()), None if shared_c else T(cs.ravel()), 0.5, 0.05, 6,
+                                       F, ub, 0, front)
+        ub = N(ub).reshape(B, -1)
+        front = N(front).reshape(B, -1)
+        for j in range(B):
+            cj = base_c if shared_c else cs[j]
+            o = oracle.Oracle(g, ks[j], cj)
+            Fo = o.face_load(synth.FACE_ZM, 1.0)
+            uo, st, it, _ = o.simulate(0.5, 0.05, 6, Fo, u0[j])
+            assert rel(ub[j], uo) <= 1e-10, (shared_c, j)
+            assert np.array_equal(front[j], ub[j][: ctx.n_plane])
+            assert stats[j]["steps_done"] == 6
+
+
+# ---------------------------------------------------------------------------------------------
+# z-slabs through the in-process transport (same kernels and exchange protocol as NCCL)
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_slab_local_transport(nranks):
+    g = synth.Grid((14, 11, 17), (0.3, 0.3, 0.2))
+    k, c = synth.random_fields(g, seed=15)
+    theta, dt, nsteps = 0.5, 0.05, 5
+    # single-context reference (GPU) and oracle
+    ctx1 = make_ctx(g, k, c)
+    F1 = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx1, synth.FACE_ZM, 1.0, None, F1)
+    u0 = synth.random_vector(g.n_nodes, 16) * 0.01
+    u1 = T(u0)
+    hf.hf_simulate(ctx1, theta, dt, nsteps, F1, u1)
+    ref = N(u1)
+    o = oracle.Oracle(g, k, c)
+    uo, _, _, _ = o.simulate(theta, dt, nsteps, o.face_load(synth.FACE_ZM, 1.0), u0)
+    assert rel(ref, uo) <= 1e-10
+
+    grp = hf.hf_local_group_create(nranks)
+    plane = (g.ne[0] + 1) * (g.ne[1] + 1)
+    out = [None] * nranks
+    errs = []
+    ctxs = [None] * nranks
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            ctx = hf.hf_create_slab(g, r, nranks, grp, transport=1, device=0)
+            ctxs[r] = ctx
+            lo, hi, lp, z0 = ctx.slab
+            hf.hf_set_coefficients(ctx, T(k), T(c))
+            F = torch.empty(ctx.n_nodes, dtype=torch.float64, device=DEV)
+            hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+            u = T(u0[z0 * plane:(z0 + lp) * plane])
+            hf.hf_simulate(ctx, theta, dt, nsteps, F, u)
+            out[r] = (lo, hi, z0, N(u))
+            # apply on the slab: owned planes must equal the global apply
+            y = torch.empty_like(u)
+            hf.hf_apply(ctx, 0.2, 1.0, T(u0[z0 * plane:(z0 + lp) * plane]), y)
+            out[r] = out[r] + (N(y),)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(nranks)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not errs, errs
+    full = np.empty(g.n_nodes)
+    yfull = np.empty(g.n_nodes)
+    for lo, hi, z0, u, y in out:
+        full[lo * plane:hi * plane] = u[(lo - z0) * plane:(hi - z0) * plane]
+        yfull[lo * plane:hi * plane] = y[(lo - z0) * plane:(hi - z0) * plane]
+    assert rel(full, ref) <= 1e-12
+    assert rel(full, uo) <= 1e-10
+    assert maxerr(yfull, o.spmv(0.2, 1.0, u0)) <= 1e-12
+    del ctxs
+    hf.hf_local_group_destroy(grp)
+
+
+# ---------------------------------------------------------------------------------------------
+# BASELINE sizes: C3 (1M DoF) in full, C4 (512^3) on sampled rows
+
+@pytest.fixture(scope="module")
+def c3():
+    return synth.c3(nsteps=2)
+
+
+def test_c3_apply_and_two_steps(c3):
+    p = c3
+    o, F = oracle.problem_oracle(p)
+    ctx = make_ctx(p.grid, p.k, p.c)
+    u = synth.random_vector(p.grid.n_nodes, 17)
+    y = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    for aK, aM in [(p.theta * p.dt, 1.0), (-(1 - p.theta) * p.dt, 1.0)]:
+        hf.hf_apply(ctx, aK, aM, T(u), y)
+        assert maxerr(N(y), o.spmv(aK, aM, u)) <= 1e-12
+    Fd = torch.empty_like(y)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, Fd)
+    assert maxerr(N(Fd), F) <= 1e-13
+    ud = T(p.u0)
+    st = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, Fd, ud, rtol=p.rtol)
+    uo, sto, it, _ = o.simulate(p.theta, p.dt, p.nsteps, F, p.u0, tol=p.rtol)
+    assert rel(N(ud), uo) <= 1e-10
+    assert abs(st["total_iters"] - int(it.sum())) <= 10
+
+
+@pytest.mark.slow
+def test_c4_apply_sampled_rows():
+    g = synth.c4_grid()
+    k, c = synth.random_fields(g, seed=18)
+    u = synth.random_vector(g.n_nodes, 19)
+    ctx = make_ctx(g, k, c)
+    y = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_apply(ctx, 0.005, 1.0, T(u), y)
+    yg = N(y)
+    del ctx
+    torch.cuda.empty_cache()
+    o = oracle.Oracle(g, k, c, assemble=False)
+    rng = np.random.default_rng(20)
+    nx, ny, nz = g.nn
+    rows = rng.integers(0, g.n_nodes, 4096)
+    # plus every boundary class: corners, faces, tile seams (x = 30/31/32, y = 30/31)
+    extra = []
+    for (i, j, kk) in [(0, 0, 0), (nx - 1, ny - 1, nz - 1), (30, 30, 7), (31, 31, 8), (32, 62, 9), (61, 93, 500),
+                       (nx - 1, 0, 3), (0, ny - 1, nz - 1)]:
+        extra.append(i + nx * (j + ny * kk))
+    rows = np.concatenate([rows, np.array(extra)])
+    yo = o.apply_rows(0.005, 1.0, u, rows)
+    assert maxerr(yg[rows], yo) <= 1e-12
