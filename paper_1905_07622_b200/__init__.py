@@ -120,13 +120,19 @@ def _ptr(a, n: Optional[int] = None, name: str = "array", allow_none: bool = Fal
     raise HfError(HF_E_ARG, f"{name}: unsupported type {type(a)}")
 
 
+CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy: torch's default stream reports handle 0
+
+
 def _stream(stream, device: int):
+    """The torch stream the context should enqueue on (its default stream -> cudaStreamLegacy,
+    so torch events and synchronisation see the library's work)."""
     if stream is not None:
         return stream
     try:
         import torch
         if torch.cuda.is_available():
-            return torch.cuda.current_stream(device).cuda_stream
+            h = torch.cuda.current_stream(device).cuda_stream
+            return h if h else CUDA_STREAM_LEGACY
     except ImportError:
         pass
     return None

@@ -215,7 +215,9 @@ __device__ __forceinline__ void fin_init(const Sync &sy, const double *s)
     st->delta = s[0]; st->rr = s[1]; st->bb = s[2];
     st->thresh = st->rtol2 * s[2];
     st->iter = 0; st->beta = 0.0; st->replace = 0; st->status = ST_OK;
-    if (s[2] == 0.0) {               // b_F = 0 -> x_F = 0, 0 iterations
+    if (!isfinite(s[0]) || !isfinite(s[1]) || !isfinite(s[2])) {   // NaN/Inf input
+        st->zero_x = 0; st->active = 0; st->status = ST_BREAKDOWN;
+    } else if (s[2] == 0.0) {        // b_F = 0 -> x_F = 0, 0 iterations
         st->zero_x = 1; st->active = 0;
     } else {
         st->zero_x = 0;

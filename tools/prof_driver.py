@@ -1,0 +1,37 @@
+"""Small workloads for ncu captures (ncu replays each kernel; keep them short)."""
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1905_07622_b200 as hf  # noqa: E402
+import synth  # noqa: E402
+
+dev = torch.device("cuda:0")
+mode = sys.argv[1] if len(sys.argv) > 1 else "sim"
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+
+if mode == "sim":
+    p = synth.c3(nsteps=steps)
+    ctx = hf.hf_create(p.grid, 0)
+    hf.hf_set_coefficients(ctx, torch.tensor(p.k, device=dev), torch.tensor(p.c, device=dev))
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=dev)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
+    u = torch.zeros(p.grid.n_nodes, dtype=torch.float64, device=dev)
+    st = hf.hf_simulate(ctx, p.theta, p.dt, steps, F, u)
+    print(st)
+elif mode.startswith("apply"):
+    n = int(mode[5:] or 512)
+    g = synth.c4_grid(n)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    k = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) + 0.5
+    c = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) + 0.5
+    u = torch.randn(g.n_nodes, dtype=torch.float64, device=dev, generator=gen)
+    y = torch.empty_like(u)
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_coefficients(ctx, k, c)
+    for _ in range(steps):
+        hf.hf_apply(ctx, 0.005, 1.0, u, y)
+    torch.cuda.synchronize()
