@@ -2,22 +2,28 @@
 //
 // Citations: P:n = PAPER.md line n.  Rn = reading n in DESIGN.md.
 //
-// The operator apply (Eq. (1)) is computed with the element matrices written in
-// their Walsh-Hadamard eigenbasis: for a trilinear voxel every K_ref and M_ref is a tensor
-// product of the 1D matrices (1/h)[[1,-1],[-1,1]] and (h/6)[[2,1],[1,2]], both diagonalised
-// by H = [[1,1],[1,-1]], so
+// The operator apply (Eq. (1)) uses the element matrices in their Walsh-Hadamard
+// eigenbasis: for a trilinear voxel every K_ref and M_ref is a tensor product of the 1D
+// matrices (1/h)[[1,-1],[-1,1]] and (h/6)[[2,1],[1,2]], both diagonalised by H = [[1,1],[1,-1]]:
 //      A_e = (1/8) H3 diag(aK k_e lamK + aM c_e lamM) H3,   H3 = H (x) H (x) H.
-// H3 is applied by sum factorisation ACROSS elements: the x butterfly of an edge, the y
-// butterfly of a face and the z butterfly of an element are each computed once and shared
-// by the neighbours that touch them.  ~58 fp64 ops per node.
+// H3 is applied by sum factorisation ACROSS elements: the x butterfly of an edge and the y
+// butterfly of a face are computed once and shared by all elements touching them; the z
+// butterfly and the diagonal scaling of an element collapse to 4 FMA-pairs per face channel:
+//      T_bottom += a Fp + b Fc,   carry_top = b Fp + a Fc,   a = t0 + t1,  b = t0 - t1.
+// About 50 fp64 operations per node.
 //
-// Thread mapping: a CTA owns a 31 x (NW*R - 1) tile of node columns and marches in z over a
-// chunk of node planes.  Lane l of warp w holds node column x = X0-1+l and node rows
-// y = Y0-1+w*R+r (r = 0..R); it computes the R elements whose lower corner is at its nodes.
-// x neighbours come by warp shuffle, the y seam between warps through shared memory,
-// z neighbours stay in registers.  No atomics: every output node is written by one thread,
-// so results are deterministic.
+// Data movement (the B200 part): a CTA owns a 31 x (NW*R - 1) tile of node columns and
+// marches in z through a chunk of node planes.  Each node plane of the tile (34 x (NW*R+1)
+// nodes of every input vector) and the element layer below it ((k, c) of 32 x NW*R elements)
+// arrive by TMA (cp.async.bulk.tensor) into an NS-stage shared-memory ring guarded by
+// mbarriers, NS-1 planes ahead of the compute.  Out-of-range coordinates are zero-filled by
+// the TMA unit, so the domain boundary, the halo and phantom elements need no code.  Lane l
+// of warp w holds node column X0-1+l and node rows Y0-1+w*R+r (r = 0..R); x neighbours are
+// read from shared memory, outputs of the x butterfly move by warp shuffle, the y seam between
+// warps through shared memory, and the z neighbours stay in registers.  No atomics on data:
+// each output node is written by exactly one thread; reductions are fixed-order.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -25,10 +31,14 @@ namespace hf {
 
 constexpr int NPART = 4;      // partial sums per block
 constexpr int TILE_X = 31;    // owned node columns per CTA
+constexpr int BOXW = 34;      // node columns in a TMA box (X0-1 .. X0+32; 34*8 B is 16-B aligned)
+constexpr int NMAPS = 6;      // node tensor maps: ring U[0..2], d[0..1], s
 
 enum { LD_RAW = 0, LD_GT = 1, LD_CGD = 2, LD_X0 = 3 };
 enum { EP_APPLY = 0, EP_CGA = 1, EP_RESID = 2, EP_RESID_INIT = 3 };
 enum { ST_OK = 0, ST_NOCONV = -3, ST_BREAKDOWN = -4 };
+enum { ROT_NONE = 0, ROT_RHS = 1, ROT_INIT = 2, ROT_X = 3 };
+enum { MAP_U0 = 0, MAP_D0 = 3, MAP_S = 5 };
 
 // PCG state of one system (Alg. 1 scalars, device resident; the paper keeps them in device
 // buffers too: delta/alpha/beta kernels P:507-573).
@@ -36,7 +46,7 @@ struct CgState {
     double delta, alpha, beta, rr, bb, thresh, dq, rtol2;
     int iter, max_iter, replace_every;
     int active, status, zero_x, replace;
-    int step;               // time-step counter (step-finalize kernel)
+    int step;               // time-step counter (step-end kernel)
     int first_failed;       // first failing step, -1 if none
     int total_iters, max_iters_step, steps_done;
 };
@@ -44,14 +54,18 @@ struct CgState {
 struct Geom {
     int nx1, ny1, nzl;      // nodes in x, y; local node planes
     int zg0, nz1g;          // global index of local plane 0; global node planes
-    int px, py;             // coefficient pitches (nx1 + 1, ny1 + 1)
-    long long plane;        // nx1 * ny1
+    int pitch;              // node row pitch (nx1 rounded up to even: TMA needs 16-B strides)
+    long long plane;        // pitch * ny1
+    int nx, ny;             // elements in x, y
     unsigned dbits;         // Dirichlet face bits (R3)
     double gval[6];
 };
 
-struct Lam {                // (1/8) aM lamM[s], (1/8) aK lamK[s], s = sx + 2 sy + 4 sz
-    double lm[8], lk[8];
+// Per face channel ch = 2 sx + sy (element wave numbers s0 = sx + 2 sy, s1 = s0 + 4):
+// a = k (lk[s0] + lk[s1]) + c (lm[s0] + lm[s1]),  b = k (lk[s0] - lk[s1]) + c (lm[s0] - lm[s1]),
+// lm[s] = aM lamM[s] / 8, lk[s] = aK lamK[s] / 8.
+struct Lam {
+    double ka[4], ma[4], kb[4], mb[4];
 };
 
 struct Sync {               // per-system reduction plumbing
@@ -64,41 +78,28 @@ struct Sync {               // per-system reduction plumbing
     int use_handles;
 };
 
+struct Maps {               // TMA descriptors, passed as a __grid_constant__ kernel parameter
+    CUtensorMap node[NMAPS];
+    CUtensorMap kc;         // fp64 view (2 nx, ny, nzl + 1) of the (k, c) pairs, layer L at z = L + 1
+};
+
 struct StencilArgs {
     Geom g;
     Lam lam;
-    const double2 *kc;      // (k, c) per element, padded layout (see coef_index)
-    const double *in0, *in1, *in2;
-    double *out0, *out1;
-    const double *bvec;
+    double *out0;                 // q (CG A), r (residual), y (apply)
+    double *out_s;                // s = P^{-1} r (residual kernels)
+    const double *bvec, *invd;
+    double *ring[3];              // time-step ring U (centre stores of the guess)
+    double *dbuf[2];              // PCG direction ping-pong (centre stores of d_new)
+    double *xout;                 // centre store of x0 when not rotating
     double c, s;
     int z_out0, z_out1, zchunk;   // output planes (local) and planes per CTA
-    int zs0, zs1;                 // planes whose centre values are stored (LD-time stores)
+    int zs0, zs1;                 // planes whose centre values are stored
     int dmode;                    // EP_APPLY: 0 none, 1 identity rows, 2 set g on D rows
     int first;                    // LD_X0: step 0 of the run (guess = u^0)
-    int rot_role;                 // time-step buffer rotation (ROT_*), resolved from st->step
-    double *rot[3];               // U^n, U^{n+1}, U^{n+2} ring (role-dependent use)
-    double *dbuf[2];              // PCG direction ping-pong, selected by iteration parity
+    int rot_role;                 // ROT_*: map slots resolved from st->step
     Sync sy;
 };
-
-enum { ROT_NONE = 0, ROT_RHS = 1, ROT_INIT = 2, ROT_X = 3 };
-
-// Pointers a stencil launch actually uses, resolved once per launch from the device state.
-// Ring of three time-step buffers: step s reads U[s%3] (u^n) and U[(s+2)%3] (u^{n-1}) and
-// writes U[(s+1)%3] (u^{n+1}); one captured graph then serves every step.  PCG directions
-// ping-pong by iteration parity: d_old = dbuf[i&1], d_new = dbuf[(i&1)^1].
-struct Ptrs {
-    const double *in0, *in1, *in2;
-    double *out1;
-    int first;
-};
-
-__device__ __forceinline__ long long coef_index(const Geom &g, int ex, int ey, int L)
-{
-    // element (ex, ey) in [-1, nx1-1] x [-1, ny1-1], local layer L in [-1, nzl-1]
-    return ((long long)(L + 1) * g.py + (ey + 1)) * g.px + (ex + 1);
-}
 
 __device__ __forceinline__ bool is_dirichlet(const Geom &g, int x, int y, int zl, double &val)
 {
@@ -114,21 +115,57 @@ __device__ __forceinline__ bool is_dirichlet(const Geom &g, int x, int y, int zl
     return false;
 }
 
-template <int LD>
-__device__ __forceinline__ double load_node(const StencilArgs &a, const Ptrs &P, long long idx, int x, int y,
-                                            int zl, double beta)
+// ---- TMA / mbarrier primitives (PTX) --------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
-    if (LD == LD_RAW) return __ldg(P.in0 + idx);
-    if (LD == LD_GT) { double v = 0.0; return is_dirichlet(a.g, x, y, zl, v) ? v : 0.0; }
-    if (LD == LD_CGD) {
-        // d_new = P^{-1} r + beta d_old  (Alg. 1 lines 15, 18; fused, never stored as s)
-        double v = __ldg(P.in0 + idx) * __ldg(P.in1 + idx);
-        if (beta != 0.0) v = fma(beta, __ldg(P.in2 + idx), v);
-        return v;
-    }
-    // LD_X0: guess of u0_update: x0 = 2 u^n - u^{n-1}, or u^0 at the first step
-    const double un = __ldg(P.in0 + idx);
-    return P.first ? un : 2.0 * un - __ldg(P.in1 + idx);
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap *m)
+{
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");
 }
 
 // ---- deterministic block reduction + last-block finalisation -----------------------------
@@ -261,22 +298,36 @@ __device__ __forceinline__ void fin_iter(const Sync &sy, const double *s)
 }
 
 // ---- the stencil kernel (operator apply with fused prologue/epilogue) ---------------------
-//
-// Element-local WHT: channel ch = 2 sx + sy of a face; element wave number s = sx + 2 sy + 4 sz.
 
-template <int R, int NW, int LD, int EP, bool MASK>
+template <int R, int NW, int LD>
+struct StencilShape {
+    static constexpr int H = NW * R + 1;                                     // node rows per box
+    static constexpr int NA = LD == LD_RAW ? 1 : (LD == LD_GT ? 0 : 2);      // node arrays per plane
+    static constexpr int NODE_DBL = H * BOXW;                                // doubles per node box
+    static constexpr int KC_DBL = NW * R * 64;                               // doubles per kc box
+    static constexpr int STAGE_DBL = NA * NODE_DBL + KC_DBL;
+    static constexpr unsigned STAGE_BYTES = STAGE_DBL * 8u;
+    static size_t smem_bytes(int ns) { return (size_t)ns * STAGE_BYTES + 16 * ns + 2 * NW * 32 * 8 + 128; }
+};
+
+template <int R, int NW, int NS, int LD, int EP, bool MASK>
 __global__ void __launch_bounds__(32 * NW)
-k_stencil(const StencilArgs a)
+k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
 {
+    using SH = StencilShape<R, NW, LD>;
     constexpr int NT = 32 * NW;
+    constexpr int NA = SH::NA;
     const Geom &g = a.g;
     const int lane = threadIdx.x, w = threadIdx.y;
+    const int tid = lane + 32 * w;
     const int blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblocks = gridDim.x * gridDim.y * gridDim.z;
-    if (blk == 0 && lane == 0 && w == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
+    if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
 
+    // ---- state checks and per-launch resolution of buffers ---------------------------------
     double beta = 0.0;
-    Ptrs P{a.in0, a.in1, a.in2, a.out1, a.first};
+    int map0 = MAP_U0, map1 = MAP_U0 + 2, first = a.first;
+    double *cstore = (EP == EP_CGA) ? a.dbuf[1] : a.xout;    // centre-value store target
     if (a.sy.st) {
         const CgState *st = a.sy.st;
         if (st->first_failed >= 0) return;       // an earlier time step failed: stop the run
@@ -285,33 +336,60 @@ k_stencil(const StencilArgs a)
             if (EP == EP_RESID && !st->replace) return;
         }
         if (LD == LD_CGD) {
+            // d_new = s + beta d_old;  d_old = dbuf[i & 1], d_new = dbuf[(i & 1) ^ 1]
             beta = st->beta;
-            const int par = st->iter & 1;        // d_old = dbuf[par], d_new = dbuf[par ^ 1]
-            P.in2 = a.dbuf[par];
-            P.out1 = a.dbuf[par ^ 1];
+            const int par = st->iter & 1;
+            map0 = MAP_S;
+            map1 = MAP_D0 + par;
+            cstore = a.dbuf[par ^ 1];
         }
         if (a.rot_role != ROT_NONE) {
+            // time-step ring: step n reads U[n%3] (u^n), U[(n+2)%3] (u^{n-1}), writes U[(n+1)%3]
             const int s = st->step % 3;
-            double *un = a.rot[s], *unext = a.rot[(s + 1) % 3], *uprev = a.rot[(s + 2) % 3];
-            if (a.rot_role == ROT_RHS) P.in0 = un;
-            else if (a.rot_role == ROT_INIT) { P.in0 = un; P.in1 = uprev; P.out1 = unext; P.first = a.first && st->step == 0; }
-            else P.in0 = unext;
+            if (a.rot_role == ROT_RHS) map0 = MAP_U0 + s;
+            else if (a.rot_role == ROT_INIT) {
+                map0 = MAP_U0 + s;
+                map1 = MAP_U0 + (s + 2) % 3;
+                cstore = a.ring[(s + 1) % 3];
+                first = a.first && st->step == 0;
+            } else map0 = MAP_U0 + (s + 1) % 3;
         }
     }
+    if (LD == LD_X0 && first) map1 = map0;       // u^{-1} unused: keep the byte count fixed
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *stage = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + NS * SH::STAGE_DBL);
+    double(*seam)[NW][32] = reinterpret_cast<double(*)[NW][32]>(bars + 2 * NS);
 
     const int X0 = blockIdx.x * TILE_X;
     const int Y0 = blockIdx.y * (NW * R - 1);
     const int xi = X0 - 1 + lane;
     const int yb = Y0 - 1 + w * R;
-    const bool xin = xi >= 0 && xi < g.nx1;
-    const bool xin1 = (xi + 1) < g.nx1;            // lane 31's extra column
-    const bool xown = lane >= 1 && xin;
     const int zb = a.z_out0 + blockIdx.z * a.zchunk;
     const int ze = min(zb + a.zchunk, a.z_out1);
+    const int nplanes = ze - zb + 2;               // planes zb-1 .. ze
+    const bool xown = lane >= 1 && xi < g.nx1;
 
-    __shared__ double seam[2][NW][32];
+    auto issue = [&](int it) {                     // TMA of plane zb-1+it into its stage
+        const int st = it % NS;
+        const int p = zb - 1 + it;
+        double *sb = stage + st * SH::STAGE_DBL;
+        mbar_expect_tx(&bars[st], SH::STAGE_BYTES);
+        if (NA >= 1) tma_load_3d(sb, &maps.node[map0], X0 - 1, Y0 - 1, p, &bars[st]);
+        if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, &maps.node[map1], X0 - 1, Y0 - 1, p, &bars[st]);
+        // element layer L = p - 1 sits at z = p in the kc tensor
+        tma_load_3d(sb + NA * SH::NODE_DBL, &maps.kc, 2 * (X0 - 1), Y0 - 1, p, &bars[st]);
+    };
 
-    // register state (z-marching)
+    if (tid == 0) {
+        for (int i = 0; i < NS; i++) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int i = 0; i < NS && i < nplanes; i++) issue(i);
+
     double Fp[R][4];          // face transforms of the lower plane p-1
     double Cy[R][4];          // face-space contributions carried from the layer below
     double cen[R];            // raw centre values of plane p-1 (rows 0..R-1)
@@ -323,46 +401,59 @@ k_stencil(const StencilArgs a)
         cen[r] = 0.0;
     }
 
-    int it = 0;
-    for (int p = zb - 1; p <= ze; ++p, ++it) {
-        // ---- load node plane p (rows 0..R), masked copy for the stencil ----------------
-        double vm[R + 1], nx[R + 1], craw[R];
-        const bool pin = p >= 0 && p < g.nzl;
-        // does this CTA store centre values of plane p (exactly one CTA per plane)?
+    for (int it = 0; it < nplanes; ++it) {
+        const int p = zb - 1 + it;
+        const int st = it % NS;
+        mbar_wait(&bars[st], (it / NS) & 1);
+        const double *sb = stage + st * SH::STAGE_DBL;
+        const double *n0 = sb;
+        const double *n1 = sb + SH::NODE_DBL;
+        const double *kcs = sb + NA * SH::NODE_DBL;
+        // ---- node values of plane p (rows 0..R), x butterfly (edges) ----------------------
+        double S[R + 1], D[R + 1], craw[R];
         const bool store_p = (p >= a.zs0 && p < a.zs1) &&
                              ((p >= zb && p < ze) || (p == zb - 1 && zb == a.z_out0) ||
                               (p == ze && ze == a.z_out1));
 #pragma unroll
         for (int r = 0; r <= R; r++) {
-            const int yi = yb + r;
-            const bool in = pin && xin && yi >= 0 && yi < g.ny1;
-            const long long idx = (long long)p * g.plane + (long long)yi * g.nx1 + xi;
-            double v = in ? load_node<LD>(a, P, idx, xi, yi, p, beta) : 0.0;
-            if (r < R) craw[r] = v;
-            if (MASK && in) { double gv; if (is_dirichlet(g, xi, yi, p, gv)) v = 0.0; }
-            vm[r] = v;
-            // lane 31 loads its right neighbour column itself
-            const bool in1 = pin && lane == 31 && xin1 && xi + 1 >= 0 && yi >= 0 && yi < g.ny1;
-            double v1 = in1 ? load_node<LD>(a, P, idx + 1, xi + 1, yi, p, beta) : 0.0;
-            if (MASK && in1) { double gv; if (is_dirichlet(g, xi + 1, yi, p, gv)) v1 = 0.0; }
-            nx[r] = v1;
-            // d_new (CG kernel A) or the guess x0 (init) is stored once, raw, by its owner
-            if ((EP == EP_CGA || EP == EP_RESID_INIT) && r < R && store_p && in && xown && (w > 0 || r > 0))
-                P.out1[idx] = craw[r];
+            const int row = w * R + r;
+            double v, v1;
+            if (LD == LD_RAW) { v = n0[row * BOXW + lane]; v1 = n0[row * BOXW + lane + 1]; }
+            else if (LD == LD_CGD) {
+                v = fma(beta, n1[row * BOXW + lane], n0[row * BOXW + lane]);
+                v1 = fma(beta, n1[row * BOXW + lane + 1], n0[row * BOXW + lane + 1]);
+            } else if (LD == LD_X0) {
+                v = n0[row * BOXW + lane];
+                v1 = n0[row * BOXW + lane + 1];
+                if (!first) { v = 2.0 * v - n1[row * BOXW + lane]; v1 = 2.0 * v1 - n1[row * BOXW + lane + 1]; }
+            } else {   // LD_GT: the Dirichlet lift g~ (g on D nodes, 0 elsewhere)
+                double gv = 0.0;
+                const int yi = yb + r;
+                const bool in = xi >= 0 && xi < g.nx1 && yi >= 0 && yi < g.ny1 && p >= 0 && p < g.nzl;
+                v = (in && is_dirichlet(g, xi, yi, p, gv)) ? gv : 0.0;
+                gv = 0.0;
+                const bool in1 = xi + 1 < g.nx1 && yi >= 0 && yi < g.ny1 && p >= 0 && p < g.nzl;
+                v1 = (in1 && is_dirichlet(g, xi + 1, yi, p, gv)) ? gv : 0.0;
+            }
+            if (r < R) {
+                craw[r] = v;
+                // d_new (CG kernel A) or the guess x0 (init) is stored once, raw, by its owner
+                if ((EP == EP_CGA || EP == EP_RESID_INIT) && store_p && xown && (w > 0 || r > 0) &&
+                    yb + r < g.ny1 && p >= 0 && p < g.nzl)
+                    cstore[(long long)p * g.plane + (long long)(yb + r) * g.pitch + xi] = v;
+            }
+            if (MASK && g.dbits) {
+                double gv;
+                const int yi = yb + r;
+                if (is_dirichlet(g, xi, yi, p, gv)) v = 0.0;
+                if (is_dirichlet(g, xi + 1, yi, p, gv)) v1 = 0.0;
+            }
+            S[r] = v + v1;
+            D[r] = v - v1;
         }
-        // ---- forward x butterfly (edges) -------------------------------------------------
-        double S[R + 1], D[R + 1];
-#pragma unroll
-        for (int r = 0; r <= R; r++) {
-            double un = __shfl_down_sync(0xffffffffu, vm[r], 1);
-            if (lane == 31) un = nx[r];
-            S[r] = vm[r] + un;
-            D[r] = vm[r] - un;
-        }
-        // ---- layer L = p-1: y butterfly (faces), z butterfly, scaling, backward z --------
-        // (skipped for the warm-up plane it == 0: it only primes Fp)
-        const int L = p - 1;
-        const bool Lin = it > 0 && L >= -1 && L < g.nzl;   // padded coefficient layers exist
+        // ---- element layer p-1: y butterfly, fused z butterfly + scaling -------------------
+        // (lane 31's element X0+30 reads node X0+31 from the box; elements outside the domain
+        //  have k = c = 0 from the TMA zero fill)
         double T[R][4];
 #pragma unroll
         for (int r = 0; r < R; r++) {
@@ -371,27 +462,17 @@ k_stencil(const StencilArgs a)
             Fc[1] = S[r] - S[r + 1];   // sx=0, sy=1
             Fc[2] = D[r] + D[r + 1];   // sx=1, sy=0
             Fc[3] = D[r] - D[r + 1];   // sx=1, sy=1
-            const int ey = yb + r;
-            double ke = 0.0, ce = 0.0;
-            if (Lin && xi < g.nx1 && ey < g.ny1) {
-                const double2 kc = __ldg(a.kc + coef_index(g, xi, ey, L));
-                ke = kc.x; ce = kc.y;
-            }
+            const double2 kc = *reinterpret_cast<const double2 *>(kcs + (w * R + r) * 64 + 2 * lane);
 #pragma unroll
             for (int ch = 0; ch < 4; ch++) {
-                const int sx = ch >> 1, syb = ch & 1;
-                const int s0 = sx + 2 * syb, s1 = s0 + 4;
-                const double v0 = Fp[r][ch] + Fc[ch];     // sz = 0
-                const double v1 = Fp[r][ch] - Fc[ch];     // sz = 1
-                const double t0 = (s0 == 0) ? ce * a.lam.lm[0] : fma(ke, a.lam.lk[s0], ce * a.lam.lm[s0]);
-                const double t1 = fma(ke, a.lam.lk[s1], ce * a.lam.lm[s1]);
-                const double w0 = v0 * t0, w1 = v1 * t1;
-                T[r][ch] = Cy[r][ch] + (w0 + w1);        // bottom plane p-1 complete
-                Cy[r][ch] = w0 - w1;                     // top plane p, carried
+                const double av = fma(kc.x, a.lam.ka[ch], kc.y * a.lam.ma[ch]);
+                const double bv = fma(kc.x, a.lam.kb[ch], kc.y * a.lam.mb[ch]);
+                T[r][ch] = fma(av, Fp[r][ch], fma(bv, Fc[ch], Cy[r][ch]));   // bottom plane p-1
+                Cy[r][ch] = fma(bv, Fp[r][ch], av * Fc[ch]);                  // top plane p
                 Fp[r][ch] = Fc[ch];
             }
         }
-        // ---- backward y and x butterflies for plane p-1, seam exchange, epilogue ---------
+        // ---- backward y and x butterflies for plane p-1 ------------------------------------
         const int pout = p - 1;
         const bool out_plane = pout >= zb && pout < ze;   // uniform across the CTA
         double yv[R + 1];
@@ -400,19 +481,22 @@ k_stencil(const StencilArgs a)
             double E0 = 0.0, E1 = 0.0;               // sx = 0, 1
             if (e < R) { E0 += T[e][0] + T[e][1]; E1 += T[e][2] + T[e][3]; }
             if (e > 0) { E0 += T[e - 1][0] - T[e - 1][1]; E1 += T[e - 1][2] - T[e - 1][3]; }
-            double left = __shfl_up_sync(0xffffffffu, E0 - E1, 1);
-            if (lane == 0) left = 0.0;
-            yv[e] = (E0 + E1) + left;
+            const double left = __shfl_up_sync(0xffffffffu, E0 - E1, 1);
+            yv[e] = (E0 + E1) + left;                // lane 0's value is not owned
+        }
+        seam[it & 1][w][lane] = yv[R];
+        __syncthreads();                              // seam visible; stage `st` fully read
+        if (tid == 0 && it + NS < nplanes) {
+            fence_proxy_async();
+            issue(it + NS);
         }
         if (out_plane) {
-            seam[it & 1][w][lane] = yv[R];
-            __syncthreads();
             if (w > 0) yv[0] += seam[it & 1][w - 1][lane];
 #pragma unroll
             for (int e = 0; e < R; e++) {
                 const int yi = yb + e;
                 if (!(xown && (w > 0 || e > 0) && yi < g.ny1)) continue;
-                const long long idx = (long long)pout * g.plane + (long long)yi * g.nx1 + xi;
+                const long long idx = (long long)pout * g.plane + (long long)yi * g.pitch + xi;
                 double gv = 0.0;
                 const bool isd = is_dirichlet(g, xi, yi, pout, gv);
                 if (EP == EP_APPLY) {
@@ -426,11 +510,12 @@ k_stencil(const StencilArgs a)
                     const double q = isd ? d : yv[e];       // identity rows (R3)
                     a.out0[idx] = q;
                     acc[0] = fma(d, q, acc[0]);
-                } else {   // EP_RESID, EP_RESID_INIT: r = b - A x (identity rows on D)
+                } else {   // EP_RESID, EP_RESID_INIT: r = b - A x (identity rows on D); s = P^{-1} r
                     const double b = __ldg(a.bvec + idx);
                     const double r = isd ? 0.0 : b - yv[e];
+                    const double sv = r * __ldg(a.invd + idx);
                     a.out0[idx] = r;
-                    const double sv = r * __ldg(a.in2 + idx);  // in2 = P^{-1} diagonal
+                    a.out_s[idx] = sv;
                     acc[0] = fma(r, sv, acc[0]);
                     acc[1] = fma(r, r, acc[1]);
                     if (EP == EP_RESID_INIT && !isd) acc[2] = fma(b, b, acc[2]);
@@ -445,7 +530,6 @@ k_stencil(const StencilArgs a)
     block_reduce_store<NT>(acc, a.sy.partials, blk);
     double sums[NPART];
     if (!last_block_sums<NT>(a.sy, nblocks, sums)) return;
-    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
     if (tid != 0) return;
     if (a.sy.sums_out) {
         for (int j = 0; j < NPART; j++) a.sy.sums_out[j] = sums[j];
@@ -459,7 +543,7 @@ k_stencil(const StencilArgs a)
 // ---- PCG kernel B: x += alpha d; r -= alpha q; s = P^{-1} r; r^T s, r^T r ---------------
 // (Alg. 1 lines 9, 13, 15, 16; the paper's knl_6, knl_7, knl_8, knl_9A-C, knl_10.)
 // x is updated on every local node (ghost planes included, so slab ghosts stay consistent);
-// r and the dot products only on owned nodes [own0, own1).  On a replacement iteration
+// r, s and the dot products only on owned nodes [own0, own1).  On a replacement iteration
 // (i > 0, i mod replace_every == 0, Alg. 1 line 10) only x is updated: the residual kernel
 // (EP_RESID) follows.
 
@@ -467,7 +551,7 @@ struct BArgs {
     double *x;
     const double *q, *invd;
     double *dbuf[2];        // d = dbuf[(iter & 1) ^ 1] (written by kernel A of this iteration)
-    double *r;
+    double *r, *s;
     long long n, own0, own1;
     double *rot[3];         // if rot[0]: x = rot[(step + 1) % 3]
     Sync sy;
@@ -490,34 +574,27 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     const double *dvec = a.dbuf[(it & 1) ^ 1];
     double *xvec = a.rot[0] ? a.rot[(st->step + 1) % 3] : a.x;
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
+    // n is even (even row pitch): every thread handles aligned pairs
     const long long stride = (long long)gridDim.x * NT * 2;
     for (long long i = ((long long)blk * NT + tid) * 2; i < a.n; i += stride) {
-        if (i + 1 < a.n) {
-            double2 xv = *reinterpret_cast<const double2 *>(xvec + i);
-            const double2 dv = *reinterpret_cast<const double2 *>(dvec + i);
-            xv.x = fma(alpha, dv.x, xv.x);
-            xv.y = fma(alpha, dv.y, xv.y);
-            *reinterpret_cast<double2 *>(xvec + i) = xv;
-            if (!replace) {
-                double2 rv = *reinterpret_cast<const double2 *>(a.r + i);
-                const double2 qv = __ldg(reinterpret_cast<const double2 *>(a.q + i));
-                const double2 iv = __ldg(reinterpret_cast<const double2 *>(a.invd + i));
-                const bool o0 = i >= a.own0 && i < a.own1, o1 = i + 1 >= a.own0 && i + 1 < a.own1;
-                if (o0) { rv.x = fma(-alpha, qv.x, rv.x); const double sv = rv.x * iv.x;
-                          acc[0] = fma(rv.x, sv, acc[0]); acc[1] = fma(rv.x, rv.x, acc[1]); }
-                if (o1) { rv.y = fma(-alpha, qv.y, rv.y); const double sv = rv.y * iv.y;
-                          acc[0] = fma(rv.y, sv, acc[0]); acc[1] = fma(rv.y, rv.y, acc[1]); }
-                if (o0 || o1) *reinterpret_cast<double2 *>(a.r + i) = rv;
-            }
-        } else {
-            xvec[i] = fma(alpha, dvec[i], xvec[i]);
-            if (!replace && i >= a.own0 && i < a.own1) {
-                const double rv = fma(-alpha, a.q[i], a.r[i]);
-                a.r[i] = rv;
-                const double sv = rv * a.invd[i];
-                acc[0] = fma(rv, sv, acc[0]);
-                acc[1] = fma(rv, rv, acc[1]);
-            }
+        double2 xv = *reinterpret_cast<const double2 *>(xvec + i);
+        const double2 dv = *reinterpret_cast<const double2 *>(dvec + i);
+        xv.x = fma(alpha, dv.x, xv.x);
+        xv.y = fma(alpha, dv.y, xv.y);
+        *reinterpret_cast<double2 *>(xvec + i) = xv;
+        if (!replace && i >= a.own0 && i < a.own1) {
+            double2 rv = *reinterpret_cast<const double2 *>(a.r + i);
+            const double2 qv = __ldg(reinterpret_cast<const double2 *>(a.q + i));
+            const double2 iv = __ldg(reinterpret_cast<const double2 *>(a.invd + i));
+            rv.x = fma(-alpha, qv.x, rv.x);
+            rv.y = fma(-alpha, qv.y, rv.y);
+            const double2 sv = make_double2(rv.x * iv.x, rv.y * iv.y);
+            acc[0] = fma(rv.x, sv.x, acc[0]);
+            acc[0] = fma(rv.y, sv.y, acc[0]);
+            acc[1] = fma(rv.x, rv.x, acc[1]);
+            acc[1] = fma(rv.y, rv.y, acc[1]);
+            *reinterpret_cast<double2 *>(a.r + i) = rv;
+            *reinterpret_cast<double2 *>(a.s + i) = sv;
         }
     }
     if (replace) {
@@ -547,6 +624,14 @@ __global__ void k_finalize(Sync sy, int mode)
     else fin_iter(sy, s);   // kernel B
 }
 
+// ---- element coefficient access (compact (nx, ny, nzl + 1) layout, layer L at index L + 1) --
+
+__device__ __forceinline__ double2 load_kc(const Geom &g, const double2 *kc, int ex, int ey, int L)
+{
+    if (ex < 0 || ey < 0 || ex >= g.nx || ey >= g.ny || L < -1 || L >= g.nzl) return make_double2(0.0, 0.0);
+    return kc[((long long)(L + 1) * g.ny + ey) * g.nx + ex];
+}
+
 // ---- Jacobi diagonal (Jacobi_A P:659-662) -------------------------------------------
 // diag_i = sum over the 8 elements around node i of aK k_e Kd + aM c_e Md, with
 // Kd = K_ref[l][l], Md = M_ref[l][l] (the same for every l of a voxel); 1 on Dirichlet rows.
@@ -558,11 +643,11 @@ __global__ void k_diag(Geom g, const double2 *kc, double aK, double aM, double K
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && launches) atomicAdd(launches, 1ull);
     if (i >= n) return;
-    const int x = (int)(i % g.nx1), y = (int)((i / g.nx1) % g.ny1), z = (int)(i / g.plane);
+    const int x = (int)(i % g.pitch), y = (int)((i / g.pitch) % g.ny1), z = (int)(i / g.plane);
+    if (x >= g.nx1) { if (diag) diag[i] = 0.0; if (invd) invd[i] = 0.0; return; }   // pitch padding
     double sk = 0.0, sc = 0.0;
     for (int l = 0; l < 8; l++) {
-        const int ex = x - (l & 1), ey = y - ((l >> 1) & 1), ez = z - ((l >> 2) & 1);
-        const double2 v = kc[coef_index(g, ex, ey, ez)];
+        const double2 v = load_kc(g, kc, x - (l & 1), y - ((l >> 1) & 1), z - ((l >> 2) & 1));
         sk += v.x;
         sc += v.y;
     }
@@ -573,23 +658,22 @@ __global__ void k_diag(Geom g, const double2 *kc, double aK, double aM, double K
     if (invd) invd[i] = 1.0 / d;
 }
 
-// ---- packing of the per-element coefficients into the padded (k, c) layout ----------------
-// padded entry (ex+1, ey+1, L+1) for ex in [-1, nx1-1], ey in [-1, ny1-1], L in [-1, nzl-1];
-// global element (ex, ey, zg0 + L) if it exists, else (0, 0).
+// ---- packing of the per-element coefficients into the (k, c) pair layout ------------------
+// pair (ex, ey, L) for local layer L in [-1, nzl-1] = global element (ex, ey, zg0 + L), or 0.
 
-__global__ void k_pack(Geom g, int nx, int ny, int nz, const double *k, const double *c, double2 *kc,
-                       long long ntot, unsigned long long *launches)
+__global__ void k_pack(Geom g, int nz, const double *k, const double *c, double2 *kc, long long ntot,
+                       unsigned long long *launches)
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && launches) atomicAdd(launches, 1ull);
     if (i >= ntot) return;
-    const int ex = (int)(i % g.px) - 1, ey = (int)((i / g.px) % g.py) - 1;
-    const int L = (int)(i / ((long long)g.px * g.py)) - 1;
+    const int ex = (int)(i % g.nx), ey = (int)((i / g.nx) % g.ny);
+    const int L = (int)(i / ((long long)g.nx * g.ny)) - 1;
     const int ez = g.zg0 + L;
     double2 v = make_double2(0.0, 0.0);
-    if (ex >= 0 && ex < nx && ey >= 0 && ey < ny && ez >= 0 && ez < nz) {
-        const long long e = ex + (long long)nx * (ey + (long long)ny * ez);
-        v = make_double2(k[e], c[e]);
+    if (ez >= 0 && ez < nz) {
+        const long long e = ex + (long long)g.nx * (ey + (long long)g.ny * ez);
+        v = make_double2(k[e], c ? c[e] : 0.0);
     }
     kc[i] = v;
 }
@@ -619,7 +703,6 @@ __global__ void k_face_load(const FaceArgs a)
     const long long nface = (long long)a.na * a.nb;
     if (i >= nface) return;
     const int ia = (int)(i % a.na), ib = (int)(i / a.na);
-    // local node coordinates
     int idx3[3];
     idx3[a.nd] = a.plane_g;
     idx3[a.ax] = ia;
@@ -650,7 +733,7 @@ __global__ void k_face_load(const FaceArgs a)
             }
         }
     }
-    const long long node = (long long)zl * a.g.plane + (long long)idx3[1] * a.g.nx1 + idx3[0];
+    const long long node = (long long)zl * a.g.plane + (long long)idx3[1] * a.g.pitch + idx3[0];
     a.F[node] = sum;
 }
 
@@ -663,9 +746,9 @@ __global__ void k_set_dirichlet(Geom g, double *v, const double *src, unsigned l
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && launches) atomicAdd(launches, 1ull);
     if (i >= n) return;
-    const int x = (int)(i % g.nx1), y = (int)((i / g.nx1) % g.ny1), z = (int)(i / g.plane);
+    const int x = (int)(i % g.pitch), y = (int)((i / g.pitch) % g.ny1), z = (int)(i / g.plane);
     double gv;
-    if (is_dirichlet(g, x, y, z, gv)) v[i] = src ? src[i] : gv;
+    if (x < g.nx1 && is_dirichlet(g, x, y, z, gv)) v[i] = src ? src[i] : gv;
 }
 
 // End of one solve / time step: x_F <- 0 if b_F = 0; per-step statistics;
@@ -675,7 +758,7 @@ struct StepArgs {
     double *x;
     double *rot[3];         // if rot[0]: x = rot[(step + 1) % 3]
     long long n;
-    double *snap;           // NULL or nsteps x plane
+    double *snap;           // NULL or nsteps x plane (padded plane layout)
     int snap_plane;         // local plane index, -1 none
     int *iters_out;         // per-step iteration counts (may be NULL)
     Sync sy;
@@ -689,23 +772,23 @@ __global__ void __launch_bounds__(256) k_step_end(const StepArgs a)
     if (st->first_failed >= 0) return;
     const int step = st->step;
     double *xv = a.rot[0] ? a.rot[(step + 1) % 3] : a.x;
-    if (st->zero_x) {
+    const bool zx = st->zero_x;
+    if (zx) {
         for (long long i = (long long)blk * 256 + tid; i < a.n; i += (long long)gridDim.x * 256) {
-            const int x = (int)(i % a.g.nx1), y = (int)((i / a.g.nx1) % a.g.ny1), z = (int)(i / a.g.plane);
+            const int x = (int)(i % a.g.pitch), y = (int)((i / a.g.pitch) % a.g.ny1), z = (int)(i / a.g.plane);
             double gv;
-            if (!is_dirichlet(a.g, x, y, z, gv)) xv[i] = 0.0;
+            if (x < a.g.nx1 && !is_dirichlet(a.g, x, y, z, gv)) xv[i] = 0.0;
         }
     }
     if (a.snap && a.snap_plane >= 0) {
         const double *src = xv + (long long)a.snap_plane * a.g.plane;
         double *dst = a.snap + (long long)step * a.g.plane;
         for (long long i = (long long)blk * 256 + tid; i < a.g.plane; i += (long long)gridDim.x * 256) {
-            // zero_x is rare; read after the zeroing above only matters for the same block
             double v = src[i];
-            if (st->zero_x) {
-                const int x = (int)(i % a.g.nx1), y = (int)(i / a.g.nx1);
+            if (zx) {
+                const int x = (int)(i % a.g.pitch), y = (int)(i / a.g.pitch);
                 double gv;
-                if (!is_dirichlet(a.g, x, y, a.snap_plane, gv)) v = 0.0;
+                if (x < a.g.nx1 && !is_dirichlet(a.g, x, y, a.snap_plane, gv)) v = 0.0;
             }
             dst[i] = v;
         }

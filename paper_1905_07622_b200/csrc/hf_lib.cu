@@ -1,20 +1,25 @@
 // hf_lib.cu -- libheatfem: the C ABI of include/heatfem.h on top of hf_kernels.cuh.
 //
-// Host runtime: contexts, workspaces, host-pointer staging, the PCG and time-loop drivers
-// (a CUDA graph with a device-side WHILE loop, or a host loop), batched simulations, z-slab
-// decomposition with NCCL (dlopen'ed) or an in-process transport.  Citations: P:n = PAPER.md.
+// Host runtime: contexts, workspaces, TMA descriptors, host-pointer staging, the PCG and
+// time-loop drivers (a CUDA graph with a device-side WHILE loop, or a host loop), batched
+// simulations, z-slab decomposition with NCCL (dlopen'ed) or an in-process transport.
+// Citations: P:n = PAPER.md line n.
+//
+// Internal layout: node vectors use a row pitch of nx1 rounded up to an even number of
+// doubles (TMA needs 16-byte global strides); user vectors use the natural pitch nx1 and are
+// converted at the boundary (no copy when nx1 is even and the pointer is on the device).
 #include "heatfem.h"
 #include "hf_kernels.cuh"
 
 #include <dlfcn.h>
 
 #include <algorithm>
-#include <atomic>
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -108,23 +113,41 @@ static hf_status load()
     } while (0)
 
 // ============================================================================================
+// TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry point)
+
+typedef CUresult (*EncodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiled_t g_encode = nullptr;
+
+static hf_status get_encode()
+{
+    if (g_encode) return HF_OK;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUCK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(HF_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = (EncodeTiled_t)fn;
+    return HF_OK;
+}
+
+// ============================================================================================
 // context
 
 struct SimKey {
-    double aK = 0, aM = 0, aKL = 0, aML = 0, rtol = 0;
-    int max_iter = 0, replace_every = 0, first = 0, snap_plane = -1, lift = 0;
+    double aK = 0, aM = 0, aKL = 0, aML = 0, rtol = 0, dt = 0;
+    int max_iter = 0, replace_every = 0, first = 0, snap_plane = -1, lift = 0, pad = 0;
     const double *F = nullptr;
-    double *snap = nullptr, *ubase = nullptr;
-    double dt = 0;
+    double *snap = nullptr;
     bool operator==(const SimKey &o) const { return std::memcmp(this, &o, sizeof(SimKey)) == 0; }
 };
 
 struct Sys {                         // one system's PCG workspace (Table 3 buffers)
-    double2 *kc = nullptr;           // padded (k, c); owned if own_kc
-    bool own_kc = false;
+    double2 *kc = nullptr;           // (k, c) pairs, compact (nx, ny, nzl + 1)
     double *U[3] = {nullptr, nullptr, nullptr};   // time-step ring
-    double *b = nullptr, *r = nullptr, *q = nullptr, *invd = nullptr;
+    double *b = nullptr, *r = nullptr, *s = nullptr, *q = nullptr, *invd = nullptr;
     double *dbuf[2] = {nullptr, nullptr};
+    Maps maps;                       // TMA maps of U[0..2], dbuf[0..1], s and kc
     CgState *st = nullptr;           // device
     CgState *st_host = nullptr;      // pinned mirror
     double *partials = nullptr, *sums = nullptr;
@@ -155,9 +178,10 @@ struct hf_ctx {
     int nsm = 148;
     hf_grid g{};
     int nx1 = 0, ny1 = 0, nz1g = 0;
+    int pitch = 0;                   // internal row pitch (even)
     int nzl = 0, zg0 = 0;            // local planes, global index of local plane 0
     int own_lo = 0, own_hi = 0;      // owned local planes [own_lo, own_hi)
-    long long plane = 0, nloc = 0;
+    long long plane = 0, nloc = 0;   // internal plane size, local node slots (padded)
     long long kc_elems = 0;
     bool coef_set = false;
     unsigned dbits = 0;
@@ -166,20 +190,17 @@ struct hf_ctx {
     Sys sys0;
     std::vector<std::unique_ptr<Sys>> pool;
     unsigned long long *launches = nullptr;
-    // host staging
-    std::vector<void *> scratch;
+    std::vector<void *> scratch;     // staging buffers (padded node layout unless noted)
     std::vector<size_t> scratch_cap;
     double *flush = nullptr;
-    // config
     int driver = 0;                  // 0 graph, 1 host loop
     int tileR = 4;
-    int ctas_per_sm = 2;
+    int zchunk_env = 0;
     int check_every = 8;
-    int tiles_x = 0, tiles_y = 0, max_blocks = 0;
-    // slab
+    int max_blocks = 0;
+    int occ = 2;                     // resident CTAs/SM of the CG stencil (occupancy API)
     int rank = 0, nranks = 1;
     Comm *comm = nullptr;
-    // profiling
     bool prof = false;
     double prof_ms[5] = {0, 0, 0, 0, 0};
     long long prof_n[5] = {0, 0, 0, 0, 0};
@@ -198,6 +219,12 @@ static bool is_device_ptr(const void *p)
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// user node vector usable in place: device, natural pitch == internal pitch, 16-B aligned
+static bool direct_ok(const hf_ctx *c, const void *p)
+{
+    return c->pitch == c->nx1 && ((uintptr_t)p % 16) == 0 && is_device_ptr(p);
+}
+
 static hf_status scratch_get(hf_ctx *c, int slot, size_t bytes, void **out)
 {
     if ((int)c->scratch.size() <= slot) {
@@ -209,13 +236,59 @@ static hf_status scratch_get(hf_ctx *c, int slot, size_t bytes, void **out)
         c->scratch[slot] = nullptr;
         c->scratch_cap[slot] = 0;
         CUCK(cudaMalloc(&c->scratch[slot], bytes));
+        CUCK(cudaMemsetAsync(c->scratch[slot], 0, bytes, c->stream));   // pitch padding stays 0
         c->scratch_cap[slot] = bytes;
     }
     *out = c->scratch[slot];
     return HF_OK;
 }
 
-// device view of an input array (host arrays are copied into scratch `slot`)
+// user (natural pitch) -> internal (padded pitch), nplanes planes
+static hf_status copy_in(hf_ctx *c, double *dst, const double *src, int nplanes, cudaStream_t s)
+{
+    CUCK(cudaMemcpy2DAsync(dst, (size_t)c->pitch * 8, src, (size_t)c->nx1 * 8, (size_t)c->nx1 * 8,
+                           (size_t)c->ny1 * nplanes, cudaMemcpyDefault, s));
+    return HF_OK;
+}
+
+static hf_status copy_out(hf_ctx *c, double *dst, const double *src, int nplanes, cudaStream_t s)
+{
+    CUCK(cudaMemcpy2DAsync(dst, (size_t)c->nx1 * 8, src, (size_t)c->pitch * 8, (size_t)c->nx1 * 8,
+                           (size_t)c->ny1 * nplanes, cudaMemcpyDefault, s));
+    return HF_OK;
+}
+
+// internal view of a user input node vector (copied into scratch `slot` unless direct)
+static hf_status node_in(hf_ctx *c, const double *p, int slot, const double **out)
+{
+    if (!p) { *out = nullptr; return HF_OK; }
+    if (direct_ok(c, p)) { *out = p; return HF_OK; }
+    void *d;
+    HFCK(scratch_get(c, slot, (size_t)c->nloc * 8, &d));
+    HFCK(copy_in(c, (double *)d, p, c->nzl, c->stream));
+    *out = (const double *)d;
+    return HF_OK;
+}
+
+// internal view of a user output (or in/out) node vector
+static hf_status node_out(hf_ctx *c, double *p, int slot, bool copy, double **out)
+{
+    if (direct_ok(c, p)) { *out = p; return HF_OK; }
+    void *d;
+    HFCK(scratch_get(c, slot, (size_t)c->nloc * 8, &d));
+    if (copy) HFCK(copy_in(c, (double *)d, p, c->nzl, c->stream));
+    *out = (double *)d;
+    return HF_OK;
+}
+
+static hf_status node_out_finish(hf_ctx *c, double *p, const double *d)
+{
+    if (p != d) HFCK(copy_out(c, p, d, c->nzl, c->stream));
+    CUCK(cudaStreamSynchronize(c->stream));
+    return HF_OK;
+}
+
+// device view of a plain (element) input array
 static hf_status dev_in(hf_ctx *c, const double *p, size_t n, int slot, const double **out)
 {
     if (!p) { *out = nullptr; return HF_OK; }
@@ -227,42 +300,27 @@ static hf_status dev_in(hf_ctx *c, const double *p, size_t n, int slot, const do
     return HF_OK;
 }
 
-// device view of an output (or in/out) array; host arrays go through scratch `slot`
-static hf_status dev_out(hf_ctx *c, double *p, size_t n, int slot, bool copy_in, double **out)
-{
-    if (is_device_ptr(p)) { *out = p; return HF_OK; }
-    void *d;
-    HFCK(scratch_get(c, slot, n * sizeof(double), &d));
-    if (copy_in) CUCK(cudaMemcpyAsync(d, p, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    *out = (double *)d;
-    return HF_OK;
-}
-
-static hf_status dev_out_finish(hf_ctx *c, double *p, const double *d, size_t n)
-{
-    if (p == d) return HF_OK;
-    CUCK(cudaMemcpyAsync(p, d, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CUCK(cudaStreamSynchronize(c->stream));
-    return HF_OK;
-}
-
 static Geom make_geom(const hf_ctx *c)
 {
     Geom g;
+    std::memset(&g, 0, sizeof(g));
     g.nx1 = c->nx1; g.ny1 = c->ny1; g.nzl = c->nzl;
     g.zg0 = c->zg0; g.nz1g = c->nz1g;
-    g.px = c->nx1 + 1; g.py = c->ny1 + 1;
+    g.pitch = c->pitch;
     g.plane = c->plane;
+    g.nx = (int)c->g.ne[0];
+    g.ny = (int)c->g.ne[1];
     g.dbits = c->dbits;
     for (int f = 0; f < 6; f++) g.gval[f] = c->gval[f];
     return g;
 }
 
 // WHT eigenvalues of the voxel matrices (1/8 folded in): mu_d(0) = h/2, mu_d(1) = h/6 for
-// (h/6)[[2,1],[1,2]]; kappa_d(0) = 0, kappa_d(1) = 2/h for (1/h)[[1,-1],[-1,1]].
+// (h/6)[[2,1],[1,2]]; kappa_d(0) = 0, kappa_d(1) = 2/h for (1/h)[[1,-1],[-1,1]].  Folded into
+// the per-channel (a, b) coefficients of the fused z butterfly.
 static Lam make_lam(const double h[3], double aK, double aM)
 {
-    Lam L;
+    double lm[8], lk[8];
     for (int s = 0; s < 8; s++) {
         const int b[3] = {s & 1, (s >> 1) & 1, (s >> 2) & 1};
         double mu[3], ka[3];
@@ -270,12 +328,48 @@ static Lam make_lam(const double h[3], double aK, double aM)
             mu[d] = b[d] ? h[d] / 6.0 : h[d] / 2.0;
             ka[d] = b[d] ? 2.0 / h[d] : 0.0;
         }
-        const double lM = mu[0] * mu[1] * mu[2];
-        const double lK = ka[0] * mu[1] * mu[2] + mu[0] * ka[1] * mu[2] + mu[0] * mu[1] * ka[2];
-        L.lm[s] = aM * lM / 8.0;
-        L.lk[s] = aK * lK / 8.0;
+        lm[s] = aM * (mu[0] * mu[1] * mu[2]) / 8.0;
+        lk[s] = aK * (ka[0] * mu[1] * mu[2] + mu[0] * ka[1] * mu[2] + mu[0] * mu[1] * ka[2]) / 8.0;
+    }
+    Lam L;
+    for (int ch = 0; ch < 4; ch++) {
+        const int sx = ch >> 1, sy = ch & 1;
+        const int s0 = sx + 2 * sy, s1 = s0 + 4;
+        L.ka[ch] = lk[s0] + lk[s1];
+        L.ma[ch] = lm[s0] + lm[s1];
+        L.kb[ch] = lk[s0] - lk[s1];
+        L.mb[ch] = lm[s0] - lm[s1];
     }
     return L;
+}
+
+static hf_status node_map(const hf_ctx *c, const double *p, CUtensorMap *m)
+{
+    HFCK(get_encode());
+    const cuuint64_t dims[3] = {(cuuint64_t)c->nx1, (cuuint64_t)c->ny1, (cuuint64_t)c->nzl};
+    const cuuint64_t strides[2] = {(cuuint64_t)c->pitch * 8, (cuuint64_t)c->plane * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)BOXW, (cuuint32_t)(NW * c->tileR + 1), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)p, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HF_E_CUDA, "cuTensorMapEncodeTiled(node) failed: " + std::to_string((int)r));
+    return HF_OK;
+}
+
+static hf_status kc_map(const hf_ctx *c, const double2 *kc, CUtensorMap *m)
+{
+    HFCK(get_encode());
+    const cuuint64_t nx = (cuuint64_t)c->g.ne[0], ny = (cuuint64_t)c->g.ne[1];
+    const cuuint64_t dims[3] = {2 * nx, ny, (cuuint64_t)c->nzl + 1};
+    const cuuint64_t strides[2] = {2 * nx * 8, 2 * nx * ny * 8};
+    const cuuint32_t box[3] = {64, (cuuint32_t)(NW * c->tileR), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)kc, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HF_E_CUDA, "cuTensorMapEncodeTiled(kc) failed: " + std::to_string((int)r));
+    return HF_OK;
 }
 
 // ============================================================================================
@@ -284,43 +378,83 @@ static Lam make_lam(const double h[3], double aK, double aM)
 struct Launch {
     const void *fn = nullptr;
     dim3 grid, block;
-    std::vector<char> arg;
+    size_t smem = 0;
+    std::vector<std::vector<char>> args;
     int cls = 4;
-    template <class T> void set(const T &v) { arg.resize(sizeof(T)); std::memcpy(arg.data(), &v, sizeof(T)); }
+    template <class T> void add(const T &v)
+    {
+        std::vector<char> b(sizeof(T));
+        std::memcpy(b.data(), &v, sizeof(T));
+        args.push_back(std::move(b));
+    }
+    template <class T> T get(int i) const
+    {
+        T v;
+        std::memcpy(&v, args[i].data(), sizeof(T));
+        return v;
+    }
+    template <class T> void put(int i, const T &v) { std::memcpy(args[i].data(), &v, sizeof(T)); }
 };
 
-template <int LD, int EP, bool MASK> static const void *stencil_fn(int R)
+template <int R, int LD> constexpr int ns_of()
 {
-    switch (R) {
-    case 4: return (const void *)k_stencil<4, NW, LD, EP, MASK>;
-    case 2: return (const void *)k_stencil<2, NW, LD, EP, MASK>;
-    default: return (const void *)k_stencil<1, NW, LD, EP, MASK>;
-    }
+    return (R >= 4 && StencilShape<R, NW, LD>::NA == 2) ? 3 : 4;
 }
 
-static const void *stencil_fn_dyn(int R, int LD, int EP, bool MASK)
+struct StencilFn {
+    const void *fn;
+    size_t smem;
+};
+
+template <int R, int LD, int EP, bool MASK> static StencilFn stencil_fn_t()
 {
-    if (LD == LD_RAW && EP == EP_APPLY && !MASK) return stencil_fn<LD_RAW, EP_APPLY, false>(R);
-    if (LD == LD_GT && EP == EP_APPLY && !MASK) return stencil_fn<LD_GT, EP_APPLY, false>(R);
-    if (LD == LD_CGD && EP == EP_CGA && !MASK) return stencil_fn<LD_CGD, EP_CGA, false>(R);
-    if (LD == LD_X0 && EP == EP_RESID_INIT && MASK) return stencil_fn<LD_X0, EP_RESID_INIT, true>(R);
-    if (LD == LD_RAW && EP == EP_RESID_INIT && MASK) return stencil_fn<LD_RAW, EP_RESID_INIT, true>(R);
-    if (LD == LD_RAW && EP == EP_RESID && MASK) return stencil_fn<LD_RAW, EP_RESID, true>(R);
-    return nullptr;
+    constexpr int NS = ns_of<R, LD>();
+    return {(const void *)k_stencil<R, NW, NS, LD, EP, MASK>, StencilShape<R, NW, LD>::smem_bytes(NS)};
+}
+
+template <int LD, int EP, bool MASK> static StencilFn stencil_fn_r(int R)
+{
+    return R >= 4 ? stencil_fn_t<4, LD, EP, MASK>() : stencil_fn_t<2, LD, EP, MASK>();
+}
+
+static StencilFn stencil_fn(int R, int LD, int EP, bool MASK)
+{
+    if (LD == LD_RAW && EP == EP_APPLY && !MASK) return stencil_fn_r<LD_RAW, EP_APPLY, false>(R);
+    if (LD == LD_GT && EP == EP_APPLY && !MASK) return stencil_fn_r<LD_GT, EP_APPLY, false>(R);
+    if (LD == LD_CGD && EP == EP_CGA && !MASK) return stencil_fn_r<LD_CGD, EP_CGA, false>(R);
+    if (LD == LD_X0 && EP == EP_RESID_INIT && MASK) return stencil_fn_r<LD_X0, EP_RESID_INIT, true>(R);
+    if (LD == LD_RAW && EP == EP_RESID_INIT && MASK) return stencil_fn_r<LD_RAW, EP_RESID_INIT, true>(R);
+    if (LD == LD_RAW && EP == EP_RESID && MASK) return stencil_fn_r<LD_RAW, EP_RESID, true>(R);
+    return {nullptr, 0};
+}
+
+static std::mutex g_attr_mu;
+static std::map<std::pair<const void *, int>, bool> g_attr_done;
+
+static hf_status ensure_smem_attr(const void *fn, size_t smem, int device)
+{
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto key = std::make_pair(fn, device);
+    if (g_attr_done.count(key)) return HF_OK;
+    CUCK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    g_attr_done[key] = true;
+    return HF_OK;
 }
 
 static int rows_per_tile(int R) { return NW * R - 1; }
 
-// grid of the stencil over output planes [z0, z1)
+// grid of the stencil over output planes [z0, z1): one (x, y) tile column per CTA, z split
+// into chunks so that the grid fills the resident slots (occupancy x SMs) once.
 static void stencil_grid(const hf_ctx *c, int z0, int z1, dim3 *grid, int *zchunk)
 {
     const int tx = (c->nx1 + TILE_X - 1) / TILE_X;
     const int ty = (c->ny1 + rows_per_tile(c->tileR) - 1) / rows_per_tile(c->tileR);
     const int planes = std::max(1, z1 - z0);
     const long long cols = (long long)tx * ty;
-    const long long target = (long long)c->nsm * c->ctas_per_sm * 2;
-    long long nch = std::max(1LL, (target + cols - 1) / cols);
-    int chunk = (int)std::max(4LL, ((long long)planes + nch - 1) / nch);
+    const long long slots = (long long)c->nsm * c->occ;
+    long long nch = std::max(1LL, slots / cols);
+    int chunk = (int)std::max(1LL, ((long long)planes + nch - 1) / nch);
+    if (c->zchunk_env > 0) chunk = c->zchunk_env;
     chunk = std::min(chunk, planes);
     nch = (planes + chunk - 1) / chunk;
     *grid = dim3(tx, ty, (unsigned)nch);
@@ -336,17 +470,15 @@ static Sync make_sync(hf_ctx *c, Sys &s)
     y.ticket = s.ticket;
     y.launches = c->launches;
     y.sums_out = (c->nranks > 1) ? s.sums : nullptr;
-    y.use_handles = 0;
     return y;
 }
 
-static StencilArgs base_args(hf_ctx *c, const double2 *kc, double aK, double aM)
+static StencilArgs base_args(hf_ctx *c, double aK, double aM)
 {
     StencilArgs a;
     std::memset(&a, 0, sizeof(a));
     a.g = make_geom(c);
     a.lam = make_lam(c->g.h, aK, aM);
-    a.kc = kc;
     a.c = 1.0;
     a.s = 0.0;
     a.z_out0 = c->own_lo;
@@ -356,33 +488,41 @@ static StencilArgs base_args(hf_ctx *c, const double2 *kc, double aK, double aM)
     return a;
 }
 
-static Launch stencil_launch(hf_ctx *c, int LD, int EP, bool MASK, StencilArgs a, int cls)
+static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool MASK, const Maps &maps, StencilArgs a, int cls,
+                                Launch *out)
 {
-    Launch L;
+    StencilFn f = stencil_fn(c->tileR, LD, EP, MASK);
+    if (!f.fn) return fail(HF_E_ARG, "internal: no stencil instantiation");
+    HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
     dim3 grid;
     int chunk;
     stencil_grid(c, a.z_out0, a.z_out1, &grid, &chunk);
     a.zchunk = chunk;
-    L.fn = stencil_fn_dyn(c->tileR, LD, EP, MASK);
+    Launch L;
+    L.fn = f.fn;
     L.grid = grid;
     L.block = dim3(32, NW, 1);
-    L.set(a);
+    L.smem = f.smem;
+    L.add(maps);
+    L.add(a);
     L.cls = cls;
-    return L;
+    *out = L;
+    return HF_OK;
 }
 
 static int b_blocks(const hf_ctx *c) { return std::max(1, std::min((int)((c->nloc + 511) / 512), c->nsm * 4)); }
 
 static hf_status run(hf_ctx *c, const Launch &L, cudaStream_t s)
 {
-    void *args[1] = {(void *)L.arg.data()};
+    void *args[4];
+    for (size_t i = 0; i < L.args.size(); i++) args[i] = (void *)L.args[i].data();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->prof) {
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, s);
     }
-    CUCK(cudaLaunchKernel(L.fn, L.grid, L.block, args, 0, s));
+    CUCK(cudaLaunchKernel(L.fn, L.grid, L.block, args, L.smem, s));
     if (c->prof) {
         cudaEventRecord(e1, s);
         cudaEventSynchronize(e1);
@@ -400,10 +540,12 @@ static hf_status add_node(cudaGraph_t g, const Launch &L, cudaGraphNode_t *dep, 
 {
     cudaKernelNodeParams p;
     std::memset(&p, 0, sizeof(p));
-    void *args[1] = {(void *)L.arg.data()};
+    void *args[4];
+    for (size_t i = 0; i < L.args.size(); i++) args[i] = (void *)L.args[i].data();
     p.func = (void *)L.fn;
     p.gridDim = L.grid;
     p.blockDim = L.block;
+    p.sharedMemBytes = (unsigned)L.smem;
     p.kernelParams = args;
     CUCK(cudaGraphAddKernelNode(out, g, dep, dep ? 1 : 0, &p));
     return HF_OK;
@@ -412,33 +554,36 @@ static hf_status add_node(cudaGraph_t g, const Launch &L, cudaGraphNode_t *dep, 
 // ============================================================================================
 // workspace
 
-static hf_status sys_alloc(hf_ctx *c, Sys &s, bool own_kc, cudaStream_t stream)
+static hf_status sys_maps(hf_ctx *c, Sys &s)
+{
+    for (int i = 0; i < 3; i++) HFCK(node_map(c, s.U[i], &s.maps.node[MAP_U0 + i]));
+    for (int i = 0; i < 2; i++) HFCK(node_map(c, s.dbuf[i], &s.maps.node[MAP_D0 + i]));
+    HFCK(node_map(c, s.s, &s.maps.node[MAP_S]));
+    HFCK(kc_map(c, s.kc, &s.maps.kc));
+    return HF_OK;
+}
+
+static hf_status sys_alloc(hf_ctx *c, Sys &s, cudaStream_t stream)
 {
     const size_t vb = (size_t)c->nloc * sizeof(double);
-    for (int i = 0; i < 3; i++) CUCK(cudaMalloc(&s.U[i], vb));
-    CUCK(cudaMalloc(&s.b, vb));
-    CUCK(cudaMalloc(&s.r, vb));
-    CUCK(cudaMalloc(&s.q, vb));
-    CUCK(cudaMalloc(&s.invd, vb));
-    CUCK(cudaMalloc(&s.dbuf[0], vb));
-    CUCK(cudaMalloc(&s.dbuf[1], vb));
-    CUCK(cudaMemsetAsync(s.dbuf[0], 0, vb, stream));
-    CUCK(cudaMemsetAsync(s.dbuf[1], 0, vb, stream));
+    double **vecs[] = {&s.U[0], &s.U[1], &s.U[2], &s.b, &s.r, &s.s, &s.q, &s.invd, &s.dbuf[0], &s.dbuf[1]};
+    for (double **v : vecs) {
+        CUCK(cudaMalloc(v, vb));
+        CUCK(cudaMemsetAsync(*v, 0, vb, stream));   // pitch padding must stay zero
+    }
+    CUCK(cudaMalloc(&s.kc, (size_t)c->kc_elems * sizeof(double2)));
+    CUCK(cudaMemsetAsync(s.kc, 0, (size_t)c->kc_elems * sizeof(double2), stream));
     CUCK(cudaMalloc(&s.st, sizeof(CgState)));
     CUCK(cudaMallocHost(&s.st_host, sizeof(CgState)));
     CUCK(cudaMalloc(&s.partials, (size_t)c->max_blocks * NPART * sizeof(double)));
     CUCK(cudaMalloc(&s.sums, NPART * sizeof(double)));
     CUCK(cudaMalloc(&s.ticket, sizeof(unsigned)));
     CUCK(cudaMemsetAsync(s.ticket, 0, sizeof(unsigned), stream));
-    CgState z;
-    std::memset(&z, 0, sizeof(z));
-    z.first_failed = -1;
-    CUCK(cudaMemcpyAsync(s.st, &z, sizeof(z), cudaMemcpyHostToDevice, stream));
-    if (own_kc) {
-        CUCK(cudaMalloc(&s.kc, (size_t)c->kc_elems * sizeof(double2)));
-        s.own_kc = true;
-    }
+    std::memset(s.st_host, 0, sizeof(CgState));
+    s.st_host->first_failed = -1;
+    CUCK(cudaMemcpyAsync(s.st, s.st_host, sizeof(CgState), cudaMemcpyHostToDevice, stream));
     s.stream = stream;
+    HFCK(sys_maps(c, s));
     CUCK(cudaStreamSynchronize(stream));
     return HF_OK;
 }
@@ -446,11 +591,11 @@ static hf_status sys_alloc(hf_ctx *c, Sys &s, bool own_kc, cudaStream_t stream)
 static void sys_free(Sys &s)
 {
     for (int i = 0; i < 3; i++) cudaFree(s.U[i]);
-    cudaFree(s.b); cudaFree(s.r); cudaFree(s.q); cudaFree(s.invd);
+    cudaFree(s.b); cudaFree(s.r); cudaFree(s.s); cudaFree(s.q); cudaFree(s.invd);
     cudaFree(s.dbuf[0]); cudaFree(s.dbuf[1]);
     cudaFree(s.st); cudaFreeHost(s.st_host);
     cudaFree(s.partials); cudaFree(s.sums); cudaFree(s.ticket); cudaFree(s.iters);
-    if (s.own_kc) cudaFree(s.kc);
+    cudaFree(s.kc);
     if (s.gexec) cudaGraphExecDestroy(s.gexec);
     if (s.graph) cudaGraphDestroy(s.graph);
     if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
@@ -461,6 +606,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
 {
     for (int d = 0; d < 3; d++)
         if (g->ne[d] < 1 || !(g->h[d] > 0.0)) return fail(HF_E_ARG, "grid: ne must be >= 1 and h > 0");
+    if (g->ne[0] > 1000000 || g->ne[1] > 1000000) return fail(HF_E_ARG, "grid too large");
     c->g = *g;
     c->device = device;
     CUCK(cudaSetDevice(device));
@@ -472,6 +618,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     c->nx1 = (int)g->ne[0] + 1;
     c->ny1 = (int)g->ne[1] + 1;
     c->nz1g = (int)g->ne[2] + 1;
+    c->pitch = (c->nx1 + 1) & ~1;
     c->rank = rank;
     c->nranks = nranks;
     int64_t lo = 0, hi = c->nz1g;
@@ -482,17 +629,22 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     c->nzl = ghi - glo;
     c->own_lo = (int)lo - glo;
     c->own_hi = (int)hi - glo;
-    c->plane = (long long)c->nx1 * c->ny1;
+    c->plane = (long long)c->pitch * c->ny1;
     c->nloc = c->plane * c->nzl;
-    c->kc_elems = (long long)(c->nx1 + 1) * (c->ny1 + 1) * (c->nzl + 1);
+    c->kc_elems = (long long)g->ne[0] * g->ne[1] * (c->nzl + 1);
     const double hx = g->h[0], hy = g->h[1], hz = g->h[2];
     c->Kd = (hy * hz / hx + hx * hz / hy + hx * hy / hz) / 9.0;
     c->Md = hx * hy * hz / 27.0;
-    if (const char *e = getenv("HF_TILE_R")) c->tileR = std::max(1, std::min(4, atoi(e)));
-    if (c->tileR == 3) c->tileR = 2;
-    if (const char *e = getenv("HF_CTAS_PER_SM")) c->ctas_per_sm = std::max(1, atoi(e));
+    if (const char *e = getenv("HF_TILE_R")) c->tileR = atoi(e) >= 4 ? 4 : 2;
+    if (const char *e = getenv("HF_ZCHUNK")) c->zchunk_env = std::max(0, atoi(e));
     if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e);
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
+    // resident CTAs per SM of the CG stencil decide the z split of the grid
+    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, false);
+    HFCK(ensure_smem_attr(f.fn, f.smem, device));
+    int occ = 0;
+    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
+    c->occ = std::max(1, occ);
     dim3 grid;
     int chunk;
     stencil_grid(c, c->own_lo, c->own_hi, &grid, &chunk);
@@ -500,7 +652,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     c->max_blocks = std::max(c->max_blocks, c->nsm * 4);
     CUCK(cudaMalloc(&c->launches, sizeof(unsigned long long)));
     CUCK(cudaMemsetAsync(c->launches, 0, sizeof(unsigned long long), c->stream));
-    HFCK(sys_alloc(c, c->sys0, true, c->stream));
+    HFCK(sys_alloc(c, c->sys0, c->stream));
     return HF_OK;
 }
 
@@ -526,8 +678,8 @@ static hf_status enqueue_pack(hf_ctx *c, Sys &s, const double *k, const double *
 {
     const long long n = c->kc_elems;
     const int bs = 256;
-    k_pack<<<(unsigned)((n + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), (int)c->g.ne[0], (int)c->g.ne[1],
-                                                               (int)c->g.ne[2], k, cc, s.kc, n, c->launches);
+    k_pack<<<(unsigned)((n + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), (int)c->g.ne[2], k, cc, s.kc, n,
+                                                               c->launches);
     CUCK(cudaGetLastError());
     return HF_OK;
 }
@@ -550,19 +702,18 @@ static hf_status enqueue_set_dirichlet(hf_ctx *c, Sys &s, double *v, const doubl
     return HF_OK;
 }
 
-// PCG kernels of one iteration for system s (operator lam), in order.
+// PCG kernels of one iteration for system s, in order.
 struct CgLaunches {
     Launch A, B, RES;
 };
 
-static CgLaunches cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x, bool rot)
+// x: the iterate (NULL: the time-step ring slot U[(step+1)%3]); xmaps: maps with node[0] = x
+static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x, const Maps &xmaps, CgLaunches *L)
 {
-    CgLaunches L;
     Sync sy = make_sync(c, s);
-    // kernel A: d = P^{-1} r + beta d; q = A d; d^T q -> alpha   (Alg. 1 lines 7-8, 15, 18)
-    StencilArgs a = base_args(c, s.kc, aK, aM);
-    a.in0 = s.r;
-    a.in1 = s.invd;
+    const bool rot = x == nullptr;
+    // kernel A: d = s + beta d; q = A d; d^T q -> alpha   (Alg. 1 lines 7-8, 15, 18)
+    StencilArgs a = base_args(c, aK, aM);
     a.dbuf[0] = s.dbuf[0];
     a.dbuf[1] = s.dbuf[1];
     a.out0 = s.q;
@@ -570,8 +721,8 @@ static CgLaunches cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x
     a.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
     a.dmode = 1;
     a.sy = sy;
-    L.A = stencil_launch(c, LD_CGD, EP_CGA, false, a, 0);
-    // kernel B: x += alpha d; r -= alpha q; s; r^T s, r^T r -> beta   (Alg. 1 lines 9-19)
+    HFCK(stencil_launch(c, LD_CGD, EP_CGA, false, s.maps, a, 0, &L->A));
+    // kernel B: x += alpha d; r -= alpha q; s = P^{-1} r; r^T s, r^T r -> beta   (lines 9-19)
     BArgs b;
     std::memset(&b, 0, sizeof(b));
     b.x = x;
@@ -580,36 +731,41 @@ static CgLaunches cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x
     b.dbuf[0] = s.dbuf[0];
     b.dbuf[1] = s.dbuf[1];
     b.r = s.r;
+    b.s = s.s;
     b.n = c->nloc;
     b.own0 = (long long)c->own_lo * c->plane;
     b.own1 = (long long)c->own_hi * c->plane;
     if (rot) for (int i = 0; i < 3; i++) b.rot[i] = s.U[i];
     b.sy = sy;
-    L.B.fn = (const void *)k_cg_b<256>;
-    L.B.grid = dim3(b_blocks(c));
-    L.B.block = dim3(256);
-    L.B.set(b);
-    L.B.cls = 1;
+    L->B = Launch();
+    L->B.fn = (const void *)k_cg_b<256>;
+    L->B.grid = dim3(b_blocks(c));
+    L->B.block = dim3(256);
+    L->B.add(b);
+    L->B.cls = 1;
     // residual replacement r = b - A x every replace_every iterations (Alg. 1 lines 10-11)
-    StencilArgs rr = base_args(c, s.kc, aK, aM);
-    rr.in0 = x;
-    rr.in2 = s.invd;
+    StencilArgs rr = base_args(c, aK, aM);
+    rr.invd = s.invd;
     rr.bvec = s.b;
     rr.out0 = s.r;
+    rr.out_s = s.s;
     rr.sy = sy;
-    if (rot) { rr.rot_role = ROT_X; for (int i = 0; i < 3; i++) rr.rot[i] = s.U[i]; }
-    L.RES = stencil_launch(c, LD_RAW, EP_RESID, true, rr, 2);
-    return L;
+    if (rot) rr.rot_role = ROT_X;
+    HFCK(stencil_launch(c, LD_RAW, EP_RESID, true, rot ? s.maps : xmaps, rr, 2, &L->RES));
+    return HF_OK;
 }
 
-static hf_status comm_after(hf_ctx *c, Sys &s, int mode, bool exch_r)
+static hf_status comm_after(hf_ctx *c, Sys &s, int mode, bool exch)
 {
     if (c->nranks <= 1) return HF_OK;
     HFCK(c->comm->allreduce(c, s, s.sums, NPART));
     Sync sy = make_sync(c, s);
     k_finalize<<<1, 1, 0, s.stream>>>(sy, mode);
     CUCK(cudaGetLastError());
-    if (exch_r) HFCK(c->comm->exchange(c, s, s.r));
+    if (exch) {   // residual ghosts (r and s) for the next apply
+        HFCK(c->comm->exchange(c, s, s.r));
+        HFCK(c->comm->exchange(c, s, s.s));
+    }
     return HF_OK;
 }
 
@@ -620,40 +776,28 @@ static hf_status read_state(hf_ctx *c, Sys &s)
     return HF_OK;
 }
 
-static hf_status set_solver_opts(hf_ctx *c, Sys &s, const hf_cg_opts *o, bool reset_steps)
+// options and counters of a new solve / run, written without a device round trip
+static hf_status set_solver_opts(hf_ctx *c, Sys &s, const hf_cg_opts &d)
 {
-    hf_cg_opts d = {1e-12, 10000, 50};
-    if (o) d = *o;
     if (!(d.rtol >= 0.0) || d.max_iter < 0 || d.replace_every < 0) return fail(HF_E_ARG, "bad hf_cg_opts");
-    // write the option fields (and reset counters) with a tiny H2D of a prepared state image
-    CUCK(cudaMemcpyAsync(s.st_host, s.st, sizeof(CgState), cudaMemcpyDeviceToHost, s.stream));
-    CUCK(cudaStreamSynchronize(s.stream));
-    CgState h = *s.st_host;
+    CUCK(cudaStreamSynchronize(s.stream));     // the pinned image may still be in flight
+    CgState &h = *s.st_host;
+    std::memset(&h, 0, sizeof(h));
     h.rtol2 = d.rtol * d.rtol;
     h.max_iter = d.max_iter;
     h.replace_every = d.replace_every;
-    h.active = 0;
-    h.status = ST_OK;
-    if (reset_steps) {
-        h.step = 0;
-        h.first_failed = -1;
-        h.total_iters = 0;
-        h.max_iters_step = 0;
-        h.steps_done = 0;
-    }
-    *s.st_host = h;
+    h.first_failed = -1;
     CUCK(cudaMemcpyAsync(s.st, s.st_host, sizeof(CgState), cudaMemcpyHostToDevice, s.stream));
-    CUCK(cudaStreamSynchronize(s.stream));
     return HF_OK;
 }
 
-static StepArgs step_args(hf_ctx *c, Sys &s, double *x, bool rot, double *snapdev, int snap_local)
+static StepArgs step_args(hf_ctx *c, Sys &s, double *x, double *snapdev, int snap_local)
 {
     StepArgs a;
     std::memset(&a, 0, sizeof(a));
     a.g = make_geom(c);
     a.x = x;
-    if (rot) for (int i = 0; i < 3; i++) a.rot[i] = s.U[i];
+    if (!x) for (int i = 0; i < 3; i++) a.rot[i] = s.U[i];
     a.n = c->nloc;
     a.snap = snapdev;
     a.snap_plane = snap_local;
@@ -668,7 +812,7 @@ static Launch step_launch(hf_ctx *c, const StepArgs &a)
     L.fn = (const void *)k_step_end;
     L.grid = dim3(std::max(1, std::min(c->nsm, (int)((c->nloc + 255) / 256))));
     L.block = dim3(256);
-    L.set(a);
+    L.add(a);
     L.cls = 4;
     return L;
 }
@@ -680,7 +824,7 @@ static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, in
     if (!s.st_host->active) return HF_OK;
     const bool slab = c->nranks > 1;
     const int check = slab && !c->comm->graph_capturable() ? 1 : c->check_every;
-    for (int i = 0;; ) {
+    for (int i = 0;;) {
         HFCK(run(c, L.A, s.stream));
         HFCK(comm_after(c, s, EP_CGA, false));
         const bool rep = i > 0 && replace_every > 0 && i % replace_every == 0;
@@ -701,21 +845,23 @@ static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, in
 
 // ---- graph with the device-side WHILE loop -------------------------------------------------
 // root: [pre...] -> init -> WHILE(active){ A -> B -> IF(replace){ RESID } } -> [post]
-static hf_status build_cg_graph(hf_ctx *c, Sys &s, std::vector<Launch> pre, Launch init, CgLaunches L,
-                                std::vector<Launch> post, cudaGraph_t *out)
+// (all stencil launches carry (Maps, StencilArgs); B carries BArgs)
+static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init, CgLaunches L, std::vector<Launch> post,
+                                cudaGraph_t *out)
 {
+    (void)c;
     cudaGraph_t g;
     CUCK(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle hw, hi;
     CUCK(cudaGraphConditionalHandleCreate(&hw, g, 0, cudaGraphCondAssignDefault));
     cudaGraphNode_t prev = nullptr, n;
     for (auto &p : pre) { HFCK(add_node(g, p, prev ? &prev : nullptr, &n)); prev = n; }
-    // the init kernel and the loop body set the WHILE handle
-    StencilArgs ia;
-    std::memcpy(&ia, init.arg.data(), sizeof(ia));
-    ia.sy.h_while = hw;
-    ia.sy.use_handles = 1;
-    init.set(ia);
+    {   // the init kernel sets the WHILE handle
+        StencilArgs ia = init.get<StencilArgs>(1);
+        ia.sy.h_while = hw;
+        ia.sy.use_handles = 1;
+        init.put(1, ia);
+    }
     HFCK(add_node(g, init, prev ? &prev : nullptr, &n));
     prev = n;
     cudaGraphNodeParams cp = {};
@@ -728,18 +874,15 @@ static hf_status build_cg_graph(hf_ctx *c, Sys &s, std::vector<Launch> pre, Laun
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CUCK(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
     {
-        StencilArgs aa;
-        std::memcpy(&aa, L.A.arg.data(), sizeof(aa));
+        StencilArgs aa = L.A.get<StencilArgs>(1);
         aa.sy.h_while = hw; aa.sy.h_if = hi; aa.sy.use_handles = 1;
-        L.A.set(aa);
-        BArgs bb;
-        std::memcpy(&bb, L.B.arg.data(), sizeof(bb));
+        L.A.put(1, aa);
+        BArgs bb = L.B.get<BArgs>(0);
         bb.sy.h_while = hw; bb.sy.h_if = hi; bb.sy.use_handles = 1;
-        L.B.set(bb);
-        StencilArgs ra;
-        std::memcpy(&ra, L.RES.arg.data(), sizeof(ra));
+        L.B.put(0, bb);
+        StencilArgs ra = L.RES.get<StencilArgs>(1);
         ra.sy.h_while = hw; ra.sy.h_if = hi; ra.sy.use_handles = 1;
-        L.RES.set(ra);
+        L.RES.put(1, ra);
     }
     cudaGraphNode_t na, nb;
     HFCK(add_node(body, L.A, nullptr, &na));
@@ -764,7 +907,7 @@ static hf_status build_cg_graph(hf_ctx *c, Sys &s, std::vector<Launch> pre, Laun
 
 extern "C" {
 
-const char *hf_version(void) { return "heatfem-b200 0.1 (sm_100a)"; }
+const char *hf_version(void) { return "heatfem-b200 0.2 (sm_100a, TMA stencil)"; }
 
 const char *hf_last_error(void) { return g_err.c_str(); }
 
@@ -812,9 +955,10 @@ hf_status hf_set_dirichlet_faces(hf_ctx *c, uint32_t bits, const double values[6
 hf_status hf_face_load(hf_ctx *c, int face, double f_const, const double beam[4], double *F)
 {
     if (!c || !F || face < 0 || face > 5) return fail(HF_E_ARG, "hf_face_load: bad argument");
+    if (beam && !(beam[1] > 0.0)) return fail(HF_E_ARG, "hf_face_load: beam sigma must be > 0");
     CUCK(cudaSetDevice(c->device));
     double *dF;
-    HFCK(dev_out(c, F, c->nloc, 2, false, &dF));
+    HFCK(node_out(c, F, 2, false, &dF));
     CUCK(cudaMemsetAsync(dF, 0, c->nloc * sizeof(double), c->stream));
     FaceArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -831,13 +975,12 @@ hf_status hf_face_load(hf_ctx *c, int face, double f_const, const double beam[4]
     a.oa = c->g.origin[a.ax]; a.ob = c->g.origin[a.bx];
     a.f_const = f_const;
     if (beam) { a.has_beam = 1; a.bP = beam[0]; a.bs = beam[1]; a.bca = beam[2]; a.bcb = beam[3]; }
-    if (beam && !(beam[1] > 0.0)) return fail(HF_E_ARG, "hf_face_load: beam sigma must be > 0");
     a.F = dF;
     a.launches = c->launches;
     const long long n = (long long)a.na * a.nb;
     k_face_load<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(a);
     CUCK(cudaGetLastError());
-    return dev_out_finish(c, F, dF, c->nloc);
+    return node_out_finish(c, F, dF);
 }
 
 hf_status hf_apply_axpby(hf_ctx *c, double aK, double aM, double cc, const double *u, const double *b, double *y)
@@ -848,19 +991,21 @@ hf_status hf_apply_axpby(hf_ctx *c, double aK, double aM, double cc, const doubl
     CUCK(cudaSetDevice(c->device));
     const double *du, *db = nullptr;
     double *dy;
-    HFCK(dev_in(c, u, c->nloc, 3, &du));
-    if (b) HFCK(dev_in(c, b, c->nloc, 4, &db));
-    HFCK(dev_out(c, y, c->nloc, 5, false, &dy));
-    StencilArgs a = base_args(c, c->sys0.kc, aK, aM);
-    a.in0 = du;
+    HFCK(node_in(c, u, 3, &du));
+    if (b) HFCK(node_in(c, b, 4, &db));
+    HFCK(node_out(c, y, 5, false, &dy));
+    Maps maps = c->sys0.maps;
+    HFCK(node_map(c, du, &maps.node[MAP_U0]));
+    StencilArgs a = base_args(c, aK, aM);
     a.out0 = dy;
     a.bvec = db;
     a.c = cc;
     a.s = 1.0;
-    // every local plane is an output plane of a plain apply (ghost planes: partial sums)
-    Launch L = stencil_launch(c, LD_RAW, EP_APPLY, false, a, 3);
+    Launch L;
+    HFCK(stencil_launch(c, LD_RAW, EP_APPLY, false, maps, a, 3, &L));
     HFCK(run(c, L, c->stream));
-    return dev_out_finish(c, y, dy, c->nloc);
+    if (y == dy) return HF_OK;               // fully asynchronous on device buffers
+    return node_out_finish(c, y, dy);
 }
 
 hf_status hf_apply(hf_ctx *c, double aK, double aM, const double *u, double *y)
@@ -874,9 +1019,10 @@ hf_status hf_diag(hf_ctx *c, double aK, double aM, double *diag)
     if (!c->coef_set) return fail(HF_E_STATE, "hf_diag: coefficients not set");
     CUCK(cudaSetDevice(c->device));
     double *dd;
-    HFCK(dev_out(c, diag, c->nloc, 5, false, &dd));
+    HFCK(node_out(c, diag, 5, false, &dd));
     HFCK(enqueue_diag(c, c->sys0, aK, aM, dd, nullptr));
-    return dev_out_finish(c, diag, dd, c->nloc);
+    if (diag == dd) return HF_OK;
+    return node_out_finish(c, diag, dd);
 }
 
 hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, const hf_cg_opts *opts,
@@ -888,36 +1034,41 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     Sys &s = c->sys0;
     hf_cg_opts o = {1e-12, 10000, 50};
     if (opts) o = *opts;
-    HFCK(set_solver_opts(c, s, &o, true));
+    HFCK(set_solver_opts(c, s, o));
     const double *db;
     double *dx;
-    HFCK(dev_in(c, b, c->nloc, 4, &db));
-    HFCK(dev_out(c, x, c->nloc, 6, true, &dx));
+    HFCK(node_in(c, b, 4, &db));
+    HFCK(node_out(c, x, 6, true, &dx));
     CUCK(cudaMemcpyAsync(s.b, db, c->nloc * sizeof(double), cudaMemcpyDeviceToDevice, s.stream));
     HFCK(enqueue_diag(c, s, aK, aM, nullptr, s.invd));
     HFCK(enqueue_set_dirichlet(c, s, dx, s.b));           // x_D = b_D
     if (c->nranks > 1) HFCK(c->comm->exchange(c, s, dx));
+    Maps xm = s.maps;
+    HFCK(node_map(c, dx, &xm.node[MAP_U0]));
     // init: r = b - A x0; s = P^{-1} r; delta; ||b_F||   (Alg. 1 lines 2-4)
-    StencilArgs ia = base_args(c, s.kc, aK, aM);
-    ia.in0 = dx;
-    ia.in2 = s.invd;
+    StencilArgs ia = base_args(c, aK, aM);
+    ia.invd = s.invd;
     ia.bvec = s.b;
     ia.out0 = s.r;
-    ia.out1 = dx;
+    ia.out_s = s.s;
+    ia.xout = dx;
     ia.sy = make_sync(c, s);
-    Launch init = stencil_launch(c, LD_RAW, EP_RESID_INIT, true, ia, 2);
-    CgLaunches L = cg_launches(c, s, aK, aM, dx, false);
-    StepArgs sa = step_args(c, s, dx, false, nullptr, -1);
+    Launch init;
+    HFCK(stencil_launch(c, LD_RAW, EP_RESID_INIT, true, xm, ia, 2, &init));
+    CgLaunches L;
+    HFCK(cg_launches(c, s, aK, aM, dx, xm, &L));
+    StepArgs sa = step_args(c, s, dx, nullptr, -1);
     sa.iters_out = nullptr;
     Launch post = step_launch(c, sa);
     const bool use_graph = c->driver == 0 && c->nranks == 1 && !c->prof;
     if (use_graph) {
         cudaGraph_t g;
-        HFCK(build_cg_graph(c, s, {}, init, L, {post}, &g));
+        HFCK(build_cg_graph(c, {}, init, L, {post}, &g));
         cudaGraphExec_t ge;
         cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
         if (e != cudaSuccess) { cudaGraphDestroy(g); CUCK(e); }
         e = cudaGraphLaunch(ge, s.stream);
+        cudaStreamSynchronize(s.stream);
         cudaGraphExecDestroy(ge);
         cudaGraphDestroy(g);
         CUCK(e);
@@ -928,7 +1079,7 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
         HFCK(run(c, post, s.stream));
     }
     HFCK(read_state(c, s));
-    HFCK(dev_out_finish(c, x, dx, c->nloc));
+    if (x != dx) HFCK(node_out_finish(c, x, dx));
     const CgState &h = *s.st_host;
     if (info) {
         info->iters = h.iter;
@@ -941,13 +1092,16 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     return HF_OK;
 }
 
-// One system's time loop; U[0] holds u^0 (and U[2] u^{-1} when resuming) on entry.
+}  // extern "C"
+
+// One system's time loop; U[0] holds u^0 (and U[2] u^{-1} when resuming) on entry, F (padded)
+// the flux load.
 static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int nsteps, const double *dF,
                               bool first, int snap_local, double *snapdev, const hf_cg_opts &o)
 {
     const double aK = theta * dt, aM = 1.0;             // A = M + theta dt K
     const double aKL = -(1.0 - theta) * dt, aML = 1.0;  // L = M - (1-theta) dt K   (R8)
-    HFCK(set_solver_opts(c, s, &o, true));
+    HFCK(set_solver_opts(c, s, o));
     if (s.iters_cap < nsteps) {
         cudaFree(s.iters);
         s.iters = nullptr;
@@ -962,57 +1116,65 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     for (int f = 0; f < 6; f++) if ((c->dbits >> f & 1u) && c->gval[f] != 0.0) lift = true;
     if (nsteps <= 0) return HF_OK;
 
-    Sync sy = make_sync(c, s);
-    // b = L u^n + dt F  (knl_RHS_A/B P:678-681), b_D = g
-    StencilArgs ra = base_args(c, s.kc, aKL, aML);
-    ra.bvec = dF;
-    ra.s = dt;
-    ra.out0 = s.b;
-    ra.dmode = 2;
-    ra.rot_role = ROT_RHS;
-    for (int i = 0; i < 3; i++) ra.rot[i] = s.U[i];
-    ra.sy = sy;
-    ra.sy.partials = nullptr;
-    std::vector<Launch> pre;
-    pre.push_back(stencil_launch(c, LD_RAW, EP_APPLY, false, ra, 3));
-    if (lift) {  // b_F -= (A g~)_F  (Dirichlet lift, R3)
-        StencilArgs la = base_args(c, s.kc, aK, aM);
-        la.bvec = s.b;
-        la.s = 1.0;
-        la.c = -1.0;
-        la.out0 = s.b;
-        la.dmode = 2;
-        la.sy = sy;
-        pre.push_back(stencil_launch(c, LD_GT, EP_APPLY, false, la, 3));
-    }
-    // init with the extrapolated guess x0 = 2u^n - u^{n-1} (u0_update)
-    StencilArgs ia = base_args(c, s.kc, aK, aM);
-    ia.in2 = s.invd;
-    ia.bvec = s.b;
-    ia.out0 = s.r;
-    ia.first = first ? 1 : 0;
-    ia.rot_role = ROT_INIT;
-    for (int i = 0; i < 3; i++) ia.rot[i] = s.U[i];
-    ia.sy = sy;
-    ia.zs0 = c->own_lo - (c->own_lo > 0 ? 1 : 0);
-    ia.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
-    Launch init = stencil_launch(c, LD_X0, EP_RESID_INIT, true, ia, 2);
-    CgLaunches L = cg_launches(c, s, aK, aM, nullptr, true);
-    StepArgs sa = step_args(c, s, nullptr, true, snapdev, snap_local);
-    Launch post = step_launch(c, sa);
-
     const bool use_graph = c->driver == 0 && c->nranks == 1 && !c->prof;
+    SimKey key;
+    std::memset(&key, 0, sizeof(key));
+    key.aK = aK; key.aM = aM; key.aKL = aKL; key.aML = aML; key.rtol = o.rtol; key.dt = dt;
+    key.max_iter = o.max_iter; key.replace_every = o.replace_every; key.first = first;
+    key.snap_plane = snap_local; key.lift = lift; key.F = dF; key.snap = snapdev;
+    const bool cached = use_graph && s.key_valid && s.key == key && s.gexec;
+
+    std::vector<Launch> pre;
+    Launch init, post;
+    CgLaunches L;
+    if (!cached) {
+        Sync sy = make_sync(c, s);
+        // b = L u^n + dt F  (knl_RHS_A/B P:678-681), b_D = g
+        StencilArgs ra = base_args(c, aKL, aML);
+        ra.bvec = dF;
+        ra.s = dt;
+        ra.out0 = s.b;
+        ra.dmode = 2;
+        ra.rot_role = ROT_RHS;
+        ra.sy = sy;
+        Launch rhs;
+        HFCK(stencil_launch(c, LD_RAW, EP_APPLY, false, s.maps, ra, 3, &rhs));
+        pre.push_back(rhs);
+        if (lift) {  // b_F -= (A g~)_F  (Dirichlet lift, R3)
+            StencilArgs la = base_args(c, aK, aM);
+            la.bvec = s.b;
+            la.s = 1.0;
+            la.c = -1.0;
+            la.out0 = s.b;
+            la.dmode = 2;
+            la.sy = sy;
+            Launch lf;
+            HFCK(stencil_launch(c, LD_GT, EP_APPLY, false, s.maps, la, 3, &lf));
+            pre.push_back(lf);
+        }
+        // init with the extrapolated guess x0 = 2u^n - u^{n-1} (u0_update)
+        StencilArgs ia = base_args(c, aK, aM);
+        ia.invd = s.invd;
+        ia.bvec = s.b;
+        ia.out0 = s.r;
+        ia.out_s = s.s;
+        ia.first = first ? 1 : 0;
+        ia.rot_role = ROT_INIT;
+        for (int i = 0; i < 3; i++) ia.ring[i] = s.U[i];
+        ia.sy = sy;
+        ia.zs0 = c->own_lo - (c->own_lo > 0 ? 1 : 0);
+        ia.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
+        HFCK(stencil_launch(c, LD_X0, EP_RESID_INIT, true, s.maps, ia, 2, &init));
+        HFCK(cg_launches(c, s, aK, aM, nullptr, s.maps, &L));
+        post = step_launch(c, step_args(c, s, nullptr, snapdev, snap_local));
+    }
+
     if (use_graph) {
-        SimKey key;
-        std::memset(&key, 0, sizeof(key));
-        key.aK = aK; key.aM = aM; key.aKL = aKL; key.aML = aML; key.rtol = o.rtol;
-        key.max_iter = o.max_iter; key.replace_every = o.replace_every; key.first = first;
-        key.snap_plane = snap_local; key.lift = lift; key.F = dF; key.snap = snapdev; key.dt = dt;
-        key.ubase = s.U[0];
-        if (!s.key_valid || !(s.key == key)) {
+        if (!cached) {
             if (s.gexec) { cudaGraphExecDestroy(s.gexec); s.gexec = nullptr; }
             if (s.graph) { cudaGraphDestroy(s.graph); s.graph = nullptr; }
-            HFCK(build_cg_graph(c, s, pre, init, L, {post}, &s.graph));
+            s.key_valid = false;
+            HFCK(build_cg_graph(c, pre, init, L, {post}, &s.graph));
             CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
             s.key = key;
             s.key_valid = true;
@@ -1021,14 +1183,13 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     } else {
         for (int n = 0; n < nsteps; n++) {
             for (auto &p : pre) HFCK(run(c, p, s.stream));
-            if (c->nranks > 1) {
-                // ghost planes of b are never read; x0 ghosts are stored by the init kernel
-            }
             HFCK(run(c, init, s.stream));
             HFCK(comm_after(c, s, EP_RESID_INIT, true));
             HFCK(host_cg_loop(c, s, L, o.max_iter, o.replace_every));
             HFCK(run(c, post, s.stream));
             if (c->nranks > 1) {
+                // the next RHS reads u^{n+1} ghosts: kernel B keeps the iterate's ghost planes
+                // consistent (x update on every local plane)
                 HFCK(read_state(c, s));
                 if (s.st_host->first_failed >= 0) break;
             }
@@ -1056,7 +1217,7 @@ static hf_status finish_stats(hf_ctx *c, Sys &s, hf_sim_stats *stats, float ms)
 }
 
 static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nsteps, const double *F, double *u,
-                                 const double *u_prev, int64_t step0, int64_t snap_plane, double *snap,
+                                 double *u_prev, int64_t step0, int64_t snap_plane, double *snap,
                                  const hf_cg_opts *opts, hf_sim_stats *stats)
 {
     if (!c || !u || nsteps < 0 || !(dt > 0.0) || !(theta >= 0.0 && theta <= 1.0))
@@ -1067,17 +1228,14 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
     Sys &s = c->sys0;
     hf_cg_opts o = {1e-12, 10000, 50};
     if (opts) o = *opts;
-    const double *dF = nullptr;
-    if (F) HFCK(dev_in(c, F, c->nloc, 7, &dF));
-    else {
-        void *z;
-        HFCK(scratch_get(c, 7, c->nloc * sizeof(double), &z));
-        CUCK(cudaMemsetAsync(z, 0, c->nloc * sizeof(double), c->stream));
-        dF = (const double *)z;
-    }
-    CUCK(cudaMemcpyAsync(s.U[0], u, c->nloc * sizeof(double), cudaMemcpyDefault, s.stream));
+    // the flux load lives in a stable internal buffer (graph parameters point at it)
+    void *fbuf;
+    HFCK(scratch_get(c, 7, (size_t)c->nloc * 8, &fbuf));
+    if (F) HFCK(copy_in(c, (double *)fbuf, F, c->nzl, s.stream));
+    else CUCK(cudaMemsetAsync(fbuf, 0, c->nloc * sizeof(double), s.stream));
+    HFCK(copy_in(c, s.U[0], u, c->nzl, s.stream));
     const bool first = step0 <= 0 || !u_prev;
-    if (!first) CUCK(cudaMemcpyAsync(s.U[2], u_prev, c->nloc * sizeof(double), cudaMemcpyDefault, s.stream));
+    if (!first) HFCK(copy_in(c, s.U[2], u_prev, c->nzl, s.stream));
     if (c->nranks > 1) {          // make the ghost planes of the input state consistent
         HFCK(c->comm->exchange(c, s, s.U[0]));
         if (!first) HFCK(c->comm->exchange(c, s, s.U[2]));
@@ -1095,24 +1253,26 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
     CUCK(cudaEventCreate(&e0));
     CUCK(cudaEventCreate(&e1));
     CUCK(cudaEventRecord(e0, s.stream));
-    hf_status st = simulate_sys(c, s, theta, dt, nsteps, dF, first, snap_local, snapdev, o);
+    hf_status st = simulate_sys(c, s, theta, dt, nsteps, (const double *)fbuf, first, snap_local, snapdev, o);
     CUCK(cudaEventRecord(e1, s.stream));
-    if (st != HF_OK) { cudaEventDestroy(e0); cudaEventDestroy(e1); return st; }
+    if (st != HF_OK) { cudaStreamSynchronize(s.stream); cudaEventDestroy(e0); cudaEventDestroy(e1); return st; }
     CUCK(cudaEventSynchronize(e1));
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     hf_status fs = finish_stats(c, s, stats, ms);
-    // the newest iterate sits in U[steps_done % 3] (or U[(failed+1) % 3])
+    // the newest iterate sits in U[steps % 3] (or U[(failed+1) % 3])
     const CgState &h = *s.st_host;
     const int last = h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done;
-    CUCK(cudaMemcpyAsync(u, s.U[last % 3], c->nloc * sizeof(double), cudaMemcpyDefault, s.stream));
-    if (snap && snap_local >= 0)
-        CUCK(cudaMemcpyAsync(snap, snapdev, (size_t)nsteps * c->plane * sizeof(double), cudaMemcpyDefault, s.stream));
+    HFCK(copy_out(c, u, s.U[last % 3], c->nzl, s.stream));
+    if (u_prev && nsteps > 0) HFCK(copy_out(c, u_prev, s.U[(last + 2) % 3], c->nzl, s.stream));
+    if (snap && snap_local >= 0) HFCK(copy_out(c, snap, snapdev, nsteps, s.stream));
     CUCK(cudaStreamSynchronize(s.stream));
     return fs;
 }
+
+extern "C" {
 
 hf_status hf_simulate(hf_ctx *c, double theta, double dt, int32_t nsteps, const double *F, double *u,
                       int64_t snap_plane, double *snap, const hf_cg_opts *opts, hf_sim_stats *stats)
@@ -1125,17 +1285,7 @@ hf_status hf_simulate_resume(hf_ctx *c, double theta, double dt, int32_t nsteps,
 {
     if (!c || !u) return fail(HF_E_ARG, "hf_simulate_resume: NULL argument");
     if (step0 > 0 && !u_prev) return fail(HF_E_ARG, "hf_simulate_resume: u_prev needed for step0 > 0");
-    hf_status st = simulate_common(c, theta, dt, nsteps, F, u, u_prev, step0, -1, nullptr, opts, stats);
-    if (st != HF_OK && st != HF_E_NOCONV && st != HF_E_BREAKDOWN) return st;
-    // u_prev <- u^{n-1} of the new state (the ring slot before the newest)
-    if (u_prev && nsteps > 0) {
-        Sys &s = c->sys0;
-        const CgState &h = *s.st_host;
-        const int last = h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done;
-        CUCK(cudaMemcpyAsync(u_prev, s.U[(last + 2) % 3], c->nloc * sizeof(double), cudaMemcpyDefault, s.stream));
-        CUCK(cudaStreamSynchronize(s.stream));
-    }
-    return st;
+    return simulate_common(c, theta, dt, nsteps, F, u, u_prev, step0, -1, nullptr, opts, stats);
 }
 
 hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const double *c_batch, double theta,
@@ -1157,23 +1307,19 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
         std::unique_ptr<Sys> p(new Sys());
         cudaStream_t st;
         CUCK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        HFCK(sys_alloc(c, *p, true, st));
         p->own_stream = true;
+        HFCK(sys_alloc(c, *p, st));
         c->pool.push_back(std::move(p));
     }
     const size_t ne = (size_t)(c->g.ne[0] * c->g.ne[1] * c->g.ne[2]);
-    const size_t nn = (size_t)c->nloc;
-    const double *dF = nullptr;
-    if (F) HFCK(dev_in(c, F, nn, 7, &dF));
-    else {
-        void *z;
-        HFCK(scratch_get(c, 7, nn * sizeof(double), &z));
-        CUCK(cudaMemsetAsync(z, 0, nn * sizeof(double), c->stream));
-        dF = (const double *)z;
-    }
-    const bool kdev = is_device_ptr(k_batch), udev = is_device_ptr(u_batch);
+    const size_t nn = (size_t)c->nx1 * c->ny1 * c->nzl;     // user (natural) node count
+    const size_t pl = (size_t)c->nx1 * c->ny1;              // user plane
+    void *fbuf;
+    HFCK(scratch_get(c, 7, (size_t)c->nloc * 8, &fbuf));
+    if (F) HFCK(copy_in(c, (double *)fbuf, F, c->nzl, c->stream));
+    else CUCK(cudaMemsetAsync(fbuf, 0, c->nloc * sizeof(double), c->stream));
+    const bool kdev = is_device_ptr(k_batch);
     const bool cdev = c_batch && is_device_ptr(c_batch);
-    // per-slot staging of the host inputs: k, c (per element) and u (per node)
     std::vector<double *> kst(nslots, nullptr), cst(nslots, nullptr);
     for (int i = 0; i < nslots; i++) {
         void *p;
@@ -1181,9 +1327,6 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
         if (c_batch && !cdev) { HFCK(scratch_get(c, 40 + i, ne * sizeof(double), &p)); cst[i] = (double *)p; }
     }
     CUCK(cudaStreamSynchronize(c->stream));
-    cudaEvent_t ready;
-    CUCK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    CUCK(cudaEventRecord(ready, c->stream));
     hf_status first_err = HF_OK;
     std::vector<int> done_sys(nslots, -1);
     auto collect = [&](int slot, int j) -> hf_status {
@@ -1191,11 +1334,10 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
         HFCK(read_state(c, s));
         const CgState &h = *s.st_host;
         const int last = h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done;
-        CUCK(cudaMemcpyAsync(u_batch + (size_t)j * nn, s.U[last % 3], nn * sizeof(double), cudaMemcpyDefault, s.stream));
+        HFCK(copy_out(c, u_batch + (size_t)j * nn, s.U[last % 3], c->nzl, s.stream));
         if (front_out) {
             const int sl = (int)(snap_plane - c->zg0);
-            CUCK(cudaMemcpyAsync(front_out + (size_t)j * c->plane, s.U[last % 3] + (size_t)sl * c->plane,
-                                 c->plane * sizeof(double), cudaMemcpyDefault, s.stream));
+            HFCK(copy_out(c, front_out + (size_t)j * pl, s.U[last % 3] + (size_t)sl * c->plane, 1, s.stream));
         }
         if (stats) {
             stats[j].steps_done = h.steps_done;
@@ -1211,32 +1353,26 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
     for (int j = 0; j < B; j++) {
         const int slot = j % nslots;
         Sys &s = *c->pool[slot];
-        CUCK(cudaStreamWaitEvent(s.stream, ready, 0));
         if (done_sys[slot] >= 0) { HFCK(collect(slot, done_sys[slot])); done_sys[slot] = -1; }
         const double *kj = k_batch + (size_t)j * ne;
         if (!kdev) { CUCK(cudaMemcpyAsync(kst[slot], kj, ne * sizeof(double), cudaMemcpyHostToDevice, s.stream)); kj = kst[slot]; }
-        const double *cj = nullptr;
         if (c_batch) {
-            cj = c_batch + (size_t)j * ne;
+            const double *cj = c_batch + (size_t)j * ne;
             if (!cdev) { CUCK(cudaMemcpyAsync(cst[slot], cj, ne * sizeof(double), cudaMemcpyHostToDevice, s.stream)); cj = cst[slot]; }
-        }
-        if (cj) HFCK(enqueue_pack(c, s, kj, cj));
-        else {
-            // shared capacity: k from this system, c copied from the context's packed array
-            HFCK(enqueue_pack(c, s, kj, kj));   // placeholder c lane, overwritten below
-            // copy the capacity lane of the context's packed array (strided y of double2)
+            HFCK(enqueue_pack(c, s, kj, cj));
+        } else {
+            // shared capacity: k from this system, the c lane copied from the context's pairs
+            HFCK(enqueue_pack(c, s, kj, nullptr));
             CUCK(cudaMemcpy2DAsync((char *)s.kc + sizeof(double), sizeof(double2), (const char *)c->sys0.kc + sizeof(double),
                                    sizeof(double2), sizeof(double), (size_t)c->kc_elems, cudaMemcpyDeviceToDevice, s.stream));
         }
-        const double *uj = u_batch + (size_t)j * nn;
-        CUCK(cudaMemcpyAsync(s.U[0], uj, nn * sizeof(double), udev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s.stream));
-        HFCK(simulate_sys(c, s, theta, dt, nsteps, dF, true, -1, nullptr, o));
+        HFCK(copy_in(c, s.U[0], u_batch + (size_t)j * nn, c->nzl, s.stream));
+        HFCK(simulate_sys(c, s, theta, dt, nsteps, (const double *)fbuf, true, -1, nullptr, o));
         done_sys[slot] = j;
     }
     for (int i = 0; i < nslots; i++)
         if (done_sys[i] >= 0) HFCK(collect(i, done_sys[i]));
     for (int i = 0; i < nslots; i++) CUCK(cudaStreamSynchronize(c->pool[i]->stream));
-    cudaEventDestroy(ready);
     if (first_err != HF_OK) return fail(first_err, "hf_simulate_batched: a system failed to converge");
     return HF_OK;
 }
@@ -1264,6 +1400,8 @@ hf_status hf_nccl_unique_id(uint8_t id[128])
     return HF_OK;
 }
 
+}  // extern "C"
+
 // ---- NCCL transport ------------------------------------------------------------------------
 struct NcclComm : Comm {
     nccl::ncclComm_t comm = nullptr;
@@ -1286,14 +1424,13 @@ struct NcclComm : Comm {
     }
     hf_status allreduce(hf_ctx *c, Sys &s, double *v, int n) override
     {
+        (void)c;
         NCCK(nccl::g_api.allReduce(v, v, (size_t)n, nccl::ncclFloat64, nccl::ncclSum, comm, s.stream));
         return HF_OK;
     }
 };
 
 // ---- in-process transport (all ranks in one process, one host thread each) -----------------
-}  // extern "C"
-
 struct hf_local_group {
     int n = 0;
     std::mutex mu;
@@ -1464,7 +1601,7 @@ hf_status hf_flush_l2(hf_ctx *c)
     if (!c) return fail(HF_E_ARG, "hf_flush_l2: NULL");
     const size_t bytes = 512ull << 20;   // 4x the 126 MB L2
     if (!c->flush) CUCK(cudaMalloc(&c->flush, bytes));
-    CUCK(cudaMemsetAsync(c->flush, c->launches ? 1 : 0, bytes, c->stream));
+    CUCK(cudaMemsetAsync(c->flush, 1, bytes, c->stream));
     return HF_OK;
 }
 
