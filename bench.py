@@ -1,0 +1,361 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: ms per time step at 1M DoF (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2]): 100^3 nodes (99^3 Q1 voxels), h = 0.2 mm,
+20 % spherical oxide inclusions in steel (P:271 materials), flux f = 1 on z = 0,
+Crank-Nicolson (theta = 0.5), dt = 0.01, Jacobi-PCG to rtol 1e-12.  A "step" is one time step
+of the theta-scheme: RHS apply + PCG solve (Alg. 1) + guess update, all on the device.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1: one GPU, the C3 problem.  N > 1 (torchrun, one process per GPU): the same global C3
+problem split into z-slabs over N GPUs (NCCL ghost planes + allreduce; strong scaling).
+--impl reference: the CPU oracle (oracle/, plain C, 1 core) on the same workload, a bounded
+sample of steps.  Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "ms per time step at 1M DOF (C3: 100^3-node heterogeneous cube, CN, Jacobi-PCG rtol 1e-12)"
+UNIT = "ms/step"
+
+
+def workload_config(p, n_gpus, extra=None):
+    cfg = {
+        "workload": "C3 (BASELINE.json configs[2]): 100^3 nodes = 1,000,000 DoF, 99^3 trilinear voxels, "
+                    "h=0.2 mm, 20% spherical Fe2O3 inclusions in steel (P:271), f=1 on z=0, theta=0.5, "
+                    "dt=0.01, rtol=1e-12, guess 2u^n-u^(n-1)",
+        "nodes": p.grid.n_nodes,
+        "elements": p.grid.n_elems,
+        "parallelism": "single GPU" if n_gpus == 1 else f"z-slabs x{n_gpus} (NCCL ghost planes + allreduce)",
+        "l2": "flushed (512 MiB memset) before every timed step; within a step the 104 MB working set "
+              "stays L2-resident, as in any real run",
+    }
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_key):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d[kernel_key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+
+def run_ours(args):
+    import torch
+    import paper_1905_07622_b200 as hf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    p = synth.c3(nsteps=args.warmup + args.steps)
+    g = p.grid
+    plane = (g.ne[0] + 1) * (g.ne[1] + 1)
+    kd = torch.tensor(p.k, device=dev)
+    cd = torch.tensor(p.c, device=dev)
+    if world == 1:
+        ctx = hf.hf_create(g, local_rank)
+        z0, lp = 0, g.ne[2] + 1
+    else:
+        uid = hf.hf_nccl_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = hf.hf_create_slab(g, rank, world, obj[0], transport=0, device=local_rank)
+        _, _, lp, z0 = ctx.slab
+    hf.hf_set_coefficients(ctx, kd, cd)
+    F = torch.empty(ctx.n_nodes, dtype=torch.float64, device=dev)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
+    u = torch.zeros(ctx.n_nodes, dtype=torch.float64, device=dev)
+    up = torch.zeros_like(u)
+    stream = torch.cuda.current_stream(dev)
+
+    # warm-up steps (state continues into the timed steps)
+    st = hf.hf_simulate_resume(ctx, p.theta, p.dt, args.warmup, F, u, up, 0, rtol=p.rtol)
+    step0 = args.warmup
+    lc0 = hf.hf_get_launch_count(ctx)
+    clocks = ClockSampler(local_rank)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    times, iters = [], 0
+    for n in range(args.steps):
+        hf.hf_flush_l2(ctx)                       # untimed L2 eviction between timed steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st = hf.hf_simulate_resume(ctx, p.theta, p.dt, 1, F, u, up, step0 + n, rtol=p.rtol)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        iters += st["total_iters"]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = hf.hf_get_launch_count(ctx) - lc0
+    total_ms = float(sum(times))
+    if dist:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+
+    # dominant kernel: PCG kernel A (stencil apply), timed per launch with CUDA events on the
+    # context stream over the same steps replayed with the profiling driver
+    u2, up2 = u.clone(), up.clone()
+    hf.hf_profile(ctx, True)
+    prof_steps = min(args.steps, 5)
+    hf.hf_simulate_resume(ctx, p.theta, p.dt, prof_steps, F, u2, up2, step0 + args.steps, rtol=p.rtol)
+    prof = hf.hf_profile_read(ctx)
+    hf.hf_profile(ctx, False)
+    a_ms, a_n = prof["stencil_cg_a"]
+    a_avg_ms = a_ms / max(a_n, 1)
+    nodes_local = plane * lp
+    elems_local = g.ne[0] * g.ne[1] * max(lp - 1, 1)
+    # algorithmic bytes of one kernel-A launch: read s, d_old (16 B/node) + (k,c) (16 B/element),
+    # write d_new, q (16 B/node)
+    a_bytes = 32.0 * nodes_local + 16.0 * elems_local
+    peak, peak_src = measured_peaks()
+    achieved = a_bytes / (a_avg_ms * 1e-3) / 1e9
+
+    # e2e: the same workload through the public API from pinned host memory: H2D of k, c, u0
+    # and D2H of the front-face plane every step + the final field, inside the timed region
+    e2e = None
+    if world == 1:
+        kh = torch.tensor(p.k).pin_memory()
+        ch = torch.tensor(p.c).pin_memory()
+        uh = torch.zeros(g.n_nodes, dtype=torch.float64).pin_memory()
+        snap = torch.empty(args.steps * plane, dtype=torch.float64).pin_memory()
+        ctx2 = hf.hf_create(g, local_rank)
+        Fe = torch.empty(g.n_nodes, dtype=torch.float64, device=dev)
+        hf.hf_set_coefficients(ctx2, kh, ch)
+        hf.hf_face_load(ctx2, p.flux_face, p.flux_const, None, Fe)
+        hf.hf_simulate(ctx2, p.theta, p.dt, 2, Fe, torch.zeros(g.n_nodes, dtype=torch.float64, device=dev))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hf.hf_set_coefficients(ctx2, kh, ch)
+        hf.hf_face_load(ctx2, p.flux_face, p.flux_const, None, Fe)
+        se = hf.hf_simulate(ctx2, p.theta, p.dt, args.steps, Fe, uh, 0, snap, rtol=p.rtol)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        e2e = {"value": wall / args.steps, "unit": UNIT,
+               "h2d_bytes_per_step": int((kh.numel() + ch.numel() + uh.numel()) * 8 / args.steps),
+               "d2h_bytes_per_step": int(plane * 8 + uh.numel() * 8 / args.steps),
+               "how": "wall clock around hf_set_coefficients + hf_face_load + hf_simulate(K steps) with pinned "
+                      "host k, c, u0, u_N and a per-step front-face snapshot (host)"}
+        del ctx2
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded inclusion field, synth.c3)",
+            "config": workload_config(p, world, {"pcg_iters_per_step": iters / args.steps,
+                                                 "us_per_pcg_iter": total_ms / max(iters, 1) * 1e3}),
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": ncu_traffic("stencil_cg_a_c3"),
+                         "kernel": "k_stencil<LD_CGD,EP_CGA> (PCG kernel A: d = s + beta d; q = A d; d.q)",
+                         "bytes_per_launch": a_bytes, "avg_launch_ms": a_avg_ms, "launches_timed": int(a_n),
+                         "peak_source": peak_src,
+                         "note": "C3 working set (~104 MB) is L2-resident during a step, so achieved can exceed "
+                                 "the HBM copy peak; see apply_512 for the HBM-bound apply"},
+        }
+    if world == 1:
+        line["apply_512"] = apply_512(hf, torch, dev, peak)
+    if rank == 0:
+        line["cpu_baseline"] = cpu_baseline(args)
+    return line
+
+
+def apply_512(hf, torch, dev, peak):
+    """Operator apply (Eq. (1)) on the 512^3-node grid of C4, HBM-bound: inputs 4.3 GB >> L2."""
+    g = synth.c4_grid(512)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    k = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) * 121.5 + 1.0
+    c = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) + 1.0
+    u = torch.randn(g.n_nodes, dtype=torch.float64, device=dev, generator=gen)
+    y = torch.empty_like(u)
+    ctx = hf.hf_create(g, dev.index)
+    hf.hf_set_coefficients(ctx, k, c)
+    del k, c
+    for _ in range(3):
+        hf.hf_apply(ctx, 0.005, 1.0, u, y)
+    s = torch.cuda.current_stream(dev)
+    ts = []
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        hf.hf_apply(ctx, 0.005, 1.0, u, y)
+        e1.record(s)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    byts = 16.0 * g.n_nodes + 16.0 * g.n_elems      # read u + write y + read (k, c)
+    ach = byts / (ms * 1e-3) / 1e9
+    del ctx
+    torch.cuda.empty_cache()
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "ms": ms,
+            "bytes_per_launch": byts, "traffic": ncu_traffic("stencil_apply_512"),
+            "kernel": "k_stencil<LD_RAW,EP_APPLY> (y = (aK K + aM M) u), 512^3 nodes, median of 10"}
+
+
+# ---------------------------------------------------------------------------------------------
+# the oracle on the host
+
+def oracle_steps(nsteps_timed, warm=1):
+    import oracle
+    p = synth.c3(nsteps=nsteps_timed + warm)
+    t0 = time.perf_counter()
+    o, F = oracle.problem_oracle(p)
+    t_setup = time.perf_counter() - t0
+    u, st, it, _ = o.simulate(p.theta, p.dt, warm, F, p.u0, tol=p.rtol)
+    # continue from u^warm: the oracle restarts with guess u (same as u^0 rule)
+    t0 = time.perf_counter()
+    u2, st, it2, _ = o.simulate(p.theta, p.dt, nsteps_timed, F, u, tol=p.rtol)
+    t = time.perf_counter() - t0
+    return t * 1e3 / nsteps_timed, int(it2.sum()), t_setup, p
+
+
+def cpu_baseline(args):
+    steps = 2
+    ms, iters, t_setup, p = oracle_steps(steps, warm=0)
+    return {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} time steps of C3 after CSR assembly ({t_setup:.1f} s, excluded): "
+                      f"{iters / steps:.0f} PCG iterations/step, plain C, 1 thread"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    steps = max(1, min(args.steps, 20))
+    warm = 1 if args.warmup > 0 else 0
+    ms, iters, t_setup, p = oracle_steps(steps, warm=warm)
+    sample = (f"{steps} of the K={args.steps} requested C3 time steps (capped at 20 to bound the run), after "
+              f"{warm} warm-up step and CSR assembly ({t_setup:.1f} s, excluded); plain C oracle, 1 thread")
+    return {"impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded inclusion field, synth.c3)",
+            "config": workload_config(p, 1, {"pcg_iters_per_step": iters / steps}),
+            "cpu_baseline": {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

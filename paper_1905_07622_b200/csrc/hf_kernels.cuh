@@ -303,11 +303,12 @@ template <int R, int NW, int LD>
 struct StencilShape {
     static constexpr int H = NW * R + 1;                                     // node rows per box
     static constexpr int NA = LD == LD_RAW ? 1 : (LD == LD_GT ? 0 : 2);      // node arrays per plane
-    static constexpr int NODE_DBL = H * BOXW;                                // doubles per node box
+    static constexpr int NODE_BOX = H * BOXW;                                // doubles per node box
+    static constexpr int NODE_DBL = (NODE_BOX + 15) / 16 * 16;               // 128-B aligned slot
     static constexpr int KC_DBL = NW * R * 64;                               // doubles per kc box
-    static constexpr int STAGE_DBL = NA * NODE_DBL + KC_DBL;
-    static constexpr unsigned STAGE_BYTES = STAGE_DBL * 8u;
-    static size_t smem_bytes(int ns) { return (size_t)ns * STAGE_BYTES + 16 * ns + 2 * NW * 32 * 8 + 128; }
+    static constexpr int STAGE_DBL = NA * NODE_DBL + KC_DBL;                 // multiple of 16
+    static constexpr unsigned STAGE_BYTES = (NA * NODE_BOX + KC_DBL) * 8u;   // TMA transaction bytes
+    static size_t smem_bytes(int ns) { return (size_t)ns * STAGE_DBL * 8 + 16 * ns + 2 * NW * 32 * 8 + 128; }
 };
 
 template <int R, int NW, int NS, int LD, int EP, bool MASK>
