@@ -31,7 +31,7 @@ namespace hf {
 
 constexpr int NPART = 4;      // partial sums per block
 constexpr int TILE_X = 31;    // owned node columns per CTA
-constexpr int BOXW = 34;      // node columns in a TMA box (X0-1 .. X0+32; 34*8 B is 16-B aligned)
+constexpr int BOXW = 34;      // node columns in a TMA box (even start <= X0-1, covers X0+31)
 constexpr int NMAPS = 6;      // node tensor maps: ring U[0..2], d[0..1], s
 
 enum { LD_RAW = 0, LD_GT = 1, LD_CGD = 2, LD_X0 = 3 };
@@ -366,6 +366,10 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
     const int X0 = blockIdx.x * TILE_X;
     const int Y0 = blockIdx.y * (NW * R - 1);
     const int xi = X0 - 1 + lane;
+    // TMA box x origin must be 16-B aligned (even for fp64): the box starts at the even column
+    // xb <= X0-1 and lane l reads box column l + xoff (xoff = 0 or 1; the box is 34 wide)
+    const int xb = (X0 - 1) & ~1;
+    const int xoff = (X0 - 1) - xb;
     const int yb = Y0 - 1 + w * R;
     const int zb = a.z_out0 + blockIdx.z * a.zchunk;
     const int ze = min(zb + a.zchunk, a.z_out1);
@@ -377,8 +381,8 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
         const int p = zb - 1 + it;
         double *sb = stage + st * SH::STAGE_DBL;
         mbar_expect_tx(&bars[st], SH::STAGE_BYTES);
-        if (NA >= 1) tma_load_3d(sb, &maps.node[map0], X0 - 1, Y0 - 1, p, &bars[st]);
-        if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, &maps.node[map1], X0 - 1, Y0 - 1, p, &bars[st]);
+        if (NA >= 1) tma_load_3d(sb, &maps.node[map0], xb, Y0 - 1, p, &bars[st]);
+        if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, &maps.node[map1], xb, Y0 - 1, p, &bars[st]);
         // element layer L = p - 1 sits at z = p in the kc tensor
         tma_load_3d(sb + NA * SH::NODE_DBL, &maps.kc, 2 * (X0 - 1), Y0 - 1, p, &bars[st]);
     };
@@ -407,8 +411,8 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
         const int st = it % NS;
         mbar_wait(&bars[st], (it / NS) & 1);
         const double *sb = stage + st * SH::STAGE_DBL;
-        const double *n0 = sb;
-        const double *n1 = sb + SH::NODE_DBL;
+        const double *n0 = sb + xoff;
+        const double *n1 = sb + SH::NODE_DBL + xoff;
         const double *kcs = sb + NA * SH::NODE_DBL;
         // ---- node values of plane p (rows 0..R), x butterfly (edges) ----------------------
         double S[R + 1], D[R + 1], craw[R];
