@@ -308,16 +308,26 @@ struct StencilShape {
     static constexpr int KC_DBL = NW * R * 64;                               // doubles per kc box
     static constexpr int STAGE_DBL = NA * NODE_DBL + KC_DBL;                 // multiple of 16
     static constexpr unsigned STAGE_BYTES = (NA * NODE_BOX + KC_DBL) * 8u;   // TMA transaction bytes
-    static size_t smem_bytes(int ns) { return (size_t)ns * STAGE_DBL * 8 + 16 * ns + 2 * NW * 32 * 8 + 128; }
+    static size_t smem_bytes(int ns) { return (size_t)ns * STAGE_DBL * 8 + 16 * ns + 2 * NW * 32 * 8; }
 };
 
-template <int R, int NW, int NS, int LD, int EP, bool MASK>
+// compile-time variant flags of the stencil kernel
+enum {
+    FL_MASK = 1,   // Dirichlet nodes enter the stencil as 0 (constrained operator P_F A P_F)
+    FL_DIR = 2,    // Dirichlet rows in the epilogue (identity rows / r_D = 0 / set g)
+    FL_HB = 4,     // EP_APPLY: y = c A u + s b (else y = c A u)
+    FL_DSET = 8,   // EP_APPLY with FL_DIR: y_D = g (else y_D = u_D, identity rows)
+};
+
+template <int R, int NW, int NS, int LD, int EP, int FL>
 __global__ void __launch_bounds__(32 * NW)
 k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
 {
     using SH = StencilShape<R, NW, LD>;
     constexpr int NT = 32 * NW;
     constexpr int NA = SH::NA;
+    constexpr bool MASK = (FL & FL_MASK) != 0, DIR = (FL & FL_DIR) != 0;
+    constexpr bool HB = (FL & FL_HB) != 0, DSET = (FL & FL_DSET) != 0;
     const Geom &g = a.g;
     const int lane = threadIdx.x, w = threadIdx.y;
     const int tid = lane + 32 * w;
@@ -358,10 +368,10 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
     }
     if (LD == LD_X0 && first) map1 = map0;       // u^{-1} unused: keep the byte count fixed
 
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *stage = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + NS * SH::STAGE_DBL);
-    double(*seam)[NW][32] = reinterpret_cast<double(*)[NW][32]>(bars + 2 * NS);
+    extern __shared__ __align__(128) double smem_d[];
+    double *stage = smem_d;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_d + NS * SH::STAGE_DBL);
+    double(*seam)[NW][32] = reinterpret_cast<double(*)[NW][32]>(smem_d + NS * SH::STAGE_DBL + 2 * NS);
 
     const int X0 = blockIdx.x * TILE_X;
     const int Y0 = blockIdx.y * (NW * R - 1);
@@ -374,7 +384,12 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
     const int zb = a.z_out0 + blockIdx.z * a.zchunk;
     const int ze = min(zb + a.zchunk, a.z_out1);
     const int nplanes = ze - zb + 2;               // planes zb-1 .. ze
-    const bool xown = lane >= 1 && xi < g.nx1;
+    // rows this thread owns (writes): lane >= 1, inside the grid, not the tile's halo row
+    unsigned own = 0;
+#pragma unroll
+    for (int e = 0; e < R; e++)
+        if (lane >= 1 && xi < g.nx1 && (w > 0 || e > 0) && yb + e < g.ny1) own |= 1u << e;
+    const long long rowbase = (long long)yb * g.pitch + xi;   // node (xi, yb) within a plane
 
     auto issue = [&](int it) {                     // TMA of plane zb-1+it into its stage
         const int st = it % NS;
@@ -388,6 +403,7 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
     };
 
     if (tid == 0) {
+        if (smem_u32(stage) & 127u) __trap();     // TMA destinations need 128-B alignment
         for (int i = 0; i < NS; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
@@ -411,26 +427,26 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
         const int st = it % NS;
         mbar_wait(&bars[st], (it / NS) & 1);
         const double *sb = stage + st * SH::STAGE_DBL;
-        const double *n0 = sb + xoff;
-        const double *n1 = sb + SH::NODE_DBL + xoff;
-        const double *kcs = sb + NA * SH::NODE_DBL;
+        const double *n0 = sb + w * R * BOXW + lane + xoff;                 // row 0 of this warp
+        const double *n1 = sb + SH::NODE_DBL + w * R * BOXW + lane + xoff;
+        const double *kcs = sb + NA * SH::NODE_DBL + w * R * 64 + 2 * lane;
         // ---- node values of plane p (rows 0..R), x butterfly (edges) ----------------------
         double S[R + 1], D[R + 1], craw[R];
-        const bool store_p = (p >= a.zs0 && p < a.zs1) &&
+        const bool store_p = (EP == EP_CGA || EP == EP_RESID_INIT) && (p >= a.zs0 && p < a.zs1) &&
                              ((p >= zb && p < ze) || (p == zb - 1 && zb == a.z_out0) ||
                               (p == ze && ze == a.z_out1));
+        double *cst = store_p ? cstore + (long long)p * g.plane + rowbase : nullptr;
 #pragma unroll
         for (int r = 0; r <= R; r++) {
-            const int row = w * R + r;
             double v, v1;
-            if (LD == LD_RAW) { v = n0[row * BOXW + lane]; v1 = n0[row * BOXW + lane + 1]; }
+            if (LD == LD_RAW) { v = n0[r * BOXW]; v1 = n0[r * BOXW + 1]; }
             else if (LD == LD_CGD) {
-                v = fma(beta, n1[row * BOXW + lane], n0[row * BOXW + lane]);
-                v1 = fma(beta, n1[row * BOXW + lane + 1], n0[row * BOXW + lane + 1]);
+                v = fma(beta, n1[r * BOXW], n0[r * BOXW]);
+                v1 = fma(beta, n1[r * BOXW + 1], n0[r * BOXW + 1]);
             } else if (LD == LD_X0) {
-                v = n0[row * BOXW + lane];
-                v1 = n0[row * BOXW + lane + 1];
-                if (!first) { v = 2.0 * v - n1[row * BOXW + lane]; v1 = 2.0 * v1 - n1[row * BOXW + lane + 1]; }
+                v = n0[r * BOXW];
+                v1 = n0[r * BOXW + 1];
+                if (!first) { v = 2.0 * v - n1[r * BOXW]; v1 = 2.0 * v1 - n1[r * BOXW + 1]; }
             } else {   // LD_GT: the Dirichlet lift g~ (g on D nodes, 0 elsewhere)
                 double gv = 0.0;
                 const int yi = yb + r;
@@ -443,11 +459,9 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
             if (r < R) {
                 craw[r] = v;
                 // d_new (CG kernel A) or the guess x0 (init) is stored once, raw, by its owner
-                if ((EP == EP_CGA || EP == EP_RESID_INIT) && store_p && xown && (w > 0 || r > 0) &&
-                    yb + r < g.ny1 && p >= 0 && p < g.nzl)
-                    cstore[(long long)p * g.plane + (long long)(yb + r) * g.pitch + xi] = v;
+                if (store_p && ((own >> r) & 1u)) cst[r * g.pitch] = v;
             }
-            if (MASK && g.dbits) {
+            if (MASK) {
                 double gv;
                 const int yi = yb + r;
                 if (is_dirichlet(g, xi, yi, p, gv)) v = 0.0;
@@ -467,7 +481,7 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
             Fc[1] = S[r] - S[r + 1];   // sx=0, sy=1
             Fc[2] = D[r] + D[r + 1];   // sx=1, sy=0
             Fc[3] = D[r] - D[r + 1];   // sx=1, sy=1
-            const double2 kc = *reinterpret_cast<const double2 *>(kcs + (w * R + r) * 64 + 2 * lane);
+            const double2 kc = *reinterpret_cast<const double2 *>(kcs + r * 64);
 #pragma unroll
             for (int ch = 0; ch < 4; ch++) {
                 const double av = fma(kc.x, a.lam.ka[ch], kc.y * a.lam.ma[ch]);
@@ -483,32 +497,36 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
         double yv[R + 1];
 #pragma unroll
         for (int e = 0; e <= R; e++) {
-            double E0 = 0.0, E1 = 0.0;               // sx = 0, 1
-            if (e < R) { E0 += T[e][0] + T[e][1]; E1 += T[e][2] + T[e][3]; }
-            if (e > 0) { E0 += T[e - 1][0] - T[e - 1][1]; E1 += T[e - 1][2] - T[e - 1][3]; }
+            double E0, E1;                              // sx = 0, 1
+            if (e == 0) { E0 = T[0][0] + T[0][1]; E1 = T[0][2] + T[0][3]; }
+            else if (e == R) { E0 = T[R - 1][0] - T[R - 1][1]; E1 = T[R - 1][2] - T[R - 1][3]; }
+            else {
+                E0 = (T[e][0] + T[e][1]) + (T[e - 1][0] - T[e - 1][1]);
+                E1 = (T[e][2] + T[e][3]) + (T[e - 1][2] - T[e - 1][3]);
+            }
             const double left = __shfl_up_sync(0xffffffffu, E0 - E1, 1);
-            yv[e] = (E0 + E1) + left;                // lane 0's value is not owned
+            yv[e] = (E0 + E1) + left;                   // lane 0's value is not owned
         }
         seam[it & 1][w][lane] = yv[R];
-        __syncthreads();                              // seam visible; stage `st` fully read
+        __syncthreads();                                // seam visible; stage `st` fully read
         if (tid == 0 && it + NS < nplanes) {
             fence_proxy_async();
             issue(it + NS);
         }
         if (out_plane) {
             if (w > 0) yv[0] += seam[it & 1][w - 1][lane];
+            const long long pofs = (long long)pout * g.plane + rowbase;
 #pragma unroll
             for (int e = 0; e < R; e++) {
-                const int yi = yb + e;
-                if (!(xown && (w > 0 || e > 0) && yi < g.ny1)) continue;
-                const long long idx = (long long)pout * g.plane + (long long)yi * g.pitch + xi;
+                if (!((own >> e) & 1u)) continue;
+                const long long idx = pofs + e * g.pitch;
                 double gv = 0.0;
-                const bool isd = is_dirichlet(g, xi, yi, pout, gv);
+                const bool isd = DIR && is_dirichlet(g, xi, yb + e, pout, gv);
                 if (EP == EP_APPLY) {
                     double y = a.c * yv[e];
-                    if (a.dmode == 1 && isd) y = cen[e];
-                    if (a.bvec) y = fma(a.s, a.bvec[idx], y);
-                    if (a.dmode == 2 && isd) y = gv;
+                    if (DIR && !DSET && isd) y = cen[e];
+                    if (HB) y = fma(a.s, a.bvec[idx], y);
+                    if (DIR && DSET && isd) y = gv;
                     a.out0[idx] = y;
                 } else if (EP == EP_CGA) {
                     const double d = cen[e];

@@ -406,27 +406,39 @@ struct StencilFn {
     size_t smem;
 };
 
-template <int R, int LD, int EP, bool MASK> static StencilFn stencil_fn_t()
+template <int R, int LD, int EP, int FL> static StencilFn stencil_fn_t()
 {
     constexpr int NS = ns_of<R, LD>();
-    return {(const void *)k_stencil<R, NW, NS, LD, EP, MASK>, StencilShape<R, NW, LD>::smem_bytes(NS)};
+    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL>, StencilShape<R, NW, LD>::smem_bytes(NS)};
 }
 
-template <int LD, int EP, bool MASK> static StencilFn stencil_fn_r(int R)
-{
-    return R >= 4 ? stencil_fn_t<4, LD, EP, MASK>() : stencil_fn_t<2, LD, EP, MASK>();
-}
+// every (loader, epilogue, flags) variant the library launches, for tile heights R = 2 and 4
+#define HF_STENCIL_VARIANTS(X)                                                                  \
+    X(LD_RAW, EP_APPLY, 0)                                                                      \
+    X(LD_RAW, EP_APPLY, FL_HB)                                                                  \
+    X(LD_RAW, EP_APPLY, FL_HB | FL_DIR | FL_DSET)                                               \
+    X(LD_GT, EP_APPLY, FL_HB | FL_DIR | FL_DSET)                                                \
+    X(LD_CGD, EP_CGA, 0)                                                                        \
+    X(LD_CGD, EP_CGA, FL_DIR)                                                                   \
+    X(LD_X0, EP_RESID_INIT, 0)                                                                  \
+    X(LD_X0, EP_RESID_INIT, FL_MASK | FL_DIR)                                                   \
+    X(LD_RAW, EP_RESID_INIT, 0)                                                                 \
+    X(LD_RAW, EP_RESID_INIT, FL_MASK | FL_DIR)                                                  \
+    X(LD_RAW, EP_RESID, 0)                                                                      \
+    X(LD_RAW, EP_RESID, FL_MASK | FL_DIR)
 
-static StencilFn stencil_fn(int R, int LD, int EP, bool MASK)
+static StencilFn stencil_fn(int R, int LD, int EP, int FL)
 {
-    if (LD == LD_RAW && EP == EP_APPLY && !MASK) return stencil_fn_r<LD_RAW, EP_APPLY, false>(R);
-    if (LD == LD_GT && EP == EP_APPLY && !MASK) return stencil_fn_r<LD_GT, EP_APPLY, false>(R);
-    if (LD == LD_CGD && EP == EP_CGA && !MASK) return stencil_fn_r<LD_CGD, EP_CGA, false>(R);
-    if (LD == LD_X0 && EP == EP_RESID_INIT && MASK) return stencil_fn_r<LD_X0, EP_RESID_INIT, true>(R);
-    if (LD == LD_RAW && EP == EP_RESID_INIT && MASK) return stencil_fn_r<LD_RAW, EP_RESID_INIT, true>(R);
-    if (LD == LD_RAW && EP == EP_RESID && MASK) return stencil_fn_r<LD_RAW, EP_RESID, true>(R);
+#define X(ld, ep, fl)                                                                           \
+    if (LD == (ld) && EP == (ep) && FL == (fl))                                                 \
+        return R >= 4 ? stencil_fn_t<4, ld, ep, fl>() : stencil_fn_t<2, ld, ep, fl>();
+    HF_STENCIL_VARIANTS(X)
+#undef X
     return {nullptr, 0};
 }
+
+// flags of a launch on this context
+static int dir_flags(const hf_ctx *c, int EP, bool has_b, bool dset);
 
 static std::mutex g_attr_mu;
 static std::map<std::pair<const void *, int>, bool> g_attr_done;
@@ -488,10 +500,24 @@ static StencilArgs base_args(hf_ctx *c, double aK, double aM)
     return a;
 }
 
-static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool MASK, const Maps &maps, StencilArgs a, int cls,
+static int dir_flags(const hf_ctx *c, int EP, bool has_b, bool dset)
+{
+    int fl = has_b && EP == EP_APPLY ? FL_HB : 0;
+    if (c->dbits) {
+        if (EP == EP_APPLY) { if (dset) fl |= FL_DIR | FL_DSET; }
+        else if (EP == EP_CGA) fl |= FL_DIR;
+        else fl |= FL_MASK | FL_DIR;
+    }
+    return fl;
+}
+
+// stencil launch spec.  dset: EP_APPLY writes g on Dirichlet rows (RHS / lift); the plain
+// apply (hf_apply) is the unconstrained operator.
+static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps &maps, StencilArgs a, int cls,
                                 Launch *out)
 {
-    StencilFn f = stencil_fn(c->tileR, LD, EP, MASK);
+    const int FL = dir_flags(c, EP, a.bvec != nullptr, dset);
+    StencilFn f = stencil_fn(c->tileR, LD, EP, FL);
     if (!f.fn) return fail(HF_E_ARG, "internal: no stencil instantiation");
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
     dim3 grid;
@@ -640,7 +666,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e);
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
     // resident CTAs per SM of the CG stencil decide the z split of the grid
-    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, false);
+    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0);
     HFCK(ensure_smem_attr(f.fn, f.smem, device));
     int occ = 0;
     CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
@@ -1138,7 +1164,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
         ra.rot_role = ROT_RHS;
         ra.sy = sy;
         Launch rhs;
-        HFCK(stencil_launch(c, LD_RAW, EP_APPLY, false, s.maps, ra, 3, &rhs));
+        HFCK(stencil_launch(c, LD_RAW, EP_APPLY, true, s.maps, ra, 3, &rhs));
         pre.push_back(rhs);
         if (lift) {  // b_F -= (A g~)_F  (Dirichlet lift, R3)
             StencilArgs la = base_args(c, aK, aM);
@@ -1149,7 +1175,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             la.dmode = 2;
             la.sy = sy;
             Launch lf;
-            HFCK(stencil_launch(c, LD_GT, EP_APPLY, false, s.maps, la, 3, &lf));
+            HFCK(stencil_launch(c, LD_GT, EP_APPLY, true, s.maps, la, 3, &lf));
             pre.push_back(lf);
         }
         // init with the extrapolated guess x0 = 2u^n - u^{n-1} (u0_update)
