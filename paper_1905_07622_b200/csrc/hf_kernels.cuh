@@ -597,26 +597,44 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     const double *dvec = a.dbuf[(it & 1) ^ 1];
     double *xvec = a.rot[0] ? a.rot[(st->step + 1) % 3] : a.x;
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
-    // n is even (even row pitch): every thread handles aligned pairs
-    const long long stride = (long long)gridDim.x * NT * 2;
-    for (long long i = ((long long)blk * NT + tid) * 2; i < a.n; i += stride) {
-        double2 xv = *reinterpret_cast<const double2 *>(xvec + i);
-        const double2 dv = *reinterpret_cast<const double2 *>(dvec + i);
-        xv.x = fma(alpha, dv.x, xv.x);
-        xv.y = fma(alpha, dv.y, xv.y);
-        *reinterpret_cast<double2 *>(xvec + i) = xv;
-        if (!replace && i >= a.own0 && i < a.own1) {
-            double2 rv = *reinterpret_cast<const double2 *>(a.r + i);
-            const double2 qv = __ldg(reinterpret_cast<const double2 *>(a.q + i));
-            const double2 iv = __ldg(reinterpret_cast<const double2 *>(a.invd + i));
-            rv.x = fma(-alpha, qv.x, rv.x);
-            rv.y = fma(-alpha, qv.y, rv.y);
-            const double2 sv = make_double2(rv.x * iv.x, rv.y * iv.y);
-            acc[0] = fma(rv.x, sv.x, acc[0]);
-            acc[0] = fma(rv.y, sv.y, acc[0]);
-            acc[1] = fma(rv.x, rv.x, acc[1]);
-            acc[1] = fma(rv.y, rv.y, acc[1]);
-            *reinterpret_cast<double2 *>(a.r + i) = rv;
+    // BP aligned pairs per thread (n is even: even row pitch), all loads issued up front;
+    // a pair never straddles the owned range (planes hold an even number of slots)
+    constexpr int BP = 2;
+    const long long base = ((long long)blk * NT * BP + tid) * 2;
+    double2 xv[BP], dv[BP], rv[BP], qv[BP], iv[BP];
+    bool in[BP], own[BP];
+#pragma unroll
+    for (int k = 0; k < BP; k++) {
+        const long long i = base + (long long)k * NT * 2;
+        in[k] = i < a.n;
+        own[k] = in[k] && !replace && i >= a.own0 && i < a.own1;
+        if (in[k]) {
+            xv[k] = *reinterpret_cast<const double2 *>(xvec + i);
+            dv[k] = *reinterpret_cast<const double2 *>(dvec + i);
+        }
+        if (own[k]) {
+            rv[k] = *reinterpret_cast<const double2 *>(a.r + i);
+            qv[k] = __ldg(reinterpret_cast<const double2 *>(a.q + i));
+            iv[k] = __ldg(reinterpret_cast<const double2 *>(a.invd + i));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < BP; k++) {
+        const long long i = base + (long long)k * NT * 2;
+        if (in[k]) {
+            xv[k].x = fma(alpha, dv[k].x, xv[k].x);
+            xv[k].y = fma(alpha, dv[k].y, xv[k].y);
+            *reinterpret_cast<double2 *>(xvec + i) = xv[k];
+        }
+        if (own[k]) {
+            rv[k].x = fma(-alpha, qv[k].x, rv[k].x);
+            rv[k].y = fma(-alpha, qv[k].y, rv[k].y);
+            const double2 sv = make_double2(rv[k].x * iv[k].x, rv[k].y * iv[k].y);
+            acc[0] = fma(rv[k].x, sv.x, acc[0]);
+            acc[0] = fma(rv[k].y, sv.y, acc[0]);
+            acc[1] = fma(rv[k].x, rv[k].x, acc[1]);
+            acc[1] = fma(rv[k].y, rv[k].y, acc[1]);
+            *reinterpret_cast<double2 *>(a.r + i) = rv[k];
             *reinterpret_cast<double2 *>(a.s + i) = sv;
         }
     }

@@ -536,7 +536,7 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
     return HF_OK;
 }
 
-static int b_blocks(const hf_ctx *c) { return std::max(1, std::min((int)((c->nloc + 511) / 512), c->nsm * 4)); }
+static int b_blocks(const hf_ctx *c) { return std::max(1, (int)((c->nloc + 1023) / 1024)); }   // 256 thr x 2 pairs
 
 static hf_status run(hf_ctx *c, const Launch &L, cudaStream_t s)
 {
