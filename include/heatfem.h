@@ -81,6 +81,8 @@ typedef struct {
     int32_t max_iters_step; /* largest PCG iteration count of one step                         */
     int32_t first_failed_step; /* -1 if every step converged                                  */
     double ms_total;        /* device time of the call (CUDA events on the context stream)     */
+    double ms_steps;        /* sum of per-step device times (events around each step; excludes
+                               the L2 flushes of hf_set_step_flush); = ms_total if not enabled */
 } hf_sim_stats;
 
 typedef struct hf_ctx hf_ctx;
@@ -217,6 +219,11 @@ hf_status hf_set_driver(hf_ctx *ctx, int32_t driver);
 
 /* Enqueue a 512 MiB memset on the context stream (evicts the 126 MB L2; bench timing rule). */
 hf_status hf_flush_l2(hf_ctx *ctx);
+
+/* Benchmark mode of hf_simulate*: enable = 1 flushes L2 (as hf_flush_l2) before every time
+ * step and times every step alone with CUDA events (hf_sim_stats.ms_steps), all enqueued
+ * asynchronously; enable = 0 restores normal operation. */
+hf_status hf_set_step_flush(hf_ctx *ctx, int32_t enable);
 
 #ifdef __cplusplus
 }

@@ -46,7 +46,7 @@ class hf_cg_info(C.Structure):
 
 class hf_sim_stats(C.Structure):
     _fields_ = [("steps_done", C.c_int32), ("total_iters", C.c_int32), ("max_iters_step", C.c_int32),
-                ("first_failed_step", C.c_int32), ("ms_total", C.c_double)]
+                ("first_failed_step", C.c_int32), ("ms_total", C.c_double), ("ms_steps", C.c_double)]
 
 
 _lib = C.CDLL(_LIB_PATH)
@@ -80,6 +80,7 @@ _SIGS = {
     "hf_profile_read": (_i32, [_vp, _P(C.c_double * 5), _P(C.c_int64 * 5)]),
     "hf_set_driver": (_i32, [_vp, _i32]),
     "hf_flush_l2": (_i32, [_vp]),
+    "hf_set_step_flush": (_i32, [_vp, _i32]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -236,7 +237,7 @@ def hf_cg(ctx: Context, aK: float, aM: float, b, x, rtol=1e-12, max_iter=10000, 
 
 def _stats(s: hf_sim_stats) -> dict:
     return {"steps_done": s.steps_done, "total_iters": s.total_iters, "max_iters_step": s.max_iters_step,
-            "first_failed_step": s.first_failed_step, "ms_total": s.ms_total}
+            "first_failed_step": s.first_failed_step, "ms_total": s.ms_total, "ms_steps": s.ms_steps}
 
 
 def hf_simulate(ctx: Context, theta: float, dt: float, nsteps: int, F, u, snap_plane: int = -1, snap=None,
@@ -346,6 +347,10 @@ def hf_set_driver(ctx: Context, driver: int):
 
 def hf_flush_l2(ctx: Context):
     _check(_lib.hf_flush_l2(ctx.ptr))
+
+
+def hf_set_step_flush(ctx: Context, enable: bool):
+    _check(_lib.hf_set_step_flush(ctx.ptr, 1 if enable else 0))
 
 
 LIB_PATH = _LIB_PATH

@@ -201,6 +201,8 @@ struct hf_ctx {
     int occ = 2;                     // resident CTAs/SM of the CG stencil (occupancy API)
     int rank = 0, nranks = 1;
     Comm *comm = nullptr;
+    bool step_flush = false;
+    double last_ms_steps = 0.0;      // per-step event total of the last run (step_flush)
     bool prof = false;
     double prof_ms[5] = {0, 0, 0, 0, 0};
     long long prof_n[5] = {0, 0, 0, 0, 0};
@@ -1143,6 +1145,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     if (nsteps <= 0) return HF_OK;
 
     const bool use_graph = c->driver == 0 && c->nranks == 1 && !c->prof;
+    c->last_ms_steps = 0.0;
     SimKey key;
     std::memset(&key, 0, sizeof(key));
     key.aK = aK; key.aM = aM; key.aKL = aKL; key.aML = aML; key.rtol = o.rtol; key.dt = dt;
@@ -1205,7 +1208,30 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             s.key = key;
             s.key_valid = true;
         }
-        for (int n = 0; n < nsteps; n++) CUCK(cudaGraphLaunch(s.gexec, s.stream));
+        if (c->step_flush) {
+            // L2 eviction between steps, each step timed alone (no host synchronisation)
+            const size_t fb = 512ull << 20;
+            if (!c->flush) CUCK(cudaMalloc(&c->flush, fb));
+            std::vector<cudaEvent_t> ev(2 * (size_t)nsteps);
+            for (auto &e : ev) CUCK(cudaEventCreate(&e));
+            for (int n = 0; n < nsteps; n++) {
+                CUCK(cudaMemsetAsync(c->flush, n & 1, fb, s.stream));
+                CUCK(cudaEventRecord(ev[2 * n], s.stream));
+                CUCK(cudaGraphLaunch(s.gexec, s.stream));
+                CUCK(cudaEventRecord(ev[2 * n + 1], s.stream));
+            }
+            CUCK(cudaEventSynchronize(ev.back()));
+            double tot = 0.0;
+            for (int n = 0; n < nsteps; n++) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, ev[2 * n], ev[2 * n + 1]);
+                tot += ms;
+            }
+            for (auto &e : ev) cudaEventDestroy(e);
+            c->last_ms_steps = tot;
+        } else {
+            for (int n = 0; n < nsteps; n++) CUCK(cudaGraphLaunch(s.gexec, s.stream));
+        }
     } else {
         for (int n = 0; n < nsteps; n++) {
             for (auto &p : pre) HFCK(run(c, p, s.stream));
@@ -1234,6 +1260,7 @@ static hf_status finish_stats(hf_ctx *c, Sys &s, hf_sim_stats *stats, float ms)
         stats->max_iters_step = h.max_iters_step;
         stats->first_failed_step = h.first_failed;
         stats->ms_total = ms;
+        stats->ms_steps = c->step_flush ? c->last_ms_steps : ms;
     }
     if (h.first_failed >= 0) {
         if (h.status == ST_BREAKDOWN) return fail(HF_E_BREAKDOWN, "hf_simulate: PCG breakdown");
@@ -1371,6 +1398,7 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
             stats[j].max_iters_step = h.max_iters_step;
             stats[j].first_failed_step = h.first_failed;
             stats[j].ms_total = 0;
+            stats[j].ms_steps = 0;
         }
         if (h.first_failed >= 0 && first_err == HF_OK)
             first_err = h.status == ST_BREAKDOWN ? HF_E_BREAKDOWN : HF_E_NOCONV;
@@ -1619,6 +1647,13 @@ hf_status hf_set_driver(hf_ctx *c, int32_t driver)
 {
     if (!c || driver < 0 || driver > 1) return fail(HF_E_ARG, "hf_set_driver: bad argument");
     c->driver = driver;
+    return HF_OK;
+}
+
+hf_status hf_set_step_flush(hf_ctx *c, int32_t enable)
+{
+    if (!c) return fail(HF_E_ARG, "hf_set_step_flush: NULL");
+    c->step_flush = enable != 0;
     return HF_OK;
 }
 
