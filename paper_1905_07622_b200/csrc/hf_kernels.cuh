@@ -41,11 +41,22 @@ enum { ROT_NONE = 0, ROT_RHS = 1, ROT_INIT = 2, ROT_X = 3 };
 enum { MAP_U0 = 0, MAP_D0 = 3, MAP_S = 5 };
 
 // PCG state of one system (Alg. 1 scalars, device resident; the paper keeps them in device
-// buffers too: delta/alpha/beta kernels P:507-573).
+// buffers too: delta/alpha/beta kernels P:507-573).  Every field is written by block 0 of one
+// kernel and read only by LATER kernels (kernel boundaries order them), never by the kernel that
+// writes it: delta is double-buffered by iteration parity for that reason.
 struct CgState {
-    double delta, alpha, beta, rr, bb, thresh, dq, rtol2;
-    int iter, max_iter, replace_every;
-    int active, status, zero_x, replace;
+    double rtol2;           // options
+    int max_iter, replace_every;
+    double delta[2];        // delta_i = r_i^T s_i in slot i & 1          (written by A_i)
+    double thresh, bb, rr;  // rtol^2 ||b_F||^2, ||b_F||^2, last r^T r      (A)
+    double alpha, dq;       // last alpha, d^T q                          (B)
+    int a_iter;             // i of the running iteration                 (A)
+    int b_iter;             // completed iterations                       (init: 0, B: i + 1)
+    int active;             // 1 while iterating                          (init 1; A, B: 0 to stop)
+    int status, zero_x;     // ST_*, b_F == 0                             (A, B)
+    int replace;            // iteration a_iter replaces the residual     (B)
+    int iter;               // iterations of the finished solve           (A or B when stopping)
+    int npart_a, npart_b;   // partial-sum counts of the last A / (init, B, RESID)
     int step;               // time-step counter (step-end kernel)
     int first_failed;       // first failing step, -1 if none
     int total_iters, max_iters_step, steps_done;
@@ -70,10 +81,10 @@ struct Lam {
 
 struct Sync {               // per-system reduction plumbing
     CgState *st;
-    double *partials;       // gridDim * NPART
-    unsigned *ticket;
+    const double *pin;      // partial sums of the previous kernel (NPART per block)
+    int pin_n;              // their count; -1: taken from the state (npart_a / npart_b)
+    double *pout;           // this kernel's partial sums (NPART per block)
     unsigned long long *launches;
-    double *sums_out;       // non-null: write local sums here and let a finalize kernel run
     cudaGraphConditionalHandle h_while, h_if;
     int use_handles;
 };
@@ -191,29 +202,20 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NPART], double 
     }
 }
 
-// Returns true in exactly one block (the last to finish); that block's threads then hold the
-// grid-wide sums in `sums` (fixed summation order: independent of which block was last).
+// Grid-wide sums of the PREVIOUS kernel's per-block partials, computed redundantly by every
+// block in one fixed order (deterministic, no atomics, no fences: the kernel boundary orders
+// the producer's writes before these reads).  All threads return the same sums.
 template <int NT>
-__device__ __forceinline__ bool last_block_sums(const Sync &sy, int nblocks, double (&sums)[NPART])
+__device__ __forceinline__ void reduce_prev(const double *part, int n, double (&sums)[NPART])
 {
-    __shared__ bool am_last;
-    __shared__ double red[NT / 32][NPART];
+    __shared__ double redp[NT / 32][NPART];
     const int tid = threadIdx.x + threadIdx.y * blockDim.x;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-        unsigned t = atomicAdd(sy.ticket, 1u);
-        am_last = (t == (unsigned)nblocks - 1u);
-    }
-    __syncthreads();
-    if (!am_last) return false;
-    __threadfence();
     double acc[NPART];
 #pragma unroll
     for (int j = 0; j < NPART; j++) acc[j] = 0.0;
-    for (int b = tid; b < nblocks; b += NT) {
+    for (int b = tid; b < n; b += NT) {
 #pragma unroll
-        for (int j = 0; j < NPART; j++) acc[j] += __ldcg(sy.partials + (long long)b * NPART + j);
+        for (int j = 0; j < NPART; j++) acc[j] += __ldcg(part + (long long)b * NPART + j);
     }
     const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
@@ -221,20 +223,24 @@ __device__ __forceinline__ bool last_block_sums(const Sync &sy, int nblocks, dou
         double v = acc[j];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[wid][j] = v;
+        if (lane == 0) redp[wid][j] = v;
     }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < NPART; j++) {
         double v = 0.0;
-        for (int w = 0; w < NT / 32; w++) v += red[w][j];
+        for (int w = 0; w < NT / 32; w++) v += redp[w][j];
         sums[j] = v;
     }
-    if (tid == 0) *sy.ticket = 0u;
-    return true;
 }
 
-// ---- scalar updates of Alg. 1 (one thread) ---------------------------------------------
+template <int NT>
+__device__ __forceinline__ void prev_sums(const Sync &sy, int n_state, double (&sums)[NPART])
+{
+    reduce_prev<NT>(sy.pin, sy.pin_n >= 0 ? sy.pin_n : n_state, sums);
+}
+
+// ---- scalar logic of Alg. 1 ------------------------------------------------------------
 
 __device__ __forceinline__ void set_while(const Sync &sy, int v)
 {
@@ -245,56 +251,37 @@ __device__ __forceinline__ void set_if(const Sync &sy, int v)
     if (sy.use_handles) cudaGraphSetConditional(sy.h_if, (unsigned)v);
 }
 
-// init: r = b - A x0, delta = r^T P^{-1} r, rr = r^T r, bb = b_F^T b_F  (Alg. 1 lines 2-4)
-__device__ __forceinline__ void fin_init(const Sync &sy, const double *s)
-{
-    CgState *st = sy.st;
-    st->delta = s[0]; st->rr = s[1]; st->bb = s[2];
-    st->thresh = st->rtol2 * s[2];
-    st->iter = 0; st->beta = 0.0; st->replace = 0; st->status = ST_OK;
-    if (!isfinite(s[0]) || !isfinite(s[1]) || !isfinite(s[2])) {   // NaN/Inf input
-        st->zero_x = 0; st->active = 0; st->status = ST_BREAKDOWN;
-    } else if (s[2] == 0.0) {        // b_F = 0 -> x_F = 0, 0 iterations
-        st->zero_x = 1; st->active = 0;
-    } else {
-        st->zero_x = 0;
-        const bool need = s[1] > st->thresh;     // R4: ||r|| > tol ||b||
-        st->active = need && st->max_iter > 0;
-        if (need && st->max_iter <= 0) st->status = ST_NOCONV;
-    }
-    set_while(sy, st->active);
-}
+// Start of iteration i (kernel A), from the sums of the init / B / RESID kernel before it:
+// i = 0: delta_0 = r^T s, ||r||^2, ||b_F||^2 (Alg. 1 lines 2-4, reading R4);
+// i > 0: delta_i, beta_i = delta_i / delta_{i-1} (lines 16-17, reading R5), stop test.
+struct IterStart {
+    bool go;
+    double beta, delta, rr, thresh, bb;
+    int status, zero_x;
+};
 
-// after q = A d: alpha = delta / (d^T q)  (Alg. 1 line 8); breakdown if d^T q <= 0
-__device__ __forceinline__ void fin_cga(const Sync &sy, const double *s)
+__device__ __forceinline__ IterStart iter_start(const CgState *st, int i, const double *s)
 {
-    CgState *st = sy.st;
-    const double dq = s[0];
-    st->dq = dq;
-    if (!(dq > 0.0) || !isfinite(dq) || !isfinite(st->delta)) {
-        st->status = ST_BREAKDOWN; st->active = 0;
+    IterStart r;
+    r.delta = s[0];
+    r.rr = s[1];
+    r.status = ST_OK;
+    r.zero_x = 0;
+    r.beta = 0.0;
+    if (i == 0) {
+        r.bb = s[2];
+        r.thresh = st->rtol2 * s[2];
     } else {
-        st->alpha = st->delta / dq;
+        r.bb = st->bb;
+        r.thresh = st->thresh;
+        r.beta = s[0] / st->delta[(i - 1) & 1];
     }
-}
-
-// after the residual update: delta_old <- delta, delta = r^T s, beta = delta/delta_old,
-// i <- i + 1, stop test (Alg. 1 lines 16-19, readings R4, R5)
-__device__ __forceinline__ void fin_iter(const Sync &sy, const double *s)
-{
-    CgState *st = sy.st;
-    const double delta_old = st->delta;
-    st->delta = s[0];
-    st->rr = s[1];
-    st->beta = s[0] / delta_old;
-    st->iter += 1;
-    const bool need = s[1] > st->thresh;
-    if (!isfinite(s[1])) { st->status = ST_BREAKDOWN; st->active = 0; }
-    else {
-        st->active = need && st->iter < st->max_iter;
-        if (need && st->iter >= st->max_iter) st->status = ST_NOCONV;
-    }
-    set_while(sy, st->active);
+    if (!isfinite(s[0]) || !isfinite(s[1]) || !isfinite(r.bb)) { r.status = ST_BREAKDOWN; r.go = false; return r; }
+    if (i == 0 && r.bb == 0.0) { r.zero_x = 1; r.go = false; return r; }   // b_F = 0 -> x_F = 0
+    const bool need = r.rr > r.thresh;                                      // R4: ||r|| > tol ||b||
+    r.go = need && i < st->max_iter;
+    if (need && i >= st->max_iter) r.status = ST_NOCONV;
+    return r;
 }
 
 // ---- the stencil kernel (operator apply with fused prologue/epilogue) ---------------------
@@ -338,6 +325,7 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
     // ---- state checks and per-launch resolution of buffers ---------------------------------
     double beta = 0.0;
     int map0 = MAP_U0, map1 = MAP_U0 + 2, first = a.first;
+    int it_i = 0;                                            // PCG iteration (kernel A)
     double *cstore = (EP == EP_CGA) ? a.dbuf[1] : a.xout;    // centre-value store target
     if (a.sy.st) {
         const CgState *st = a.sy.st;
@@ -347,9 +335,9 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
             if (EP == EP_RESID && !st->replace) return;
         }
         if (LD == LD_CGD) {
-            // d_new = s + beta d_old;  d_old = dbuf[i & 1], d_new = dbuf[(i & 1) ^ 1]
-            beta = st->beta;
-            const int par = st->iter & 1;
+            // d_i = s_i + beta_i d_{i-1};  d_{i-1} = dbuf[i & 1], d_i = dbuf[(i & 1) ^ 1]
+            it_i = st->b_iter;
+            const int par = it_i & 1;
             map0 = MAP_S;
             map1 = MAP_D0 + par;
             cstore = a.dbuf[par ^ 1];
@@ -410,6 +398,37 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
     __syncthreads();
     if (tid == 0)
         for (int i = 0; i < NS && i < nplanes; i++) issue(i);
+
+    if (EP == EP_CGA) {
+        // start of PCG iteration i from the previous kernel's partial sums (overlaps the TMA)
+        double ps[NPART];
+        prev_sums<NT>(a.sy, a.sy.st->npart_b, ps);
+        const IterStart is = iter_start(a.sy.st, it_i, ps);
+        if (!is.go) {
+            if (blk == 0 && tid == 0) {
+                CgState *stw = a.sy.st;
+                stw->active = 0;
+                stw->status = is.status;
+                stw->zero_x = is.zero_x;
+                stw->iter = it_i;
+                stw->rr = is.rr;
+                if (it_i == 0) { stw->bb = is.bb; stw->thresh = is.thresh; }
+                stw->delta[it_i & 1] = is.delta;
+                set_while(a.sy, 0);
+                set_if(a.sy, 0);
+            }
+            for (int i = 0; i < NS && i < nplanes; i++) mbar_wait(&bars[i], 0);   // drain the TMA
+            return;
+        }
+        beta = is.beta;
+        if (blk == 0 && tid == 0) {
+            CgState *stw = a.sy.st;
+            stw->delta[it_i & 1] = is.delta;
+            stw->a_iter = it_i;
+            stw->rr = is.rr;
+            if (it_i == 0) { stw->bb = is.bb; stw->thresh = is.thresh; }
+        }
+    }
 
     double Fp[R][4];          // face transforms of the lower plane p-1
     double Cy[R][4];          // face-space contributions carried from the layer below
@@ -550,17 +569,21 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
     }
 
     if (EP == EP_APPLY) return;
-    block_reduce_store<NT>(acc, a.sy.partials, blk);
-    double sums[NPART];
-    if (!last_block_sums<NT>(a.sy, nblocks, sums)) return;
-    if (tid != 0) return;
-    if (a.sy.sums_out) {
-        for (int j = 0; j < NPART; j++) a.sy.sums_out[j] = sums[j];
-        return;
+    // per-block partial sums for the next kernel: A -> (d^T q); init, RESID -> (r^T s, r^T r, b^T b)
+    block_reduce_store<NT>(acc, a.sy.pout, blk);
+    if (blk == 0 && tid == 0) {
+        CgState *stw = a.sy.st;
+        if (EP == EP_CGA) stw->npart_a = nblocks;
+        else stw->npart_b = nblocks;
+        if (EP == EP_RESID_INIT) {              // a new solve starts: A_0 follows
+            stw->b_iter = 0;
+            stw->active = 1;
+            stw->status = ST_OK;
+            stw->zero_x = 0;
+            stw->replace = 0;
+            stw->iter = 0;
+        }
     }
-    if (EP == EP_CGA) fin_cga(a.sy, sums);
-    else if (EP == EP_RESID_INIT) fin_init(a.sy, sums);
-    else fin_iter(a.sy, sums);
 }
 
 // ---- PCG kernel B: x += alpha d; r -= alpha q; s = P^{-1} r; r^T s, r^T r ---------------
@@ -587,82 +610,94 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     const int blk = blockIdx.x;
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
     CgState *st = a.sy.st;
+    if (st->first_failed >= 0) return;
     if (!st->active) {
         if (blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
         return;
     }
-    const int it = st->iter, re = st->replace_every;
-    const bool replace = it > 0 && re > 0 && (it % re) == 0;
-    const double alpha = st->alpha;
+    const int it = st->a_iter, re = st->replace_every;
+    // alpha_i = delta_i / (d_i^T q_i)  (Alg. 1 line 8) from kernel A's partials
+    double ps[NPART];
+    prev_sums<NT>(a.sy, st->npart_a, ps);
+    const double dq = ps[0], delta = st->delta[it & 1];
+    if (!(dq > 0.0) || !isfinite(dq) || !isfinite(delta)) {           // breakdown
+        if (blk == 0 && tid == 0) {
+            st->status = ST_BREAKDOWN;
+            st->active = 0;
+            st->iter = it;
+            set_while(a.sy, 0);
+            set_if(a.sy, 0);
+        }
+        return;
+    }
+    const double alpha = delta / dq;
+    const bool replace = it > 0 && re > 0 && (it % re) == 0;           // Alg. 1 line 10 (R6)
     const double *dvec = a.dbuf[(it & 1) ^ 1];
     double *xvec = a.rot[0] ? a.rot[(st->step + 1) % 3] : a.x;
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
-    // BP aligned pairs per thread (n is even: even row pitch), all loads issued up front;
+    // BP aligned pairs per thread per sweep (n is even: even row pitch), loads issued up front;
     // a pair never straddles the owned range (planes hold an even number of slots)
     constexpr int BP = 2;
-    const long long base = ((long long)blk * NT * BP + tid) * 2;
-    double2 xv[BP], dv[BP], rv[BP], qv[BP], iv[BP];
-    bool in[BP], own[BP];
+    const long long sweep = (long long)gridDim.x * NT * BP * 2;
+    for (long long base = ((long long)blk * NT * BP + tid) * 2; base < a.n; base += sweep) {
+        double2 xv[BP], dv[BP], rv[BP], qv[BP], iv[BP];
+        bool in[BP], own[BP];
 #pragma unroll
-    for (int k = 0; k < BP; k++) {
-        const long long i = base + (long long)k * NT * 2;
-        in[k] = i < a.n;
-        own[k] = in[k] && !replace && i >= a.own0 && i < a.own1;
-        if (in[k]) {
-            xv[k] = *reinterpret_cast<const double2 *>(xvec + i);
-            dv[k] = *reinterpret_cast<const double2 *>(dvec + i);
+        for (int k = 0; k < BP; k++) {
+            const long long i = base + (long long)k * NT * 2;
+            in[k] = i < a.n;
+            own[k] = in[k] && !replace && i >= a.own0 && i < a.own1;
+            if (in[k]) {
+                xv[k] = *reinterpret_cast<const double2 *>(xvec + i);
+                dv[k] = *reinterpret_cast<const double2 *>(dvec + i);
+            }
+            if (own[k]) {
+                rv[k] = *reinterpret_cast<const double2 *>(a.r + i);
+                qv[k] = __ldg(reinterpret_cast<const double2 *>(a.q + i));
+                iv[k] = __ldg(reinterpret_cast<const double2 *>(a.invd + i));
+            }
         }
-        if (own[k]) {
-            rv[k] = *reinterpret_cast<const double2 *>(a.r + i);
-            qv[k] = __ldg(reinterpret_cast<const double2 *>(a.q + i));
-            iv[k] = __ldg(reinterpret_cast<const double2 *>(a.invd + i));
-        }
-    }
 #pragma unroll
-    for (int k = 0; k < BP; k++) {
-        const long long i = base + (long long)k * NT * 2;
-        if (in[k]) {
-            xv[k].x = fma(alpha, dv[k].x, xv[k].x);
-            xv[k].y = fma(alpha, dv[k].y, xv[k].y);
-            *reinterpret_cast<double2 *>(xvec + i) = xv[k];
-        }
-        if (own[k]) {
-            rv[k].x = fma(-alpha, qv[k].x, rv[k].x);
-            rv[k].y = fma(-alpha, qv[k].y, rv[k].y);
-            const double2 sv = make_double2(rv[k].x * iv[k].x, rv[k].y * iv[k].y);
-            acc[0] = fma(rv[k].x, sv.x, acc[0]);
-            acc[0] = fma(rv[k].y, sv.y, acc[0]);
-            acc[1] = fma(rv[k].x, rv[k].x, acc[1]);
-            acc[1] = fma(rv[k].y, rv[k].y, acc[1]);
-            *reinterpret_cast<double2 *>(a.r + i) = rv[k];
-            *reinterpret_cast<double2 *>(a.s + i) = sv;
+        for (int k = 0; k < BP; k++) {
+            const long long i = base + (long long)k * NT * 2;
+            if (in[k]) {                        // x += alpha d  (line 9)
+                xv[k].x = fma(alpha, dv[k].x, xv[k].x);
+                xv[k].y = fma(alpha, dv[k].y, xv[k].y);
+                *reinterpret_cast<double2 *>(xvec + i) = xv[k];
+            }
+            if (own[k]) {                       // r -= alpha q; s = P^{-1} r (lines 13, 15)
+                rv[k].x = fma(-alpha, qv[k].x, rv[k].x);
+                rv[k].y = fma(-alpha, qv[k].y, rv[k].y);
+                const double2 sv = make_double2(rv[k].x * iv[k].x, rv[k].y * iv[k].y);
+                acc[0] = fma(rv[k].x, sv.x, acc[0]);
+                acc[0] = fma(rv[k].y, sv.y, acc[0]);
+                acc[1] = fma(rv[k].x, rv[k].x, acc[1]);
+                acc[1] = fma(rv[k].y, rv[k].y, acc[1]);
+                *reinterpret_cast<double2 *>(a.r + i) = rv[k];
+                *reinterpret_cast<double2 *>(a.s + i) = sv;
+            }
         }
     }
-    if (replace) {
-        if (blk == 0 && tid == 0) { st->replace = 1; set_if(a.sy, 1); }
-        return;
+    if (!replace) block_reduce_store<NT>(acc, a.sy.pout, blk);
+    if (blk == 0 && tid == 0) {
+        st->b_iter = it + 1;
+        st->replace = replace;
+        st->alpha = alpha;
+        st->dq = dq;
+        if (!replace) st->npart_b = gridDim.x;
+        set_if(a.sy, replace ? 1 : 0);
     }
-    block_reduce_store<NT>(acc, a.sy.partials, blk);
-    double sums[NPART];
-    if (!last_block_sums<NT>(a.sy, gridDim.x, sums)) return;
-    if (tid != 0) return;
-    st->replace = 0;
-    set_if(a.sy, 0);
-    if (a.sy.sums_out) { for (int j = 0; j < NPART; j++) a.sy.sums_out[j] = sums[j]; return; }
-    fin_iter(a.sy, sums);
 }
 
-// Finalisation after a cross-rank allreduce of the local sums (slab mode).
-__global__ void k_finalize(Sync sy, int mode)
+// Local sums of the last producer's partials (slab mode: before the cross-rank allreduce).
+// which = 0: kernel A's partials, 1: init / B / RESID partials.
+__global__ void __launch_bounds__(256) k_localsum(Sync sy, int which, double *sums)
 {
-    if (sy.launches) atomicAdd(sy.launches, 1ull);
-    CgState *st = sy.st;
-    const double *s = sy.sums_out;
-    if (mode == EP_RESID_INIT) { if (st->first_failed < 0) fin_init(sy, s); }
-    else if (!st->active) return;
-    else if (mode == EP_CGA) fin_cga(sy, s);
-    else if (mode == EP_RESID) { if (st->replace) fin_iter(sy, s); }
-    else fin_iter(sy, s);   // kernel B
+    if (threadIdx.x == 0 && sy.launches) atomicAdd(sy.launches, 1ull);
+    const CgState *st = sy.st;
+    double s[NPART];
+    reduce_prev<256>(sy.pin, which == 0 ? st->npart_a : st->npart_b, s);
+    if (threadIdx.x < NPART) sums[threadIdx.x] = s[threadIdx.x];
 }
 
 // ---- element coefficient access (compact (nx, ny, nzl + 1) layout, layer L at index L + 1) --
@@ -809,7 +844,7 @@ __global__ void __launch_bounds__(256) k_step_end(const StepArgs a)
 {
     const int tid = threadIdx.x, blk = blockIdx.x;
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
-    CgState *st = a.sy.st;
+    const CgState *st = a.sy.st;
     if (st->first_failed >= 0) return;
     const int step = st->step;
     double *xv = a.rot[0] ? a.rot[(step + 1) % 3] : a.x;
@@ -834,14 +869,16 @@ __global__ void __launch_bounds__(256) k_step_end(const StepArgs a)
             dst[i] = v;
         }
     }
-    __shared__ bool am_last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) am_last = atomicAdd(a.sy.ticket, 1u) == gridDim.x - 1u;
-    __syncthreads();
-    if (!am_last || tid != 0) return;
-    *a.sy.ticket = 0u;
-    if (a.iters_out) a.iters_out[step] = st->iter;
+}
+
+// Per-step bookkeeping after k_step_end (one thread): iteration statistics, failure, step++.
+__global__ void k_step_commit(Sync sy, int *iters_out)
+{
+    if (sy.launches) atomicAdd(sy.launches, 1ull);
+    CgState *st = sy.st;
+    if (st->first_failed >= 0) return;
+    const int step = st->step;
+    if (iters_out) iters_out[step] = st->iter;
     st->total_iters += st->iter;
     if (st->iter > st->max_iters_step) st->max_iters_step = st->iter;
     st->steps_done = step + 1;

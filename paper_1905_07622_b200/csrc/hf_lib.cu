@@ -150,8 +150,9 @@ struct Sys {                         // one system's PCG workspace (Table 3 buff
     Maps maps;                       // TMA maps of U[0..2], dbuf[0..1], s and kc
     CgState *st = nullptr;           // device
     CgState *st_host = nullptr;      // pinned mirror
-    double *partials = nullptr, *sums = nullptr;
-    unsigned *ticket = nullptr;
+    double *partA = nullptr, *partB = nullptr;   // per-block partial sums of A / (init, B, RESID)
+    double *sums = nullptr;                      // slab mode: allreduced sums
+
     int *iters = nullptr;
     int iters_cap = 0;
     cudaStream_t stream = nullptr;   // == ctx stream for the primary system
@@ -475,15 +476,20 @@ static void stencil_grid(const hf_ctx *c, int z0, int z1, dim3 *grid, int *zchun
     *zchunk = chunk;
 }
 
-static Sync make_sync(hf_ctx *c, Sys &s)
+// which = 0: consumes kernel A's partials, 1: consumes init/B/RESID partials, -1: none.
+// pout = 0: writes A partials, 1: writes init/B/RESID partials, -1: none.  In slab mode the
+// consumer reads the allreduced sums instead (count 1).
+static Sync make_sync(hf_ctx *c, Sys &s, int consumes = -1, int produces = -1)
 {
     Sync y;
     std::memset(&y, 0, sizeof(y));
     y.st = s.st;
-    y.partials = s.partials;
-    y.ticket = s.ticket;
     y.launches = c->launches;
-    y.sums_out = (c->nranks > 1) ? s.sums : nullptr;
+    if (consumes >= 0) {
+        if (c->nranks > 1) { y.pin = s.sums; y.pin_n = 1; }
+        else { y.pin = consumes == 0 ? s.partA : s.partB; y.pin_n = -1; }
+    }
+    if (produces >= 0) y.pout = produces == 0 ? s.partA : s.partB;
     return y;
 }
 
@@ -538,7 +544,7 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
     return HF_OK;
 }
 
-static int b_blocks(const hf_ctx *c) { return std::max(1, (int)((c->nloc + 1023) / 1024)); }   // 256 thr x 2 pairs
+static int b_blocks(const hf_ctx *c) { return std::max(1, std::min((int)((c->nloc + 1023) / 1024), c->nsm * 4)); }
 
 static hf_status run(hf_ctx *c, const Launch &L, cudaStream_t s)
 {
@@ -603,10 +609,9 @@ static hf_status sys_alloc(hf_ctx *c, Sys &s, cudaStream_t stream)
     CUCK(cudaMemsetAsync(s.kc, 0, (size_t)c->kc_elems * sizeof(double2), stream));
     CUCK(cudaMalloc(&s.st, sizeof(CgState)));
     CUCK(cudaMallocHost(&s.st_host, sizeof(CgState)));
-    CUCK(cudaMalloc(&s.partials, (size_t)c->max_blocks * NPART * sizeof(double)));
+    CUCK(cudaMalloc(&s.partA, (size_t)c->max_blocks * NPART * sizeof(double)));
+    CUCK(cudaMalloc(&s.partB, (size_t)c->max_blocks * NPART * sizeof(double)));
     CUCK(cudaMalloc(&s.sums, NPART * sizeof(double)));
-    CUCK(cudaMalloc(&s.ticket, sizeof(unsigned)));
-    CUCK(cudaMemsetAsync(s.ticket, 0, sizeof(unsigned), stream));
     std::memset(s.st_host, 0, sizeof(CgState));
     s.st_host->first_failed = -1;
     CUCK(cudaMemcpyAsync(s.st, s.st_host, sizeof(CgState), cudaMemcpyHostToDevice, stream));
@@ -622,7 +627,7 @@ static void sys_free(Sys &s)
     cudaFree(s.b); cudaFree(s.r); cudaFree(s.s); cudaFree(s.q); cudaFree(s.invd);
     cudaFree(s.dbuf[0]); cudaFree(s.dbuf[1]);
     cudaFree(s.st); cudaFreeHost(s.st_host);
-    cudaFree(s.partials); cudaFree(s.sums); cudaFree(s.ticket); cudaFree(s.iters);
+    cudaFree(s.partA); cudaFree(s.partB); cudaFree(s.sums); cudaFree(s.iters);
     cudaFree(s.kc);
     if (s.gexec) cudaGraphExecDestroy(s.gexec);
     if (s.graph) cudaGraphDestroy(s.graph);
@@ -738,7 +743,6 @@ struct CgLaunches {
 // x: the iterate (NULL: the time-step ring slot U[(step+1)%3]); xmaps: maps with node[0] = x
 static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x, const Maps &xmaps, CgLaunches *L)
 {
-    Sync sy = make_sync(c, s);
     const bool rot = x == nullptr;
     // kernel A: d = s + beta d; q = A d; d^T q -> alpha   (Alg. 1 lines 7-8, 15, 18)
     StencilArgs a = base_args(c, aK, aM);
@@ -748,7 +752,7 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
     a.zs0 = c->own_lo - (c->own_lo > 0 ? 1 : 0);   // store d on ghost planes too (slab)
     a.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
     a.dmode = 1;
-    a.sy = sy;
+    a.sy = make_sync(c, s, 1, 0);
     HFCK(stencil_launch(c, LD_CGD, EP_CGA, false, s.maps, a, 0, &L->A));
     // kernel B: x += alpha d; r -= alpha q; s = P^{-1} r; r^T s, r^T r -> beta   (lines 9-19)
     BArgs b;
@@ -764,7 +768,7 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
     b.own0 = (long long)c->own_lo * c->plane;
     b.own1 = (long long)c->own_hi * c->plane;
     if (rot) for (int i = 0; i < 3; i++) b.rot[i] = s.U[i];
-    b.sy = sy;
+    b.sy = make_sync(c, s, 0, 1);
     L->B = Launch();
     L->B.fn = (const void *)k_cg_b<256>;
     L->B.grid = dim3(b_blocks(c));
@@ -777,23 +781,22 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
     rr.bvec = s.b;
     rr.out0 = s.r;
     rr.out_s = s.s;
-    rr.sy = sy;
+    rr.sy = make_sync(c, s, -1, 1);
     if (rot) rr.rot_role = ROT_X;
     HFCK(stencil_launch(c, LD_RAW, EP_RESID, true, rot ? s.maps : xmaps, rr, 2, &L->RES));
     return HF_OK;
 }
 
-static hf_status comm_after(hf_ctx *c, Sys &s, int mode, bool exch)
+// slab mode, after a producer kernel: local sums -> allreduce -> (ghosts of s for the next apply)
+static hf_status comm_after(hf_ctx *c, Sys &s, int which, bool exch)
 {
     if (c->nranks <= 1) return HF_OK;
-    HFCK(c->comm->allreduce(c, s, s.sums, NPART));
     Sync sy = make_sync(c, s);
-    k_finalize<<<1, 1, 0, s.stream>>>(sy, mode);
+    sy.pin = which == 0 ? s.partA : s.partB;
+    k_localsum<<<1, 256, 0, s.stream>>>(sy, which, s.sums);
     CUCK(cudaGetLastError());
-    if (exch) {   // residual ghosts (r and s) for the next apply
-        HFCK(c->comm->exchange(c, s, s.r));
-        HFCK(c->comm->exchange(c, s, s.s));
-    }
+    HFCK(c->comm->allreduce(c, s, s.sums, NPART));
+    if (exch) HFCK(c->comm->exchange(c, s, s.s));
     return HF_OK;
 }
 
@@ -834,15 +837,28 @@ static StepArgs step_args(hf_ctx *c, Sys &s, double *x, double *snapdev, int sna
     return a;
 }
 
-static Launch step_launch(hf_ctx *c, const StepArgs &a)
+// end of a solve / time step: k_step_end (x_F = 0 if b_F = 0, snapshot) + k_step_commit
+static std::vector<Launch> step_launches(hf_ctx *c, const StepArgs &a, bool commit)
 {
+    std::vector<Launch> v;
     Launch L;
     L.fn = (const void *)k_step_end;
     L.grid = dim3(std::max(1, std::min(c->nsm, (int)((c->nloc + 255) / 256))));
     L.block = dim3(256);
     L.add(a);
     L.cls = 4;
-    return L;
+    v.push_back(L);
+    if (commit) {
+        Launch C;
+        C.fn = (const void *)k_step_commit;
+        C.grid = dim3(1);
+        C.block = dim3(1);
+        C.add(a.sy);
+        C.add(a.iters_out);
+        C.cls = 4;
+        v.push_back(C);
+    }
+    return v;
 }
 
 // ---- host-loop PCG (profiling, slab transports) ------------------------------------------
@@ -854,13 +870,13 @@ static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, in
     const int check = slab && !c->comm->graph_capturable() ? 1 : c->check_every;
     for (int i = 0;;) {
         HFCK(run(c, L.A, s.stream));
-        HFCK(comm_after(c, s, EP_CGA, false));
+        HFCK(comm_after(c, s, 0, false));
         const bool rep = i > 0 && replace_every > 0 && i % replace_every == 0;
         HFCK(run(c, L.B, s.stream));
-        if (!rep) HFCK(comm_after(c, s, 100, true));
+        if (!rep) HFCK(comm_after(c, s, 1, true));
         if (rep) {
             HFCK(run(c, L.RES, s.stream));
-            HFCK(comm_after(c, s, EP_RESID, true));
+            HFCK(comm_after(c, s, 1, true));
         }
         i++;
         if (i % check == 0 || i >= max_iter) {
@@ -881,15 +897,11 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
     cudaGraph_t g;
     CUCK(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle hw, hi;
-    CUCK(cudaGraphConditionalHandleCreate(&hw, g, 0, cudaGraphCondAssignDefault));
+    CUCK(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
     cudaGraphNode_t prev = nullptr, n;
     for (auto &p : pre) { HFCK(add_node(g, p, prev ? &prev : nullptr, &n)); prev = n; }
-    {   // the init kernel sets the WHILE handle
-        StencilArgs ia = init.get<StencilArgs>(1);
-        ia.sy.h_while = hw;
-        ia.sy.use_handles = 1;
-        init.put(1, ia);
-    }
+    // the loop is entered once at least; kernel A of the iteration after the last decides to
+    // stop (it clears the WHILE handle), kernel B sets the IF handle of the replacement
     HFCK(add_node(g, init, prev ? &prev : nullptr, &n));
     prev = n;
     cudaGraphNodeParams cp = {};
@@ -1080,18 +1092,18 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     ia.out0 = s.r;
     ia.out_s = s.s;
     ia.xout = dx;
-    ia.sy = make_sync(c, s);
+    ia.sy = make_sync(c, s, -1, 1);
     Launch init;
     HFCK(stencil_launch(c, LD_RAW, EP_RESID_INIT, true, xm, ia, 2, &init));
     CgLaunches L;
     HFCK(cg_launches(c, s, aK, aM, dx, xm, &L));
     StepArgs sa = step_args(c, s, dx, nullptr, -1);
     sa.iters_out = nullptr;
-    Launch post = step_launch(c, sa);
+    std::vector<Launch> post = step_launches(c, sa, false);
     const bool use_graph = c->driver == 0 && c->nranks == 1 && !c->prof;
     if (use_graph) {
         cudaGraph_t g;
-        HFCK(build_cg_graph(c, {}, init, L, {post}, &g));
+        HFCK(build_cg_graph(c, {}, init, L, post, &g));
         cudaGraphExec_t ge;
         cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
         if (e != cudaSuccess) { cudaGraphDestroy(g); CUCK(e); }
@@ -1102,9 +1114,9 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
         CUCK(e);
     } else {
         HFCK(run(c, init, s.stream));
-        HFCK(comm_after(c, s, EP_RESID_INIT, true));
+        HFCK(comm_after(c, s, 1, true));
         HFCK(host_cg_loop(c, s, L, o.max_iter, o.replace_every));
-        HFCK(run(c, post, s.stream));
+        for (auto &p : post) HFCK(run(c, p, s.stream));
     }
     HFCK(read_state(c, s));
     if (x != dx) HFCK(node_out_finish(c, x, dx));
@@ -1113,7 +1125,7 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
         info->iters = h.iter;
         info->status = h.status;
         info->relres = h.bb > 0 ? std::sqrt(h.rr / h.bb) : 0.0;
-        info->delta = h.delta;
+        info->delta = h.delta[h.iter & 1];
     }
     if (h.status == ST_NOCONV) return fail(HF_E_NOCONV, "hf_cg: max_iter reached");
     if (h.status == ST_BREAKDOWN) return fail(HF_E_BREAKDOWN, "hf_cg: breakdown (d^T q <= 0 or non-finite)");
@@ -1153,8 +1165,8 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     key.snap_plane = snap_local; key.lift = lift; key.F = dF; key.snap = snapdev;
     const bool cached = use_graph && s.key_valid && s.key == key && s.gexec;
 
-    std::vector<Launch> pre;
-    Launch init, post;
+    std::vector<Launch> pre, post;
+    Launch init;
     CgLaunches L;
     if (!cached) {
         Sync sy = make_sync(c, s);
@@ -1190,12 +1202,12 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
         ia.first = first ? 1 : 0;
         ia.rot_role = ROT_INIT;
         for (int i = 0; i < 3; i++) ia.ring[i] = s.U[i];
-        ia.sy = sy;
+        ia.sy = make_sync(c, s, -1, 1);
         ia.zs0 = c->own_lo - (c->own_lo > 0 ? 1 : 0);
         ia.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
         HFCK(stencil_launch(c, LD_X0, EP_RESID_INIT, true, s.maps, ia, 2, &init));
         HFCK(cg_launches(c, s, aK, aM, nullptr, s.maps, &L));
-        post = step_launch(c, step_args(c, s, nullptr, snapdev, snap_local));
+        post = step_launches(c, step_args(c, s, nullptr, snapdev, snap_local), true);
     }
 
     if (use_graph) {
@@ -1203,7 +1215,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             if (s.gexec) { cudaGraphExecDestroy(s.gexec); s.gexec = nullptr; }
             if (s.graph) { cudaGraphDestroy(s.graph); s.graph = nullptr; }
             s.key_valid = false;
-            HFCK(build_cg_graph(c, pre, init, L, {post}, &s.graph));
+            HFCK(build_cg_graph(c, pre, init, L, post, &s.graph));
             CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
             s.key = key;
             s.key_valid = true;
@@ -1236,9 +1248,9 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
         for (int n = 0; n < nsteps; n++) {
             for (auto &p : pre) HFCK(run(c, p, s.stream));
             HFCK(run(c, init, s.stream));
-            HFCK(comm_after(c, s, EP_RESID_INIT, true));
+            HFCK(comm_after(c, s, 1, true));
             HFCK(host_cg_loop(c, s, L, o.max_iter, o.replace_every));
-            HFCK(run(c, post, s.stream));
+            for (auto &p : post) HFCK(run(c, p, s.stream));
             if (c->nranks > 1) {
                 // the next RHS reads u^{n+1} ghosts: kernel B keeps the iterate's ghost planes
                 // consistent (x update on every local plane)
