@@ -267,6 +267,7 @@ def run_ours(args):
         }
     if world == 1:
         line["apply_512"] = apply_512(hf, torch, dev, peak)
+        line["c5_batched"] = c5_batched(hf, torch, dev, world)
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(args)
     return line
@@ -302,6 +303,38 @@ def apply_512(hf, torch, dev, peak):
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "ms": ms,
             "bytes_per_launch": byts, "traffic": ncu_traffic("stencil_apply_512"),
             "kernel": "k_stencil<LD_RAW,EP_APPLY> (y = (aK K + aM M) u), 512^3 nodes, median of 10"}
+
+
+def c5_batched(hf, torch, dev, world, nsims=2, nsteps=300):
+    """C5 (BASELINE configs[4]): corrosion-inverse forward simulations, 99^3 voxels each
+    (1M DoF), T_F = 10 s in 300 CN steps, Gaussian beam 10 W sigma 2 mm, per-sim depth and
+    log-normal k perturbation; nsims of them through hf_simulate_batched on this GPU."""
+    probs = [synth.c5(j, nsteps=nsteps) for j in range(nsims)]
+    g = probs[0].grid
+    kb = torch.tensor(np.stack([p.k for p in probs]).ravel(), device=dev)
+    cb = torch.tensor(np.stack([p.c for p in probs]).ravel(), device=dev)
+    ctx = hf.hf_create(g, dev.index)
+    hf.hf_set_coefficients(ctx, kb[:g.n_elems], cb[:g.n_elems])
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=dev)
+    p0 = probs[0]
+    hf.hf_face_load(ctx, p0.flux_face, p0.flux_const, p0.beam, F)
+    ub = torch.zeros(nsims * g.n_nodes, dtype=torch.float64, device=dev)
+    front = torch.empty(nsims * (g.ne[0] + 1) * (g.ne[1] + 1), dtype=torch.float64, device=dev)
+    hf.hf_simulate_batched(ctx, 1, kb[:g.n_elems], cb[:g.n_elems], p0.theta, p0.dt, 2, F, ub[:g.n_nodes])  # warm
+    ub.zero_()
+    s = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    stats = hf.hf_simulate_batched(ctx, nsims, kb, cb, p0.theta, p0.dt, nsteps, F, ub, 0, front, rtol=p0.rtol)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    its = sum(st["total_iters"] for st in stats)
+    del ctx
+    return {"sims": nsims, "steps_per_sim": nsteps, "seconds": sec, "sims_per_s_per_gpu": nsims / sec,
+            "ms_per_step": sec * 1e3 / (nsims * nsteps), "pcg_iters_per_step": its / (nsims * nsteps),
+            "projected_1000_sims_8_gpus_s": 1000 / (8 * nsims / sec),
+            "depths_mm": [round(p.extra["depth"], 3) for p in probs],
+            "front_face_max_C": float(front.max().item())}
 
 
 # ---------------------------------------------------------------------------------------------

@@ -417,3 +417,28 @@ def test_c4_apply_sampled_rows():
     rows = np.concatenate([rows, np.array(extra)])
     yo = o.apply_rows(0.005, 1.0, u, rows)
     assert maxerr(yg[rows], yo) <= 1e-12
+
+
+def test_c5_corrosion_batched_small():
+    """C5 recipe (corrosion plate, anisotropic voxels, Gaussian beam, perturbed k) at 20^3 nodes:
+    each batched forward simulation matches the oracle; front-face output is the z = 0 plane."""
+    B, nax, nsteps = 3, 20, 12
+    probs = [synth.c5(j, n_nodes_axis=nax, nsteps=nsteps) for j in range(B)]
+    g = probs[0].grid
+    ctx = make_ctx(g, probs[0].k, probs[0].c)
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, probs[0].flux_face, probs[0].flux_const, probs[0].beam, F)
+    ub = T(np.zeros(B * g.n_nodes))
+    front = torch.empty(B * ctx.n_plane, dtype=torch.float64, device=DEV)
+    kb = np.stack([p.k for p in probs]).ravel()
+    cb = np.stack([p.c for p in probs]).ravel()
+    hf.hf_simulate_batched(ctx, B, T(kb), T(cb), probs[0].theta, probs[0].dt, nsteps, F, ub, 0, front)
+    ub = N(ub).reshape(B, -1)
+    front = N(front).reshape(B, -1)
+    for j, p in enumerate(probs):
+        o, Fo = oracle.problem_oracle(p)
+        uo, st, it, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
+        assert st == 0 and rel(ub[j], uo) <= 1e-10, j
+        assert np.array_equal(front[j], ub[j][:ctx.n_plane])
+    # deeper corrosion (less conductive oxide near the rear) -> different front-face fields
+    assert not np.allclose(front[0], front[1])
