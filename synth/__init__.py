@@ -26,6 +26,11 @@ import numpy as np
 STEEL = (3.724e6, 4.9e8)   # (c = rhoC, k)
 OXIDE = (1.65e6, 4.0e6)
 
+# 10 W laser in the unit system of the paper's rho C and k: those are SI values
+# read in (g, mm, s) units (J/(m^3 K) == g/(mm s^2 K)), where 1 W = 1e9 g mm^2 s^-3.
+# (reading R12.)
+BEAM_POWER = 10.0 * 1e9
+
 # face ids used by both sides: bit f of a Dirichlet mask / the ``face`` argument
 FACE_XM, FACE_XP, FACE_YM, FACE_YP, FACE_ZM, FACE_ZP = range(6)
 
@@ -234,7 +239,7 @@ def c5(j: int, depth: Optional[float] = None, n_nodes_axis: int = 100, nsteps: i
         k = k * lognormal_perturbation(g.n_elems, seed=2 + j)
     return Problem(f"c5[{j}]", g, k, c, np.zeros(g.n_nodes), theta=0.5, dt=10.0 / nsteps,
                    nsteps=nsteps, rtol=1e-12, flux_face=FACE_ZM, flux_const=0.0,
-                   beam=(10.0, 2.0, 0.0, 0.0), extra={"depth": depth})
+                   beam=(BEAM_POWER, 2.0, 0.0, 0.0), extra={"depth": depth})
 
 
 def laminate(s: int) -> Problem:

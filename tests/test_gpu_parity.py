@@ -441,4 +441,4 @@ def test_c5_corrosion_batched_small():
         assert st == 0 and rel(ub[j], uo) <= 1e-10, j
         assert np.array_equal(front[j], ub[j][:ctx.n_plane])
     # deeper corrosion (less conductive oxide near the rear) -> different front-face fields
-    assert not np.allclose(front[0], front[1])
+    assert np.abs(front[0] - front[1]).max() > 1e-6 * np.abs(front[0]).max()
