@@ -486,7 +486,7 @@ static Sync make_sync(hf_ctx *c, Sys &s, int consumes = -1, int produces = -1)
     y.st = s.st;
     y.launches = c->launches;
     if (consumes >= 0) {
-        if (c->nranks > 1) { y.pin = s.sums; y.pin_n = 1; }
+        if (c->comm) { y.pin = s.sums; y.pin_n = 1; }
         else { y.pin = consumes == 0 ? s.partA : s.partB; y.pin_n = -1; }
     }
     if (produces >= 0) y.pout = produces == 0 ? s.partA : s.partB;
@@ -790,7 +790,7 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
 // slab mode, after a producer kernel: local sums -> allreduce -> (ghosts of s for the next apply)
 static hf_status comm_after(hf_ctx *c, Sys &s, int which, bool exch)
 {
-    if (c->nranks <= 1) return HF_OK;
+    if (!c->comm) return HF_OK;
     Sync sy = make_sync(c, s);
     sy.pin = which == 0 ? s.partA : s.partB;
     k_localsum<<<1, 256, 0, s.stream>>>(sy, which, s.sums);
@@ -866,7 +866,7 @@ static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, in
 {
     HFCK(read_state(c, s));
     if (!s.st_host->active) return HF_OK;
-    const bool slab = c->nranks > 1;
+    const bool slab = c->comm != nullptr;
     const int check = slab && !c->comm->graph_capturable() ? 1 : c->check_every;
     for (int i = 0;;) {
         HFCK(run(c, L.A, s.stream));
@@ -1082,7 +1082,7 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     CUCK(cudaMemcpyAsync(s.b, db, c->nloc * sizeof(double), cudaMemcpyDeviceToDevice, s.stream));
     HFCK(enqueue_diag(c, s, aK, aM, nullptr, s.invd));
     HFCK(enqueue_set_dirichlet(c, s, dx, s.b));           // x_D = b_D
-    if (c->nranks > 1) HFCK(c->comm->exchange(c, s, dx));
+    if (c->comm) HFCK(c->comm->exchange(c, s, dx));
     Maps xm = s.maps;
     HFCK(node_map(c, dx, &xm.node[MAP_U0]));
     // init: r = b - A x0; s = P^{-1} r; delta; ||b_F||   (Alg. 1 lines 2-4)
@@ -1100,7 +1100,7 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     StepArgs sa = step_args(c, s, dx, nullptr, -1);
     sa.iters_out = nullptr;
     std::vector<Launch> post = step_launches(c, sa, false);
-    const bool use_graph = c->driver == 0 && c->nranks == 1 && !c->prof;
+    const bool use_graph = c->driver == 0 && !c->comm && !c->prof;
     if (use_graph) {
         cudaGraph_t g;
         HFCK(build_cg_graph(c, {}, init, L, post, &g));
@@ -1156,7 +1156,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     for (int f = 0; f < 6; f++) if ((c->dbits >> f & 1u) && c->gval[f] != 0.0) lift = true;
     if (nsteps <= 0) return HF_OK;
 
-    const bool use_graph = c->driver == 0 && c->nranks == 1 && !c->prof;
+    const bool use_graph = c->driver == 0 && !c->comm && !c->prof;
     c->last_ms_steps = 0.0;
     SimKey key;
     std::memset(&key, 0, sizeof(key));
@@ -1251,7 +1251,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             HFCK(comm_after(c, s, 1, true));
             HFCK(host_cg_loop(c, s, L, o.max_iter, o.replace_every));
             for (auto &p : post) HFCK(run(c, p, s.stream));
-            if (c->nranks > 1) {
+            if (c->comm) {
                 // the next RHS reads u^{n+1} ghosts: kernel B keeps the iterate's ghost planes
                 // consistent (x update on every local plane)
                 HFCK(read_state(c, s));
@@ -1301,7 +1301,7 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
     HFCK(copy_in(c, s.U[0], u, c->nzl, s.stream));
     const bool first = step0 <= 0 || !u_prev;
     if (!first) HFCK(copy_in(c, s.U[2], u_prev, c->nzl, s.stream));
-    if (c->nranks > 1) {          // make the ghost planes of the input state consistent
+    if (c->comm) {                // make the ghost planes of the input state consistent
         HFCK(c->comm->exchange(c, s, s.U[0]));
         if (!first) HFCK(c->comm->exchange(c, s, s.U[2]));
     }
@@ -1360,7 +1360,7 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
     if (!c || B < 0 || !k_batch || !u_batch || nsteps < 0 || !(dt > 0.0))
         return fail(HF_E_ARG, "hf_simulate_batched: bad argument");
     if (!c_batch && !c->coef_set) return fail(HF_E_STATE, "hf_simulate_batched: no capacity field");
-    if (c->nranks > 1) return fail(HF_E_ARG, "hf_simulate_batched: not available on slab contexts");
+    if (c->comm) return fail(HF_E_ARG, "hf_simulate_batched: not available on slab contexts");
     if (front_out && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "snap_plane");
     CUCK(cudaSetDevice(c->device));
     hf_cg_opts o = {1e-12, 10000, 50};

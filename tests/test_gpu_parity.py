@@ -442,3 +442,26 @@ def test_c5_corrosion_batched_small():
         assert np.array_equal(front[j], ub[j][:ctx.n_plane])
     # deeper corrosion (less conductive oxide near the rear) -> different front-face fields
     assert np.abs(front[0] - front[1]).max() > 1e-6 * np.abs(front[0]).max()
+
+
+@pytest.mark.parametrize("transport", [0, 1])
+def test_slab_single_rank_nccl_and_local(transport):
+    """A 1-rank slab context runs the slab driver (host loop, k_localsum, transport allreduce,
+    ghost exchange calls) -- through real NCCL for transport 0 -- and must reproduce the plain
+    single-GPU run bit for bit (same kernels, same reduction order)."""
+    p = synth.c1()
+    ug, st, _, _ = _gpu_sim(p)
+    if transport == 0:
+        uid = hf.hf_nccl_unique_id()
+        ctx = hf.hf_create_slab(p.grid, 0, 1, uid, transport=0, device=0)
+    else:
+        grp = hf.hf_local_group_create(1)
+        ctx = hf.hf_create_slab(p.grid, 0, 1, grp, transport=1, device=0)
+    hf.hf_set_coefficients(ctx, T(p.k), T(p.c))
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
+    u = T(p.u0)
+    st2 = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, F, u, rtol=p.rtol)
+    assert np.array_equal(N(u), ug)
+    assert st2["total_iters"] == st["total_iters"]
+    del ctx
