@@ -112,10 +112,18 @@ hf_status hf_set_coefficients(hf_ctx *ctx, const double *k_elem, const double *c
  * and hf_simulate*; hf_apply is always the unconstrained operator. */
 hf_status hf_set_dirichlet_faces(hf_ctx *ctx, uint32_t face_bits, const double values[6]);
 
+/* Element variant (NEXT row f1).  type 0 (default): trilinear hexahedron per voxel (reading R1).
+ * type 1: the paper's mesh -- every voxel split into 6 linear tetrahedra along its (0,0,0)-(1,1,1)
+ * diagonal (Fig. 2), each tet carrying its voxel's (k_e, c_e) (reading R1b); boundary
+ * quads become two P1 triangles for hf_face_load.  Affects every operator of the context.
+ * Errors: HF_E_ARG. */
+hf_status hf_set_element(hf_ctx *ctx, int32_t type);
+
 /* Flux load F_i = int_face f phi_i ds over face `face` (0..5) (P:44, P:50-52 boundary term):
  * f = f_const + beam, beam(a,b) = P/(2 pi s^2) exp(-((a-ca)^2 + (b-cb)^2) / (2 s^2)) with
  * beam = {P, s, ca, cb} (or NULL), (a, b) the face's in-plane coordinates in increasing axis
- * order (reading R12).  2x2 Gauss quadrature per boundary quad.  F: n_nodes fp64, written
+ * order (reading R12).  2x2 Gauss quadrature per boundary quad (type-1 elements: 3-point rule per
+ * triangle).  F: n_nodes fp64, written
  * entirely (zero off the face).  Errors: HF_E_ARG (face, NULL F). */
 hf_status hf_face_load(hf_ctx *ctx, int face, double f_const, const double beam[4], double *F);
 

@@ -44,7 +44,8 @@ def lib():
     if _lib is None:
         L = C.CDLL(build())
         L.or_create.restype = C.c_void_p
-        L.or_create.argtypes = [_i64p, _dp, _dp, _dp, _dp, C.c_int]
+        L.or_create.argtypes = [_i64p, _dp, _dp, _dp, _dp, C.c_int, C.c_int]
+        L.or_tet_voxel_matrices.argtypes = [_dp, _dp, _dp]
         L.or_destroy.argtypes = [C.c_void_p]
         L.or_element_matrices.argtypes = [_dp, _dp, _dp]
         L.or_get_element_matrices.argtypes = [C.c_void_p, _dp, _dp]
@@ -75,6 +76,14 @@ def element_matrices(h: Sequence[float]):
     return Ke.reshape(8, 8), Me.reshape(8, 8)
 
 
+def tet_voxel_matrices(h: Sequence[float]):
+    """(K, M) 8x8 of a voxel split into 6 Kuhn P1 tetrahedra (NEXT row f1)."""
+    Ke = np.zeros(64)
+    Me = np.zeros(64)
+    lib().or_tet_voxel_matrices(np.asarray(h, dtype=np.float64), Ke, Me)
+    return Ke.reshape(8, 8), Me.reshape(8, 8)
+
+
 def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
@@ -82,14 +91,15 @@ def _f64(a):
 class Oracle:
     """Assembled-matrix reference for one grid and one (k, c) field."""
 
-    def __init__(self, grid, k, c, assemble: bool = True):
+    def __init__(self, grid, k, c, assemble: bool = True, elem: int = 0):
         self.grid = grid
         self.nn = grid.n_nodes
         self._k = _f64(k)
         self._c = _f64(c)
         assert self._k.size == grid.n_elems and self._c.size == grid.n_elems
         self._p = lib().or_create(np.asarray(grid.ne, dtype=np.int64), _f64(grid.h), _f64(grid.origin),
-                                  self._k, self._c, 1 if assemble else 0)
+                                  self._k, self._c, 1 if assemble else 0, elem)
+        self.elem = elem
         if not self._p:
             raise MemoryError("or_create failed")
 
@@ -174,9 +184,9 @@ class Oracle:
         return u, st, iters[:nsteps], snap
 
 
-def problem_oracle(p, assemble=True):
+def problem_oracle(p, assemble=True, elem=0):
     """Oracle for a synth.Problem with its Dirichlet faces and flux load applied."""
-    o = Oracle(p.grid, p.k, p.c, assemble=assemble)
+    o = Oracle(p.grid, p.k, p.c, assemble=assemble, elem=elem)
     if p.dirichlet_bits:
         o.set_dirichlet(p.dirichlet_bits, p.dirichlet_values)
     F = o.face_load(p.flux_face, p.flux_const, p.beam)

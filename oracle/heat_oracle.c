@@ -39,7 +39,8 @@ typedef struct {
     double h[3];
     double origin[3];
     int64_t nnodes, nelems;
-    double Ke[64], Me[64]; /* reference element matrices (unit k, unit c) */
+    int elem;              /* 0: trilinear hexahedron (R1), 1: 6 P1 tets per voxel (f1)       */
+    double Ke[64], Me[64]; /* voxel element matrices (unit k, unit c) */
     double *k, *c;         /* per-element coefficients (copies) */
     /* CSR of K and M (same pattern) */
     int has_csr;
@@ -85,6 +86,79 @@ void or_element_matrices(const double h[3], double Ke[64], double Me[64])
             for (int b = 0; b < 8; b++) {
                 Me[a * 8 + b] += w * N[a] * N[b];
                 Ke[a * 8 + b] += w * (G[a][0] * G[b][0] + G[a][1] * G[b][1] + G[a][2] * G[b][2]);
+            }
+    }
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Paper's element (NEXT row f1): each voxel split into 6 linear tetrahedra (Fig. 2)  */
+/* along the diagonal from local node 0 (0,0,0) to local node 7 (1,1,1): tet number t follows    */
+/* the lattice path 0 -> e_a -> e_a + e_b -> 7 for the t-th permutation (a, b, c) of the axes.    */
+/* P1 matrices from vertex coordinates: J = [p1-p0, p2-p0, p3-p0], V = |det J| / 6,              */
+/* grad(lambda_i) = row i of J^{-1} (i = 1..3), grad(lambda_0) = -sum; K_ij = V g_i . g_j,        */
+/* M_ij = V (1 + delta_ij) / 20.  Each tet carries its voxel's (k_e, c_e) (reading R1b), so the   */
+/* voxel's element matrices are the assembly of its 6 tets into the 8 voxel nodes.        */
+
+static const int tet_perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+
+void or_tet_vertices(int t, int local[4])
+{
+    int b[3] = {0, 0, 0};
+    local[0] = 0;
+    for (int s = 0; s < 3; s++) {
+        b[tet_perm[t][s]] = 1;
+        local[s + 1] = b[0] + 2 * b[1] + 4 * b[2];
+    }
+}
+
+void or_tet_matrices(const double p[4][3], double K[16], double M[16])
+{
+    double J[3][3];
+    for (int r = 0; r < 3; r++)
+        for (int c = 0; c < 3; c++) J[r][c] = p[c + 1][r] - p[0][r];   /* columns p_i - p_0 */
+    double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1])
+               - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0])
+               + J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    double inv[3][3];   /* inverse by cofactors */
+    inv[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / det;
+    inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+    inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+    inv[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / det;
+    inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+    inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+    inv[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
+    inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+    inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+    double g[4][3];
+    for (int d = 0; d < 3; d++) {
+        g[1][d] = inv[0][d];
+        g[2][d] = inv[1][d];
+        g[3][d] = inv[2][d];
+        g[0][d] = -(g[1][d] + g[2][d] + g[3][d]);
+    }
+    double V = fabs(det) / 6.0;
+    for (int i = 0; i < 4; i++)
+        for (int j = 0; j < 4; j++) {
+            K[i * 4 + j] = V * (g[i][0] * g[j][0] + g[i][1] * g[j][1] + g[i][2] * g[j][2]);
+            M[i * 4 + j] = V * (i == j ? 2.0 : 1.0) / 20.0;
+        }
+}
+
+/* voxel matrices of the 6-tet split (sum of the tets' matrices over the voxel's 8 nodes) */
+void or_tet_voxel_matrices(const double h[3], double Ke[64], double Me[64])
+{
+    for (int i = 0; i < 64; i++) { Ke[i] = 0.0; Me[i] = 0.0; }
+    for (int t = 0; t < 6; t++) {
+        int loc[4];
+        or_tet_vertices(t, loc);
+        double p[4][3], K[16], M[16];
+        for (int v = 0; v < 4; v++)
+            for (int d = 0; d < 3; d++) p[v][d] = ((loc[v] >> d) & 1) * h[d];
+        or_tet_matrices(p, K, M);
+        for (int a = 0; a < 4; a++)
+            for (int b = 0; b < 4; b++) {
+                Ke[loc[a] * 8 + loc[b]] += K[a * 4 + b];
+                Me[loc[a] * 8 + loc[b]] += M[a * 4 + b];
             }
     }
 }
@@ -163,7 +237,7 @@ static int assemble_csr(or_ctx *o)
 /* ------------------------------------------------------------------------------------------ */
 
 or_ctx *or_create(const int64_t ne[3], const double h[3], const double origin[3],
-                  const double *k, const double *c, int assemble)
+                  const double *k, const double *c, int assemble, int elem)
 {
     or_ctx *o = calloc(1, sizeof(or_ctx));
     if (!o) return NULL;
@@ -172,7 +246,9 @@ or_ctx *or_create(const int64_t ne[3], const double h[3], const double origin[3]
     }
     o->nnodes = o->nn[0] * o->nn[1] * o->nn[2];
     o->nelems = ne[0] * ne[1] * ne[2];
-    or_element_matrices(o->h, o->Ke, o->Me);
+    o->elem = elem;
+    if (elem == 1) or_tet_voxel_matrices(o->h, o->Ke, o->Me);
+    else or_element_matrices(o->h, o->Ke, o->Me);
     o->k = malloc(sizeof(double) * (size_t)o->nelems);
     o->c = malloc(sizeof(double) * (size_t)o->nelems);
     o->isD = calloc((size_t)o->nnodes, 1);
@@ -264,8 +340,50 @@ void or_apply_rows(const or_ctx *o, double aK, double aM, const double *u,
 /*   beam(a,b) = P/(2 pi s^2) exp(-((a-ca)^2 + (b-cb)^2)/(2 s^2)),  (a, b) the in-plane        */
 /*   coordinates of the face in increasing axis order.  2x2 Gauss per boundary quad.            */
 
+static double beam_f(double f_const, const double *beam, double a, double b)
+{
+    double f = f_const;
+    if (beam) {
+        double P = beam[0], s = beam[1], ca = beam[2], cb = beam[3];
+        f += P / (2.0 * M_PI * s * s) * exp(-((a - ca) * (a - ca) + (b - cb) * (b - cb)) / (2.0 * s * s));
+    }
+    return f;
+}
+
+/* Tet mesh: every boundary quad is two triangles {(0,0),(1,0),(1,1)} and {(0,0),(0,1),(1,1)}
+ * in the face's (a, b) corner coordinates (the boundary faces of the Kuhn tets); P1 basis on
+ * each triangle; 3-point quadrature (barycentric (2/3,1/6,1/6) and permutations, weight 1/3,
+ * exact for quadratics). */
+static int face_load_tets(const or_ctx *o, int face, double f_const, const double *beam, double *F)
+{
+    int nd = face / 2, ax = nd == 0 ? 1 : 0, bx = nd == 2 ? 1 : 2;
+    int64_t plane = (face & 1) ? o->ne[nd] : 0;
+    const int tri[2][3][2] = {{{0, 0}, {1, 0}, {1, 1}}, {{0, 0}, {0, 1}, {1, 1}}};
+    const double bary[3][3] = {{2.0 / 3, 1.0 / 6, 1.0 / 6}, {1.0 / 6, 2.0 / 3, 1.0 / 6}, {1.0 / 6, 1.0 / 6, 2.0 / 3}};
+    for (int64_t n = 0; n < o->nnodes; n++) F[n] = 0.0;
+    double area = 0.5 * o->h[ax] * o->h[bx];
+    for (int64_t qb = 0; qb < o->ne[bx]; qb++)
+    for (int64_t qa = 0; qa < o->ne[ax]; qa++)
+        for (int t = 0; t < 2; t++)
+            for (int g = 0; g < 3; g++) {
+                double a = o->origin[ax], b = o->origin[bx];
+                for (int v = 0; v < 3; v++) {
+                    a += bary[g][v] * (qa + tri[t][v][0]) * o->h[ax];
+                    b += bary[g][v] * (qb + tri[t][v][1]) * o->h[bx];
+                }
+                double f = beam_f(f_const, beam, a, b);
+                for (int v = 0; v < 3; v++) {
+                    int64_t idx[3];
+                    idx[nd] = plane; idx[ax] = qa + tri[t][v][0]; idx[bx] = qb + tri[t][v][1];
+                    F[node_id(o, idx[0], idx[1], idx[2])] += (area / 3.0) * f * bary[g][v];
+                }
+            }
+    return OR_OK;
+}
+
 int or_face_load(const or_ctx *o, int face, double f_const, const double *beam, double *F)
 {
+    if (o->elem == 1) return (face < 0 || face > 5) ? OR_E_ARG : face_load_tets(o, face, f_const, beam, F);
     if (face < 0 || face > 5) return OR_E_ARG;
     int nd = face / 2;                       /* normal axis */
     int ax = nd == 0 ? 1 : 0;                /* first in-plane axis */

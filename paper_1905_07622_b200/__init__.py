@@ -81,6 +81,7 @@ _SIGS = {
     "hf_set_driver": (_i32, [_vp, _i32]),
     "hf_flush_l2": (_i32, [_vp]),
     "hf_set_step_flush": (_i32, [_vp, _i32]),
+    "hf_set_element": (_i32, [_vp, _i32]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -347,6 +348,11 @@ def hf_set_driver(ctx: Context, driver: int):
 
 def hf_flush_l2(ctx: Context):
     _check(_lib.hf_flush_l2(ctx.ptr))
+
+
+def hf_set_element(ctx: Context, elem_type: int):
+    """0: trilinear hexahedra (default); 1: the paper's 6 P1 tets per voxel."""
+    _check(_lib.hf_set_element(ctx.ptr, elem_type))
 
 
 def hf_set_step_flush(ctx: Context, enable: bool):

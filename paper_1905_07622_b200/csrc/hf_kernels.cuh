@@ -79,6 +79,14 @@ struct Lam {
     double ka[4], ma[4], kb[4], mb[4];
 };
 
+// Dense voxel matrices (element variant EL_DENSE: the paper's 6-tet split, NEXT row f1):
+// y_e = (k_e Ks + c_e Ms) u_e with Ks = aK K_ref, Ms = aM M_ref (8 x 8, local l = bx+2by+4bz).
+struct Dense {
+    double K[64], M[64];
+};
+
+enum { EL_Q1 = 0, EL_DENSE = 1 };
+
 struct Sync {               // per-system reduction plumbing
     CgState *st;
     const double *pin;      // partial sums of the previous kernel (NPART per block)
@@ -110,6 +118,7 @@ struct StencilArgs {
     int first;                    // LD_X0: step 0 of the run (guess = u^0)
     int rot_role;                 // ROT_*: map slots resolved from st->step
     Sync sy;
+    Dense dn;                     // EL_DENSE only
 };
 
 __device__ __forceinline__ bool is_dirichlet(const Geom &g, int x, int y, int zl, double &val)
@@ -306,9 +315,9 @@ enum {
     FL_DSET = 8,   // EP_APPLY with FL_DIR: y_D = g (else y_D = u_D, identity rows)
 };
 
-template <int R, int NW, int NS, int LD, int EP, int FL>
+template <int R, int NW, int NS, int LD, int EP, int FL, int EL>
 __global__ void __launch_bounds__(32 * NW)
-k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
+k_stencil(const __grid_constant__ Maps maps, const __grid_constant__ StencilArgs a)
 {
     using SH = StencilShape<R, NW, LD>;
     constexpr int NT = 32 * NW;
@@ -430,8 +439,9 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
         }
     }
 
-    double Fp[R][4];          // face transforms of the lower plane p-1
-    double Cy[R][4];          // face-space contributions carried from the layer below
+    double Fp[R][4];          // Q1: face transforms of the lower plane p-1
+    double Cy[R][4];          // contributions carried from the layer below (face / node space)
+    double Pv[R + 1], Pv1[R + 1];   // dense: node values of plane p-1 at x and x+1
     double cen[R];            // raw centre values of plane p-1 (rows 0..R-1)
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -440,6 +450,8 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
         for (int ch = 0; ch < 4; ch++) { Fp[r][ch] = 0.0; Cy[r][ch] = 0.0; }
         cen[r] = 0.0;
     }
+#pragma unroll
+    for (int r = 0; r <= R; r++) { Pv[r] = 0.0; Pv1[r] = 0.0; }
 
     for (int it = 0; it < nplanes; ++it) {
         const int p = zb - 1 + it;
@@ -450,7 +462,7 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
         const double *n1 = sb + SH::NODE_DBL + w * R * BOXW + lane + xoff;
         const double *kcs = sb + NA * SH::NODE_DBL + w * R * 64 + 2 * lane;
         // ---- node values of plane p (rows 0..R), x butterfly (edges) ----------------------
-        double S[R + 1], D[R + 1], craw[R];
+        double S[R + 1], D[R + 1], V0[R + 1], V1[R + 1], craw[R];
         const bool store_p = (EP == EP_CGA || EP == EP_RESID_INIT) && (p >= a.zs0 && p < a.zs1) &&
                              ((p >= zb && p < ze) || (p == zb - 1 && zb == a.z_out0) ||
                               (p == ze && ze == a.z_out1));
@@ -488,43 +500,79 @@ k_stencil(const __grid_constant__ Maps maps, const StencilArgs a)
             }
             S[r] = v + v1;
             D[r] = v - v1;
+            V0[r] = v;
+            V1[r] = v1;
         }
-        // ---- element layer p-1: y butterfly, fused z butterfly + scaling -------------------
-        // (lane 31's element X0+30 reads node X0+31 from the box; elements outside the domain
-        //  have k = c = 0 from the TMA zero fill)
-        double T[R][4];
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            double Fc[4];
-            Fc[0] = S[r] + S[r + 1];   // sx=0, sy=0
-            Fc[1] = S[r] - S[r + 1];   // sx=0, sy=1
-            Fc[2] = D[r] + D[r + 1];   // sx=1, sy=0
-            Fc[3] = D[r] - D[r + 1];   // sx=1, sy=1
-            const double2 kc = *reinterpret_cast<const double2 *>(kcs + r * 64);
-#pragma unroll
-            for (int ch = 0; ch < 4; ch++) {
-                const double av = fma(kc.x, a.lam.ka[ch], kc.y * a.lam.ma[ch]);
-                const double bv = fma(kc.x, a.lam.kb[ch], kc.y * a.lam.mb[ch]);
-                T[r][ch] = fma(av, Fp[r][ch], fma(bv, Fc[ch], Cy[r][ch]));   // bottom plane p-1
-                Cy[r][ch] = fma(bv, Fp[r][ch], av * Fc[ch]);                  // top plane p
-                Fp[r][ch] = Fc[ch];
-            }
-        }
-        // ---- backward y and x butterflies for plane p-1 ------------------------------------
         const int pout = p - 1;
         const bool out_plane = pout >= zb && pout < ze;   // uniform across the CTA
         double yv[R + 1];
+        if (EL == EL_Q1) {
+            // ---- element layer p-1: y butterfly, fused z butterfly + scaling -------------------
+            // (lane 31's element X0+30 reads node X0+31 from the box; elements outside the domain
+            //  have k = c = 0 from the TMA zero fill)
+            double T[R][4];
 #pragma unroll
-        for (int e = 0; e <= R; e++) {
-            double E0, E1;                              // sx = 0, 1
-            if (e == 0) { E0 = T[0][0] + T[0][1]; E1 = T[0][2] + T[0][3]; }
-            else if (e == R) { E0 = T[R - 1][0] - T[R - 1][1]; E1 = T[R - 1][2] - T[R - 1][3]; }
-            else {
-                E0 = (T[e][0] + T[e][1]) + (T[e - 1][0] - T[e - 1][1]);
-                E1 = (T[e][2] + T[e][3]) + (T[e - 1][2] - T[e - 1][3]);
+            for (int r = 0; r < R; r++) {
+                double Fc[4];
+                Fc[0] = S[r] + S[r + 1];   // sx=0, sy=0
+                Fc[1] = S[r] - S[r + 1];   // sx=0, sy=1
+                Fc[2] = D[r] + D[r + 1];   // sx=1, sy=0
+                Fc[3] = D[r] - D[r + 1];   // sx=1, sy=1
+                const double2 kc = *reinterpret_cast<const double2 *>(kcs + r * 64);
+#pragma unroll
+                for (int ch = 0; ch < 4; ch++) {
+                    const double av = fma(kc.x, a.lam.ka[ch], kc.y * a.lam.ma[ch]);
+                    const double bv = fma(kc.x, a.lam.kb[ch], kc.y * a.lam.mb[ch]);
+                    T[r][ch] = fma(av, Fp[r][ch], fma(bv, Fc[ch], Cy[r][ch]));   // bottom plane p-1
+                    Cy[r][ch] = fma(bv, Fp[r][ch], av * Fc[ch]);                  // top plane p
+                    Fp[r][ch] = Fc[ch];
+                }
             }
-            const double left = __shfl_up_sync(0xffffffffu, E0 - E1, 1);
-            yv[e] = (E0 + E1) + left;                   // lane 0's value is not owned
+            // ---- backward y and x butterflies for plane p-1 ------------------------------------
+#pragma unroll
+            for (int e = 0; e <= R; e++) {
+                double E0, E1;                              // sx = 0, 1
+                if (e == 0) { E0 = T[0][0] + T[0][1]; E1 = T[0][2] + T[0][3]; }
+                else if (e == R) { E0 = T[R - 1][0] - T[R - 1][1]; E1 = T[R - 1][2] - T[R - 1][3]; }
+                else {
+                    E0 = (T[e][0] + T[e][1]) + (T[e - 1][0] - T[e - 1][1]);
+                    E1 = (T[e][2] + T[e][3]) + (T[e - 1][2] - T[e - 1][3]);
+                }
+                const double left = __shfl_up_sync(0xffffffffu, E0 - E1, 1);
+                yv[e] = (E0 + E1) + left;                   // lane 0's value is not owned
+            }
+        } else {
+            // ---- dense voxel matrices (6-tet split): u_e = 4 values of plane p-1 + 4 of p ----
+            double B4[R][4];
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const double2 kc = *reinterpret_cast<const double2 *>(kcs + r * 64);
+                const double ue[8] = {Pv[r], Pv1[r], Pv[r + 1], Pv1[r + 1], V0[r], V1[r], V0[r + 1], V1[r + 1]};
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    double yk = 0.0, ym = 0.0;
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        yk = fma(a.dn.K[i * 8 + j], ue[j], yk);
+                        ym = fma(a.dn.M[i * 8 + j], ue[j], ym);
+                    }
+                    const double y = fma(kc.x, yk, kc.y * ym);
+                    if (i < 4) B4[r][i] = Cy[r][i] + y;      // bottom plane p-1 complete
+                    else Cy[r][i - 4] = y;                   // top plane p, carried
+                }
+            }
+#pragma unroll
+            for (int r = 0; r <= R; r++) { Pv[r] = V0[r]; Pv1[r] = V1[r]; }
+            // node (x, row e) of plane p-1 collects element rows e (by = 0) and e-1 (by = 1);
+            // the bx = 1 parts belong to node x+1 (next lane)
+#pragma unroll
+            for (int e = 0; e <= R; e++) {
+                double X0v = 0.0, X1v = 0.0;
+                if (e < R) { X0v += B4[e][0]; X1v += B4[e][1]; }
+                if (e > 0) { X0v += B4[e - 1][2]; X1v += B4[e - 1][3]; }
+                const double left = __shfl_up_sync(0xffffffffu, X1v, 1);
+                yv[e] = X0v + left;
+            }
         }
         seam[it & 1][w][lane] = yv[R];
         __syncthreads();                                // seam visible; stage `st` fully read
@@ -712,7 +760,11 @@ __device__ __forceinline__ double2 load_kc(const Geom &g, const double2 *kc, int
 // diag_i = sum over the 8 elements around node i of aK k_e Kd + aM c_e Md, with
 // Kd = K_ref[l][l], Md = M_ref[l][l] (the same for every l of a voxel); 1 on Dirichlet rows.
 
-__global__ void k_diag(Geom g, const double2 *kc, double aK, double aM, double Kd, double Md,
+struct DiagC {              // diagonal entries K_ref[l][l], M_ref[l][l] per local node l
+    double Kd[8], Md[8];
+};
+
+__global__ void k_diag(Geom g, const double2 *kc, double aK, double aM, DiagC dc,
                        double *diag, double *invd, unsigned long long *launches)
 {
     const long long n = g.plane * g.nzl;
@@ -722,12 +774,12 @@ __global__ void k_diag(Geom g, const double2 *kc, double aK, double aM, double K
     const int x = (int)(i % g.pitch), y = (int)((i / g.pitch) % g.ny1), z = (int)(i / g.plane);
     if (x >= g.nx1) { if (diag) diag[i] = 0.0; if (invd) invd[i] = 0.0; return; }   // pitch padding
     double sk = 0.0, sc = 0.0;
-    for (int l = 0; l < 8; l++) {
+    for (int l = 0; l < 8; l++) {   // node is local node l of element (x - bx, y - by, z - bz)
         const double2 v = load_kc(g, kc, x - (l & 1), y - ((l >> 1) & 1), z - ((l >> 2) & 1));
-        sk += v.x;
-        sc += v.y;
+        sk = fma(v.x, dc.Kd[l], sk);
+        sc = fma(v.y, dc.Md[l], sc);
     }
-    double d = aK * Kd * sk + aM * Md * sc;
+    double d = aK * sk + aM * sc;
     double gv;
     if (is_dirichlet(g, x, y, z, gv)) d = 1.0;
     if (diag) diag[i] = d;
@@ -766,6 +818,7 @@ struct FaceArgs {
     double f_const;
     int has_beam;
     double bP, bs, bca, bcb;
+    int tets;                 // 1: boundary quads are two P1 triangles (6-tet split, f1)
     double *F;
     unsigned long long *launches;
 };
@@ -788,6 +841,45 @@ __global__ void k_face_load(const FaceArgs a)
     const double gp0 = 0.5 * (1.0 - 0.57735026918962576451), gp1 = 0.5 * (1.0 + 0.57735026918962576451);
     const double w = (a.ha * 0.5) * (a.hb * 0.5);
     double sum = 0.0;
+    if (a.tets) {
+        // quad (qa, qb) = triangles {(0,0),(1,0),(1,1)} and {(0,0),(0,1),(1,1)} (the Kuhn tets'
+        // boundary faces); P1 hat of the node; 3-point rule (barycentric 2/3,1/6,1/6; weight 1/3)
+        const double area3 = (0.5 * a.ha * a.hb) / 3.0;
+        for (int cb = 0; cb < 2; cb++) {
+            const int qb = ib - cb;
+            if (qb < 0 || qb >= a.nb - 1) continue;
+            for (int ca = 0; ca < 2; ca++) {
+                const int qa = ia - ca;
+                if (qa < 0 || qa >= a.na - 1) continue;
+                for (int t = 0; t < 2; t++) {
+                    // triangle vertices in corner coordinates
+                    const int va[3] = {0, t ? 0 : 1, 1}, vb[3] = {0, t ? 1 : 0, 1};
+                    int me = -1;
+                    for (int v = 0; v < 3; v++) if (va[v] == ca && vb[v] == cb) me = v;
+                    if (me < 0) continue;                 // node not a vertex of this triangle
+                    for (int gq = 0; gq < 3; gq++) {
+                        double pa = 0.0, pb = 0.0, lam = 0.0;
+                        for (int v = 0; v < 3; v++) {
+                            const double bw = (v == gq) ? (2.0 / 3.0) : (1.0 / 6.0);
+                            pa += bw * va[v];
+                            pb += bw * vb[v];
+                            if (v == me) lam = bw;
+                        }
+                        double f = a.f_const;
+                        if (a.has_beam) {
+                            const double xa = a.oa + (qa + pa) * a.ha - a.bca, xb = a.ob + (qb + pb) * a.hb - a.bcb;
+                            f += a.bP / (2.0 * 3.14159265358979323846 * a.bs * a.bs) *
+                                 exp(-(xa * xa + xb * xb) / (2.0 * a.bs * a.bs));
+                        }
+                        sum += area3 * f * lam;
+                    }
+                }
+            }
+        }
+        const long long node = (long long)zl * a.g.plane + (long long)idx3[1] * a.g.pitch + idx3[0];
+        a.F[node] = sum;
+        return;
+    }
     for (int cb = 0; cb < 2; cb++) {             // node is corner (ca, cb) of quad (ia-ca, ib-cb)
         const int qb = ib - cb;
         if (qb < 0 || qb >= a.nb - 1) continue;

@@ -187,7 +187,8 @@ struct hf_ctx {
     bool coef_set = false;
     unsigned dbits = 0;
     double gval[6] = {0, 0, 0, 0, 0, 0};
-    double Kd = 0, Md = 0;           // diagonal entry of K_ref, M_ref
+    int elem = EL_Q1;                // element variant (hf_set_element)
+    DiagC dg;                        // diagonal entries of K_ref, M_ref per local node
     Sys sys0;
     std::vector<std::unique_ptr<Sys>> pool;
     unsigned long long *launches = nullptr;
@@ -346,6 +347,34 @@ static Lam make_lam(const double h[3], double aK, double aM)
     return L;
 }
 
+// Voxel matrices of the 6-tet split (NEXT row f1): tet t follows the lattice path
+// 0 -> e_a -> e_a + e_b -> 7 for the t-th axis permutation (a, b, c).  On that tet the P1
+// barycentric coordinates are 1 - x_a/h_a, x_a/h_a - x_b/h_b, x_b/h_b - x_c/h_c, x_c/h_c, so
+// their gradients are -e_a/h_a, e_a/h_a - e_b/h_b, e_b/h_b - e_c/h_c, e_c/h_c; V = hx hy hz / 6;
+// K_ij = V g_i . g_j, M_ij = V (1 + delta_ij) / 20, summed into the voxel's 8 nodes.
+static void tet_voxel(const double h[3], double K[64], double M[64])
+{
+    static const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    for (int i = 0; i < 64; i++) { K[i] = 0.0; M[i] = 0.0; }
+    const double V = h[0] * h[1] * h[2] / 6.0;
+    for (int t = 0; t < 6; t++) {
+        int loc[4] = {0, 0, 0, 0}, bits = 0;
+        double g[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        for (int s = 0; s < 3; s++) {
+            const int ax = perm[t][s];
+            bits |= 1 << ax;
+            loc[s + 1] = bits;
+            g[s][ax] -= 1.0 / h[ax];          // lambda_s decreases along its axis
+            g[s + 1][ax] += 1.0 / h[ax];      // lambda_{s+1} increases
+        }
+        for (int i = 0; i < 4; i++)
+            for (int j = 0; j < 4; j++) {
+                K[loc[i] * 8 + loc[j]] += V * (g[i][0] * g[j][0] + g[i][1] * g[j][1] + g[i][2] * g[j][2]);
+                M[loc[i] * 8 + loc[j]] += V * (i == j ? 2.0 : 1.0) / 20.0;
+            }
+    }
+}
+
 static hf_status node_map(const hf_ctx *c, const double *p, CUtensorMap *m)
 {
     HFCK(get_encode());
@@ -409,10 +438,10 @@ struct StencilFn {
     size_t smem;
 };
 
-template <int R, int LD, int EP, int FL> static StencilFn stencil_fn_t()
+template <int R, int LD, int EP, int FL, int EL> static StencilFn stencil_fn_t()
 {
     constexpr int NS = ns_of<R, LD>();
-    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL>, StencilShape<R, NW, LD>::smem_bytes(NS)};
+    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL>, StencilShape<R, NW, LD>::smem_bytes(NS)};
 }
 
 // every (loader, epilogue, flags) variant the library launches, for tile heights R = 2 and 4
@@ -430,11 +459,13 @@ template <int R, int LD, int EP, int FL> static StencilFn stencil_fn_t()
     X(LD_RAW, EP_RESID, 0)                                                                      \
     X(LD_RAW, EP_RESID, FL_MASK | FL_DIR)
 
-static StencilFn stencil_fn(int R, int LD, int EP, int FL)
+static StencilFn stencil_fn(int R, int LD, int EP, int FL, int EL)
 {
 #define X(ld, ep, fl)                                                                           \
-    if (LD == (ld) && EP == (ep) && FL == (fl))                                                 \
-        return R >= 4 ? stencil_fn_t<4, ld, ep, fl>() : stencil_fn_t<2, ld, ep, fl>();
+    if (LD == (ld) && EP == (ep) && FL == (fl)) {                                               \
+        if (EL == EL_DENSE) return stencil_fn_t<2, ld, ep, fl, EL_DENSE>();                    \
+        return R >= 4 ? stencil_fn_t<4, ld, ep, fl, EL_Q1>() : stencil_fn_t<2, ld, ep, fl, EL_Q1>();       \
+    }
     HF_STENCIL_VARIANTS(X)
 #undef X
     return {nullptr, 0};
@@ -499,6 +530,11 @@ static StencilArgs base_args(hf_ctx *c, double aK, double aM)
     std::memset(&a, 0, sizeof(a));
     a.g = make_geom(c);
     a.lam = make_lam(c->g.h, aK, aM);
+    if (c->elem == EL_DENSE) {
+        double K[64], M[64];
+        tet_voxel(c->g.h, K, M);
+        for (int i = 0; i < 64; i++) { a.dn.K[i] = aK * K[i]; a.dn.M[i] = aM * M[i]; }
+    }
     a.c = 1.0;
     a.s = 0.0;
     a.z_out0 = c->own_lo;
@@ -525,7 +561,7 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
                                 Launch *out)
 {
     const int FL = dir_flags(c, EP, a.bvec != nullptr, dset);
-    StencilFn f = stencil_fn(c->tileR, LD, EP, FL);
+    StencilFn f = stencil_fn(c->tileR, LD, EP, FL, c->elem);
     if (!f.fn) return fail(HF_E_ARG, "internal: no stencil instantiation");
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
     dim3 grid;
@@ -666,23 +702,26 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     c->nloc = c->plane * c->nzl;
     c->kc_elems = (long long)g->ne[0] * g->ne[1] * (c->nzl + 1);
     const double hx = g->h[0], hy = g->h[1], hz = g->h[2];
-    c->Kd = (hy * hz / hx + hx * hz / hy + hx * hy / hz) / 9.0;
-    c->Md = hx * hy * hz / 27.0;
+    for (int l = 0; l < 8; l++) {     // Q1: the same for every local node
+        c->dg.Kd[l] = (hy * hz / hx + hx * hz / hy + hx * hy / hz) / 9.0;
+        c->dg.Md[l] = hx * hy * hz / 27.0;
+    }
     if (const char *e = getenv("HF_TILE_R")) c->tileR = atoi(e) >= 4 ? 4 : 2;
     if (const char *e = getenv("HF_ZCHUNK")) c->zchunk_env = std::max(0, atoi(e));
     if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e);
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
     // resident CTAs per SM of the CG stencil decide the z split of the grid
-    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0);
+    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem);
     HFCK(ensure_smem_attr(f.fn, f.smem, device));
     int occ = 0;
     CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
     c->occ = std::max(1, occ);
-    dim3 grid;
-    int chunk;
-    stencil_grid(c, c->own_lo, c->own_hi, &grid, &chunk);
-    c->max_blocks = std::max((int)(grid.x * grid.y * grid.z), b_blocks(c));
-    c->max_blocks = std::max(c->max_blocks, c->nsm * 4);
+    // partial-sum buffers sized for any tile height / z split (upper bound: one plane per CTA)
+    {
+        const long long tx = (c->nx1 + TILE_X - 1) / TILE_X, ty = (c->ny1 + rows_per_tile(2) - 1) / rows_per_tile(2);
+        const long long worst = tx * ty * std::max(1, c->own_hi - c->own_lo);
+        c->max_blocks = (int)std::max<long long>(worst, std::max(b_blocks(c), c->nsm * 4));
+    }
     CUCK(cudaMalloc(&c->launches, sizeof(unsigned long long)));
     CUCK(cudaMemsetAsync(c->launches, 0, sizeof(unsigned long long), c->stream));
     HFCK(sys_alloc(c, c->sys0, c->stream));
@@ -720,7 +759,7 @@ static hf_status enqueue_pack(hf_ctx *c, Sys &s, const double *k, const double *
 static hf_status enqueue_diag(hf_ctx *c, Sys &s, double aK, double aM, double *diag, double *invd)
 {
     const int bs = 256;
-    k_diag<<<(unsigned)((c->nloc + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), s.kc, aK, aM, c->Kd, c->Md,
+    k_diag<<<(unsigned)((c->nloc + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), s.kc, aK, aM, c->dg,
                                                                      diag, invd, c->launches);
     CUCK(cudaGetLastError());
     return HF_OK;
@@ -1015,6 +1054,7 @@ hf_status hf_face_load(hf_ctx *c, int face, double f_const, const double beam[4]
     a.oa = c->g.origin[a.ax]; a.ob = c->g.origin[a.bx];
     a.f_const = f_const;
     if (beam) { a.has_beam = 1; a.bP = beam[0]; a.bs = beam[1]; a.bca = beam[2]; a.bcb = beam[3]; }
+    a.tets = c->elem == EL_DENSE;
     a.F = dF;
     a.launches = c->launches;
     const long long n = (long long)a.na * a.nb;
@@ -1659,6 +1699,40 @@ hf_status hf_set_driver(hf_ctx *c, int32_t driver)
 {
     if (!c || driver < 0 || driver > 1) return fail(HF_E_ARG, "hf_set_driver: bad argument");
     c->driver = driver;
+    return HF_OK;
+}
+
+hf_status hf_set_element(hf_ctx *c, int32_t type)
+{
+    if (!c || type < 0 || type > 1) return fail(HF_E_ARG, "hf_set_element: type must be 0 (Q1) or 1 (6 P1 tets)");
+    CUCK(cudaSetDevice(c->device));
+    c->elem = type;
+    const double *h = c->g.h;
+    // the dense (tet) element keeps R = 2 tiles (R = 4 spills); TMA boxes follow the tile height
+    const int want_r = type == EL_DENSE ? 2 : (getenv("HF_TILE_R") && atoi(getenv("HF_TILE_R")) < 4 ? 2 : 4);
+    if (want_r != c->tileR) {
+        CUCK(cudaStreamSynchronize(c->stream));
+        c->tileR = want_r;
+        HFCK(sys_maps(c, c->sys0));
+        for (auto &p : c->pool) HFCK(sys_maps(c, *p));
+    }
+    if (type == EL_DENSE) {
+        double K[64], M[64];
+        tet_voxel(h, K, M);
+        for (int l = 0; l < 8; l++) { c->dg.Kd[l] = K[l * 9]; c->dg.Md[l] = M[l * 9]; }
+    } else {
+        for (int l = 0; l < 8; l++) {
+            c->dg.Kd[l] = (h[1] * h[2] / h[0] + h[0] * h[2] / h[1] + h[0] * h[1] / h[2]) / 9.0;
+            c->dg.Md[l] = h[0] * h[1] * h[2] / 27.0;
+        }
+    }
+    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem);
+    HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
+    int occ = 0;
+    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
+    c->occ = std::max(1, occ);
+    c->sys0.key_valid = false;
+    for (auto &p : c->pool) p->key_valid = false;
     return HF_OK;
 }
 

@@ -465,3 +465,49 @@ def test_slab_single_rank_nccl_and_local(transport):
     assert np.array_equal(N(u), ug)
     assert st2["total_iters"] == st["total_iters"]
     del ctx
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT row f1: the paper's element (6 P1 tets per voxel)
+
+@pytest.mark.parametrize("gname", ["1x1x1", "c1", "ragged", "seams"])
+def test_tet_apply_diag_load(gname):
+    g = GRIDS[gname]
+    k, c = synth.random_fields(g, seed=41)
+    o = oracle.Oracle(g, k, c, elem=1)
+    ctx = make_ctx(g, k, c)
+    hf.hf_set_element(ctx, 1)
+    u = synth.random_vector(g.n_nodes, seed=42)
+    y = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    for aK, aM in [(1.0, 0.0), (0.0, 1.0), (0.005, 1.0)]:
+        hf.hf_apply(ctx, aK, aM, T(u), y)
+        assert maxerr(N(y), o.spmv(aK, aM, u)) <= 1e-12, (gname, aK, aM)
+    d = torch.empty_like(y)
+    hf.hf_diag(ctx, 0.02, 1.0, d)
+    assert maxerr(N(d), o.diag(0.02, 1.0)) <= 1e-13
+    for face in (synth.FACE_ZM, synth.FACE_XP):
+        for fc, beam in [(1.0, None), (0.0, (10.0, 0.7, 0.5, 0.3))]:
+            hf.hf_face_load(ctx, face, fc, beam, y)
+            assert maxerr(N(y), o.face_load(face, fc, beam)) <= 1e-13, (face, fc)
+
+
+@pytest.mark.parametrize("driver", [0, 1])
+def test_tet_simulate_matches_oracle(driver):
+    g = synth.Grid((14, 11, 9), (0.3, 0.3, 0.25), (-2.0, -1.5, 0.0))
+    ids = synth.inclusion_ids(g, seed=43)
+    k, c = synth.ids_to_fields(ids)
+    p = synth.Problem("tet", g, k, c, np.zeros(g.n_nodes), theta=0.5, dt=0.02, nsteps=6,
+                      beam=(synth.BEAM_POWER, 1.5, 0.0, 0.0), dirichlet_bits=1 << synth.FACE_ZP,
+                      dirichlet_values=(0, 0, 0, 0, 0, 0.25))
+    ctx = make_ctx(g, k, c)
+    hf.hf_set_element(ctx, 1)
+    hf.hf_set_driver(ctx, driver)
+    hf.hf_set_dirichlet_faces(ctx, p.dirichlet_bits, p.dirichlet_values)
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
+    u = T(p.u0)
+    st = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, F, u, rtol=p.rtol)
+    o, Fo = oracle.problem_oracle(p, elem=1)
+    uo, sto, it, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
+    assert sto == 0 and st["steps_done"] == p.nsteps
+    assert rel(N(u), uo) <= 1e-10

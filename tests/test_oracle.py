@@ -326,3 +326,92 @@ def test_table2_grid_sizes(golden_dir):
 def test_paper_materials(golden_dir):
     rows = {r[0]: (float(r[1]), float(r[2])) for r in read_golden(f"{golden_dir}/materials.txt")}
     assert synth.STEEL == rows["steel"] and synth.OXIDE == rows["oxide"]
+
+
+# ---------------------------------------------------------------------------------------------
+# the paper's element (NEXT row f1): 6 Kuhn P1 tetrahedra per voxel
+
+def test_tet_voxel_unit_cube_closed_form():
+    """Row 0 of the voxel matrix of the 6-tet split of the unit cube: node 0 lies in all 6 tets
+    (diagonal 1), couples to its 3 edge neighbours with -1/3 and to nothing else in K."""
+    K, M = oracle.tet_voxel_matrices([1.0, 1.0, 1.0])
+    np.testing.assert_allclose(K[0], [1, -1 / 3, -1 / 3, 0, -1 / 3, 0, 0, 0], atol=1e-15)
+    np.testing.assert_allclose(K[7], [0, 0, 0, -1 / 3, 0, -1 / 3, -1 / 3, 1], atol=1e-15)
+    assert abs(M.sum() - 1.0) < 1e-15                          # six tets of volume 1/6
+    assert np.allclose(K, K.T) and np.abs(K.sum(1)).max() < 1e-15
+
+
+def test_tet_assembly_is_the_seven_point_laplacian():
+    """Classical result: P1 elements on the Kuhn (Freudenthal) triangulation of a cubic grid give
+    the 7-point finite-difference Laplacian times h (all diagonal-edge couplings cancel), while the
+    mass matrix keeps the 15-point pattern with interior row sums h^3."""
+    h = 0.5
+    g = synth.Grid((5, 5, 5), (h, h, h))
+    o = oracle.Oracle(g, np.ones(g.n_elems), np.ones(g.n_elems), elem=1)
+    K = o.csr(1.0, 0.0).toarray()
+    M = o.csr(0.0, 1.0).toarray()
+    n = g.nn[0]
+    i = 2 + n * (2 + n * 2)
+    nz = np.flatnonzero(np.abs(K[i]) > 1e-14)
+    expect = sorted([i, i - 1, i + 1, i - n, i + n, i - n * n, i + n * n])
+    assert list(nz) == expect
+    assert abs(K[i, i] - 6 * h) < 1e-14 and np.allclose(K[i, [i - 1, i + 1, i - n, i + n, i - n * n, i + n * n]], -h)
+    assert np.count_nonzero(np.abs(M[i]) > 1e-16) == 15
+    assert abs(M[i].sum() - h ** 3) < 1e-15
+
+
+def test_tet_patch_test_and_invariants():
+    g = synth.Grid((4, 5, 3), (0.3, 0.2, 0.7), (1.0, -2.0, 0.0))
+    k, c = synth.random_fields(g, seed=31)
+    o = oracle.Oracle(g, k, c, elem=1)
+    K = o.csr(1.0, 0.0).toarray()
+    M = o.csr(0.0, 1.0).toarray()
+    assert np.abs(K - K.T).max() <= 1e-13 * np.abs(K).max()
+    assert np.abs(K.sum(axis=1)).max() <= 1e-12 * np.abs(K).max()
+    vol = g.h[0] * g.h[1] * g.h[2]
+    assert abs(M.sum() - (c * vol).sum()) <= 1e-12 * (c * vol).sum()
+    assert np.linalg.eigvalsh(M).min() > 0
+    # linear fields are reproduced exactly by P1 (constant k): interior rows vanish
+    o1 = oracle.Oracle(g, np.full(g.n_elems, 3.0), np.ones(g.n_elems), elem=1)
+    x, y, z = g.node_coords()
+    u = (0.4 - 1.3 * x + 2.1 * y + 0.7 * z).ravel()
+    r = o1.spmv(1.0, 0.0, u).reshape(g.nn[::-1])
+    assert np.abs(r[1:-1, 1:-1, 1:-1]).max() <= 1e-12 * 3.0 * np.abs(u).max()
+    # EbE = assembled = per-row for the tet voxel matrices too
+    uu = synth.random_vector(g.n_nodes, 32)
+    y1 = o.spmv(0.01, 1.0, uu)
+    assert np.abs(o.apply_ebe(0.01, 1.0, uu) - y1).max() <= 1e-13 * np.abs(y1).max()
+    assert np.abs(o.apply_rows(0.01, 1.0, uu, np.arange(g.n_nodes)) - y1).max() <= 1e-13 * np.abs(y1).max()
+
+
+def test_tet_face_load():
+    g = synth.Grid((4, 3, 2), (0.5, 0.25, 1.0), (-1.0, 0.0, 0.0))
+    o = oracle.Oracle(g, np.ones(g.n_elems), np.ones(g.n_elems), assemble=False, elem=1)
+    F = o.face_load(synth.FACE_ZM, 2.0).reshape(g.nn[::-1])[0]
+    A = 0.5 * 0.25
+    # interior node: 6 triangles touch it (2 quads on the diagonal side x 2 + 2 singles): f A
+    assert abs(F[1, 1] - 2.0 * A) < 1e-15
+    # corner (0,0) lies on its quad's diagonal (2 triangles): f A / 3; corner (nx,0): 1 tri: f A/6
+    assert abs(F[0, 0] - 2.0 * A / 3) < 1e-15 and abs(F[0, -1] - 2.0 * A / 6) < 1e-15
+    for face in range(6):
+        Ff = o.face_load(face, 1.0)
+        d = face // 2
+        dims = [g.ne[a] * g.h[a] for a in range(3) if a != d]
+        assert abs(Ff.sum() - dims[0] * dims[1]) <= 1e-13
+    gb = synth.c5_grid(60)
+    ob = oracle.Oracle(gb, np.ones(gb.n_elems), np.ones(gb.n_elems), assemble=False, elem=1)
+    P, s = 10.0, 2.0
+    tot = ob.face_load(synth.FACE_ZM, 0.0, (P, s, 0.0, 0.0)).sum()
+    ex = P * math.erf(15 / (s * math.sqrt(2))) ** 2
+    assert abs(tot - ex) <= 1e-3 * ex
+
+
+def test_tet_time_stepper_matches_direct():
+    g = synth.Grid((6, 5, 4), (0.3, 0.3, 0.3))
+    k, c = synth.random_fields(g, seed=33)
+    o = oracle.Oracle(g, k, c, elem=1)
+    F = o.face_load(synth.FACE_ZM, 1.0)
+    u, st, it, _ = o.simulate(0.5, 0.05, 1, F, np.zeros(g.n_nodes), tol=1e-13)
+    A = o.csr(0.025, 1.0).tocsc()
+    xd = spla.spsolve(A, o.rhs(0.5, 0.05, F, np.zeros(g.n_nodes)))
+    assert st == 0 and np.linalg.norm(u - xd) <= 1e-10 * np.linalg.norm(xd)
