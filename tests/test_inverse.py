@@ -38,6 +38,20 @@ def test_observe_quantised_and_loglik_peaks_at_truth():
     assert np.isfinite(cam.loglik(data, field + 5.0))
 
 
+def test_loglik_matches_quadrature_of_the_gaussian_over_the_rounding_cell():
+    """log p(D|T) = sum_p log int_{D_p - q/2}^{D_p + q/2} N(t; T_p, sigma^2) dt,
+    checked pixel by pixel against numerical quadrature, incl. a datum 4 sigma in the tail."""
+    from scipy.integrate import quad
+    g, cam = _cam()
+    cam1 = inv.Camera(cam.nodes_x, cam.nodes_y, cam.x0, cam.x1, cam.y0, cam.y1, px=1, py=1, sub=2)
+    front = np.full((g.ne[1] + 1, g.ne[0] + 1), 0.0)
+    for T, D in ((20.0, 20.0), (20.0, 20.1), (20.03, 19.9), (20.0, 20.4), (20.0, 19.6)):
+        front[:] = T
+        dens = lambda t: np.exp(-0.5 * ((t - T) / 0.1) ** 2) / (0.1 * np.sqrt(2 * np.pi))
+        ref = np.log(quad(dens, D - 0.05, D + 0.05, epsabs=0, epsrel=1e-12)[0])
+        assert abs(cam1.loglik(np.array([[D]]), front) - ref) < 1e-9 * max(1.0, abs(ref))
+
+
 def test_metropolis_hastings_recovers_gaussian_posterior():
     rng = np.random.default_rng(1)
     mu, sd = 3.175, 0.2
