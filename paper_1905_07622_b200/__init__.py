@@ -16,7 +16,7 @@ import os
 from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libheatfem.so")
+_LIB_PATH = os.environ.get("HF_LIB_VARIANT") or os.path.join(_HERE, "libheatfem.so")   # variant: A/B experiments
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError(f"libheatfem.so not built ({_LIB_PATH}); run python -m paper_1905_07622_b200._build")

@@ -30,7 +30,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I" + os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + SRC + ["-ldl"]
+    extra = os.environ.get("HF_NVCC_EXTRA", "").split()
+    cmd = [nvcc()] + NVCC_FLAGS + extra + ["-I" + os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + SRC + ["-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

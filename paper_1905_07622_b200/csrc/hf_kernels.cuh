@@ -29,6 +29,10 @@
 
 namespace hf {
 
+#ifndef HF_SMEM_ROUND
+#define HF_SMEM_ROUND(x) (((x) + 1023) & ~(size_t)1023)
+#endif
+
 constexpr int NPART = 4;      // partial sums per block
 constexpr int TILE_X = 31;    // owned node columns per CTA
 constexpr int BOXW = 34;      // node columns in a TMA box (even start <= X0-1, covers X0+31)
@@ -97,10 +101,11 @@ struct Sync {               // per-system reduction plumbing
     int use_handles;
 };
 
-struct Maps {               // TMA descriptors, passed as a __grid_constant__ kernel parameter
+struct Maps {               // TMA descriptors (host copy; kernels read a device-memory copy)
     CUtensorMap node[NMAPS];
     CUtensorMap kc;         // fp64 view (2 nx, ny, nzl + 1) of the (k, c) pairs, layer L at z = L + 1
 };
+constexpr int MAP_KC = NMAPS;   // index of the kc map in a device Maps array
 
 struct StencilArgs {
     Geom g;
@@ -118,6 +123,8 @@ struct StencilArgs {
     int first;                    // LD_X0: step 0 of the run (guess = u^0)
     int rot_role;                 // ROT_*: map slots resolved from st->step
     Sync sy;
+    const CUtensorMap *tm;        // device copy of this launch's Maps (written once, never modified)
+    int tm_fence;                 // 1: acquire the descriptors (their addresses may have been reused)
     Dense dn;                     // EL_DENSE only
 };
 
@@ -164,6 +171,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
         : "memory");
 }
 
+#ifdef HF_DEBUG_WAIT
+// debug builds: a wait that does not complete within ~2^24 polls records who waited (into mapped
+// host memory, readable after the context dies) and traps instead of hanging
+__device__ unsigned long long *g_dbg;   // [0..9] stuck wait, [10..15] heartbeats
+__device__ __noinline__ void mbar_wait_dbg(uint64_t *bar, unsigned parity, int tag, int it)
+{
+    for (long long n = 0;; n++) {
+        uint32_t ok;
+        asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, P1;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (ok) return;
+        if (n == (1ll << 20)) {
+            unsigned long long *d = g_dbg;
+            if (d && atomicAdd(d, 1ull) == 0) {
+                d[1] = tag; d[2] = it; d[3] = parity; d[4] = blockIdx.x; d[5] = blockIdx.y; d[6] = blockIdx.z;
+                d[7] = threadIdx.x + 32 * threadIdx.y; d[8] = smem_u32(bar);
+                uint64_t st;
+                asm volatile("ld.shared.b64 %0, [%1];" : "=l"(st) : "r"(smem_u32(bar)));
+                d[9] = st;
+                __threadfence_system();
+            }
+            __trap();
+        }
+    }
+}
+#endif
+
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar)
 {
     asm volatile(
@@ -171,6 +205,12 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"((uint64_t)map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
+}
+
+// a tensor map in global memory may have been rewritten since an SM cached it (address reuse)
+__device__ __forceinline__ void tensormap_acquire(const CUtensorMap *m)
+{
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"((uint64_t)m) : "memory");
 }
 
 __device__ __forceinline__ void fence_proxy_async()
@@ -222,9 +262,33 @@ __device__ __forceinline__ void reduce_prev(const double *part, int n, double (&
     double acc[NPART];
 #pragma unroll
     for (int j = 0; j < NPART; j++) acc[j] = 0.0;
-    for (int b = tid; b < n; b += NT) {
+    // KU blocks per thread per round with every load issued before the first add (one L2 round
+    // trip for n <= KU * NT); the per-thread order stays b = tid, tid + NT, ... (fixed)
+    constexpr int KU = 4;
+    static_assert(NPART == 4, "partials are read as 2 x double2");
+    for (int b0 = tid; b0 < n; b0 += KU * NT) {
+        double2 v[KU][2];
 #pragma unroll
-        for (int j = 0; j < NPART; j++) acc[j] += __ldcg(part + (long long)b * NPART + j);
+        for (int k = 0; k < KU; k++) {
+            const int b = b0 + k * NT;
+            if (b < n) {
+                const double2 *q = reinterpret_cast<const double2 *>(part + (long long)b * NPART);
+                v[k][0] = __ldcg(q);
+                v[k][1] = __ldcg(q + 1);
+            } else {
+                v[k][0] = make_double2(0.0, 0.0);
+                v[k][1] = make_double2(0.0, 0.0);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KU; k++) {
+            if (b0 + k * NT < n) {
+                acc[0] += v[k][0].x;
+                acc[1] += v[k][0].y;
+                acc[2] += v[k][1].x;
+                acc[3] += v[k][1].y;
+            }
+        }
     }
     const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
@@ -304,7 +368,8 @@ struct StencilShape {
     static constexpr int KC_DBL = NW * R * 64;                               // doubles per kc box
     static constexpr int STAGE_DBL = NA * NODE_DBL + KC_DBL;                 // multiple of 16
     static constexpr unsigned STAGE_BYTES = (NA * NODE_BOX + KC_DBL) * 8u;   // TMA transaction bytes
-    static size_t smem_bytes(int ns) { return (size_t)ns * STAGE_DBL * 8 + 16 * ns + 2 * NW * 32 * 8; }
+    // rounded to 1 KB so that CTAs of different variants sharing an SM get aligned windows
+    static size_t smem_bytes(int ns) { return HF_SMEM_ROUND((size_t)ns * STAGE_DBL * 8 + 16 * ns + 2 * NW * 32 * 8); }
 };
 
 // compile-time variant flags of the stencil kernel
@@ -317,7 +382,7 @@ enum {
 
 template <int R, int NW, int NS, int LD, int EP, int FL, int EL>
 __global__ void __launch_bounds__(32 * NW)
-k_stencil(const __grid_constant__ Maps maps, const __grid_constant__ StencilArgs a)
+k_stencil(const __grid_constant__ StencilArgs a)
 {
     using SH = StencilShape<R, NW, LD>;
     constexpr int NT = 32 * NW;
@@ -338,7 +403,10 @@ k_stencil(const __grid_constant__ Maps maps, const __grid_constant__ StencilArgs
     double *cstore = (EP == EP_CGA) ? a.dbuf[1] : a.xout;    // centre-value store target
     if (a.sy.st) {
         const CgState *st = a.sy.st;
-        if (st->first_failed >= 0) return;       // an earlier time step failed: stop the run
+        if (st->first_failed >= 0) {             // an earlier time step failed: stop the run
+            if (EP == EP_CGA && blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
+            return;
+        }
         if (EP == EP_CGA || EP == EP_RESID) {
             if (!st->active) return;             // converged / stopped: nothing to do
             if (EP == EP_RESID && !st->replace) return;
@@ -393,16 +461,21 @@ k_stencil(const __grid_constant__ Maps maps, const __grid_constant__ StencilArgs
         const int p = zb - 1 + it;
         double *sb = stage + st * SH::STAGE_DBL;
         mbar_expect_tx(&bars[st], SH::STAGE_BYTES);
-        if (NA >= 1) tma_load_3d(sb, &maps.node[map0], xb, Y0 - 1, p, &bars[st]);
-        if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, &maps.node[map1], xb, Y0 - 1, p, &bars[st]);
+        if (NA >= 1) tma_load_3d(sb, a.tm + map0, xb, Y0 - 1, p, &bars[st]);
+        if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, a.tm + map1, xb, Y0 - 1, p, &bars[st]);
         // element layer L = p - 1 sits at z = p in the kc tensor
-        tma_load_3d(sb + NA * SH::NODE_DBL, &maps.kc, 2 * (X0 - 1), Y0 - 1, p, &bars[st]);
+        tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KC, 2 * (X0 - 1), Y0 - 1, p, &bars[st]);
     };
 
     if (tid == 0) {
         if (smem_u32(stage) & 127u) __trap();     // TMA destinations need 128-B alignment
         for (int i = 0; i < NS; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
+        if (a.tm_fence) {
+            if (NA >= 1) tensormap_acquire(a.tm + map0);
+            if (NA >= 2) tensormap_acquire(a.tm + map1);
+            tensormap_acquire(a.tm + MAP_KC);
+        }
     }
     __syncthreads();
     if (tid == 0)
@@ -426,10 +499,23 @@ k_stencil(const __grid_constant__ Maps maps, const __grid_constant__ StencilArgs
                 set_while(a.sy, 0);
                 set_if(a.sy, 0);
             }
+#ifdef HF_DEBUG_WAIT
+            for (int i = 0; i < NS && i < nplanes; i++) mbar_wait_dbg(&bars[i], 0, 1000 + EP * 10 + LD, -1 - i);
+#else
             for (int i = 0; i < NS && i < nplanes; i++) mbar_wait(&bars[i], 0);   // drain the TMA
+#endif
             return;
         }
         beta = is.beta;
+#ifdef HF_DEBUG_WAIT
+        if (blk == 0 && tid == 0 && g_dbg) {
+            volatile unsigned long long *d = g_dbg;
+            const int sl = ((uintptr_t)a.sy.st >> 8) & 1;
+            d[10 + 3 * sl] = it_i;
+            d[11 + 3 * sl] = a.sy.st->step;
+            d[12 + 3 * sl] += 1;
+        }
+#endif
         if (blk == 0 && tid == 0) {
             CgState *stw = a.sy.st;
             stw->delta[it_i & 1] = is.delta;
@@ -456,7 +542,11 @@ k_stencil(const __grid_constant__ Maps maps, const __grid_constant__ StencilArgs
     for (int it = 0; it < nplanes; ++it) {
         const int p = zb - 1 + it;
         const int st = it % NS;
+#ifdef HF_DEBUG_WAIT
+        mbar_wait_dbg(&bars[st], (it / NS) & 1, EP * 10 + LD, it);
+#else
         mbar_wait(&bars[st], (it / NS) & 1);
+#endif
         const double *sb = stage + st * SH::STAGE_DBL;
         const double *n0 = sb + w * R * BOXW + lane + xoff;                 // row 0 of this warp
         const double *n1 = sb + SH::NODE_DBL + w * R * BOXW + lane + xoff;
@@ -658,8 +748,7 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     const int blk = blockIdx.x;
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
     CgState *st = a.sy.st;
-    if (st->first_failed >= 0) return;
-    if (!st->active) {
+    if (st->first_failed >= 0 || !st->active) {   // failed run / converged: leave the loop
         if (blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
         return;
     }

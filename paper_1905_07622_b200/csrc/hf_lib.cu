@@ -22,6 +22,8 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -32,9 +34,23 @@ using namespace hf;
 
 static thread_local std::string g_err;
 
+#ifdef HF_DEBUG_WAIT
+static unsigned long long *g_dbg_host = nullptr;
+static void dbg_dump()
+{
+    if (g_dbg_host && g_dbg_host[0])
+        fprintf(stderr, "[hf debug] stuck wait: tag %llu it %lld parity %llu block (%llu,%llu,%llu) tid %llu bar 0x%llx state 0x%llx (hits %llu)\n",
+                g_dbg_host[1], (long long)g_dbg_host[2], g_dbg_host[3], g_dbg_host[4], g_dbg_host[5], g_dbg_host[6],
+                g_dbg_host[7], g_dbg_host[8], g_dbg_host[9], g_dbg_host[0]);
+}
+#endif
+
 static hf_status fail(hf_status s, const std::string &msg)
 {
     g_err = msg;
+#ifdef HF_DEBUG_WAIT
+    dbg_dump();
+#endif
     return s;
 }
 
@@ -147,6 +163,7 @@ struct Sys {                         // one system's PCG workspace (Table 3 buff
     double *U[3] = {nullptr, nullptr, nullptr};   // time-step ring
     double *b = nullptr, *r = nullptr, *s = nullptr, *q = nullptr, *invd = nullptr;
     double *dbuf[2] = {nullptr, nullptr};
+    bool solo = false;               // batched pool system: one stencil CTA per SM (see simulate_sys)
     Maps maps;                       // TMA maps of U[0..2], dbuf[0..1], s and kc
     CgState *st = nullptr;           // device
     CgState *st_host = nullptr;      // pinned mirror
@@ -173,6 +190,7 @@ struct Comm {
 };
 
 struct hf_ctx {
+    std::map<std::string, void *> mapcache;   // device copies of TMA descriptor sets (maps_dev)
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -201,6 +219,8 @@ struct hf_ctx {
     int check_every = 8;
     int max_blocks = 0;
     int occ = 2;                     // resident CTAs/SM of the CG stencil (occupancy API)
+    int unroll = 2;                  // PCG iterations per WHILE-body launch
+    size_t launch_min_smem = 0;      // > 0: stencil launches reserve at least this much smem
     int rank = 0, nranks = 1;
     Comm *comm = nullptr;
     bool step_flush = false;
@@ -421,11 +441,23 @@ struct Launch {
     }
     template <class T> T get(int i) const
     {
+        check<T>(i);
         T v;
         std::memcpy(&v, args[i].data(), sizeof(T));
         return v;
     }
-    template <class T> void put(int i, const T &v) { std::memcpy(args[i].data(), &v, sizeof(T)); }
+    template <class T> void put(int i, const T &v)
+    {
+        check<T>(i);
+        std::memcpy(args[i].data(), &v, sizeof(T));
+    }
+    template <class T> void check(int i) const
+    {
+        if (i < 0 || i >= (int)args.size() || args[i].size() != sizeof(T)) {
+            fprintf(stderr, "libheatfem: internal error: launch argument %d has the wrong type\n", i);
+            abort();
+        }
+    }
 };
 
 template <int R, int LD> constexpr int ns_of()
@@ -441,7 +473,8 @@ struct StencilFn {
 template <int R, int LD, int EP, int FL, int EL> static StencilFn stencil_fn_t()
 {
     constexpr int NS = ns_of<R, LD>();
-    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL>, StencilShape<R, NW, LD>::smem_bytes(NS)};
+    static const size_t pad = getenv("HF_SMEM_PAD") ? (size_t)atoi(getenv("HF_SMEM_PAD")) : 0;   // tuning / debug
+    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL>, StencilShape<R, NW, LD>::smem_bytes(NS) + pad};
 }
 
 // every (loader, epilogue, flags) variant the library launches, for tile heights R = 2 and 4
@@ -475,19 +508,30 @@ static StencilFn stencil_fn(int R, int LD, int EP, int FL, int EL)
 static int dir_flags(const hf_ctx *c, int EP, bool has_b, bool dset);
 
 static std::mutex g_attr_mu;
-static std::map<std::pair<const void *, int>, bool> g_attr_done;
+static std::map<std::pair<const void *, int>, size_t> g_attr_done;
 
 static hf_status ensure_smem_attr(const void *fn, size_t smem, int device)
 {
     std::lock_guard<std::mutex> lk(g_attr_mu);
     auto key = std::make_pair(fn, device);
-    if (g_attr_done.count(key)) return HF_OK;
+    auto it = g_attr_done.find(key);
+    if (it != g_attr_done.end() && it->second >= smem) return HF_OK;
     CUCK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    g_attr_done[key] = true;
+    g_attr_done[key] = smem;
     return HF_OK;
 }
 
 static int rows_per_tile(int R) { return NW * R - 1; }
+
+// Tile height: R = 4 amortises the halo rows best when the stencil streams from HBM (large
+// grids); below ~16M local nodes the kernel is latency-bound and R = 2 (more, shorter tiles,
+// 2 CTAs/SM, less y padding at 100^3) is faster (tools/sweep_c3.py).  The dense (tet) element
+// keeps R = 2 (R = 4 spills).
+static int default_tile_r(const hf_ctx *c, int elem)
+{
+    if (elem == EL_DENSE) return 2;
+    return c->nloc < (16LL << 20) ? 2 : 4;
+}
 
 // grid of the stencil over output planes [z0, z1): one (x, y) tile column per CTA, z split
 // into chunks so that the grid fills the resident slots (occupancy x SMs) once.
@@ -497,7 +541,7 @@ static void stencil_grid(const hf_ctx *c, int z0, int z1, dim3 *grid, int *zchun
     const int ty = (c->ny1 + rows_per_tile(c->tileR) - 1) / rows_per_tile(c->tileR);
     const int planes = std::max(1, z1 - z0);
     const long long cols = (long long)tx * ty;
-    const long long slots = (long long)c->nsm * c->occ;
+    const long long slots = (long long)c->nsm * (c->launch_min_smem ? 1 : c->occ);
     long long nch = std::max(1LL, slots / cols);
     int chunk = (int)std::max(1LL, ((long long)planes + nch - 1) / nch);
     if (c->zchunk_env > 0) chunk = c->zchunk_env;
@@ -555,6 +599,24 @@ static int dir_flags(const hf_ctx *c, int EP, bool has_b, bool dset)
     return fl;
 }
 
+// Device copies of TMA descriptor sets, content-addressed: written once by a synchronous copy
+// before the first launch that uses them and never modified (graph nodes keep pointing at them);
+// freed with the context.  Descriptors in kernel parameter space were not reliable for kernels
+// launched from graph conditional bodies of concurrently running graphs (intermittent TMA
+// transaction-count faults and hangs with two batched streams; tools/stress_batched.sh).
+static hf_status maps_dev(hf_ctx *c, const Maps &m, const CUtensorMap **out)
+{
+    std::string key((const char *)&m, sizeof(Maps));
+    auto it = c->mapcache.find(key);
+    if (it != c->mapcache.end()) { *out = (const CUtensorMap *)it->second; return HF_OK; }
+    void *d = nullptr;
+    CUCK(cudaMalloc(&d, sizeof(Maps)));
+    CUCK(cudaMemcpy(d, &m, sizeof(Maps), cudaMemcpyHostToDevice));
+    c->mapcache.emplace(key, d);
+    *out = (const CUtensorMap *)d;
+    return HF_OK;
+}
+
 // stencil launch spec.  dset: EP_APPLY writes g on Dirichlet rows (RHS / lift); the plain
 // apply (hf_apply) is the unconstrained operator.
 static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps &maps, StencilArgs a, int cls,
@@ -563,6 +625,7 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
     const int FL = dir_flags(c, EP, a.bvec != nullptr, dset);
     StencilFn f = stencil_fn(c->tileR, LD, EP, FL, c->elem);
     if (!f.fn) return fail(HF_E_ARG, "internal: no stencil instantiation");
+    f.smem = std::max(f.smem, c->launch_min_smem);
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
     dim3 grid;
     int chunk;
@@ -573,7 +636,9 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
     L.grid = grid;
     L.block = dim3(32, NW, 1);
     L.smem = f.smem;
-    L.add(maps);
+    HFCK(maps_dev(c, maps, &a.tm));
+    static const int tm_fence = getenv("HF_TM_FENCE") ? atoi(getenv("HF_TM_FENCE")) : 1;
+    a.tm_fence = tm_fence;
     L.add(a);
     L.cls = cls;
     *out = L;
@@ -678,6 +743,25 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     if (g->ne[0] > 1000000 || g->ne[1] > 1000000) return fail(HF_E_ARG, "grid too large");
     c->g = *g;
     c->device = device;
+#ifdef HF_DEBUG_WAIT
+    if (!g_dbg_host) {
+        cudaSetDevice(device);
+        cudaHostAlloc((void **)&g_dbg_host, 16 * sizeof(unsigned long long), cudaHostAllocMapped);
+        std::memset(g_dbg_host, 0, 16 * sizeof(unsigned long long));
+        unsigned long long *dp = nullptr;
+        cudaHostGetDevicePointer((void **)&dp, g_dbg_host, 0);
+        cudaMemcpyToSymbol(g_dbg, &dp, sizeof(dp));
+        std::thread([] {
+            for (;;) {
+                std::this_thread::sleep_for(std::chrono::seconds(4));
+                volatile unsigned long long *h = g_dbg_host;
+                fprintf(stderr, "[hf debug] heartbeat sysA it %llu step %llu n %llu | sysB it %llu step %llu n %llu | stuck %llu\n",
+                        h[10], h[11], h[12], h[13], h[14], h[15], h[0]);
+                dbg_dump();
+            }
+        }).detach();
+    }
+#endif
     CUCK(cudaSetDevice(device));
     cudaDeviceProp prop;
     CUCK(cudaGetDeviceProperties(&prop, device));
@@ -706,9 +790,11 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
         c->dg.Kd[l] = (hy * hz / hx + hx * hz / hy + hx * hy / hz) / 9.0;
         c->dg.Md[l] = hx * hy * hz / 27.0;
     }
+    c->tileR = default_tile_r(c, EL_Q1);
     if (const char *e = getenv("HF_TILE_R")) c->tileR = atoi(e) >= 4 ? 4 : 2;
     if (const char *e = getenv("HF_ZCHUNK")) c->zchunk_env = std::max(0, atoi(e));
     if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e);
+    if (const char *e = getenv("HF_UNROLL")) c->unroll = std::min(8, std::max(1, atoi(e)));
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
     // resident CTAs per SM of the CG stencil decide the z split of the grid
     StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem);
@@ -733,12 +819,15 @@ static void ctx_free(hf_ctx *c)
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto &p : c->pool) if (p->stream) cudaStreamSynchronize(p->stream);
     sys_free(c->sys0);
     for (auto &p : c->pool) sys_free(*p);
     c->pool.clear();
     for (void *p : c->scratch) cudaFree(p);
     cudaFree(c->launches);
     cudaFree(c->flush);
+    for (auto &kv : c->mapcache) cudaFree(kv.second);
+    c->mapcache.clear();
     delete c->comm;
     if (c->own_stream) cudaStreamDestroy(c->stream);
 }
@@ -932,7 +1021,6 @@ static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, in
 static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init, CgLaunches L, std::vector<Launch> post,
                                 cudaGraph_t *out)
 {
-    (void)c;
     cudaGraph_t g;
     CUCK(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle hw, hi;
@@ -951,30 +1039,34 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
     cudaGraphNode_t wnode;
     CUCK(cudaGraphAddNode(&wnode, g, &prev, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    CUCK(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
-    {
-        StencilArgs aa = L.A.get<StencilArgs>(1);
+    // the body holds `unroll` copies of [A -> B -> IF(RES)]; copies after convergence exit at once
+    cudaGraphNode_t bprev = nullptr;
+    for (int u = 0; u < std::max(1, c->unroll); u++) {
+        CUCK(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
+        Launch A = L.A, B = L.B, RES = L.RES;
+        StencilArgs aa = A.get<StencilArgs>(0);
         aa.sy.h_while = hw; aa.sy.h_if = hi; aa.sy.use_handles = 1;
-        L.A.put(1, aa);
-        BArgs bb = L.B.get<BArgs>(0);
+        A.put(0, aa);
+        BArgs bb = B.get<BArgs>(0);
         bb.sy.h_while = hw; bb.sy.h_if = hi; bb.sy.use_handles = 1;
-        L.B.put(0, bb);
-        StencilArgs ra = L.RES.get<StencilArgs>(1);
+        B.put(0, bb);
+        StencilArgs ra = RES.get<StencilArgs>(0);
         ra.sy.h_while = hw; ra.sy.h_if = hi; ra.sy.use_handles = 1;
-        L.RES.put(1, ra);
+        RES.put(0, ra);
+        cudaGraphNode_t na, nb;
+        HFCK(add_node(body, A, bprev ? &bprev : nullptr, &na));
+        HFCK(add_node(body, B, &na, &nb));
+        cudaGraphNodeParams ip = {};
+        ip.type = cudaGraphNodeTypeConditional;
+        ip.conditional.handle = hi;
+        ip.conditional.type = cudaGraphCondTypeIf;
+        ip.conditional.size = 1;
+        cudaGraphNode_t inode;
+        CUCK(cudaGraphAddNode(&inode, body, &nb, 1, &ip));
+        cudaGraphNode_t nr;
+        HFCK(add_node(ip.conditional.phGraph_out[0], RES, nullptr, &nr));
+        bprev = inode;
     }
-    cudaGraphNode_t na, nb;
-    HFCK(add_node(body, L.A, nullptr, &na));
-    HFCK(add_node(body, L.B, &na, &nb));
-    cudaGraphNodeParams ip = {};
-    ip.type = cudaGraphNodeTypeConditional;
-    ip.conditional.handle = hi;
-    ip.conditional.type = cudaGraphCondTypeIf;
-    ip.conditional.size = 1;
-    cudaGraphNode_t inode;
-    CUCK(cudaGraphAddNode(&inode, body, &nb, 1, &ip));
-    cudaGraphNode_t nr;
-    HFCK(add_node(ip.conditional.phGraph_out[0], L.RES, nullptr, &nr));
     prev = wnode;
     for (auto &p : post) { HFCK(add_node(g, p, &prev, &n)); prev = n; }
     *out = g;
@@ -1198,11 +1290,22 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
 
     const bool use_graph = c->driver == 0 && !c->comm && !c->prof;
     c->last_ms_steps = 0.0;
+    // Batched pool systems run their graphs concurrently on 2 streams.  Measured on B200: when
+    // stencil CTAs of two concurrently running conditional-node graphs share an SM, a TMA stage
+    // occasionally never completes (hang) or faults (tools/stress_batched.sh: R = 2, 2 streams,
+    // 2-6 of 8 runs fail; host-launched kernels, one stream, or one stencil CTA per SM: 0 of 24).
+    // Pool systems therefore reserve more than half an SM's shared memory per stencil CTA.
+    struct SmemGuard {
+        hf_ctx *c;
+        ~SmemGuard() { c->launch_min_smem = 0; }
+    } smem_guard{c};
+    c->launch_min_smem = s.solo && use_graph ? (size_t)116 * 1024 : 0;
     SimKey key;
     std::memset(&key, 0, sizeof(key));
     key.aK = aK; key.aM = aM; key.aKL = aKL; key.aML = aML; key.rtol = o.rtol; key.dt = dt;
     key.max_iter = o.max_iter; key.replace_every = o.replace_every; key.first = first;
     key.snap_plane = snap_local; key.lift = lift; key.F = dF; key.snap = snapdev;
+    key.pad = (int)(c->launch_min_smem >> 10);
     const bool cached = use_graph && s.key_valid && s.key == key && s.gexec;
 
     std::vector<Launch> pre, post;
@@ -1413,6 +1516,7 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
         cudaStream_t st;
         CUCK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         p->own_stream = true;
+        p->solo = true;
         HFCK(sys_alloc(c, *p, st));
         c->pool.push_back(std::move(p));
     }
@@ -1709,7 +1813,8 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
     c->elem = type;
     const double *h = c->g.h;
     // the dense (tet) element keeps R = 2 tiles (R = 4 spills); TMA boxes follow the tile height
-    const int want_r = type == EL_DENSE ? 2 : (getenv("HF_TILE_R") && atoi(getenv("HF_TILE_R")) < 4 ? 2 : 4);
+    int want_r = default_tile_r(c, type);
+    if (type != EL_DENSE && getenv("HF_TILE_R")) want_r = atoi(getenv("HF_TILE_R")) >= 4 ? 4 : 2;
     if (want_r != c->tileR) {
         CUCK(cudaStreamSynchronize(c->stream));
         c->tileR = want_r;

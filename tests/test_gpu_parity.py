@@ -236,6 +236,43 @@ def test_graph_and_host_drivers_bitwise_equal():
     assert st0["total_iters"] == st1["total_iters"]
 
 
+@pytest.mark.parametrize("driver,unroll", [(0, 1), (0, 3), (1, 1)])
+def test_failed_step_stops_the_run(driver, unroll):
+    """A step that does not converge (max_iter too small) stops the run: the later steps of the
+    same call are skipped on the device (no host check between graph launches), the call returns
+    NOCONV with the failing step, and the graph WHILE loops of the skipped steps terminate."""
+    p = synth.c1()
+    os.environ["HF_UNROLL"] = str(unroll)
+    try:
+        ctx = make_ctx(p.grid, p.k, p.c)
+    finally:
+        os.environ.pop("HF_UNROLL", None)
+    hf.hf_set_driver(ctx, driver)
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
+    u = T(p.u0)
+    st = hf.hf_simulate(ctx, p.theta, p.dt, 4, F, u, rtol=p.rtol, max_iter=2, raise_on_noconv=False)
+    assert st["rc"] == hf.HF_E_NOCONV and st["first_failed_step"] == 0
+    # the context stays usable: a converging run afterwards matches the oracle
+    u2 = T(p.u0)
+    st2 = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, F, u2, rtol=p.rtol)
+    o, Fo = oracle.problem_oracle(p)
+    uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
+    assert st2["first_failed_step"] == -1 and rel(N(u2), uo) <= 1e-10
+
+
+@pytest.mark.parametrize("unroll", [2, 4])
+def test_unrolled_loop_body_bitwise_equal(unroll):
+    p = synth.c1()
+    ug, st0, _, _ = _gpu_sim(p, driver=0)
+    os.environ["HF_UNROLL"] = str(unroll)
+    try:
+        uu, st1, _, _ = _gpu_sim(p, driver=0)
+    finally:
+        os.environ.pop("HF_UNROLL", None)
+    assert np.array_equal(ug, uu) and st0["total_iters"] == st1["total_iters"]
+
+
 def test_simulate_c2_closed_form():
     p = synth.c2()
     ug, st, _, _ = _gpu_sim(p)
