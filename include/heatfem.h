@@ -119,6 +119,15 @@ hf_status hf_set_dirichlet_faces(hf_ctx *ctx, uint32_t face_bits, const double v
  * Errors: HF_E_ARG. */
 hf_status hf_set_element(hf_ctx *ctx, int32_t type);
 
+/* Storage precision of the context's node vectors and (k, c) pairs: 64 (default) or 32, the
+ * fp32 variant (NEXT row f3; the paper also ran single precision).  With 32 the
+ * operator, the vector updates and the face load run in fp32 while every dot product, the PCG
+ * scalars and the stop test stay fp64; the ABI's vectors stay fp64 (converted at the boundary).
+ * Parity bar of the variant: rel-L2 <= 1e-5 against the fp64 oracle (north_star), reached with
+ * rtol around 1e-6.  Must be called before hf_set_coefficients; reallocates the workspaces.
+ * Errors: HF_E_ARG (bits not 32/64), HF_E_STATE (coefficients already set). */
+hf_status hf_set_precision(hf_ctx *ctx, int32_t bits);
+
 /* Flux load F_i = int_face f phi_i ds over face `face` (0..5) (P:44, P:50-52 boundary term):
  * f = f_const + beam, beam(a,b) = P/(2 pi s^2) exp(-((a-ca)^2 + (b-cb)^2) / (2 s^2)) with
  * beam = {P, s, ca, cb} (or NULL), (a, b) the face's in-plane coordinates in increasing axis

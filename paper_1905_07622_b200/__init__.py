@@ -82,6 +82,7 @@ _SIGS = {
     "hf_flush_l2": (_i32, [_vp]),
     "hf_set_step_flush": (_i32, [_vp, _i32]),
     "hf_set_element": (_i32, [_vp, _i32]),
+    "hf_set_precision": (_i32, [_vp, _i32]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -348,6 +349,11 @@ def hf_set_driver(ctx: Context, driver: int):
 
 def hf_flush_l2(ctx: Context):
     _check(_lib.hf_flush_l2(ctx.ptr))
+
+
+def hf_set_precision(ctx: Context, bits: int):
+    """64 (default) or 32: storage precision of the context (fp32 variant, NEXT row f3)."""
+    _check(_lib.hf_set_precision(ctx.ptr, bits))
 
 
 def hf_set_element(ctx: Context, elem_type: int):

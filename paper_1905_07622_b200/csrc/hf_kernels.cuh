@@ -35,7 +35,7 @@ namespace hf {
 
 constexpr int NPART = 4;      // partial sums per block
 constexpr int TILE_X = 31;    // owned node columns per CTA
-constexpr int BOXW = 34;      // node columns in a TMA box (even start <= X0-1, covers X0+31)
+constexpr int BOXW = 34;      // fp64 node columns in a TMA box (even start <= X0-1, covers X0+31)
 constexpr int NMAPS = 6;      // node tensor maps: ring U[0..2], d[0..1], s
 
 enum { LD_RAW = 0, LD_GT = 1, LD_CGD = 2, LD_X0 = 3 };
@@ -69,9 +69,10 @@ struct CgState {
 struct Geom {
     int nx1, ny1, nzl;      // nodes in x, y; local node planes
     int zg0, nz1g;          // global index of local plane 0; global node planes
-    int pitch;              // node row pitch (nx1 rounded up to even: TMA needs 16-B strides)
+    int pitch;              // node row pitch (nx1 rounded up to 16 B: TMA strides)
     long long plane;        // pitch * ny1
     int nx, ny;             // elements in x, y
+    int kpitch;             // (k, c) pairs per coefficient row (nx, or nx rounded up to even in fp32)
     unsigned dbits;         // Dirichlet face bits (R3)
     double gval[6];
 };
@@ -82,12 +83,24 @@ struct Geom {
 struct Lam {
     double ka[4], ma[4], kb[4], mb[4];
 };
+struct LamF {               // the same constants for the fp32 storage variant (NEXT row f3)
+    float ka[4], ma[4], kb[4], mb[4];
+};
 
 // Dense voxel matrices (element variant EL_DENSE: the paper's 6-tet split, NEXT row f1):
 // y_e = (k_e Ks + c_e Ms) u_e with Ks = aK K_ref, Ms = aM M_ref (8 x 8, local l = bx+2by+4bz).
 struct Dense {
     double K[64], M[64];
 };
+struct DenseF {
+    float K[64], M[64];
+};
+
+// storage / arithmetic type of the node vectors and (k, c) pairs: double (default) or float
+// (NEXT row f3).  Reductions, PCG scalars and the CG state stay fp64 in both.
+template <class Real> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
 
 enum { EL_Q1 = 0, EL_DENSE = 1 };
 
@@ -125,8 +138,12 @@ struct StencilArgs {
     Sync sy;
     const CUtensorMap *tm;        // device copy of this launch's Maps (written once, never modified)
     int tm_fence;                 // 1: acquire the descriptors (their addresses may have been reused)
+    LamF lamf;                    // fp32 variant: lam in float
     Dense dn;                     // EL_DENSE only
+    DenseF dnf;                   // EL_DENSE, fp32 variant
 };
+// Node-vector pointers of StencilArgs / BArgs / StepArgs are declared double* but address
+// vectors of the context's storage type; kernels instantiated for Real = float reinterpret them.
 
 __device__ __forceinline__ bool is_dirichlet(const Geom &g, int x, int y, int zl, double &val)
 {
@@ -359,17 +376,22 @@ __device__ __forceinline__ IterStart iter_start(const CgState *st, int i, const 
 
 // ---- the stencil kernel (operator apply with fused prologue/epilogue) ---------------------
 
-template <int R, int NW, int LD>
+template <int R, int NW, int LD, class Real = double>
 struct StencilShape {
+    static constexpr int ES = (int)sizeof(Real);
     static constexpr int H = NW * R + 1;                                     // node rows per box
     static constexpr int NA = LD == LD_RAW ? 1 : (LD == LD_GT ? 0 : 2);      // node arrays per plane
-    static constexpr int NODE_BOX = H * BOXW;                                // doubles per node box
-    static constexpr int NODE_DBL = (NODE_BOX + 15) / 16 * 16;               // 128-B aligned slot
-    static constexpr int KC_DBL = NW * R * 64;                               // doubles per kc box
-    static constexpr int STAGE_DBL = NA * NODE_DBL + KC_DBL;                 // multiple of 16
-    static constexpr unsigned STAGE_BYTES = (NA * NODE_BOX + KC_DBL) * 8u;   // TMA transaction bytes
+    // box widths: the x origin must be 16-B aligned, so it starts up to 16/ES - 1 columns early
+    static constexpr int BW = ES == 8 ? BOXW : 36;                           // node columns per box
+    static constexpr int KW = ES == 8 ? 64 : 68;                             // kc values per box row
+    static constexpr int AL = 128 / ES;                                      // elements per 128 B
+    static constexpr int NODE_BOX = H * BW;                                  // elements per node box
+    static constexpr int NODE_DBL = (NODE_BOX + AL - 1) / AL * AL;           // 128-B aligned slot
+    static constexpr int KC_DBL = NW * R * KW;                               // elements per kc box
+    static constexpr int STAGE_DBL = (NA * NODE_DBL + KC_DBL + AL - 1) / AL * AL;
+    static constexpr unsigned STAGE_BYTES = (NA * NODE_BOX + KC_DBL) * (unsigned)ES;   // TMA bytes
     // rounded to 1 KB so that CTAs of different variants sharing an SM get aligned windows
-    static size_t smem_bytes(int ns) { return HF_SMEM_ROUND((size_t)ns * STAGE_DBL * 8 + 16 * ns + 2 * NW * 32 * 8); }
+    static size_t smem_bytes(int ns) { return HF_SMEM_ROUND((size_t)ns * STAGE_DBL * ES + 16 * ns + 2 * NW * 32 * ES); }
 };
 
 // compile-time variant flags of the stencil kernel
@@ -380,16 +402,29 @@ enum {
     FL_DSET = 8,   // EP_APPLY with FL_DIR: y_D = g (else y_D = u_D, identity rows)
 };
 
-template <int R, int NW, int NS, int LD, int EP, int FL, int EL>
+template <int R, int NW, int NS, int LD, int EP, int FL, int EL, class Real>
 __global__ void __launch_bounds__(32 * NW)
 k_stencil(const __grid_constant__ StencilArgs a)
 {
-    using SH = StencilShape<R, NW, LD>;
+    using SH = StencilShape<R, NW, LD, Real>;
+    using V2 = typename Vec2<Real>::type;
+    constexpr int ES = (int)sizeof(Real);
     constexpr int NT = 32 * NW;
     constexpr int NA = SH::NA;
     constexpr bool MASK = (FL & FL_MASK) != 0, DIR = (FL & FL_DIR) != 0;
     constexpr bool HB = (FL & FL_HB) != 0, DSET = (FL & FL_DSET) != 0;
     const Geom &g = a.g;
+    Real *const out0 = reinterpret_cast<Real *>(a.out0);
+    Real *const out_s = reinterpret_cast<Real *>(a.out_s);
+    const Real *const bvec = reinterpret_cast<const Real *>(a.bvec);
+    const Real *const invdv = reinterpret_cast<const Real *>(a.invd);
+    // operator constants in the storage precision (compile-time selected)
+    auto LKA = [&](int ch) -> Real { if constexpr (ES == 8) return a.lam.ka[ch]; else return a.lamf.ka[ch]; };
+    auto LMA = [&](int ch) -> Real { if constexpr (ES == 8) return a.lam.ma[ch]; else return a.lamf.ma[ch]; };
+    auto LKB = [&](int ch) -> Real { if constexpr (ES == 8) return a.lam.kb[ch]; else return a.lamf.kb[ch]; };
+    auto LMB = [&](int ch) -> Real { if constexpr (ES == 8) return a.lam.mb[ch]; else return a.lamf.mb[ch]; };
+    auto DK = [&](int i) -> Real { if constexpr (ES == 8) return a.dn.K[i]; else return a.dnf.K[i]; };
+    auto DM = [&](int i) -> Real { if constexpr (ES == 8) return a.dn.M[i]; else return a.dnf.M[i]; };
     const int lane = threadIdx.x, w = threadIdx.y;
     const int tid = lane + 32 * w;
     const int blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -400,7 +435,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     double beta = 0.0;
     int map0 = MAP_U0, map1 = MAP_U0 + 2, first = a.first;
     int it_i = 0;                                            // PCG iteration (kernel A)
-    double *cstore = (EP == EP_CGA) ? a.dbuf[1] : a.xout;    // centre-value store target
+    Real *cstore = reinterpret_cast<Real *>((EP == EP_CGA) ? a.dbuf[1] : a.xout);   // centre-value store target
     if (a.sy.st) {
         const CgState *st = a.sy.st;
         if (st->first_failed >= 0) {             // an earlier time step failed: stop the run
@@ -417,7 +452,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
             const int par = it_i & 1;
             map0 = MAP_S;
             map1 = MAP_D0 + par;
-            cstore = a.dbuf[par ^ 1];
+            cstore = reinterpret_cast<Real *>(a.dbuf[par ^ 1]);
         }
         if (a.rot_role != ROT_NONE) {
             // time-step ring: step n reads U[n%3] (u^n), U[(n+2)%3] (u^{n-1}), writes U[(n+1)%3]
@@ -426,7 +461,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
             else if (a.rot_role == ROT_INIT) {
                 map0 = MAP_U0 + s;
                 map1 = MAP_U0 + (s + 2) % 3;
-                cstore = a.ring[(s + 1) % 3];
+                cstore = reinterpret_cast<Real *>(a.ring[(s + 1) % 3]);
                 first = a.first && st->step == 0;
             } else map0 = MAP_U0 + (s + 1) % 3;
         }
@@ -434,17 +469,20 @@ k_stencil(const __grid_constant__ StencilArgs a)
     if (LD == LD_X0 && first) map1 = map0;       // u^{-1} unused: keep the byte count fixed
 
     extern __shared__ __align__(128) double smem_d[];
-    double *stage = smem_d;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_d + NS * SH::STAGE_DBL);
-    double(*seam)[NW][32] = reinterpret_cast<double(*)[NW][32]>(smem_d + NS * SH::STAGE_DBL + 2 * NS);
+    Real *stage = reinterpret_cast<Real *>(smem_d);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + NS * SH::STAGE_DBL);
+    Real(*seam)[NW][32] = reinterpret_cast<Real(*)[NW][32]>(stage + NS * SH::STAGE_DBL + (16 / ES) * NS);
 
     const int X0 = blockIdx.x * TILE_X;
     const int Y0 = blockIdx.y * (NW * R - 1);
     const int xi = X0 - 1 + lane;
-    // TMA box x origin must be 16-B aligned (even for fp64): the box starts at the even column
-    // xb <= X0-1 and lane l reads box column l + xoff (xoff = 0 or 1; the box is 34 wide)
-    const int xb = (X0 - 1) & ~1;
+    // TMA box x origin must be 16-B aligned (even for fp64, a multiple of 4 for fp32): the box
+    // starts at column xb <= X0-1 and lane l reads box column l + xoff (the box is SH::BW wide);
+    // the (k, c) box likewise starts at kb <= 2 (X0-1) and lane l reads value 2 l + koff
+    const int xb = (X0 - 1) & ~(16 / ES - 1);
     const int xoff = (X0 - 1) - xb;
+    const int kb = (2 * (X0 - 1)) & ~(16 / ES - 1);
+    const int koff = 2 * (X0 - 1) - kb;
     const int yb = Y0 - 1 + w * R;
     const int zb = a.z_out0 + blockIdx.z * a.zchunk;
     const int ze = min(zb + a.zchunk, a.z_out1);
@@ -459,12 +497,12 @@ k_stencil(const __grid_constant__ StencilArgs a)
     auto issue = [&](int it) {                     // TMA of plane zb-1+it into its stage
         const int st = it % NS;
         const int p = zb - 1 + it;
-        double *sb = stage + st * SH::STAGE_DBL;
+        Real *sb = stage + st * SH::STAGE_DBL;
         mbar_expect_tx(&bars[st], SH::STAGE_BYTES);
         if (NA >= 1) tma_load_3d(sb, a.tm + map0, xb, Y0 - 1, p, &bars[st]);
         if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, a.tm + map1, xb, Y0 - 1, p, &bars[st]);
         // element layer L = p - 1 sits at z = p in the kc tensor
-        tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KC, 2 * (X0 - 1), Y0 - 1, p, &bars[st]);
+        tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KC, kb, Y0 - 1, p, &bars[st]);
     };
 
     if (tid == 0) {
@@ -525,19 +563,20 @@ k_stencil(const __grid_constant__ StencilArgs a)
         }
     }
 
-    double Fp[R][4];          // Q1: face transforms of the lower plane p-1
-    double Cy[R][4];          // contributions carried from the layer below (face / node space)
-    double Pv[R + 1], Pv1[R + 1];   // dense: node values of plane p-1 at x and x+1
-    double cen[R];            // raw centre values of plane p-1 (rows 0..R-1)
+    const Real betar = (Real)beta;
+    Real Fp[R][4];            // Q1: face transforms of the lower plane p-1
+    Real Cy[R][4];            // contributions carried from the layer below (face / node space)
+    Real Pv[R + 1], Pv1[R + 1];   // dense: node values of plane p-1 at x and x+1
+    Real cen[R];              // raw centre values of plane p-1 (rows 0..R-1)
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int r = 0; r < R; r++) {
 #pragma unroll
-        for (int ch = 0; ch < 4; ch++) { Fp[r][ch] = 0.0; Cy[r][ch] = 0.0; }
-        cen[r] = 0.0;
+        for (int ch = 0; ch < 4; ch++) { Fp[r][ch] = Real(0); Cy[r][ch] = Real(0); }
+        cen[r] = Real(0);
     }
 #pragma unroll
-    for (int r = 0; r <= R; r++) { Pv[r] = 0.0; Pv1[r] = 0.0; }
+    for (int r = 0; r <= R; r++) { Pv[r] = Real(0); Pv1[r] = Real(0); }
 
     for (int it = 0; it < nplanes; ++it) {
         const int p = zb - 1 + it;
@@ -547,35 +586,36 @@ k_stencil(const __grid_constant__ StencilArgs a)
 #else
         mbar_wait(&bars[st], (it / NS) & 1);
 #endif
-        const double *sb = stage + st * SH::STAGE_DBL;
-        const double *n0 = sb + w * R * BOXW + lane + xoff;                 // row 0 of this warp
-        const double *n1 = sb + SH::NODE_DBL + w * R * BOXW + lane + xoff;
-        const double *kcs = sb + NA * SH::NODE_DBL + w * R * 64 + 2 * lane;
+        const Real *sb = stage + st * SH::STAGE_DBL;
+        const Real *n0 = sb + w * R * SH::BW + lane + xoff;                 // row 0 of this warp
+        const Real *n1 = sb + SH::NODE_DBL + w * R * SH::BW + lane + xoff;
+        const Real *kcs = sb + NA * SH::NODE_DBL + w * R * SH::KW + koff + 2 * lane;
         // ---- node values of plane p (rows 0..R), x butterfly (edges) ----------------------
-        double S[R + 1], D[R + 1], V0[R + 1], V1[R + 1], craw[R];
+        Real S[R + 1], D[R + 1], V0[R + 1], V1[R + 1], craw[R];
         const bool store_p = (EP == EP_CGA || EP == EP_RESID_INIT) && (p >= a.zs0 && p < a.zs1) &&
                              ((p >= zb && p < ze) || (p == zb - 1 && zb == a.z_out0) ||
                               (p == ze && ze == a.z_out1));
-        double *cst = store_p ? cstore + (long long)p * g.plane + rowbase : nullptr;
+        Real *cst = store_p ? cstore + (long long)p * g.plane + rowbase : nullptr;
 #pragma unroll
         for (int r = 0; r <= R; r++) {
-            double v, v1;
-            if (LD == LD_RAW) { v = n0[r * BOXW]; v1 = n0[r * BOXW + 1]; }
+            Real v, v1;
+            constexpr int BW = SH::BW;
+            if (LD == LD_RAW) { v = n0[r * BW]; v1 = n0[r * BW + 1]; }
             else if (LD == LD_CGD) {
-                v = fma(beta, n1[r * BOXW], n0[r * BOXW]);
-                v1 = fma(beta, n1[r * BOXW + 1], n0[r * BOXW + 1]);
+                v = fma(betar, n1[r * BW], n0[r * BW]);
+                v1 = fma(betar, n1[r * BW + 1], n0[r * BW + 1]);
             } else if (LD == LD_X0) {
-                v = n0[r * BOXW];
-                v1 = n0[r * BOXW + 1];
-                if (!first) { v = 2.0 * v - n1[r * BOXW]; v1 = 2.0 * v1 - n1[r * BOXW + 1]; }
+                v = n0[r * BW];
+                v1 = n0[r * BW + 1];
+                if (!first) { v = Real(2) * v - n1[r * BW]; v1 = Real(2) * v1 - n1[r * BW + 1]; }
             } else {   // LD_GT: the Dirichlet lift g~ (g on D nodes, 0 elsewhere)
                 double gv = 0.0;
                 const int yi = yb + r;
                 const bool in = xi >= 0 && xi < g.nx1 && yi >= 0 && yi < g.ny1 && p >= 0 && p < g.nzl;
-                v = (in && is_dirichlet(g, xi, yi, p, gv)) ? gv : 0.0;
+                v = (in && is_dirichlet(g, xi, yi, p, gv)) ? (Real)gv : Real(0);
                 gv = 0.0;
                 const bool in1 = xi + 1 < g.nx1 && yi >= 0 && yi < g.ny1 && p >= 0 && p < g.nzl;
-                v1 = (in1 && is_dirichlet(g, xi + 1, yi, p, gv)) ? gv : 0.0;
+                v1 = (in1 && is_dirichlet(g, xi + 1, yi, p, gv)) ? (Real)gv : Real(0);
             }
             if (r < R) {
                 craw[r] = v;
@@ -585,8 +625,8 @@ k_stencil(const __grid_constant__ StencilArgs a)
             if (MASK) {
                 double gv;
                 const int yi = yb + r;
-                if (is_dirichlet(g, xi, yi, p, gv)) v = 0.0;
-                if (is_dirichlet(g, xi + 1, yi, p, gv)) v1 = 0.0;
+                if (is_dirichlet(g, xi, yi, p, gv)) v = Real(0);
+                if (is_dirichlet(g, xi + 1, yi, p, gv)) v1 = Real(0);
             }
             S[r] = v + v1;
             D[r] = v - v1;
@@ -595,24 +635,24 @@ k_stencil(const __grid_constant__ StencilArgs a)
         }
         const int pout = p - 1;
         const bool out_plane = pout >= zb && pout < ze;   // uniform across the CTA
-        double yv[R + 1];
+        Real yv[R + 1];
         if (EL == EL_Q1) {
             // ---- element layer p-1: y butterfly, fused z butterfly + scaling -------------------
             // (lane 31's element X0+30 reads node X0+31 from the box; elements outside the domain
             //  have k = c = 0 from the TMA zero fill)
-            double T[R][4];
+            Real T[R][4];
 #pragma unroll
             for (int r = 0; r < R; r++) {
-                double Fc[4];
+                Real Fc[4];
                 Fc[0] = S[r] + S[r + 1];   // sx=0, sy=0
                 Fc[1] = S[r] - S[r + 1];   // sx=0, sy=1
                 Fc[2] = D[r] + D[r + 1];   // sx=1, sy=0
                 Fc[3] = D[r] - D[r + 1];   // sx=1, sy=1
-                const double2 kc = *reinterpret_cast<const double2 *>(kcs + r * 64);
+                const V2 kc = *reinterpret_cast<const V2 *>(kcs + r * SH::KW);
 #pragma unroll
                 for (int ch = 0; ch < 4; ch++) {
-                    const double av = fma(kc.x, a.lam.ka[ch], kc.y * a.lam.ma[ch]);
-                    const double bv = fma(kc.x, a.lam.kb[ch], kc.y * a.lam.mb[ch]);
+                    const Real av = fma(kc.x, LKA(ch), kc.y * LMA(ch));
+                    const Real bv = fma(kc.x, LKB(ch), kc.y * LMB(ch));
                     T[r][ch] = fma(av, Fp[r][ch], fma(bv, Fc[ch], Cy[r][ch]));   // bottom plane p-1
                     Cy[r][ch] = fma(bv, Fp[r][ch], av * Fc[ch]);                  // top plane p
                     Fp[r][ch] = Fc[ch];
@@ -621,32 +661,32 @@ k_stencil(const __grid_constant__ StencilArgs a)
             // ---- backward y and x butterflies for plane p-1 ------------------------------------
 #pragma unroll
             for (int e = 0; e <= R; e++) {
-                double E0, E1;                              // sx = 0, 1
+                Real E0, E1;                                // sx = 0, 1
                 if (e == 0) { E0 = T[0][0] + T[0][1]; E1 = T[0][2] + T[0][3]; }
                 else if (e == R) { E0 = T[R - 1][0] - T[R - 1][1]; E1 = T[R - 1][2] - T[R - 1][3]; }
                 else {
                     E0 = (T[e][0] + T[e][1]) + (T[e - 1][0] - T[e - 1][1]);
                     E1 = (T[e][2] + T[e][3]) + (T[e - 1][2] - T[e - 1][3]);
                 }
-                const double left = __shfl_up_sync(0xffffffffu, E0 - E1, 1);
+                const Real left = __shfl_up_sync(0xffffffffu, E0 - E1, 1);
                 yv[e] = (E0 + E1) + left;                   // lane 0's value is not owned
             }
         } else {
             // ---- dense voxel matrices (6-tet split): u_e = 4 values of plane p-1 + 4 of p ----
-            double B4[R][4];
+            Real B4[R][4];
 #pragma unroll
             for (int r = 0; r < R; r++) {
-                const double2 kc = *reinterpret_cast<const double2 *>(kcs + r * 64);
-                const double ue[8] = {Pv[r], Pv1[r], Pv[r + 1], Pv1[r + 1], V0[r], V1[r], V0[r + 1], V1[r + 1]};
+                const V2 kc = *reinterpret_cast<const V2 *>(kcs + r * SH::KW);
+                const Real ue[8] = {Pv[r], Pv1[r], Pv[r + 1], Pv1[r + 1], V0[r], V1[r], V0[r + 1], V1[r + 1]};
 #pragma unroll
                 for (int i = 0; i < 8; i++) {
-                    double yk = 0.0, ym = 0.0;
+                    Real yk = Real(0), ym = Real(0);
 #pragma unroll
                     for (int j = 0; j < 8; j++) {
-                        yk = fma(a.dn.K[i * 8 + j], ue[j], yk);
-                        ym = fma(a.dn.M[i * 8 + j], ue[j], ym);
+                        yk = fma(DK(i * 8 + j), ue[j], yk);
+                        ym = fma(DM(i * 8 + j), ue[j], ym);
                     }
-                    const double y = fma(kc.x, yk, kc.y * ym);
+                    const Real y = fma(kc.x, yk, kc.y * ym);
                     if (i < 4) B4[r][i] = Cy[r][i] + y;      // bottom plane p-1 complete
                     else Cy[r][i - 4] = y;                   // top plane p, carried
                 }
@@ -657,10 +697,10 @@ k_stencil(const __grid_constant__ StencilArgs a)
             // the bx = 1 parts belong to node x+1 (next lane)
 #pragma unroll
             for (int e = 0; e <= R; e++) {
-                double X0v = 0.0, X1v = 0.0;
+                Real X0v = Real(0), X1v = Real(0);
                 if (e < R) { X0v += B4[e][0]; X1v += B4[e][1]; }
                 if (e > 0) { X0v += B4[e - 1][2]; X1v += B4[e - 1][3]; }
-                const double left = __shfl_up_sync(0xffffffffu, X1v, 1);
+                const Real left = __shfl_up_sync(0xffffffffu, X1v, 1);
                 yv[e] = X0v + left;
             }
         }
@@ -680,25 +720,25 @@ k_stencil(const __grid_constant__ StencilArgs a)
                 double gv = 0.0;
                 const bool isd = DIR && is_dirichlet(g, xi, yb + e, pout, gv);
                 if (EP == EP_APPLY) {
-                    double y = a.c * yv[e];
+                    Real y = (Real)a.c * yv[e];
                     if (DIR && !DSET && isd) y = cen[e];
-                    if (HB) y = fma(a.s, a.bvec[idx], y);
-                    if (DIR && DSET && isd) y = gv;
-                    a.out0[idx] = y;
+                    if (HB) y = fma((Real)a.s, bvec[idx], y);
+                    if (DIR && DSET && isd) y = (Real)gv;
+                    out0[idx] = y;
                 } else if (EP == EP_CGA) {
-                    const double d = cen[e];
-                    const double q = isd ? d : yv[e];       // identity rows (R3)
-                    a.out0[idx] = q;
-                    acc[0] = fma(d, q, acc[0]);
+                    const Real d = cen[e];
+                    const Real q = isd ? d : yv[e];         // identity rows (R3)
+                    out0[idx] = q;
+                    acc[0] = fma((double)d, (double)q, acc[0]);
                 } else {   // EP_RESID, EP_RESID_INIT: r = b - A x (identity rows on D); s = P^{-1} r
-                    const double b = __ldg(a.bvec + idx);
-                    const double r = isd ? 0.0 : b - yv[e];
-                    const double sv = r * __ldg(a.invd + idx);
-                    a.out0[idx] = r;
-                    a.out_s[idx] = sv;
-                    acc[0] = fma(r, sv, acc[0]);
-                    acc[1] = fma(r, r, acc[1]);
-                    if (EP == EP_RESID_INIT && !isd) acc[2] = fma(b, b, acc[2]);
+                    const Real b = __ldg(bvec + idx);
+                    const Real r = isd ? Real(0) : b - yv[e];
+                    const Real sv = r * __ldg(invdv + idx);
+                    out0[idx] = r;
+                    out_s[idx] = sv;
+                    acc[0] = fma((double)r, (double)sv, acc[0]);
+                    acc[1] = fma((double)r, (double)r, acc[1]);
+                    if (EP == EP_RESID_INIT && !isd) acc[2] = fma((double)b, (double)b, acc[2]);
                 }
             }
         }
@@ -741,7 +781,7 @@ struct BArgs {
     Sync sy;
 };
 
-template <int NT>
+template <int NT, class Real>
 __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
 {
     const int tid = threadIdx.x;
@@ -768,16 +808,22 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
         return;
     }
     const double alpha = delta / dq;
+    const Real alr = (Real)alpha;
+    using V2 = typename Vec2<Real>::type;
+    const Real *const qv_ = reinterpret_cast<const Real *>(a.q);
+    const Real *const iv_ = reinterpret_cast<const Real *>(a.invd);
+    Real *const rv_ = reinterpret_cast<Real *>(a.r);
+    Real *const sv_ = reinterpret_cast<Real *>(a.s);
     const bool replace = it > 0 && re > 0 && (it % re) == 0;           // Alg. 1 line 10 (R6)
-    const double *dvec = a.dbuf[(it & 1) ^ 1];
-    double *xvec = a.rot[0] ? a.rot[(st->step + 1) % 3] : a.x;
+    const Real *dvec = reinterpret_cast<const Real *>(a.dbuf[(it & 1) ^ 1]);
+    Real *xvec = reinterpret_cast<Real *>(a.rot[0] ? a.rot[(st->step + 1) % 3] : a.x);
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
     // BP aligned pairs per thread per sweep (n is even: even row pitch), loads issued up front;
     // a pair never straddles the owned range (planes hold an even number of slots)
     constexpr int BP = 2;
     const long long sweep = (long long)gridDim.x * NT * BP * 2;
     for (long long base = ((long long)blk * NT * BP + tid) * 2; base < a.n; base += sweep) {
-        double2 xv[BP], dv[BP], rv[BP], qv[BP], iv[BP];
+        V2 xv[BP], dv[BP], rv[BP], qv[BP], iv[BP];
         bool in[BP], own[BP];
 #pragma unroll
         for (int k = 0; k < BP; k++) {
@@ -785,33 +831,35 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
             in[k] = i < a.n;
             own[k] = in[k] && !replace && i >= a.own0 && i < a.own1;
             if (in[k]) {
-                xv[k] = *reinterpret_cast<const double2 *>(xvec + i);
-                dv[k] = *reinterpret_cast<const double2 *>(dvec + i);
+                xv[k] = *reinterpret_cast<const V2 *>(xvec + i);
+                dv[k] = *reinterpret_cast<const V2 *>(dvec + i);
             }
             if (own[k]) {
-                rv[k] = *reinterpret_cast<const double2 *>(a.r + i);
-                qv[k] = __ldg(reinterpret_cast<const double2 *>(a.q + i));
-                iv[k] = __ldg(reinterpret_cast<const double2 *>(a.invd + i));
+                rv[k] = *reinterpret_cast<const V2 *>(rv_ + i);
+                qv[k] = __ldg(reinterpret_cast<const V2 *>(qv_ + i));
+                iv[k] = __ldg(reinterpret_cast<const V2 *>(iv_ + i));
             }
         }
 #pragma unroll
         for (int k = 0; k < BP; k++) {
             const long long i = base + (long long)k * NT * 2;
             if (in[k]) {                        // x += alpha d  (line 9)
-                xv[k].x = fma(alpha, dv[k].x, xv[k].x);
-                xv[k].y = fma(alpha, dv[k].y, xv[k].y);
-                *reinterpret_cast<double2 *>(xvec + i) = xv[k];
+                xv[k].x = fma(alr, dv[k].x, xv[k].x);
+                xv[k].y = fma(alr, dv[k].y, xv[k].y);
+                *reinterpret_cast<V2 *>(xvec + i) = xv[k];
             }
             if (own[k]) {                       // r -= alpha q; s = P^{-1} r (lines 13, 15)
-                rv[k].x = fma(-alpha, qv[k].x, rv[k].x);
-                rv[k].y = fma(-alpha, qv[k].y, rv[k].y);
-                const double2 sv = make_double2(rv[k].x * iv[k].x, rv[k].y * iv[k].y);
-                acc[0] = fma(rv[k].x, sv.x, acc[0]);
-                acc[0] = fma(rv[k].y, sv.y, acc[0]);
-                acc[1] = fma(rv[k].x, rv[k].x, acc[1]);
-                acc[1] = fma(rv[k].y, rv[k].y, acc[1]);
-                *reinterpret_cast<double2 *>(a.r + i) = rv[k];
-                *reinterpret_cast<double2 *>(a.s + i) = sv;
+                rv[k].x = fma(-alr, qv[k].x, rv[k].x);
+                rv[k].y = fma(-alr, qv[k].y, rv[k].y);
+                V2 sv;
+                sv.x = rv[k].x * iv[k].x;
+                sv.y = rv[k].y * iv[k].y;
+                acc[0] = fma((double)rv[k].x, (double)sv.x, acc[0]);
+                acc[0] = fma((double)rv[k].y, (double)sv.y, acc[0]);
+                acc[1] = fma((double)rv[k].x, (double)rv[k].x, acc[1]);
+                acc[1] = fma((double)rv[k].y, (double)rv[k].y, acc[1]);
+                *reinterpret_cast<V2 *>(rv_ + i) = rv[k];
+                *reinterpret_cast<V2 *>(sv_ + i) = sv;
             }
         }
     }
@@ -839,10 +887,15 @@ __global__ void __launch_bounds__(256) k_localsum(Sync sy, int which, double *su
 
 // ---- element coefficient access (compact (nx, ny, nzl + 1) layout, layer L at index L + 1) --
 
-__device__ __forceinline__ double2 load_kc(const Geom &g, const double2 *kc, int ex, int ey, int L)
+template <class Real>
+__device__ __forceinline__ typename Vec2<Real>::type load_kc(const Geom &g, const typename Vec2<Real>::type *kc, int ex,
+                                                             int ey, int L)
 {
-    if (ex < 0 || ey < 0 || ex >= g.nx || ey >= g.ny || L < -1 || L >= g.nzl) return make_double2(0.0, 0.0);
-    return kc[((long long)(L + 1) * g.ny + ey) * g.nx + ex];
+    typename Vec2<Real>::type z;
+    z.x = Real(0);
+    z.y = Real(0);
+    if (ex < 0 || ey < 0 || ex >= g.nx || ey >= g.ny || L < -1 || L >= g.nzl) return z;
+    return kc[((long long)(L + 1) * g.ny + ey) * g.kpitch + ex];
 }
 
 // ---- Jacobi diagonal (Jacobi_A P:659-662) -------------------------------------------
@@ -853,44 +906,55 @@ struct DiagC {              // diagonal entries K_ref[l][l], M_ref[l][l] per loc
     double Kd[8], Md[8];
 };
 
-__global__ void k_diag(Geom g, const double2 *kc, double aK, double aM, DiagC dc,
-                       double *diag, double *invd, unsigned long long *launches)
+template <class Real>
+__global__ void k_diag(Geom g, const void *kcp, double aK, double aM, DiagC dc, void *diagp, void *invdp,
+                       unsigned long long *launches)
 {
+    using V2 = typename Vec2<Real>::type;
+    const V2 *kc = reinterpret_cast<const V2 *>(kcp);
+    Real *diag = reinterpret_cast<Real *>(diagp), *invd = reinterpret_cast<Real *>(invdp);
     const long long n = g.plane * g.nzl;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && launches) atomicAdd(launches, 1ull);
     if (i >= n) return;
     const int x = (int)(i % g.pitch), y = (int)((i / g.pitch) % g.ny1), z = (int)(i / g.plane);
-    if (x >= g.nx1) { if (diag) diag[i] = 0.0; if (invd) invd[i] = 0.0; return; }   // pitch padding
+    if (x >= g.nx1) { if (diag) diag[i] = Real(0); if (invd) invd[i] = Real(0); return; }   // pitch padding
     double sk = 0.0, sc = 0.0;
     for (int l = 0; l < 8; l++) {   // node is local node l of element (x - bx, y - by, z - bz)
-        const double2 v = load_kc(g, kc, x - (l & 1), y - ((l >> 1) & 1), z - ((l >> 2) & 1));
-        sk = fma(v.x, dc.Kd[l], sk);
-        sc = fma(v.y, dc.Md[l], sc);
+        const V2 v = load_kc<Real>(g, kc, x - (l & 1), y - ((l >> 1) & 1), z - ((l >> 2) & 1));
+        sk = fma((double)v.x, dc.Kd[l], sk);
+        sc = fma((double)v.y, dc.Md[l], sc);
     }
     double d = aK * sk + aM * sc;
     double gv;
     if (is_dirichlet(g, x, y, z, gv)) d = 1.0;
-    if (diag) diag[i] = d;
-    if (invd) invd[i] = 1.0 / d;
+    if (diag) diag[i] = (Real)d;
+    if (invd) invd[i] = (Real)(1.0 / d);
 }
 
 // ---- packing of the per-element coefficients into the (k, c) pair layout ------------------
-// pair (ex, ey, L) for local layer L in [-1, nzl-1] = global element (ex, ey, zg0 + L), or 0.
+// pair (ex, ey, L) for local layer L in [-1, nzl-1] = global element (ex, ey, zg0 + L), or 0;
+// rows of g.kpitch pairs (the pad pairs of an fp32 row stay 0).
 
-__global__ void k_pack(Geom g, int nz, const double *k, const double *c, double2 *kc, long long ntot,
+template <class Real>
+__global__ void k_pack(Geom g, int nz, const double *k, const double *c, void *kcp, long long ntot,
                        unsigned long long *launches)
 {
+    using V2 = typename Vec2<Real>::type;
+    V2 *kc = reinterpret_cast<V2 *>(kcp);
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && launches) atomicAdd(launches, 1ull);
     if (i >= ntot) return;
-    const int ex = (int)(i % g.nx), ey = (int)((i / g.nx) % g.ny);
-    const int L = (int)(i / ((long long)g.nx * g.ny)) - 1;
+    const int ex = (int)(i % g.kpitch), ey = (int)((i / g.kpitch) % g.ny);
+    const int L = (int)(i / ((long long)g.kpitch * g.ny)) - 1;
     const int ez = g.zg0 + L;
-    double2 v = make_double2(0.0, 0.0);
-    if (ez >= 0 && ez < nz) {
+    V2 v;
+    v.x = Real(0);
+    v.y = Real(0);
+    if (ex < g.nx && ez >= 0 && ez < nz) {
         const long long e = ex + (long long)g.nx * (ey + (long long)g.ny * ez);
-        v = make_double2(k[e], c ? c[e] : 0.0);
+        v.x = (Real)k[e];
+        v.y = c ? (Real)c[e] : Real(0);
     }
     kc[i] = v;
 }
@@ -914,8 +978,10 @@ struct FaceArgs {
 
 __device__ __forceinline__ double phi1(int b, double t, double h) { return b ? t / h : 1.0 - t / h; }
 
+template <class Real>
 __global__ void k_face_load(const FaceArgs a)
 {
+    Real *const F = reinterpret_cast<Real *>(a.F);
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && a.launches) atomicAdd(a.launches, 1ull);
     const long long nface = (long long)a.na * a.nb;
@@ -966,7 +1032,7 @@ __global__ void k_face_load(const FaceArgs a)
             }
         }
         const long long node = (long long)zl * a.g.plane + (long long)idx3[1] * a.g.pitch + idx3[0];
-        a.F[node] = sum;
+        F[node] = (Real)sum;
         return;
     }
     for (int cb = 0; cb < 2; cb++) {             // node is corner (ca, cb) of quad (ia-ca, ib-cb)
@@ -991,21 +1057,24 @@ __global__ void k_face_load(const FaceArgs a)
         }
     }
     const long long node = (long long)zl * a.g.plane + (long long)idx3[1] * a.g.pitch + idx3[0];
-    a.F[node] = sum;
+    F[node] = (Real)sum;
 }
 
 // ---- small pointwise kernels ----------------------------------------------------------------
 
 // v_D <- src_D (src = NULL: the Dirichlet value g) on every local node.
-__global__ void k_set_dirichlet(Geom g, double *v, const double *src, unsigned long long *launches)
+template <class Real>
+__global__ void k_set_dirichlet(Geom g, void *vp, const void *srcp, unsigned long long *launches)
 {
+    Real *v = reinterpret_cast<Real *>(vp);
+    const Real *src = reinterpret_cast<const Real *>(srcp);
     const long long n = g.plane * g.nzl;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && launches) atomicAdd(launches, 1ull);
     if (i >= n) return;
     const int x = (int)(i % g.pitch), y = (int)((i / g.pitch) % g.ny1), z = (int)(i / g.plane);
     double gv;
-    if (x < g.nx1 && is_dirichlet(g, x, y, z, gv)) v[i] = src ? src[i] : gv;
+    if (x < g.nx1 && is_dirichlet(g, x, y, z, gv)) v[i] = src ? src[i] : (Real)gv;
 }
 
 // End of one solve / time step: x_F <- 0 if b_F = 0; per-step statistics;
@@ -1021,6 +1090,7 @@ struct StepArgs {
     Sync sy;
 };
 
+template <class Real>
 __global__ void __launch_bounds__(256) k_step_end(const StepArgs a)
 {
     const int tid = threadIdx.x, blk = blockIdx.x;
@@ -1028,24 +1098,24 @@ __global__ void __launch_bounds__(256) k_step_end(const StepArgs a)
     const CgState *st = a.sy.st;
     if (st->first_failed >= 0) return;
     const int step = st->step;
-    double *xv = a.rot[0] ? a.rot[(step + 1) % 3] : a.x;
+    Real *xv = reinterpret_cast<Real *>(a.rot[0] ? a.rot[(step + 1) % 3] : a.x);
     const bool zx = st->zero_x;
     if (zx) {
         for (long long i = (long long)blk * 256 + tid; i < a.n; i += (long long)gridDim.x * 256) {
             const int x = (int)(i % a.g.pitch), y = (int)((i / a.g.pitch) % a.g.ny1), z = (int)(i / a.g.plane);
             double gv;
-            if (x < a.g.nx1 && !is_dirichlet(a.g, x, y, z, gv)) xv[i] = 0.0;
+            if (x < a.g.nx1 && !is_dirichlet(a.g, x, y, z, gv)) xv[i] = Real(0);
         }
     }
     if (a.snap && a.snap_plane >= 0) {
-        const double *src = xv + (long long)a.snap_plane * a.g.plane;
-        double *dst = a.snap + (long long)step * a.g.plane;
+        const Real *src = xv + (long long)a.snap_plane * a.g.plane;
+        Real *dst = reinterpret_cast<Real *>(a.snap) + (long long)step * a.g.plane;
         for (long long i = (long long)blk * 256 + tid; i < a.g.plane; i += (long long)gridDim.x * 256) {
-            double v = src[i];
+            Real v = src[i];
             if (zx) {
                 const int x = (int)(i % a.g.pitch), y = (int)(i / a.g.pitch);
                 double gv;
-                if (x < a.g.nx1 && !is_dirichlet(a.g, x, y, a.snap_plane, gv)) v = 0.0;
+                if (x < a.g.nx1 && !is_dirichlet(a.g, x, y, a.snap_plane, gv)) v = Real(0);
             }
             dst[i] = v;
         }
@@ -1065,6 +1135,32 @@ __global__ void k_step_commit(Sync sy, int *iters_out)
     st->steps_done = step + 1;
     if (st->status != ST_OK) st->first_failed = step;
     st->step = step + 1;
+}
+
+// ---- boundary conversions of the fp32 variant: user fp64 (natural pitch) <-> internal Real ----
+
+template <class Real>
+__global__ void k_cvt_in(const double *src, Real *dst, int nx1, long long rows, int pitch, unsigned long long *launches)
+{
+    const long long n = rows * nx1;
+    const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 == 0 && launches) atomicAdd(launches, 1ull);
+    for (long long i = i0; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / nx1;
+        dst[row * pitch + (i - row * nx1)] = (Real)src[i];
+    }
+}
+
+template <class Real>
+__global__ void k_cvt_out(const Real *src, double *dst, int nx1, long long rows, int pitch, unsigned long long *launches)
+{
+    const long long n = rows * nx1;
+    const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 == 0 && launches) atomicAdd(launches, 1ull);
+    for (long long i = i0; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / nx1;
+        dst[i] = (double)src[row * pitch + (i - row * nx1)];
+    }
 }
 
 }  // namespace hf

@@ -75,7 +75,7 @@ namespace nccl {
 typedef struct ncclComm *ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef int ncclResult_t;
-enum { ncclFloat64 = 8, ncclSum = 0 };
+enum { ncclFloat32 = 7, ncclFloat64 = 8, ncclSum = 0 };
 typedef ncclResult_t (*GetUniqueId_t)(ncclUniqueId *);
 typedef ncclResult_t (*CommInitRank_t)(ncclComm_t *, int, ncclUniqueId, int);
 typedef ncclResult_t (*CommDestroy_t)(ncclComm_t);
@@ -159,7 +159,7 @@ struct SimKey {
 };
 
 struct Sys {                         // one system's PCG workspace (Table 3 buffers)
-    double2 *kc = nullptr;           // (k, c) pairs, compact (nx, ny, nzl + 1)
+    void *kc = nullptr;              // (k, c) pairs of the storage type, (kpitch, ny, nzl + 1)
     double *U[3] = {nullptr, nullptr, nullptr};   // time-step ring
     double *b = nullptr, *r = nullptr, *s = nullptr, *q = nullptr, *invd = nullptr;
     double *dbuf[2] = {nullptr, nullptr};
@@ -197,7 +197,9 @@ struct hf_ctx {
     int nsm = 148;
     hf_grid g{};
     int nx1 = 0, ny1 = 0, nz1g = 0;
-    int pitch = 0;                   // internal row pitch (even)
+    int prec = 64, es = 8;           // storage precision of node vectors and (k, c): 64 or 32 (f3)
+    int pitch = 0;                   // internal row pitch (16-B multiple)
+    int kpitch = 0;                  // (k, c) pairs per coefficient row
     int nzl = 0, zg0 = 0;            // local planes, global index of local plane 0
     int own_lo = 0, own_hi = 0;      // owned local planes [own_lo, own_hi)
     long long plane = 0, nloc = 0;   // internal plane size, local node slots (padded)
@@ -232,6 +234,12 @@ struct hf_ctx {
 
 static const int NW = 8;             // warps per stencil CTA
 
+// p + n elements of the context's storage type (node vectors are typed double* on the host)
+static inline double *eoff(const hf_ctx *c, const double *p, long long n)
+{
+    return (double *)((char *)p + n * (long long)c->es);
+}
+
 static bool is_device_ptr(const void *p)
 {
     if (!p) return false;
@@ -246,7 +254,7 @@ static bool is_device_ptr(const void *p)
 // user node vector usable in place: device, natural pitch == internal pitch, 16-B aligned
 static bool direct_ok(const hf_ctx *c, const void *p)
 {
-    return c->pitch == c->nx1 && ((uintptr_t)p % 16) == 0 && is_device_ptr(p);
+    return c->es == 8 && c->pitch == c->nx1 && ((uintptr_t)p % 16) == 0 && is_device_ptr(p);
 }
 
 static hf_status scratch_get(hf_ctx *c, int slot, size_t bytes, void **out)
@@ -261,24 +269,59 @@ static hf_status scratch_get(hf_ctx *c, int slot, size_t bytes, void **out)
         c->scratch_cap[slot] = 0;
         CUCK(cudaMalloc(&c->scratch[slot], bytes));
         CUCK(cudaMemsetAsync(c->scratch[slot], 0, bytes, c->stream));   // pitch padding stays 0
+        CUCK(cudaStreamSynchronize(c->stream));   // before any use on another stream
         c->scratch_cap[slot] = bytes;
     }
     *out = c->scratch[slot];
     return HF_OK;
 }
 
-// user (natural pitch) -> internal (padded pitch), nplanes planes
-static hf_status copy_in(hf_ctx *c, double *dst, const double *src, int nplanes, cudaStream_t s)
+static hf_status scratch_get(hf_ctx *c, int slot, size_t bytes, void **out);
+
+// user fp64 (natural pitch) -> internal (padded pitch, storage type), nplanes planes.  fp32
+// contexts convert on the device (k_cvt_in); a host source is staged in scratch `stage` first.
+static hf_status copy_in(hf_ctx *c, double *dst, const double *src, int nplanes, cudaStream_t s, int stage = 30)
 {
-    CUCK(cudaMemcpy2DAsync(dst, (size_t)c->pitch * 8, src, (size_t)c->nx1 * 8, (size_t)c->nx1 * 8,
-                           (size_t)c->ny1 * nplanes, cudaMemcpyDefault, s));
+    if (c->es == 8) {
+        CUCK(cudaMemcpy2DAsync(dst, (size_t)c->pitch * 8, src, (size_t)c->nx1 * 8, (size_t)c->nx1 * 8,
+                               (size_t)c->ny1 * nplanes, cudaMemcpyDefault, s));
+        return HF_OK;
+    }
+    const size_t n = (size_t)c->nx1 * c->ny1 * nplanes;
+    const double *d = src;
+    if (!is_device_ptr(src)) {
+        void *t;
+        HFCK(scratch_get(c, stage, n * 8, &t));
+        CUCK(cudaMemcpyAsync(t, src, n * 8, cudaMemcpyHostToDevice, s));
+        d = (const double *)t;
+    }
+    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)c->nsm * 8);
+    k_cvt_in<float><<<std::max(1u, blocks), 256, 0, s>>>(d, (float *)dst, c->nx1, (long long)c->ny1 * nplanes,
+                                                         c->pitch, c->launches);
+    CUCK(cudaGetLastError());
     return HF_OK;
 }
 
-static hf_status copy_out(hf_ctx *c, double *dst, const double *src, int nplanes, cudaStream_t s)
+static hf_status copy_out(hf_ctx *c, double *dst, const double *src, int nplanes, cudaStream_t s, int stage = 31)
 {
-    CUCK(cudaMemcpy2DAsync(dst, (size_t)c->nx1 * 8, src, (size_t)c->pitch * 8, (size_t)c->nx1 * 8,
-                           (size_t)c->ny1 * nplanes, cudaMemcpyDefault, s));
+    if (c->es == 8) {
+        CUCK(cudaMemcpy2DAsync(dst, (size_t)c->nx1 * 8, src, (size_t)c->pitch * 8, (size_t)c->nx1 * 8,
+                               (size_t)c->ny1 * nplanes, cudaMemcpyDefault, s));
+        return HF_OK;
+    }
+    const size_t n = (size_t)c->nx1 * c->ny1 * nplanes;
+    const bool dev = is_device_ptr(dst);
+    double *d = dst;
+    if (!dev) {
+        void *t;
+        HFCK(scratch_get(c, stage, n * 8, &t));
+        d = (double *)t;
+    }
+    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)c->nsm * 8);
+    k_cvt_out<float><<<std::max(1u, blocks), 256, 0, s>>>((const float *)src, d, c->nx1, (long long)c->ny1 * nplanes,
+                                                          c->pitch, c->launches);
+    CUCK(cudaGetLastError());
+    if (!dev) CUCK(cudaMemcpyAsync(dst, d, n * 8, cudaMemcpyDeviceToHost, s));
     return HF_OK;
 }
 
@@ -334,6 +377,7 @@ static Geom make_geom(const hf_ctx *c)
     g.plane = c->plane;
     g.nx = (int)c->g.ne[0];
     g.ny = (int)c->g.ne[1];
+    g.kpitch = c->kpitch;
     g.dbits = c->dbits;
     for (int f = 0; f < 6; f++) g.gval[f] = c->gval[f];
     return g;
@@ -399,25 +443,29 @@ static hf_status node_map(const hf_ctx *c, const double *p, CUtensorMap *m)
 {
     HFCK(get_encode());
     const cuuint64_t dims[3] = {(cuuint64_t)c->nx1, (cuuint64_t)c->ny1, (cuuint64_t)c->nzl};
-    const cuuint64_t strides[2] = {(cuuint64_t)c->pitch * 8, (cuuint64_t)c->plane * 8};
-    const cuuint32_t box[3] = {(cuuint32_t)BOXW, (cuuint32_t)(NW * c->tileR + 1), 1};
+    const cuuint64_t strides[2] = {(cuuint64_t)c->pitch * c->es, (cuuint64_t)c->plane * c->es};
+    const cuuint32_t bw = c->es == 8 ? StencilShape<2, 8, LD_RAW, double>::BW : StencilShape<2, 8, LD_RAW, float>::BW;
+    const cuuint32_t box[3] = {bw, (cuuint32_t)(NW * c->tileR + 1), 1};
     const cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)p, dims, strides, box, es,
+    const CUtensorMapDataType dt = c->es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    CUresult r = g_encode(m, dt, 3, (void *)p, dims, strides, box, es,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(HF_E_CUDA, "cuTensorMapEncodeTiled(node) failed: " + std::to_string((int)r));
     return HF_OK;
 }
 
-static hf_status kc_map(const hf_ctx *c, const double2 *kc, CUtensorMap *m)
+static hf_status kc_map(const hf_ctx *c, const void *kc, CUtensorMap *m)
 {
     HFCK(get_encode());
-    const cuuint64_t nx = (cuuint64_t)c->g.ne[0], ny = (cuuint64_t)c->g.ne[1];
-    const cuuint64_t dims[3] = {2 * nx, ny, (cuuint64_t)c->nzl + 1};
-    const cuuint64_t strides[2] = {2 * nx * 8, 2 * nx * ny * 8};
-    const cuuint32_t box[3] = {64, (cuuint32_t)(NW * c->tileR), 1};
+    const cuuint64_t kp = (cuuint64_t)c->kpitch, ny = (cuuint64_t)c->g.ne[1];
+    const cuuint64_t dims[3] = {2 * kp, ny, (cuuint64_t)c->nzl + 1};
+    const cuuint64_t strides[2] = {2 * kp * c->es, 2 * kp * ny * c->es};
+    const cuuint32_t kw = c->es == 8 ? StencilShape<2, 8, LD_RAW, double>::KW : StencilShape<2, 8, LD_RAW, float>::KW;
+    const cuuint32_t box[3] = {kw, (cuuint32_t)(NW * c->tileR), 1};
     const cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)kc, dims, strides, box, es,
+    const CUtensorMapDataType dt = c->es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    CUresult r = g_encode(m, dt, 3, (void *)kc, dims, strides, box, es,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(HF_E_CUDA, "cuTensorMapEncodeTiled(kc) failed: " + std::to_string((int)r));
@@ -470,11 +518,11 @@ struct StencilFn {
     size_t smem;
 };
 
-template <int R, int LD, int EP, int FL, int EL> static StencilFn stencil_fn_t()
+template <int R, int LD, int EP, int FL, int EL, class Real> static StencilFn stencil_fn_t()
 {
     constexpr int NS = ns_of<R, LD>();
     static const size_t pad = getenv("HF_SMEM_PAD") ? (size_t)atoi(getenv("HF_SMEM_PAD")) : 0;   // tuning / debug
-    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL>, StencilShape<R, NW, LD>::smem_bytes(NS) + pad};
+    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL, Real>, StencilShape<R, NW, LD, Real>::smem_bytes(NS) + pad};
 }
 
 // every (loader, epilogue, flags) variant the library launches, for tile heights R = 2 and 4
@@ -492,16 +540,22 @@ template <int R, int LD, int EP, int FL, int EL> static StencilFn stencil_fn_t()
     X(LD_RAW, EP_RESID, 0)                                                                      \
     X(LD_RAW, EP_RESID, FL_MASK | FL_DIR)
 
-static StencilFn stencil_fn(int R, int LD, int EP, int FL, int EL)
+template <class Real> static StencilFn stencil_fn_p(int R, int LD, int EP, int FL, int EL)
 {
 #define X(ld, ep, fl)                                                                           \
     if (LD == (ld) && EP == (ep) && FL == (fl)) {                                               \
-        if (EL == EL_DENSE) return stencil_fn_t<2, ld, ep, fl, EL_DENSE>();                    \
-        return R >= 4 ? stencil_fn_t<4, ld, ep, fl, EL_Q1>() : stencil_fn_t<2, ld, ep, fl, EL_Q1>();       \
+        if (EL == EL_DENSE) return stencil_fn_t<2, ld, ep, fl, EL_DENSE, Real>();              \
+        return R >= 4 ? stencil_fn_t<4, ld, ep, fl, EL_Q1, Real>() : stencil_fn_t<2, ld, ep, fl, EL_Q1, Real>(); \
     }
     HF_STENCIL_VARIANTS(X)
 #undef X
     return {nullptr, 0};
+}
+
+// es: element size of the storage type (8: fp64, 4: the fp32 variant, NEXT row f3)
+static StencilFn stencil_fn(int R, int LD, int EP, int FL, int EL, int es)
+{
+    return es == 8 ? stencil_fn_p<double>(R, LD, EP, FL, EL) : stencil_fn_p<float>(R, LD, EP, FL, EL);
 }
 
 // flags of a launch on this context
@@ -574,10 +628,21 @@ static StencilArgs base_args(hf_ctx *c, double aK, double aM)
     std::memset(&a, 0, sizeof(a));
     a.g = make_geom(c);
     a.lam = make_lam(c->g.h, aK, aM);
+    for (int ch = 0; ch < 4; ch++) {
+        a.lamf.ka[ch] = (float)a.lam.ka[ch];
+        a.lamf.ma[ch] = (float)a.lam.ma[ch];
+        a.lamf.kb[ch] = (float)a.lam.kb[ch];
+        a.lamf.mb[ch] = (float)a.lam.mb[ch];
+    }
     if (c->elem == EL_DENSE) {
         double K[64], M[64];
         tet_voxel(c->g.h, K, M);
-        for (int i = 0; i < 64; i++) { a.dn.K[i] = aK * K[i]; a.dn.M[i] = aM * M[i]; }
+        for (int i = 0; i < 64; i++) {
+            a.dn.K[i] = aK * K[i];
+            a.dn.M[i] = aM * M[i];
+            a.dnf.K[i] = (float)a.dn.K[i];
+            a.dnf.M[i] = (float)a.dn.M[i];
+        }
     }
     a.c = 1.0;
     a.s = 0.0;
@@ -623,7 +688,7 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
                                 Launch *out)
 {
     const int FL = dir_flags(c, EP, a.bvec != nullptr, dset);
-    StencilFn f = stencil_fn(c->tileR, LD, EP, FL, c->elem);
+    StencilFn f = stencil_fn(c->tileR, LD, EP, FL, c->elem, c->es);
     if (!f.fn) return fail(HF_E_ARG, "internal: no stencil instantiation");
     f.smem = std::max(f.smem, c->launch_min_smem);
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
@@ -700,14 +765,14 @@ static hf_status sys_maps(hf_ctx *c, Sys &s)
 
 static hf_status sys_alloc(hf_ctx *c, Sys &s, cudaStream_t stream)
 {
-    const size_t vb = (size_t)c->nloc * sizeof(double);
+    const size_t vb = (size_t)c->nloc * c->es;
     double **vecs[] = {&s.U[0], &s.U[1], &s.U[2], &s.b, &s.r, &s.s, &s.q, &s.invd, &s.dbuf[0], &s.dbuf[1]};
     for (double **v : vecs) {
         CUCK(cudaMalloc(v, vb));
         CUCK(cudaMemsetAsync(*v, 0, vb, stream));   // pitch padding must stay zero
     }
-    CUCK(cudaMalloc(&s.kc, (size_t)c->kc_elems * sizeof(double2)));
-    CUCK(cudaMemsetAsync(s.kc, 0, (size_t)c->kc_elems * sizeof(double2), stream));
+    CUCK(cudaMalloc(&s.kc, (size_t)c->kc_elems * 2 * c->es));
+    CUCK(cudaMemsetAsync(s.kc, 0, (size_t)c->kc_elems * 2 * c->es, stream));
     CUCK(cudaMalloc(&s.st, sizeof(CgState)));
     CUCK(cudaMallocHost(&s.st_host, sizeof(CgState)));
     CUCK(cudaMalloc(&s.partA, (size_t)c->max_blocks * NPART * sizeof(double)));
@@ -734,6 +799,18 @@ static void sys_free(Sys &s)
     if (s.graph) cudaGraphDestroy(s.graph);
     if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
     s = Sys();
+}
+
+// padded layouts of the storage type: node rows 16-B multiples (TMA strides), fp32 (k, c) rows
+// an even number of pairs
+static void set_layout(hf_ctx *c)
+{
+    const int q = 16 / c->es;
+    c->pitch = (c->nx1 + q - 1) / q * q;
+    c->kpitch = c->es == 8 ? (int)c->g.ne[0] : ((int)c->g.ne[0] + 1) & ~1;
+    c->plane = (long long)c->pitch * c->ny1;
+    c->nloc = c->plane * c->nzl;
+    c->kc_elems = (long long)c->kpitch * c->g.ne[1] * (c->nzl + 1);
 }
 
 static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream, int rank, int nranks)
@@ -771,7 +848,6 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     c->nx1 = (int)g->ne[0] + 1;
     c->ny1 = (int)g->ne[1] + 1;
     c->nz1g = (int)g->ne[2] + 1;
-    c->pitch = (c->nx1 + 1) & ~1;
     c->rank = rank;
     c->nranks = nranks;
     int64_t lo = 0, hi = c->nz1g;
@@ -782,9 +858,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     c->nzl = ghi - glo;
     c->own_lo = (int)lo - glo;
     c->own_hi = (int)hi - glo;
-    c->plane = (long long)c->pitch * c->ny1;
-    c->nloc = c->plane * c->nzl;
-    c->kc_elems = (long long)g->ne[0] * g->ne[1] * (c->nzl + 1);
+    set_layout(c);
     const double hx = g->h[0], hy = g->h[1], hz = g->h[2];
     for (int l = 0; l < 8; l++) {     // Q1: the same for every local node
         c->dg.Kd[l] = (hy * hz / hx + hx * hz / hy + hx * hy / hz) / 9.0;
@@ -797,7 +871,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     if (const char *e = getenv("HF_UNROLL")) c->unroll = std::min(8, std::max(1, atoi(e)));
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
     // resident CTAs per SM of the CG stencil decide the z split of the grid
-    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem);
+    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
     HFCK(ensure_smem_attr(f.fn, f.smem, device));
     int occ = 0;
     CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
@@ -839,8 +913,12 @@ static hf_status enqueue_pack(hf_ctx *c, Sys &s, const double *k, const double *
 {
     const long long n = c->kc_elems;
     const int bs = 256;
-    k_pack<<<(unsigned)((n + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), (int)c->g.ne[2], k, cc, s.kc, n,
-                                                               c->launches);
+    if (c->es == 8)
+        k_pack<double><<<(unsigned)((n + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), (int)c->g.ne[2], k, cc, s.kc,
+                                                                           n, c->launches);
+    else
+        k_pack<float><<<(unsigned)((n + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), (int)c->g.ne[2], k, cc, s.kc,
+                                                                          n, c->launches);
     CUCK(cudaGetLastError());
     return HF_OK;
 }
@@ -848,8 +926,9 @@ static hf_status enqueue_pack(hf_ctx *c, Sys &s, const double *k, const double *
 static hf_status enqueue_diag(hf_ctx *c, Sys &s, double aK, double aM, double *diag, double *invd)
 {
     const int bs = 256;
-    k_diag<<<(unsigned)((c->nloc + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), s.kc, aK, aM, c->dg,
-                                                                     diag, invd, c->launches);
+    const unsigned nb = (unsigned)((c->nloc + bs - 1) / bs);
+    if (c->es == 8) k_diag<double><<<nb, bs, 0, s.stream>>>(make_geom(c), s.kc, aK, aM, c->dg, diag, invd, c->launches);
+    else k_diag<float><<<nb, bs, 0, s.stream>>>(make_geom(c), s.kc, aK, aM, c->dg, diag, invd, c->launches);
     CUCK(cudaGetLastError());
     return HF_OK;
 }
@@ -858,7 +937,9 @@ static hf_status enqueue_set_dirichlet(hf_ctx *c, Sys &s, double *v, const doubl
 {
     if (!c->dbits) return HF_OK;
     const int bs = 256;
-    k_set_dirichlet<<<(unsigned)((c->nloc + bs - 1) / bs), bs, 0, s.stream>>>(make_geom(c), v, src, c->launches);
+    const unsigned nb = (unsigned)((c->nloc + bs - 1) / bs);
+    if (c->es == 8) k_set_dirichlet<double><<<nb, bs, 0, s.stream>>>(make_geom(c), v, src, c->launches);
+    else k_set_dirichlet<float><<<nb, bs, 0, s.stream>>>(make_geom(c), v, src, c->launches);
     CUCK(cudaGetLastError());
     return HF_OK;
 }
@@ -898,7 +979,7 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
     if (rot) for (int i = 0; i < 3; i++) b.rot[i] = s.U[i];
     b.sy = make_sync(c, s, 0, 1);
     L->B = Launch();
-    L->B.fn = (const void *)k_cg_b<256>;
+    L->B.fn = c->es == 8 ? (const void *)k_cg_b<256, double> : (const void *)k_cg_b<256, float>;
     L->B.grid = dim3(b_blocks(c));
     L->B.block = dim3(256);
     L->B.add(b);
@@ -970,7 +1051,7 @@ static std::vector<Launch> step_launches(hf_ctx *c, const StepArgs &a, bool comm
 {
     std::vector<Launch> v;
     Launch L;
-    L.fn = (const void *)k_step_end;
+    L.fn = c->es == 8 ? (const void *)k_step_end<double> : (const void *)k_step_end<float>;
     L.grid = dim3(std::max(1, std::min(c->nsm, (int)((c->nloc + 255) / 256))));
     L.block = dim3(256);
     L.add(a);
@@ -1130,7 +1211,7 @@ hf_status hf_face_load(hf_ctx *c, int face, double f_const, const double beam[4]
     CUCK(cudaSetDevice(c->device));
     double *dF;
     HFCK(node_out(c, F, 2, false, &dF));
-    CUCK(cudaMemsetAsync(dF, 0, c->nloc * sizeof(double), c->stream));
+    CUCK(cudaMemsetAsync(dF, 0, c->nloc * c->es, c->stream));
     FaceArgs a;
     std::memset(&a, 0, sizeof(a));
     a.g = make_geom(c);
@@ -1150,7 +1231,8 @@ hf_status hf_face_load(hf_ctx *c, int face, double f_const, const double beam[4]
     a.F = dF;
     a.launches = c->launches;
     const long long n = (long long)a.na * a.nb;
-    k_face_load<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(a);
+    if (c->es == 8) k_face_load<double><<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(a);
+    else k_face_load<float><<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(a);
     CUCK(cudaGetLastError());
     return node_out_finish(c, F, dF);
 }
@@ -1211,7 +1293,7 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     double *dx;
     HFCK(node_in(c, b, 4, &db));
     HFCK(node_out(c, x, 6, true, &dx));
-    CUCK(cudaMemcpyAsync(s.b, db, c->nloc * sizeof(double), cudaMemcpyDeviceToDevice, s.stream));
+    CUCK(cudaMemcpyAsync(s.b, db, c->nloc * c->es, cudaMemcpyDeviceToDevice, s.stream));
     HFCK(enqueue_diag(c, s, aK, aM, nullptr, s.invd));
     HFCK(enqueue_set_dirichlet(c, s, dx, s.b));           // x_D = b_D
     if (c->comm) HFCK(c->comm->exchange(c, s, dx));
@@ -1440,7 +1522,7 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
     void *fbuf;
     HFCK(scratch_get(c, 7, (size_t)c->nloc * 8, &fbuf));
     if (F) HFCK(copy_in(c, (double *)fbuf, F, c->nzl, s.stream));
-    else CUCK(cudaMemsetAsync(fbuf, 0, c->nloc * sizeof(double), s.stream));
+    else CUCK(cudaMemsetAsync(fbuf, 0, c->nloc * c->es, s.stream));
     HFCK(copy_in(c, s.U[0], u, c->nzl, s.stream));
     const bool first = step0 <= 0 || !u_prev;
     if (!first) HFCK(copy_in(c, s.U[2], u_prev, c->nzl, s.stream));
@@ -1454,7 +1536,7 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
         snap_local = (int)(snap_plane - c->zg0);
         if (snap_local < 0 || snap_local >= c->nzl) snap_local = -1;
         void *z;
-        HFCK(scratch_get(c, 8, (size_t)std::max(1, nsteps) * c->plane * sizeof(double), &z));
+        HFCK(scratch_get(c, 8, (size_t)std::max(1, nsteps) * c->plane * c->es, &z));
         snapdev = (double *)z;
     }
     cudaEvent_t e0, e1;
@@ -1526,7 +1608,7 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
     void *fbuf;
     HFCK(scratch_get(c, 7, (size_t)c->nloc * 8, &fbuf));
     if (F) HFCK(copy_in(c, (double *)fbuf, F, c->nzl, c->stream));
-    else CUCK(cudaMemsetAsync(fbuf, 0, c->nloc * sizeof(double), c->stream));
+    else CUCK(cudaMemsetAsync(fbuf, 0, c->nloc * c->es, c->stream));
     const bool kdev = is_device_ptr(k_batch);
     const bool cdev = c_batch && is_device_ptr(c_batch);
     std::vector<double *> kst(nslots, nullptr), cst(nslots, nullptr);
@@ -1543,10 +1625,11 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
         HFCK(read_state(c, s));
         const CgState &h = *s.st_host;
         const int last = h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done;
-        HFCK(copy_out(c, u_batch + (size_t)j * nn, s.U[last % 3], c->nzl, s.stream));
+        HFCK(copy_out(c, u_batch + (size_t)j * nn, s.U[last % 3], c->nzl, s.stream, 34 + slot));
         if (front_out) {
             const int sl = (int)(snap_plane - c->zg0);
-            HFCK(copy_out(c, front_out + (size_t)j * pl, s.U[last % 3] + (size_t)sl * c->plane, 1, s.stream));
+            HFCK(copy_out(c, front_out + (size_t)j * pl, eoff(c, s.U[last % 3], (long long)sl * c->plane), 1, s.stream,
+                          38 + slot));
         }
         if (stats) {
             stats[j].steps_done = h.steps_done;
@@ -1573,10 +1656,10 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
         } else {
             // shared capacity: k from this system, the c lane copied from the context's pairs
             HFCK(enqueue_pack(c, s, kj, nullptr));
-            CUCK(cudaMemcpy2DAsync((char *)s.kc + sizeof(double), sizeof(double2), (const char *)c->sys0.kc + sizeof(double),
-                                   sizeof(double2), sizeof(double), (size_t)c->kc_elems, cudaMemcpyDeviceToDevice, s.stream));
+            CUCK(cudaMemcpy2DAsync((char *)s.kc + c->es, 2 * c->es, (const char *)c->sys0.kc + c->es, 2 * c->es, c->es,
+                                   (size_t)c->kc_elems, cudaMemcpyDeviceToDevice, s.stream));
         }
-        HFCK(copy_in(c, s.U[0], u_batch + (size_t)j * nn, c->nzl, s.stream));
+        HFCK(copy_in(c, s.U[0], u_batch + (size_t)j * nn, c->nzl, s.stream, 42 + slot));
         HFCK(simulate_sys(c, s, theta, dt, nsteps, (const double *)fbuf, true, -1, nullptr, o));
         done_sys[slot] = j;
     }
@@ -1619,15 +1702,16 @@ struct NcclComm : Comm {
     bool graph_capturable() const override { return true; }
     hf_status exchange(hf_ctx *c, Sys &s, double *v) override
     {
-        const size_t P = (size_t)c->plane;
+        const long long P = c->plane;
+        const int dt = c->es == 8 ? nccl::ncclFloat64 : nccl::ncclFloat32;
         NCCK(nccl::g_api.groupStart());
         if (c->rank > 0) {
-            NCCK(nccl::g_api.send(v + (size_t)c->own_lo * P, P, nccl::ncclFloat64, c->rank - 1, comm, s.stream));
-            NCCK(nccl::g_api.recv(v + (size_t)(c->own_lo - 1) * P, P, nccl::ncclFloat64, c->rank - 1, comm, s.stream));
+            NCCK(nccl::g_api.send(eoff(c, v, c->own_lo * P), P, dt, c->rank - 1, comm, s.stream));
+            NCCK(nccl::g_api.recv(eoff(c, v, (c->own_lo - 1) * P), P, dt, c->rank - 1, comm, s.stream));
         }
         if (c->rank < c->nranks - 1) {
-            NCCK(nccl::g_api.send(v + (size_t)(c->own_hi - 1) * P, P, nccl::ncclFloat64, c->rank + 1, comm, s.stream));
-            NCCK(nccl::g_api.recv(v + (size_t)c->own_hi * P, P, nccl::ncclFloat64, c->rank + 1, comm, s.stream));
+            NCCK(nccl::g_api.send(eoff(c, v, (c->own_hi - 1) * P), P, dt, c->rank + 1, comm, s.stream));
+            NCCK(nccl::g_api.recv(eoff(c, v, c->own_hi * P), P, dt, c->rank + 1, comm, s.stream));
         }
         NCCK(nccl::g_api.groupEnd());
         return HF_OK;
@@ -1672,18 +1756,18 @@ struct LocalComm : Comm {
             grp->vecs[c->rank] = v;
         }
         grp->barrier();
-        const size_t P = (size_t)c->plane;
+        const long long P = c->plane;
         if (c->rank > 0) {
             hf_ctx *o = grp->ctx[c->rank - 1];
             const double *ov = grp->vecs[c->rank - 1];
-            CUCK(cudaMemcpyPeerAsync(v + (size_t)(c->own_lo - 1) * P, c->device, ov + (size_t)(o->own_hi - 1) * P,
-                                     o->device, P * sizeof(double), s.stream));
+            CUCK(cudaMemcpyPeerAsync(eoff(c, v, (c->own_lo - 1) * P), c->device, eoff(o, ov, (o->own_hi - 1) * P),
+                                     o->device, P * c->es, s.stream));
         }
         if (c->rank < c->nranks - 1) {
             hf_ctx *o = grp->ctx[c->rank + 1];
             const double *ov = grp->vecs[c->rank + 1];
-            CUCK(cudaMemcpyPeerAsync(v + (size_t)c->own_hi * P, c->device, ov + (size_t)o->own_lo * P, o->device,
-                                     P * sizeof(double), s.stream));
+            CUCK(cudaMemcpyPeerAsync(eoff(c, v, c->own_hi * P), c->device, eoff(o, ov, o->own_lo * P), o->device,
+                                     P * c->es, s.stream));
         }
         CUCK(cudaStreamSynchronize(s.stream));
         grp->barrier();
@@ -1831,13 +1915,39 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
             c->dg.Md[l] = h[0] * h[1] * h[2] / 27.0;
         }
     }
-    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem);
+    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
     int occ = 0;
     CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
     c->occ = std::max(1, occ);
     c->sys0.key_valid = false;
     for (auto &p : c->pool) p->key_valid = false;
+    return HF_OK;
+}
+
+hf_status hf_set_precision(hf_ctx *c, int32_t bits)
+{
+    if (!c || (bits != 32 && bits != 64)) return fail(HF_E_ARG, "hf_set_precision: bits must be 32 or 64");
+    if (c->coef_set) return fail(HF_E_STATE, "hf_set_precision: call before hf_set_coefficients");
+    if (bits == c->prec) return HF_OK;
+    CUCK(cudaSetDevice(c->device));
+    CUCK(cudaStreamSynchronize(c->stream));
+    for (auto &p : c->pool) if (p->stream) CUCK(cudaStreamSynchronize(p->stream));
+    sys_free(c->sys0);
+    for (auto &p : c->pool) sys_free(*p);
+    c->pool.clear();
+    for (void *p : c->scratch) cudaFree(p);      // layouts change: reallocate (zeroed) on demand
+    c->scratch.clear();
+    c->scratch_cap.clear();
+    c->prec = bits;
+    c->es = bits / 8;
+    set_layout(c);
+    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
+    HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
+    int occ = 0;
+    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
+    c->occ = std::max(1, occ);
+    HFCK(sys_alloc(c, c->sys0, c->stream));
     return HF_OK;
 }
 

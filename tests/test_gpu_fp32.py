@@ -1,0 +1,201 @@
+"""fp32 storage variant (NEXT row f3, hf_set_precision(ctx, 32)) against the fp64
+CPU oracle.  The variant keeps node vectors and (k, c) in fp32 and every dot product, PCG scalar
+and stop test in fp64.  Bar (BASELINE.json north_star): rel-L2 <= 1e-5 against the oracle.  The
+solves run at rtol 1e-6 (the paper's tolerance); the oracle solves to 1e-12."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1905_07622_b200 as hf  # noqa: E402
+
+DEV = torch.device("cuda:0")
+BAR = 1e-5
+
+
+def T(a):
+    return torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device=DEV)
+
+
+def N(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def ctx32(grid, k, c, elem=0):
+    ctx = hf.hf_create(grid, 0)
+    hf.hf_set_precision(ctx, 32)
+    if elem:
+        hf.hf_set_element(ctx, elem)
+    hf.hf_set_coefficients(ctx, T(k), T(c))
+    return ctx
+
+
+GRIDS = {
+    "c1": synth.Grid((8, 8, 8), (0.125, 0.125, 0.125)),
+    "ragged": synth.Grid((70, 40, 13), (0.3, 0.2, 0.7), (-1.0, 2.0, 0.5)),   # odd nx: padded fp32 rows
+    "seams": synth.Grid((33, 65, 9), (0.2, 0.2, 0.2)),
+}
+
+
+@pytest.mark.parametrize("elem", [0, 1])
+@pytest.mark.parametrize("gname", list(GRIDS))
+def test_fp32_apply_diag_load(gname, elem):
+    g = GRIDS[gname]
+    k, c = synth.random_fields(g, seed=31)
+    o = oracle.Oracle(g, k, c, elem=elem)
+    ctx = ctx32(g, k, c, elem)
+    u = synth.random_vector(g.n_nodes, seed=32)
+    y = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    for aK, aM in [(1.0, 0.0), (0.0, 1.0), (0.005, 1.0)]:
+        hf.hf_apply(ctx, aK, aM, T(u), y)
+        assert rel(N(y), o.spmv(aK, aM, u)) <= BAR, (gname, aK, aM)
+    d = torch.empty_like(y)
+    hf.hf_diag(ctx, 0.005, 1.0, d)
+    assert rel(N(d), o.diag(0.005, 1.0)) <= 1e-6
+    F = torch.empty_like(y)
+    hf.hf_face_load(ctx, synth.FACE_ZM, 0.5, (3.0, 1.0, 0.0, 0.0), F)
+    assert rel(N(F), o.face_load(synth.FACE_ZM, 0.5, (3.0, 1.0, 0.0, 0.0))) <= 1e-6
+
+
+def test_fp32_set_precision_order_and_host_buffers():
+    g = GRIDS["ragged"]
+    k, c = synth.random_fields(g, seed=33)
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_coefficients(ctx, T(k), T(c))
+    with pytest.raises(hf.HfError):
+        hf.hf_set_precision(ctx, 32)              # after the coefficients: HF_E_STATE
+    with pytest.raises(hf.HfError):
+        hf.hf_set_precision(hf.hf_create(g, 0), 16)
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_precision(ctx, 32)
+    hf.hf_set_coefficients(ctx, k, c)             # host arrays
+    u = synth.random_vector(g.n_nodes, seed=34)
+    yh = np.empty_like(u)
+    hf.hf_apply(ctx, 0.3, 1.0, u, yh)             # host in / host out through the converters
+    yd = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_apply(ctx, 0.3, 1.0, T(u), yd)
+    assert np.array_equal(yh, N(yd))
+    assert rel(yh, oracle.Oracle(g, k, c).spmv(0.3, 1.0, u)) <= BAR
+
+
+def test_fp32_cg_and_simulate_c1():
+    p = synth.c1()
+    o, F = oracle.problem_oracle(p)
+    ctx = ctx32(p.grid, p.k, p.c)
+    Fd = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, Fd)
+    b = synth.random_vector(p.grid.n_nodes, 35)
+    x = T(np.zeros(p.grid.n_nodes))
+    info = hf.hf_cg(ctx, 0.01, 1.0, T(b), x, rtol=1e-6)
+    xo, _, _, _ = o.pcg(0.01, 1.0, b, np.zeros(p.grid.n_nodes), tol=1e-12)
+    assert info["relres"] <= 1e-6 and rel(N(x), xo) <= BAR
+    u = T(p.u0)
+    st = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, Fd, u, rtol=1e-6)
+    uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, F, p.u0, tol=1e-12)
+    # C1's backward-Euler matrix has kappa(D^-1 A) ~ 300: a solve with an fp32
+    # operator is accurate to ~kappa * eps_32 = 300 * 6e-8 ~ 2e-5 per step whatever rtol is
+    # (measured 3.4e-5 .. 4.0e-5 after 10 steps for rtol 1e-6 .. 1e-9, tools/fp32_probe.py), so the
+    # 1e-5 bar is met on C3 (below) and here the bar is the conditioning floor (R18)
+    assert st["first_failed_step"] == -1 and rel(N(u), uo) <= 1e-4
+
+
+def test_fp32_dirichlet_beam_snapshot():
+    g = synth.Grid((20, 14, 9), (0.3, 0.3, 0.25), (-3.0, -2.0, 0.0))
+    k, c = synth.random_fields(g, seed=36)
+    p = synth.Problem("dir", g, k, c, synth.random_vector(g.n_nodes, 37), theta=0.5, dt=0.05, nsteps=8,
+                      beam=(10.0, 1.0, 0.0, 0.0), flux_const=0.2, dirichlet_bits=0b100001,
+                      dirichlet_values=(1.5, 0.0, 0.0, 0.0, 0.0, -0.5))
+    ctx = ctx32(g, k, c)
+    hf.hf_set_dirichlet_faces(ctx, p.dirichlet_bits, p.dirichlet_values)
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
+    u = T(p.u0)
+    snap = torch.empty(p.nsteps * ctx.n_plane, dtype=torch.float64, device=DEV)
+    hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, F, u, 0, snap, rtol=1e-6)
+    o, Fo = oracle.problem_oracle(p)
+    uo, _, _, so = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=1e-12, snap_plane=0)
+    assert rel(N(u), uo) <= BAR and rel(N(snap), so.ravel()) <= BAR
+
+
+def test_fp32_c3_two_steps():
+    p = synth.c3(nsteps=2)
+    o, F = oracle.problem_oracle(p)
+    ctx = ctx32(p.grid, p.k, p.c)
+    Fd = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, Fd)
+    u = T(p.u0)
+    hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, Fd, u, rtol=1e-6)
+    uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, F, p.u0, tol=1e-12)
+    assert rel(N(u), uo) <= BAR
+
+
+def test_fp32_batched_matches_individual():
+    g = synth.Grid((12, 10, 9), (0.3, 0.3, 0.2))
+    B = 3
+    ks = [synth.random_fields(g, seed=40 + j)[0] for j in range(B)]
+    _, c = synth.random_fields(g, seed=39)
+    ctx = ctx32(g, ks[0], c)
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+    ub = torch.zeros(B * g.n_nodes, dtype=torch.float64, device=DEV)
+    plane = (g.ne[0] + 1) * (g.ne[1] + 1)
+    front = torch.empty(B * plane, dtype=torch.float64, device=DEV)
+    hf.hf_simulate_batched(ctx, B, T(np.concatenate(ks)), None, 0.5, 0.05, 6, F, ub, 0, front, rtol=1e-6)
+    ub, front = N(ub).reshape(B, -1), N(front).reshape(B, -1)
+    for j in range(B):
+        o = oracle.Oracle(g, ks[j], c)
+        uo, _, _, _ = o.simulate(0.5, 0.05, 6, o.face_load(synth.FACE_ZM, 1.0), np.zeros(g.n_nodes))
+        assert rel(ub[j], uo) <= BAR and rel(front[j], uo[:plane]) <= BAR
+
+
+def test_fp32_slab_local_transport():
+    g = synth.Grid((14, 11, 17), (0.3, 0.3, 0.2))
+    k, c = synth.random_fields(g, seed=41)
+    theta, dt, nsteps, nranks = 0.5, 0.05, 5, 2
+    u0 = synth.random_vector(g.n_nodes, 42) * 0.01
+    o = oracle.Oracle(g, k, c)
+    uo, _, _, _ = o.simulate(theta, dt, nsteps, o.face_load(synth.FACE_ZM, 1.0), u0)
+    grp = hf.hf_local_group_create(nranks)
+    plane = (g.ne[0] + 1) * (g.ne[1] + 1)
+    out, errs, ctxs = [None] * nranks, [], [None] * nranks
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            ctx = hf.hf_create_slab(g, r, nranks, grp, transport=1, device=0)
+            ctxs[r] = ctx
+            hf.hf_set_precision(ctx, 32)
+            lo, hi, lp, z0 = ctx.slab
+            hf.hf_set_coefficients(ctx, T(k), T(c))
+            F = torch.empty(ctx.n_nodes, dtype=torch.float64, device=DEV)
+            hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+            u = T(u0[z0 * plane:(z0 + lp) * plane])
+            hf.hf_simulate(ctx, theta, dt, nsteps, F, u, rtol=1e-6)
+            out[r] = (lo, hi, z0, N(u))
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(nranks)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not errs, errs
+    full = np.empty(g.n_nodes)
+    for lo, hi, z0, u in out:
+        full[lo * plane:hi * plane] = u[(lo - z0) * plane:(hi - z0) * plane]
+    assert rel(full, uo) <= BAR
+    del ctxs
+    hf.hf_local_group_destroy(grp)
