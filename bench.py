@@ -313,7 +313,7 @@ def _apply_time_internal(hf, torch, dev, peak, ctx, g, prec):
     del ctx
     torch.cuda.empty_cache()
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "ms": ms,
-            "bytes_per_launch": byts, "traffic": None,
+            "bytes_per_launch": byts, "traffic": ncu_traffic("stencil_apply_512_f32"),
             "kernel": f"k_stencil<LD_RAW,EP_APPLY,fp{prec}> 512^3 nodes, mean of 10 (per-launch events)"}
 
 

@@ -16,6 +16,8 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 if mode == "sim":
     p = synth.c3(nsteps=steps)
     ctx = hf.hf_create(p.grid, 0)
+    if os.environ.get("HF_PREC"):
+        hf.hf_set_precision(ctx, int(os.environ["HF_PREC"]))
     hf.hf_set_coefficients(ctx, torch.tensor(p.k, device=dev), torch.tensor(p.c, device=dev))
     F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=dev)
     hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
@@ -31,6 +33,8 @@ elif mode.startswith("apply"):
     u = torch.randn(g.n_nodes, dtype=torch.float64, device=dev, generator=gen)
     y = torch.empty_like(u)
     ctx = hf.hf_create(g, 0)
+    if os.environ.get("HF_PREC"):
+        hf.hf_set_precision(ctx, int(os.environ["HF_PREC"]))
     hf.hf_set_coefficients(ctx, k, c)
     for _ in range(steps):
         hf.hf_apply(ctx, 0.005, 1.0, u, y)
