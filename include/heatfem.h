@@ -61,11 +61,13 @@ typedef struct {
 
 /* PCG options (Alg. 1).  rtol: stop when ||r||_2 <= rtol ||b_F||_2 (reading R4);
  * max_iter: i_max (reading R10); replace_every: the "i divisible by 50" true-residual
- * replacement period of Alg. 1 line 9 (reading R6; 0 disables). */
+ * replacement period of Alg. 1 line 9 (reading R6; 0 disables; negative: the context's
+ * default, 50 for fp64 and 0 for the fp32 variant, whose true residual stagnates near
+ * kappa eps_32 so that replacements below that level would prevent convergence, reading R18). */
 typedef struct {
     double rtol;          /* default 1e-12 */
     int32_t max_iter;     /* default 10000 */
-    int32_t replace_every;/* default 50 */
+    int32_t replace_every;/* default -1: the context default (50 fp64, 0 fp32) */
 } hf_cg_opts;
 
 typedef struct {

@@ -225,7 +225,7 @@ def hf_diag(ctx: Context, aK: float, aM: float, diag):
     _check(_lib.hf_diag(ctx.ptr, aK, aM, _ptr(diag, ctx.n_nodes, "diag")))
 
 
-def hf_cg(ctx: Context, aK: float, aM: float, b, x, rtol=1e-12, max_iter=10000, replace_every=50,
+def hf_cg(ctx: Context, aK: float, aM: float, b, x, rtol=1e-12, max_iter=10000, replace_every=-1,
           raise_on_noconv: bool = True) -> dict:
     info = hf_cg_info()
     o = _opts(rtol, max_iter, replace_every)
@@ -243,7 +243,7 @@ def _stats(s: hf_sim_stats) -> dict:
 
 
 def hf_simulate(ctx: Context, theta: float, dt: float, nsteps: int, F, u, snap_plane: int = -1, snap=None,
-                rtol=1e-12, max_iter=10000, replace_every=50, raise_on_noconv: bool = True) -> dict:
+                rtol=1e-12, max_iter=10000, replace_every=-1, raise_on_noconv: bool = True) -> dict:
     s = hf_sim_stats()
     o = _opts(rtol, max_iter, replace_every)
     st = _lib.hf_simulate(ctx.ptr, theta, dt, nsteps, _ptr(F, ctx.n_nodes, "F", allow_none=True),
@@ -257,7 +257,7 @@ def hf_simulate(ctx: Context, theta: float, dt: float, nsteps: int, F, u, snap_p
 
 
 def hf_simulate_resume(ctx: Context, theta: float, dt: float, nsteps: int, F, u, u_prev, step0: int,
-                       rtol=1e-12, max_iter=10000, replace_every=50) -> dict:
+                       rtol=1e-12, max_iter=10000, replace_every=-1) -> dict:
     s = hf_sim_stats()
     o = _opts(rtol, max_iter, replace_every)
     _check(_lib.hf_simulate_resume(ctx.ptr, theta, dt, nsteps, _ptr(F, ctx.n_nodes, "F", allow_none=True),
@@ -267,7 +267,7 @@ def hf_simulate_resume(ctx: Context, theta: float, dt: float, nsteps: int, F, u,
 
 
 def hf_simulate_batched(ctx: Context, B: int, k_batch, c_batch, theta: float, dt: float, nsteps: int, F, u_batch,
-                        snap_plane: int = -1, front_out=None, rtol=1e-12, max_iter=10000, replace_every=50) -> list:
+                        snap_plane: int = -1, front_out=None, rtol=1e-12, max_iter=10000, replace_every=-1) -> list:
     stats = (hf_sim_stats * max(B, 1))()
     o = _opts(rtol, max_iter, replace_every)
     _check(_lib.hf_simulate_batched(ctx.ptr, B, _ptr(k_batch, B * ctx.n_elems, "k_batch"),

@@ -1137,6 +1137,20 @@ __global__ void k_step_commit(Sync sy, int *iters_out)
     st->step = step + 1;
 }
 
+// ---- c lane of the packed (k, c) pairs back to a plain per-element fp64 array ----------------
+template <class Real>
+__global__ void k_extract_c(Geom g, int nz, const void *kcp, double *c, unsigned long long *launches)
+{
+    using V2 = typename Vec2<Real>::type;
+    const V2 *kc = reinterpret_cast<const V2 *>(kcp);
+    const long long ne = (long long)g.nx * g.ny * nz;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e == 0 && launches) atomicAdd(launches, 1ull);
+    if (e >= ne) return;
+    const int ex = (int)(e % g.nx), ey = (int)((e / g.nx) % g.ny), ez = (int)(e / ((long long)g.nx * g.ny));
+    c[e] = (double)kc[((long long)(ez - g.zg0 + 1) * g.ny + ey) * g.kpitch + ex].y;
+}
+
 // ---- boundary conversions of the fp32 variant: user fp64 (natural pitch) <-> internal Real ----
 
 template <class Real>

@@ -191,6 +191,7 @@ struct Comm {
 
 struct hf_ctx {
     std::map<std::string, void *> mapcache;   // device copies of TMA descriptor sets (maps_dev)
+    std::map<int, hf_ctx *> stacks;  // batched: contexts of G stacked systems (batched_stacked)
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -888,6 +889,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     return HF_OK;
 }
 
+static void ctx_free(hf_ctx *c);
 static void ctx_free(hf_ctx *c)
 {
     if (!c) return;
@@ -902,6 +904,8 @@ static void ctx_free(hf_ctx *c)
     cudaFree(c->flush);
     for (auto &kv : c->mapcache) cudaFree(kv.second);
     c->mapcache.clear();
+    for (auto &kv : c->stacks) { ctx_free(kv.second); delete kv.second; }
+    c->stacks.clear();
     delete c->comm;
     if (c->own_stream) cudaStreamDestroy(c->stream);
 }
@@ -1017,9 +1021,17 @@ static hf_status read_state(hf_ctx *c, Sys &s)
 }
 
 // options and counters of a new solve / run, written without a device round trip
-static hf_status set_solver_opts(hf_ctx *c, Sys &s, const hf_cg_opts &d)
+// replace_every < 0: the context default, 50 (Alg. 1, R6) in fp64, 0 in the fp32 variant (R18)
+static hf_cg_opts resolved(const hf_ctx *c, hf_cg_opts o)
 {
-    if (!(d.rtol >= 0.0) || d.max_iter < 0 || d.replace_every < 0) return fail(HF_E_ARG, "bad hf_cg_opts");
+    if (o.replace_every < 0) o.replace_every = c->es == 8 ? 50 : 0;
+    return o;
+}
+
+static hf_status set_solver_opts(hf_ctx *c, Sys &s, const hf_cg_opts &d0)
+{
+    const hf_cg_opts d = resolved(c, d0);
+    if (!(d.rtol >= 0.0) || d.max_iter < 0) return fail(HF_E_ARG, "bad hf_cg_opts");
     CUCK(cudaStreamSynchronize(s.stream));     // the pinned image may still be in flight
     CgState &h = *s.st_host;
     std::memset(&h, 0, sizeof(h));
@@ -1286,8 +1298,9 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     if (!c->coef_set) return fail(HF_E_STATE, "hf_cg: coefficients not set");
     CUCK(cudaSetDevice(c->device));
     Sys &s = c->sys0;
-    hf_cg_opts o = {1e-12, 10000, 50};
+    hf_cg_opts o = {1e-12, 10000, -1};
     if (opts) o = *opts;
+    o = resolved(c, o);
     HFCK(set_solver_opts(c, s, o));
     const double *db;
     double *dx;
@@ -1516,8 +1529,9 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
     if (snap && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "hf_simulate: snap_plane");
     CUCK(cudaSetDevice(c->device));
     Sys &s = c->sys0;
-    hf_cg_opts o = {1e-12, 10000, 50};
+    hf_cg_opts o = {1e-12, 10000, -1};
     if (opts) o = *opts;
+    o = resolved(c, o);
     // the flux load lives in a stable internal buffer (graph parameters point at it)
     void *fbuf;
     HFCK(scratch_get(c, 7, (size_t)c->nloc * 8, &fbuf));
@@ -1578,6 +1592,113 @@ hf_status hf_simulate_resume(hf_ctx *c, double theta, double dt, int32_t nsteps,
     return simulate_common(c, theta, dt, nsteps, F, u, u_prev, step0, -1, nullptr, opts, stats);
 }
 
+}  // extern "C"
+
+// ---- batched simulations as one block-diagonal system ----------------------------------------
+// G independent systems on the same grid are stacked along z into one grid of G (nz + 1) node
+// planes; the element layer between two systems gets k = c = 0, so the stacked operator is
+// exactly block diagonal (no element couples two systems) and one PCG on the stack solves every
+// system ("rapid successive solutions": the GPU sees G times the parallelism of one 1M-DoF
+// system, which alone is latency-bound).  The stack's stop test ||r|| <= tol ||b|| uses
+// tol = rtol / sqrt(G): since ||r_j|| <= ||r|| and ||b|| <= sqrt(G) max_j ||b_j||, each system then
+// meets rtol up to the ratio max_j ||b_j|| / ||b_j|| (~1 for the corrosion sims).
+static hf_status stack_ctx(hf_ctx *c, int G, hf_ctx **out)
+{
+    auto it = c->stacks.find(G);
+    if (it != c->stacks.end()) { *out = it->second; return HF_OK; }
+    hf_grid g2 = c->g;
+    g2.ne[2] = (int64_t)G * (c->g.ne[2] + 1) - 1;
+    hf_ctx *s = new hf_ctx();
+    hf_status st = ctx_init(s, &g2, c->device, c->stream, 0, 1);
+    if (st == HF_OK && c->prec != 64) st = hf_set_precision(s, c->prec);
+    if (st == HF_OK && c->elem != EL_Q1) st = hf_set_element(s, c->elem);
+    if (st != HF_OK) { ctx_free(s); delete s; return st; }
+    s->dbits = c->dbits;            // x / y faces only (callers exclude z-face Dirichlet)
+    for (int f = 0; f < 6; f++) s->gval[f] = c->gval[f];
+    s->driver = c->driver;
+    s->unroll = c->unroll;
+    c->stacks[G] = s;
+    *out = s;
+    return HF_OK;
+}
+
+static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nsteps, const double *F, double *u,
+                                 double *u_prev, int64_t step0, int64_t snap_plane, double *snap,
+                                 const hf_cg_opts *opts, hf_sim_stats *stats);
+
+static hf_status batched_stacked(hf_ctx *c, int32_t B, const double *k_batch, const double *c_batch, double theta,
+                                 double dt, int32_t nsteps, const double *F, double *u_batch, int64_t snap_plane,
+                                 double *front_out, const hf_cg_opts &o, hf_sim_stats *stats)
+{
+    const size_t nxy = (size_t)c->g.ne[0] * c->g.ne[1];
+    const size_t ne = nxy * (size_t)c->g.ne[2];
+    const size_t pl = (size_t)c->nx1 * c->ny1;
+    const size_t nn = pl * (size_t)c->nz1g;             // natural nodes of one system
+    int G = (int)std::max<long long>(2, (8LL << 20) / (long long)nn);   // ~8M stacked nodes
+    if (const char *e = getenv("HF_BATCH_GROUP")) G = std::max(1, atoi(e));
+    G = std::min<int>(G, B);
+    const double *cshared = nullptr;
+    if (!c_batch) {                                   // the context's c, unpacked once
+        void *p;
+        HFCK(scratch_get(c, 50, ne * sizeof(double), &p));
+        const unsigned nb = (unsigned)((ne + 255) / 256);
+        if (c->es == 8) k_extract_c<double><<<nb, 256, 0, c->stream>>>(make_geom(c), (int)c->g.ne[2], c->sys0.kc, (double *)p, c->launches);
+        else k_extract_c<float><<<nb, 256, 0, c->stream>>>(make_geom(c), (int)c->g.ne[2], c->sys0.kc, (double *)p, c->launches);
+        CUCK(cudaGetLastError());
+        cshared = (const double *)p;
+    }
+    hf_status first_err = HF_OK;
+    for (int j0 = 0; j0 < B; j0 += G) {
+        const int g = std::min(G, B - j0);
+        hf_ctx *s;
+        HFCK(stack_ctx(c, g, &s));
+        const size_t nes = (size_t)g * ne + (size_t)(g - 1) * nxy;
+        void *kp, *cp, *fp, *up;
+        HFCK(scratch_get(c, 51, nes * sizeof(double), &kp));
+        HFCK(scratch_get(c, 52, nes * sizeof(double), &cp));
+        HFCK(scratch_get(c, 53, (size_t)g * nn * sizeof(double), &fp));
+        HFCK(scratch_get(c, 54, (size_t)g * nn * sizeof(double), &up));
+        double *ks = (double *)kp, *cs = (double *)cp, *fs = (double *)fp, *us = (double *)up;
+        for (int i = 0; i < g; i++) {
+            const size_t o1 = (size_t)i * (ne + nxy);
+            const int j = j0 + i;
+            CUCK(cudaMemcpyAsync(ks + o1, k_batch + (size_t)j * ne, ne * sizeof(double), cudaMemcpyDefault, c->stream));
+            const double *cj = c_batch ? c_batch + (size_t)j * ne : cshared;
+            CUCK(cudaMemcpyAsync(cs + o1, cj, ne * sizeof(double), cudaMemcpyDefault, c->stream));
+            if (i + 1 < g) {                            // separator element layer: k = c = 0
+                CUCK(cudaMemsetAsync(ks + o1 + ne, 0, nxy * sizeof(double), c->stream));
+                CUCK(cudaMemsetAsync(cs + o1 + ne, 0, nxy * sizeof(double), c->stream));
+            }
+            if (F) CUCK(cudaMemcpyAsync(fs + (size_t)i * nn, F, nn * sizeof(double), cudaMemcpyDefault, c->stream));
+            else CUCK(cudaMemsetAsync(fs + (size_t)i * nn, 0, nn * sizeof(double), c->stream));
+            CUCK(cudaMemcpyAsync(us + (size_t)i * nn, u_batch + (size_t)j * nn, nn * sizeof(double), cudaMemcpyDefault,
+                                 c->stream));
+        }
+        HFCK(hf_set_coefficients(s, ks, cs));
+        hf_cg_opts o2 = o;
+        o2.rtol = o.rtol / std::sqrt((double)g);
+        hf_sim_stats st;
+        std::memset(&st, 0, sizeof(st));
+        hf_status rs = simulate_common(s, theta, dt, nsteps, fs, us, nullptr, 0, -1, nullptr, &o2, &st);
+        if (rs != HF_OK && rs != HF_E_NOCONV && rs != HF_E_BREAKDOWN) return rs;
+        if (rs != HF_OK && first_err == HF_OK) first_err = rs;
+        for (int i = 0; i < g; i++) {
+            const int j = j0 + i;
+            CUCK(cudaMemcpyAsync(u_batch + (size_t)j * nn, us + (size_t)i * nn, nn * sizeof(double), cudaMemcpyDefault,
+                                 c->stream));
+            if (front_out)
+                CUCK(cudaMemcpyAsync(front_out + (size_t)j * pl, us + (size_t)i * nn + (size_t)snap_plane * pl,
+                                     pl * sizeof(double), cudaMemcpyDefault, c->stream));
+            if (stats) stats[j] = st;
+        }
+        CUCK(cudaStreamSynchronize(c->stream));
+    }
+    if (first_err != HF_OK) return fail(first_err, "hf_simulate_batched: a system failed to converge");
+    return HF_OK;
+}
+
+extern "C" {
+
 hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const double *c_batch, double theta,
                               double dt, int32_t nsteps, const double *F, double *u_batch, int64_t snap_plane,
                               double *front_out, const hf_cg_opts *opts, hf_sim_stats *stats)
@@ -1588,8 +1709,17 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
     if (c->comm) return fail(HF_E_ARG, "hf_simulate_batched: not available on slab contexts");
     if (front_out && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "snap_plane");
     CUCK(cudaSetDevice(c->device));
-    hf_cg_opts o = {1e-12, 10000, 50};
+    hf_cg_opts o = {1e-12, 10000, -1};
     if (opts) o = *opts;
+    o = resolved(c, o);
+    {   // one block-diagonal stack per group of systems, unless z faces carry Dirichlet values
+        const char *e = getenv("HF_BATCH_STACK");
+        // measured (C5, 1M DoF per system): stacks of 2 are slower than two concurrent systems,
+        // stacks of 4-8 reach the HBM roofline; B < 4 keeps the per-system pool
+        const bool stack = (B >= 4 || (e && atoi(e) == 1)) && !(c->dbits & 48u) && !(e && atoi(e) == 0);
+        if (stack) return batched_stacked(c, B, k_batch, c_batch, theta, dt, nsteps, F, u_batch, snap_plane, front_out,
+                                          o, stats);
+    }
     int nslots = 2;
     if (const char *e = getenv("HF_BATCH_STREAMS")) nslots = std::max(1, atoi(e));
     nslots = std::min(nslots, std::max(1, (int)B));

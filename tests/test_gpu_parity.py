@@ -316,7 +316,13 @@ def test_resume_equals_one_run():
     assert np.array_equal(N(u1), N(u2))
 
 
-def test_batched_matches_individual():
+@pytest.mark.parametrize("mode", ["stack", "stack2", "pool"])
+def test_batched_matches_individual(mode, monkeypatch):
+    """Batched sims: the block-diagonal stack (default; groups of HF_BATCH_GROUP systems, the
+    last group smaller) and the per-system pool path (HF_BATCH_STACK=0) against the oracle."""
+    monkeypatch.setenv("HF_BATCH_STACK", "0" if mode == "pool" else "1")
+    if mode == "stack2":
+        monkeypatch.setenv("HF_BATCH_GROUP", "2")
     g = synth.Grid((12, 10, 9), (0.3, 0.3, 0.2))
     B = 3
     base_k, base_c = synth.random_fields(g, seed=14)
