@@ -232,6 +232,15 @@ hf_status hf_get_launch_count(hf_ctx *ctx, int64_t *count);
 hf_status hf_profile(hf_ctx *ctx, int32_t enable);
 hf_status hf_profile_read(hf_ctx *ctx, double ms[5], int64_t n[5]);
 
+/* Instrumentation: average duration of PCG kernel A (the dominant kernel, Alg. 1 lines 6-7)
+ * replayed `reps` times back to back on the context stream, bracketed by one pair of CUDA
+ * events (no per-launch event overhead).  Uses the operator (theta dt, 1) of the last
+ * hf_simulate* call and the primary system's current vectors; the replay runs the init kernel
+ * first so that every replayed launch computes PCG iteration 0 (d = s, q = A d, d.q), which costs
+ * the same as any other iteration.  Leaves the primary system's PCG state undefined (the next
+ * hf_cg / hf_simulate* call resets it).  Errors: HF_E_STATE (no previous simulation). */
+hf_status hf_time_kernel_a(hf_ctx *ctx, int32_t reps, double *ms_per_launch);
+
 /* Loop driver: 0 = CUDA graph with device-side WHILE loop (default), 1 = host loop.
  * Profiling (hf_profile) and the in-process slab transport always use the host loop. */
 hf_status hf_set_driver(hf_ctx *ctx, int32_t driver);

@@ -83,6 +83,7 @@ _SIGS = {
     "hf_set_step_flush": (_i32, [_vp, _i32]),
     "hf_set_element": (_i32, [_vp, _i32]),
     "hf_set_precision": (_i32, [_vp, _i32]),
+    "hf_time_kernel_a": (_i32, [_vp, _i32, C.POINTER(C.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -349,6 +350,13 @@ def hf_set_driver(ctx: Context, driver: int):
 
 def hf_flush_l2(ctx: Context):
     _check(_lib.hf_flush_l2(ctx.ptr))
+
+
+def hf_time_kernel_a(ctx: Context, reps: int = 200) -> float:
+    """ms per launch of PCG kernel A replayed back to back (instrumentation, see heatfem.h)."""
+    ms = C.c_double()
+    _check(_lib.hf_time_kernel_a(ctx.ptr, reps, C.byref(ms)))
+    return ms.value
 
 
 def hf_set_precision(ctx: Context, bits: int):

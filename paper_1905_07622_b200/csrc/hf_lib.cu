@@ -228,6 +228,7 @@ struct hf_ctx {
     Comm *comm = nullptr;
     bool step_flush = false;
     double last_ms_steps = 0.0;      // per-step event total of the last run (step_flush)
+    double last_aK = 0.0;            // operator (aK, 1) of the last time loop (hf_time_kernel_a)
     bool prof = false;
     double prof_ms[5] = {0, 0, 0, 0, 0};
     long long prof_n[5] = {0, 0, 0, 0, 0};
@@ -1367,6 +1368,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
                               bool first, int snap_local, double *snapdev, const hf_cg_opts &o)
 {
     const double aK = theta * dt, aM = 1.0;             // A = M + theta dt K
+    c->last_aK = aK;
     const double aKL = -(1.0 - theta) * dt, aML = 1.0;  // L = M - (1-theta) dt K   (R8)
     HFCK(set_solver_opts(c, s, o));
     if (s.iters_cap < nsteps) {
@@ -2010,6 +2012,50 @@ hf_status hf_profile_read(hf_ctx *c, double ms[5], int64_t n[5])
         if (ms) ms[i] = c->prof_ms[i];
         if (n) n[i] = c->prof_n[i];
     }
+    return HF_OK;
+}
+
+hf_status hf_time_kernel_a(hf_ctx *c, int32_t reps, double *ms_per_launch)
+{
+    if (!c || reps < 1 || !ms_per_launch) return fail(HF_E_ARG, "hf_time_kernel_a: bad argument");
+    if (!(c->last_aK > 0.0)) return fail(HF_E_STATE, "hf_time_kernel_a: no previous simulation");
+    CUCK(cudaSetDevice(c->device));
+    Sys &s = c->sys0;
+    hf_cg_opts o = resolved(c, {1e-12, 10000, -1});
+    o.max_iter = 1 << 30;                       // every replayed launch must run
+    HFCK(set_solver_opts(c, s, o));
+    StencilArgs ia = base_args(c, c->last_aK, 1.0);
+    ia.invd = s.invd;
+    ia.bvec = s.b;
+    ia.out0 = s.r;
+    ia.out_s = s.s;
+    ia.first = 1;
+    ia.rot_role = ROT_INIT;
+    for (int i = 0; i < 3; i++) ia.ring[i] = s.U[i];
+    ia.sy = make_sync(c, s, -1, 1);
+    ia.zs0 = c->own_lo;
+    ia.zs1 = c->own_hi;
+    Launch init;
+    HFCK(stencil_launch(c, LD_X0, EP_RESID_INIT, true, s.maps, ia, 2, &init));
+    CgLaunches L;
+    HFCK(cg_launches(c, s, c->last_aK, 1.0, nullptr, s.maps, &L));
+    const bool prof = c->prof;
+    c->prof = false;
+    HFCK(run(c, init, s.stream));
+    HFCK(run(c, L.A, s.stream));                // warm
+    cudaEvent_t e0, e1;
+    CUCK(cudaEventCreate(&e0));
+    CUCK(cudaEventCreate(&e1));
+    CUCK(cudaEventRecord(e0, s.stream));
+    for (int i = 0; i < reps; i++) HFCK(run(c, L.A, s.stream));
+    CUCK(cudaEventRecord(e1, s.stream));
+    CUCK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    c->prof = prof;
+    *ms_per_launch = ms / reps;
     return HF_OK;
 }
 

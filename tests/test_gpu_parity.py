@@ -261,6 +261,21 @@ def test_failed_step_stops_the_run(driver, unroll):
     assert st2["first_failed_step"] == -1 and rel(N(u2), uo) <= 1e-10
 
 
+def test_time_kernel_a_replay_then_simulate():
+    """Instrumentation replay of kernel A leaves the context usable: the next run matches."""
+    p = synth.c1()
+    ug, st0, _, ctx = _gpu_sim(p)
+    with pytest.raises(hf.HfError):
+        hf.hf_time_kernel_a(make_ctx(p.grid, p.k, p.c), 5)      # no simulation yet: HF_E_STATE
+    ms = hf.hf_time_kernel_a(ctx, 20)
+    assert 0.0 < ms < 10.0
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
+    u = T(p.u0)
+    st1 = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, F, u, rtol=p.rtol)
+    assert np.array_equal(N(u), ug) and st1["total_iters"] == st0["total_iters"]
+
+
 @pytest.mark.parametrize("unroll", [2, 4])
 def test_unrolled_loop_body_bitwise_equal(unroll):
     p = synth.c1()
