@@ -46,6 +46,8 @@ def lib():
         L.or_create.restype = C.c_void_p
         L.or_create.argtypes = [_i64p, _dp, _dp, _dp, _dp, C.c_int, C.c_int]
         L.or_tet_voxel_matrices.argtypes = [_dp, _dp, _dp]
+        L.or_create_vertex.restype = C.c_void_p
+        L.or_create_vertex.argtypes = [_i64p, _dp, _dp, _dp, _dp, C.c_int, C.c_int]
         L.or_destroy.argtypes = [C.c_void_p]
         L.or_element_matrices.argtypes = [_dp, _dp, _dp]
         L.or_get_element_matrices.argtypes = [C.c_void_p, _dp, _dp]
@@ -91,14 +93,18 @@ def _f64(a):
 class Oracle:
     """Assembled-matrix reference for one grid and one (k, c) field."""
 
-    def __init__(self, grid, k, c, assemble: bool = True, elem: int = 0):
+    def __init__(self, grid, k, c, assemble: bool = True, elem: int = 0, vertex: bool = False):
+        """k, c per element; vertex=True: k, c per node, averaged over each element's vertices
+        (Q1: the voxel's 8 corners; elem=1: each tet's 4 vertices)."""
         self.grid = grid
         self.nn = grid.n_nodes
         self._k = _f64(k)
         self._c = _f64(c)
-        assert self._k.size == grid.n_elems and self._c.size == grid.n_elems
-        self._p = lib().or_create(np.asarray(grid.ne, dtype=np.int64), _f64(grid.h), _f64(grid.origin),
-                                  self._k, self._c, 1 if assemble else 0, elem)
+        n = grid.n_nodes if vertex else grid.n_elems
+        assert self._k.size == n and self._c.size == n
+        create = lib().or_create_vertex if vertex else lib().or_create
+        self._p = create(np.asarray(grid.ne, dtype=np.int64), _f64(grid.h), _f64(grid.origin),
+                         self._k, self._c, 1 if assemble else 0, elem)
         self.elem = elem
         if not self._p:
             raise MemoryError("or_create failed")

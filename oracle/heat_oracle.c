@@ -39,9 +39,13 @@ typedef struct {
     double h[3];
     double origin[3];
     int64_t nnodes, nelems;
-    int elem;              /* 0: trilinear hexahedron (R1), 1: 6 P1 tets per voxel (f1)       */
+    int elem;              /* 0: trilinear hexahedron (R1), 1: 6 P1 tets per voxel (f1),          */
+                           /* 2: 6 P1 tets, each with its own coefficient (vertex averages) */
     double Ke[64], Me[64]; /* voxel element matrices (unit k, unit c) */
     double *k, *c;         /* per-element coefficients (copies) */
+    double *kt, *ct;       /* elem 2: per-tet coefficients, 6 per voxel */
+    double Kt[6][16], Mt[6][16];   /* elem 2: unit-coefficient tet matrices, local order of tloc */
+    int tloc[6][4];        /* elem 2: voxel-local nodes of each tet */
     /* CSR of K and M (same pattern) */
     int has_csr;
     int64_t *rowptr;
@@ -180,6 +184,25 @@ static void elem_nodes(const or_ctx *o, int64_t e, int64_t nodes[8])
         nodes[l] = node_id(o, ex + (l & 1), ey + ((l >> 1) & 1), ez + ((l >> 2) & 1));
 }
 
+/* Coefficient-scaled matrices of voxel e in its 8 local nodes: k_e K_e, c_e M_e (elem 0, 1), or */
+/* the sum over its 6 tets of k_t K_t, c_t M_t with per-tet coefficients (elem 2).              */
+static void elem_scaled(const or_ctx *o, int64_t e, double Kel[64], double Mel[64])
+{
+    if (o->elem != 2) {
+        for (int i = 0; i < 64; i++) { Kel[i] = o->k[e] * o->Ke[i]; Mel[i] = o->c[e] * o->Me[i]; }
+        return;
+    }
+    for (int i = 0; i < 64; i++) { Kel[i] = 0.0; Mel[i] = 0.0; }
+    for (int t = 0; t < 6; t++) {
+        double kt = o->kt[6 * e + t], ct = o->ct[6 * e + t];
+        for (int a = 0; a < 4; a++)
+            for (int b = 0; b < 4; b++) {
+                Kel[o->tloc[t][a] * 8 + o->tloc[t][b]] += kt * o->Kt[t][a * 4 + b];
+                Mel[o->tloc[t][a] * 8 + o->tloc[t][b]] += ct * o->Mt[t][a * 4 + b];
+            }
+    }
+}
+
 /* ------------------------------------------------------------------------------------------ */
 /* Assembly: scatter-add every element matrix into 27 structured slots per row,      */
 /* then compact to CSR (rows sorted, columns ascending).                                        */
@@ -193,15 +216,17 @@ static int assemble_csr(or_ctx *o)
     if (!Ks || !Ms || !used) { free(Ks); free(Ms); free(used); return OR_E_OOM; }
     for (int64_t e = 0; e < o->nelems; e++) {
         int64_t nodes[8];
+        double Kel[64], Mel[64];
         elem_nodes(o, e, nodes);
+        elem_scaled(o, e, Kel, Mel);
         for (int a = 0; a < 8; a++)
             for (int b = 0; b < 8; b++) {
                 /* slot = offset of node b relative to node a, (dx,dy,dz) in {-1,0,1}^3 */
                 int dx = (b & 1) - (a & 1), dy = ((b >> 1) & 1) - ((a >> 1) & 1), dz = ((b >> 2) & 1) - ((a >> 2) & 1);
                 int slot = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
                 size_t at = (size_t)nodes[a] * 27 + slot;
-                Ks[at] += o->k[e] * o->Ke[a * 8 + b];
-                Ms[at] += o->c[e] * o->Me[a * 8 + b];
+                Ks[at] += Kel[a * 8 + b];
+                Ms[at] += Mel[a * 8 + b];
                 used[at] = 1;
             }
     }
@@ -260,10 +285,63 @@ or_ctx *or_create(const int64_t ne[3], const double h[3], const double origin[3]
     return o;
 }
 
+/* Materials given per node (vertex values, "computed ... at each vertex and the values      */
+/* averaged over each element", "averaged over the element"): elem 0 -> each voxel's        */
+/* coefficient is the mean of its 8 corners; elem 1 -> each tet's coefficient is the mean of its 4 */
+/* vertices (the oracle then runs in elem mode 2).                                                */
+or_ctx *or_create_vertex(const int64_t ne[3], const double h[3], const double origin[3],
+                         const double *kn, const double *cn, int assemble, int elem)
+{
+    const int64_t nx1 = ne[0] + 1, ny1 = ne[1] + 1, nel = ne[0] * ne[1] * ne[2];
+    double *ke = malloc(sizeof(double) * (size_t)nel), *ce = malloc(sizeof(double) * (size_t)nel);
+    if (!ke || !ce) { free(ke); free(ce); return NULL; }
+    for (int64_t e = 0; e < nel; e++) {      /* per-voxel corner means (elem 0; placeholders for 1) */
+        int64_t ex = e % ne[0], ey = (e / ne[0]) % ne[1], ez = e / (ne[0] * ne[1]);
+        double sk = 0.0, sc = 0.0;
+        for (int l = 0; l < 8; l++) {
+            int64_t n = (ex + (l & 1)) + nx1 * ((ey + ((l >> 1) & 1)) + ny1 * (ez + ((l >> 2) & 1)));
+            sk += kn[n];
+            sc += cn[n];
+        }
+        ke[e] = sk / 8.0;
+        ce[e] = sc / 8.0;
+    }
+    or_ctx *o = or_create(ne, h, origin, ke, ce, elem == 1 ? 0 : assemble, elem);
+    free(ke);
+    free(ce);
+    if (!o || elem != 1) return o;
+    o->elem = 2;
+    o->kt = malloc(sizeof(double) * (size_t)nel * 6);
+    o->ct = malloc(sizeof(double) * (size_t)nel * 6);
+    if (!o->kt || !o->ct) return NULL;
+    for (int t = 0; t < 6; t++) {
+        or_tet_vertices(t, o->tloc[t]);
+        double p[4][3];
+        for (int v = 0; v < 4; v++)
+            for (int d = 0; d < 3; d++) p[v][d] = ((o->tloc[t][v] >> d) & 1) * h[d];
+        or_tet_matrices(p, o->Kt[t], o->Mt[t]);
+    }
+    for (int64_t e = 0; e < nel; e++) {
+        int64_t nodes[8];
+        elem_nodes(o, e, nodes);
+        for (int t = 0; t < 6; t++) {
+            double sk = 0.0, sc = 0.0;
+            for (int v = 0; v < 4; v++) {
+                sk += kn[nodes[o->tloc[t][v]]];
+                sc += cn[nodes[o->tloc[t][v]]];
+            }
+            o->kt[6 * e + t] = sk / 4.0;
+            o->ct[6 * e + t] = sc / 4.0;
+        }
+    }
+    if (assemble && assemble_csr(o) != OR_OK) return NULL;
+    return o;
+}
+
 void or_destroy(or_ctx *o)
 {
     if (!o) return;
-    free(o->k); free(o->c); free(o->rowptr); free(o->col); free(o->Kv); free(o->Mv);
+    free(o->k); free(o->c); free(o->kt); free(o->ct); free(o->rowptr); free(o->col); free(o->Kv); free(o->Mv);
     free(o->isD); free(o->g); free(o);
 }
 
@@ -304,11 +382,13 @@ void or_apply_ebe(const or_ctx *o, double aK, double aM, const double *u, double
     for (int64_t n = 0; n < o->nnodes; n++) y[n] = 0.0;
     for (int64_t e = 0; e < o->nelems; e++) {
         int64_t nodes[8];
+        double Kel[64], Mel[64];
         elem_nodes(o, e, nodes);
+        elem_scaled(o, e, Kel, Mel);
         for (int a = 0; a < 8; a++) {
             double s = 0.0;
             for (int b = 0; b < 8; b++)
-                s += (aK * o->k[e] * o->Ke[a * 8 + b] + aM * o->c[e] * o->Me[a * 8 + b]) * u[nodes[b]];
+                s += (aK * Kel[a * 8 + b] + aM * Mel[a * 8 + b]) * u[nodes[b]];
             y[nodes[a]] += s;
         }
     }
@@ -327,9 +407,11 @@ void or_apply_rows(const or_ctx *o, double aK, double aM, const double *u,
             if (ex < 0 || ey < 0 || ez < 0 || ex >= o->ne[0] || ey >= o->ne[1] || ez >= o->ne[2]) continue;
             int64_t e = ex + o->ne[0] * (ey + o->ne[1] * ez);
             int64_t nodes[8];
+            double Kel[64], Mel[64];
             elem_nodes(o, e, nodes);
+            elem_scaled(o, e, Kel, Mel);
             for (int b = 0; b < 8; b++)
-                s += (aK * o->k[e] * o->Ke[l * 8 + b] + aM * o->c[e] * o->Me[l * 8 + b]) * u[nodes[b]];
+                s += (aK * Kel[l * 8 + b] + aM * Mel[l * 8 + b]) * u[nodes[b]];
         }
         out[t] = s;
     }
@@ -383,7 +465,7 @@ static int face_load_tets(const or_ctx *o, int face, double f_const, const doubl
 
 int or_face_load(const or_ctx *o, int face, double f_const, const double *beam, double *F)
 {
-    if (o->elem == 1) return (face < 0 || face > 5) ? OR_E_ARG : face_load_tets(o, face, f_const, beam, F);
+    if (o->elem >= 1) return (face < 0 || face > 5) ? OR_E_ARG : face_load_tets(o, face, f_const, beam, F);
     if (face < 0 || face > 5) return OR_E_ARG;
     int nd = face / 2;                       /* normal axis */
     int ax = nd == 0 ? 1 : 0;                /* first in-plane axis */

@@ -415,3 +415,78 @@ def test_tet_time_stepper_matches_direct():
     A = o.csr(0.025, 1.0).tocsc()
     xd = spla.spsolve(A, o.rhs(0.5, 0.05, F, np.zeros(g.n_nodes)))
     assert st == 0 and np.linalg.norm(u - xd) <= 1e-10 * np.linalg.norm(xd)
+
+
+# ---------------------------------------------------------------------------------------------
+# Vertex materials averaged over each element ("computed ... at each vertex and the values
+# averaged over each element"): Q1 voxels average 8 corners, tets average their 4 vertices.
+
+def _brute_tet_vertex_assembly(g, kn, cn):
+    """Dense K, M of the Kuhn 6-tet mesh with per-tet coefficients = mean of the tet's 4 vertex
+    values, built here from scratch (numpy: edge matrix inverse for the P1 gradients)."""
+    import itertools
+    nx, ny, nz = g.ne
+    nx1, ny1 = nx + 1, ny + 1
+    N = g.n_nodes
+    K = np.zeros((N, N))
+    M = np.zeros((N, N))
+    h = np.asarray(g.h)
+    for ez, ey, ex in itertools.product(range(nz), range(ny), range(nx)):
+        for perm in itertools.permutations(range(3)):
+            b = np.zeros(3, dtype=int)
+            verts = [b.copy()]
+            for ax in perm:
+                b[ax] = 1
+                verts.append(b.copy())
+            idx = [(ex + v[0]) + nx1 * ((ey + v[1]) + ny1 * (ez + v[2])) for v in verts]
+            P = np.array([v * h for v in verts], dtype=float)
+            E = (P[1:] - P[0]).T                        # columns p_i - p_0
+            Ginv = np.linalg.inv(E)                     # rows: grad lambda_1..3
+            grads = np.vstack([-Ginv.sum(axis=0), Ginv])
+            vol = abs(np.linalg.det(E)) / 6.0
+            kt = np.mean(kn[idx])
+            ct = np.mean(cn[idx])
+            Kt = vol * grads @ grads.T
+            Mt = vol * (np.ones((4, 4)) + np.eye(4)) / 20.0
+            for a in range(4):
+                for bb in range(4):
+                    K[idx[a], idx[bb]] += kt * Kt[a, bb]
+                    M[idx[a], idx[bb]] += ct * Mt[a, bb]
+    return K, M
+
+
+def test_vertex_materials_tets_match_brute_force():
+    g = synth.Grid((3, 2, 2), (0.5, 0.4, 0.3), (1.0, -1.0, 0.0))
+    rng = np.random.default_rng(5)
+    kn = rng.uniform(1.0, 100.0, g.n_nodes)
+    cn = rng.uniform(0.5, 2.0, g.n_nodes)
+    o = oracle.Oracle(g, kn, cn, elem=1, vertex=True)
+    K, M = _brute_tet_vertex_assembly(g, kn, cn)
+    assert np.allclose(o.csr(1.0, 0.0).toarray(), K, rtol=0, atol=1e-12 * np.abs(K).max())
+    assert np.allclose(o.csr(0.0, 1.0).toarray(), M, rtol=0, atol=1e-14 * np.abs(M).max())
+    u = rng.standard_normal(g.n_nodes)
+    assert np.allclose(o.apply_ebe(0.3, 1.2, u), (0.3 * K + 1.2 * M) @ u, atol=1e-11)
+    rows = np.array([0, 5, 17, g.n_nodes - 1])
+    assert np.allclose(o.apply_rows(0.3, 1.2, u, rows), ((0.3 * K + 1.2 * M) @ u)[rows], atol=1e-11)
+
+
+def test_vertex_materials_constant_field_and_q1_corner_mean():
+    g = synth.Grid((4, 3, 2), (0.3, 0.3, 0.2))
+    ones = np.ones(g.n_nodes)
+    # constant vertex fields: per-tet coefficients all equal -> the per-voxel tet operator
+    o1 = oracle.Oracle(g, 7.0 * ones, 2.0 * ones, elem=1, vertex=True)
+    o2 = oracle.Oracle(g, np.full(g.n_elems, 7.0), np.full(g.n_elems, 2.0), elem=1)
+    assert np.allclose(o1.csr(1.0, 1.0).toarray(), o2.csr(1.0, 1.0).toarray(), rtol=1e-14, atol=0)
+    # Q1: each voxel's coefficient is the mean of its 8 corners (computed here by slicing)
+    rng = np.random.default_rng(6)
+    kn = rng.uniform(1.0, 5.0, g.n_nodes)
+    cn = rng.uniform(1.0, 5.0, g.n_nodes)
+    nx, ny, nz = g.ne
+    kv = kn.reshape(nz + 1, ny + 1, nx + 1)
+    cv = cn.reshape(nz + 1, ny + 1, nx + 1)
+    corner = lambda a: sum(a[dz:dz + nz, dy:dy + ny, dx:dx + nx] for dz in (0, 1) for dy in (0, 1) for dx in (0, 1)) / 8
+    oq = oracle.Oracle(g, kn, cn, elem=0, vertex=True)
+    oe = oracle.Oracle(g, corner(kv).ravel(), corner(cv).ravel(), elem=0)
+    assert np.allclose(oq.csr(0.4, 1.0).toarray(), oe.csr(0.4, 1.0).toarray(), rtol=1e-14, atol=0)
+    # tets: the face load does not depend on the coefficients
+    assert np.array_equal(o1.face_load(synth.FACE_ZM, 1.0), o2.face_load(synth.FACE_ZM, 1.0))
