@@ -121,6 +121,16 @@ hf_status hf_set_dirichlet_faces(hf_ctx *ctx, uint32_t face_bits, const double v
  * Errors: HF_E_ARG. */
 hf_status hf_set_element(hf_ctx *ctx, int32_t type);
 
+/* Materials given per node instead of per element (the paper's scheme: the material function is
+ * "computed ... at each vertex and the values averaged over each element").
+ * k_node, c_node: n_nodes fp64 of the GLOBAL grid (natural node order; slab contexts use their
+ * planes).  Q1 elements: each voxel's (k_e, c_e) is the mean of its 8 corners.  Type-1 elements
+ * (6 tets): each tet's (k_t, c_t) is the mean of its 4 vertices, evaluated inside the stencil from
+ * per-node pairs (kernel variant EL_TETV).  Set the element type first; hf_set_coefficients
+ * switches back to per-element values.  Not available with hf_simulate_batched (HF_E_STATE).
+ * Errors: HF_E_ARG. */
+hf_status hf_set_vertex_coefficients(hf_ctx *ctx, const double *k_node, const double *c_node);
+
 /* Storage precision of the context's node vectors and (k, c) pairs: 64 (default) or 32, the
  * fp32 variant (NEXT row f3; the paper also ran single precision).  With 32 the
  * operator, the vector updates and the face load run in fp32 while every dot product, the PCG

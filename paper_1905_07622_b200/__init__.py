@@ -83,6 +83,7 @@ _SIGS = {
     "hf_set_step_flush": (_i32, [_vp, _i32]),
     "hf_set_element": (_i32, [_vp, _i32]),
     "hf_set_precision": (_i32, [_vp, _i32]),
+    "hf_set_vertex_coefficients": (_i32, [_vp, _vp, _vp]),
     "hf_time_kernel_a": (_i32, [_vp, _i32, C.POINTER(C.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -169,6 +170,7 @@ class Context:
         self.n_elems = self.ne[0] * self.ne[1] * self.ne[2]
         self.n_plane = (self.ne[0] + 1) * (self.ne[1] + 1)
         self.n_nodes = self.n_plane * local_planes   # local (slab) node count
+        self.n_nodes_global = self.n_plane * (self.ne[2] + 1)
 
     def __del__(self):
         if getattr(self, "ptr", None) and self.ptr.value:
@@ -201,6 +203,12 @@ def hf_destroy(ctx: Context):
 
 def hf_set_coefficients(ctx: Context, k, c):
     _check(_lib.hf_set_coefficients(ctx.ptr, _ptr(k, ctx.n_elems, "k"), _ptr(c, ctx.n_elems, "c")))
+
+
+def hf_set_vertex_coefficients(ctx: Context, k_node, c_node):
+    """Per-node materials of the global grid, averaged over each element's vertices."""
+    n = ctx.n_nodes_global
+    _check(_lib.hf_set_vertex_coefficients(ctx.ptr, _ptr(k_node, n, "k_node"), _ptr(c_node, n, "c_node")))
 
 
 def hf_set_dirichlet_faces(ctx: Context, face_bits: int, values: Optional[Sequence[float]] = None):

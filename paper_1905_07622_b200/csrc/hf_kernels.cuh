@@ -102,7 +102,29 @@ template <class Real> struct Vec2;
 template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
 
-enum { EL_Q1 = 0, EL_DENSE = 1 };
+// element variants: Q1 hexahedra; the 6-tet split with one (k, c) per voxel (dense 8x8 voxel
+// matrices); the 6-tet split with per-tet coefficients averaged from vertex values
+enum { EL_Q1 = 0, EL_DENSE = 1, EL_TETV = 2 };
+
+// Kuhn tets of a voxel (local node l = bx + 2 by + 4 bz): tet t follows 0 -> e_a -> e_a+e_b -> 7
+// for the t-th axis order (x,y,z), (x,z,y), (y,x,z), (y,z,x), (z,x,y), (z,y,x)
+__host__ __device__ constexpr int tet_loc(int t, int v)
+{
+    return v == 0 ? 0 : v == 3 ? 7
+         : (t == 0 ? (v == 1 ? 1 : 3) : t == 1 ? (v == 1 ? 1 : 5) : t == 2 ? (v == 1 ? 2 : 3)
+          : t == 3 ? (v == 1 ? 2 : 6) : t == 4 ? (v == 1 ? 4 : 5) : (v == 1 ? 4 : 6));
+}
+
+// EL_TETV constants: aK-scaled tet stiffness matrices in tet_loc order and the mass scale
+// m = aM V_tet / 20 (M_ij = m (1 + delta_ij) for every tet)
+struct TetV {
+    double K[6][16];
+    double m;
+};
+struct TetVF {
+    float K[6][16];
+    float m;
+};
 
 struct Sync {               // per-system reduction plumbing
     CgState *st;
@@ -117,8 +139,10 @@ struct Sync {               // per-system reduction plumbing
 struct Maps {               // TMA descriptors (host copy; kernels read a device-memory copy)
     CUtensorMap node[NMAPS];
     CUtensorMap kc;         // fp64 view (2 nx, ny, nzl + 1) of the (k, c) pairs, layer L at z = L + 1
+    CUtensorMap kcn;        // EL_TETV: per-node (k, c) pairs, view (2 nx1, ny1, nzl), node layout
 };
-constexpr int MAP_KC = NMAPS;   // index of the kc map in a device Maps array
+constexpr int MAP_KC = NMAPS;       // index of the kc map in a device Maps array
+constexpr int MAP_KCN = NMAPS + 1;  // index of the per-node pair map
 
 struct StencilArgs {
     Geom g;
@@ -141,6 +165,8 @@ struct StencilArgs {
     LamF lamf;                    // fp32 variant: lam in float
     Dense dn;                     // EL_DENSE only
     DenseF dnf;                   // EL_DENSE, fp32 variant
+    TetV tv;                      // EL_TETV only
+    TetVF tvf;                    // EL_TETV, fp32 variant
 };
 // Node-vector pointers of StencilArgs / BArgs / StepArgs are declared double* but address
 // vectors of the context's storage type; kernels instantiated for Real = float reinterpret them.
@@ -376,7 +402,7 @@ __device__ __forceinline__ IterStart iter_start(const CgState *st, int i, const 
 
 // ---- the stencil kernel (operator apply with fused prologue/epilogue) ---------------------
 
-template <int R, int NW, int LD, class Real = double>
+template <int R, int NW, int LD, class Real = double, int EL = EL_Q1>
 struct StencilShape {
     static constexpr int ES = (int)sizeof(Real);
     static constexpr int H = NW * R + 1;                                     // node rows per box
@@ -387,7 +413,8 @@ struct StencilShape {
     static constexpr int AL = 128 / ES;                                      // elements per 128 B
     static constexpr int NODE_BOX = H * BW;                                  // elements per node box
     static constexpr int NODE_DBL = (NODE_BOX + AL - 1) / AL * AL;           // 128-B aligned slot
-    static constexpr int KC_DBL = NW * R * KW;                               // elements per kc box
+    // per-element (k, c) box: NW R element rows x KW; EL_TETV: per-node pairs, H rows x 2 BW
+    static constexpr int KC_DBL = EL == EL_TETV ? H * 2 * BW : NW * R * KW;
     static constexpr int STAGE_DBL = (NA * NODE_DBL + KC_DBL + AL - 1) / AL * AL;
     static constexpr unsigned STAGE_BYTES = (NA * NODE_BOX + KC_DBL) * (unsigned)ES;   // TMA bytes
     // rounded to 1 KB so that CTAs of different variants sharing an SM get aligned windows
@@ -406,7 +433,8 @@ template <int R, int NW, int NS, int LD, int EP, int FL, int EL, class Real>
 __global__ void __launch_bounds__(32 * NW)
 k_stencil(const __grid_constant__ StencilArgs a)
 {
-    using SH = StencilShape<R, NW, LD, Real>;
+    using SH = StencilShape<R, NW, LD, Real, EL>;
+    constexpr int KMAP = EL == EL_TETV ? MAP_KCN : MAP_KC;
     using V2 = typename Vec2<Real>::type;
     constexpr int ES = (int)sizeof(Real);
     constexpr int NT = 32 * NW;
@@ -425,6 +453,8 @@ k_stencil(const __grid_constant__ StencilArgs a)
     auto LMB = [&](int ch) -> Real { if constexpr (ES == 8) return a.lam.mb[ch]; else return a.lamf.mb[ch]; };
     auto DK = [&](int i) -> Real { if constexpr (ES == 8) return a.dn.K[i]; else return a.dnf.K[i]; };
     auto DM = [&](int i) -> Real { if constexpr (ES == 8) return a.dn.M[i]; else return a.dnf.M[i]; };
+    auto TK = [&](int t, int i) -> Real { if constexpr (ES == 8) return a.tv.K[t][i]; else return a.tvf.K[t][i]; };
+    auto TMS = [&]() -> Real { if constexpr (ES == 8) return a.tv.m; else return a.tvf.m; };
     const int lane = threadIdx.x, w = threadIdx.y;
     const int tid = lane + 32 * w;
     const int blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -501,8 +531,10 @@ k_stencil(const __grid_constant__ StencilArgs a)
         mbar_expect_tx(&bars[st], SH::STAGE_BYTES);
         if (NA >= 1) tma_load_3d(sb, a.tm + map0, xb, Y0 - 1, p, &bars[st]);
         if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, a.tm + map1, xb, Y0 - 1, p, &bars[st]);
-        // element layer L = p - 1 sits at z = p in the kc tensor
-        tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KC, kb, Y0 - 1, p, &bars[st]);
+        if (EL == EL_TETV)   // per-node (k, c) pairs of plane p, same rows as the node box
+            tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KCN, 2 * xb, Y0 - 1, p, &bars[st]);
+        else                 // element layer L = p - 1 sits at z = p in the kc tensor
+            tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KC, kb, Y0 - 1, p, &bars[st]);
     };
 
     if (tid == 0) {
@@ -512,7 +544,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
         if (a.tm_fence) {
             if (NA >= 1) tensormap_acquire(a.tm + map0);
             if (NA >= 2) tensormap_acquire(a.tm + map1);
-            tensormap_acquire(a.tm + MAP_KC);
+            tensormap_acquire(a.tm + KMAP);
         }
     }
     __syncthreads();
@@ -567,6 +599,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     Real Fp[R][4];            // Q1: face transforms of the lower plane p-1
     Real Cy[R][4];            // contributions carried from the layer below (face / node space)
     Real Pv[R + 1], Pv1[R + 1];   // dense: node values of plane p-1 at x and x+1
+    V2 PK0[R + 1], PK1[R + 1];    // EL_TETV: node (k, c) pairs of plane p-1 at x and x+1
     Real cen[R];              // raw centre values of plane p-1 (rows 0..R-1)
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -576,7 +609,11 @@ k_stencil(const __grid_constant__ StencilArgs a)
         cen[r] = Real(0);
     }
 #pragma unroll
-    for (int r = 0; r <= R; r++) { Pv[r] = Real(0); Pv1[r] = Real(0); }
+    for (int r = 0; r <= R; r++) {
+        Pv[r] = Real(0);
+        Pv1[r] = Real(0);
+        PK0[r].x = PK0[r].y = PK1[r].x = PK1[r].y = Real(0);
+    }
 
     for (int it = 0; it < nplanes; ++it) {
         const int p = zb - 1 + it;
@@ -590,6 +627,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
         const Real *n0 = sb + w * R * SH::BW + lane + xoff;                 // row 0 of this warp
         const Real *n1 = sb + SH::NODE_DBL + w * R * SH::BW + lane + xoff;
         const Real *kcs = sb + NA * SH::NODE_DBL + w * R * SH::KW + koff + 2 * lane;
+        const Real *kns = sb + NA * SH::NODE_DBL + w * R * (2 * SH::BW) + 2 * (lane + xoff);   // EL_TETV
         // ---- node values of plane p (rows 0..R), x butterfly (edges) ----------------------
         Real S[R + 1], D[R + 1], V0[R + 1], V1[R + 1], craw[R];
         const bool store_p = (EP == EP_CGA || EP == EP_RESID_INIT) && (p >= a.zs0 && p < a.zs1) &&
@@ -672,24 +710,69 @@ k_stencil(const __grid_constant__ StencilArgs a)
                 yv[e] = (E0 + E1) + left;                   // lane 0's value is not owned
             }
         } else {
-            // ---- dense voxel matrices (6-tet split): u_e = 4 values of plane p-1 + 4 of p ----
+            // ---- 6-tet split: u_e = 4 values of plane p-1 + 4 of p ----------------------------
             Real B4[R][4];
+            V2 KN0[R + 1], KN1[R + 1];             // EL_TETV: node pairs of plane p at x, x+1
+            if constexpr (EL == EL_TETV) {
+#pragma unroll
+                for (int r = 0; r <= R; r++) {
+                    KN0[r] = *reinterpret_cast<const V2 *>(kns + r * 2 * SH::BW);
+                    KN1[r] = *reinterpret_cast<const V2 *>(kns + r * 2 * SH::BW + 2);
+                }
+            }
 #pragma unroll
             for (int r = 0; r < R; r++) {
-                const V2 kc = *reinterpret_cast<const V2 *>(kcs + r * SH::KW);
                 const Real ue[8] = {Pv[r], Pv1[r], Pv[r + 1], Pv1[r + 1], V0[r], V1[r], V0[r + 1], V1[r + 1]};
+                if constexpr (EL == EL_DENSE) {
+                    // one (k, c) per voxel: dense 8x8 voxel matrices
+                    const V2 kc = *reinterpret_cast<const V2 *>(kcs + r * SH::KW);
 #pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    Real yk = Real(0), ym = Real(0);
+                    for (int i = 0; i < 8; i++) {
+                        Real yk = Real(0), ym = Real(0);
 #pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        yk = fma(DK(i * 8 + j), ue[j], yk);
-                        ym = fma(DM(i * 8 + j), ue[j], ym);
+                        for (int j = 0; j < 8; j++) {
+                            yk = fma(DK(i * 8 + j), ue[j], yk);
+                            ym = fma(DM(i * 8 + j), ue[j], ym);
+                        }
+                        const Real y = fma(kc.x, yk, kc.y * ym);
+                        if (i < 4) B4[r][i] = Cy[r][i] + y;      // bottom plane p-1 complete
+                        else Cy[r][i - 4] = y;                   // top plane p, carried
                     }
-                    const Real y = fma(kc.x, yk, kc.y * ym);
-                    if (i < 4) B4[r][i] = Cy[r][i] + y;      // bottom plane p-1 complete
-                    else Cy[r][i - 4] = y;                   // top plane p, carried
+                } else {
+                    // per-tet coefficients = means of the tet's 4 vertex values
+                    const V2 ke[8] = {PK0[r], PK1[r], PK0[r + 1], PK1[r + 1], KN0[r], KN1[r], KN0[r + 1], KN1[r + 1]};
+                    const int ey = yb + r, ez = p - 1 + g.zg0;
+                    const bool vin = xi >= 0 && xi < g.nx && ey >= 0 && ey < g.ny && ez >= 0 && ez < g.nz1g - 1;
+                    Real yl[8];
+#pragma unroll
+                    for (int i = 0; i < 8; i++) yl[i] = Real(0);
+#pragma unroll
+                    for (int t = 0; t < 6; t++) {
+                        const int l0 = tet_loc(t, 0), l1 = tet_loc(t, 1), l2 = tet_loc(t, 2), l3 = tet_loc(t, 3);
+                        const int lv[4] = {l0, l1, l2, l3};
+                        // voxels outside the domain (halo lanes, phantom layers) would average
+                        // boundary vertex values: their tets carry no coefficient
+                        const Real kt = vin ? Real(0.25) * ((ke[l0].x + ke[l1].x) + (ke[l2].x + ke[l3].x)) : Real(0);
+                        const Real cm = vin ? Real(0.25) * ((ke[l0].y + ke[l1].y) + (ke[l2].y + ke[l3].y)) * TMS() : Real(0);
+                        const Real su = (ue[l0] + ue[l1]) + (ue[l2] + ue[l3]);
+#pragma unroll
+                        for (int i = 0; i < 4; i++) {
+                            Real ku = Real(0);
+#pragma unroll
+                            for (int j = 0; j < 4; j++) ku = fma(TK(t, i * 4 + j), ue[lv[j]], ku);
+                            yl[lv[i]] = fma(kt, ku, fma(cm, su + ue[lv[i]], yl[lv[i]]));
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        B4[r][i] = Cy[r][i] + yl[i];
+                        Cy[r][i] = yl[i + 4];
+                    }
                 }
+            }
+            if constexpr (EL == EL_TETV) {
+#pragma unroll
+                for (int r = 0; r <= R; r++) { PK0[r] = KN0[r]; PK1[r] = KN1[r]; }
             }
 #pragma unroll
             for (int r = 0; r <= R; r++) { Pv[r] = V0[r]; Pv1[r] = V1[r]; }
@@ -930,6 +1013,96 @@ __global__ void k_diag(Geom g, const void *kcp, double aK, double aM, DiagC dc, 
     if (is_dirichlet(g, x, y, z, gv)) d = 1.0;
     if (diag) diag[i] = (Real)d;
     if (invd) invd[i] = (Real)(1.0 / d);
+}
+
+// EL_TETV diagonal: diag_i = sum over the voxels and tets containing node i of
+// aK k_t K_t[ii] + aM c_t 2m, k_t, c_t the means of the tet's 4 vertex pairs; 1 on
+// Dirichlet rows.  kd[t][v]: unit-coefficient K_t diagonal (tet_loc order), md = 2 V_tet / 20.
+struct TetDiag {
+    double kd[6][4];
+    double md;
+};
+
+template <class Real>
+__global__ void k_diag_tv(Geom g, const void *kcnp, double aK, double aM, TetDiag td, void *diagp, void *invdp,
+                          unsigned long long *launches)
+{
+    using V2 = typename Vec2<Real>::type;
+    const V2 *kcn = reinterpret_cast<const V2 *>(kcnp);
+    Real *diag = reinterpret_cast<Real *>(diagp), *invd = reinterpret_cast<Real *>(invdp);
+    const long long n = g.plane * g.nzl;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && launches) atomicAdd(launches, 1ull);
+    if (i >= n) return;
+    const int x = (int)(i % g.pitch), y = (int)((i / g.pitch) % g.ny1), z = (int)(i / g.plane);
+    if (x >= g.nx1) { if (diag) diag[i] = Real(0); if (invd) invd[i] = Real(0); return; }
+    double d = 0.0;
+    for (int l = 0; l < 8; l++) {                  // node is local node l of voxel (x-bx, y-by, z-bz)
+        const int vx = x - (l & 1), vy = y - ((l >> 1) & 1), vz = z - ((l >> 2) & 1);
+        if (vx < 0 || vy < 0 || vx >= g.nx || vy >= g.ny) continue;
+        const int zg = vz + g.zg0;
+        if (zg < 0 || zg >= g.nz1g - 1 || vz < -1 || vz + 1 >= g.nzl + 1) continue;
+        for (int t = 0; t < 6; t++) {
+            int me = -1;
+            for (int v = 0; v < 4; v++) if (tet_loc(t, v) == l) me = v;
+            if (me < 0) continue;
+            double kt = 0.0, ct = 0.0;
+            for (int v = 0; v < 4; v++) {
+                const int lv = tet_loc(t, v);
+                const int nzp = vz + ((lv >> 2) & 1);
+                if (nzp < 0 || nzp >= g.nzl) continue;   // (slab ghosts carry the pairs they need)
+                const V2 p = kcn[(long long)nzp * g.plane + (long long)(vy + ((lv >> 1) & 1)) * g.pitch + vx + (lv & 1)];
+                kt += (double)p.x;
+                ct += (double)p.y;
+            }
+            d += aK * 0.25 * kt * td.kd[t][me] + aM * 0.25 * ct * td.md;
+        }
+    }
+    double gv;
+    if (is_dirichlet(g, x, y, z, gv)) d = 1.0;
+    if (diag) diag[i] = (Real)d;
+    if (invd) invd[i] = (Real)(1.0 / d);
+}
+
+// per-node (k, c) pairs in the padded node layout (EL_TETV), from global natural node arrays
+template <class Real>
+__global__ void k_pack_nodes(Geom g, const double *k, const double *c, void *kcnp, unsigned long long *launches)
+{
+    using V2 = typename Vec2<Real>::type;
+    V2 *kcn = reinterpret_cast<V2 *>(kcnp);
+    const long long n = g.plane * g.nzl;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && launches) atomicAdd(launches, 1ull);
+    if (i >= n) return;
+    const int x = (int)(i % g.pitch), y = (int)((i / g.pitch) % g.ny1), z = (int)(i / g.plane);
+    V2 v;
+    v.x = Real(0);
+    v.y = Real(0);
+    if (x < g.nx1) {
+        const long long gi = x + (long long)g.nx1 * (y + (long long)g.ny1 * (z + g.zg0));
+        v.x = (Real)k[gi];
+        v.y = (Real)c[gi];
+    }
+    kcn[i] = v;
+}
+
+// per-voxel means of the 8 corner values (Q1 with vertex materials)
+__global__ void k_vertex_means(Geom g, int nz, const double *kn, const double *cn, double *ke, double *ce,
+                               unsigned long long *launches)
+{
+    const long long ne = (long long)g.nx * g.ny * nz;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e == 0 && launches) atomicAdd(launches, 1ull);
+    if (e >= ne) return;
+    const int ex = (int)(e % g.nx), ey = (int)((e / g.nx) % g.ny), ez = (int)(e / ((long long)g.nx * g.ny));
+    double sk = 0.0, sc = 0.0;
+    for (int l = 0; l < 8; l++) {
+        const long long n = (ex + (l & 1)) + (long long)g.nx1 * ((ey + ((l >> 1) & 1)) + (long long)g.ny1 * (ez + ((l >> 2) & 1)));
+        sk += kn[n];
+        sc += cn[n];
+    }
+    ke[e] = sk / 8.0;
+    ce[e] = sc / 8.0;
 }
 
 // ---- packing of the per-element coefficients into the (k, c) pair layout ------------------

@@ -160,6 +160,7 @@ struct SimKey {
 
 struct Sys {                         // one system's PCG workspace (Table 3 buffers)
     void *kc = nullptr;              // (k, c) pairs of the storage type, (kpitch, ny, nzl + 1)
+    void *kcn = nullptr;             // EL_TETV: per-node (k, c) pairs, padded node layout
     double *U[3] = {nullptr, nullptr, nullptr};   // time-step ring
     double *b = nullptr, *r = nullptr, *s = nullptr, *q = nullptr, *invd = nullptr;
     double *dbuf[2] = {nullptr, nullptr};
@@ -209,6 +210,7 @@ struct hf_ctx {
     unsigned dbits = 0;
     double gval[6] = {0, 0, 0, 0, 0, 0};
     int elem = EL_Q1;                // element variant (hf_set_element)
+    bool tetv = false;               // tets with per-tet vertex-averaged coefficients (EL_TETV)
     DiagC dg;                        // diagonal entries of K_ref, M_ref per local node
     Sys sys0;
     std::vector<std::unique_ptr<Sys>> pool;
@@ -441,6 +443,25 @@ static void tet_voxel(const double h[3], double K[64], double M[64])
     }
 }
 
+// Unit-coefficient stiffness of each Kuhn tet in tet_loc order (gradient-path formula as in
+// tet_voxel) and the tet volume (EL_TETV).
+static void tet_matrices(const double h[3], double K[6][16], double *V)
+{
+    *V = h[0] * h[1] * h[2] / 6.0;
+    for (int t = 0; t < 6; t++) {
+        double g[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        for (int s = 0; s < 3; s++) {
+            const int prev = tet_loc(t, s), next = tet_loc(t, s + 1);
+            const int ax = (prev ^ next) == 1 ? 0 : ((prev ^ next) == 2 ? 1 : 2);   // axis of this path step
+            g[s][ax] -= 1.0 / h[ax];
+            g[s + 1][ax] += 1.0 / h[ax];
+        }
+        for (int i = 0; i < 4; i++)
+            for (int j = 0; j < 4; j++)
+                K[t][i * 4 + j] = *V * (g[i][0] * g[j][0] + g[i][1] * g[j][1] + g[i][2] * g[j][2]);
+    }
+}
+
 static hf_status node_map(const hf_ctx *c, const double *p, CUtensorMap *m)
 {
     HFCK(get_encode());
@@ -471,6 +492,21 @@ static hf_status kc_map(const hf_ctx *c, const void *kc, CUtensorMap *m)
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(HF_E_CUDA, "cuTensorMapEncodeTiled(kc) failed: " + std::to_string((int)r));
+    return HF_OK;
+}
+
+static hf_status kcn_map(const hf_ctx *c, const void *kcn, CUtensorMap *m)
+{
+    HFCK(get_encode());
+    const cuuint64_t dims[3] = {2 * (cuuint64_t)c->nx1, (cuuint64_t)c->ny1, (cuuint64_t)c->nzl};
+    const cuuint64_t strides[2] = {2 * (cuuint64_t)c->pitch * c->es, 2 * (cuuint64_t)c->plane * c->es};
+    const cuuint32_t bw = c->es == 8 ? StencilShape<2, 8, LD_RAW, double>::BW : StencilShape<2, 8, LD_RAW, float>::BW;
+    const cuuint32_t box[3] = {2 * bw, (cuuint32_t)(NW * c->tileR + 1), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUtensorMapDataType dt = c->es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    CUresult r = g_encode(m, dt, 3, (void *)kcn, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HF_E_CUDA, "cuTensorMapEncodeTiled(kcn) failed: " + std::to_string((int)r));
     return HF_OK;
 }
 
@@ -524,7 +560,7 @@ template <int R, int LD, int EP, int FL, int EL, class Real> static StencilFn st
 {
     constexpr int NS = ns_of<R, LD>();
     static const size_t pad = getenv("HF_SMEM_PAD") ? (size_t)atoi(getenv("HF_SMEM_PAD")) : 0;   // tuning / debug
-    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL, Real>, StencilShape<R, NW, LD, Real>::smem_bytes(NS) + pad};
+    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL, Real>, StencilShape<R, NW, LD, Real, EL>::smem_bytes(NS) + pad};
 }
 
 // every (loader, epilogue, flags) variant the library launches, for tile heights R = 2 and 4
@@ -547,6 +583,7 @@ template <class Real> static StencilFn stencil_fn_p(int R, int LD, int EP, int F
 #define X(ld, ep, fl)                                                                           \
     if (LD == (ld) && EP == (ep) && FL == (fl)) {                                               \
         if (EL == EL_DENSE) return stencil_fn_t<2, ld, ep, fl, EL_DENSE, Real>();              \
+        if (EL == EL_TETV) return stencil_fn_t<2, ld, ep, fl, EL_TETV, Real>();                \
         return R >= 4 ? stencil_fn_t<4, ld, ep, fl, EL_Q1, Real>() : stencil_fn_t<2, ld, ep, fl, EL_Q1, Real>(); \
     }
     HF_STENCIL_VARIANTS(X)
@@ -559,6 +596,9 @@ static StencilFn stencil_fn(int R, int LD, int EP, int FL, int EL, int es)
 {
     return es == 8 ? stencil_fn_p<double>(R, LD, EP, FL, EL) : stencil_fn_p<float>(R, LD, EP, FL, EL);
 }
+
+// element variant of the stencil kernels on this context
+static int kernel_elem(const hf_ctx *c) { return c->elem == EL_DENSE && c->tetv ? EL_TETV : c->elem; }
 
 // flags of a launch on this context
 static int dir_flags(const hf_ctx *c, int EP, bool has_b, bool dset);
@@ -636,6 +676,17 @@ static StencilArgs base_args(hf_ctx *c, double aK, double aM)
         a.lamf.kb[ch] = (float)a.lam.kb[ch];
         a.lamf.mb[ch] = (float)a.lam.mb[ch];
     }
+    if (c->elem == EL_DENSE && c->tetv) {
+        double K[6][16], V;
+        tet_matrices(c->g.h, K, &V);
+        for (int t = 0; t < 6; t++)
+            for (int i = 0; i < 16; i++) {
+                a.tv.K[t][i] = aK * K[t][i];
+                a.tvf.K[t][i] = (float)a.tv.K[t][i];
+            }
+        a.tv.m = aM * V / 20.0;
+        a.tvf.m = (float)a.tv.m;
+    }
     if (c->elem == EL_DENSE) {
         double K[64], M[64];
         tet_voxel(c->g.h, K, M);
@@ -690,7 +741,7 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
                                 Launch *out)
 {
     const int FL = dir_flags(c, EP, a.bvec != nullptr, dset);
-    StencilFn f = stencil_fn(c->tileR, LD, EP, FL, c->elem, c->es);
+    StencilFn f = stencil_fn(c->tileR, LD, EP, FL, kernel_elem(c), c->es);
     if (!f.fn) return fail(HF_E_ARG, "internal: no stencil instantiation");
     f.smem = std::max(f.smem, c->launch_min_smem);
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
@@ -762,6 +813,8 @@ static hf_status sys_maps(hf_ctx *c, Sys &s)
     for (int i = 0; i < 2; i++) HFCK(node_map(c, s.dbuf[i], &s.maps.node[MAP_D0 + i]));
     HFCK(node_map(c, s.s, &s.maps.node[MAP_S]));
     HFCK(kc_map(c, s.kc, &s.maps.kc));
+    if (s.kcn) HFCK(kcn_map(c, s.kcn, &s.maps.kcn));
+    else s.maps.kcn = s.maps.kc;            // unused unless EL_TETV
     return HF_OK;
 }
 
@@ -797,6 +850,7 @@ static void sys_free(Sys &s)
     cudaFree(s.st); cudaFreeHost(s.st_host);
     cudaFree(s.partA); cudaFree(s.partB); cudaFree(s.sums); cudaFree(s.iters);
     cudaFree(s.kc);
+    cudaFree(s.kcn);
     if (s.gexec) cudaGraphExecDestroy(s.gexec);
     if (s.graph) cudaGraphDestroy(s.graph);
     if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
@@ -932,7 +986,16 @@ static hf_status enqueue_diag(hf_ctx *c, Sys &s, double aK, double aM, double *d
 {
     const int bs = 256;
     const unsigned nb = (unsigned)((c->nloc + bs - 1) / bs);
-    if (c->es == 8) k_diag<double><<<nb, bs, 0, s.stream>>>(make_geom(c), s.kc, aK, aM, c->dg, diag, invd, c->launches);
+    if (kernel_elem(c) == EL_TETV) {
+        TetDiag td;
+        double K[6][16], V;
+        tet_matrices(c->g.h, K, &V);
+        for (int t = 0; t < 6; t++)
+            for (int v = 0; v < 4; v++) td.kd[t][v] = K[t][v * 5];
+        td.md = 2.0 * V / 20.0;
+        if (c->es == 8) k_diag_tv<double><<<nb, bs, 0, s.stream>>>(make_geom(c), s.kcn, aK, aM, td, diag, invd, c->launches);
+        else k_diag_tv<float><<<nb, bs, 0, s.stream>>>(make_geom(c), s.kcn, aK, aM, td, diag, invd, c->launches);
+    } else if (c->es == 8) k_diag<double><<<nb, bs, 0, s.stream>>>(make_geom(c), s.kc, aK, aM, c->dg, diag, invd, c->launches);
     else k_diag<float><<<nb, bs, 0, s.stream>>>(make_geom(c), s.kc, aK, aM, c->dg, diag, invd, c->launches);
     CUCK(cudaGetLastError());
     return HF_OK;
@@ -1203,6 +1266,49 @@ hf_status hf_set_coefficients(hf_ctx *c, const double *k, const double *cc)
     HFCK(dev_in(c, cc, ne, 1, &dc));
     HFCK(enqueue_pack(c, c->sys0, dk, dc));
     CUCK(cudaStreamSynchronize(c->stream));
+    if (c->tetv) {                              // back to one coefficient per element
+        c->tetv = false;
+        c->sys0.key_valid = false;
+        for (auto &p : c->pool) p->key_valid = false;
+    }
+    c->coef_set = true;
+    return HF_OK;
+}
+
+hf_status hf_set_vertex_coefficients(hf_ctx *c, const double *k, const double *cc)
+{
+    if (!c || !k || !cc) return fail(HF_E_ARG, "hf_set_vertex_coefficients: NULL argument");
+    CUCK(cudaSetDevice(c->device));
+    const size_t nng = (size_t)c->nx1 * c->ny1 * c->nz1g;     // global natural nodes
+    const double *dk, *dc;
+    HFCK(dev_in(c, k, nng, 0, &dk));
+    HFCK(dev_in(c, cc, nng, 1, &dc));
+    if (c->elem == EL_Q1) {
+        // Q1: each voxel's coefficient is the mean of its 8 corners
+        const size_t ne = (size_t)(c->g.ne[0] * c->g.ne[1] * c->g.ne[2]);
+        void *ke, *ce;
+        HFCK(scratch_get(c, 55, ne * sizeof(double), &ke));
+        HFCK(scratch_get(c, 56, ne * sizeof(double), &ce));
+        k_vertex_means<<<(unsigned)((ne + 255) / 256), 256, 0, c->stream>>>(make_geom(c), (int)c->g.ne[2], dk, dc,
+                                                                            (double *)ke, (double *)ce, c->launches);
+        CUCK(cudaGetLastError());
+        return hf_set_coefficients(c, (const double *)ke, (const double *)ce);
+    }
+    // tets: per-node pairs; each tet averages its 4 vertices inside the stencil (EL_TETV)
+    Sys &s = c->sys0;
+    if (!s.kcn) {
+        CUCK(cudaMalloc(&s.kcn, (size_t)c->nloc * 2 * c->es));
+        CUCK(cudaMemsetAsync(s.kcn, 0, (size_t)c->nloc * 2 * c->es, c->stream));
+    }
+    const unsigned nb = (unsigned)((c->nloc + 255) / 256);
+    if (c->es == 8) k_pack_nodes<double><<<nb, 256, 0, c->stream>>>(make_geom(c), dk, dc, s.kcn, c->launches);
+    else k_pack_nodes<float><<<nb, 256, 0, c->stream>>>(make_geom(c), dk, dc, s.kcn, c->launches);
+    CUCK(cudaGetLastError());
+    HFCK(sys_maps(c, s));
+    CUCK(cudaStreamSynchronize(c->stream));
+    c->tetv = true;
+    s.key_valid = false;
+    for (auto &p : c->pool) p->key_valid = false;
     c->coef_set = true;
     return HF_OK;
 }
@@ -1709,6 +1815,7 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
         return fail(HF_E_ARG, "hf_simulate_batched: bad argument");
     if (!c_batch && !c->coef_set) return fail(HF_E_STATE, "hf_simulate_batched: no capacity field");
     if (c->comm) return fail(HF_E_ARG, "hf_simulate_batched: not available on slab contexts");
+    if (c->tetv) return fail(HF_E_STATE, "hf_simulate_batched: per-element coefficients only (not vertex materials)");
     if (front_out && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "snap_plane");
     CUCK(cudaSetDevice(c->device));
     hf_cg_opts o = {1e-12, 10000, -1};
