@@ -598,6 +598,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     const Real betar = (Real)beta;
     Real Fp[R][4];            // Q1: face transforms of the lower plane p-1
     Real Cy[R][4];            // contributions carried from the layer below (face / node space)
+    float2 Fp2[R][2], Cy2[R][2];  // fp32 Q1: the same per channel pair (0,2), (1,3), packed math
     Real Pv[R + 1], Pv1[R + 1];   // dense: node values of plane p-1 at x and x+1
     V2 PK0[R + 1], PK1[R + 1];    // EL_TETV: node (k, c) pairs of plane p-1 at x and x+1
     Real cen[R];              // raw centre values of plane p-1 (rows 0..R-1)
@@ -606,6 +607,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     for (int r = 0; r < R; r++) {
 #pragma unroll
         for (int ch = 0; ch < 4; ch++) { Fp[r][ch] = Real(0); Cy[r][ch] = Real(0); }
+        for (int q = 0; q < 2; q++) { Fp2[r][q] = make_float2(0.f, 0.f); Cy2[r][q] = make_float2(0.f, 0.f); }
         cen[r] = Real(0);
     }
 #pragma unroll
@@ -678,6 +680,40 @@ k_stencil(const __grid_constant__ StencilArgs a)
             // ---- element layer p-1: y butterfly, fused z butterfly + scaling -------------------
             // (lane 31's element X0+30 reads node X0+31 from the box; elements outside the domain
             //  have k = c = 0 from the TMA zero fill)
+            if constexpr (ES == 4) {
+                // fp32: the same algebra on channel pairs (0,2) and (1,3) with Blackwell's packed
+                // FP32x2 instructions (FFMA2 / FMUL2 / FADD2), half the FP instruction count
+                const float2 M1 = make_float2(-1.f, -1.f);
+                const float2 LKA[2] = {make_float2(a.lamf.ka[0], a.lamf.ka[2]), make_float2(a.lamf.ka[1], a.lamf.ka[3])};
+                const float2 LMA[2] = {make_float2(a.lamf.ma[0], a.lamf.ma[2]), make_float2(a.lamf.ma[1], a.lamf.ma[3])};
+                const float2 LKB[2] = {make_float2(a.lamf.kb[0], a.lamf.kb[2]), make_float2(a.lamf.kb[1], a.lamf.kb[3])};
+                const float2 LMB[2] = {make_float2(a.lamf.mb[0], a.lamf.mb[2]), make_float2(a.lamf.mb[1], a.lamf.mb[3])};
+                float2 T2[R][2];
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    const float2 sd0 = make_float2(S[r], D[r]), sd1 = make_float2(S[r + 1], D[r + 1]);
+                    const float2 Fc2[2] = {__fadd2_rn(sd0, sd1), __ffma2_rn(sd1, M1, sd0)};   // (0,2), (1,3)
+                    const V2 kc = *reinterpret_cast<const V2 *>(kcs + r * SH::KW);
+                    const float2 k2 = make_float2(kc.x, kc.x), c2 = make_float2(kc.y, kc.y);
+#pragma unroll
+                    for (int q = 0; q < 2; q++) {
+                        const float2 av = __ffma2_rn(k2, LKA[q], __fmul2_rn(c2, LMA[q]));
+                        const float2 bv = __ffma2_rn(k2, LKB[q], __fmul2_rn(c2, LMB[q]));
+                        T2[r][q] = __ffma2_rn(av, Fp2[r][q], __ffma2_rn(bv, Fc2[q], Cy2[r][q]));
+                        Cy2[r][q] = __ffma2_rn(bv, Fp2[r][q], __fmul2_rn(av, Fc2[q]));
+                        Fp2[r][q] = Fc2[q];
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e <= R; e++) {
+                    float2 E;                                   // (E0, E1): channel sums (0+1, 2+3)
+                    if (e == 0) E = __fadd2_rn(T2[0][0], T2[0][1]);
+                    else if (e == R) E = __ffma2_rn(T2[R - 1][1], M1, T2[R - 1][0]);
+                    else E = __fadd2_rn(__fadd2_rn(T2[e][0], T2[e][1]), __ffma2_rn(T2[e - 1][1], M1, T2[e - 1][0]));
+                    const Real left = __shfl_up_sync(0xffffffffu, E.x - E.y, 1);
+                    yv[e] = (E.x + E.y) + left;                 // lane 0's value is not owned
+                }
+            } else {
             Real T[R][4];
 #pragma unroll
             for (int r = 0; r < R; r++) {
@@ -708,6 +744,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
                 }
                 const Real left = __shfl_up_sync(0xffffffffu, E0 - E1, 1);
                 yv[e] = (E0 + E1) + left;                   // lane 0's value is not owned
+            }
             }
         } else {
             // ---- 6-tet split: u_e = 4 values of plane p-1 + 4 of p ----------------------------
