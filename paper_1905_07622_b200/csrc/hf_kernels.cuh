@@ -133,7 +133,8 @@ struct Sync {               // per-system reduction plumbing
     double *pout;           // this kernel's partial sums (NPART per block)
     unsigned long long *launches;
     cudaGraphConditionalHandle h_while, h_if;
-    int use_handles;
+    int use_handles;        // set the WHILE handle (graph driver)
+    int use_if;             // set the IF handle (only where the body has an IF node)
 };
 
 struct Maps {               // TMA descriptors (host copy; kernels read a device-memory copy)
@@ -364,7 +365,7 @@ __device__ __forceinline__ void set_while(const Sync &sy, int v)
 }
 __device__ __forceinline__ void set_if(const Sync &sy, int v)
 {
-    if (sy.use_handles) cudaGraphSetConditional(sy.h_if, (unsigned)v);
+    if (sy.use_handles && sy.use_if) cudaGraphSetConditional(sy.h_if, (unsigned)v);
 }
 
 // Start of iteration i (kernel A), from the sums of the init / B / RESID kernel before it:

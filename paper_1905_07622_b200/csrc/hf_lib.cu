@@ -224,7 +224,7 @@ struct hf_ctx {
     int check_every = 8;
     int max_blocks = 0;
     int occ = 2;                     // resident CTAs/SM of the CG stencil (occupancy API)
-    int unroll = 2;                  // PCG iterations per WHILE-body launch
+    int unroll = 5;                  // PCG iterations per WHILE-body launch (5 divides the replacement period 50)
     size_t launch_min_smem = 0;      // > 0: stencil launches reserve at least this much smem
     int rank = 0, nranks = 1;
     Comm *comm = nullptr;
@@ -1176,7 +1176,7 @@ static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, in
 // root: [pre...] -> init -> WHILE(active){ A -> B -> IF(replace){ RESID } } -> [post]
 // (all stencil launches carry (Maps, StencilArgs); B carries BArgs)
 static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init, CgLaunches L, std::vector<Launch> post,
-                                cudaGraph_t *out)
+                                int replace_every, cudaGraph_t *out)
 {
     cudaGraph_t g;
     CUCK(cudaGraphCreate(&g, 0));
@@ -1196,23 +1196,33 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
     cudaGraphNode_t wnode;
     CUCK(cudaGraphAddNode(&wnode, g, &prev, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    // the body holds `unroll` copies of [A -> B -> IF(RES)]; copies after convergence exit at once
+    // the body holds `unroll` copies of [A -> B -> IF(RES)]; copies after convergence exit at once.
+    // Every body starts at an iteration that is a multiple of `unroll`, so when unroll divides the
+    // replacement period only the first copy can meet a replacement iteration: the others get no
+    // IF node (an IF node costs about a microsecond per evaluation).
+    const int U = std::max(1, c->unroll);
+    const bool if_first_only = replace_every > 0 && replace_every % U == 0;
     cudaGraphNode_t bprev = nullptr;
-    for (int u = 0; u < std::max(1, c->unroll); u++) {
-        CUCK(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
+    for (int u = 0; u < U; u++) {
+        const bool with_if = replace_every > 0 && !(u > 0 && if_first_only);
+        if (with_if) CUCK(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
         Launch A = L.A, B = L.B, RES = L.RES;
         StencilArgs aa = A.get<StencilArgs>(0);
-        aa.sy.h_while = hw; aa.sy.h_if = hi; aa.sy.use_handles = 1;
+        aa.sy.h_while = hw; aa.sy.h_if = hi; aa.sy.use_handles = 1; aa.sy.use_if = with_if;
         A.put(0, aa);
         BArgs bb = B.get<BArgs>(0);
-        bb.sy.h_while = hw; bb.sy.h_if = hi; bb.sy.use_handles = 1;
+        bb.sy.h_while = hw; bb.sy.h_if = hi; bb.sy.use_handles = 1; bb.sy.use_if = with_if;
         B.put(0, bb);
         StencilArgs ra = RES.get<StencilArgs>(0);
-        ra.sy.h_while = hw; ra.sy.h_if = hi; ra.sy.use_handles = 1;
+        ra.sy.h_while = hw; ra.sy.h_if = hi; ra.sy.use_handles = 1; ra.sy.use_if = with_if;
         RES.put(0, ra);
         cudaGraphNode_t na, nb;
         HFCK(add_node(body, A, bprev ? &bprev : nullptr, &na));
         HFCK(add_node(body, B, &na, &nb));
+        if (!with_if) {                          // no replacement can occur in this copy
+            bprev = nb;
+            continue;
+        }
         cudaGraphNodeParams ip = {};
         ip.type = cudaGraphNodeTypeConditional;
         ip.conditional.handle = hi;
@@ -1437,7 +1447,7 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     const bool use_graph = c->driver == 0 && !c->comm && !c->prof;
     if (use_graph) {
         cudaGraph_t g;
-        HFCK(build_cg_graph(c, {}, init, L, post, &g));
+        HFCK(build_cg_graph(c, {}, init, L, post, o.replace_every, &g));
         cudaGraphExec_t ge;
         cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
         if (e != cudaSuccess) { cudaGraphDestroy(g); CUCK(e); }
@@ -1561,7 +1571,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             if (s.gexec) { cudaGraphExecDestroy(s.gexec); s.gexec = nullptr; }
             if (s.graph) { cudaGraphDestroy(s.graph); s.graph = nullptr; }
             s.key_valid = false;
-            HFCK(build_cg_graph(c, pre, init, L, post, &s.graph));
+            HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph));
             CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
             s.key = key;
             s.key_valid = true;
