@@ -143,9 +143,10 @@ def test_fp32_c3_two_steps():
     assert rel(N(u), uo) <= BAR
 
 
-def test_fp32_batched_matches_individual():
+@pytest.mark.parametrize("B", [3, 5])
+def test_fp32_batched_matches_individual(B):
+    """B = 3: per-system pool; B = 5: block-diagonal stacks (groups of up to 8)."""
     g = synth.Grid((12, 10, 9), (0.3, 0.3, 0.2))
-    B = 3
     ks = [synth.random_fields(g, seed=40 + j)[0] for j in range(B)]
     _, c = synth.random_fields(g, seed=39)
     ctx = ctx32(g, ks[0], c)

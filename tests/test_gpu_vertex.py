@@ -1,6 +1,8 @@
 """Vertex materials averaged over each element (hf_set_vertex_coefficients) against
 the oracle's vertex mode: Q1 voxels take the mean of their 8 corners; the paper's 6 tets per voxel
 each take the mean of their 4 vertices (kernel variant EL_TETV)."""
+import threading
+
 import numpy as np
 import pytest
 
@@ -112,3 +114,43 @@ def test_vertex_tets_fp32_and_switch_back():
     with pytest.raises(hf.HfError):              # batched runs take per-element fields only
         ctx2 = vctx(g, kn, cn, 1)
         hf.hf_simulate_batched(ctx2, 1, T(k), None, 0.5, 0.01, 1, None, T(np.zeros(g.n_nodes)))
+
+
+def test_vertex_tets_on_slabs_local_transport():
+    """z-slabs carry the per-node pairs of their ghost planes: 2 slabs equal the oracle."""
+    g = synth.Grid((10, 9, 13), (0.3, 0.3, 0.2))
+    kn, cn = vertex_fields(g, 56)
+    o = oracle.Oracle(g, kn, cn, elem=1, vertex=True)
+    u0 = synth.random_vector(g.n_nodes, 57) * 0.01
+    uo, _, _, _ = o.simulate(0.5, 0.05, 4, o.face_load(synth.FACE_ZM, 1.0), u0)
+    nranks = 2
+    grp = hf.hf_local_group_create(nranks)
+    plane = (g.ne[0] + 1) * (g.ne[1] + 1)
+    out, errs, ctxs = [None] * nranks, [], [None] * nranks
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            ctx = hf.hf_create_slab(g, r, nranks, grp, transport=1, device=0)
+            ctxs[r] = ctx
+            hf.hf_set_element(ctx, 1)
+            lo, hi, lp, z0 = ctx.slab
+            hf.hf_set_vertex_coefficients(ctx, T(kn), T(cn))
+            F = torch.empty(ctx.n_nodes, dtype=torch.float64, device=DEV)
+            hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+            u = T(u0[z0 * plane:(z0 + lp) * plane])
+            hf.hf_simulate(ctx, 0.5, 0.05, 4, F, u)
+            out[r] = (lo, hi, z0, N(u))
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(nranks)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not errs, errs
+    full = np.empty(g.n_nodes)
+    for lo, hi, z0, u in out:
+        full[lo * plane:hi * plane] = u[(lo - z0) * plane:(hi - z0) * plane]
+    assert rel(full, uo) <= 1e-10
+    del ctxs
+    hf.hf_local_group_destroy(grp)
