@@ -502,6 +502,28 @@ def test_c5_corrosion_batched_small():
     assert np.abs(front[0] - front[1]).max() > 1e-6 * np.abs(front[0]).max()
 
 
+def test_c5_full_size_stacked_two_steps():
+    """C5 at its BASELINE size (100^3 nodes per sim) in bench.py's launch configuration (a
+    block-diagonal stack of 4 systems): 2 steps of two of the systems against the oracle."""
+    B, nsteps = 4, 2
+    probs = [synth.c5(j) for j in range(B)]            # the bench's dt = T_F / 300; 2 of its steps
+    g = probs[0].grid
+    ctx = make_ctx(g, probs[0].k, probs[0].c)
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, probs[0].flux_face, probs[0].flux_const, probs[0].beam, F)
+    ub = T(np.zeros(B * g.n_nodes))
+    front = torch.empty(B * ctx.n_plane, dtype=torch.float64, device=DEV)
+    kb = np.stack([p.k for p in probs]).ravel()
+    cb = np.stack([p.c for p in probs]).ravel()
+    st = hf.hf_simulate_batched(ctx, B, T(kb), T(cb), probs[0].theta, probs[0].dt, nsteps, F, ub, 0, front)
+    assert all(s["steps_done"] == nsteps for s in st)
+    ub = N(ub).reshape(B, -1)
+    for j in (0, 3):
+        o, Fo = oracle.problem_oracle(probs[j])
+        uo, sto, _, _ = o.simulate(probs[j].theta, probs[j].dt, nsteps, Fo, probs[j].u0, tol=probs[j].rtol)
+        assert sto == 0 and rel(ub[j], uo) <= 1e-10, j
+
+
 @pytest.mark.parametrize("transport", [0, 1])
 def test_slab_single_rank_nccl_and_local(transport):
     """A 1-rank slab context runs the slab driver (host loop, k_localsum, transport allreduce,
