@@ -132,19 +132,27 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    slab = world > 1 or args.force_slab          # --force-slab: the N > 1 code path on 1 rank
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
-    if world > 1:
+    if slab:
+        # stdout carries exactly one JSON line: keep NCCL's version banner off it
+        os.environ["NCCL_DEBUG"] = os.environ.get("HF_BENCH_NCCL_DEBUG", "WARN")
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+            dist.init_process_group("nccl", device_id=dev)
 
     p = synth.c3(nsteps=args.warmup + args.steps)
     g = p.grid
     plane = (g.ne[0] + 1) * (g.ne[1] + 1)
     kd = torch.tensor(p.k, device=dev)
     cd = torch.tensor(p.c, device=dev)
-    if world == 1:
+    if not slab:
         ctx = hf.hf_create(g, local_rank)
         z0, lp = 0, g.ne[2] + 1
     else:
@@ -170,7 +178,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks.start()
     times, iters = [], 0
-    if world == 1:
+    if not slab:
         # one call: the library flushes L2 (512 MiB memset) before every step and times each
         # step alone with CUDA events on the context stream (= this torch stream)
         hf.hf_set_step_flush(ctx, True)
@@ -212,7 +220,7 @@ def run_ours(args):
     a_bracketed_ms = a_ms / max(a_n, 1)          # each launch bracketed by its own event pair
     # kernel A replayed 200x back to back between one event pair on the context stream (no
     # per-launch event overhead); this is the duration the roofline uses
-    a_avg_ms = hf.hf_time_kernel_a(ctx, 200) if world == 1 else a_bracketed_ms
+    a_avg_ms = hf.hf_time_kernel_a(ctx, 200) if not slab else a_bracketed_ms
     nodes_local = plane * lp
     elems_local = g.ne[0] * g.ne[1] * max(lp - 1, 1)
     # algorithmic bytes of one kernel-A launch: read s, d_old (16 B/node) + (k,c) (16 B/element),
@@ -224,7 +232,7 @@ def run_ours(args):
     # e2e: the same workload through the public API from pinned host memory: H2D of k, c, u0
     # and D2H of the front-face plane every step + the final field, inside the timed region
     e2e = None
-    if world == 1:
+    if not slab:
         kh = torch.tensor(p.k).pin_memory()
         ch = torch.tensor(p.c).pin_memory()
         uh = torch.zeros(g.n_nodes, dtype=torch.float64).pin_memory()
@@ -247,6 +255,26 @@ def run_ours(args):
                "how": "wall clock around hf_set_coefficients + hf_face_load + hf_simulate(K steps) with pinned "
                       "host k, c, u0, u_N and a per-step front-face snapshot (host)"}
         del ctx2
+    else:
+        # N ranks: each rank feeds its slab from pinned host memory (global k, c; its planes of
+        # u0) through the same calls on the existing slab context; wall clock, max over ranks
+        kh = torch.tensor(p.k).pin_memory()
+        ch = torch.tensor(p.c).pin_memory()
+        uh = torch.zeros(ctx.n_nodes, dtype=torch.float64).pin_memory()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hf.hf_set_coefficients(ctx, kh, ch)
+        hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
+        se = hf.hf_simulate(ctx, p.theta, p.dt, args.steps, F, uh, rtol=p.rtol)
+        torch.cuda.synchronize()
+        wall = torch.tensor([(time.perf_counter() - t0) * 1e3], device=dev, dtype=torch.float64)
+        dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(wall.item()) / args.steps, "unit": UNIT,
+               "h2d_bytes_per_step": int((kh.numel() + ch.numel() + uh.numel()) * 8 / args.steps),
+               "d2h_bytes_per_step": int(uh.numel() * 8 / args.steps),
+               "how": "per rank: wall clock around hf_set_coefficients + hf_face_load + hf_simulate(K steps) "
+                      "with pinned host k, c, u0 (its slab) and u_N; max over ranks"}
 
     line = None
     if rank == 0:
@@ -271,7 +299,13 @@ def run_ours(args):
                          "note": "C3 working set (~104 MB) is L2-resident during a step, so achieved can exceed "
                                  "the HBM copy peak; see apply_512 for the HBM-bound apply"},
         }
-    if world == 1:
+    if slab:
+        # the metric's second half at N GPUs: the 512^3 operator apply on N z-slabs (BASELINE
+        # configs[3]), each rank its slab + ghosts, time = max over ranks
+        a512 = apply_512_slabs(hf, torch, dev, peak, rank, world, dist)
+        if rank == 0:
+            line["apply_512_slabs"] = a512
+    if not slab:
         line["apply_512"] = apply_512(hf, torch, dev, peak)
         line["c5_batched"] = c5_batched(hf, torch, dev, world)
         # the paper's settings for the inverse problem: rtol 1e-6, single precision
@@ -300,6 +334,47 @@ def apply_512(hf, torch, dev, peak, prec=64):
         y = torch.empty_like(u)
         return _apply_time(hf, torch, dev, peak, ctx, g, u, y, 8)
     return _apply_time_internal(hf, torch, dev, peak, ctx, g, prec)
+
+
+def apply_512_slabs(hf, torch, dev, peak, rank, world, dist, _unused=None):
+    """512^3 apply on this rank's z-slab (strong scaling of configs[3]); aggregate GB/s from the
+    slowest rank.  No exchange is needed: the input vector carries its ghost planes."""
+    g = synth.c4_grid(512)
+    uid = hf.hf_nccl_unique_id() if rank == 0 else bytes(128)
+    obj = [uid]
+    dist.broadcast_object_list(obj, src=0)
+    ctx = hf.hf_create_slab(g, rank, world, obj[0], transport=0, device=dev.index)
+    lo, hi, lp, z0 = ctx.slab
+    gen = torch.Generator(device=dev).manual_seed(0)
+    k = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) * 121.5 + 1.0
+    c = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) + 1.0
+    hf.hf_set_coefficients(ctx, k, c)
+    del k, c
+    torch.cuda.empty_cache()
+    u = torch.randn(ctx.n_nodes, dtype=torch.float64, device=dev)
+    y = torch.empty_like(u)
+    for _ in range(3):
+        hf.hf_apply(ctx, 0.005, 1.0, u, y)
+    s = torch.cuda.current_stream(dev)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(10):
+        hf.hf_apply(ctx, 0.005, 1.0, u, y)
+    e1.record(s)
+    e1.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / 10], device=dev, dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    nodes = (g.ne[0] + 1) * (g.ne[1] + 1) * (hi - lo)          # owned output nodes of this rank
+    byts_total = 16.0 * g.n_nodes + 16.0 * g.n_elems              # all ranks together
+    del ctx
+    torch.cuda.empty_cache()
+    agg = byts_total / (ms * 1e-3) / 1e9
+    return {"ms_max_over_ranks": ms, "aggregate_GBps": agg, "per_gpu_GBps": agg / world,
+            "frac_per_gpu": agg / world / peak, "peak": peak, "owned_nodes_rank0": nodes,
+            "kernel": "k_stencil<LD_RAW,EP_APPLY> on each rank's 512^3 z-slab, mean of 10, max over ranks"}
 
 
 def _apply_time_internal(hf, torch, dev, peak, ctx, g, prec):
@@ -465,13 +540,15 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--force-slab", action="store_true",
+                    help="run the multi-GPU (z-slab, NCCL) code path even on one rank (validation)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None:
         print(json.dumps(line), flush=True)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "ours":
+    if (int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.force_slab) and args.impl == "ours":
         import torch.distributed as dist
         if dist.is_initialized():
             dist.destroy_process_group()

@@ -546,9 +546,12 @@ struct Launch {
     }
 };
 
+#ifndef HF_NS_R2
+#define HF_NS_R2 4
+#endif
 template <int R, int LD> constexpr int ns_of()
 {
-    return (R >= 4 && StencilShape<R, NW, LD>::NA == 2) ? 3 : 4;
+    return (R >= 4 && StencilShape<R, NW, LD>::NA == 2) ? 3 : (R == 2 ? HF_NS_R2 : 4);
 }
 
 struct StencilFn {
