@@ -49,22 +49,42 @@ enum { MAP_U0 = 0, MAP_D0 = 3, MAP_S = 5 };
 // kernel and read only by LATER kernels (kernel boundaries order them), never by the kernel that
 // writes it: delta is double-buffered by iteration parity for that reason.
 struct CgState {
-    double rtol2;           // options
-    int max_iter, replace_every;
+    // header: read by every PCG kernel at its start as 16-byte loads issued together (one L2
+    // round trip instead of a chain of dependent scalar loads)
+    int first_failed;       // first failing step, -1 if none
+    int active;             // 1 while iterating                          (init 1; A, B: 0 to stop)
+    int b_iter;             // completed iterations                       (init: 0, B: i + 1)
+    int step;               // time-step counter (step-end kernel)
+    int a_iter;             // i of the running iteration                 (A)
+    int replace_every;      // option
+    int replace;            // iteration a_iter replaces the residual     (B)
+    int npart_b;            // partial-sum count of the last init / B / RESID
+    int npart_a;            // partial-sum count of the last A
+    int max_iter;           // option
+    int status, zero_x;     // ST_*, b_F == 0                             (A, B)
+    int iter;               // iterations of the finished solve           (A or B when stopping)
+    int total_iters, max_iters_step, steps_done;
+    double rtol2;           // option
     double delta[2];        // delta_i = r_i^T s_i in slot i & 1          (written by A_i)
     double thresh, bb, rr;  // rtol^2 ||b_F||^2, ||b_F||^2, last r^T r      (A)
     double alpha, dq;       // last alpha, d^T q                          (B)
-    int a_iter;             // i of the running iteration                 (A)
-    int b_iter;             // completed iterations                       (init: 0, B: i + 1)
-    int active;             // 1 while iterating                          (init 1; A, B: 0 to stop)
-    int status, zero_x;     // ST_*, b_F == 0                             (A, B)
-    int replace;            // iteration a_iter replaces the residual     (B)
-    int iter;               // iterations of the finished solve           (A or B when stopping)
-    int npart_a, npart_b;   // partial-sum counts of the last A / (init, B, RESID)
-    int step;               // time-step counter (step-end kernel)
-    int first_failed;       // first failing step, -1 if none
-    int total_iters, max_iters_step, steps_done;
 };
+static_assert(offsetof(CgState, a_iter) == 16 && offsetof(CgState, npart_a) == 32, "CgState header layout");
+
+// the header words of a state (3 x 16 B, one round trip)
+struct CgHdr {
+    int4 h0, h1, h2;        // (first_failed, active, b_iter, step), (a_iter, replace_every, replace, npart_b),
+                            // (npart_a, max_iter, status, zero_x)
+};
+// Through the read-only (L1) path: every warp of the grid reads these 48 bytes, and L2-only loads
+// (__ldcg) made them an L2 hot spot (C3 kernel A +1.7 us); the kernel boundary makes the
+// previous kernel's writes visible, and no block of this kernel reads a header word that a block
+// of the same kernel writes.
+__device__ __forceinline__ CgHdr load_hdr(const CgState *st)
+{
+    const int4 *p = reinterpret_cast<const int4 *>(st);
+    return {__ldg(p), __ldg(p + 1), __ldg(p + 2)};
+}
 
 struct Geom {
     int nx1, ny1, nzl;      // nodes in x, y; local node planes
@@ -467,19 +487,22 @@ k_stencil(const __grid_constant__ StencilArgs a)
     int map0 = MAP_U0, map1 = MAP_U0 + 2, first = a.first;
     int it_i = 0;                                            // PCG iteration (kernel A)
     Real *cstore = reinterpret_cast<Real *>((EP == EP_CGA) ? a.dbuf[1] : a.xout);   // centre-value store target
+    int npart_b = 0;
     if (a.sy.st) {
-        const CgState *st = a.sy.st;
-        if (st->first_failed >= 0) {             // an earlier time step failed: stop the run
+        const CgHdr hd = load_hdr(a.sy.st);
+        const int first_failed = hd.h0.x, active = hd.h0.y, b_iter = hd.h0.z, step = hd.h0.w;
+        npart_b = hd.h1.w;
+        if (first_failed >= 0) {                 // an earlier time step failed: stop the run
             if (EP == EP_CGA && blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
             return;
         }
         if (EP == EP_CGA || EP == EP_RESID) {
-            if (!st->active) return;             // converged / stopped: nothing to do
-            if (EP == EP_RESID && !st->replace) return;
+            if (!active) return;                 // converged / stopped: nothing to do
+            if (EP == EP_RESID && !hd.h1.z) return;
         }
         if (LD == LD_CGD) {
             // d_i = s_i + beta_i d_{i-1};  d_{i-1} = dbuf[i & 1], d_i = dbuf[(i & 1) ^ 1]
-            it_i = st->b_iter;
+            it_i = b_iter;
             const int par = it_i & 1;
             map0 = MAP_S;
             map1 = MAP_D0 + par;
@@ -487,13 +510,13 @@ k_stencil(const __grid_constant__ StencilArgs a)
         }
         if (a.rot_role != ROT_NONE) {
             // time-step ring: step n reads U[n%3] (u^n), U[(n+2)%3] (u^{n-1}), writes U[(n+1)%3]
-            const int s = st->step % 3;
+            const int s = step % 3;
             if (a.rot_role == ROT_RHS) map0 = MAP_U0 + s;
             else if (a.rot_role == ROT_INIT) {
                 map0 = MAP_U0 + s;
                 map1 = MAP_U0 + (s + 2) % 3;
                 cstore = reinterpret_cast<Real *>(a.ring[(s + 1) % 3]);
-                first = a.first && st->step == 0;
+                first = a.first && step == 0;
             } else map0 = MAP_U0 + (s + 1) % 3;
         }
     }
@@ -555,7 +578,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     if (EP == EP_CGA) {
         // start of PCG iteration i from the previous kernel's partial sums (overlaps the TMA)
         double ps[NPART];
-        prev_sums<NT>(a.sy, a.sy.st->npart_b, ps);
+        prev_sums<NT>(a.sy, npart_b, ps);
         const IterStart is = iter_start(a.sy.st, it_i, ps);
         if (!is.go) {
             if (blk == 0 && tid == 0) {
@@ -909,14 +932,15 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     const int blk = blockIdx.x;
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
     CgState *st = a.sy.st;
-    if (st->first_failed >= 0 || !st->active) {   // failed run / converged: leave the loop
+    const CgHdr hd = load_hdr(st);
+    if (hd.h0.x >= 0 || !hd.h0.y) {               // failed run / converged: leave the loop
         if (blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
         return;
     }
-    const int it = st->a_iter, re = st->replace_every;
+    const int it = hd.h1.x, re = hd.h1.y, step = hd.h0.w;
     // alpha_i = delta_i / (d_i^T q_i)  (Alg. 1 line 8) from kernel A's partials
     double ps[NPART];
-    prev_sums<NT>(a.sy, st->npart_a, ps);
+    prev_sums<NT>(a.sy, hd.h2.x, ps);
     const double dq = ps[0], delta = st->delta[it & 1];
     if (!(dq > 0.0) || !isfinite(dq) || !isfinite(delta)) {           // breakdown
         if (blk == 0 && tid == 0) {
@@ -937,7 +961,7 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     Real *const sv_ = reinterpret_cast<Real *>(a.s);
     const bool replace = it > 0 && re > 0 && (it % re) == 0;           // Alg. 1 line 10 (R6)
     const Real *dvec = reinterpret_cast<const Real *>(a.dbuf[(it & 1) ^ 1]);
-    Real *xvec = reinterpret_cast<Real *>(a.rot[0] ? a.rot[(st->step + 1) % 3] : a.x);
+    Real *xvec = reinterpret_cast<Real *>(a.rot[0] ? a.rot[(step + 1) % 3] : a.x);
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
     // BP aligned pairs per thread per sweep (n is even: even row pitch), loads issued up front;
     // a pair never straddles the owned range (planes hold an even number of slots)
