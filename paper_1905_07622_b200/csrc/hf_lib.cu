@@ -191,7 +191,6 @@ struct Comm {
 };
 
 struct hf_ctx {
-    std::map<std::string, void *> mapcache;   // device copies of TMA descriptor sets (maps_dev)
     std::map<int, hf_ctx *> stacks;  // batched: contexts of G stacked systems (batched_stacked)
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -720,20 +719,36 @@ static int dir_flags(const hf_ctx *c, int EP, bool has_b, bool dset)
     return fl;
 }
 
-// Device copies of TMA descriptor sets, content-addressed: written once by a synchronous copy
-// before the first launch that uses them and never modified (graph nodes keep pointing at them);
-// freed with the context.  Descriptors in kernel parameter space were not reliable for kernels
-// launched from graph conditional bodies of concurrently running graphs (intermittent TMA
-// transaction-count faults and hangs with two batched streams; tools/stress_batched.sh).
+// Device copies of TMA descriptor sets.  They live in a per-device arena that is never freed and
+// is deduplicated by content, so a descriptor address is written exactly once in the life of the
+// process: an SM's descriptor cache can never hold a stale entry for it, and the kernels need no
+// fence.proxy.tensormap acquire (which cost 1.6 us per C3 PCG iteration: every CTA re-fetched its
+// 3 descriptors).  Growth is bounded by the number of distinct descriptor sets the process
+// creates (1 KB each; a context creates a few, hf_apply one per distinct user buffer).
+// Descriptors in kernel parameter space were not reliable for kernels launched from graph
+// conditional bodies of concurrently running graphs (intermittent TMA transaction-count faults
+// and hangs with two batched streams; tools/stress_batched.sh), hence device memory.
+static std::mutex g_maps_mu;
+static std::map<std::pair<int, std::string>, void *> g_maps;       // (device, content) -> address
+static std::map<int, std::pair<char *, size_t>> g_maps_chunk;      // device -> (chunk, used bytes)
+
 static hf_status maps_dev(hf_ctx *c, const Maps &m, const CUtensorMap **out)
 {
-    std::string key((const char *)&m, sizeof(Maps));
-    auto it = c->mapcache.find(key);
-    if (it != c->mapcache.end()) { *out = (const CUtensorMap *)it->second; return HF_OK; }
-    void *d = nullptr;
-    CUCK(cudaMalloc(&d, sizeof(Maps)));
+    std::lock_guard<std::mutex> lk(g_maps_mu);
+    auto key = std::make_pair(c->device, std::string((const char *)&m, sizeof(Maps)));
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) { *out = (const CUtensorMap *)it->second; return HF_OK; }
+    const size_t chunk = 256 * sizeof(Maps);
+    auto &ch = g_maps_chunk[c->device];
+    if (!ch.first || ch.second + sizeof(Maps) > chunk) {
+        void *p = nullptr;
+        CUCK(cudaMalloc(&p, chunk));                                // never freed (see above)
+        ch = {(char *)p, 0};
+    }
+    void *d = ch.first + ch.second;
+    ch.second += sizeof(Maps);
     CUCK(cudaMemcpy(d, &m, sizeof(Maps), cudaMemcpyHostToDevice));
-    c->mapcache.emplace(key, d);
+    g_maps.emplace(key, d);
     *out = (const CUtensorMap *)d;
     return HF_OK;
 }
@@ -758,7 +773,7 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
     L.block = dim3(32, NW, 1);
     L.smem = f.smem;
     HFCK(maps_dev(c, maps, &a.tm));
-    static const int tm_fence = getenv("HF_TM_FENCE") ? atoi(getenv("HF_TM_FENCE")) : 1;
+    static const int tm_fence = getenv("HF_TM_FENCE") ? atoi(getenv("HF_TM_FENCE")) : 0;   // see maps_dev
     a.tm_fence = tm_fence;
     L.add(a);
     L.cls = cls;
@@ -960,8 +975,6 @@ static void ctx_free(hf_ctx *c)
     for (void *p : c->scratch) cudaFree(p);
     cudaFree(c->launches);
     cudaFree(c->flush);
-    for (auto &kv : c->mapcache) cudaFree(kv.second);
-    c->mapcache.clear();
     for (auto &kv : c->stacks) { ctx_free(kv.second); delete kv.second; }
     c->stacks.clear();
     delete c->comm;
