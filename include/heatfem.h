@@ -157,6 +157,30 @@ hf_status hf_apply(hf_ctx *ctx, double aK, double aM, const double *u, double *y
 hf_status hf_apply_axpby(hf_ctx *ctx, double aK, double aM, double c, const double *u,
                          const double *b, double *y);
 
+/* NEXT row f4 (ablation): the paper's earlier interpretations of the assembly operator, rebuilt
+ * on sm_100a for the comparison of §5.1 (Fig. 5, Table 1).  Same result as
+ * hf_apply_axpby (Eq. (1)), different data movement:
+ *   impl 1 = "flexible DbD" (Eq. (3)): every scaled element matrix A_e stored in
+ *            global memory in element order (512 B per element, fp64 8 x 8, written by
+ *            hf_ablation_prepare); pass 1 one thread per element-DoF pair writes its row dot
+ *            product in vertex order (8 contributions per node, ctx-owned, 64 B per node);
+ *            pass 2 sums them per node and adds b.
+ *   impl 2 = "single pass FG DbD" (Eq. (4)): one thread per output node gathers its
+ *            27 inputs and 8 elements' (k, c) (3 x 3 strips staged in shared memory) and loops
+ *            over the 8 element-DoF contributions; reference matrices in constant memory.
+ *   impl 3 = the production stencil (= hf_apply_axpby).
+ * u, b (may be NULL), y: n_nodes fp64 as hf_apply_axpby; u and y must not alias.
+ * Asynchronous on the context stream.  fp64 contexts with one (k, c) per voxel, no slabs.
+ * Errors: HF_E_ARG (impl, NULL, alias), HF_E_STATE (fp32 / slab / vertex-averaged tets; impl 1
+ * without hf_ablation_prepare for the same (aK, aM), or coefficients changed since). */
+hf_status hf_apply_impl(hf_ctx *ctx, int32_t impl, double aK, double aM, double c, const double *u,
+                        const double *b, double *y);
+
+/* Implementation 1's preprocessing: A_e = aK k_e K_ref + aM c_e M_ref for every
+ * element, stored in ctx-owned device memory (n_elements x 64 fp64; plus n_nodes x 8 fp64 of
+ * contribution space).  Asynchronous.  Errors: HF_E_STATE (as hf_apply_impl), HF_E_OOM. */
+hf_status hf_ablation_prepare(hf_ctx *ctx, double aK, double aM);
+
 /* Jacobi diagonal diag_i = sum_{e ni i} (aK k_e K_ref[l,l] + aM c_e M_ref[l,l]) (P:117,
  * Jacobi_A P:659-662); 1 on Dirichlet rows (reading R3).  diag: n_nodes fp64. */
 hf_status hf_diag(hf_ctx *ctx, double aK, double aM, double *diag);

@@ -85,6 +85,8 @@ _SIGS = {
     "hf_set_precision": (_i32, [_vp, _i32]),
     "hf_set_vertex_coefficients": (_i32, [_vp, _vp, _vp]),
     "hf_time_kernel_a": (_i32, [_vp, _i32, C.POINTER(C.c_double)]),
+    "hf_apply_impl": (_i32, [_vp, _i32, _d, _d, _d, _dp, _dp, _dp]),
+    "hf_ablation_prepare": (_i32, [_vp, _d, _d]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -173,7 +175,7 @@ class Context:
         self.n_nodes_global = self.n_plane * (self.ne[2] + 1)
 
     def __del__(self):
-        if getattr(self, "ptr", None) and self.ptr.value:
+        if getattr(self, "ptr", None) and self.ptr.value and _lib is not None:   # (interpreter shutdown)
             _lib.hf_destroy(self.ptr)
             self.ptr = C.c_void_p(None)
 
@@ -228,6 +230,17 @@ def hf_apply(ctx: Context, aK: float, aM: float, u, y):
 def hf_apply_axpby(ctx: Context, aK: float, aM: float, c: float, u, b, y):
     _check(_lib.hf_apply_axpby(ctx.ptr, aK, aM, c, _ptr(u, ctx.n_nodes, "u"),
                                _ptr(b, ctx.n_nodes, "b", allow_none=True), _ptr(y, ctx.n_nodes, "y")))
+
+
+def hf_apply_impl(ctx: Context, impl: int, aK: float, aM: float, c: float, u, b, y):
+    """NEXT f4 ablation: Implementation 1 (two-pass, stored element matrices), 2 (single-pass
+    gather) or 3 (the production stencil) of the same apply."""
+    _check(_lib.hf_apply_impl(ctx.ptr, int(impl), aK, aM, c, _ptr(u, ctx.n_nodes, "u"),
+                              _ptr(b, ctx.n_nodes, "b", allow_none=True), _ptr(y, ctx.n_nodes, "y")))
+
+
+def hf_ablation_prepare(ctx: Context, aK: float, aM: float):
+    _check(_lib.hf_ablation_prepare(ctx.ptr, aK, aM))
 
 
 def hf_diag(ctx: Context, aK: float, aM: float, diag):

@@ -6,7 +6,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "hf_lib.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "hf_kernels.cuh"), os.path.join(ROOT, "include", "heatfem.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", "hf_kernels.cuh"), os.path.join(HERE, "csrc", "hf_ablate.cuh"),
+              os.path.join(ROOT, "include", "heatfem.h")]
 LIB = os.path.join(HERE, "libheatfem.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -10,6 +10,7 @@
 // converted at the boundary (no copy when nx1 is even and the pointer is on the device).
 #include "heatfem.h"
 #include "hf_kernels.cuh"
+#include "hf_ablate.cuh"
 
 #include <dlfcn.h>
 
@@ -233,6 +234,11 @@ struct hf_ctx {
     bool prof = false;
     double prof_ms[5] = {0, 0, 0, 0, 0};
     long long prof_n[5] = {0, 0, 0, 0, 0};
+    // NEXT f4 ablation (Implementation 1): stored scaled element matrices and vertex-order
+    // contributions (hf_ablation_prepare)
+    double *ab_A = nullptr, *ab_contrib = nullptr;
+    double ab_aK = 0.0, ab_aM = 0.0;
+    bool ab_ready = false;
 };
 
 static const int NW = 8;             // warps per stencil CTA
@@ -440,6 +446,24 @@ static void tet_voxel(const double h[3], double K[64], double M[64])
                 M[loc[i] * 8 + loc[j]] += V * (i == j ? 2.0 : 1.0) / 20.0;
             }
     }
+}
+
+// Q1 voxel matrices as dense 8 x 8 (NEXT f4 ablation kernels): tensor products of the 1D
+// k = (1/h)[[1,-1],[-1,1]] and m = (h/6)[[2,1],[1,2]], K = kx my mz + mx ky mz + mx my kz,
+// local node l = bx + 2 by + 4 bz.
+static void q1_voxel(const double h[3], double K[64], double M[64])
+{
+    for (int a = 0; a < 8; a++)
+        for (int b = 0; b < 8; b++) {
+            double m[3], k[3];
+            for (int d = 0; d < 3; d++) {
+                const bool same = ((a >> d) & 1) == ((b >> d) & 1);
+                m[d] = h[d] / 6.0 * (same ? 2.0 : 1.0);
+                k[d] = (same ? 1.0 : -1.0) / h[d];
+            }
+            K[a * 8 + b] = k[0] * m[1] * m[2] + m[0] * k[1] * m[2] + m[0] * m[1] * k[2];
+            M[a * 8 + b] = m[0] * m[1] * m[2];
+        }
 }
 
 // Unit-coefficient stiffness of each Kuhn tet in tet_loc order (gradient-path formula as in
@@ -975,6 +999,8 @@ static void ctx_free(hf_ctx *c)
     for (void *p : c->scratch) cudaFree(p);
     cudaFree(c->launches);
     cudaFree(c->flush);
+    cudaFree(c->ab_A);
+    cudaFree(c->ab_contrib);
     for (auto &kv : c->stacks) { ctx_free(kv.second); delete kv.second; }
     c->stacks.clear();
     delete c->comm;
@@ -1298,6 +1324,7 @@ hf_status hf_set_coefficients(hf_ctx *c, const double *k, const double *cc)
         for (auto &p : c->pool) p->key_valid = false;
     }
     c->coef_set = true;
+    c->ab_ready = false;
     return HF_OK;
 }
 
@@ -1336,6 +1363,7 @@ hf_status hf_set_vertex_coefficients(hf_ctx *c, const double *k, const double *c
     s.key_valid = false;
     for (auto &p : c->pool) p->key_valid = false;
     c->coef_set = true;
+    c->ab_ready = false;
     return HF_OK;
 }
 
@@ -1422,6 +1450,87 @@ hf_status hf_diag(hf_ctx *c, double aK, double aM, double *diag)
     HFCK(enqueue_diag(c, c->sys0, aK, aM, dd, nullptr));
     if (diag == dd) return HF_OK;
     return node_out_finish(c, diag, dd);
+}
+
+// ---- NEXT f4: the paper's earlier interpretations of the assembly operator (hf_ablate.cuh) ----
+
+static hf_status ablation_ok(const hf_ctx *c, const char *who)
+{
+    if (!c->coef_set) return fail(HF_E_STATE, std::string(who) + ": coefficients not set");
+    if (c->es != 8) return fail(HF_E_STATE, std::string(who) + ": the ablation kernels are fp64 only");
+    if (c->nranks > 1 || c->comm) return fail(HF_E_STATE, std::string(who) + ": not available on a slab context");
+    if (c->elem == EL_DENSE && c->tetv)
+        return fail(HF_E_STATE, std::string(who) + ": not available with per-tet vertex-averaged coefficients");
+    return HF_OK;
+}
+
+static Dense ablation_dense(const hf_ctx *c, double aK, double aM)
+{
+    double K[64], M[64];
+    if (c->elem == EL_DENSE) tet_voxel(c->g.h, K, M);
+    else q1_voxel(c->g.h, K, M);
+    Dense dn;
+    for (int i = 0; i < 64; i++) {
+        dn.K[i] = aK * K[i];
+        dn.M[i] = aM * M[i];
+    }
+    return dn;
+}
+
+hf_status hf_ablation_prepare(hf_ctx *c, double aK, double aM)
+{
+    if (!c) return fail(HF_E_ARG, "hf_ablation_prepare: NULL context");
+    HFCK(ablation_ok(c, "hf_ablation_prepare"));
+    CUCK(cudaSetDevice(c->device));
+    const long long nelem = c->g.ne[0] * c->g.ne[1] * c->g.ne[2];
+    if (!c->ab_A) {
+        CUCK(cudaMalloc(&c->ab_A, (size_t)nelem * 64 * sizeof(double)));
+        CUCK(cudaMalloc(&c->ab_contrib, (size_t)c->nloc * 8 * sizeof(double)));
+    }
+    const long long nrows = nelem * 8;
+    k_ebe_store<<<(unsigned)((nrows + 255) / 256), 256, 0, c->stream>>>(make_geom(c), c->sys0.kc,
+                                                                      ablation_dense(c, aK, aM), c->ab_A, nrows,
+                                                                      c->launches);
+    CUCK(cudaGetLastError());
+    c->ab_aK = aK;
+    c->ab_aM = aM;
+    c->ab_ready = true;
+    return HF_OK;
+}
+
+hf_status hf_apply_impl(hf_ctx *c, int32_t impl, double aK, double aM, double cc, const double *u, const double *b,
+                        double *y)
+{
+    if (impl == 3) return hf_apply_axpby(c, aK, aM, cc, u, b, y);
+    if (!c || !u || !y) return fail(HF_E_ARG, "hf_apply_impl: NULL argument");
+    if (impl != 1 && impl != 2) return fail(HF_E_ARG, "hf_apply_impl: impl must be 1, 2 or 3");
+    if ((const double *)y == u) return fail(HF_E_ARG, "hf_apply_impl: u and y must not alias");
+    HFCK(ablation_ok(c, "hf_apply_impl"));
+    if (impl == 1 && (!c->ab_ready || aK != c->ab_aK || aM != c->ab_aM))
+        return fail(HF_E_STATE, "hf_apply_impl: Implementation 1 needs hf_ablation_prepare with the same (aK, aM)");
+    CUCK(cudaSetDevice(c->device));
+    const double *du, *db = nullptr;
+    double *dy;
+    HFCK(node_in(c, u, 3, &du));
+    if (b) HFCK(node_in(c, b, 4, &db));
+    HFCK(node_out(c, y, 5, false, &dy));
+    const Geom g = make_geom(c);
+    const int nz = (int)c->g.ne[2];
+    if (impl == 1) {
+        const long long nelem = c->g.ne[0] * c->g.ne[1] * c->g.ne[2];
+        k_ebe_pass1<<<(unsigned)((nelem + 31) / 32), 256, 0, c->stream>>>(g, du, c->ab_A, c->ab_contrib, nelem,
+                                                                         c->launches);
+        CUCK(cudaGetLastError());
+        k_ebe_pass2<<<(unsigned)((c->nloc + 255) / 256), 256, 0, c->stream>>>(g, nz, c->ab_contrib, cc, db, dy,
+                                                                             c->nloc, c->launches);
+    } else {
+        const dim3 grid((unsigned)((c->nx1 + DBD_W - 1) / DBD_W), (unsigned)c->ny1, (unsigned)c->nzl);
+        k_dbd<<<grid, DBD_W, 0, c->stream>>>(g, nz, du, c->sys0.kc, ablation_dense(c, aK, aM), cc, db, dy,
+                                             c->launches);
+    }
+    CUCK(cudaGetLastError());
+    if (y == dy) return HF_OK;
+    return node_out_finish(c, y, dy);
 }
 
 hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, const hf_cg_opts *opts,
@@ -2204,6 +2313,7 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
     if (!c || type < 0 || type > 1) return fail(HF_E_ARG, "hf_set_element: type must be 0 (Q1) or 1 (6 P1 tets)");
     CUCK(cudaSetDevice(c->device));
     c->elem = type;
+    c->ab_ready = false;
     const double *h = c->g.h;
     // the dense (tet) element keeps R = 2 tiles (R = 4 spills); TMA boxes follow the tile height
     int want_r = default_tile_r(c, type);
