@@ -152,6 +152,18 @@ def run_ours(args):
     plane = (g.ne[0] + 1) * (g.ne[1] + 1)
     kd = torch.tensor(p.k, device=dev)
     cd = torch.tensor(p.c, device=dev)
+    # per-element fp64 (k, c) pairs (default), or the paper's material description -- two
+    # materials by region, one uint8 id per element (hf_set_material_ids, --coef ids)
+    use_ids = args.coef == "ids"
+    kmat = [m[1] for m in p.extra["materials"]]
+    cmat = [m[0] for m in p.extra["materials"]]
+    idsd = torch.tensor(p.extra["ids"], device=dev)
+
+    def set_coef(c_, k_, c2_, ids_):
+        if use_ids:
+            hf.hf_set_material_ids(c_, ids_, kmat, cmat)
+        else:
+            hf.hf_set_coefficients(c_, k_, c2_)
     if not slab:
         ctx = hf.hf_create(g, local_rank)
         z0, lp = 0, g.ne[2] + 1
@@ -161,7 +173,7 @@ def run_ours(args):
         dist.broadcast_object_list(obj, src=0)
         ctx = hf.hf_create_slab(g, rank, world, obj[0], transport=0, device=local_rank)
         _, _, lp, z0 = ctx.slab
-    hf.hf_set_coefficients(ctx, kd, cd)
+    set_coef(ctx, kd, cd, idsd)
     F = torch.empty(ctx.n_nodes, dtype=torch.float64, device=dev)
     hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
     u = torch.zeros(ctx.n_nodes, dtype=torch.float64, device=dev)
@@ -223,9 +235,9 @@ def run_ours(args):
     a_avg_ms = hf.hf_time_kernel_a(ctx, 200) if not slab else a_bracketed_ms
     nodes_local = plane * lp
     elems_local = g.ne[0] * g.ne[1] * max(lp - 1, 1)
-    # algorithmic bytes of one kernel-A launch: read s, d_old (16 B/node) + (k,c) (16 B/element),
-    # write d_new, q (16 B/node)
-    a_bytes = 32.0 * nodes_local + 16.0 * elems_local
+    # algorithmic bytes of one kernel-A launch: read s, d_old (16 B/node) + the element
+    # coefficients (a uint8 material id, or a (k, c) fp64 pair: 16 B/element), write d_new, q
+    a_bytes = 32.0 * nodes_local + (1.0 if use_ids else 16.0) * elems_local
     peak, peak_src = measured_peaks()
     achieved = a_bytes / (a_avg_ms * 1e-3) / 1e9
 
@@ -235,25 +247,29 @@ def run_ours(args):
     if not slab:
         kh = torch.tensor(p.k).pin_memory()
         ch = torch.tensor(p.c).pin_memory()
+        idh = torch.tensor(p.extra["ids"]).pin_memory()
         uh = torch.zeros(g.n_nodes, dtype=torch.float64).pin_memory()
         snap = torch.empty(args.steps * plane, dtype=torch.float64).pin_memory()
         ctx2 = hf.hf_create(g, local_rank)
         Fe = torch.empty(g.n_nodes, dtype=torch.float64, device=dev)
-        hf.hf_set_coefficients(ctx2, kh, ch)
+        set_coef(ctx2, kh, ch, idh)
         hf.hf_face_load(ctx2, p.flux_face, p.flux_const, None, Fe)
         hf.hf_simulate(ctx2, p.theta, p.dt, 2, Fe, torch.zeros(g.n_nodes, dtype=torch.float64, device=dev))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        hf.hf_set_coefficients(ctx2, kh, ch)
+        set_coef(ctx2, kh, ch, idh)
         hf.hf_face_load(ctx2, p.flux_face, p.flux_const, None, Fe)
         se = hf.hf_simulate(ctx2, p.theta, p.dt, args.steps, Fe, uh, 0, snap, rtol=p.rtol)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - t0) * 1e3
+        coef_bytes = idh.numel() + 16 * len(kmat) if use_ids else (kh.numel() + ch.numel()) * 8
         e2e = {"value": wall / args.steps, "unit": UNIT,
-               "h2d_bytes_per_step": int((kh.numel() + ch.numel() + uh.numel()) * 8 / args.steps),
+               "h2d_bytes_per_step": int((coef_bytes + uh.numel() * 8) / args.steps),
                "d2h_bytes_per_step": int(plane * 8 + uh.numel() * 8 / args.steps),
-               "how": "wall clock around hf_set_coefficients + hf_face_load + hf_simulate(K steps) with pinned "
-                      "host k, c, u0, u_N and a per-step front-face snapshot (host)"}
+               "how": "wall clock around " + ("hf_set_material_ids (pinned uint8 ids)" if use_ids else
+                                              "hf_set_coefficients (pinned k, c)") +
+                      " + hf_face_load + hf_simulate(K steps) with pinned host u0, u_N and a per-step "
+                      "front-face snapshot (host)"}
         del ctx2
     else:
         # N ranks: each rank feeds its slab from pinned host memory (global k, c; its planes of
@@ -264,7 +280,7 @@ def run_ours(args):
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        hf.hf_set_coefficients(ctx, kh, ch)
+        set_coef(ctx, kh, ch, torch.tensor(p.extra["ids"]).pin_memory())
         hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
         se = hf.hf_simulate(ctx, p.theta, p.dt, args.steps, F, uh, rtol=p.rtol)
         torch.cuda.synchronize()
@@ -283,14 +299,17 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded inclusion field, synth.c3)",
+            "coefficients": ("material ids (uint8 per element, 2-entry table: steel / Fe2O3, P:271)" if use_ids
+                             else "per-element fp64 (k, c) pairs"),
             "config": workload_config(p, world, {"pcg_iters_per_step": iters / args.steps,
                                                  "us_per_pcg_iter": total_ms / max(iters, 1) * 1e3}),
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic("stencil_cg_a_c3"),
-                         "kernel": "k_stencil<LD_CGD,EP_CGA> (PCG kernel A: d = s + beta d; q = A d; d.q)",
+                         "traffic": ncu_traffic("stencil_cg_a_c3_ids" if use_ids else "stencil_cg_a_c3"),
+                         "kernel": "k_stencil<LD_CGD,EP_CGA,%s> (PCG kernel A: d = s + beta d; q = A d; d.q)"
+                                   % ("EL_Q1P" if use_ids else "EL_Q1"),
                          "bytes_per_launch": a_bytes, "avg_launch_ms": a_avg_ms,
                          "avg_launch_ms_how": "200 back-to-back launches between one CUDA event pair on the "
                                               "context stream (hf_time_kernel_a)",
@@ -306,7 +325,9 @@ def run_ours(args):
         if rank == 0:
             line["apply_512_slabs"] = a512
     if not slab:
+        line["c3_other_coef"] = variant_c3(hf, torch, dev, 64, p.rtol, coef="pairs" if use_ids else "ids")
         line["apply_512"] = apply_512(hf, torch, dev, peak)
+        line["apply_512_ids"] = apply_512(hf, torch, dev, peak, ids=True)
         line["c5_batched"] = c5_batched(hf, torch, dev, world)
         # the paper's settings for the inverse problem: rtol 1e-6, single precision
         line["c5_batched_fp32_rtol1e-6"] = c5_batched(hf, torch, dev, world, prec=32, rtol=1e-6)
@@ -316,23 +337,29 @@ def run_ours(args):
     return line
 
 
-def apply_512(hf, torch, dev, peak, prec=64):
+def apply_512(hf, torch, dev, peak, prec=64, ids=False):
     """Operator apply (Eq. (1)) on the 512^3-node grid of C4, HBM-bound: inputs 4.3 GB >> L2.
-    prec=32: the fp32 storage variant (NEXT f3), half the bytes."""
+    prec=32: the fp32 storage variant (NEXT f3), half the bytes.  ids=True: two materials by id
+    (steel / Fe2O3, 20 % oxide, i.i.d. per element), 1 B per element instead of a 16-B pair."""
     g = synth.c4_grid(512)
     gen = torch.Generator(device=dev).manual_seed(0)
-    k = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) * 121.5 + 1.0
-    c = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) + 1.0
     ctx = hf.hf_create(g, dev.index)
     if prec != 64:
         hf.hf_set_precision(ctx, prec)
-    hf.hf_set_coefficients(ctx, k, c)
-    del k, c
+    if ids:
+        idv = (torch.rand(g.n_elems, device=dev, generator=gen) < 0.2).to(torch.uint8)
+        hf.hf_set_material_ids(ctx, idv, [synth.STEEL[1], synth.OXIDE[1]], [synth.STEEL[0], synth.OXIDE[0]])
+        del idv
+    else:
+        k = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) * 121.5 + 1.0
+        c = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) + 1.0
+        hf.hf_set_coefficients(ctx, k, c)
+        del k, c
     torch.cuda.empty_cache()
     if prec == 64:
         u = torch.randn(g.n_nodes, dtype=torch.float64, device=dev, generator=gen)
         y = torch.empty_like(u)
-        return _apply_time(hf, torch, dev, peak, ctx, g, u, y, 8)
+        return _apply_time(hf, torch, dev, peak, ctx, g, u, y, 8, ids=ids)
     return _apply_time_internal(hf, torch, dev, peak, ctx, g, prec)
 
 
@@ -400,7 +427,7 @@ def _apply_time_internal(hf, torch, dev, peak, ctx, g, prec):
             "kernel": f"k_stencil<LD_RAW,EP_APPLY,fp{prec}> 512^3 nodes, mean of 10 (per-launch events)"}
 
 
-def _apply_time(hf, torch, dev, peak, ctx, g, u, y, es):
+def _apply_time(hf, torch, dev, peak, ctx, g, u, y, es, ids=False):
     for _ in range(3):
         hf.hf_apply(ctx, 0.005, 1.0, u, y)
     s = torch.cuda.current_stream(dev)
@@ -413,22 +440,29 @@ def _apply_time(hf, torch, dev, peak, ctx, g, u, y, es):
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = statistics.median(ts)
-    byts = 2.0 * es * g.n_nodes + 2.0 * es * g.n_elems      # read u + write y + read (k, c)
+    # read u + write y + read (k, c) pairs (2 es B per element) or material ids (1 B per element)
+    byts = 2.0 * es * g.n_nodes + (1.0 if ids else 2.0 * es) * g.n_elems
     ach = byts / (ms * 1e-3) / 1e9
     del ctx
     torch.cuda.empty_cache()
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "ms": ms,
-            "bytes_per_launch": byts, "traffic": ncu_traffic("stencil_apply_512"),
-            "kernel": "k_stencil<LD_RAW,EP_APPLY> (y = (aK K + aM M) u), 512^3 nodes, median of 10"}
+            "bytes_per_launch": byts, "traffic": ncu_traffic("stencil_apply_512_ids" if ids else "stencil_apply_512"),
+            "kernel": "k_stencil<LD_RAW,EP_APPLY,%s> (y = (aK K + aM M) u), 512^3 nodes, median of 10"
+                      % ("EL_Q1P, material ids" if ids else "EL_Q1, (k, c) pairs")}
 
 
-def variant_c3(hf, torch, dev, prec, rtol, steps=10, warm=3):
-    """C3 time steps of a precision / tolerance variant, L2 flushed before each timed step."""
+def variant_c3(hf, torch, dev, prec, rtol, steps=10, warm=3, coef="pairs"):
+    """C3 time steps of a precision / tolerance / coefficient-layout variant, L2 flushed before
+    each timed step."""
     p = synth.c3(nsteps=steps + warm)
     ctx = hf.hf_create(p.grid, dev.index)
     if prec != 64:
         hf.hf_set_precision(ctx, prec)
-    hf.hf_set_coefficients(ctx, torch.tensor(p.k, device=dev), torch.tensor(p.c, device=dev))
+    if coef == "ids":
+        hf.hf_set_material_ids(ctx, torch.tensor(p.extra["ids"], device=dev),
+                               [m[1] for m in p.extra["materials"]], [m[0] for m in p.extra["materials"]])
+    else:
+        hf.hf_set_coefficients(ctx, torch.tensor(p.k, device=dev), torch.tensor(p.c, device=dev))
     F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=dev)
     hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
     u = torch.zeros(p.grid.n_nodes, dtype=torch.float64, device=dev)
@@ -438,7 +472,8 @@ def variant_c3(hf, torch, dev, prec, rtol, steps=10, warm=3):
     st = hf.hf_simulate_resume(ctx, p.theta, p.dt, steps, F, u, up, warm, rtol=rtol)
     hf.hf_set_step_flush(ctx, False)
     del ctx
-    return {"precision": f"fp{prec}", "rtol": rtol, "steps": steps, "ms_per_step": st["ms_steps"] / steps,
+    return {"precision": f"fp{prec}", "coefficients": coef, "rtol": rtol, "steps": steps,
+            "ms_per_step": st["ms_steps"] / steps,
             "pcg_iters_per_step": st["total_iters"] / steps,
             "us_per_pcg_iter": st["ms_steps"] / max(st["total_iters"], 1) * 1e3}
 
@@ -540,6 +575,10 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--coef", choices=["ids", "pairs"], default="pairs",
+                    help="element coefficients as per-element fp64 (k, c) pairs (default) or material ids "
+                         "(the paper's two-material field, 1 B per element; no faster at C3, whose kernel A "
+                         "is latency-bound, but 16 %% faster for the HBM-bound 512^3 apply)")
     ap.add_argument("--force-slab", action="store_true",
                     help="run the multi-GPU (z-slab, NCCL) code path even on one rank (validation)")
     args = ap.parse_args()

@@ -121,6 +121,19 @@ hf_status hf_set_dirichlet_faces(hf_ctx *ctx, uint32_t face_bits, const double v
  * Errors: HF_E_ARG. */
 hf_status hf_set_element(hf_ctx *ctx, int32_t type);
 
+/* Materials by id: element e has conductivity k_mat[ids[e]] and capacity c_mat[ids[e]] -- the
+ * paper's material description (a few materials by region: steel / oxide; the corrosion
+ * plate), i.e. a segmented voxel model.  The operator is exactly the one
+ * hf_set_coefficients gives for k_e = k_mat[ids[e]], c_e = c_mat[ids[e]] (bit for bit); on fp64
+ * Q1 contexts the stencil then streams one byte per element instead of a 16-byte (k, c) pair and
+ * looks the element's coefficients up in a per-CTA shared-memory table (kernel variant EL_Q1P;
+ * other element types and fp32 use the pair layout, filled from the table).
+ * ids: n_elements uint8 (host or device, natural element order); n_materials in [1, 63];
+ * k_mat, c_mat: n_materials fp64 (host).  hf_set_coefficients switches back to per-element pairs.
+ * Synchronises.  Errors: HF_E_ARG (NULL, n_materials), HF_E_INDEX (an id >= n_materials). */
+hf_status hf_set_material_ids(hf_ctx *ctx, const uint8_t *ids, int32_t n_materials, const double *k_mat,
+                              const double *c_mat);
+
 /* Materials given per node instead of per element (the paper's scheme: the material function is
  * "computed ... at each vertex and the values averaged over each element").
  * k_node, c_node: n_nodes fp64 of the GLOBAL grid (natural node order; slab contexts use their

@@ -87,6 +87,7 @@ _SIGS = {
     "hf_time_kernel_a": (_i32, [_vp, _i32, C.POINTER(C.c_double)]),
     "hf_apply_impl": (_i32, [_vp, _i32, _d, _d, _d, _dp, _dp, _dp]),
     "hf_ablation_prepare": (_i32, [_vp, _d, _d]),
+    "hf_set_material_ids": (_i32, [_vp, _vp, _i32, _P(C.c_double), _P(C.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -230,6 +231,31 @@ def hf_apply(ctx: Context, aK: float, aM: float, u, y):
 def hf_apply_axpby(ctx: Context, aK: float, aM: float, c: float, u, b, y):
     _check(_lib.hf_apply_axpby(ctx.ptr, aK, aM, c, _ptr(u, ctx.n_nodes, "u"),
                                _ptr(b, ctx.n_nodes, "b", allow_none=True), _ptr(y, ctx.n_nodes, "y")))
+
+
+def hf_set_material_ids(ctx: Context, ids, k_mat: Sequence[float], c_mat: Sequence[float]):
+    """Materials by id: k_e = k_mat[ids[e]], c_e = c_mat[ids[e]] (uint8 ids, torch or numpy)."""
+    n = len(k_mat)
+    if len(c_mat) != n:
+        raise HfError(HF_E_ARG, "k_mat and c_mat differ in length")
+    ptr = None
+    try:
+        import torch
+        if isinstance(ids, torch.Tensor):
+            if ids.dtype != torch.uint8 or not ids.is_contiguous() or ids.numel() != ctx.n_elems:
+                raise HfError(HF_E_ARG, "ids: need a contiguous uint8 tensor of n_elements")
+            ptr = ids.data_ptr()
+    except ImportError:
+        pass
+    if ptr is None:
+        import numpy as np
+        if not isinstance(ids, np.ndarray) or ids.dtype != np.uint8 or not ids.flags.c_contiguous \
+                or ids.size != ctx.n_elems:
+            raise HfError(HF_E_ARG, "ids: need a contiguous uint8 array of n_elements")
+        ptr = ids.ctypes.data
+    km = (C.c_double * n)(*[float(v) for v in k_mat])
+    cm = (C.c_double * n)(*[float(v) for v in c_mat])
+    _check(_lib.hf_set_material_ids(ctx.ptr, C.c_void_p(ptr), n, km, cm))
 
 
 def hf_apply_impl(ctx: Context, impl: int, aK: float, aM: float, c: float, u, b, y):

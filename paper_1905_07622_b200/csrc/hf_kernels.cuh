@@ -123,8 +123,13 @@ template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
 
 // element variants: Q1 hexahedra; the 6-tet split with one (k, c) per voxel (dense 8x8 voxel
-// matrices); the 6-tet split with per-tet coefficients averaged from vertex values
-enum { EL_Q1 = 0, EL_DENSE = 1, EL_TETV = 2 };
+// matrices); the 6-tet split with per-tet coefficients averaged from vertex values;
+// Q1 hexahedra with coefficients given by material id (hf_set_material_ids, fp64 only): the
+// stencil streams one uint8 id per element instead of a 16-B (k, c) pair and looks the
+// element's z-butterfly coefficients up in a per-CTA shared-memory table
+enum { EL_Q1 = 0, EL_DENSE = 1, EL_TETV = 2, EL_Q1P = 3 };
+constexpr int PAL_MAX = 64;        // material table entries; entry 0 = (0, 0) (outside the domain)
+constexpr int PAL_BW = 48;         // ids per TMA box row: 16-aligned origin <= X0-1, covers X0+30
 
 // Kuhn tets of a voxel (local node l = bx + 2 by + 4 bz): tet t follows 0 -> e_a -> e_a+e_b -> 7
 // for the t-th axis order (x,y,z), (x,z,y), (y,x,z), (y,z,x), (z,x,y), (z,y,x)
@@ -188,6 +193,8 @@ struct StencilArgs {
     DenseF dnf;                   // EL_DENSE, fp32 variant
     TetV tv;                      // EL_TETV only
     TetVF tvf;                    // EL_TETV, fp32 variant
+    double pal[PAL_MAX][2];       // EL_Q1P: (k, c) of material id m (entry 0 = (0, 0))
+    int npal;                     // EL_Q1P: table entries in use (materials + 1)
 };
 // Node-vector pointers of StencilArgs / BArgs / StepArgs are declared double* but address
 // vectors of the context's storage type; kernels instantiated for Real = float reinterpret them.
@@ -436,12 +443,18 @@ struct StencilShape {
     static constexpr int AL = 128 / ES;                                      // elements per 128 B
     static constexpr int NODE_BOX = H * BW;                                  // elements per node box
     static constexpr int NODE_DBL = (NODE_BOX + AL - 1) / AL * AL;           // 128-B aligned slot
-    // per-element (k, c) box: NW R element rows x KW; EL_TETV: per-node pairs, H rows x 2 BW
-    static constexpr int KC_DBL = EL == EL_TETV ? H * 2 * BW : NW * R * KW;
+    // per-element (k, c) box: NW R element rows x KW; EL_TETV: per-node pairs, H rows x 2 BW;
+    // EL_Q1P: NW R rows of PAL_BW uint8 material ids
+    static constexpr int KC_BYTES = EL == EL_TETV ? H * 2 * BW * ES : (EL == EL_Q1P ? NW * R * PAL_BW : NW * R * KW * ES);
+    static constexpr int KC_DBL = (KC_BYTES + ES - 1) / ES;
     static constexpr int STAGE_DBL = (NA * NODE_DBL + KC_DBL + AL - 1) / AL * AL;
-    static constexpr unsigned STAGE_BYTES = (NA * NODE_BOX + KC_DBL) * (unsigned)ES;   // TMA bytes
+    static constexpr unsigned STAGE_BYTES = NA * NODE_BOX * (unsigned)ES + KC_BYTES;   // TMA bytes
+    static constexpr int PAL_BYTES = EL == EL_Q1P ? PAL_MAX * 8 * 8 : 0;    // (a, b) x 4 channels per material
     // rounded to 1 KB so that CTAs of different variants sharing an SM get aligned windows
-    static size_t smem_bytes(int ns) { return HF_SMEM_ROUND((size_t)ns * STAGE_DBL * ES + 16 * ns + 2 * NW * 32 * ES); }
+    static size_t smem_bytes(int ns)
+    {
+        return HF_SMEM_ROUND((size_t)ns * STAGE_DBL * ES + 16 * ns + 2 * NW * 32 * ES + PAL_BYTES);
+    }
 };
 
 // compile-time variant flags of the stencil kernel
@@ -528,6 +541,9 @@ k_stencil(const __grid_constant__ StencilArgs a)
     Real *stage = reinterpret_cast<Real *>(smem_d);
     uint64_t *bars = reinterpret_cast<uint64_t *>(stage + NS * SH::STAGE_DBL);
     Real(*seam)[NW][32] = reinterpret_cast<Real(*)[NW][32]>(stage + NS * SH::STAGE_DBL + (16 / ES) * NS);
+    // EL_Q1P: per material the (a, b) coefficients of the fused z butterfly, as the pair path
+    // computes them from (k, c) (bit-identical): palt[m] = {a0, b0, a1, b1, a2, b2, a3, b3}
+    double(*palt)[8] = reinterpret_cast<double(*)[8]>(seam + 2);
 
     const int X0 = blockIdx.x * TILE_X;
     const int Y0 = blockIdx.y * (NW * R - 1);
@@ -559,6 +575,8 @@ k_stencil(const __grid_constant__ StencilArgs a)
         if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, a.tm + map1, xb, Y0 - 1, p, &bars[st]);
         if (EL == EL_TETV)   // per-node (k, c) pairs of plane p, same rows as the node box
             tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KCN, 2 * xb, Y0 - 1, p, &bars[st]);
+        else if (EL == EL_Q1P)   // material ids of element layer p - 1 (16-B aligned x origin)
+            tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KC, (X0 - 1) & ~15, Y0 - 1, p, &bars[st]);
         else                 // element layer L = p - 1 sits at z = p in the kc tensor
             tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KC, kb, Y0 - 1, p, &bars[st]);
     };
@@ -576,6 +594,16 @@ k_stencil(const __grid_constant__ StencilArgs a)
     __syncthreads();
     if (tid == 0)
         for (int i = 0; i < NS && i < nplanes; i++) issue(i);
+    if constexpr (EL == EL_Q1P) {
+        // the material table, built while the first TMA loads are in flight (entries in use only)
+        for (int i = tid; i < a.npal * 4; i += NT) {
+            const int m = i >> 2, ch = i & 3;
+            const double kk = a.pal[m][0], cc = a.pal[m][1];
+            palt[m][2 * ch] = fma(kk, a.lam.ka[ch], cc * a.lam.ma[ch]);
+            palt[m][2 * ch + 1] = fma(kk, a.lam.kb[ch], cc * a.lam.mb[ch]);
+        }
+        __syncthreads();
+    }
 
     if (EP == EP_CGA) {
         // start of PCG iteration i from the previous kernel's partial sums (overlaps the TMA)
@@ -655,9 +683,25 @@ k_stencil(const __grid_constant__ StencilArgs a)
         const Real *n0 = sb + w * R * SH::BW + lane + xoff;                 // row 0 of this warp
         const Real *n1 = sb + SH::NODE_DBL + w * R * SH::BW + lane + xoff;
         const Real *kcs = sb + NA * SH::NODE_DBL + w * R * SH::KW + koff + 2 * lane;
+        const unsigned char *kis = reinterpret_cast<const unsigned char *>(sb + NA * SH::NODE_DBL) + w * R * PAL_BW +
+                                   ((X0 - 1) - ((X0 - 1) & ~15)) + lane;                      // EL_Q1P
         const Real *kns = sb + NA * SH::NODE_DBL + w * R * (2 * SH::BW) + 2 * (lane + xoff);   // EL_TETV
         // ---- node values of plane p (rows 0..R), x butterfly (edges) ----------------------
         Real S[R + 1], D[R + 1], V0[R + 1], V1[R + 1], craw[R];
+        // EL_Q1P: the element layer's (a, b) coefficients are looked up first (id, then table),
+        // so the two dependent shared-memory round trips overlap the node loads and butterflies
+        double2 pabr[EL == EL_Q1P ? R : 1][4];
+        if constexpr (EL == EL_Q1P) {
+            int idr[R];
+#pragma unroll
+            for (int r = 0; r < R; r++) idr[r] = kis[r * PAL_BW];
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const double2 *pe = reinterpret_cast<const double2 *>(palt[idr[r]]);
+#pragma unroll
+                for (int ch = 0; ch < 4; ch++) pabr[r][ch] = pe[ch];
+            }
+        }
         const bool store_p = (EP == EP_CGA || EP == EP_RESID_INIT) && (p >= a.zs0 && p < a.zs1) &&
                              ((p >= zb && p < ze) || (p == zb - 1 && zb == a.z_out0) ||
                               (p == ze && ze == a.z_out1));
@@ -702,7 +746,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
         const int pout = p - 1;
         const bool out_plane = pout >= zb && pout < ze;   // uniform across the CTA
         Real yv[R + 1];
-        if (EL == EL_Q1) {
+        if (EL == EL_Q1 || EL == EL_Q1P) {
             // ---- element layer p-1: y butterfly, fused z butterfly + scaling -------------------
             // (lane 31's element X0+30 reads node X0+31 from the box; elements outside the domain
             //  have k = c = 0 from the TMA zero fill)
@@ -748,11 +792,16 @@ k_stencil(const __grid_constant__ StencilArgs a)
                 Fc[1] = S[r] - S[r + 1];   // sx=0, sy=1
                 Fc[2] = D[r] + D[r + 1];   // sx=1, sy=0
                 Fc[3] = D[r] - D[r + 1];   // sx=1, sy=1
-                const V2 kc = *reinterpret_cast<const V2 *>(kcs + r * SH::KW);
+                V2 kc;
+                if constexpr (EL != EL_Q1P) kc = *reinterpret_cast<const V2 *>(kcs + r * SH::KW);
 #pragma unroll
                 for (int ch = 0; ch < 4; ch++) {
-                    const Real av = fma(kc.x, LKA(ch), kc.y * LMA(ch));
-                    const Real bv = fma(kc.x, LKB(ch), kc.y * LMB(ch));
+                    Real av, bv;
+                    if constexpr (EL == EL_Q1P) { av = pabr[r][ch].x; bv = pabr[r][ch].y; }
+                    else {
+                        av = fma(kc.x, LKA(ch), kc.y * LMA(ch));
+                        bv = fma(kc.x, LKB(ch), kc.y * LMB(ch));
+                    }
                     T[r][ch] = fma(av, Fp[r][ch], fma(bv, Fc[ch], Cy[r][ch]));   // bottom plane p-1
                     Cy[r][ch] = fma(bv, Fp[r][ch], av * Fc[ch]);                  // top plane p
                     Fp[r][ch] = Fc[ch];
@@ -1194,6 +1243,53 @@ __global__ void k_pack(Geom g, int nz, const double *k, const double *c, void *k
         v.y = c ? (Real)c[e] : Real(0);
     }
     kc[i] = v;
+}
+
+// ---- materials by id (hf_set_material_ids) --------------------------------------------------
+struct PalTab {
+    double kc[PAL_MAX][2];  // (k, c) of material m (m < n_materials)
+};
+
+// (k, c) pairs from ids, in the k_pack layout (for the kernels that read pairs: diagonal,
+// extraction, the other element variants); *bad = 1 if an id is out of range
+template <class Real>
+__global__ void k_pack_ids(Geom g, int nz, const unsigned char *ids, int nmat, PalTab pt, void *kcp, long long ntot,
+                           int *bad, unsigned long long *launches)
+{
+    using V2 = typename Vec2<Real>::type;
+    V2 *kc = reinterpret_cast<V2 *>(kcp);
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && launches) atomicAdd(launches, 1ull);
+    if (i >= ntot) return;
+    const int ex = (int)(i % g.kpitch), ey = (int)((i / g.kpitch) % g.ny);
+    const int L = (int)(i / ((long long)g.kpitch * g.ny)) - 1;
+    const int ez = g.zg0 + L;
+    V2 v;
+    v.x = Real(0);
+    v.y = Real(0);
+    if (ex < g.nx && ez >= 0 && ez < nz) {
+        const int m = ids[ex + (long long)g.nx * (ey + (long long)g.ny * ez)];
+        if (m < nmat) {
+            v.x = (Real)pt.kc[m][0];
+            v.y = (Real)pt.kc[m][1];
+        } else *bad = 1;
+    }
+    kc[i] = v;
+}
+
+// id + 1 per element in the (kp, ny, nzl + 1) layer layout (0 = outside the domain / padding)
+__global__ void k_pack_kid(Geom g, int nz, const unsigned char *ids, int kp, unsigned char *kid, long long ntot,
+                           unsigned long long *launches)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && launches) atomicAdd(launches, 1ull);
+    if (i >= ntot) return;
+    const int ex = (int)(i % kp), ey = (int)((i / kp) % g.ny);
+    const int L = (int)(i / ((long long)kp * g.ny)) - 1;
+    const int ez = g.zg0 + L;
+    unsigned char v = 0;
+    if (ex < g.nx && ez >= 0 && ez < nz) v = (unsigned char)(ids[ex + (long long)g.nx * (ey + (long long)g.ny * ez)] + 1);
+    kid[i] = v;
 }
 
 // ---- flux load F_i = int_face f phi_i ds (reading R12) ----------------------------

@@ -239,6 +239,14 @@ struct hf_ctx {
     double *ab_A = nullptr, *ab_contrib = nullptr;
     double ab_aK = 0.0, ab_aM = 0.0;
     bool ab_ready = false;
+    // materials by id (hf_set_material_ids): uint8 ids + 1 in the (k, c) layer layout, the
+    // material table, and the id tensor's TMA descriptor (sys0's kc map while pal_on)
+    unsigned char *kid = nullptr;
+    int kid_pitch = 0;               // ids per row (nx rounded up to 16: TMA strides)
+    double pal[PAL_MAX][2] = {};
+    int npal = 0;                    // table entries in use (materials + 1)
+    bool pal_on = false;
+    CUtensorMap kid_map;
 };
 
 static const int NW = 8;             // warps per stencil CTA
@@ -533,6 +541,22 @@ static hf_status kcn_map(const hf_ctx *c, const void *kcn, CUtensorMap *m)
     return HF_OK;
 }
 
+// material ids (EL_Q1P): uint8 view (kid_pitch, ny, nzl + 1), layer L at z = L + 1 as kc
+static hf_status kid_map_enc(const hf_ctx *c, const void *kid, CUtensorMap *m)
+{
+    HFCK(get_encode());
+    const cuuint64_t kp = (cuuint64_t)c->kid_pitch, ny = (cuuint64_t)c->g.ne[1];
+    const cuuint64_t dims[3] = {kp, ny, (cuuint64_t)c->nzl + 1};
+    const cuuint64_t strides[2] = {kp, kp * ny};
+    const cuuint32_t box[3] = {(cuuint32_t)PAL_BW, (cuuint32_t)(NW * c->tileR), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void *)kid, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HF_E_CUDA, "cuTensorMapEncodeTiled(kid) failed: " + std::to_string((int)r));
+    return HF_OK;
+}
+
 // ============================================================================================
 // launches (one spec -> direct launch, or a graph kernel node)
 
@@ -610,6 +634,9 @@ template <class Real> static StencilFn stencil_fn_p(int R, int LD, int EP, int F
     if (LD == (ld) && EP == (ep) && FL == (fl)) {                                               \
         if (EL == EL_DENSE) return stencil_fn_t<2, ld, ep, fl, EL_DENSE, Real>();              \
         if (EL == EL_TETV) return stencil_fn_t<2, ld, ep, fl, EL_TETV, Real>();                \
+        if constexpr (sizeof(Real) == 8)                                                        \
+            if (EL == EL_Q1P)                                                                   \
+                return R >= 4 ? stencil_fn_t<4, ld, ep, fl, EL_Q1P, Real>() : stencil_fn_t<2, ld, ep, fl, EL_Q1P, Real>(); \
         return R >= 4 ? stencil_fn_t<4, ld, ep, fl, EL_Q1, Real>() : stencil_fn_t<2, ld, ep, fl, EL_Q1, Real>(); \
     }
     HF_STENCIL_VARIANTS(X)
@@ -640,6 +667,21 @@ static hf_status ensure_smem_attr(const void *fn, size_t smem, int device)
     if (it != g_attr_done.end() && it->second >= smem) return HF_OK;
     CUCK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     g_attr_done[key] = smem;
+    return HF_OK;
+}
+
+// resident CTAs per SM of this context's PCG kernel A (grid sizing of every stencil launch).
+// The material-id variant (EL_Q1P) uses fewer registers and could fit 3 CTAs per SM at R = 2,
+// but more, shorter z-chunks cost more than they hide (measured at C3: kernel A 18.5 vs 16.4 us),
+// so grids are sized by the pair kernel for both layouts.
+static hf_status update_occ(hf_ctx *c)
+{
+    const int el = kernel_elem(c);
+    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, el, c->es);
+    HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
+    int occ = 0;
+    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
+    c->occ = std::max(1, occ);
     return HF_OK;
 }
 
@@ -783,7 +825,13 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
                                 Launch *out)
 {
     const int FL = dir_flags(c, EP, a.bvec != nullptr, dset);
-    StencilFn f = stencil_fn(c->tileR, LD, EP, FL, kernel_elem(c), c->es);
+    int el = kernel_elem(c);
+    if (el == EL_Q1 && c->pal_on && std::memcmp(&maps.kc, &c->kid_map, sizeof(CUtensorMap)) == 0) {
+        el = EL_Q1P;                          // this map set streams material ids (sys0 of the context)
+        std::memcpy(a.pal, c->pal, sizeof(a.pal));
+        a.npal = c->npal;
+    }
+    StencilFn f = stencil_fn(c->tileR, LD, EP, FL, el, c->es);
     if (!f.fn) return fail(HF_E_ARG, "internal: no stencil instantiation");
     f.smem = std::max(f.smem, c->launch_min_smem);
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
@@ -854,7 +902,10 @@ static hf_status sys_maps(hf_ctx *c, Sys &s)
     for (int i = 0; i < 3; i++) HFCK(node_map(c, s.U[i], &s.maps.node[MAP_U0 + i]));
     for (int i = 0; i < 2; i++) HFCK(node_map(c, s.dbuf[i], &s.maps.node[MAP_D0 + i]));
     HFCK(node_map(c, s.s, &s.maps.node[MAP_S]));
-    HFCK(kc_map(c, s.kc, &s.maps.kc));
+    if (&s == &c->sys0 && c->pal_on && c->elem == EL_Q1 && c->es == 8) {
+        HFCK(kid_map_enc(c, c->kid, &c->kid_map));
+        s.maps.kc = c->kid_map;
+    } else HFCK(kc_map(c, s.kc, &s.maps.kc));
     if (s.kcn) HFCK(kcn_map(c, s.kcn, &s.maps.kcn));
     else s.maps.kcn = s.maps.kc;            // unused unless EL_TETV
     return HF_OK;
@@ -1001,6 +1052,7 @@ static void ctx_free(hf_ctx *c)
     cudaFree(c->flush);
     cudaFree(c->ab_A);
     cudaFree(c->ab_contrib);
+    cudaFree(c->kid);
     for (auto &kv : c->stacks) { ctx_free(kv.second); delete kv.second; }
     c->stacks.clear();
     delete c->comm;
@@ -1323,6 +1375,71 @@ hf_status hf_set_coefficients(hf_ctx *c, const double *k, const double *cc)
         c->sys0.key_valid = false;
         for (auto &p : c->pool) p->key_valid = false;
     }
+    if (c->pal_on) {                            // back to (k, c) pairs from material ids
+        c->pal_on = false;
+        HFCK(update_occ(c));
+        HFCK(sys_maps(c, c->sys0));
+        c->sys0.key_valid = false;
+    }
+    c->coef_set = true;
+    c->ab_ready = false;
+    return HF_OK;
+}
+
+hf_status hf_set_material_ids(hf_ctx *c, const uint8_t *ids, int32_t nmat, const double *k_mat, const double *c_mat)
+{
+    if (!c || !ids || !k_mat || !c_mat) return fail(HF_E_ARG, "hf_set_material_ids: NULL argument");
+    if (nmat < 1 || nmat > PAL_MAX - 1)
+        return fail(HF_E_ARG, "hf_set_material_ids: n_materials must be in [1, " + std::to_string(PAL_MAX - 1) + "]");
+    CUCK(cudaSetDevice(c->device));
+    const size_t ne = (size_t)(c->g.ne[0] * c->g.ne[1] * c->g.ne[2]);
+    const uint8_t *dids = ids;
+    if (!is_device_ptr(ids)) {
+        void *d;
+        HFCK(scratch_get(c, 57, ne, &d));
+        CUCK(cudaMemcpyAsync(d, ids, ne, cudaMemcpyHostToDevice, c->stream));
+        dids = (const uint8_t *)d;
+    }
+    const int nx = (int)c->g.ne[0];
+    const int kp = (nx + 15) & ~15;
+    const long long nkid = (long long)kp * c->g.ne[1] * (c->nzl + 1);
+    if (!c->kid || c->kid_pitch != kp) {
+        cudaFree(c->kid);
+        c->kid = nullptr;
+        CUCK(cudaMalloc(&c->kid, (size_t)nkid));
+        c->kid_pitch = kp;
+    }
+    PalTab pt;
+    std::memset(&pt, 0, sizeof(pt));
+    for (int m = 0; m < nmat; m++) { pt.kc[m][0] = k_mat[m]; pt.kc[m][1] = c_mat[m]; }
+    int *bad;
+    HFCK(scratch_get(c, 58, sizeof(int), (void **)&bad));
+    CUCK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+    const long long nkc = c->kc_elems;
+    if (c->es == 8)
+        k_pack_ids<double><<<(unsigned)((nkc + 255) / 256), 256, 0, c->stream>>>(make_geom(c), (int)c->g.ne[2], dids, nmat,
+                                                                                pt, c->sys0.kc, nkc, bad, c->launches);
+    else
+        k_pack_ids<float><<<(unsigned)((nkc + 255) / 256), 256, 0, c->stream>>>(make_geom(c), (int)c->g.ne[2], dids, nmat,
+                                                                               pt, c->sys0.kc, nkc, bad, c->launches);
+    CUCK(cudaGetLastError());
+    k_pack_kid<<<(unsigned)((nkid + 255) / 256), 256, 0, c->stream>>>(make_geom(c), (int)c->g.ne[2], dids, kp,
+                                                                      c->kid, nkid, c->launches);
+    CUCK(cudaGetLastError());
+    int hbad = 0;
+    CUCK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUCK(cudaStreamSynchronize(c->stream));
+    if (hbad) return fail(HF_E_INDEX, "hf_set_material_ids: a material id >= n_materials");
+    // material 0 of the table is the void outside the domain; ids are stored + 1
+    std::memset(c->pal, 0, sizeof(c->pal));
+    for (int m = 0; m < nmat; m++) { c->pal[m + 1][0] = k_mat[m]; c->pal[m + 1][1] = c_mat[m]; }
+    c->npal = nmat + 1;
+    c->pal_on = true;
+    HFCK(update_occ(c));
+    c->tetv = false;
+    HFCK(sys_maps(c, c->sys0));
+    c->sys0.key_valid = false;
+    for (auto &p : c->pool) p->key_valid = false;
     c->coef_set = true;
     c->ab_ready = false;
     return HF_OK;
@@ -2318,12 +2435,12 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
     // the dense (tet) element keeps R = 2 tiles (R = 4 spills); TMA boxes follow the tile height
     int want_r = default_tile_r(c, type);
     if (type != EL_DENSE && getenv("HF_TILE_R")) want_r = atoi(getenv("HF_TILE_R")) >= 4 ? 4 : 2;
+    CUCK(cudaStreamSynchronize(c->stream));
     if (want_r != c->tileR) {
-        CUCK(cudaStreamSynchronize(c->stream));
         c->tileR = want_r;
-        HFCK(sys_maps(c, c->sys0));
         for (auto &p : c->pool) HFCK(sys_maps(c, *p));
     }
+    HFCK(sys_maps(c, c->sys0));              // also selects the material-id map (Q1 only)
     if (type == EL_DENSE) {
         double K[64], M[64];
         tet_voxel(h, K, M);
@@ -2334,11 +2451,7 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
             c->dg.Md[l] = h[0] * h[1] * h[2] / 27.0;
         }
     }
-    StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
-    HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
-    int occ = 0;
-    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
-    c->occ = std::max(1, occ);
+    HFCK(update_occ(c));
     c->sys0.key_valid = false;
     for (auto &p : c->pool) p->key_valid = false;
     return HF_OK;

@@ -209,7 +209,8 @@ def c3(n_nodes_axis: int = 100, nsteps: int = 300, seed: int = 0) -> Problem:
     ids = inclusion_ids(g, seed=seed)
     k, c = ids_to_fields(ids)
     return Problem("c3", g, k, c, np.zeros(g.n_nodes), theta=0.5, dt=0.01, nsteps=nsteps,
-                   rtol=1e-12, flux_face=FACE_ZM, flux_const=1.0)
+                   rtol=1e-12, flux_face=FACE_ZM, flux_const=1.0,
+                   extra={"ids": ids.ravel().copy(), "materials": (STEEL, OXIDE)})
 
 
 def c4_grid(n_nodes_axis: int = 512) -> Grid:

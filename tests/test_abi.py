@@ -69,6 +69,7 @@ def test_product_never_uses_oracle():
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
                 assert "heat_oracle" not in src and "liboracle" not in src, f
                 assert not re.search(r"^\s*(import|from)\s+synth\b", src, re.M), f
+                assert not re.search(r"^\s*(import|from)\s+comparator\b", src, re.M), f
     # and the oracle never includes product code
     osrc = open(os.path.join(ROOT, "oracle", "heat_oracle.c")).read()
     includes = re.findall(r"^\s*#\s*include\s*[<\"]([^>\"]+)", osrc, re.M)

@@ -18,7 +18,11 @@ if mode == "sim":
     ctx = hf.hf_create(p.grid, 0)
     if os.environ.get("HF_PREC"):
         hf.hf_set_precision(ctx, int(os.environ["HF_PREC"]))
-    hf.hf_set_coefficients(ctx, torch.tensor(p.k, device=dev), torch.tensor(p.c, device=dev))
+    if os.environ.get("HF_IDS"):        # materials by id (stencil variant EL_Q1P)
+        hf.hf_set_material_ids(ctx, torch.tensor(p.extra["ids"], device=dev),
+                               [m[1] for m in p.extra["materials"]], [m[0] for m in p.extra["materials"]])
+    else:
+        hf.hf_set_coefficients(ctx, torch.tensor(p.k, device=dev), torch.tensor(p.c, device=dev))
     F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=dev)
     hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
     u = torch.zeros(p.grid.n_nodes, dtype=torch.float64, device=dev)
@@ -35,7 +39,11 @@ elif mode.startswith("apply"):
     ctx = hf.hf_create(g, 0)
     if os.environ.get("HF_PREC"):
         hf.hf_set_precision(ctx, int(os.environ["HF_PREC"]))
-    hf.hf_set_coefficients(ctx, k, c)
+    if os.environ.get("HF_IDS"):
+        ids = (torch.rand(g.n_elems, device=dev, generator=gen) < 0.2).to(torch.uint8)
+        hf.hf_set_material_ids(ctx, ids, [synth.STEEL[1], synth.OXIDE[1]], [synth.STEEL[0], synth.OXIDE[0]])
+    else:
+        hf.hf_set_coefficients(ctx, k, c)
     for _ in range(steps):
         hf.hf_apply(ctx, 0.005, 1.0, u, y)
     torch.cuda.synchronize()
