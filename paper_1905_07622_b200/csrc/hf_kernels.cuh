@@ -128,6 +128,10 @@ template <> struct Vec2<float> { using type = float2; };
 // stencil streams one uint8 id per element instead of a 16-B (k, c) pair and looks the
 // element's z-butterfly coefficients up in a per-CTA shared-memory table
 enum { EL_Q1 = 0, EL_DENSE = 1, EL_TETV = 2, EL_Q1P = 3 };
+#ifndef HF_PLANE_UNROLL
+#define HF_PLANE_UNROLL 1
+#endif
+constexpr int kPlaneUnroll = HF_PLANE_UNROLL;   // unroll of the stencil's z-plane loop
 constexpr int PAL_MAX = 64;        // material table entries; entry 0 = (0, 0) (outside the domain)
 constexpr int PAL_BW = 48;         // ids per TMA box row: 16-aligned origin <= X0-1, covers X0+30
 
@@ -231,8 +235,33 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
                  : "memory");
 }
 
+#ifndef HF_WAIT_MODE
+#define HF_WAIT_MODE 0
+#endif
+#ifndef HF_WAIT_HINT_NS
+#define HF_WAIT_HINT_NS 100
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
 {
+#if HF_WAIT_MODE == 1
+    // non-blocking probe in a spin loop (no suspension of the waiting warp)
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#elif HF_WAIT_MODE == 2
+    // potentially blocking probe with a short suspend-time hint (ns)
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(HF_WAIT_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
@@ -240,6 +269,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 #ifdef HF_DEBUG_WAIT
@@ -671,6 +701,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
         PK0[r].x = PK0[r].y = PK1[r].x = PK1[r].y = Real(0);
     }
 
+#pragma unroll kPlaneUnroll
     for (int it = 0; it < nplanes; ++it) {
         const int p = zb - 1 + it;
         const int st = it % NS;
