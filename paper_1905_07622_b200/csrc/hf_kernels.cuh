@@ -495,6 +495,20 @@ enum {
     FL_DSET = 8,   // EP_APPLY with FL_DIR: y_D = g (else y_D = u_D, identity rows)
 };
 
+#ifdef HF_TRACE
+// debug builds (-DHF_TRACE): %globaltimer stamps of thread 0 of every kernel-A block
+__device__ unsigned long long g_trace[4096][8];
+__device__ __forceinline__ unsigned long long gtime()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define HF_TR(k) do { if (EP == EP_CGA && tid == 0 && blk < 4096) g_trace[blk][k] = gtime(); } while (0)
+#else
+#define HF_TR(k) do { } while (0)
+#endif
+
 template <int R, int NW, int NS, int LD, int EP, int FL, int EL, class Real>
 __global__ void __launch_bounds__(32 * NW)
 k_stencil(const __grid_constant__ StencilArgs a)
@@ -526,6 +540,17 @@ k_stencil(const __grid_constant__ StencilArgs a)
     const int blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblocks = gridDim.x * gridDim.y * gridDim.z;
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
+    // warm the SM's descriptor cache for every map this launch may use (which node maps it
+    // uses depends on the state header, read next): one prefetch per lane of warp 0
+    if (w == 0 && lane < NMAPS + 2) prefetch_map(a.tm + lane);
+    HF_TR(0);
+#ifdef HF_TRACE
+    if (EP == EP_CGA && tid == 0 && blk < 4096) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_trace[blk][7] = sm;
+    }
+#endif
 
     // ---- state checks and per-launch resolution of buffers ---------------------------------
     double beta = 0.0;
@@ -566,6 +591,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
         }
     }
     if (LD == LD_X0 && first) map1 = map0;       // u^{-1} unused: keep the byte count fixed
+    HF_TR(1);
 
     extern __shared__ __align__(128) double smem_d[];
     Real *stage = reinterpret_cast<Real *>(smem_d);
@@ -624,6 +650,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     __syncthreads();
     if (tid == 0)
         for (int i = 0; i < NS && i < nplanes; i++) issue(i);
+    HF_TR(2);
     if constexpr (EL == EL_Q1P) {
         // the material table, built while the first TMA loads are in flight (entries in use only)
         for (int i = tid; i < a.npal * 4; i += NT) {
@@ -661,6 +688,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
             return;
         }
         beta = is.beta;
+        HF_TR(3);
 #ifdef HF_DEBUG_WAIT
         if (blk == 0 && tid == 0 && g_dbg) {
             volatile unsigned long long *d = g_dbg;
@@ -710,6 +738,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
 #else
         mbar_wait(&bars[st], (it / NS) & 1);
 #endif
+        if (it == 0) HF_TR(4);
         const Real *sb = stage + st * SH::STAGE_DBL;
         const Real *n0 = sb + w * R * SH::BW + lane + xoff;                 // row 0 of this warp
         const Real *n1 = sb + SH::NODE_DBL + w * R * SH::BW + lane + xoff;
@@ -973,8 +1002,10 @@ k_stencil(const __grid_constant__ StencilArgs a)
     }
 
     if (EP == EP_APPLY) return;
+    HF_TR(5);
     // per-block partial sums for the next kernel: A -> (d^T q); init, RESID -> (r^T s, r^T r, b^T b)
     block_reduce_store<NT>(acc, a.sy.pout, blk);
+    HF_TR(6);
     if (blk == 0 && tid == 0) {
         CgState *stw = a.sy.st;
         if (EP == EP_CGA) stw->npart_a = nblocks;

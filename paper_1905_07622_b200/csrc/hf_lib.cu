@@ -2420,6 +2420,16 @@ hf_status hf_time_kernel_a(hf_ctx *c, int32_t reps, double *ms_per_launch)
     return HF_OK;
 }
 
+#ifdef HF_TRACE
+// debug builds only (not part of the ABI): kernel-A timestamps of the last traced launch
+hf_status hf_trace_read(unsigned long long *out, int32_t nblocks)
+{
+    CUCK(cudaDeviceSynchronize());
+    CUCK(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 8 * (size_t)std::min(nblocks, 4096)));
+    return HF_OK;
+}
+#endif
+
 hf_status hf_set_driver(hf_ctx *c, int32_t driver)
 {
     if (!c || driver < 0 || driver > 1) return fail(HF_E_ARG, "hf_set_driver: bad argument");
