@@ -324,6 +324,12 @@ __device__ __forceinline__ void fence_mbar_init()
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// programmatic dependent launch (graph edges of type Programmatic, hf_ctx::pdl): wait for the
+// previous kernel's completion and memory; allow the next kernel's CTAs to start launching.
+// Both are no-ops for kernels launched without a programmatic dependency.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap *m)
 {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");
@@ -552,6 +558,18 @@ k_stencil(const __grid_constant__ StencilArgs a)
     }
 #endif
 
+    extern __shared__ __align__(128) double smem_d[];
+    Real *stage = reinterpret_cast<Real *>(smem_d);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + NS * SH::STAGE_DBL);
+    if constexpr (EP == EP_CGA) {
+        // independent of the previous kernel: may overlap its tail under a programmatic edge
+        if (tid == 0) {
+            for (int i = 0; i < NS; i++) mbar_init(&bars[i], 1);
+            fence_mbar_init();
+        }
+        pdl_wait();
+    }
+
     // ---- state checks and per-launch resolution of buffers ---------------------------------
     double beta = 0.0;
     int map0 = MAP_U0, map1 = MAP_U0 + 2, first = a.first;
@@ -593,9 +611,6 @@ k_stencil(const __grid_constant__ StencilArgs a)
     if (LD == LD_X0 && first) map1 = map0;       // u^{-1} unused: keep the byte count fixed
     HF_TR(1);
 
-    extern __shared__ __align__(128) double smem_d[];
-    Real *stage = reinterpret_cast<Real *>(smem_d);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + NS * SH::STAGE_DBL);
     Real(*seam)[NW][32] = reinterpret_cast<Real(*)[NW][32]>(stage + NS * SH::STAGE_DBL + (16 / ES) * NS);
     // EL_Q1P: per material the (a, b) coefficients of the fused z butterfly, as the pair path
     // computes them from (k, c) (bit-identical): palt[m] = {a0, b0, a1, b1, a2, b2, a3, b3}
@@ -639,8 +654,10 @@ k_stencil(const __grid_constant__ StencilArgs a)
 
     if (tid == 0) {
         if (smem_u32(stage) & 127u) __trap();     // TMA destinations need 128-B alignment
-        for (int i = 0; i < NS; i++) mbar_init(&bars[i], 1);
-        fence_mbar_init();
+        if (EP != EP_CGA) {                       // (kernel A initialised them before its wait)
+            for (int i = 0; i < NS; i++) mbar_init(&bars[i], 1);
+            fence_mbar_init();
+        }
         if (a.tm_fence) {
             if (NA >= 1) tensormap_acquire(a.tm + map0);
             if (NA >= 2) tensormap_acquire(a.tm + map1);
@@ -1002,6 +1019,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     }
 
     if (EP == EP_APPLY) return;
+    if (EP == EP_CGA) pdl_trigger();
     HF_TR(5);
     // per-block partial sums for the next kernel: A -> (d^T q); init, RESID -> (r^T s, r^T r, b^T b)
     block_reduce_store<NT>(acc, a.sy.pout, blk);
@@ -1044,6 +1062,7 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     const int tid = threadIdx.x;
     const int blk = blockIdx.x;
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
+    pdl_wait();
     CgState *st = a.sy.st;
     const CgHdr hd = load_hdr(st);
     if (hd.h0.x >= 0 || !hd.h0.y) {               // failed run / converged: leave the loop
@@ -1121,6 +1140,7 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
             }
         }
     }
+    pdl_trigger();
     if (!replace) block_reduce_store<NT>(acc, a.sy.pout, blk);
     if (blk == 0 && tid == 0) {
         st->b_iter = it + 1;

@@ -225,6 +225,7 @@ struct hf_ctx {
     int max_blocks = 0;
     int occ = 2;                     // resident CTAs/SM of the CG stencil (occupancy API)
     int unroll = 5;                  // PCG iterations per WHILE-body launch (5 divides the replacement period 50)
+    int pdl = 1;                     // programmatic A <-> B edges in the loop body (HF_PDL=0 disables)
     size_t launch_min_smem = 0;      // > 0: stencil launches reserve at least this much smem
     int rank = 0, nranks = 1;
     Comm *comm = nullptr;
@@ -894,6 +895,18 @@ static hf_status add_node(cudaGraph_t g, const Launch &L, cudaGraphNode_t *dep, 
     return HF_OK;
 }
 
+// edge from -> to of type Programmatic: `to` may launch once every CTA of `from` has called
+// griddepcontrol.launch_dependents (or exited); it waits for `from` with griddepcontrol.wait
+static hf_status add_pdl_edge(cudaGraph_t g, cudaGraphNode_t from, cudaGraphNode_t to)
+{
+    cudaGraphEdgeData e;
+    std::memset(&e, 0, sizeof(e));
+    e.from_port = cudaGraphKernelNodePortProgrammatic;
+    e.type = cudaGraphDependencyTypeProgrammatic;
+    CUCK(cudaGraphAddDependencies_v2(g, &from, &to, &e, 1));
+    return HF_OK;
+}
+
 // ============================================================================================
 // workspace
 
@@ -1018,6 +1031,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     if (const char *e = getenv("HF_ZCHUNK")) c->zchunk_env = std::max(0, atoi(e));
     if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e);
     if (const char *e = getenv("HF_UNROLL")) c->unroll = std::min(8, std::max(1, atoi(e)));
+    if (const char *e = getenv("HF_PDL")) c->pdl = atoi(e) != 0;
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
     // resident CTAs per SM of the CG stencil decide the z split of the grid
     StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
@@ -1270,8 +1284,11 @@ static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, in
 // root: [pre...] -> init -> WHILE(active){ A -> B -> IF(replace){ RESID } } -> [post]
 // (all stencil launches carry (Maps, StencilArgs); B carries BArgs)
 static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init, CgLaunches L, std::vector<Launch> post,
-                                int replace_every, cudaGraph_t *out)
+                                int replace_every, cudaGraph_t *out, bool pdl_ok = true)
 {
+    // programmatic edges only for the context's own system: batched pool systems run graphs on
+    // concurrent streams, where the TMA issue of DESIGN §8 was seen; they keep full serialisation
+    const bool pdl = c->pdl && pdl_ok;
     cudaGraph_t g;
     CUCK(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle hw, hi;
@@ -1297,6 +1314,7 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
     const int U = std::max(1, c->unroll);
     const bool if_first_only = replace_every > 0 && replace_every % U == 0;
     cudaGraphNode_t bprev = nullptr;
+    bool bprev_is_b = false;
     for (int u = 0; u < U; u++) {
         const bool with_if = replace_every > 0 && !(u > 0 && if_first_only);
         if (with_if) CUCK(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
@@ -1311,8 +1329,19 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
         ra.sy.h_while = hw; ra.sy.h_if = hi; ra.sy.use_handles = 1; ra.sy.use_if = with_if;
         RES.put(0, ra);
         cudaGraphNode_t na, nb;
-        HFCK(add_node(body, A, bprev ? &bprev : nullptr, &na));
-        HFCK(add_node(body, B, &na, &nb));
+        if (pdl) {
+            // A after B of the previous copy (when no IF node sits between them) and B after A
+            // through programmatic edges: the next kernel's launch and prologue overlap the tail
+            const bool prog_in = bprev && bprev_is_b;
+            HFCK(add_node(body, A, (bprev && !prog_in) ? &bprev : nullptr, &na));
+            if (prog_in) HFCK(add_pdl_edge(body, bprev, na));
+            HFCK(add_node(body, B, nullptr, &nb));
+            HFCK(add_pdl_edge(body, na, nb));
+        } else {
+            HFCK(add_node(body, A, bprev ? &bprev : nullptr, &na));
+            HFCK(add_node(body, B, &na, &nb));
+        }
+        bprev_is_b = true;
         if (!with_if) {                          // no replacement can occur in this copy
             bprev = nb;
             continue;
@@ -1327,6 +1356,7 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
         cudaGraphNode_t nr;
         HFCK(add_node(ip.conditional.phGraph_out[0], RES, nullptr, &nr));
         bprev = inode;
+        bprev_is_b = false;
     }
     prev = wnode;
     for (auto &p : post) { HFCK(add_node(g, p, &prev, &n)); prev = n; }
@@ -1813,7 +1843,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             if (s.gexec) { cudaGraphExecDestroy(s.gexec); s.gexec = nullptr; }
             if (s.graph) { cudaGraphDestroy(s.graph); s.graph = nullptr; }
             s.key_valid = false;
-            HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph));
+            HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph, &s == &c->sys0));
             CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
             s.key = key;
             s.key_valid = true;
