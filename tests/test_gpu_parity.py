@@ -591,3 +591,23 @@ def test_tet_simulate_matches_oracle(driver):
     uo, sto, it, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
     assert sto == 0 and st["steps_done"] == p.nsteps
     assert rel(N(u), uo) <= 1e-10
+
+
+def test_pdl_edges_do_not_change_results():
+    """The programmatic-launch edges of the PCG loop body (HF_PDL, default on) only let the next
+    kernel start early: the solution is bit-identical to fully serialised edges."""
+    p = synth.c1()
+    outs = []
+    for pdl in ("0", "1"):
+        os.environ["HF_PDL"] = pdl
+        try:
+            ctx = hf.hf_create(p.grid, 0)
+        finally:
+            os.environ.pop("HF_PDL", None)
+        hf.hf_set_coefficients(ctx, T(p.k), T(p.c))
+        F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+        hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
+        u = T(p.u0)
+        st = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, F, u, rtol=p.rtol)
+        outs.append((N(u), st["total_iters"]))
+    assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
