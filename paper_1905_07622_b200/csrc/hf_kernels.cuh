@@ -174,6 +174,16 @@ struct Maps {               // TMA descriptors (host copy; kernels read a device
 constexpr int MAP_KC = NMAPS;       // index of the kc map in a device Maps array
 constexpr int MAP_KCN = NMAPS + 1;  // index of the per-node pair map
 
+struct BArgs {
+    double *x;
+    const double *q, *invd;
+    double *dbuf[2];        // d = dbuf[(iter & 1) ^ 1] (written by kernel A of this iteration)
+    double *r, *s;
+    long long n, own0, own1;
+    double *rot[3];         // if rot[0]: x = rot[(step + 1) % 3]
+    Sync sy;
+};
+
 struct StencilArgs {
     Geom g;
     Lam lam;
@@ -199,6 +209,8 @@ struct StencilArgs {
     TetVF tvf;                    // EL_TETV, fp32 variant
     double pal[PAL_MAX][2];       // EL_Q1P: (k, c) of material id m (entry 0 = (0, 0))
     int npal;                     // EL_Q1P: table entries in use (materials + 1)
+    BArgs fb;                     // FL_FUSEB: kernel B's arguments
+    unsigned long long *gbar;     // FL_FUSEB: grid-barrier counter (monotonic)
 };
 // Node-vector pointers of StencilArgs / BArgs / StepArgs are declared double* but address
 // vectors of the context's storage type; kernels instantiated for Real = float reinterpret them.
@@ -361,7 +373,7 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NPART], double 
 // Grid-wide sums of the PREVIOUS kernel's per-block partials, computed redundantly by every
 // block in one fixed order (deterministic, no atomics, no fences: the kernel boundary orders
 // the producer's writes before these reads).  All threads return the same sums.
-template <int NT>
+template <int NT, bool CG = false>
 __device__ __forceinline__ void reduce_prev(const double *part, int n, double (&sums)[NPART])
 {
     __shared__ double redp[NT / 32][NPART];
@@ -382,8 +394,10 @@ __device__ __forceinline__ void reduce_prev(const double *part, int n, double (&
             const int b = b0 + k * NT;
             if (b < n) {
                 const double2 *q = reinterpret_cast<const double2 *>(part + (long long)b * NPART);
-                v[k][0] = __ldg(q);
-                v[k][1] = __ldg(q + 1);
+                // CG: partials written by other CTAs of the SAME kernel (fused A+B, after the
+                // grid barrier): through L2, never the non-coherent read-only path
+                v[k][0] = CG ? __ldcg(q) : __ldg(q);
+                v[k][1] = CG ? __ldcg(q + 1) : __ldg(q + 1);
             } else {
                 v[k][0] = make_double2(0.0, 0.0);
                 v[k][1] = make_double2(0.0, 0.0);
@@ -499,7 +513,142 @@ enum {
     FL_DIR = 2,    // Dirichlet rows in the epilogue (identity rows / r_D = 0 / set g)
     FL_HB = 4,     // EP_APPLY: y = c A u + s b (else y = c A u)
     FL_DSET = 8,   // EP_APPLY with FL_DIR: y_D = g (else y_D = u_D, identity rows)
+    FL_FUSEB = 16, // EP_CGA: kernel B's work follows in the same launch after a grid barrier
 };
+
+// ---- PCG kernel B: x += alpha d; r -= alpha q; s = P^{-1} r; r^T s, r^T r ---------------
+// (Alg. 1 lines 9, 13, 15, 16; the paper's knl_6, knl_7, knl_8, knl_9A-C, knl_10.)
+// x is updated on every local node (ghost planes included, so slab ghosts stay consistent);
+// r, s and the dot products only on owned nodes [own0, own1).  On a replacement iteration
+// (i > 0, i mod replace_every == 0, Alg. 1 line 10) only x is updated: the residual kernel
+// (EP_RESID) follows.  Also run inside kernel A's launch (FL_FUSEB) after a grid barrier.
+
+// Kernel B's work of iteration `it` on blocks blk of nblk: alpha = delta / d^T q (Alg. 1
+// line 8); x += alpha d; r -= alpha q; s = P^{-1} r; partials r^T s, r^T r (lines 9-16).
+// FUSED: d and q were written by other CTAs of the same launch before a grid barrier, so they
+// are read through L2 (ld.cg), never through the non-coherent read-only path.
+template <int NT, class Real, bool FUSED>
+__device__ __forceinline__ void cg_b_work(const BArgs &a, int blk, int nblk, int tid, int it, int re, int step,
+                                          double delta, double dq)
+{
+    CgState *st = a.sy.st;
+    if (!(dq > 0.0) || !isfinite(dq) || !isfinite(delta)) {           // breakdown
+        if (blk == 0 && tid == 0) {
+            st->status = ST_BREAKDOWN;
+            st->active = 0;
+            st->iter = it;
+            set_while(a.sy, 0);
+            set_if(a.sy, 0);
+        }
+        return;
+    }
+    const double alpha = delta / dq;
+    const Real alr = (Real)alpha;
+    using V2 = typename Vec2<Real>::type;
+    const Real *const qv_ = reinterpret_cast<const Real *>(a.q);
+    const Real *const iv_ = reinterpret_cast<const Real *>(a.invd);
+    Real *const rv_ = reinterpret_cast<Real *>(a.r);
+    Real *const sv_ = reinterpret_cast<Real *>(a.s);
+    const bool replace = it > 0 && re > 0 && (it % re) == 0;           // Alg. 1 line 10 (R6)
+    const Real *dvec = reinterpret_cast<const Real *>(a.dbuf[(it & 1) ^ 1]);
+    Real *xvec = reinterpret_cast<Real *>(a.rot[0] ? a.rot[(step + 1) % 3] : a.x);
+    double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
+    // BP aligned pairs per thread per sweep (n is even: even row pitch), loads issued up front;
+    // a pair never straddles the owned range (planes hold an even number of slots)
+    constexpr int BP = 2;
+    const long long sweep = (long long)nblk * NT * BP * 2;
+    for (long long base = ((long long)blk * NT * BP + tid) * 2; base < a.n; base += sweep) {
+        V2 xv[BP], dv[BP], rv[BP], qv[BP], iv[BP];
+        bool in[BP], own[BP];
+#pragma unroll
+        for (int k = 0; k < BP; k++) {
+            const long long i = base + (long long)k * NT * 2;
+            in[k] = i < a.n;
+            own[k] = in[k] && !replace && i >= a.own0 && i < a.own1;
+            if (in[k]) {
+                xv[k] = *reinterpret_cast<const V2 *>(xvec + i);
+                dv[k] = FUSED ? __ldcg(reinterpret_cast<const V2 *>(dvec + i)) : *reinterpret_cast<const V2 *>(dvec + i);
+            }
+            if (own[k]) {
+                rv[k] = *reinterpret_cast<const V2 *>(rv_ + i);
+                qv[k] = FUSED ? __ldcg(reinterpret_cast<const V2 *>(qv_ + i)) : __ldg(reinterpret_cast<const V2 *>(qv_ + i));
+                iv[k] = __ldg(reinterpret_cast<const V2 *>(iv_ + i));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < BP; k++) {
+            const long long i = base + (long long)k * NT * 2;
+            if (in[k]) {                        // x += alpha d  (line 9)
+                xv[k].x = fma(alr, dv[k].x, xv[k].x);
+                xv[k].y = fma(alr, dv[k].y, xv[k].y);
+                *reinterpret_cast<V2 *>(xvec + i) = xv[k];
+            }
+            if (own[k]) {                       // r -= alpha q; s = P^{-1} r (lines 13, 15)
+                rv[k].x = fma(-alr, qv[k].x, rv[k].x);
+                rv[k].y = fma(-alr, qv[k].y, rv[k].y);
+                V2 sv;
+                sv.x = rv[k].x * iv[k].x;
+                sv.y = rv[k].y * iv[k].y;
+                acc[0] = fma((double)rv[k].x, (double)sv.x, acc[0]);
+                acc[0] = fma((double)rv[k].y, (double)sv.y, acc[0]);
+                acc[1] = fma((double)rv[k].x, (double)rv[k].x, acc[1]);
+                acc[1] = fma((double)rv[k].y, (double)rv[k].y, acc[1]);
+                *reinterpret_cast<V2 *>(rv_ + i) = rv[k];
+                *reinterpret_cast<V2 *>(sv_ + i) = sv;
+            }
+        }
+    }
+    pdl_trigger();
+    if (!replace) block_reduce_store<NT>(acc, a.sy.pout, blk);
+    if (blk == 0 && tid == 0) {
+        st->b_iter = it + 1;
+        st->replace = replace;
+        st->alpha = alpha;
+        st->dq = dq;
+        if (!replace) st->npart_b = nblk;
+        set_if(a.sy, replace ? 1 : 0);
+    }
+}
+
+template <int NT, class Real>
+__global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
+{
+    const int tid = threadIdx.x;
+    const int blk = blockIdx.x;
+    if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
+    pdl_wait();
+    CgState *st = a.sy.st;
+    const CgHdr hd = load_hdr(st);
+    if (hd.h0.x >= 0 || !hd.h0.y) {               // failed run / converged: leave the loop
+        if (blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
+        return;
+    }
+    const int it = hd.h1.x, re = hd.h1.y, step = hd.h0.w;
+    // alpha_i = delta_i / (d_i^T q_i)  (Alg. 1 line 8) from kernel A's partials
+    double ps[NPART];
+    prev_sums<NT>(a.sy, hd.h2.x, ps);
+    cg_b_work<NT, Real, false>(a, blk, (int)gridDim.x, tid, it, re, step, st->delta[it & 1], ps[0]);
+}
+
+// Grid-wide barrier of a launch whose CTAs are all co-resident (checked on the host with the
+// occupancy API before a fused launch is used).  The counter only grows: a launch of nblk CTAs
+// waits for the next multiple of nblk.  A wait that does not complete traps (no silent hang).
+__device__ __forceinline__ void grid_barrier(unsigned long long *ctr, unsigned nblk, int tid)
+{
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned long long old = atomicAdd(ctr, 1ull);
+        const unsigned long long target = (old / nblk + 1) * nblk;
+        unsigned long long v;
+        long long spins = 0;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+            if (++spins > (1ll << 26)) __trap();
+        } while (v < target);
+    }
+    __syncthreads();
+}
 
 #ifdef HF_TRACE
 // debug builds (-DHF_TRACE): %globaltimer stamps of thread 0 of every kernel-A block
@@ -571,7 +720,8 @@ k_stencil(const __grid_constant__ StencilArgs a)
     }
 
     // ---- state checks and per-launch resolution of buffers ---------------------------------
-    double beta = 0.0;
+    double beta = 0.0, delta_i = 0.0;
+    int re_ = 0, step_ = 0;                                  // FL_FUSEB: header values for B
     int map0 = MAP_U0, map1 = MAP_U0 + 2, first = a.first;
     int it_i = 0;                                            // PCG iteration (kernel A)
     Real *cstore = reinterpret_cast<Real *>((EP == EP_CGA) ? a.dbuf[1] : a.xout);   // centre-value store target
@@ -580,6 +730,8 @@ k_stencil(const __grid_constant__ StencilArgs a)
         const CgHdr hd = load_hdr(a.sy.st);
         const int first_failed = hd.h0.x, active = hd.h0.y, b_iter = hd.h0.z, step = hd.h0.w;
         npart_b = hd.h1.w;
+        re_ = hd.h1.y;
+        step_ = hd.h0.w;
         if (first_failed >= 0) {                 // an earlier time step failed: stop the run
             if (EP == EP_CGA && blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
             return;
@@ -705,6 +857,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
             return;
         }
         beta = is.beta;
+        delta_i = is.delta;
         HF_TR(3);
 #ifdef HF_DEBUG_WAIT
         if (blk == 0 && tid == 0 && g_dbg) {
@@ -1037,120 +1190,17 @@ k_stencil(const __grid_constant__ StencilArgs a)
             stw->iter = 0;
         }
     }
-}
-
-// ---- PCG kernel B: x += alpha d; r -= alpha q; s = P^{-1} r; r^T s, r^T r ---------------
-// (Alg. 1 lines 9, 13, 15, 16; the paper's knl_6, knl_7, knl_8, knl_9A-C, knl_10.)
-// x is updated on every local node (ghost planes included, so slab ghosts stay consistent);
-// r, s and the dot products only on owned nodes [own0, own1).  On a replacement iteration
-// (i > 0, i mod replace_every == 0, Alg. 1 line 10) only x is updated: the residual kernel
-// (EP_RESID) follows.
-
-struct BArgs {
-    double *x;
-    const double *q, *invd;
-    double *dbuf[2];        // d = dbuf[(iter & 1) ^ 1] (written by kernel A of this iteration)
-    double *r, *s;
-    long long n, own0, own1;
-    double *rot[3];         // if rot[0]: x = rot[(step + 1) % 3]
-    Sync sy;
-};
-
-template <int NT, class Real>
-__global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
-{
-    const int tid = threadIdx.x;
-    const int blk = blockIdx.x;
-    if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
-    pdl_wait();
-    CgState *st = a.sy.st;
-    const CgHdr hd = load_hdr(st);
-    if (hd.h0.x >= 0 || !hd.h0.y) {               // failed run / converged: leave the loop
-        if (blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
-        return;
-    }
-    const int it = hd.h1.x, re = hd.h1.y, step = hd.h0.w;
-    // alpha_i = delta_i / (d_i^T q_i)  (Alg. 1 line 8) from kernel A's partials
-    double ps[NPART];
-    prev_sums<NT>(a.sy, hd.h2.x, ps);
-    const double dq = ps[0], delta = st->delta[it & 1];
-    if (!(dq > 0.0) || !isfinite(dq) || !isfinite(delta)) {           // breakdown
-        if (blk == 0 && tid == 0) {
-            st->status = ST_BREAKDOWN;
-            st->active = 0;
-            st->iter = it;
-            set_while(a.sy, 0);
-            set_if(a.sy, 0);
-        }
-        return;
-    }
-    const double alpha = delta / dq;
-    const Real alr = (Real)alpha;
-    using V2 = typename Vec2<Real>::type;
-    const Real *const qv_ = reinterpret_cast<const Real *>(a.q);
-    const Real *const iv_ = reinterpret_cast<const Real *>(a.invd);
-    Real *const rv_ = reinterpret_cast<Real *>(a.r);
-    Real *const sv_ = reinterpret_cast<Real *>(a.s);
-    const bool replace = it > 0 && re > 0 && (it % re) == 0;           // Alg. 1 line 10 (R6)
-    const Real *dvec = reinterpret_cast<const Real *>(a.dbuf[(it & 1) ^ 1]);
-    Real *xvec = reinterpret_cast<Real *>(a.rot[0] ? a.rot[(step + 1) % 3] : a.x);
-    double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
-    // BP aligned pairs per thread per sweep (n is even: even row pitch), loads issued up front;
-    // a pair never straddles the owned range (planes hold an even number of slots)
-    constexpr int BP = 2;
-    const long long sweep = (long long)gridDim.x * NT * BP * 2;
-    for (long long base = ((long long)blk * NT * BP + tid) * 2; base < a.n; base += sweep) {
-        V2 xv[BP], dv[BP], rv[BP], qv[BP], iv[BP];
-        bool in[BP], own[BP];
-#pragma unroll
-        for (int k = 0; k < BP; k++) {
-            const long long i = base + (long long)k * NT * 2;
-            in[k] = i < a.n;
-            own[k] = in[k] && !replace && i >= a.own0 && i < a.own1;
-            if (in[k]) {
-                xv[k] = *reinterpret_cast<const V2 *>(xvec + i);
-                dv[k] = *reinterpret_cast<const V2 *>(dvec + i);
-            }
-            if (own[k]) {
-                rv[k] = *reinterpret_cast<const V2 *>(rv_ + i);
-                qv[k] = __ldg(reinterpret_cast<const V2 *>(qv_ + i));
-                iv[k] = __ldg(reinterpret_cast<const V2 *>(iv_ + i));
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < BP; k++) {
-            const long long i = base + (long long)k * NT * 2;
-            if (in[k]) {                        // x += alpha d  (line 9)
-                xv[k].x = fma(alr, dv[k].x, xv[k].x);
-                xv[k].y = fma(alr, dv[k].y, xv[k].y);
-                *reinterpret_cast<V2 *>(xvec + i) = xv[k];
-            }
-            if (own[k]) {                       // r -= alpha q; s = P^{-1} r (lines 13, 15)
-                rv[k].x = fma(-alr, qv[k].x, rv[k].x);
-                rv[k].y = fma(-alr, qv[k].y, rv[k].y);
-                V2 sv;
-                sv.x = rv[k].x * iv[k].x;
-                sv.y = rv[k].y * iv[k].y;
-                acc[0] = fma((double)rv[k].x, (double)sv.x, acc[0]);
-                acc[0] = fma((double)rv[k].y, (double)sv.y, acc[0]);
-                acc[1] = fma((double)rv[k].x, (double)rv[k].x, acc[1]);
-                acc[1] = fma((double)rv[k].y, (double)rv[k].y, acc[1]);
-                *reinterpret_cast<V2 *>(rv_ + i) = rv[k];
-                *reinterpret_cast<V2 *>(sv_ + i) = sv;
-            }
-        }
-    }
-    pdl_trigger();
-    if (!replace) block_reduce_store<NT>(acc, a.sy.pout, blk);
-    if (blk == 0 && tid == 0) {
-        st->b_iter = it + 1;
-        st->replace = replace;
-        st->alpha = alpha;
-        st->dq = dq;
-        if (!replace) st->npart_b = gridDim.x;
-        set_if(a.sy, replace ? 1 : 0);
+    if constexpr (EP == EP_CGA && (FL & FL_FUSEB) != 0) {
+        // kernel B of the same iteration in the same launch: every CTA's q, d and d^T q partial
+        // are in L2 after the barrier; each block reduces them (same order as kernel B) and
+        // updates its contiguous share of the nodes
+        grid_barrier(a.gbar, (unsigned)nblocks, tid);
+        double ps[NPART];
+        reduce_prev<NT, true>(a.sy.pout, nblocks, ps);
+        cg_b_work<NT, Real, true>(a.fb, blk, nblocks, tid, it_i, re_, step_, delta_i, ps[0]);
     }
 }
+
 
 // Local sums of the last producer's partials (slab mode: before the cross-rank allreduce).
 // which = 0: kernel A's partials, 1: init / B / RESID partials.

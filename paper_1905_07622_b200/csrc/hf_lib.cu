@@ -171,6 +171,7 @@ struct Sys {                         // one system's PCG workspace (Table 3 buff
     CgState *st_host = nullptr;      // pinned mirror
     double *partA = nullptr, *partB = nullptr;   // per-block partial sums of A / (init, B, RESID)
     double *sums = nullptr;                      // slab mode: allreduced sums
+    unsigned long long *gbar = nullptr;          // grid-barrier counter of the fused A+B launch
 
     int *iters = nullptr;
     int iters_cap = 0;
@@ -226,6 +227,7 @@ struct hf_ctx {
     int occ = 2;                     // resident CTAs/SM of the CG stencil (occupancy API)
     int unroll = 5;                  // PCG iterations per WHILE-body launch (5 divides the replacement period 50)
     int pdl = 1;                     // programmatic A <-> B edges in the loop body (HF_PDL=0 disables)
+    int fuse_ab = 0;                 // A and B of an iteration in one launch (HF_FUSE_AB=1)
     size_t launch_min_smem = 0;      // > 0: stencil launches reserve at least this much smem
     int rank = 0, nranks = 1;
     Comm *comm = nullptr;
@@ -622,6 +624,8 @@ template <int R, int LD, int EP, int FL, int EL, class Real> static StencilFn st
     X(LD_GT, EP_APPLY, FL_HB | FL_DIR | FL_DSET)                                                \
     X(LD_CGD, EP_CGA, 0)                                                                        \
     X(LD_CGD, EP_CGA, FL_DIR)                                                                   \
+    X(LD_CGD, EP_CGA, FL_FUSEB)                                                                 \
+    X(LD_CGD, EP_CGA, FL_DIR | FL_FUSEB)                                                        \
     X(LD_X0, EP_RESID_INIT, 0)                                                                  \
     X(LD_X0, EP_RESID_INIT, FL_MASK | FL_DIR)                                                   \
     X(LD_RAW, EP_RESID_INIT, 0)                                                                 \
@@ -823,9 +827,9 @@ static hf_status maps_dev(hf_ctx *c, const Maps &m, const CUtensorMap **out)
 // stencil launch spec.  dset: EP_APPLY writes g on Dirichlet rows (RHS / lift); the plain
 // apply (hf_apply) is the unconstrained operator.
 static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps &maps, StencilArgs a, int cls,
-                                Launch *out)
+                                Launch *out, int extra_fl = 0)
 {
-    const int FL = dir_flags(c, EP, a.bvec != nullptr, dset);
+    const int FL = dir_flags(c, EP, a.bvec != nullptr, dset) | extra_fl;
     int el = kernel_elem(c);
     if (el == EL_Q1 && c->pal_on && std::memcmp(&maps.kc, &c->kid_map, sizeof(CUtensorMap)) == 0) {
         el = EL_Q1P;                          // this map set streams material ids (sys0 of the context)
@@ -939,6 +943,8 @@ static hf_status sys_alloc(hf_ctx *c, Sys &s, cudaStream_t stream)
     CUCK(cudaMalloc(&s.partA, (size_t)c->max_blocks * NPART * sizeof(double)));
     CUCK(cudaMalloc(&s.partB, (size_t)c->max_blocks * NPART * sizeof(double)));
     CUCK(cudaMalloc(&s.sums, NPART * sizeof(double)));
+    CUCK(cudaMalloc(&s.gbar, sizeof(unsigned long long)));
+    CUCK(cudaMemsetAsync(s.gbar, 0, sizeof(unsigned long long), stream));
     std::memset(s.st_host, 0, sizeof(CgState));
     s.st_host->first_failed = -1;
     CUCK(cudaMemcpyAsync(s.st, s.st_host, sizeof(CgState), cudaMemcpyHostToDevice, stream));
@@ -954,7 +960,7 @@ static void sys_free(Sys &s)
     cudaFree(s.b); cudaFree(s.r); cudaFree(s.s); cudaFree(s.q); cudaFree(s.invd);
     cudaFree(s.dbuf[0]); cudaFree(s.dbuf[1]);
     cudaFree(s.st); cudaFreeHost(s.st_host);
-    cudaFree(s.partA); cudaFree(s.partB); cudaFree(s.sums); cudaFree(s.iters);
+    cudaFree(s.partA); cudaFree(s.partB); cudaFree(s.sums); cudaFree(s.iters); cudaFree(s.gbar);
     cudaFree(s.kc);
     cudaFree(s.kcn);
     if (s.gexec) cudaGraphExecDestroy(s.gexec);
@@ -1032,6 +1038,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e);
     if (const char *e = getenv("HF_UNROLL")) c->unroll = std::min(8, std::max(1, atoi(e)));
     if (const char *e = getenv("HF_PDL")) c->pdl = atoi(e) != 0;
+    if (const char *e = getenv("HF_FUSE_AB")) c->fuse_ab = atoi(e) != 0;
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
     // resident CTAs per SM of the CG stencil decide the z split of the grid
     StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
@@ -1123,6 +1130,8 @@ static hf_status enqueue_set_dirichlet(hf_ctx *c, Sys &s, double *v, const doubl
 // PCG kernels of one iteration for system s, in order.
 struct CgLaunches {
     Launch A, B, RES;
+    Launch AB;                       // A and B in one launch with a grid barrier (FL_FUSEB)
+    bool has_ab = false;
 };
 
 // x: the iterate (NULL: the time-step ring slot U[(step+1)%3]); xmaps: maps with node[0] = x
@@ -1160,6 +1169,20 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
     L->B.block = dim3(256);
     L->B.add(b);
     L->B.cls = 1;
+    // the fused A+B launch for graph loop bodies of the context's own system (no slabs: their
+    // exchange and allreduce sit between A and B).  Its grid barrier needs every CTA resident
+    // at once: used only if the occupancy API says the whole grid fits.
+    L->has_ab = false;
+    if (c->fuse_ab && !c->comm && &s == &c->sys0) {
+        StencilArgs f = a;
+        f.fb = b;
+        f.gbar = s.gbar;
+        HFCK(stencil_launch(c, LD_CGD, EP_CGA, false, s.maps, f, 0, &L->AB, FL_FUSEB));
+        int occ = 0;
+        CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->AB.fn, 32 * NW, L->AB.smem));
+        const long long grid = (long long)L->AB.grid.x * L->AB.grid.y * L->AB.grid.z;
+        L->has_ab = (long long)occ * c->nsm >= grid;
+    }
     // residual replacement r = b - A x every replace_every iterations (Alg. 1 lines 10-11)
     StencilArgs rr = base_args(c, aK, aM);
     rr.invd = s.invd;
@@ -1322,6 +1345,14 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
         StencilArgs aa = A.get<StencilArgs>(0);
         aa.sy.h_while = hw; aa.sy.h_if = hi; aa.sy.use_handles = 1; aa.sy.use_if = with_if;
         A.put(0, aa);
+        const bool fused = pdl && L.has_ab;
+        Launch AB = L.AB;
+        if (fused) {
+            StencilArgs fa = AB.get<StencilArgs>(0);
+            fa.sy.h_while = hw; fa.sy.h_if = hi; fa.sy.use_handles = 1; fa.sy.use_if = with_if;
+            fa.fb.sy.h_while = hw; fa.fb.sy.h_if = hi; fa.fb.sy.use_handles = 1; fa.fb.sy.use_if = with_if;
+            AB.put(0, fa);
+        }
         BArgs bb = B.get<BArgs>(0);
         bb.sy.h_while = hw; bb.sy.h_if = hi; bb.sy.use_handles = 1; bb.sy.use_if = with_if;
         B.put(0, bb);
@@ -1329,7 +1360,13 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
         ra.sy.h_while = hw; ra.sy.h_if = hi; ra.sy.use_handles = 1; ra.sy.use_if = with_if;
         RES.put(0, ra);
         cudaGraphNode_t na, nb;
-        if (pdl) {
+        if (fused) {
+            // one launch per iteration: A, grid barrier, B (programmatic edge from the previous
+            // copy's launch when no IF node sits between them)
+            const bool prog_in = bprev && bprev_is_b;
+            HFCK(add_node(body, AB, (bprev && !prog_in) ? &bprev : nullptr, &nb));
+            if (prog_in) HFCK(add_pdl_edge(body, bprev, nb));
+        } else if (pdl) {
             // A after B of the previous copy (when no IF node sits between them) and B after A
             // through programmatic edges: the next kernel's launch and prologue overlap the tail
             const bool prog_in = bprev && bprev_is_b;
