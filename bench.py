@@ -139,6 +139,8 @@ def run_ours(args):
     if slab:
         # stdout carries exactly one JSON line: keep NCCL's version banner off it
         os.environ["NCCL_DEBUG"] = os.environ.get("HF_BENCH_NCCL_DEBUG", "WARN")
+        # NCCL prints its version banner at WARN level through its log file, stdout by default
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
