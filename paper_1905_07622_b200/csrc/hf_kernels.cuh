@@ -555,7 +555,10 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, int blk, int nblk, int
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
     // BP aligned pairs per thread per sweep (n is even: even row pitch), loads issued up front;
     // a pair never straddles the owned range (planes hold an even number of slots)
-    constexpr int BP = 2;
+#ifndef HF_B_BP
+#define HF_B_BP 2
+#endif
+    constexpr int BP = HF_B_BP;
     const long long sweep = (long long)nblk * NT * BP * 2;
     for (long long base = ((long long)blk * NT * BP + tid) * 2; base < a.n; base += sweep) {
         V2 xv[BP], dv[BP], rv[BP], qv[BP], iv[BP];

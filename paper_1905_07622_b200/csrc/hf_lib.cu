@@ -858,7 +858,14 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
     return HF_OK;
 }
 
-static int b_blocks(const hf_ctx *c) { return std::max(1, std::min((int)((c->nloc + 1023) / 1024), c->nsm * 4)); }
+// Kernel B's grid: 3 CTAs per SM.  Every CTA first reduces kernel A's partials (~9 KB of L2
+// reads each); fewer CTAs doing more sweeps measured best at C3 (per-iteration 25.3 / 24.3 / 24.7 /
+// 25.9 / 27.2 us for 4 / 3 / 2 / 6 / 8 per SM; 4 pairs per thread per sweep instead of 2: no gain).
+static int b_blocks(const hf_ctx *c)
+{
+    static const int per_sm = getenv("HF_B_PER_SM") ? std::max(1, atoi(getenv("HF_B_PER_SM"))) : 3;
+    return std::max(1, std::min((int)((c->nloc + 1023) / 1024), c->nsm * per_sm));
+}
 
 static hf_status run(hf_ctx *c, const Launch &L, cudaStream_t s)
 {
