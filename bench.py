@@ -306,6 +306,15 @@ def run_ours(args):
             "config": workload_config(p, world, {"pcg_iters_per_step": iters / args.steps,
                                                  "us_per_pcg_iter": total_ms / max(iters, 1) * 1e3}),
             "e2e": e2e,
+            # the whole PCG iteration against the same peak: kernel A (48 B/node + coefficients)
+            # + kernel B (64 B/node) algorithmic bytes / the measured time per iteration
+            "pcg_iteration_roofline": {
+                "bytes_per_iter": a_bytes + 64.0 * nodes_local,
+                "us_per_iter": total_ms / max(iters, 1) * 1e3,
+                "achieved_GBps": (a_bytes + 64.0 * nodes_local) / (total_ms / max(iters, 1) * 1e-3) / 1e9,
+                "frac": (a_bytes + 64.0 * nodes_local) / (total_ms / max(iters, 1) * 1e-3) / 1e9 / peak,
+                "note": "time per iteration includes the per-step kernels (RHS, init, step end) spread "
+                        "over the step's iterations"},
             "gpu_launches": int(launches),
             "clocks": clk,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
