@@ -207,3 +207,32 @@ def test_ids_c3_two_steps():
     o, Fo = oracle.problem_oracle(p)
     uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
     assert rel(res[0], uo) <= 1e-10
+
+
+@pytest.mark.slow
+def test_ids_c4_apply_sampled_rows():
+    """The 512^3 apply through material ids in the launch configuration bench.py times
+    (apply_512_ids: two materials, 20 % oxide, R = 4 tiles) on sampled rows, boundary classes
+    and tile seams included, against the oracle's per-row evaluation."""
+    g = synth.c4_grid()
+    rng = np.random.default_rng(97)
+    ids = (rng.random(g.n_elems) < 0.2).astype(np.uint8)
+    km = np.array([synth.STEEL[1], synth.OXIDE[1]])
+    cm = np.array([synth.STEEL[0], synth.OXIDE[0]])
+    u = synth.random_vector(g.n_nodes, 98)
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_material_ids(ctx, ids, km, cm)
+    y = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_apply(ctx, 0.005, 1.0, T(u), y)
+    yg = N(y)
+    del ctx
+    torch.cuda.empty_cache()
+    o = oracle.Oracle(g, km[ids], cm[ids], assemble=False)
+    nx, ny, nz = g.nn
+    rows = rng.integers(0, g.n_nodes, 4096)
+    extra = [i + nx * (j + ny * kk) for (i, j, kk) in
+             [(0, 0, 0), (nx - 1, ny - 1, nz - 1), (30, 30, 7), (31, 31, 8), (32, 62, 9), (61, 93, 500),
+              (nx - 1, 0, 3), (0, ny - 1, nz - 1)]]
+    rows = np.concatenate([rows, np.array(extra)])
+    yo = o.apply_rows(0.005, 1.0, u, rows)
+    assert maxerr(yg[rows], yo) <= 1e-12
