@@ -225,7 +225,7 @@ struct hf_ctx {
     int check_every = 8;
     int max_blocks = 0;
     int occ = 2;                     // resident CTAs/SM of the CG stencil (occupancy API)
-    int unroll = 5;                  // PCG iterations per WHILE-body launch (5 divides the replacement period 50)
+    int unroll = 0;                  // PCG iterations per WHILE-body launch (0: by grid size, see build_cg_graph)
     int pdl = 1;                     // programmatic A <-> B edges in the loop body (HF_PDL=0 disables)
     int fuse_ab = 0;                 // A and B of an iteration in one launch (HF_FUSE_AB=1)
     size_t launch_min_smem = 0;      // > 0: stencil launches reserve at least this much smem
@@ -1043,7 +1043,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     if (const char *e = getenv("HF_TILE_R")) c->tileR = atoi(e) >= 4 ? 4 : 2;
     if (const char *e = getenv("HF_ZCHUNK")) c->zchunk_env = std::max(0, atoi(e));
     if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e);
-    if (const char *e = getenv("HF_UNROLL")) c->unroll = std::min(8, std::max(1, atoi(e)));
+    if (const char *e = getenv("HF_UNROLL")) c->unroll = std::min(50, std::max(1, atoi(e)));
     if (const char *e = getenv("HF_PDL")) c->pdl = atoi(e) != 0;
     if (const char *e = getenv("HF_FUSE_AB")) c->fuse_ab = atoi(e) != 0;
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
@@ -1341,7 +1341,14 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
     // Every body starts at an iteration that is a multiple of `unroll`, so when unroll divides the
     // replacement period only the first copy can meet a replacement iteration: the others get no
     // IF node (an IF node costs about a microsecond per evaluation).
-    const int U = std::max(1, c->unroll);
+    // Copies per body: with programmatic edges a long chain of copies keeps the GPU fed (C3:
+    // 25.0 / 23.9 / 23.4 / 23.5 us per iteration for 5 / 10 / 25 / 50), but copies after
+    // convergence still launch, which small grids (short iterations, few per step) feel more:
+    // 25 from 0.5M nodes, else 5.  Reduced to a divisor of the replacement period so that only
+    // the first copy needs an IF node.
+    int U = c->unroll > 0 ? c->unroll : (c->nloc >= 500000 ? 25 : 5);
+    if (replace_every > 0)
+        while (U > 1 && replace_every % U != 0) U--;
     const bool if_first_only = replace_every > 0 && replace_every % U == 0;
     cudaGraphNode_t bprev = nullptr;
     bool bprev_is_b = false;
