@@ -172,6 +172,8 @@ struct Sys {                         // one system's PCG workspace (Table 3 buff
     double *partA = nullptr, *partB = nullptr;   // per-block partial sums of A / (init, B, RESID)
     double *sums = nullptr;                      // slab mode: allreduced sums
     unsigned long long *gbar = nullptr;          // grid-barrier counter of the fused A+B launch
+    CgState *st_ring = nullptr;                  // pinned state copies of the pipelined host loop
+    cudaEvent_t ev_ring[2] = {nullptr, nullptr};
 
     int *iters = nullptr;
     int iters_cap = 0;
@@ -968,6 +970,8 @@ static void sys_free(Sys &s)
     cudaFree(s.dbuf[0]); cudaFree(s.dbuf[1]);
     cudaFree(s.st); cudaFreeHost(s.st_host);
     cudaFree(s.partA); cudaFree(s.partB); cudaFree(s.sums); cudaFree(s.iters); cudaFree(s.gbar);
+    if (s.st_ring) cudaFreeHost(s.st_ring);
+    for (int i = 0; i < 2; i++) if (s.ev_ring[i]) cudaEventDestroy(s.ev_ring[i]);
     cudaFree(s.kc);
     cudaFree(s.kcn);
     if (s.gexec) cudaGraphExecDestroy(s.gexec);
@@ -1285,12 +1289,65 @@ static std::vector<Launch> step_launches(hf_ctx *c, const StepArgs &a, bool comm
 }
 
 // ---- host-loop PCG (profiling, slab transports) ------------------------------------------
+// one PCG iteration on the host-loop driver (slab transports exchange / allreduce in between)
+static hf_status host_cg_iter(hf_ctx *c, Sys &s, CgLaunches &L, int i, int replace_every)
+{
+    HFCK(run(c, L.A, s.stream));
+    HFCK(comm_after(c, s, 0, false));
+    const bool rep = i > 0 && replace_every > 0 && i % replace_every == 0;
+    HFCK(run(c, L.B, s.stream));
+    if (!rep) HFCK(comm_after(c, s, 1, true));
+    if (rep) {
+        HFCK(run(c, L.RES, s.stream));
+        HFCK(comm_after(c, s, 1, true));
+    }
+    return HF_OK;
+}
+
+// Host loop without a stall per check: after every batch of `check` iterations the state is
+// copied to pinned memory with an event behind it, and batch k + 1 is enqueued before batch
+// k - 1's copy is waited on, so the stream always holds queued work.  Iterations enqueued after
+// convergence exit at their first instruction (the kernels test `active`); every rank of a slab
+// run enqueues the same sequence (the stop decision comes from allreduced sums).
+static hf_status host_cg_loop_pipelined(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, int replace_every,
+                                        int check)
+{
+    if (!s.st_ring) {
+        CUCK(cudaMallocHost(&s.st_ring, 2 * sizeof(CgState)));
+        CUCK(cudaEventCreateWithFlags(&s.ev_ring[0], cudaEventDisableTiming));
+        CUCK(cudaEventCreateWithFlags(&s.ev_ring[1], cudaEventDisableTiming));
+    }
+    int i = 0, batch = 0;
+    bool pending[2] = {false, false};
+    for (;;) {
+        const int slot = batch & 1;
+        // the device ends the solve itself (kernel A of iteration max_iter records NOCONV), so
+        // batches are enqueued until a copied state says inactive; the bound is a safety net
+        for (int k = 0; k < check; k++, i++) HFCK(host_cg_iter(c, s, L, i, replace_every));
+        CUCK(cudaMemcpyAsync(&s.st_ring[slot], s.st, sizeof(CgState), cudaMemcpyDeviceToHost, s.stream));
+        CUCK(cudaEventRecord(s.ev_ring[slot], s.stream));
+        pending[slot] = true;
+        const int prev = slot ^ 1;
+        if (i > max_iter + 2 * check + 2) break;
+        if (pending[prev]) {                      // the batch before this one
+            CUCK(cudaEventSynchronize(s.ev_ring[prev]));
+            pending[prev] = false;
+            if (!s.st_ring[prev].active) break;
+        }
+        batch++;
+    }
+    CUCK(cudaStreamSynchronize(s.stream));
+    *s.st_host = s.st_ring[batch & 1];
+    return HF_OK;
+}
+
 static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, int replace_every)
 {
     HFCK(read_state(c, s));
     if (!s.st_host->active) return HF_OK;
     const bool slab = c->comm != nullptr;
     const int check = slab && !c->comm->graph_capturable() ? 1 : c->check_every;
+    if (check > 1) return host_cg_loop_pipelined(c, s, L, max_iter, replace_every, check);
     for (int i = 0;;) {
         HFCK(run(c, L.A, s.stream));
         HFCK(comm_after(c, s, 0, false));
