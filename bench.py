@@ -342,6 +342,7 @@ def run_ours(args):
         line["c3_other_coef"] = variant_c3(hf, torch, dev, 64, p.rtol, coef="pairs" if use_ids else "ids")
         line["apply_512"] = apply_512(hf, torch, dev, peak)
         line["apply_512_ids"] = apply_512(hf, torch, dev, peak, ids=True)
+        line["c4_steps"] = c4_steps(hf, torch, dev, peak)
         line["c5_batched"] = c5_batched(hf, torch, dev, world)
         # the paper's settings for the inverse problem: rtol 1e-6, single precision
         line["c5_batched_fp32_rtol1e-6"] = c5_batched(hf, torch, dev, world, prec=32, rtol=1e-6)
@@ -499,6 +500,43 @@ def fp32_variant(hf, torch, dev, peak):
             "c3_fp64_rtol1e-6": variant_c3(hf, torch, dev, 64, 1e-6),
             "apply_512_fp32": apply_512(hf, torch, dev, peak, 32),
             "parity": "fp32 vs the fp64 oracle: rel-L2 1.9e-7 after 2 C3 steps at rtol 1e-6 (bar 1e-5)"}
+
+
+def c4_steps(hf, torch, dev, peak, steps=2):
+    """C4 (BASELINE configs[3] grid, 512^3 nodes = 134M DoF) time steps on one GPU: two
+    materials (steel / Fe2O3, 20 % oxide, i.i.d. per element, generated on the device), f = 1 on
+    z = 0, CN, dt = 0.01, rtol 1e-12, after one warm-up step.  Every iteration streams ~15 GB, far
+    beyond L2.  Reports ms/step, ms/iteration and the iteration's algorithmic GB/s."""
+    g = synth.c4_grid(512)
+    gen = torch.Generator(device=dev).manual_seed(3)
+    ox = torch.rand(g.n_elems, device=dev, generator=gen) < 0.2
+    k = torch.where(ox, synth.OXIDE[1], synth.STEEL[1]).to(torch.float64)
+    c = torch.where(ox, synth.OXIDE[0], synth.STEEL[0]).to(torch.float64)
+    del ox
+    ctx = hf.hf_create(g, dev.index)
+    hf.hf_set_coefficients(ctx, k, c)
+    del k, c
+    torch.cuda.empty_cache()
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=dev)
+    hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+    u = torch.zeros(g.n_nodes, dtype=torch.float64, device=dev)
+    up = torch.zeros_like(u)
+    hf.hf_simulate_resume(ctx, 0.5, 0.01, 1, F, u, up, 0, rtol=1e-12)
+    s = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    st = hf.hf_simulate_resume(ctx, 0.5, 0.01, steps, F, u, up, 1, rtol=1e-12)
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    it = max(st["total_iters"], 1)
+    byts = 112.0 * g.n_nodes + 16.0 * g.n_elems          # kernel A 48 B/node + (k, c); kernel B 64 B/node
+    del ctx, F, u, up
+    torch.cuda.empty_cache()
+    return {"nodes": g.n_nodes, "steps": steps, "ms_per_step": ms / steps, "pcg_iters_per_step": it / steps,
+            "ms_per_iter": ms / it, "iteration_GBps": byts / (ms / it * 1e-3) / 1e9,
+            "frac": byts / (ms / it * 1e-3) / 1e9 / peak, "rtol": 1e-12,
+            "fields": "two materials, 20 % oxide i.i.d. per element (device RNG, seed 3)"}
 
 
 def c5_batched(hf, torch, dev, world, nsims=8, nsteps=300, prec=64, rtol=None):

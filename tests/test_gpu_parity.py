@@ -611,3 +611,37 @@ def test_pdl_edges_do_not_change_results():
         st = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, F, u, rtol=p.rtol)
         outs.append((N(u), st["total_iters"]))
     assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
+
+
+@pytest.mark.slow
+def test_c4_time_step_properties():
+    """C4 (512^3 nodes, 134M DoF) in the configuration bench.py's c4_steps times: one backward-
+    free CN step from u0 = 0 must leave a true residual ||dt F - A u1|| <= 1e-10 ||dt F|| (the
+    solve met rtol 1e-12 on the recurrence residual; Alg. 1 replaces it every 50 iterations), and
+    the stiffness part must carry no heat: sum(A u1) = sum(M u1) (K 1 = 0, K symmetric)."""
+    g = synth.c4_grid()
+    gen = torch.Generator(device=DEV).manual_seed(3)
+    ox = torch.rand(g.n_elems, device=DEV, generator=gen) < 0.2
+    k = torch.where(ox, synth.OXIDE[1], synth.STEEL[1]).to(torch.float64)
+    c = torch.where(ox, synth.OXIDE[0], synth.STEEL[0]).to(torch.float64)
+    del ox
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_coefficients(ctx, k, c)
+    del k, c
+    torch.cuda.empty_cache()
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+    u = torch.zeros(g.n_nodes, dtype=torch.float64, device=DEV)
+    theta, dt = 0.5, 0.01
+    st = hf.hf_simulate(ctx, theta, dt, 1, F, u, rtol=1e-12)
+    assert st["total_iters"] > 0
+    y = torch.empty_like(u)
+    hf.hf_apply_axpby(ctx, theta * dt, 1.0, -1.0, u, F * dt, y)         # r = dt F - A u1
+    rel_res = float(torch.linalg.norm(y) / torch.linalg.norm(F * dt))
+    assert rel_res <= 1e-10, rel_res
+    hf.hf_apply(ctx, theta * dt, 1.0, u, y)
+    sa = float(y.sum())
+    hf.hf_apply(ctx, 0.0, 1.0, u, y)
+    sm = float(y.sum())
+    assert abs(sa - sm) <= 1e-9 * abs(sm), (sa, sm)
+    assert abs(sm - dt * float(F.sum())) <= 1e-9 * abs(sm)
