@@ -336,8 +336,10 @@ def run_ours(args):
         # the metric's second half at N GPUs: the 512^3 operator apply on N z-slabs (BASELINE
         # configs[3]), each rank its slab + ghosts, time = max over ranks
         a512 = apply_512_slabs(hf, torch, dev, peak, rank, world, dist)
+        c4s = c4_steps(hf, torch, dev, peak, rank=rank, world=world, dist=dist)
         if rank == 0:
             line["apply_512_slabs"] = a512
+            line["c4_steps_slabs"] = c4s
     if not slab:
         line["c3_other_coef"] = variant_c3(hf, torch, dev, 64, p.rtol, coef="pairs" if use_ids else "ids")
         line["apply_512"] = apply_512(hf, torch, dev, peak)
@@ -502,40 +504,56 @@ def fp32_variant(hf, torch, dev, peak):
             "parity": "fp32 vs the fp64 oracle: rel-L2 1.9e-7 after 2 C3 steps at rtol 1e-6 (bar 1e-5)"}
 
 
-def c4_steps(hf, torch, dev, peak, steps=2):
-    """C4 (BASELINE configs[3] grid, 512^3 nodes = 134M DoF) time steps on one GPU: two
-    materials (steel / Fe2O3, 20 % oxide, i.i.d. per element, generated on the device), f = 1 on
-    z = 0, CN, dt = 0.01, rtol 1e-12, after one warm-up step.  Every iteration streams ~15 GB, far
-    beyond L2.  Reports ms/step, ms/iteration and the iteration's algorithmic GB/s."""
+def c4_steps(hf, torch, dev, peak, steps=2, rank=0, world=1, dist=None):
+    """C4 (BASELINE configs[3] grid, 512^3 nodes = 134M DoF) time steps: two materials (steel /
+    Fe2O3, 20 % oxide, i.i.d. per element, generated on the device), f = 1 on z = 0, CN,
+    dt = 0.01, rtol 1e-12, after one warm-up step.  Every iteration streams ~17 GB, far beyond
+    L2.  With dist (N ranks): the same problem on N z-slabs (NCCL ghost planes + allreduce, strong
+    scaling of configs[3]), time = max over ranks.  Reports ms/step, ms/iteration and the
+    iteration's aggregate algorithmic GB/s."""
     g = synth.c4_grid(512)
     gen = torch.Generator(device=dev).manual_seed(3)
     ox = torch.rand(g.n_elems, device=dev, generator=gen) < 0.2
     k = torch.where(ox, synth.OXIDE[1], synth.STEEL[1]).to(torch.float64)
     c = torch.where(ox, synth.OXIDE[0], synth.STEEL[0]).to(torch.float64)
     del ox
-    ctx = hf.hf_create(g, dev.index)
+    if dist is None:
+        ctx = hf.hf_create(g, dev.index)
+    else:
+        uid = hf.hf_nccl_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = hf.hf_create_slab(g, rank, world, obj[0], transport=0, device=dev.index)
     hf.hf_set_coefficients(ctx, k, c)
     del k, c
     torch.cuda.empty_cache()
-    F = torch.empty(g.n_nodes, dtype=torch.float64, device=dev)
+    F = torch.empty(ctx.n_nodes, dtype=torch.float64, device=dev)
     hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
-    u = torch.zeros(g.n_nodes, dtype=torch.float64, device=dev)
+    u = torch.zeros(ctx.n_nodes, dtype=torch.float64, device=dev)
     up = torch.zeros_like(u)
     hf.hf_simulate_resume(ctx, 0.5, 0.01, 1, F, u, up, 0, rtol=1e-12)
     s = torch.cuda.current_stream(dev)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     st = hf.hf_simulate_resume(ctx, 0.5, 0.01, steps, F, u, up, 1, rtol=1e-12)
     e1.record(s)
     e1.synchronize()
     ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     it = max(st["total_iters"], 1)
     byts = 112.0 * g.n_nodes + 16.0 * g.n_elems          # kernel A 48 B/node + (k, c); kernel B 64 B/node
     del ctx, F, u, up
     torch.cuda.empty_cache()
-    return {"nodes": g.n_nodes, "steps": steps, "ms_per_step": ms / steps, "pcg_iters_per_step": it / steps,
-            "ms_per_iter": ms / it, "iteration_GBps": byts / (ms / it * 1e-3) / 1e9,
-            "frac": byts / (ms / it * 1e-3) / 1e9 / peak, "rtol": 1e-12,
+    return {"nodes": g.n_nodes, "ranks": world, "steps": steps, "ms_per_step": ms / steps,
+            "pcg_iters_per_step": it / steps, "ms_per_iter": ms / it,
+            "iteration_GBps": byts / (ms / it * 1e-3) / 1e9,
+            "frac_per_gpu": byts / (ms / it * 1e-3) / 1e9 / peak / world, "rtol": 1e-12,
             "fields": "two materials, 20 % oxide i.i.d. per element (device RNG, seed 3)"}
 
 
