@@ -631,7 +631,7 @@ def run_reference(args):
     sample = (f"{steps} of the K={args.steps} requested C3 time steps (capped at 20 to bound the run), after "
               f"{warm} warm-up step and CSR assembly ({t_setup:.1f} s, excluded); plain C oracle, 1 thread")
     return {"impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": steps,
-            "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded inclusion field, synth.c3)",
             "config": workload_config(p, 1, {"pcg_iters_per_step": iters / steps}),
             "cpu_baseline": {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
