@@ -2,7 +2,8 @@
 
 TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
 cpu_baseline / ``--impl reference`` legs may import this module.  The product
-package ``paper_1905_07622_b200`` never imports it (tests/test_layout.py checks).
+package ``paper_1905_07622_b200`` never imports it (tests/test_abi.py::test_product_never_uses_oracle
+checks).
 
 Every function follows the passage of PAPER.md cited in heat_oracle.c.  This file
 only marshals numpy arrays; all arithmetic is in the C file.
@@ -24,9 +25,9 @@ OR_OK, OR_E_ARG, OR_E_NOCONV, OR_E_BREAKDOWN, OR_E_OOM = 0, -1, -3, -4, -8
 
 
 def build(force: bool = False) -> str:
-    """Compile heat_oracle.c into oracle/liboracle.so (plain -O2, no FMA contraction)."""
+    """Compile heat_oracle.c into oracle/liboracle.so (plain -O2, no FMA contraction, OpenMP)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-std=c99", "-D_GNU_SOURCE", "-ffp-contract=off", "-fPIC", "-shared",
+        cmd = ["gcc", "-O2", "-std=c99", "-D_GNU_SOURCE", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
                "-o", _LIB, _SRC, "-lm"]
         subprocess.run(cmd, check=True)
     return _LIB
@@ -64,10 +65,17 @@ def lib():
         L.or_pcg.argtypes = [C.c_void_p, C.c_double, C.c_double, _dp, _dp, C.c_double, C.c_int,
                              C.c_int, _dp]
         L.or_rhs.argtypes = [C.c_void_p, C.c_double, C.c_double, _dp, _dp, _dp]
+        L.or_num_threads.restype = C.c_int
+        L.or_num_threads.argtypes = []
         L.or_simulate.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int, _dp, _dp, C.c_double,
                                   C.c_int, C.c_int, _i32p, C.c_int64, C.c_void_p]
         _lib = L
     return _lib
+
+
+def num_threads() -> int:
+    """OpenMP threads the oracle runs on (OMP_NUM_THREADS, default all host cores)."""
+    return int(lib().or_num_threads())
 
 
 def element_matrices(h: Sequence[float]):

@@ -20,9 +20,15 @@
  *   - PCG exactly in the order of Algorithm 1 with readings R4-R6, R10.
  *   - theta-scheme time loop  [M + theta dt K] U^i = [M - (1-theta) dt K] U^{i-1} + dt F
  *      with the extrapolated guess of u0_update (reading R9).
- * All arithmetic is fp64 with sequential (left-to-right) sums.  Single-threaded.
+ * All arithmetic is fp64.  Parallel with OpenMP (static schedules) in a way that leaves every
+ * result independent of the thread count: a row sum (SpMV, diagonal) is one thread's sequential
+ * left-to-right sum; a dot product is a sum of fixed 4096-node chunks (each chunk summed left to
+ * right, the chunk sums added left to right in chunk order: reading R15); pointwise
+ * vector updates are per-node.  Element scatter-add assembly stays sequential.
+ * or_num_threads() reports the OpenMP thread count (OMP_NUM_THREADS, default all host cores).
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -32,6 +38,10 @@
 #define OR_E_NOCONV (-3)
 #define OR_E_BREAKDOWN (-4)
 #define OR_E_OOM (-8)
+
+#define OR_CHUNK 4096      /* nodes per partial sum of a dot product (fixed: thread-count independent) */
+
+int or_num_threads(void) { return omp_get_max_threads(); }
 
 typedef struct {
     int64_t ne[3];         /* elements per axis */
@@ -367,6 +377,7 @@ int or_csr_copy(const or_ctx *o, int64_t *rowptr, int64_t *col, double *Kv, doub
 int or_spmv(const or_ctx *o, double aK, double aM, const double *u, double *y)
 {
     if (!o->has_csr) return OR_E_ARG;
+#pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < o->nnodes; r++) {
         double s = 0.0;
         for (int64_t p = o->rowptr[r]; p < o->rowptr[r + 1]; p++)
@@ -531,6 +542,7 @@ int or_is_dirichlet(const or_ctx *o, unsigned char *mask)
 int or_diag(const or_ctx *o, double aK, double aM, double *diag)
 {
     if (!o->has_csr) return OR_E_ARG;
+#pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < o->nnodes; r++) {
         double d = 0.0;
         for (int64_t p = o->rowptr[r]; p < o->rowptr[r + 1]; p++)
@@ -543,15 +555,29 @@ int or_diag(const or_ctx *o, double aK, double aM, double *diag)
 /* Eliminated operator on free nodes: y_F = A_FF x_F, y_D = 0 (reading R3). */
 static void spmv_free(const or_ctx *o, double aK, double aM, const double *x, double *y, double *tmp)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t n = 0; n < o->nnodes; n++) tmp[n] = o->isD[n] ? 0.0 : x[n];
     or_spmv(o, aK, aM, tmp, y);
+#pragma omp parallel for schedule(static)
     for (int64_t n = 0; n < o->nnodes; n++) if (o->isD[n]) y[n] = 0.0;
 }
 
+/* sum over free nodes of a_n b_n: chunks of OR_CHUNK nodes summed left to right, then the chunk
+ * sums left to right (fixed order for any thread count) */
 static double dot_free(const or_ctx *o, const double *a, const double *b)
 {
+    const int64_t N = o->nnodes, nch = (N + OR_CHUNK - 1) / OR_CHUNK;
+    double *part = malloc(sizeof(double) * (size_t)(nch > 0 ? nch : 1));
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nch; c++) {
+        const int64_t n1 = (c + 1) * OR_CHUNK < N ? (c + 1) * OR_CHUNK : N;
+        double s = 0.0;
+        for (int64_t n = c * OR_CHUNK; n < n1; n++) if (!o->isD[n]) s += a[n] * b[n];
+        part[c] = s;
+    }
     double s = 0.0;
-    for (int64_t n = 0; n < o->nnodes; n++) if (!o->isD[n]) s += a[n] * b[n];
+    for (int64_t c = 0; c < nch; c++) s += part[c];
+    free(part);
     return s;
 }
 
@@ -573,6 +599,7 @@ int or_pcg(const or_ctx *o, double aK, double aM, const double *b, double *x,
     double *P = malloc(sizeof(double) * N), *tmp = malloc(sizeof(double) * N);
     if (!r || !s || !d || !q || !P || !tmp) return OR_E_OOM;
     or_diag(o, aK, aM, P);
+#pragma omp parallel for schedule(static)
     for (int64_t n = 0; n < N; n++) if (o->isD[n]) x[n] = b[n];
     double bnorm = sqrt(dot_free(o, b, b));
     int status = OR_OK, i = 0;
@@ -585,8 +612,10 @@ int or_pcg(const or_ctx *o, double aK, double aM, const double *b, double *x,
     }
     /* line 3: r <- b - A x */
     spmv_free(o, aK, aM, x, q, tmp);
+#pragma omp parallel for schedule(static)
     for (int64_t n = 0; n < N; n++) r[n] = o->isD[n] ? 0.0 : b[n] - q[n];
     /* line 4: d <- P^{-1} r ; line 5: delta <- r^T d */
+#pragma omp parallel for schedule(static)
     for (int64_t n = 0; n < N; n++) d[n] = r[n] / P[n];
     delta = dot_free(o, r, d);
     rr = dot_free(o, r, r);
@@ -595,18 +624,23 @@ int or_pcg(const or_ctx *o, double aK, double aM, const double *b, double *x,
         double dq = dot_free(o, d, q);
         if (!(dq > 0.0) || !isfinite(dq)) { status = OR_E_BREAKDOWN; break; }
         double alpha = delta / dq;                        /* line 8 */
+#pragma omp parallel for schedule(static)
         for (int64_t n = 0; n < N; n++) if (!o->isD[n]) x[n] += alpha * d[n];   /* line 9 */
         if (i > 0 && replace_every > 0 && i % replace_every == 0) {               /* line 10-11 */
             spmv_free(o, aK, aM, x, q, tmp);
+#pragma omp parallel for schedule(static)
             for (int64_t n = 0; n < N; n++) r[n] = o->isD[n] ? 0.0 : b[n] - q[n];
         } else {
+#pragma omp parallel for schedule(static)
             for (int64_t n = 0; n < N; n++) r[n] -= alpha * q[n];                 /* line 13 */
         }
+#pragma omp parallel for schedule(static)
         for (int64_t n = 0; n < N; n++) s[n] = r[n] / P[n];                       /* line 15 */
         double delta_old = delta;                                                 /* R5 */
         delta = dot_free(o, r, s);                                                /* line 16 */
         rr = dot_free(o, r, r);
         double beta = delta / delta_old;                                          /* line 17 */
+#pragma omp parallel for schedule(static)
         for (int64_t n = 0; n < N; n++) d[n] = s[n] + beta * d[n];                /* line 18 */
         i++;                                                                      /* line 19 */
     }
@@ -625,6 +659,7 @@ void or_rhs(const or_ctx *o, double theta, double dt, const double *F, const dou
 {
     const int64_t N = o->nnodes;
     or_spmv(o, -(1.0 - theta) * dt, 1.0, un, b);
+#pragma omp parallel for schedule(static)
     for (int64_t n = 0; n < N; n++) b[n] += dt * F[n];
     if (o->bits) {
         double *Ag = malloc(sizeof(double) * N);
@@ -655,6 +690,7 @@ int or_simulate(const or_ctx *o, double theta, double dt, int nsteps, const doub
     int status = OR_OK;
     for (int step = 0; step < nsteps; step++) {
         or_rhs(o, theta, dt, F, u, b);
+#pragma omp parallel for schedule(static)
         for (int64_t n = 0; n < N; n++) x[n] = step == 0 ? u[n] : 2.0 * u[n] - uprev[n];
         double info[3];
         status = or_pcg(o, theta * dt, 1.0, b, x, tol, max_iter, replace_every, info);

@@ -73,7 +73,7 @@ def test_product_never_uses_oracle():
     # and the oracle never includes product code
     osrc = open(os.path.join(ROOT, "oracle", "heat_oracle.c")).read()
     includes = re.findall(r"^\s*#\s*include\s*[<\"]([^>\"]+)", osrc, re.M)
-    assert includes and all(i in ("math.h", "stdint.h", "stdlib.h", "string.h") for i in includes), includes
+    assert includes and all(i in ("math.h", "omp.h", "stdint.h", "stdlib.h", "string.h") for i in includes), includes
 
 
 def test_binding_rejects_bad_arrays():
