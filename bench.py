@@ -137,9 +137,8 @@ def run_ours(args):
     dev = torch.device("cuda", local_rank)
     dist = None
     if slab:
-        # stdout carries exactly one JSON line: keep NCCL's version banner off it
-        os.environ["NCCL_DEBUG"] = os.environ.get("HF_BENCH_NCCL_DEBUG", "WARN")
-        # NCCL prints its version banner at WARN level through its log file, stdout by default
+        # stdout carries exactly one JSON line: NCCL's log (NCCL_DEBUG as the caller set it,
+        # e.g. INFO for the communicator lines) goes to stderr unless a log file is given
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         if not dist.is_initialized():
@@ -612,12 +611,30 @@ def oracle_steps(nsteps_timed, warm=1):
     return t * 1e3 / nsteps_timed, int(it2.sum()), t_setup, p
 
 
+def _omp_threads(n):
+    """Run the oracle on n OpenMP threads from here on (omp_set_num_threads through libgomp)."""
+    import ctypes
+    import oracle
+    oracle.lib()
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+    except OSError:
+        pass
+    return oracle.num_threads()
+
+
 def cpu_baseline(args):
+    """The oracle as it stands on this host: all cores (OpenMP, the value) and one core."""
     steps = 2
+    cores = _omp_threads(os.cpu_count() or 1)
     ms, iters, t_setup, p = oracle_steps(steps, warm=0)
-    return {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle",
+    _omp_threads(1)
+    ms1, _, _, _ = oracle_steps(1, warm=0)
+    _omp_threads(cores)
+    return {"value": ms, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{steps} time steps of C3 after CSR assembly ({t_setup:.1f} s, excluded): "
-                      f"{iters / steps:.0f} PCG iterations/step, plain C, 1 thread"}
+                      f"{iters / steps:.0f} PCG iterations/step, plain C + OpenMP on {cores} threads",
+            "single_core": {"value": ms1, "unit": UNIT, "cores": 1, "sample": "1 time step of C3, 1 thread"}}
 
 
 def run_reference(args):
@@ -627,14 +644,16 @@ def run_reference(args):
         return None
     steps = max(1, min(args.steps, 20))
     warm = 1 if args.warmup > 0 else 0
+    cores = _omp_threads(os.cpu_count() or 1)
     ms, iters, t_setup, p = oracle_steps(steps, warm=warm)
     sample = (f"{steps} of the K={args.steps} requested C3 time steps (capped at 20 to bound the run), after "
-              f"{warm} warm-up step and CSR assembly ({t_setup:.1f} s, excluded); plain C oracle, 1 thread")
+              f"{warm} warm-up step and CSR assembly ({t_setup:.1f} s, excluded); plain C oracle, OpenMP on "
+              f"{cores} threads")
     return {"impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded inclusion field, synth.c3)",
             "config": workload_config(p, 1, {"pcg_iters_per_step": iters / steps}),
-            "cpu_baseline": {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": ms, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
 
@@ -654,6 +673,24 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun (127.0.0.1 rendezvous)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "ours":
+        import torch
+        if torch.cuda.device_count() < int(os.environ.get("LOCAL_WORLD_SIZE", world)):
+            sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {torch.cuda.device_count()}")
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None:
         print(json.dumps(line), flush=True)

@@ -65,6 +65,8 @@ def lib():
         L.or_pcg.argtypes = [C.c_void_p, C.c_double, C.c_double, _dp, _dp, C.c_double, C.c_int,
                              C.c_int, _dp]
         L.or_rhs.argtypes = [C.c_void_p, C.c_double, C.c_double, _dp, _dp, _dp]
+        L.or_simulate_resume.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int, _dp, _dp, C.c_void_p,
+                                         C.c_int64, C.c_double, C.c_int, C.c_int, _i32p, C.c_int64, C.c_void_p]
         L.or_num_threads.restype = C.c_int
         L.or_num_threads.argtypes = []
         L.or_simulate.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int, _dp, _dp, C.c_double,
@@ -196,6 +198,25 @@ class Oracle:
         st = lib().or_simulate(self._p, theta, dt, nsteps, _f64(F), u, tol, max_iter, replace_every,
                                iters, -1 if snap_plane is None else snap_plane, sp_arg)
         return u, st, iters[:nsteps], snap
+
+
+    def simulate_resume(self, theta, dt, nsteps, F, u, u_prev, step0, tol=1e-12, max_iter=10000,
+                        replace_every=50, snap_plane: Optional[int] = None):
+        """Checkpoint / resume of the time loop: the guess of the first step is 2 u - u_prev when
+        step0 > 0 (R9).  Returns (u^{n+nsteps}, u^{n+nsteps-1}, status, iters, snap)."""
+        u = _f64(u).copy()
+        up = _f64(u_prev if u_prev is not None else u).copy()
+        iters = np.zeros(max(nsteps, 1), dtype=np.int32)
+        snap = None
+        sp_arg = None
+        if snap_plane is not None:
+            plane = (self.grid.ne[0] + 1) * (self.grid.ne[1] + 1)
+            snap = np.zeros((max(nsteps, 1), plane))
+            sp_arg = snap.ctypes.data_as(C.c_void_p)
+        st = lib().or_simulate_resume(self._p, theta, dt, nsteps, _f64(F), u, up.ctypes.data_as(C.c_void_p),
+                                      step0 if u_prev is not None else 0, tol, max_iter, replace_every, iters,
+                                      -1 if snap_plane is None else snap_plane, sp_arg)
+        return u, up, st, iters[:nsteps], snap
 
 
 def problem_oracle(p, assemble=True, elem=0):

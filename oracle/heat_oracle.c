@@ -670,28 +670,35 @@ void or_rhs(const or_ctx *o, double theta, double dt, const double *F, const dou
 }
 
 /*
- * theta-scheme time loop: for n = 0..nsteps-1 solve A u^{n+1} = b(u^n).
- * Guess (reading R9): x0 = u^0 at n = 0, else 2 u^n - u^{n-1}.
- * u: in u^0 (Dirichlet nodes are set to g first), out u^{nsteps}.
- * iters[n] receives the PCG iteration count of step n (may be NULL).
+ * theta-scheme time loop: for n = step0..step0+nsteps-1 solve A u^{n+1} = b(u^n).
+ * Guess (reading R9): x0 = u^n at n = 0 of a run, else 2 u^n - u^{n-1}.
+ * u: in u^{step0} (Dirichlet nodes are set to g first), out u^{step0+nsteps}.
+ * uprev (may be NULL): in u^{step0-1} (used when step0 > 0: a resumed run), out the iterate
+ * before the final one.  iters[n] receives the PCG iteration count of step n (may be NULL).
  * snap (may be NULL): after each step, the plane k = snap_plane of u is appended.
  */
-int or_simulate(const or_ctx *o, double theta, double dt, int nsteps, const double *F, double *u,
-                double tol, int max_iter, int replace_every, int32_t *iters,
-                int64_t snap_plane, double *snap)
+int or_simulate_resume(const or_ctx *o, double theta, double dt, int nsteps, const double *F, double *u,
+                       double *uprev_io, int64_t step0, double tol, int max_iter, int replace_every,
+                       int32_t *iters, int64_t snap_plane, double *snap)
 {
     const int64_t N = o->nnodes;
     const int64_t plane = o->nn[0] * o->nn[1];
     double *uprev = malloc(sizeof(double) * N), *b = malloc(sizeof(double) * N);
     double *x = malloc(sizeof(double) * N);
     if (!uprev || !b || !x) return OR_E_OOM;
+    const int first = step0 <= 0 || !uprev_io;
     for (int64_t n = 0; n < N; n++) if (o->isD[n]) u[n] = o->g[n];
-    memcpy(uprev, u, sizeof(double) * N);
+    if (first) memcpy(uprev, u, sizeof(double) * N);
+    else {
+        memcpy(uprev, uprev_io, sizeof(double) * N);
+        for (int64_t n = 0; n < N; n++) if (o->isD[n]) uprev[n] = o->g[n];
+    }
     int status = OR_OK;
     for (int step = 0; step < nsteps; step++) {
         or_rhs(o, theta, dt, F, u, b);
+        const int guess_u = step == 0 && first;
 #pragma omp parallel for schedule(static)
-        for (int64_t n = 0; n < N; n++) x[n] = step == 0 ? u[n] : 2.0 * u[n] - uprev[n];
+        for (int64_t n = 0; n < N; n++) x[n] = guess_u ? u[n] : 2.0 * u[n] - uprev[n];
         double info[3];
         status = or_pcg(o, theta * dt, 1.0, b, x, tol, max_iter, replace_every, info);
         if (iters) iters[step] = (int32_t)info[0];
@@ -700,6 +707,15 @@ int or_simulate(const or_ctx *o, double theta, double dt, int nsteps, const doub
         if (snap) memcpy(snap + (int64_t)step * plane, u + snap_plane * plane, sizeof(double) * plane);
         if (status != OR_OK) break;
     }
+    if (uprev_io) memcpy(uprev_io, uprev, sizeof(double) * N);
     free(uprev); free(b); free(x);
     return status;
+}
+
+int or_simulate(const or_ctx *o, double theta, double dt, int nsteps, const double *F, double *u,
+                double tol, int max_iter, int replace_every, int32_t *iters,
+                int64_t snap_plane, double *snap)
+{
+    return or_simulate_resume(o, theta, dt, nsteps, F, u, NULL, 0, tol, max_iter, replace_every, iters,
+                              snap_plane, snap);
 }

@@ -128,6 +128,17 @@ def _ptr(a, n: Optional[int] = None, name: str = "array", allow_none: bool = Fal
     raise HfError(HF_E_ARG, f"{name}: unsupported type {type(a)}")
 
 
+def _cptr(ctx, a, n: Optional[int] = None, name: str = "array", allow_none: bool = False):
+    """_ptr for an array passed to context `ctx`: a CUDA tensor must live on the context's device."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor) and a.is_cuda and a.device.index != ctx.device:
+            raise HfError(HF_E_ARG, f"{name}: tensor on {a.device}, context on cuda:{ctx.device}")
+    except ImportError:
+        pass
+    return _ptr(a, n, name, allow_none)
+
+
 CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy: torch's default stream reports handle 0
 
 
@@ -205,13 +216,13 @@ def hf_destroy(ctx: Context):
 
 
 def hf_set_coefficients(ctx: Context, k, c):
-    _check(_lib.hf_set_coefficients(ctx.ptr, _ptr(k, ctx.n_elems, "k"), _ptr(c, ctx.n_elems, "c")))
+    _check(_lib.hf_set_coefficients(ctx.ptr, _cptr(ctx, k, ctx.n_elems, "k"), _cptr(ctx, c, ctx.n_elems, "c")))
 
 
 def hf_set_vertex_coefficients(ctx: Context, k_node, c_node):
     """Per-node materials of the global grid, averaged over each element's vertices."""
     n = ctx.n_nodes_global
-    _check(_lib.hf_set_vertex_coefficients(ctx.ptr, _ptr(k_node, n, "k_node"), _ptr(c_node, n, "c_node")))
+    _check(_lib.hf_set_vertex_coefficients(ctx.ptr, _cptr(ctx, k_node, n, "k_node"), _cptr(ctx, c_node, n, "c_node")))
 
 
 def hf_set_dirichlet_faces(ctx: Context, face_bits: int, values: Optional[Sequence[float]] = None):
@@ -221,16 +232,16 @@ def hf_set_dirichlet_faces(ctx: Context, face_bits: int, values: Optional[Sequen
 
 def hf_face_load(ctx: Context, face: int, f_const: float, beam, F):
     b = None if beam is None else C.byref((C.c_double * 4)(*beam))
-    _check(_lib.hf_face_load(ctx.ptr, face, f_const, b, _ptr(F, ctx.n_nodes, "F")))
+    _check(_lib.hf_face_load(ctx.ptr, face, f_const, b, _cptr(ctx, F, ctx.n_nodes, "F")))
 
 
 def hf_apply(ctx: Context, aK: float, aM: float, u, y):
-    _check(_lib.hf_apply(ctx.ptr, aK, aM, _ptr(u, ctx.n_nodes, "u"), _ptr(y, ctx.n_nodes, "y")))
+    _check(_lib.hf_apply(ctx.ptr, aK, aM, _cptr(ctx, u, ctx.n_nodes, "u"), _cptr(ctx, y, ctx.n_nodes, "y")))
 
 
 def hf_apply_axpby(ctx: Context, aK: float, aM: float, c: float, u, b, y):
-    _check(_lib.hf_apply_axpby(ctx.ptr, aK, aM, c, _ptr(u, ctx.n_nodes, "u"),
-                               _ptr(b, ctx.n_nodes, "b", allow_none=True), _ptr(y, ctx.n_nodes, "y")))
+    _check(_lib.hf_apply_axpby(ctx.ptr, aK, aM, c, _cptr(ctx, u, ctx.n_nodes, "u"),
+                               _cptr(ctx, b, ctx.n_nodes, "b", allow_none=True), _cptr(ctx, y, ctx.n_nodes, "y")))
 
 
 def hf_set_material_ids(ctx: Context, ids, k_mat: Sequence[float], c_mat: Sequence[float]):
@@ -244,6 +255,8 @@ def hf_set_material_ids(ctx: Context, ids, k_mat: Sequence[float], c_mat: Sequen
         if isinstance(ids, torch.Tensor):
             if ids.dtype != torch.uint8 or not ids.is_contiguous() or ids.numel() != ctx.n_elems:
                 raise HfError(HF_E_ARG, "ids: need a contiguous uint8 tensor of n_elements")
+            if ids.is_cuda and ids.device.index != ctx.device:
+                raise HfError(HF_E_ARG, f"ids: tensor on {ids.device}, context on cuda:{ctx.device}")
             ptr = ids.data_ptr()
     except ImportError:
         pass
@@ -261,8 +274,8 @@ def hf_set_material_ids(ctx: Context, ids, k_mat: Sequence[float], c_mat: Sequen
 def hf_apply_impl(ctx: Context, impl: int, aK: float, aM: float, c: float, u, b, y):
     """NEXT f4 ablation: Implementation 1 (two-pass, stored element matrices), 2 (single-pass
     gather) or 3 (the production stencil) of the same apply."""
-    _check(_lib.hf_apply_impl(ctx.ptr, int(impl), aK, aM, c, _ptr(u, ctx.n_nodes, "u"),
-                              _ptr(b, ctx.n_nodes, "b", allow_none=True), _ptr(y, ctx.n_nodes, "y")))
+    _check(_lib.hf_apply_impl(ctx.ptr, int(impl), aK, aM, c, _cptr(ctx, u, ctx.n_nodes, "u"),
+                              _cptr(ctx, b, ctx.n_nodes, "b", allow_none=True), _cptr(ctx, y, ctx.n_nodes, "y")))
 
 
 def hf_ablation_prepare(ctx: Context, aK: float, aM: float):
@@ -270,14 +283,14 @@ def hf_ablation_prepare(ctx: Context, aK: float, aM: float):
 
 
 def hf_diag(ctx: Context, aK: float, aM: float, diag):
-    _check(_lib.hf_diag(ctx.ptr, aK, aM, _ptr(diag, ctx.n_nodes, "diag")))
+    _check(_lib.hf_diag(ctx.ptr, aK, aM, _cptr(ctx, diag, ctx.n_nodes, "diag")))
 
 
 def hf_cg(ctx: Context, aK: float, aM: float, b, x, rtol=1e-12, max_iter=10000, replace_every=-1,
           raise_on_noconv: bool = True) -> dict:
     info = hf_cg_info()
     o = _opts(rtol, max_iter, replace_every)
-    st = _lib.hf_cg(ctx.ptr, aK, aM, _ptr(b, ctx.n_nodes, "b"), _ptr(x, ctx.n_nodes, "x"), C.byref(o), C.byref(info))
+    st = _lib.hf_cg(ctx.ptr, aK, aM, _cptr(ctx, b, ctx.n_nodes, "b"), _cptr(ctx, x, ctx.n_nodes, "x"), C.byref(o), C.byref(info))
     res = {"iters": info.iters, "status": info.status, "relres": info.relres, "delta": info.delta}
     if st != HF_OK and (raise_on_noconv or st not in (HF_E_NOCONV, HF_E_BREAKDOWN)):
         _check(st)
@@ -294,9 +307,9 @@ def hf_simulate(ctx: Context, theta: float, dt: float, nsteps: int, F, u, snap_p
                 rtol=1e-12, max_iter=10000, replace_every=-1, raise_on_noconv: bool = True) -> dict:
     s = hf_sim_stats()
     o = _opts(rtol, max_iter, replace_every)
-    st = _lib.hf_simulate(ctx.ptr, theta, dt, nsteps, _ptr(F, ctx.n_nodes, "F", allow_none=True),
-                          _ptr(u, ctx.n_nodes, "u"), snap_plane,
-                          _ptr(snap, nsteps * ctx.n_plane, "snap", allow_none=True), C.byref(o), C.byref(s))
+    st = _lib.hf_simulate(ctx.ptr, theta, dt, nsteps, _cptr(ctx, F, ctx.n_nodes, "F", allow_none=True),
+                          _cptr(ctx, u, ctx.n_nodes, "u"), snap_plane,
+                          _cptr(ctx, snap, nsteps * ctx.n_plane, "snap", allow_none=True), C.byref(o), C.byref(s))
     res = _stats(s)
     if st != HF_OK and (raise_on_noconv or st not in (HF_E_NOCONV, HF_E_BREAKDOWN)):
         _check(st)
@@ -308,8 +321,8 @@ def hf_simulate_resume(ctx: Context, theta: float, dt: float, nsteps: int, F, u,
                        rtol=1e-12, max_iter=10000, replace_every=-1) -> dict:
     s = hf_sim_stats()
     o = _opts(rtol, max_iter, replace_every)
-    _check(_lib.hf_simulate_resume(ctx.ptr, theta, dt, nsteps, _ptr(F, ctx.n_nodes, "F", allow_none=True),
-                                   _ptr(u, ctx.n_nodes, "u"), _ptr(u_prev, ctx.n_nodes, "u_prev", allow_none=True),
+    _check(_lib.hf_simulate_resume(ctx.ptr, theta, dt, nsteps, _cptr(ctx, F, ctx.n_nodes, "F", allow_none=True),
+                                   _cptr(ctx, u, ctx.n_nodes, "u"), _cptr(ctx, u_prev, ctx.n_nodes, "u_prev", allow_none=True),
                                    step0, C.byref(o), C.byref(s)))
     return _stats(s)
 
@@ -318,11 +331,11 @@ def hf_simulate_batched(ctx: Context, B: int, k_batch, c_batch, theta: float, dt
                         snap_plane: int = -1, front_out=None, rtol=1e-12, max_iter=10000, replace_every=-1) -> list:
     stats = (hf_sim_stats * max(B, 1))()
     o = _opts(rtol, max_iter, replace_every)
-    _check(_lib.hf_simulate_batched(ctx.ptr, B, _ptr(k_batch, B * ctx.n_elems, "k_batch"),
-                                    _ptr(c_batch, B * ctx.n_elems, "c_batch", allow_none=True), theta, dt, nsteps,
-                                    _ptr(F, ctx.n_nodes, "F", allow_none=True),
-                                    _ptr(u_batch, B * ctx.n_nodes, "u_batch"), snap_plane,
-                                    _ptr(front_out, B * ctx.n_plane, "front_out", allow_none=True), C.byref(o), stats))
+    _check(_lib.hf_simulate_batched(ctx.ptr, B, _cptr(ctx, k_batch, B * ctx.n_elems, "k_batch"),
+                                    _cptr(ctx, c_batch, B * ctx.n_elems, "c_batch", allow_none=True), theta, dt, nsteps,
+                                    _cptr(ctx, F, ctx.n_nodes, "F", allow_none=True),
+                                    _cptr(ctx, u_batch, B * ctx.n_nodes, "u_batch"), snap_plane,
+                                    _cptr(ctx, front_out, B * ctx.n_plane, "front_out", allow_none=True), C.byref(o), stats))
     return [_stats(stats[j]) for j in range(B)]
 
 

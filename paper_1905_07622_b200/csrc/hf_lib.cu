@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -273,10 +274,34 @@ static bool is_device_ptr(const void *p)
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// device memory of another GPU than the context's: rejected at the ABI (HF_E_ARG) instead of
+// being used in TMA maps and kernels of this device
+static bool foreign_ptr(const hf_ctx *c, const void *p)
+{
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice && at.device != c->device;
+}
+
+static hf_status check_ptrs(const hf_ctx *c, const char *who, std::initializer_list<const void *> ps);
+
 // user node vector usable in place: device, natural pitch == internal pitch, 16-B aligned
 static bool direct_ok(const hf_ctx *c, const void *p)
 {
     return c->es == 8 && c->pitch == c->nx1 && ((uintptr_t)p % 16) == 0 && is_device_ptr(p);
+}
+
+static hf_status check_ptrs(const hf_ctx *c, const char *who, std::initializer_list<const void *> ps)
+{
+    for (const void *p : ps)
+        if (foreign_ptr(c, p))
+            return fail(HF_E_ARG, std::string(who) + ": array on another CUDA device than the context's (device " +
+                                      std::to_string(c->device) + ")");
+    return HF_OK;
 }
 
 static hf_status scratch_get(hf_ctx *c, int slot, size_t bytes, void **out)
@@ -1070,6 +1095,15 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
 }
 
 static void ctx_free(hf_ctx *c);
+
+// batched stacks copy the operator settings (Dirichlet faces, element, precision, driver) of
+// their parent when created: every setter that changes them drops the stacks
+static void drop_stacks(hf_ctx *c)
+{
+    for (auto &kv : c->stacks) { ctx_free(kv.second); delete kv.second; }
+    c->stacks.clear();
+}
+
 static void ctx_free(hf_ctx *c)
 {
     if (!c) return;
@@ -1381,6 +1415,20 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
     cudaGraphConditionalHandle hw, hi;
     CUCK(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
     cudaGraphNode_t prev = nullptr, n;
+    if (pdl && L.has_ab) {
+        // the fused A+B launch's grid barrier counts arrivals in multiples of its grid size: every
+        // launch of this graph starts it from zero (the grid may differ from an earlier graph's)
+        unsigned long long *ctr = L.AB.get<StencilArgs>(0).gbar;
+        cudaMemsetParams mp;
+        std::memset(&mp, 0, sizeof(mp));
+        mp.dst = ctr;
+        mp.elementSize = 4;
+        mp.width = 2;
+        mp.height = 1;
+        mp.value = 0;
+        CUCK(cudaGraphAddMemsetNode(&n, g, nullptr, 0, &mp));
+        prev = n;
+    }
     for (auto &p : pre) { HFCK(add_node(g, p, prev ? &prev : nullptr, &n)); prev = n; }
     // the loop is entered once at least; kernel A of the iteration after the last decides to
     // stop (it clears the WHILE handle), kernel B sets the IF handle of the replacement
@@ -1501,6 +1549,7 @@ void hf_destroy(hf_ctx *c)
 hf_status hf_set_coefficients(hf_ctx *c, const double *k, const double *cc)
 {
     if (!c || !k || !cc) return fail(HF_E_ARG, "hf_set_coefficients: NULL argument");
+    HFCK(check_ptrs(c, "hf_set_coefficients", {k, cc}));
     CUCK(cudaSetDevice(c->device));
     const size_t ne = (size_t)(c->g.ne[0] * c->g.ne[1] * c->g.ne[2]);
     const double *dk, *dc;
@@ -1529,6 +1578,7 @@ hf_status hf_set_material_ids(hf_ctx *c, const uint8_t *ids, int32_t nmat, const
     if (!c || !ids || !k_mat || !c_mat) return fail(HF_E_ARG, "hf_set_material_ids: NULL argument");
     if (nmat < 1 || nmat > PAL_MAX - 1)
         return fail(HF_E_ARG, "hf_set_material_ids: n_materials must be in [1, " + std::to_string(PAL_MAX - 1) + "]");
+    HFCK(check_ptrs(c, "hf_set_material_ids", {ids}));
     CUCK(cudaSetDevice(c->device));
     const size_t ne = (size_t)(c->g.ne[0] * c->g.ne[1] * c->g.ne[2]);
     const uint8_t *dids = ids;
@@ -1586,6 +1636,7 @@ hf_status hf_set_material_ids(hf_ctx *c, const uint8_t *ids, int32_t nmat, const
 hf_status hf_set_vertex_coefficients(hf_ctx *c, const double *k, const double *cc)
 {
     if (!c || !k || !cc) return fail(HF_E_ARG, "hf_set_vertex_coefficients: NULL argument");
+    HFCK(check_ptrs(c, "hf_set_vertex_coefficients", {k, cc}));
     CUCK(cudaSetDevice(c->device));
     const size_t nng = (size_t)c->nx1 * c->ny1 * c->nz1g;     // global natural nodes
     const double *dk, *dc;
@@ -1627,6 +1678,7 @@ hf_status hf_set_dirichlet_faces(hf_ctx *c, uint32_t bits, const double values[6
     if (!c || bits > 63u) return fail(HF_E_ARG, "hf_set_dirichlet_faces: bad argument");
     c->dbits = bits;
     for (int f = 0; f < 6; f++) c->gval[f] = values ? values[f] : 0.0;
+    drop_stacks(c);
     c->sys0.key_valid = false;
     for (auto &p : c->pool) p->key_valid = false;
     return HF_OK;
@@ -1636,6 +1688,7 @@ hf_status hf_face_load(hf_ctx *c, int face, double f_const, const double beam[4]
 {
     if (!c || !F || face < 0 || face > 5) return fail(HF_E_ARG, "hf_face_load: bad argument");
     if (beam && !(beam[1] > 0.0)) return fail(HF_E_ARG, "hf_face_load: beam sigma must be > 0");
+    HFCK(check_ptrs(c, "hf_face_load", {F}));
     CUCK(cudaSetDevice(c->device));
     double *dF;
     HFCK(node_out(c, F, 2, false, &dF));
@@ -1670,6 +1723,7 @@ hf_status hf_apply_axpby(hf_ctx *c, double aK, double aM, double cc, const doubl
     if (!c || !u || !y) return fail(HF_E_ARG, "hf_apply: NULL argument");
     if (!c->coef_set) return fail(HF_E_STATE, "hf_apply: coefficients not set");
     if ((const double *)y == u) return fail(HF_E_ARG, "hf_apply: u and y must not alias");
+    HFCK(check_ptrs(c, "hf_apply", {u, b, y}));
     CUCK(cudaSetDevice(c->device));
     const double *du, *db = nullptr;
     double *dy;
@@ -1699,6 +1753,7 @@ hf_status hf_diag(hf_ctx *c, double aK, double aM, double *diag)
 {
     if (!c || !diag) return fail(HF_E_ARG, "hf_diag: NULL argument");
     if (!c->coef_set) return fail(HF_E_STATE, "hf_diag: coefficients not set");
+    HFCK(check_ptrs(c, "hf_diag", {diag}));
     CUCK(cudaSetDevice(c->device));
     double *dd;
     HFCK(node_out(c, diag, 5, false, &dd));
@@ -1761,6 +1816,7 @@ hf_status hf_apply_impl(hf_ctx *c, int32_t impl, double aK, double aM, double cc
     if (impl != 1 && impl != 2) return fail(HF_E_ARG, "hf_apply_impl: impl must be 1, 2 or 3");
     if ((const double *)y == u) return fail(HF_E_ARG, "hf_apply_impl: u and y must not alias");
     HFCK(ablation_ok(c, "hf_apply_impl"));
+    HFCK(check_ptrs(c, "hf_apply_impl", {u, b, y}));
     if (impl == 1 && (!c->ab_ready || aK != c->ab_aK || aM != c->ab_aM))
         return fail(HF_E_STATE, "hf_apply_impl: Implementation 1 needs hf_ablation_prepare with the same (aK, aM)");
     CUCK(cudaSetDevice(c->device));
@@ -1793,6 +1849,7 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
 {
     if (!c || !b || !x) return fail(HF_E_ARG, "hf_cg: NULL argument");
     if (!c->coef_set) return fail(HF_E_STATE, "hf_cg: coefficients not set");
+    HFCK(check_ptrs(c, "hf_cg", {b, x}));
     CUCK(cudaSetDevice(c->device));
     Sys &s = c->sys0;
     hf_cg_opts o = {1e-12, 10000, -1};
@@ -2025,6 +2082,7 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
         return fail(HF_E_ARG, "hf_simulate: bad argument");
     if (!c->coef_set) return fail(HF_E_STATE, "hf_simulate: coefficients not set");
     if (snap && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "hf_simulate: snap_plane");
+    HFCK(check_ptrs(c, "hf_simulate", {F, u, u_prev, snap}));
     CUCK(cudaSetDevice(c->device));
     Sys &s = c->sys0;
     hf_cg_opts o = {1e-12, 10000, -1};
@@ -2207,6 +2265,7 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
     if (c->comm) return fail(HF_E_ARG, "hf_simulate_batched: not available on slab contexts");
     if (c->tetv) return fail(HF_E_STATE, "hf_simulate_batched: per-element coefficients only (not vertex materials)");
     if (front_out && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "snap_plane");
+    HFCK(check_ptrs(c, "hf_simulate_batched", {k_batch, c_batch, F, u_batch, front_out}));
     CUCK(cudaSetDevice(c->device));
     hf_cg_opts o = {1e-12, 10000, -1};
     if (opts) o = *opts;
@@ -2572,6 +2631,7 @@ hf_status hf_set_driver(hf_ctx *c, int32_t driver)
 {
     if (!c || driver < 0 || driver > 1) return fail(HF_E_ARG, "hf_set_driver: bad argument");
     c->driver = driver;
+    drop_stacks(c);
     return HF_OK;
 }
 
@@ -2581,6 +2641,7 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
     CUCK(cudaSetDevice(c->device));
     c->elem = type;
     c->ab_ready = false;
+    drop_stacks(c);
     const double *h = c->g.h;
     // the dense (tet) element keeps R = 2 tiles (R = 4 spills); TMA boxes follow the tile height
     int want_r = default_tile_r(c, type);
@@ -2618,6 +2679,7 @@ hf_status hf_set_precision(hf_ctx *c, int32_t bits)
     sys_free(c->sys0);
     for (auto &p : c->pool) sys_free(*p);
     c->pool.clear();
+    drop_stacks(c);
     for (void *p : c->scratch) cudaFree(p);      // layouts change: reallocate (zeroed) on demand
     c->scratch.clear();
     c->scratch_cap.clear();

@@ -364,6 +364,35 @@ def test_batched_matches_individual(mode, monkeypatch):
             assert stats[j]["steps_done"] == 6
 
 
+def test_batched_follows_operator_setters():
+    """Dirichlet faces / values and the element type changed between two batched calls on the
+    same context reach every later call (the batched path must not keep stale operators)."""
+    g = synth.Grid((10, 9, 8), (0.3, 0.3, 0.2))
+    B = 4
+    base_k, base_c = synth.random_fields(g, seed=31)
+    ks = np.stack([base_k * synth.lognormal_perturbation(g.n_elems, seed=40 + j) for j in range(B)])
+    ctx = make_ctx(g, base_k, base_c)
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+    Fh = N(F)
+    for bits, vals, elem in [(1, (0.0,) * 6, 0), (3, (0.5, -0.25, 0, 0, 0, 0), 0), (3, (0.5, -0.25, 0, 0, 0, 0), 1),
+                             (0, (0.0,) * 6, 1)]:
+        hf.hf_set_dirichlet_faces(ctx, bits, vals)
+        hf.hf_set_element(ctx, elem)
+        if elem == 1:
+            hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+            Fh = N(F)
+        ub = torch.zeros(B * g.n_nodes, dtype=torch.float64, device=DEV)
+        hf.hf_simulate_batched(ctx, B, T(ks.ravel()), None, 0.5, 0.05, 4, F, ub)
+        ub = N(ub).reshape(B, -1)
+        for j in range(B):
+            o = oracle.Oracle(g, ks[j], base_c, elem=elem)
+            if bits:
+                o.set_dirichlet(bits, vals)
+            uo, st, it, _ = o.simulate(0.5, 0.05, 4, Fh, np.zeros(g.n_nodes))
+            assert rel(ub[j], uo) <= 1e-10, (bits, vals, elem, j)
+
+
 # ---------------------------------------------------------------------------------------------
 # z-slabs through the in-process transport (same kernels and exchange protocol as NCCL)
 

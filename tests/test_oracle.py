@@ -246,6 +246,23 @@ def test_bar_discrete_closed_form_cn():
     assert np.linalg.norm(u - ex) <= 1e-10 * np.linalg.norm(ex)
 
 
+def test_bar_closed_form_through_resume_segments():
+    """Checkpoint / resume (R9 guess 2u^n - u^{n-1} across the seam): 200 CN steps as 70 + 130
+    meet the same exact discrete solution, and the segments chain to the one-run trajectory."""
+    p = synth.c2()
+    o, F = oracle.problem_oracle(p)
+    u1, up1, st1, it1, _ = o.simulate_resume(p.theta, p.dt, 70, F, p.u0, None, 0)
+    u2, up2, st2, it2, _ = o.simulate_resume(p.theta, p.dt, 130, F, u1, up1, 70)
+    assert st1 == 0 and st2 == 0
+    ex = _bar_closed_form(p, [(1, 1.0)])
+    assert np.linalg.norm(u2 - ex) <= 1e-10 * np.linalg.norm(ex)
+    u, st, it, _ = o.simulate(p.theta, p.dt, p.nsteps, F, p.u0)
+    assert np.array_equal(u, u2) and np.array_equal(it, np.concatenate([it1, it2]))
+    # u_prev out is the iterate one step before the end
+    u3, up3, _, _, _ = o.simulate_resume(p.theta, p.dt, 199, F, p.u0, None, 0)
+    assert np.array_equal(up2, u3)
+
+
 @pytest.mark.parametrize("theta", [1.0, 0.5, 0.0 + 0.6])
 def test_bar_sine_series_any_theta(theta):
     """1D analytic series (north_star): u0 = sin(pi x) + 0.5 sin(3 pi x) decays mode by mode."""
