@@ -45,9 +45,16 @@ enum { ROT_NONE = 0, ROT_RHS = 1, ROT_INIT = 2, ROT_X = 3 };
 enum { MAP_U0 = 0, MAP_D0 = 3, MAP_S = 5 };
 
 // PCG state of one system (Alg. 1 scalars, device resident; the paper keeps them in device
-// buffers too: delta/alpha/beta kernels P:507-573).  Every field is written by block 0 of one
+// buffers too: delta/alpha/beta kernels P:507-573).  Every field is written by one block of one
 // kernel and read only by LATER kernels (kernel boundaries order them), never by the kernel that
 // writes it: delta is double-buffered by iteration parity for that reason.
+// Several independent systems stacked along z in one context (batched forward simulations,
+// a13) have one CgState each, st[0..nsys-1].  The LOOP fields (b_iter, step, a_iter,
+// replace_every, replace, npart_b, npart_a, max_iter) are shared and live in st[0]: every active
+// system is at the same PCG iteration of the same time step, so one loop counter serves all.
+// The SYSTEM fields (first_failed, active, status, zero_x, iter, statistics, rtol2, delta,
+// thresh, bb, rr, alpha, dq) are per system: each system has its own scalars and stop test.
+// npart_a / npart_b count partial sums per system (the blocks of system j are contiguous).
 struct CgState {
     // header: read by every PCG kernel at its start as 16-byte loads issued together (one L2
     // round trip instead of a chain of dependent scalar loads)
@@ -94,6 +101,7 @@ struct Geom {
     int nx, ny;             // elements in x, y
     int kpitch;             // (k, c) pairs per coefficient row (nx, or nx rounded up to even in fp32)
     unsigned dbits;         // Dirichlet face bits (R3)
+    int zper;               // global node planes per stacked system (= nz1g for one system)
     double gval[6];
 };
 
@@ -164,6 +172,7 @@ struct Sync {               // per-system reduction plumbing
     cudaGraphConditionalHandle h_while, h_if;
     int use_handles;        // set the WHILE handle (graph driver)
     int use_if;             // set the IF handle (only where the body has an IF node)
+    int nsys;               // systems stacked along z (>= 1); st points at st[0..nsys-1]
 };
 
 struct Maps {               // TMA descriptors (host copy; kernels read a device-memory copy)
@@ -180,6 +189,7 @@ struct BArgs {
     double *dbuf[2];        // d = dbuf[(iter & 1) ^ 1] (written by kernel A of this iteration)
     double *r, *s;
     long long n, own0, own1;
+    long long sysn;         // node slots per stacked system (= n for one system)
     double *rot[3];         // if rot[0]: x = rot[(step + 1) % 3]
     Sync sy;
 };
@@ -195,6 +205,7 @@ struct StencilArgs {
     double *xout;                 // centre store of x0 when not rotating
     double c, s;
     int z_out0, z_out1, zchunk;   // output planes (local) and planes per CTA
+    int zper_out;                 // output planes per stacked system (= z_out1 - z_out0 for one)
     int zs0, zs1;                 // planes whose centre values are stored
     int dmode;                    // EP_APPLY: 0 none, 1 identity rows, 2 set g on D rows
     int first;                    // LD_X0: step 0 of the run (guess = u^0)
@@ -224,8 +235,11 @@ __device__ __forceinline__ bool is_dirichlet(const Geom &g, int x, int y, int zl
     if ((b & 2u) && x == g.nx1 - 1) { val = g.gval[1]; return true; }
     if ((b & 4u) && y == 0) { val = g.gval[2]; return true; }
     if ((b & 8u) && y == g.ny1 - 1) { val = g.gval[3]; return true; }
-    if ((b & 16u) && zg == 0) { val = g.gval[4]; return true; }
-    if ((b & 32u) && zg == g.nz1g - 1) { val = g.gval[5]; return true; }
+    if (b & 48u) {                       // z faces of the system the plane belongs to
+        const int zs = g.zper == g.nz1g ? zg : zg % g.zper;
+        if ((b & 16u) && zs == 0) { val = g.gval[4]; return true; }
+        if ((b & 32u) && zs == g.zper - 1) { val = g.gval[5]; return true; }
+    }
     return false;
 }
 
@@ -430,10 +444,12 @@ __device__ __forceinline__ void reduce_prev(const double *part, int n, double (&
     }
 }
 
+// sums of system sj's partials (the previous kernel's blocks of system sj are contiguous)
 template <int NT>
-__device__ __forceinline__ void prev_sums(const Sync &sy, int n_state, double (&sums)[NPART])
+__device__ __forceinline__ void prev_sums(const Sync &sy, int n_state, double (&sums)[NPART], int sj = 0)
 {
-    reduce_prev<NT>(sy.pin, sy.pin_n >= 0 ? sy.pin_n : n_state, sums);
+    const int n = sy.pin_n >= 0 ? sy.pin_n : n_state;
+    reduce_prev<NT>(sy.pin + (long long)sj * n * NPART, n, sums);
 }
 
 // ---- scalar logic of Alg. 1 ------------------------------------------------------------
@@ -456,7 +472,8 @@ struct IterStart {
     int status, zero_x;
 };
 
-__device__ __forceinline__ IterStart iter_start(const CgState *st, int i, const double *s)
+// st: the system's state (delta, bb, thresh, rtol2); max_iter: the loop option
+__device__ __forceinline__ IterStart iter_start(const CgState *st, int i, const double *s, int max_iter)
 {
     IterStart r;
     r.delta = s[0];
@@ -475,8 +492,8 @@ __device__ __forceinline__ IterStart iter_start(const CgState *st, int i, const 
     if (!isfinite(s[0]) || !isfinite(s[1]) || !isfinite(r.bb)) { r.status = ST_BREAKDOWN; r.go = false; return r; }
     if (i == 0 && r.bb == 0.0) { r.zero_x = 1; r.go = false; return r; }   // b_F = 0 -> x_F = 0
     const bool need = r.rr > r.thresh;                                      // R4: ||r|| > tol ||b||
-    r.go = need && i < st->max_iter;
-    if (need && i >= st->max_iter) r.status = ST_NOCONV;
+    r.go = need && i < max_iter;
+    if (need && i >= max_iter) r.status = ST_NOCONV;
     return r;
 }
 
@@ -523,22 +540,27 @@ enum {
 // (i > 0, i mod replace_every == 0, Alg. 1 line 10) only x is updated: the residual kernel
 // (EP_RESID) follows.  Also run inside kernel A's launch (FL_FUSEB) after a grid barrier.
 
-// Kernel B's work of iteration `it` on blocks blk of nblk: alpha = delta / d^T q (Alg. 1
-// line 8); x += alpha d; r -= alpha q; s = P^{-1} r; partials r^T s, r^T r (lines 9-16).
+// Kernel B's work of iteration `it` for one system (node slots [base, base + a.sysn)) on its
+// blocks blk of nblk: alpha = delta / d^T q (Alg. 1 line 8); x += alpha d; r -= alpha q;
+// s = P^{-1} r; partials r^T s, r^T r (lines 9-16), stored at partial slot pblk.  sst: the
+// system's state; one_sys: the context has one system (its kernels drive the loop handles
+// directly); glob: also do the loop duties (fused A+B launch, one system).
 // FUSED: d and q were written by other CTAs of the same launch before a grid barrier, so they
 // are read through L2 (ld.cg), never through the non-coherent read-only path.
 template <int NT, class Real, bool FUSED>
-__device__ __forceinline__ void cg_b_work(const BArgs &a, int blk, int nblk, int tid, int it, int re, int step,
-                                          double delta, double dq)
+__device__ __forceinline__ void cg_b_work(const BArgs &a, CgState *sst, bool one_sys, long long base, int blk,
+                                          int nblk, int pblk, int tid, int it, int re, int step, double delta,
+                                          double dq, bool glob)
 {
-    CgState *st = a.sy.st;
     if (!(dq > 0.0) || !isfinite(dq) || !isfinite(delta)) {           // breakdown
         if (blk == 0 && tid == 0) {
-            st->status = ST_BREAKDOWN;
-            st->active = 0;
-            st->iter = it;
-            set_while(a.sy, 0);
-            set_if(a.sy, 0);
+            sst->status = ST_BREAKDOWN;
+            sst->active = 0;
+            sst->iter = it;
+            if (one_sys) {
+                set_while(a.sy, 0);
+                set_if(a.sy, 0);
+            }
         }
         return;
     }
@@ -553,20 +575,21 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, int blk, int nblk, int
     const Real *dvec = reinterpret_cast<const Real *>(a.dbuf[(it & 1) ^ 1]);
     Real *xvec = reinterpret_cast<Real *>(a.rot[0] ? a.rot[(step + 1) % 3] : a.x);
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
-    // BP aligned pairs per thread per sweep (n is even: even row pitch), loads issued up front;
-    // a pair never straddles the owned range (planes hold an even number of slots)
+    const long long end = base + a.sysn;
+    // BP aligned pairs per thread per sweep (slot counts are even: even row pitch), loads issued
+    // up front; a pair never straddles the owned range (planes hold an even number of slots)
 #ifndef HF_B_BP
 #define HF_B_BP 2
 #endif
     constexpr int BP = HF_B_BP;
     const long long sweep = (long long)nblk * NT * BP * 2;
-    for (long long base = ((long long)blk * NT * BP + tid) * 2; base < a.n; base += sweep) {
+    for (long long i0 = base + ((long long)blk * NT * BP + tid) * 2; i0 < end; i0 += sweep) {
         V2 xv[BP], dv[BP], rv[BP], qv[BP], iv[BP];
         bool in[BP], own[BP];
 #pragma unroll
         for (int k = 0; k < BP; k++) {
-            const long long i = base + (long long)k * NT * 2;
-            in[k] = i < a.n;
+            const long long i = i0 + (long long)k * NT * 2;
+            in[k] = i < end;
             own[k] = in[k] && !replace && i >= a.own0 && i < a.own1;
             if (in[k]) {
                 xv[k] = *reinterpret_cast<const V2 *>(xvec + i);
@@ -580,7 +603,7 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, int blk, int nblk, int
         }
 #pragma unroll
         for (int k = 0; k < BP; k++) {
-            const long long i = base + (long long)k * NT * 2;
+            const long long i = i0 + (long long)k * NT * 2;
             if (in[k]) {                        // x += alpha d  (line 9)
                 xv[k].x = fma(alr, dv[k].x, xv[k].x);
                 xv[k].y = fma(alr, dv[k].y, xv[k].y);
@@ -602,14 +625,17 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, int blk, int nblk, int
         }
     }
     pdl_trigger();
-    if (!replace) block_reduce_store<NT>(acc, a.sy.pout, blk);
+    if (!replace) block_reduce_store<NT>(acc, a.sy.pout, pblk);
     if (blk == 0 && tid == 0) {
-        st->b_iter = it + 1;
-        st->replace = replace;
-        st->alpha = alpha;
-        st->dq = dq;
-        if (!replace) st->npart_b = nblk;
-        set_if(a.sy, replace ? 1 : 0);
+        sst->alpha = alpha;
+        sst->dq = dq;
+        if (glob) {
+            CgState *st0 = a.sy.st;
+            st0->b_iter = it + 1;
+            st0->replace = replace;
+            if (!replace) st0->npart_b = nblk;
+            set_if(a.sy, replace ? 1 : 0);
+        }
     }
 }
 
@@ -617,20 +643,38 @@ template <int NT, class Real>
 __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
 {
     const int tid = threadIdx.x;
-    const int blk = blockIdx.x;
-    if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
+    const int nsys = a.sy.nsys > 0 ? a.sy.nsys : 1;
+    const int bps = (int)gridDim.x / nsys;                // blocks per system (contiguous)
+    const int sj = (int)blockIdx.x / bps, blk = (int)blockIdx.x - sj * bps;
+    if (blockIdx.x == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
     pdl_wait();
-    CgState *st = a.sy.st;
-    const CgHdr hd = load_hdr(st);
-    if (hd.h0.x >= 0 || !hd.h0.y) {               // failed run / converged: leave the loop
-        if (blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
-        return;
-    }
+    CgState *st0 = a.sy.st, *sst = st0 + sj;
+    const CgHdr hd = load_hdr(st0);
+    const CgHdr hs = sj ? load_hdr(sst) : hd;
     const int it = hd.h1.x, re = hd.h1.y, step = hd.h0.w;
-    // alpha_i = delta_i / (d_i^T q_i)  (Alg. 1 line 8) from kernel A's partials
+    if (blockIdx.x == 0) {
+        // loop duties (shared by the systems): leave the loop when no system iterates any more,
+        // else advance the iteration and arm the replacement IF node (Alg. 1 line 10, R6)
+        bool mine = tid == 0 && hd.h0.x < 0 && hd.h0.y;
+        for (int j = 1 + tid; j < nsys; j += NT) mine |= st0[j].first_failed < 0 && st0[j].active;
+        const bool any = nsys == 1 ? (hd.h0.x < 0 && hd.h0.y) : __syncthreads_or(mine);
+        if (tid == 0 && !any) {
+            set_while(a.sy, 0);
+            set_if(a.sy, 0);
+        } else if (tid == 0) {
+            const bool replace = it > 0 && re > 0 && (it % re) == 0;
+            st0->b_iter = it + 1;
+            st0->replace = replace;
+            if (!replace) st0->npart_b = bps;
+            set_if(a.sy, replace ? 1 : 0);
+        }
+    }
+    if (hs.h0.x >= 0 || !hs.h0.y) return;          // this system failed earlier / has converged
+    // alpha_i = delta_i / (d_i^T q_i)  (Alg. 1 line 8) from kernel A's partials of this system
     double ps[NPART];
-    prev_sums<NT>(a.sy, hd.h2.x, ps);
-    cg_b_work<NT, Real, false>(a, blk, (int)gridDim.x, tid, it, re, step, st->delta[it & 1], ps[0]);
+    prev_sums<NT>(a.sy, hd.h2.x, ps, sj);
+    cg_b_work<NT, Real, false>(a, sst, nsys == 1, (long long)sj * a.sysn, blk, bps, (int)blockIdx.x, tid, it, re,
+                               step, sst->delta[it & 1], ps[0], false);
 }
 
 // Grid-wide barrier of a launch whose CTAs are all co-resident (checked on the host with the
@@ -697,6 +741,14 @@ k_stencil(const __grid_constant__ StencilArgs a)
     const int tid = lane + 32 * w;
     const int blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblocks = gridDim.x * gridDim.y * gridDim.z;
+    // stacked systems (a13): blockIdx.z = system * chunks-per-system + chunk, so the blocks of
+    // system sj are contiguous (its partial sums too) and each z-chunk stays inside its system
+    const int nsys = a.sy.nsys > 0 ? a.sy.nsys : 1;
+    const int nchs = (int)gridDim.z / nsys;
+    const int sj = (int)blockIdx.z / nchs;
+    const int bps = nblocks / nsys;                        // blocks (partials) per system
+    const bool sys_lead = blk == sj * bps && tid == 0;     // writes the system's scalars
+    const bool glob_lead = blk == 0 && tid == 0;           // writes the shared loop fields
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
     // warm the SM's descriptor cache for every map this launch may use (which node maps it
     // uses depends on the state header, read next): one prefetch per lane of warp 0
@@ -728,15 +780,25 @@ k_stencil(const __grid_constant__ StencilArgs a)
     int map0 = MAP_U0, map1 = MAP_U0 + 2, first = a.first;
     int it_i = 0;                                            // PCG iteration (kernel A)
     Real *cstore = reinterpret_cast<Real *>((EP == EP_CGA) ? a.dbuf[1] : a.xout);   // centre-value store target
-    int npart_b = 0;
+    int npart_b = 0, max_iter = 0;
+    CgState *const sst = a.sy.st ? a.sy.st + sj : nullptr;   // this block's system
     if (a.sy.st) {
         const CgHdr hd = load_hdr(a.sy.st);
-        const int first_failed = hd.h0.x, active = hd.h0.y, b_iter = hd.h0.z, step = hd.h0.w;
+        const CgHdr hs = sj ? load_hdr(sst) : hd;
+        const int first_failed = hs.h0.x, active = hs.h0.y, b_iter = hd.h0.z, step = hd.h0.w;
         npart_b = hd.h1.w;
+        max_iter = hd.h2.y;
         re_ = hd.h1.y;
         step_ = hd.h0.w;
-        if (first_failed >= 0) {                 // an earlier time step failed: stop the run
-            if (EP == EP_CGA && blk == 0 && tid == 0) { set_while(a.sy, 0); set_if(a.sy, 0); }
+        if (glob_lead) {
+            // shared loop fields, written before any early exit (no block of this kernel reads them)
+            CgState *st0 = a.sy.st;
+            if (EP == EP_CGA) { st0->npart_a = bps; st0->a_iter = b_iter; }
+            else if (EP == EP_RESID_INIT) { st0->npart_b = bps; st0->b_iter = 0; st0->replace = 0; }
+            else if (EP == EP_RESID && hd.h1.z) st0->npart_b = bps;
+        }
+        if (first_failed >= 0) {                 // an earlier time step of this system failed
+            if (EP == EP_CGA && nsys == 1 && sys_lead) { set_while(a.sy, 0); set_if(a.sy, 0); }
             return;
         }
         if (EP == EP_CGA || EP == EP_RESID) {
@@ -782,8 +844,9 @@ k_stencil(const __grid_constant__ StencilArgs a)
     const int kb = (2 * (X0 - 1)) & ~(16 / ES - 1);
     const int koff = 2 * (X0 - 1) - kb;
     const int yb = Y0 - 1 + w * R;
-    const int zb = a.z_out0 + blockIdx.z * a.zchunk;
-    const int ze = min(zb + a.zchunk, a.z_out1);
+    const int zsb = a.z_out0 + sj * a.zper_out;                  // output planes of this system
+    const int zb = zsb + ((int)blockIdx.z - sj * nchs) * a.zchunk;
+    const int ze = min(min(zb + a.zchunk, zsb + a.zper_out), a.z_out1);
     const int nplanes = ze - zb + 2;               // planes zb-1 .. ze
     // rows this thread owns (writes): lane >= 1, inside the grid, not the tile's halo row
     unsigned own = 0;
@@ -837,11 +900,11 @@ k_stencil(const __grid_constant__ StencilArgs a)
     if (EP == EP_CGA) {
         // start of PCG iteration i from the previous kernel's partial sums (overlaps the TMA)
         double ps[NPART];
-        prev_sums<NT>(a.sy, npart_b, ps);
-        const IterStart is = iter_start(a.sy.st, it_i, ps);
+        prev_sums<NT>(a.sy, npart_b, ps, sj);
+        const IterStart is = iter_start(sst, it_i, ps, max_iter);
         if (!is.go) {
-            if (blk == 0 && tid == 0) {
-                CgState *stw = a.sy.st;
+            if (sys_lead) {
+                CgState *stw = sst;
                 stw->active = 0;
                 stw->status = is.status;
                 stw->zero_x = is.zero_x;
@@ -849,8 +912,10 @@ k_stencil(const __grid_constant__ StencilArgs a)
                 stw->rr = is.rr;
                 if (it_i == 0) { stw->bb = is.bb; stw->thresh = is.thresh; }
                 stw->delta[it_i & 1] = is.delta;
-                set_while(a.sy, 0);
-                set_if(a.sy, 0);
+                if (nsys == 1) {                 // one system: its stop ends the loop here
+                    set_while(a.sy, 0);
+                    set_if(a.sy, 0);
+                }
             }
 #ifdef HF_DEBUG_WAIT
             for (int i = 0; i < NS && i < nplanes; i++) mbar_wait_dbg(&bars[i], 0, 1000 + EP * 10 + LD, -1 - i);
@@ -871,10 +936,9 @@ k_stencil(const __grid_constant__ StencilArgs a)
             d[12 + 3 * sl] += 1;
         }
 #endif
-        if (blk == 0 && tid == 0) {
-            CgState *stw = a.sy.st;
+        if (sys_lead) {
+            CgState *stw = sst;
             stw->delta[it_i & 1] = is.delta;
-            stw->a_iter = it_i;
             stw->rr = is.rr;
             if (it_i == 0) { stw->bb = is.bb; stw->thresh = is.thresh; }
         }
@@ -1180,18 +1244,12 @@ k_stencil(const __grid_constant__ StencilArgs a)
     // per-block partial sums for the next kernel: A -> (d^T q); init, RESID -> (r^T s, r^T r, b^T b)
     block_reduce_store<NT>(acc, a.sy.pout, blk);
     HF_TR(6);
-    if (blk == 0 && tid == 0) {
-        CgState *stw = a.sy.st;
-        if (EP == EP_CGA) stw->npart_a = nblocks;
-        else stw->npart_b = nblocks;
-        if (EP == EP_RESID_INIT) {              // a new solve starts: A_0 follows
-            stw->b_iter = 0;
-            stw->active = 1;
-            stw->status = ST_OK;
-            stw->zero_x = 0;
-            stw->replace = 0;
-            stw->iter = 0;
-        }
+    if (EP == EP_RESID_INIT && sys_lead) {      // a new solve of this system starts: A_0 follows
+        CgState *stw = sst;
+        stw->active = 1;
+        stw->status = ST_OK;
+        stw->zero_x = 0;
+        stw->iter = 0;
     }
     if constexpr (EP == EP_CGA && (FL & FL_FUSEB) != 0) {
         // kernel B of the same iteration in the same launch: every CTA's q, d and d^T q partial
@@ -1200,7 +1258,8 @@ k_stencil(const __grid_constant__ StencilArgs a)
         grid_barrier(a.gbar, (unsigned)nblocks, tid);
         double ps[NPART];
         reduce_prev<NT, true>(a.sy.pout, nblocks, ps);
-        cg_b_work<NT, Real, true>(a.fb, blk, nblocks, tid, it_i, re_, step_, delta_i, ps[0]);
+        cg_b_work<NT, Real, true>(a.fb, a.sy.st, true, 0, blk, nblocks, blk, tid, it_i, re_, step_, delta_i, ps[0],
+                                  true);
     }
 }
 
@@ -1545,16 +1604,17 @@ __global__ void k_set_dirichlet(Geom g, void *vp, const void *srcp, unsigned lon
     if (x < g.nx1 && is_dirichlet(g, x, y, z, gv)) v[i] = src ? src[i] : (Real)gv;
 }
 
-// End of one solve / time step: x_F <- 0 if b_F = 0; per-step statistics;
-// snapshot of one plane of x; advance the step counter.  Last block does the bookkeeping.
+// End of one solve / time step: x_F <- 0 if b_F = 0; snapshot of one plane of x
+// (one-system contexts).  Stacked systems: node slot i belongs to system i / sysn.
 struct StepArgs {
     Geom g;
     double *x;
     double *rot[3];         // if rot[0]: x = rot[(step + 1) % 3]
     long long n;
+    long long sysn;         // node slots per stacked system (= n for one system)
     double *snap;           // NULL or nsteps x plane (padded plane layout)
     int snap_plane;         // local plane index, -1 none
-    int *iters_out;         // per-step iteration counts (may be NULL)
+    int *iters_out;         // per-step iteration counts (may be NULL; one-system contexts)
     Sync sy;
 };
 
@@ -1564,17 +1624,22 @@ __global__ void __launch_bounds__(256) k_step_end(const StepArgs a)
     const int tid = threadIdx.x, blk = blockIdx.x;
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
     const CgState *st = a.sy.st;
-    if (st->first_failed >= 0) return;
+    const int nsys = a.sy.nsys > 0 ? a.sy.nsys : 1;
     const int step = st->step;
     Real *xv = reinterpret_cast<Real *>(a.rot[0] ? a.rot[(step + 1) % 3] : a.x);
-    const bool zx = st->zero_x;
-    if (zx) {
+    bool any_zx = false;
+    for (int j = 0; j < nsys; j++) any_zx |= st[j].first_failed < 0 && st[j].zero_x;
+    if (any_zx) {
         for (long long i = (long long)blk * 256 + tid; i < a.n; i += (long long)gridDim.x * 256) {
+            const CgState &sj = st[nsys == 1 ? 0 : (int)(i / a.sysn)];
+            if (sj.first_failed >= 0 || !sj.zero_x) continue;
             const int x = (int)(i % a.g.pitch), y = (int)((i / a.g.pitch) % a.g.ny1), z = (int)(i / a.g.plane);
             double gv;
             if (x < a.g.nx1 && !is_dirichlet(a.g, x, y, z, gv)) xv[i] = Real(0);
         }
     }
+    if (st->first_failed >= 0) return;
+    const bool zx = st->zero_x;
     if (a.snap && a.snap_plane >= 0) {
         const Real *src = xv + (long long)a.snap_plane * a.g.plane;
         Real *dst = reinterpret_cast<Real *>(a.snap) + (long long)step * a.g.plane;
@@ -1590,19 +1655,26 @@ __global__ void __launch_bounds__(256) k_step_end(const StepArgs a)
     }
 }
 
-// Per-step bookkeeping after k_step_end (one thread): iteration statistics, failure, step++.
+// Per-step bookkeeping after k_step_end (thread j: system j): iteration statistics, failure;
+// thread 0 then advances the shared step counter.
 __global__ void k_step_commit(Sync sy, int *iters_out)
 {
-    if (sy.launches) atomicAdd(sy.launches, 1ull);
-    CgState *st = sy.st;
-    if (st->first_failed >= 0) return;
-    const int step = st->step;
-    if (iters_out) iters_out[step] = st->iter;
-    st->total_iters += st->iter;
-    if (st->iter > st->max_iters_step) st->max_iters_step = st->iter;
-    st->steps_done = step + 1;
-    if (st->status != ST_OK) st->first_failed = step;
-    st->step = step + 1;
+    const int j = threadIdx.x;
+    const int nsys = sy.nsys > 0 ? sy.nsys : 1;
+    if (j == 0 && sy.launches) atomicAdd(sy.launches, 1ull);
+    CgState *st0 = sy.st;
+    const int step = st0->step;
+    for (int k = j; k < nsys; k += blockDim.x) {
+        CgState *st = st0 + k;
+        if (st->first_failed >= 0) continue;
+        if (iters_out && nsys == 1) iters_out[step] = st->iter;
+        st->total_iters += st->iter;
+        if (st->iter > st->max_iters_step) st->max_iters_step = st->iter;
+        st->steps_done = step + 1;
+        if (st->status != ST_OK) st->first_failed = step;
+    }
+    __syncthreads();
+    if (j == 0) st0->step = step + 1;
 }
 
 // ---- c lane of the packed (k, c) pairs back to a plain per-element fp64 array ----------------

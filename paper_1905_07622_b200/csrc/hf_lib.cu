@@ -166,9 +166,8 @@ struct Sys {                         // one system's PCG workspace (Table 3 buff
     double *U[3] = {nullptr, nullptr, nullptr};   // time-step ring
     double *b = nullptr, *r = nullptr, *s = nullptr, *q = nullptr, *invd = nullptr;
     double *dbuf[2] = {nullptr, nullptr};
-    bool solo = false;               // batched pool system: one stencil CTA per SM (see simulate_sys)
     Maps maps;                       // TMA maps of U[0..2], dbuf[0..1], s and kc
-    CgState *st = nullptr;           // device
+    CgState *st = nullptr;           // device, one per stacked system (hf_ctx::nsys)
     CgState *st_host = nullptr;      // pinned mirror
     double *partA = nullptr, *partB = nullptr;   // per-block partial sums of A / (init, B, RESID)
     double *sums = nullptr;                      // slab mode: allreduced sums
@@ -217,7 +216,6 @@ struct hf_ctx {
     bool tetv = false;               // tets with per-tet vertex-averaged coefficients (EL_TETV)
     DiagC dg;                        // diagonal entries of K_ref, M_ref per local node
     Sys sys0;
-    std::vector<std::unique_ptr<Sys>> pool;
     unsigned long long *launches = nullptr;
     std::vector<void *> scratch;     // staging buffers (padded node layout unless noted)
     std::vector<size_t> scratch_cap;
@@ -231,7 +229,8 @@ struct hf_ctx {
     int unroll = 0;                  // PCG iterations per WHILE-body launch (0: by grid size, see build_cg_graph)
     int pdl = 1;                     // programmatic A <-> B edges in the loop body (HF_PDL=0 disables)
     int fuse_ab = 0;                 // A and B of an iteration in one launch (HF_FUSE_AB=1)
-    size_t launch_min_smem = 0;      // > 0: stencil launches reserve at least this much smem
+    int nsys = 1;                    // systems stacked along z (batched forward simulations, a13)
+    int sys_planes = 0;              // local node planes per system (= nzl for one system)
     int rank = 0, nranks = 1;
     Comm *comm = nullptr;
     bool step_flush = false;
@@ -426,6 +425,7 @@ static Geom make_geom(const hf_ctx *c)
     g.ny = (int)c->g.ne[1];
     g.kpitch = c->kpitch;
     g.dbits = c->dbits;
+    g.zper = c->nz1g / c->nsys;
     for (int f = 0; f < 6; f++) g.gval[f] = c->gval[f];
     return g;
 }
@@ -731,20 +731,25 @@ static int default_tile_r(const hf_ctx *c, int elem)
 
 // grid of the stencil over output planes [z0, z1): one (x, y) tile column per CTA, z split
 // into chunks so that the grid fills the resident slots (occupancy x SMs) once.
-static void stencil_grid(const hf_ctx *c, int z0, int z1, dim3 *grid, int *zchunk)
+// Stacked systems (nsys > 1): every system's planes get their own chunks (blockIdx.z = system *
+// chunks + chunk), so no CTA straddles two systems and the partial sums stay per system; *zper
+// receives the output planes per system.
+static void stencil_grid(const hf_ctx *c, int z0, int z1, dim3 *grid, int *zchunk, int *zper)
 {
     const int tx = (c->nx1 + TILE_X - 1) / TILE_X;
     const int ty = (c->ny1 + rows_per_tile(c->tileR) - 1) / rows_per_tile(c->tileR);
-    const int planes = std::max(1, z1 - z0);
+    const int ns = c->nsys;
+    const int planes = ns > 1 ? c->sys_planes : std::max(1, z1 - z0);
     const long long cols = (long long)tx * ty;
-    const long long slots = (long long)c->nsm * (c->launch_min_smem ? 1 : c->occ);
-    long long nch = std::max(1LL, slots / cols);
+    const long long slots = (long long)c->nsm * c->occ;
+    long long nch = std::max(1LL, slots / (cols * ns));
     int chunk = (int)std::max(1LL, ((long long)planes + nch - 1) / nch);
     if (c->zchunk_env > 0) chunk = c->zchunk_env;
     chunk = std::min(chunk, planes);
     nch = (planes + chunk - 1) / chunk;
-    *grid = dim3(tx, ty, (unsigned)nch);
+    *grid = dim3(tx, ty, (unsigned)(nch * ns));
     *zchunk = chunk;
+    *zper = planes;
 }
 
 // which = 0: consumes kernel A's partials, 1: consumes init/B/RESID partials, -1: none.
@@ -756,6 +761,7 @@ static Sync make_sync(hf_ctx *c, Sys &s, int consumes = -1, int produces = -1)
     std::memset(&y, 0, sizeof(y));
     y.st = s.st;
     y.launches = c->launches;
+    y.nsys = c->nsys;
     if (consumes >= 0) {
         if (c->comm) { y.pin = s.sums; y.pin_n = 1; }
         else { y.pin = consumes == 0 ? s.partA : s.partB; y.pin_n = -1; }
@@ -865,12 +871,12 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
     }
     StencilFn f = stencil_fn(c->tileR, LD, EP, FL, el, c->es);
     if (!f.fn) return fail(HF_E_ARG, "internal: no stencil instantiation");
-    f.smem = std::max(f.smem, c->launch_min_smem);
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
     dim3 grid;
-    int chunk;
-    stencil_grid(c, a.z_out0, a.z_out1, &grid, &chunk);
+    int chunk, zper;
+    stencil_grid(c, a.z_out0, a.z_out1, &grid, &chunk, &zper);
     a.zchunk = chunk;
+    a.zper_out = zper;
     Launch L;
     L.fn = f.fn;
     L.grid = grid;
@@ -890,8 +896,10 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
 // 25.9 / 27.2 us for 4 / 3 / 2 / 6 / 8 per SM; 4 pairs per thread per sweep instead of 2: no gain).
 static int b_blocks(const hf_ctx *c)
 {
-    static const int per_sm = getenv("HF_B_PER_SM") ? std::max(1, atoi(getenv("HF_B_PER_SM"))) : 3;
-    return std::max(1, std::min((int)((c->nloc + 1023) / 1024), c->nsm * per_sm));
+    const int per_sm = 3;
+    const long long sysn = c->nloc / c->nsys;
+    const int bps = std::max(1, std::min((int)((sysn + 1023) / 1024), c->nsm * per_sm / c->nsys));
+    return bps * c->nsys;                  // bps blocks per system, contiguous
 }
 
 static hf_status run(hf_ctx *c, const Launch &L, cudaStream_t s)
@@ -972,16 +980,16 @@ static hf_status sys_alloc(hf_ctx *c, Sys &s, cudaStream_t stream)
     }
     CUCK(cudaMalloc(&s.kc, (size_t)c->kc_elems * 2 * c->es));
     CUCK(cudaMemsetAsync(s.kc, 0, (size_t)c->kc_elems * 2 * c->es, stream));
-    CUCK(cudaMalloc(&s.st, sizeof(CgState)));
-    CUCK(cudaMallocHost(&s.st_host, sizeof(CgState)));
+    CUCK(cudaMalloc(&s.st, c->nsys * sizeof(CgState)));
+    CUCK(cudaMallocHost(&s.st_host, c->nsys * sizeof(CgState)));
     CUCK(cudaMalloc(&s.partA, (size_t)c->max_blocks * NPART * sizeof(double)));
     CUCK(cudaMalloc(&s.partB, (size_t)c->max_blocks * NPART * sizeof(double)));
     CUCK(cudaMalloc(&s.sums, NPART * sizeof(double)));
     CUCK(cudaMalloc(&s.gbar, sizeof(unsigned long long)));
     CUCK(cudaMemsetAsync(s.gbar, 0, sizeof(unsigned long long), stream));
-    std::memset(s.st_host, 0, sizeof(CgState));
-    s.st_host->first_failed = -1;
-    CUCK(cudaMemcpyAsync(s.st, s.st_host, sizeof(CgState), cudaMemcpyHostToDevice, stream));
+    std::memset(s.st_host, 0, c->nsys * sizeof(CgState));
+    for (int j = 0; j < c->nsys; j++) s.st_host[j].first_failed = -1;
+    CUCK(cudaMemcpyAsync(s.st, s.st_host, c->nsys * sizeof(CgState), cudaMemcpyHostToDevice, stream));
     s.stream = stream;
     HFCK(sys_maps(c, s));
     CUCK(cudaStreamSynchronize(stream));
@@ -1017,7 +1025,7 @@ static void set_layout(hf_ctx *c)
     c->kc_elems = (long long)c->kpitch * c->g.ne[1] * (c->nzl + 1);
 }
 
-static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream, int rank, int nranks)
+static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream, int rank, int nranks, int nsys = 1)
 {
     for (int d = 0; d < 3; d++)
         if (g->ne[d] < 1 || !(g->h[d] > 0.0)) return fail(HF_E_ARG, "grid: ne must be >= 1 and h > 0");
@@ -1062,6 +1070,9 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     c->nzl = ghi - glo;
     c->own_lo = (int)lo - glo;
     c->own_hi = (int)hi - glo;
+    c->nsys = std::max(1, nsys);
+    if (c->nz1g % c->nsys != 0 || (c->nsys > 1 && nranks > 1)) return fail(HF_E_ARG, "internal: bad system stack");
+    c->sys_planes = c->nzl / c->nsys;
     set_layout(c);
     const double hx = g->h[0], hy = g->h[1], hz = g->h[2];
     for (int l = 0; l < 8; l++) {     // Q1: the same for every local node
@@ -1109,10 +1120,7 @@ static void ctx_free(hf_ctx *c)
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    for (auto &p : c->pool) if (p->stream) cudaStreamSynchronize(p->stream);
     sys_free(c->sys0);
-    for (auto &p : c->pool) sys_free(*p);
-    c->pool.clear();
     for (void *p : c->scratch) cudaFree(p);
     cudaFree(c->launches);
     cudaFree(c->flush);
@@ -1204,6 +1212,7 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
     b.r = s.r;
     b.s = s.s;
     b.n = c->nloc;
+    b.sysn = c->nloc / c->nsys;
     b.own0 = (long long)c->own_lo * c->plane;
     b.own1 = (long long)c->own_hi * c->plane;
     if (rot) for (int i = 0; i < 3; i++) b.rot[i] = s.U[i];
@@ -1218,7 +1227,7 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
     // exchange and allreduce sit between A and B).  Its grid barrier needs every CTA resident
     // at once: used only if the occupancy API says the whole grid fits.
     L->has_ab = false;
-    if (c->fuse_ab && !c->comm && &s == &c->sys0) {
+    if (c->fuse_ab && !c->comm && c->nsys == 1) {
         StencilArgs f = a;
         f.fb = b;
         f.gbar = s.gbar;
@@ -1255,7 +1264,7 @@ static hf_status comm_after(hf_ctx *c, Sys &s, int which, bool exch)
 
 static hf_status read_state(hf_ctx *c, Sys &s)
 {
-    CUCK(cudaMemcpyAsync(s.st_host, s.st, sizeof(CgState), cudaMemcpyDeviceToHost, s.stream));
+    CUCK(cudaMemcpyAsync(s.st_host, s.st, c->nsys * sizeof(CgState), cudaMemcpyDeviceToHost, s.stream));
     CUCK(cudaStreamSynchronize(s.stream));
     return HF_OK;
 }
@@ -1273,13 +1282,15 @@ static hf_status set_solver_opts(hf_ctx *c, Sys &s, const hf_cg_opts &d0)
     const hf_cg_opts d = resolved(c, d0);
     if (!(d.rtol >= 0.0) || d.max_iter < 0) return fail(HF_E_ARG, "bad hf_cg_opts");
     CUCK(cudaStreamSynchronize(s.stream));     // the pinned image may still be in flight
-    CgState &h = *s.st_host;
-    std::memset(&h, 0, sizeof(h));
-    h.rtol2 = d.rtol * d.rtol;
-    h.max_iter = d.max_iter;
-    h.replace_every = d.replace_every;
-    h.first_failed = -1;
-    CUCK(cudaMemcpyAsync(s.st, s.st_host, sizeof(CgState), cudaMemcpyHostToDevice, s.stream));
+    for (int j = 0; j < c->nsys; j++) {       // every system: its own scalars, the same options
+        CgState &h = s.st_host[j];
+        std::memset(&h, 0, sizeof(h));
+        h.rtol2 = d.rtol * d.rtol;
+        h.max_iter = d.max_iter;
+        h.replace_every = d.replace_every;
+        h.first_failed = -1;
+    }
+    CUCK(cudaMemcpyAsync(s.st, s.st_host, c->nsys * sizeof(CgState), cudaMemcpyHostToDevice, s.stream));
     return HF_OK;
 }
 
@@ -1291,6 +1302,7 @@ static StepArgs step_args(hf_ctx *c, Sys &s, double *x, double *snapdev, int sna
     a.x = x;
     if (!x) for (int i = 0; i < 3; i++) a.rot[i] = s.U[i];
     a.n = c->nloc;
+    a.sysn = c->nloc / c->nsys;
     a.snap = snapdev;
     a.snap_plane = snap_local;
     a.iters_out = s.iters;
@@ -1313,7 +1325,7 @@ static std::vector<Launch> step_launches(hf_ctx *c, const StepArgs &a, bool comm
         Launch C;
         C.fn = (const void *)k_step_commit;
         C.grid = dim3(1);
-        C.block = dim3(1);
+        C.block = dim3(std::min(256, ((c->nsys + 31) / 32) * 32));
         C.add(a.sy);
         C.add(a.iters_out);
         C.cls = 4;
@@ -1407,8 +1419,6 @@ static hf_status host_cg_loop(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, in
 static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init, CgLaunches L, std::vector<Launch> post,
                                 int replace_every, cudaGraph_t *out, bool pdl_ok = true)
 {
-    // programmatic edges only for the context's own system: batched pool systems run graphs on
-    // concurrent streams, where the TMA issue of DESIGN §8 was seen; they keep full serialisation
     const bool pdl = c->pdl && pdl_ok;
     cudaGraph_t g;
     CUCK(cudaGraphCreate(&g, 0));
@@ -1560,7 +1570,6 @@ hf_status hf_set_coefficients(hf_ctx *c, const double *k, const double *cc)
     if (c->tetv) {                              // back to one coefficient per element
         c->tetv = false;
         c->sys0.key_valid = false;
-        for (auto &p : c->pool) p->key_valid = false;
     }
     if (c->pal_on) {                            // back to (k, c) pairs from material ids
         c->pal_on = false;
@@ -1627,7 +1636,6 @@ hf_status hf_set_material_ids(hf_ctx *c, const uint8_t *ids, int32_t nmat, const
     c->tetv = false;
     HFCK(sys_maps(c, c->sys0));
     c->sys0.key_valid = false;
-    for (auto &p : c->pool) p->key_valid = false;
     c->coef_set = true;
     c->ab_ready = false;
     return HF_OK;
@@ -1667,7 +1675,6 @@ hf_status hf_set_vertex_coefficients(hf_ctx *c, const double *k, const double *c
     CUCK(cudaStreamSynchronize(c->stream));
     c->tetv = true;
     s.key_valid = false;
-    for (auto &p : c->pool) p->key_valid = false;
     c->coef_set = true;
     c->ab_ready = false;
     return HF_OK;
@@ -1680,7 +1687,6 @@ hf_status hf_set_dirichlet_faces(hf_ctx *c, uint32_t bits, const double values[6
     for (int f = 0; f < 6; f++) c->gval[f] = values ? values[f] : 0.0;
     drop_stacks(c);
     c->sys0.key_valid = false;
-    for (auto &p : c->pool) p->key_valid = false;
     return HF_OK;
 }
 
@@ -1940,22 +1946,11 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
 
     const bool use_graph = c->driver == 0 && !c->comm && !c->prof;
     c->last_ms_steps = 0.0;
-    // Batched pool systems run their graphs concurrently on 2 streams.  Measured on B200: when
-    // stencil CTAs of two concurrently running conditional-node graphs share an SM, a TMA stage
-    // occasionally never completes (hang) or faults (tools/stress_batched.sh: R = 2, 2 streams,
-    // 2-6 of 8 runs fail; host-launched kernels, one stream, or one stencil CTA per SM: 0 of 24).
-    // Pool systems therefore reserve more than half an SM's shared memory per stencil CTA.
-    struct SmemGuard {
-        hf_ctx *c;
-        ~SmemGuard() { c->launch_min_smem = 0; }
-    } smem_guard{c};
-    c->launch_min_smem = s.solo && use_graph ? (size_t)116 * 1024 : 0;
     SimKey key;
     std::memset(&key, 0, sizeof(key));
     key.aK = aK; key.aM = aM; key.aKL = aKL; key.aML = aML; key.rtol = o.rtol; key.dt = dt;
     key.max_iter = o.max_iter; key.replace_every = o.replace_every; key.first = first;
     key.snap_plane = snap_local; key.lift = lift; key.F = dF; key.snap = snapdev;
-    key.pad = (int)(c->launch_min_smem >> 10);
     const bool cached = use_graph && s.key_valid && s.key == key && s.gexec;
 
     std::vector<Launch> pre, post;
@@ -2008,7 +2003,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             if (s.gexec) { cudaGraphExecDestroy(s.gexec); s.gexec = nullptr; }
             if (s.graph) { cudaGraphDestroy(s.graph); s.graph = nullptr; }
             s.key_valid = false;
-            HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph, &s == &c->sys0));
+            HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph));
             CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
             s.key = key;
             s.key_valid = true;
@@ -2067,6 +2062,7 @@ static hf_status finish_stats(hf_ctx *c, Sys &s, hf_sim_stats *stats, float ms)
         stats->ms_total = ms;
         stats->ms_steps = c->step_flush ? c->last_ms_steps : ms;
     }
+    if (c->nsys > 1) return HF_OK;             // stacked systems: per-system results (batched_stacked)
     if (h.first_failed >= 0) {
         if (h.status == ST_BREAKDOWN) return fail(HF_E_BREAKDOWN, "hf_simulate: PCG breakdown");
         return fail(HF_E_NOCONV, "hf_simulate: PCG did not converge");
@@ -2122,9 +2118,10 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     hf_status fs = finish_stats(c, s, stats, ms);
-    // the newest iterate sits in U[steps % 3] (or U[(failed+1) % 3])
+    // the newest iterate sits in U[steps % 3] (or U[(failed+1) % 3]); stacked systems: the
+    // converged ones in U[nsteps % 3], a failed system's slice is fetched by batched_stacked
     const CgState &h = *s.st_host;
-    const int last = h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done;
+    const int last = c->nsys > 1 ? nsteps : (h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done);
     HFCK(copy_out(c, u, s.U[last % 3], c->nzl, s.stream));
     if (u_prev && nsteps > 0) HFCK(copy_out(c, u_prev, s.U[(last + 2) % 3], c->nzl, s.stream));
     if (snap && snap_local >= 0) HFCK(copy_out(c, snap, snapdev, nsteps, s.stream));
@@ -2150,14 +2147,16 @@ hf_status hf_simulate_resume(hf_ctx *c, double theta, double dt, int32_t nsteps,
 
 }  // extern "C"
 
-// ---- batched simulations as one block-diagonal system ----------------------------------------
-// G independent systems on the same grid are stacked along z into one grid of G (nz + 1) node
-// planes; the element layer between two systems gets k = c = 0, so the stacked operator is
-// exactly block diagonal (no element couples two systems) and one PCG on the stack solves every
-// system ("rapid successive solutions": the GPU sees G times the parallelism of one 1M-DoF
-// system, which alone is latency-bound).  The stack's stop test ||r|| <= tol ||b|| uses
-// tol = rtol / sqrt(G): since ||r_j|| <= ||r|| and ||b|| <= sqrt(G) max_j ||b_j||, each system then
-// meets rtol up to the ratio max_j ||b_j|| / ||b_j|| (~1 for the corrosion sims).
+// ---- batched simulations: independent systems stacked along z ------------------------------
+// G independent systems on the same grid are stacked along z into one context of G (nz + 1)
+// node planes; the element layer between two systems gets k = c = 0, so no element couples two
+// systems and the stacked operator is exactly block diagonal ("rapid successive solutions":
+// the GPU sees G times the parallelism of one 1M-DoF system, which alone is latency-bound).
+// Each system keeps its own PCG (Alg. 1): its own delta, alpha, beta, ||b_j|| and stop test
+// ||r_j|| <= rtol ||b_j||, its own iteration count and failure status.  Every stencil CTA and
+// every kernel-B block works inside one system and writes that system's partial sums; a system
+// that has converged (or failed) stops while the others iterate on; the loop ends when none
+// iterates.  z-face Dirichlet values apply to each system's own z faces (Geom::zper).
 static hf_status stack_ctx(hf_ctx *c, int G, hf_ctx **out)
 {
     auto it = c->stacks.find(G);
@@ -2165,11 +2164,11 @@ static hf_status stack_ctx(hf_ctx *c, int G, hf_ctx **out)
     hf_grid g2 = c->g;
     g2.ne[2] = (int64_t)G * (c->g.ne[2] + 1) - 1;
     hf_ctx *s = new hf_ctx();
-    hf_status st = ctx_init(s, &g2, c->device, c->stream, 0, 1);
+    hf_status st = ctx_init(s, &g2, c->device, c->stream, 0, 1, G);
     if (st == HF_OK && c->prec != 64) st = hf_set_precision(s, c->prec);
     if (st == HF_OK && c->elem != EL_Q1) st = hf_set_element(s, c->elem);
     if (st != HF_OK) { ctx_free(s); delete s; return st; }
-    s->dbits = c->dbits;            // x / y faces only (callers exclude z-face Dirichlet)
+    s->dbits = c->dbits;
     for (int f = 0; f < 6; f++) s->gval[f] = c->gval[f];
     s->driver = c->driver;
     s->unroll = c->unroll;
@@ -2182,6 +2181,17 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
                                  double *u_prev, int64_t step0, int64_t snap_plane, double *snap,
                                  const hf_cg_opts *opts, hf_sim_stats *stats);
 
+// systems per stack: about 8M stacked nodes (a 1M-DoF system alone is latency-bound, a stack of
+// 8 streams at the HBM roofline), at most 256 (kernel B's loop duties scan the systems with one
+// block) and at most B
+static int stack_group(const hf_ctx *c, int B)
+{
+    const long long nn = (long long)c->nx1 * c->ny1 * c->nz1g;
+    long long G = std::max(1LL, (8LL << 20) / nn);
+    if (const char *e = getenv("HF_BATCH_GROUP")) G = std::max(1, atoi(e));
+    return (int)std::min<long long>(std::min<long long>(G, 256), B);
+}
+
 static hf_status batched_stacked(hf_ctx *c, int32_t B, const double *k_batch, const double *c_batch, double theta,
                                  double dt, int32_t nsteps, const double *F, double *u_batch, int64_t snap_plane,
                                  double *front_out, const hf_cg_opts &o, hf_sim_stats *stats)
@@ -2190,9 +2200,7 @@ static hf_status batched_stacked(hf_ctx *c, int32_t B, const double *k_batch, co
     const size_t ne = nxy * (size_t)c->g.ne[2];
     const size_t pl = (size_t)c->nx1 * c->ny1;
     const size_t nn = pl * (size_t)c->nz1g;             // natural nodes of one system
-    int G = (int)std::max<long long>(2, (8LL << 20) / (long long)nn);   // ~8M stacked nodes
-    if (const char *e = getenv("HF_BATCH_GROUP")) G = std::max(1, atoi(e));
-    G = std::min<int>(G, B);
+    const int G = stack_group(c, B);
     const double *cshared = nullptr;
     if (!c_batch) {                                   // the context's c, unpacked once
         void *p;
@@ -2231,21 +2239,35 @@ static hf_status batched_stacked(hf_ctx *c, int32_t B, const double *k_batch, co
                                  c->stream));
         }
         HFCK(hf_set_coefficients(s, ks, cs));
-        hf_cg_opts o2 = o;
-        o2.rtol = o.rtol / std::sqrt((double)g);
         hf_sim_stats st;
         std::memset(&st, 0, sizeof(st));
-        hf_status rs = simulate_common(s, theta, dt, nsteps, fs, us, nullptr, 0, -1, nullptr, &o2, &st);
+        hf_status rs = simulate_common(s, theta, dt, nsteps, fs, us, nullptr, 0, -1, nullptr, &o, &st);
         if (rs != HF_OK && rs != HF_E_NOCONV && rs != HF_E_BREAKDOWN) return rs;
-        if (rs != HF_OK && first_err == HF_OK) first_err = rs;
+        // per-system results: each system's newest iterate is in U[steps % 3] (all steps done) or
+        // U[(failed + 1) % 3] of its own slice (simulate_common copied the former into us)
+        const CgState *h = s->sys0.st_host;             // read back by simulate_common
         for (int i = 0; i < g; i++) {
             const int j = j0 + i;
-            CUCK(cudaMemcpyAsync(u_batch + (size_t)j * nn, us + (size_t)i * nn, nn * sizeof(double), cudaMemcpyDefault,
-                                 c->stream));
+            const double *src = us + (size_t)i * nn;
+            if (h[i].first_failed >= 0) {
+                // the failed system's slice of U[(failed + 1) % 3] (padded layout of the stack)
+                const double *ring = s->sys0.U[(h[i].first_failed + 1) % 3];
+                HFCK(copy_out(s, us + (size_t)i * nn, eoff(s, ring, (long long)i * s->sys_planes * s->plane),
+                              s->sys_planes, c->stream));
+                if (first_err == HF_OK) first_err = h[i].status == ST_BREAKDOWN ? HF_E_BREAKDOWN : HF_E_NOCONV;
+            }
+            CUCK(cudaMemcpyAsync(u_batch + (size_t)j * nn, src, nn * sizeof(double), cudaMemcpyDefault, c->stream));
             if (front_out)
-                CUCK(cudaMemcpyAsync(front_out + (size_t)j * pl, us + (size_t)i * nn + (size_t)snap_plane * pl,
-                                     pl * sizeof(double), cudaMemcpyDefault, c->stream));
-            if (stats) stats[j] = st;
+                CUCK(cudaMemcpyAsync(front_out + (size_t)j * pl, src + (size_t)snap_plane * pl, pl * sizeof(double),
+                                     cudaMemcpyDefault, c->stream));
+            if (stats) {
+                stats[j].steps_done = h[i].steps_done;
+                stats[j].total_iters = h[i].total_iters;
+                stats[j].max_iters_step = h[i].max_iters_step;
+                stats[j].first_failed_step = h[i].first_failed;
+                stats[j].ms_total = st.ms_total;
+                stats[j].ms_steps = st.ms_steps;
+            }
         }
         CUCK(cudaStreamSynchronize(c->stream));
     }
@@ -2267,95 +2289,11 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
     if (front_out && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "snap_plane");
     HFCK(check_ptrs(c, "hf_simulate_batched", {k_batch, c_batch, F, u_batch, front_out}));
     CUCK(cudaSetDevice(c->device));
+    if (B == 0) return HF_OK;
     hf_cg_opts o = {1e-12, 10000, -1};
     if (opts) o = *opts;
     o = resolved(c, o);
-    {   // one block-diagonal stack per group of systems, unless z faces carry Dirichlet values
-        const char *e = getenv("HF_BATCH_STACK");
-        // measured (C5, 1M DoF per system): stacks of 2 are slower than two concurrent systems,
-        // stacks of 4-8 reach the HBM roofline; B < 4 keeps the per-system pool
-        const bool stack = (B >= 4 || (e && atoi(e) == 1)) && !(c->dbits & 48u) && !(e && atoi(e) == 0);
-        if (stack) return batched_stacked(c, B, k_batch, c_batch, theta, dt, nsteps, F, u_batch, snap_plane, front_out,
-                                          o, stats);
-    }
-    int nslots = 2;
-    if (const char *e = getenv("HF_BATCH_STREAMS")) nslots = std::max(1, atoi(e));
-    nslots = std::min(nslots, std::max(1, (int)B));
-    while ((int)c->pool.size() < nslots) {
-        std::unique_ptr<Sys> p(new Sys());
-        cudaStream_t st;
-        CUCK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        p->own_stream = true;
-        p->solo = true;
-        HFCK(sys_alloc(c, *p, st));
-        c->pool.push_back(std::move(p));
-    }
-    const size_t ne = (size_t)(c->g.ne[0] * c->g.ne[1] * c->g.ne[2]);
-    const size_t nn = (size_t)c->nx1 * c->ny1 * c->nzl;     // user (natural) node count
-    const size_t pl = (size_t)c->nx1 * c->ny1;              // user plane
-    void *fbuf;
-    HFCK(scratch_get(c, 7, (size_t)c->nloc * 8, &fbuf));
-    if (F) HFCK(copy_in(c, (double *)fbuf, F, c->nzl, c->stream));
-    else CUCK(cudaMemsetAsync(fbuf, 0, c->nloc * c->es, c->stream));
-    const bool kdev = is_device_ptr(k_batch);
-    const bool cdev = c_batch && is_device_ptr(c_batch);
-    std::vector<double *> kst(nslots, nullptr), cst(nslots, nullptr);
-    for (int i = 0; i < nslots; i++) {
-        void *p;
-        if (!kdev) { HFCK(scratch_get(c, 20 + i, ne * sizeof(double), &p)); kst[i] = (double *)p; }
-        if (c_batch && !cdev) { HFCK(scratch_get(c, 40 + i, ne * sizeof(double), &p)); cst[i] = (double *)p; }
-    }
-    CUCK(cudaStreamSynchronize(c->stream));
-    hf_status first_err = HF_OK;
-    std::vector<int> done_sys(nslots, -1);
-    auto collect = [&](int slot, int j) -> hf_status {
-        Sys &s = *c->pool[slot];
-        HFCK(read_state(c, s));
-        const CgState &h = *s.st_host;
-        const int last = h.first_failed >= 0 ? h.first_failed + 1 : h.steps_done;
-        HFCK(copy_out(c, u_batch + (size_t)j * nn, s.U[last % 3], c->nzl, s.stream, 34 + slot));
-        if (front_out) {
-            const int sl = (int)(snap_plane - c->zg0);
-            HFCK(copy_out(c, front_out + (size_t)j * pl, eoff(c, s.U[last % 3], (long long)sl * c->plane), 1, s.stream,
-                          38 + slot));
-        }
-        if (stats) {
-            stats[j].steps_done = h.steps_done;
-            stats[j].total_iters = h.total_iters;
-            stats[j].max_iters_step = h.max_iters_step;
-            stats[j].first_failed_step = h.first_failed;
-            stats[j].ms_total = 0;
-            stats[j].ms_steps = 0;
-        }
-        if (h.first_failed >= 0 && first_err == HF_OK)
-            first_err = h.status == ST_BREAKDOWN ? HF_E_BREAKDOWN : HF_E_NOCONV;
-        return HF_OK;
-    };
-    for (int j = 0; j < B; j++) {
-        const int slot = j % nslots;
-        Sys &s = *c->pool[slot];
-        if (done_sys[slot] >= 0) { HFCK(collect(slot, done_sys[slot])); done_sys[slot] = -1; }
-        const double *kj = k_batch + (size_t)j * ne;
-        if (!kdev) { CUCK(cudaMemcpyAsync(kst[slot], kj, ne * sizeof(double), cudaMemcpyHostToDevice, s.stream)); kj = kst[slot]; }
-        if (c_batch) {
-            const double *cj = c_batch + (size_t)j * ne;
-            if (!cdev) { CUCK(cudaMemcpyAsync(cst[slot], cj, ne * sizeof(double), cudaMemcpyHostToDevice, s.stream)); cj = cst[slot]; }
-            HFCK(enqueue_pack(c, s, kj, cj));
-        } else {
-            // shared capacity: k from this system, the c lane copied from the context's pairs
-            HFCK(enqueue_pack(c, s, kj, nullptr));
-            CUCK(cudaMemcpy2DAsync((char *)s.kc + c->es, 2 * c->es, (const char *)c->sys0.kc + c->es, 2 * c->es, c->es,
-                                   (size_t)c->kc_elems, cudaMemcpyDeviceToDevice, s.stream));
-        }
-        HFCK(copy_in(c, s.U[0], u_batch + (size_t)j * nn, c->nzl, s.stream, 42 + slot));
-        HFCK(simulate_sys(c, s, theta, dt, nsteps, (const double *)fbuf, true, -1, nullptr, o));
-        done_sys[slot] = j;
-    }
-    for (int i = 0; i < nslots; i++)
-        if (done_sys[i] >= 0) HFCK(collect(i, done_sys[i]));
-    for (int i = 0; i < nslots; i++) CUCK(cudaStreamSynchronize(c->pool[i]->stream));
-    if (first_err != HF_OK) return fail(first_err, "hf_simulate_batched: a system failed to converge");
-    return HF_OK;
+    return batched_stacked(c, B, k_batch, c_batch, theta, dt, nsteps, F, u_batch, snap_plane, front_out, o, stats);
 }
 
 // ============================================================================================
@@ -2647,10 +2585,7 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
     int want_r = default_tile_r(c, type);
     if (type != EL_DENSE && getenv("HF_TILE_R")) want_r = atoi(getenv("HF_TILE_R")) >= 4 ? 4 : 2;
     CUCK(cudaStreamSynchronize(c->stream));
-    if (want_r != c->tileR) {
-        c->tileR = want_r;
-        for (auto &p : c->pool) HFCK(sys_maps(c, *p));
-    }
+    if (want_r != c->tileR) c->tileR = want_r;
     HFCK(sys_maps(c, c->sys0));              // also selects the material-id map (Q1 only)
     if (type == EL_DENSE) {
         double K[64], M[64];
@@ -2664,7 +2599,6 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
     }
     HFCK(update_occ(c));
     c->sys0.key_valid = false;
-    for (auto &p : c->pool) p->key_valid = false;
     return HF_OK;
 }
 
@@ -2675,10 +2609,7 @@ hf_status hf_set_precision(hf_ctx *c, int32_t bits)
     if (bits == c->prec) return HF_OK;
     CUCK(cudaSetDevice(c->device));
     CUCK(cudaStreamSynchronize(c->stream));
-    for (auto &p : c->pool) if (p->stream) CUCK(cudaStreamSynchronize(p->stream));
     sys_free(c->sys0);
-    for (auto &p : c->pool) sys_free(*p);
-    c->pool.clear();
     drop_stacks(c);
     for (void *p : c->scratch) cudaFree(p);      // layouts change: reallocate (zeroed) on demand
     c->scratch.clear();

@@ -100,8 +100,11 @@ def metropolis_hastings(loglik_batch: Callable[[np.ndarray], np.ndarray], theta0
                         lo: float, hi: float, n_samples: int, burn_in: int, step: float,
                         rng: np.random.Generator) -> MHResult:
     """theta_{i+1} = theta_hat with probability min(1, p(D|theta_hat)/p(D|theta_i)), else theta_i
-    (P:363-364); uniform prior on [lo, hi]: proposals outside are rejected without a
-    forward solve.  loglik_batch evaluates a vector of candidate thetas (one batched GPU call)."""
+    (P:363-364); uniform prior on [lo, hi]: proposals outside are rejected (their
+    likelihood is never used).  loglik_batch evaluates a vector of candidate thetas (one batched
+    GPU call) of a FIXED size, one per chain: an outside proposal is evaluated at its clipped
+    value and discarded, so every forward batch has the same shape (the same stack grouping and
+    reduction order) whatever the number of proposals inside the prior."""
     theta = np.asarray(theta0, dtype=np.float64).copy()
     chains = theta.size
     ll = loglik_batch(theta)
@@ -114,8 +117,8 @@ def metropolis_hastings(loglik_batch: Callable[[np.ndarray], np.ndarray], theta0
         inside = (prop >= lo) & (prop <= hi)
         llp = np.full(chains, -np.inf)
         if inside.any():
-            llp[inside] = loglik_batch(prop[inside])
-            calls += int(inside.sum())
+            llp = np.where(inside, loglik_batch(np.clip(prop, lo, hi)), -np.inf)
+            calls += chains
         logu = np.log(rng.uniform(size=chains))
         take = inside & (logu < llp - ll)
         theta = np.where(take, prop, theta)

@@ -145,7 +145,7 @@ def test_fp32_c3_two_steps():
 
 @pytest.mark.parametrize("B", [3, 5])
 def test_fp32_batched_matches_individual(B):
-    """B = 3: per-system pool; B = 5: block-diagonal stacks (groups of up to 8)."""
+    """B = 3 and B = 5 stacked systems with per-system PCG (groups of up to 8)."""
     g = synth.Grid((12, 10, 9), (0.3, 0.3, 0.2))
     ks = [synth.random_fields(g, seed=40 + j)[0] for j in range(B)]
     _, c = synth.random_fields(g, seed=39)

@@ -331,13 +331,12 @@ def test_resume_equals_one_run():
     assert np.array_equal(N(u1), N(u2))
 
 
-@pytest.mark.parametrize("mode", ["stack", "stack2", "pool"])
-def test_batched_matches_individual(mode, monkeypatch):
-    """Batched sims: the block-diagonal stack (default; groups of HF_BATCH_GROUP systems, the
-    last group smaller) and the per-system pool path (HF_BATCH_STACK=0) against the oracle."""
-    monkeypatch.setenv("HF_BATCH_STACK", "0" if mode == "pool" else "1")
-    if mode == "stack2":
-        monkeypatch.setenv("HF_BATCH_GROUP", "2")
+@pytest.mark.parametrize("group", [None, 2, 1])
+def test_batched_matches_individual(group, monkeypatch):
+    """Batched sims: systems stacked along z with per-system PCG (default group; groups of 2, the
+    last group smaller; one system per group) against the oracle."""
+    if group:
+        monkeypatch.setenv("HF_BATCH_GROUP", str(group))
     g = synth.Grid((12, 10, 9), (0.3, 0.3, 0.2))
     B = 3
     base_k, base_c = synth.random_fields(g, seed=14)
@@ -362,6 +361,58 @@ def test_batched_matches_individual(mode, monkeypatch):
             assert rel(ub[j], uo) <= 1e-10, (shared_c, j)
             assert np.array_equal(front[j], ub[j][: ctx.n_plane])
             assert stats[j]["steps_done"] == 6
+
+
+def test_batched_systems_have_their_own_pcg():
+    """Per-system PCG in a stack (a13; Alg. 1 per solve): one system's load is 1e-3 x the others',
+    another system is insulated with a zero load (b = 0: 0 iterations, x = 0); every system still
+    meets rtol against its own ||b_j||, matches its oracle, and the iteration counts differ."""
+    g = synth.Grid((12, 10, 9), (0.3, 0.3, 0.2))
+    B = 5
+    base_k, base_c = synth.random_fields(g, seed=51)
+    ks = np.stack([base_k * synth.lognormal_perturbation(g.n_elems, seed=60 + j) for j in range(B)])
+    ctx = make_ctx(g, base_k, base_c)
+    # no flux; the systems differ by their initial fields, so b_j = L u0_j: system 1's right-hand
+    # side is 1e-3 x the others', system 3's is zero
+    scale = np.array([1.0, 1e-3, 1.0, 0.0, 1.0])
+    rng = np.random.default_rng(7)
+    u0 = np.stack([scale[j] * rng.standard_normal(g.n_nodes) for j in range(B)])
+    Fz = np.zeros(g.n_nodes)
+    ub = T(u0.ravel())
+    stats = hf.hf_simulate_batched(ctx, B, T(ks.ravel()), None, 0.5, 0.05, 5, T(Fz), ub)
+    ub = N(ub).reshape(B, -1)
+    its = []
+    for j in range(B):
+        o = oracle.Oracle(g, ks[j], base_c)
+        uo, st, it, _ = o.simulate(0.5, 0.05, 5, Fz, u0[j])
+        if scale[j] == 0.0:
+            assert np.all(ub[j] == 0.0) and stats[j]["total_iters"] == 0
+        else:
+            assert rel(ub[j], uo) <= 1e-10, j
+            assert abs(stats[j]["total_iters"] - int(it.sum())) <= 2, (j, stats[j], it)
+        its.append(stats[j]["total_iters"])
+        assert stats[j]["steps_done"] == 5 and stats[j]["first_failed_step"] == -1
+    assert len(set(its)) > 1, its
+
+
+def test_batched_z_face_dirichlet():
+    """Dirichlet values on the z faces apply to each stacked system's own z faces."""
+    g = synth.Grid((8, 7, 6), (0.3, 0.3, 0.2))
+    B = 3
+    base_k, base_c = synth.random_fields(g, seed=71)
+    ks = np.stack([base_k * synth.lognormal_perturbation(g.n_elems, seed=80 + j) for j in range(B)])
+    vals = (0.0, 0.0, 0.0, 0.0, 1.5, -0.5)
+    ctx = make_ctx(g, base_k, base_c)
+    hf.hf_set_dirichlet_faces(ctx, 48, vals)
+    ub = torch.zeros(B * g.n_nodes, dtype=torch.float64, device=DEV)
+    stats = hf.hf_simulate_batched(ctx, B, T(ks.ravel()), None, 0.5, 0.05, 4, None, ub)
+    ub = N(ub).reshape(B, -1)
+    for j in range(B):
+        o = oracle.Oracle(g, ks[j], base_c)
+        o.set_dirichlet(48, vals)
+        uo, st, it, _ = o.simulate(0.5, 0.05, 4, np.zeros(g.n_nodes), np.zeros(g.n_nodes))
+        assert rel(ub[j], uo) <= 1e-10, j
+        assert abs(stats[j]["total_iters"] - int(it.sum())) <= 2
 
 
 def test_batched_follows_operator_setters():
