@@ -8,8 +8,11 @@ of the theta-scheme: RHS apply + PCG solve (Alg. 1) + guess update, all on the d
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N = 1: one GPU, the C3 problem.  N > 1 (torchrun, one process per GPU): the same global C3
-problem split into z-slabs over N GPUs (NCCL ghost planes + allreduce; strong scaling).
+N = 1: one GPU, the C3 problem.  N > 1 (torchrun, one process per GPU; `--gpus N` launches it):
+the same global C3 problem split into z-slabs over N GPUs (strong scaling).  The slabs talk over
+peer memory (CUDA IPC mailboxes over NVLink: the kernels store ghost planes into the neighbours'
+buffers and publish their reduction sums to every rank; the whole solve stays in the step graph);
+`--transport nccl` selects the NCCL send/recv + allreduce baseline instead.
 --impl reference: the CPU oracle (oracle/, plain C, 1 core) on the same workload, a bounded
 sample of steps.  Prints ONE JSON line on rank 0.
 """
@@ -29,6 +32,7 @@ import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
 
+TRANSPORT_NAME = "peer-memory mailboxes over NVLink, in-kernel exchange"
 METRIC = "ms per time step at 1M DOF (C3: 100^3-node heterogeneous cube, CN, Jacobi-PCG rtol 1e-12)"
 UNIT = "ms/step"
 
@@ -40,7 +44,7 @@ def workload_config(p, n_gpus, extra=None):
                     "dt=0.01, rtol=1e-12, guess 2u^n-u^(n-1)",
         "nodes": p.grid.n_nodes,
         "elements": p.grid.n_elems,
-        "parallelism": "single GPU" if n_gpus == 1 else f"z-slabs x{n_gpus} (NCCL ghost planes + allreduce)",
+        "parallelism": "single GPU" if n_gpus == 1 else f"z-slabs x{n_gpus} ({TRANSPORT_NAME})",
         "l2": "flushed (512 MiB memset) before every timed step; within a step the 104 MB working set "
               "stays L2-resident, as in any real run",
     }
@@ -169,10 +173,7 @@ def run_ours(args):
         ctx = hf.hf_create(g, local_rank)
         z0, lp = 0, g.ne[2] + 1
     else:
-        uid = hf.hf_nccl_unique_id() if rank == 0 else bytes(128)
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        ctx = hf.hf_create_slab(g, rank, world, obj[0], transport=0, device=local_rank)
+        ctx = make_slab_ctx(hf, g, rank, world, dist, local_rank, args.transport)
         _, _, lp, z0 = ctx.slab
     set_coef(ctx, kd, cd, idsd)
     F = torch.empty(ctx.n_nodes, dtype=torch.float64, device=dev)
@@ -336,9 +337,11 @@ def run_ours(args):
         # configs[3]), each rank its slab + ghosts, time = max over ranks
         a512 = apply_512_slabs(hf, torch, dev, peak, rank, world, dist)
         c4s = c4_steps(hf, torch, dev, peak, rank=rank, world=world, dist=dist)
+        c5r = c5_batched(hf, torch, dev, world, rank=rank, dist=dist)
         if rank == 0:
             line["apply_512_slabs"] = a512
             line["c4_steps_slabs"] = c4s
+            line["c5_batched_replicas"] = c5r
     if not slab:
         line["c3_other_coef"] = variant_c3(hf, torch, dev, 64, p.rtol, coef="pairs" if use_ids else "ids")
         line["apply_512"] = apply_512(hf, torch, dev, peak)
@@ -351,6 +354,23 @@ def run_ours(args):
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(args)
     return line
+
+
+def make_slab_ctx(hf, g, rank, world, dist, device, transport):
+    """Slab context of this rank: peer memory (IPC handshake over torch.distributed) or NCCL."""
+    if transport == "nccl":
+        uid = hf.hf_nccl_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        return hf.hf_create_slab(g, rank, world, obj[0], transport=hf.TRANSPORT_NCCL, device=device)
+    ctx = hf.hf_create_slab(g, rank, world, None, transport=hf.TRANSPORT_PEER_IPC, device=device)
+
+    def all_gather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+    hf.hf_peer_setup(ctx, all_gather)
+    return ctx
 
 
 def apply_512(hf, torch, dev, peak, prec=64, ids=False):
@@ -383,10 +403,7 @@ def apply_512_slabs(hf, torch, dev, peak, rank, world, dist, _unused=None):
     """512^3 apply on this rank's z-slab (strong scaling of configs[3]); aggregate GB/s from the
     slowest rank.  No exchange is needed: the input vector carries its ghost planes."""
     g = synth.c4_grid(512)
-    uid = hf.hf_nccl_unique_id() if rank == 0 else bytes(128)
-    obj = [uid]
-    dist.broadcast_object_list(obj, src=0)
-    ctx = hf.hf_create_slab(g, rank, world, obj[0], transport=0, device=dev.index)
+    ctx = make_slab_ctx(hf, g, rank, world, dist, dev.index, _TRANSPORT[0])
     lo, hi, lp, z0 = ctx.slab
     gen = torch.Generator(device=dev).manual_seed(0)
     k = torch.rand(g.n_elems, dtype=torch.float64, device=dev, generator=gen) * 121.5 + 1.0
@@ -519,10 +536,7 @@ def c4_steps(hf, torch, dev, peak, steps=2, rank=0, world=1, dist=None):
     if dist is None:
         ctx = hf.hf_create(g, dev.index)
     else:
-        uid = hf.hf_nccl_unique_id() if rank == 0 else bytes(128)
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        ctx = hf.hf_create_slab(g, rank, world, obj[0], transport=0, device=dev.index)
+        ctx = make_slab_ctx(hf, g, rank, world, dist, dev.index, _TRANSPORT[0])
     hf.hf_set_coefficients(ctx, k, c)
     del k, c
     torch.cuda.empty_cache()
@@ -556,11 +570,13 @@ def c4_steps(hf, torch, dev, peak, steps=2, rank=0, world=1, dist=None):
             "fields": "two materials, 20 % oxide i.i.d. per element (device RNG, seed 3)"}
 
 
-def c5_batched(hf, torch, dev, world, nsims=8, nsteps=300, prec=64, rtol=None):
+def c5_batched(hf, torch, dev, world, nsims=8, nsteps=300, prec=64, rtol=None, rank=0, dist=None):
     """C5 (BASELINE configs[4]): corrosion-inverse forward simulations, 99^3 voxels each
     (1M DoF), T_F = 10 s in 300 CN steps, Gaussian beam 10 W sigma 2 mm, per-sim depth and
-    log-normal k perturbation; nsims of them through hf_simulate_batched on this GPU."""
-    probs = [synth.c5(j, nsteps=nsteps) for j in range(nsims)]
+    log-normal k perturbation; nsims of them through hf_simulate_batched on this GPU.  With dist
+    (N ranks): independent replicas, rank r runs sims r*nsims .. (r+1)*nsims-1 (weak scaling, no
+    collective in the data path), time = max over ranks."""
+    probs = [synth.c5(rank * nsims + j, nsteps=nsteps) for j in range(nsims)]
     g = probs[0].grid
     kb = torch.tensor(np.stack([p.k for p in probs]).ravel(), device=dev)
     cb = torch.tensor(np.stack([p.c for p in probs]).ravel(), device=dev)
@@ -578,16 +594,23 @@ def c5_batched(hf, torch, dev, world, nsims=8, nsteps=300, prec=64, rtol=None):
     ub.zero_()
     s = torch.cuda.current_stream(dev)
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
     t0 = time.perf_counter()
     stats = hf.hf_simulate_batched(ctx, nsims, kb, cb, p0.theta, p0.dt, nsteps, F, ub, 0, front,
                                    rtol=rtol if rtol else p0.rtol)
     torch.cuda.synchronize()
     sec = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([sec], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
     its = sum(st["total_iters"] for st in stats)
     del ctx
-    return {"sims": nsims, "steps_per_sim": nsteps, "seconds": sec, "sims_per_s_per_gpu": nsims / sec,
+    return {"sims": nsims * world, "ranks": world, "sims_per_rank": nsims, "steps_per_sim": nsteps, "seconds": sec,
+            "sims_per_s": nsims * world / sec, "sims_per_s_per_gpu": nsims / sec,
             "ms_per_step": sec * 1e3 / (nsims * nsteps), "pcg_iters_per_step": its / (nsims * nsteps),
-            "projected_1000_sims_8_gpus_s": 1000 / (8 * nsims / sec),
+            "scaling": "weak (independent replicas, max over ranks)" if dist is not None else "single GPU",
             "precision": f"fp{prec}", "rtol": rtol if rtol else p0.rtol,
             "path": "systems stacked along z (groups of up to 8), per-system PCG scalars and stop tests",
             "depths_mm": [round(p.extra["depth"], 3) for p in probs],
@@ -658,6 +681,9 @@ def run_reference(args):
             "gpu_launches": 0}
 
 
+_TRANSPORT = ["peer"]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -669,8 +695,14 @@ def main():
                          "(the paper's two-material field, 1 B per element; no faster at C3, whose kernel A "
                          "is latency-bound, but 16 %% faster for the HBM-bound 512^3 apply)")
     ap.add_argument("--force-slab", action="store_true",
-                    help="run the multi-GPU (z-slab, NCCL) code path even on one rank (validation)")
+                    help="run the multi-GPU (z-slab) code path even on one rank (validation)")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="z-slab transport for N > 1: peer-memory mailboxes (default) or NCCL")
     args = ap.parse_args()
+    _TRANSPORT[0] = args.transport
+    global TRANSPORT_NAME
+    if args.transport == "nccl":
+        TRANSPORT_NAME = "NCCL send/recv ghost planes + allreduce, host loop"
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.gpus < 1:

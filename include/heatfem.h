@@ -230,8 +230,13 @@ hf_status hf_simulate_resume(hf_ctx *ctx, double theta, double dt, int32_t nstep
  * paper's "rapid successive solutions").  k_batch: B x n_elements; c_batch: B x n_elements
  * or NULL (= the context's c for every system); F: n_nodes shared load; u_batch: B x n_nodes
  * (in u^0, out u^nsteps); front_out: NULL or B x n_plane receiving plane snap_plane of
- * u^nsteps per system; stats: B entries (may be NULL).  Systems are independent: each has
- * its own PCG scalars and convergence.  Returns the first failing status (others run on). */
+ * u^nsteps per system (a failed system: its last iterate); stats: B entries (may be NULL).
+ * Systems are independent: each has its own PCG (Alg. 1) scalars, its own stop test
+ * ||r_j|| <= rtol ||b_j||, iteration counts and failure status.  Groups of up to ~8M stacked
+ * nodes (at most 256 systems) run as one grid: the systems are stacked along z with a
+ * coefficient-free element layer between them, each kernel block works inside one system and
+ * a converged system stops while the others iterate on.  Dirichlet faces apply per system.
+ * Returns the first failing status (the other systems run on and are returned). */
 hf_status hf_simulate_batched(hf_ctx *ctx, int32_t B, const double *k_batch,
                               const double *c_batch, double theta, double dt, int32_t nsteps,
                               const double *F, double *u_batch, int64_t snap_plane,
@@ -248,13 +253,25 @@ hf_status hf_slab_plan(int64_t nz1, int32_t rank, int32_t nranks, int64_t *z_lo,
  * Loads libnccl.so.2 at run time.  Errors: HF_E_NCCL. */
 hf_status hf_nccl_unique_id(uint8_t id[128]);
 
-/* Slab context of rank `rank` of `nranks` for the GLOBAL grid g.  Vectors passed to a slab
- * context cover the rank's LOCAL planes: owned planes [z_lo, z_hi) plus one ghost plane on
- * each interior side (hf_slab_range).  Ghost entries of outputs are kept consistent by the
- * library; dot products run over owned nodes only.  transport: 0 = NCCL (one process
- * per GPU, id from hf_nccl_unique_id), 1 = in-process (all ranks in one process, one thread
- * each, possibly on one device; `id` must then be the same hf_local_group pointer cast to
- * uint8_t*).  The call blocks until every rank has joined. */
+/* Slab context of rank `rank` of `nranks` for the GLOBAL grid g (z-slabs, the paper's split of
+ * the domain between GPUs generalised to R ranks).  Vectors passed to a slab context
+ * cover the rank's LOCAL planes: owned planes [z_lo, z_hi) plus one ghost plane on each interior
+ * side (hf_slab_range).  Ghost entries of outputs are kept consistent by the library; dot products
+ * run over owned nodes only.  Every rank must make the same sequence of hf_cg /
+ * hf_simulate* calls.  transport:
+ *   0 = NCCL (one process per GPU; id = 128 bytes from hf_nccl_unique_id).  Ghost planes and the
+ *       sums of each reduction go through ncclSend/Recv and ncclAllReduce between the kernels,
+ *       driven by the host loop (the baseline transport).
+ *   1 = peer memory, every rank in THIS process (one host thread per rank, any devices; id = the
+ *       hf_local_group of the ranks cast to uint8_t*).  The call blocks until every rank joined.
+ *   2 = peer memory, one process per rank (id ignored, may be NULL): each rank then calls
+ *       hf_peer_export, all-gathers the blobs (e.g. torch.distributed) and calls hf_peer_connect.
+ * With peer memory (1, 2) the kernels exchange everything themselves (heatfem kernels store the
+ * boundary planes of P^{-1} r into the neighbours' ghost buffers and publish their reduction sums
+ * into every rank's mailbox over NVLink; a consumer kernel waits for every rank's flag): the
+ * whole slab solve runs in the device-side step graph with no host step and no NCCL call.  A
+ * rank that stops making progress makes the others fail (device trap after 30 s) instead of
+ * hanging.  At most 8 ranks (one node).  Errors: HF_E_ARG, HF_E_PARTITION, HF_E_NCCL, HF_E_CUDA. */
 hf_status hf_create_slab(const hf_grid *g, int32_t rank, int32_t nranks, const uint8_t *id,
                          int32_t transport, int device, void *cuda_stream, hf_ctx **out);
 
@@ -262,6 +279,18 @@ hf_status hf_create_slab(const hf_grid *g, int32_t rank, int32_t nranks, const u
 typedef struct hf_local_group hf_local_group;
 hf_status hf_local_group_create(int32_t nranks, hf_local_group **out);
 void hf_local_group_destroy(hf_local_group *grp);
+
+/* Transport 2: this rank's connection blob (its mailbox as a CUDA IPC handle, its GPU's PCI bus
+ * id, its rank).  blob: HF_PEER_BLOB_BYTES bytes, written.  Errors: HF_E_ARG (not a transport-2
+ * context), HF_E_CUDA. */
+#define HF_PEER_BLOB_BYTES 256
+hf_status hf_peer_export(hf_ctx *ctx, uint8_t blob[HF_PEER_BLOB_BYTES]);
+
+/* Transport 2: connect to every rank.  blobs: nranks x HF_PEER_BLOB_BYTES, rank order (the
+ * all-gathered hf_peer_export blobs, this rank's included).  Maps the peers' mailboxes (IPC).
+ * hf_cg / hf_simulate* on a transport-2 context fail with HF_E_STATE before this call.
+ * Errors: HF_E_ARG (blob of another group), HF_E_STATE (connected already), HF_E_CUDA. */
+hf_status hf_peer_connect(hf_ctx *ctx, const uint8_t *blobs);
 
 /* Global node planes [z_lo, z_hi) owned by this context, and the local plane count
  * (owned + ghosts) and the global index of local plane 0. */
@@ -289,7 +318,7 @@ hf_status hf_profile_read(hf_ctx *ctx, double ms[5], int64_t n[5]);
 hf_status hf_time_kernel_a(hf_ctx *ctx, int32_t reps, double *ms_per_launch);
 
 /* Loop driver: 0 = CUDA graph with device-side WHILE loop (default), 1 = host loop.
- * Profiling (hf_profile) and the in-process slab transport always use the host loop. */
+ * Profiling (hf_profile) and the NCCL slab transport always use the host loop. */
 hf_status hf_set_driver(hf_ctx *ctx, int32_t driver);
 
 /* Enqueue a 512 MiB memset on the context stream (evicts the 126 MB L2; bench timing rule). */

@@ -74,6 +74,8 @@ _SIGS = {
     "hf_create_slab": (_i32, [_P(hf_grid), _i32, _i32, _vp, _i32, C.c_int, _vp, _P(_vp)]),
     "hf_local_group_create": (_i32, [_i32, _P(_vp)]),
     "hf_local_group_destroy": (None, [_vp]),
+    "hf_peer_export": (_i32, [_vp, C.c_char_p]),
+    "hf_peer_connect": (_i32, [_vp, C.c_char_p]),
     "hf_slab_range": (_i32, [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)]),
     "hf_get_launch_count": (_i32, [_vp, _P(_i64)]),
     "hf_profile": (_i32, [_vp, _i32]),
@@ -361,12 +363,18 @@ def hf_local_group_destroy(grp):
     _lib.hf_local_group_destroy(grp)
 
 
-def hf_create_slab(grid, rank: int, nranks: int, uid, transport: int = 0, device: int = 0, stream=None) -> Context:
-    """uid: 128 NCCL id bytes (transport 0) or the hf_local_group handle (transport 1)."""
+HF_PEER_BLOB_BYTES = 256
+TRANSPORT_NCCL, TRANSPORT_PEER_LOCAL, TRANSPORT_PEER_IPC = 0, 1, 2
+
+
+def hf_create_slab(grid, rank: int, nranks: int, uid=None, transport: int = TRANSPORT_PEER_IPC, device: int = 0,
+                   stream=None) -> Context:
+    """uid: 128 NCCL id bytes (transport 0), the hf_local_group handle (transport 1), or None
+    (transport 2: then hf_peer_export / all-gather / hf_peer_connect, see hf_peer_setup)."""
     g = make_grid(grid)
     out = C.c_void_p()
     keep = None
-    if transport == 0:
+    if transport == TRANSPORT_NCCL:
         keep = C.create_string_buffer(bytes(uid), 128)
         idp = C.cast(keep, C.c_void_p)
     else:
@@ -378,6 +386,25 @@ def hf_create_slab(grid, rank: int, nranks: int, uid, transport: int = 0, device
     ctx = Context(out.value, g, device, lp.value)
     ctx.slab = (lo.value, hi.value, lp.value, z0.value)
     return ctx
+
+
+def hf_peer_export(ctx: Context) -> bytes:
+    buf = C.create_string_buffer(HF_PEER_BLOB_BYTES)
+    _check(_lib.hf_peer_export(ctx.ptr, buf))
+    return buf.raw
+
+
+def hf_peer_connect(ctx: Context, blobs: Sequence[bytes]):
+    data = b"".join(bytes(b) for b in blobs)
+    if any(len(b) != HF_PEER_BLOB_BYTES for b in blobs):
+        raise HfError(HF_E_ARG, "peer blobs must be HF_PEER_BLOB_BYTES each")
+    _check(_lib.hf_peer_connect(ctx.ptr, data))
+
+
+def hf_peer_setup(ctx: Context, all_gather):
+    """Transport 2 handshake: all_gather(bytes) -> list of every rank's bytes in rank order
+    (e.g. torch.distributed.all_gather_object); marshalling only."""
+    hf_peer_connect(ctx, all_gather(hf_peer_export(ctx)))
 
 
 def hf_slab_range(ctx: Context):

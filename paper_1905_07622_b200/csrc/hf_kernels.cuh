@@ -163,6 +163,39 @@ struct TetVF {
     float m;
 };
 
+// ---- multi-GPU z-slabs over peer memory (the paper's dual-GPU split) ----
+// Every rank owns a mailbox in its device memory; peers write into it over NVLink (CUDA IPC
+// mappings across processes, plain pointers within one).  A kernel that produces PCG partial sums
+// (init, A, B, residual replacement) publishes them itself: each block counts itself done, the
+// last block sums the kernel's per-block partials in a fixed order, stores the NPART sums into
+// slot (seq & 1) of EVERY rank's mailbox and then releases its flag there (= seq).  The kernels
+// that produce s = P^{-1} r also store the first / last owned plane of s straight into the
+// lower / upper neighbour's ghost-plane buffer.  A consumer kernel waits (one thread per CTA,
+// acquire at system scope) until every rank's flag reached its own seq, then adds the ranks'
+// sums in rank order -- bitwise the same on every rank, so every rank takes the same loop
+// decisions.  No host call, no NCCL: the whole slab solve runs in the step graph.
+constexpr int HF_MAX_RANKS = 8;
+
+struct MailHdr {                      // head of a mailbox (device memory of its owner)
+    double sums[2][HF_MAX_RANKS][NPART];      // slot, source rank
+    unsigned long long flags[HF_MAX_RANKS];   // latest seq published by each rank
+    unsigned long long xflags[HF_MAX_RANKS];  // latest one-off exchange sequence of each rank
+    unsigned long long seq, xseq;             // this rank's counters (local use)
+    unsigned int done, xdone;                 // blocks of the running producer that finished
+};
+
+struct PeerSync {                     // device copy per slab context
+    int nranks, rank;
+    MailHdr *mine;                    // this rank's mailbox
+    MailHdr *peer[HF_MAX_RANKS];      // every rank's mailbox (peer[rank] == mine)
+    void *gdst_lo, *gdst_hi;          // neighbour's ghost buffer for my first / last owned plane
+    void *xdst_lo, *xdst_hi;          // neighbour's one-off exchange buffers (2 parity slots each)
+    const void *xsrc_lo, *xsrc_hi;    // my one-off exchange buffers (written by the neighbours)
+    long long lo0, hi0;               // slot offsets of my first / last owned plane
+    long long plane;                  // slots per plane
+    long long xslot;                  // slots per parity slot of an exchange buffer
+};
+
 struct Sync {               // per-system reduction plumbing
     CgState *st;
     const double *pin;      // partial sums of the previous kernel (NPART per block)
@@ -173,15 +206,18 @@ struct Sync {               // per-system reduction plumbing
     int use_handles;        // set the WHILE handle (graph driver)
     int use_if;             // set the IF handle (only where the body has an IF node)
     int nsys;               // systems stacked along z (>= 1); st points at st[0..nsys-1]
+    const PeerSync *peer;   // slab over peer memory: sums come from / go to the mailboxes
 };
 
 struct Maps {               // TMA descriptors (host copy; kernels read a device-memory copy)
     CUtensorMap node[NMAPS];
     CUtensorMap kc;         // fp64 view (2 nx, ny, nzl + 1) of the (k, c) pairs, layer L at z = L + 1
     CUtensorMap kcn;        // EL_TETV: per-node (k, c) pairs, view (2 nx1, ny1, nzl), node layout
+    CUtensorMap ghost;      // slab over peer memory: s ghost planes (lo, hi) written by the neighbours
 };
 constexpr int MAP_KC = NMAPS;       // index of the kc map in a device Maps array
 constexpr int MAP_KCN = NMAPS + 1;  // index of the per-node pair map
+constexpr int MAP_GHOST = NMAPS + 2;   // index of the ghost-plane map
 
 struct BArgs {
     double *x;
@@ -206,6 +242,7 @@ struct StencilArgs {
     double c, s;
     int z_out0, z_out1, zchunk;   // output planes (local) and planes per CTA
     int zper_out;                 // output planes per stacked system (= z_out1 - z_out0 for one)
+    int gz_lo, gz_hi;             // LD_CGD over peer memory: local planes whose s comes from the ghost map
     int zs0, zs1;                 // planes whose centre values are stored
     int dmode;                    // EP_APPLY: 0 none, 1 identity rows, 2 set g on D rows
     int first;                    // LD_X0: step 0 of the run (guess = u^0)
@@ -452,6 +489,145 @@ __device__ __forceinline__ void prev_sums(const Sync &sy, int n_state, double (&
     reduce_prev<NT>(sy.pin + (long long)sj * n * NPART, n, sums);
 }
 
+// ---- peer-memory protocol (see PeerSync) -------------------------------------------------
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// thread-level wait until flags[q] >= k for every rank q in [0, n) (mask: ranks to wait for);
+// a peer that does not arrive within 30 s traps (a dead rank never hangs the GPU)
+__device__ __forceinline__ void peer_spin(const unsigned long long *flags, unsigned mask, unsigned long long k)
+{
+    const unsigned long long t0 = globaltimer();
+    for (int q = 0; mask >> q; q++) {
+        if (!((mask >> q) & 1u)) continue;
+        while (ld_acquire_sys(flags + q) < k) {
+            __nanosleep(64);
+            if (globaltimer() - t0 > 30000000000ull) __trap();
+        }
+    }
+}
+
+// sums of the latest published sequence over every rank, in rank order (consumer side)
+template <int NT>
+__device__ __forceinline__ void peer_sums(const PeerSync *pp, double (&sums)[NPART])
+{
+    __shared__ double ps_sh[NPART];
+    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+    if (tid == 0) {
+        const unsigned long long k = __ldcg(&pp->mine->seq);
+        peer_spin(pp->mine->flags, (1u << pp->nranks) - 1u, k);
+        double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = 0; q < pp->nranks; q++)
+            for (int j = 0; j < NPART; j++) acc[j] += __ldcg(&pp->mine->sums[k & 1][q][j]);
+        for (int j = 0; j < NPART; j++) ps_sh[j] = acc[j];
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // TMA reads of peer-written ghosts
+    }
+    __syncthreads();
+    for (int j = 0; j < NPART; j++) sums[j] = ps_sh[j];
+}
+
+// producer side: after every block stored its partials (and ghost planes), the last block of
+// the kernel publishes the fixed-order sums to every rank
+template <int NT>
+__device__ void peer_publish(const PeerSync *pp, const double *part, int nblk)
+{
+    __shared__ int last_sh;
+    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+    __threadfence_system();               // this thread's remote ghost stores and partials
+    __syncthreads();
+    if (tid == 0) last_sh = atomicAdd(&pp->mine->done, 1u) == (unsigned)nblk - 1u;
+    __syncthreads();
+    if (!last_sh) return;
+    __threadfence();
+    double s[NPART];
+    reduce_prev<NT, true>(part, nblk, s);
+    if (tid == 0) {
+        MailHdr *m = pp->mine;
+        const unsigned long long k = m->seq + 1;
+        m->seq = k;
+        m->done = 0u;
+        for (int q = 0; q < pp->nranks; q++)
+            for (int j = 0; j < NPART; j++) pp->peer[q]->sums[k & 1][pp->rank][j] = s[j];
+        __threadfence_system();
+        for (int q = 0; q < pp->nranks; q++) st_release_sys(&pp->peer[q]->flags[pp->rank], k);
+    }
+}
+
+// my first / last owned plane of s, stored into the neighbours' ghost buffers (slot index i)
+template <class Real>
+__device__ __forceinline__ void peer_ghost(const PeerSync *pp, long long i, Real v)
+{
+    if (pp->gdst_lo && i >= pp->lo0 && i < pp->lo0 + pp->plane) reinterpret_cast<Real *>(pp->gdst_lo)[i - pp->lo0] = v;
+    if (pp->gdst_hi && i >= pp->hi0 && i < pp->hi0 + pp->plane) reinterpret_cast<Real *>(pp->gdst_hi)[i - pp->hi0] = v;
+}
+
+// one-off exchange of a vector's ghost planes (state vectors at the start of a solve): send my
+// boundary planes into the neighbours' exchange buffers, then receive theirs into my ghosts
+template <class Real>
+__global__ void k_xsend(const PeerSync *pp, const void *vp, unsigned long long *launches)
+{
+    const Real *v = reinterpret_cast<const Real *>(vp);
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0 && tid == 0 && launches) atomicAdd(launches, 1ull);
+    const unsigned long long k = __ldcg(&pp->mine->xseq) + 1;   // this exchange's sequence
+    const long long par = (long long)(k & 1) * pp->xslot;
+    for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < pp->plane; i += (long long)gridDim.x * blockDim.x) {
+        if (pp->xdst_lo) reinterpret_cast<Real *>(pp->xdst_lo)[par + i] = v[pp->lo0 + i];
+        if (pp->xdst_hi) reinterpret_cast<Real *>(pp->xdst_hi)[par + i] = v[pp->hi0 + i];
+    }
+    __shared__ int last_sh;
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) last_sh = atomicAdd(&pp->mine->xdone, 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!last_sh || tid != 0) return;
+    MailHdr *m = pp->mine;
+    m->xseq = k;
+    m->xdone = 0u;
+    __threadfence_system();
+    if (pp->rank > 0) st_release_sys(&pp->peer[pp->rank - 1]->xflags[pp->rank], k);
+    if (pp->rank + 1 < pp->nranks) st_release_sys(&pp->peer[pp->rank + 1]->xflags[pp->rank], k);
+}
+
+template <class Real>
+__global__ void k_xrecv(const PeerSync *pp, void *vp, long long ghost_lo, long long ghost_hi, unsigned long long *launches)
+{
+    Real *v = reinterpret_cast<Real *>(vp);
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0 && tid == 0 && launches) atomicAdd(launches, 1ull);
+    const unsigned long long k = __ldcg(&pp->mine->xseq);
+    if (tid == 0) {
+        unsigned mask = 0;
+        if (pp->rank > 0) mask |= 1u << (pp->rank - 1);
+        if (pp->rank + 1 < pp->nranks) mask |= 1u << (pp->rank + 1);
+        peer_spin(pp->mine->xflags, mask, k);
+    }
+    __syncthreads();
+    const long long par = (long long)(k & 1) * pp->xslot;
+    const Real *lo = reinterpret_cast<const Real *>(pp->xsrc_lo), *hi = reinterpret_cast<const Real *>(pp->xsrc_hi);
+    for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < pp->plane; i += (long long)gridDim.x * blockDim.x) {
+        if (ghost_lo >= 0) v[ghost_lo + i] = __ldcg(lo + par + i);
+        if (ghost_hi >= 0) v[ghost_hi + i] = __ldcg(hi + par + i);
+    }
+}
+
 // ---- scalar logic of Alg. 1 ------------------------------------------------------------
 
 __device__ __forceinline__ void set_while(const Sync &sy, int v)
@@ -621,11 +797,16 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, CgState *sst, bool one
                 acc[1] = fma((double)rv[k].y, (double)rv[k].y, acc[1]);
                 *reinterpret_cast<V2 *>(rv_ + i) = rv[k];
                 *reinterpret_cast<V2 *>(sv_ + i) = sv;
+                if (a.sy.peer) {
+                    peer_ghost<Real>(a.sy.peer, i, sv.x);
+                    peer_ghost<Real>(a.sy.peer, i + 1, sv.y);
+                }
             }
         }
     }
     pdl_trigger();
     if (!replace) block_reduce_store<NT>(acc, a.sy.pout, pblk);
+    if (!replace && a.sy.peer) peer_publish<NT>(a.sy.peer, a.sy.pout, nblk);
     if (blk == 0 && tid == 0) {
         sst->alpha = alpha;
         sst->dq = dq;
@@ -672,7 +853,8 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     if (hs.h0.x >= 0 || !hs.h0.y) return;          // this system failed earlier / has converged
     // alpha_i = delta_i / (d_i^T q_i)  (Alg. 1 line 8) from kernel A's partials of this system
     double ps[NPART];
-    prev_sums<NT>(a.sy, hd.h2.x, ps, sj);
+    if (a.sy.peer) peer_sums<NT>(a.sy.peer, ps);
+    else prev_sums<NT>(a.sy, hd.h2.x, ps, sj);
     cg_b_work<NT, Real, false>(a, sst, nsys == 1, (long long)sj * a.sysn, blk, bps, (int)blockIdx.x, tid, it, re,
                                step, sst->delta[it & 1], ps[0], false);
 }
@@ -752,7 +934,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
     // warm the SM's descriptor cache for every map this launch may use (which node maps it
     // uses depends on the state header, read next): one prefetch per lane of warp 0
-    if (w == 0 && lane < NMAPS + 2) prefetch_map(a.tm + lane);
+    if (w == 0 && lane < NMAPS + 3) prefetch_map(a.tm + lane);
     HF_TR(0);
 #ifdef HF_TRACE
     if (EP == EP_CGA && tid == 0 && blk < 4096) {
@@ -860,7 +1042,9 @@ k_stencil(const __grid_constant__ StencilArgs a)
         const int p = zb - 1 + it;
         Real *sb = stage + st * SH::STAGE_DBL;
         mbar_expect_tx(&bars[st], SH::STAGE_BYTES);
-        if (NA >= 1) tma_load_3d(sb, a.tm + map0, xb, Y0 - 1, p, &bars[st]);
+        if (LD == LD_CGD && a.sy.peer && (p == a.gz_lo || p == a.gz_hi))   // s of a neighbour's plane
+            tma_load_3d(sb, a.tm + MAP_GHOST, xb, Y0 - 1, p == a.gz_lo ? 0 : 1, &bars[st]);
+        else if (NA >= 1) tma_load_3d(sb, a.tm + map0, xb, Y0 - 1, p, &bars[st]);
         if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, a.tm + map1, xb, Y0 - 1, p, &bars[st]);
         if (EL == EL_TETV)   // per-node (k, c) pairs of plane p, same rows as the node box
             tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KCN, 2 * xb, Y0 - 1, p, &bars[st]);
@@ -883,6 +1067,12 @@ k_stencil(const __grid_constant__ StencilArgs a)
         }
     }
     __syncthreads();
+    // slab over peer memory: a CTA whose planes include a ghost plane of s waits for the
+    // neighbours' data (and every rank's sums) before its first TMA; the others wait after
+    const PeerSync *const pp = a.sy.peer;
+    double ps_peer[NPART];
+    const bool peer_early = EP == EP_CGA && pp && ((a.gz_lo >= zb - 1 && a.gz_lo <= ze) || (a.gz_hi >= zb - 1 && a.gz_hi <= ze));
+    if (peer_early) peer_sums<NT>(pp, ps_peer);
     if (tid == 0)
         for (int i = 0; i < NS && i < nplanes; i++) issue(i);
     HF_TR(2);
@@ -900,7 +1090,9 @@ k_stencil(const __grid_constant__ StencilArgs a)
     if (EP == EP_CGA) {
         // start of PCG iteration i from the previous kernel's partial sums (overlaps the TMA)
         double ps[NPART];
-        prev_sums<NT>(a.sy, npart_b, ps, sj);
+        if (peer_early) for (int j = 0; j < NPART; j++) ps[j] = ps_peer[j];
+        else if (pp) peer_sums<NT>(pp, ps);
+        else prev_sums<NT>(a.sy, npart_b, ps, sj);
         const IterStart is = iter_start(sst, it_i, ps, max_iter);
         if (!is.go) {
             if (sys_lead) {
@@ -1228,6 +1420,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
                     const Real sv = r * __ldg(invdv + idx);
                     out0[idx] = r;
                     out_s[idx] = sv;
+                    if (pp) peer_ghost<Real>(pp, idx, sv);
                     acc[0] = fma((double)r, (double)sv, acc[0]);
                     acc[1] = fma((double)r, (double)r, acc[1]);
                     if (EP == EP_RESID_INIT && !isd) acc[2] = fma((double)b, (double)b, acc[2]);
@@ -1243,6 +1436,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     HF_TR(5);
     // per-block partial sums for the next kernel: A -> (d^T q); init, RESID -> (r^T s, r^T r, b^T b)
     block_reduce_store<NT>(acc, a.sy.pout, blk);
+    if (pp) peer_publish<NT>(pp, a.sy.pout, nblocks);
     HF_TR(6);
     if (EP == EP_RESID_INIT && sys_lead) {      // a new solve of this system starts: A_0 follows
         CgState *stw = sst;

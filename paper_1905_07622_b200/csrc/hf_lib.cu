@@ -13,6 +13,7 @@
 #include "hf_ablate.cuh"
 
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -86,6 +87,8 @@ typedef ncclResult_t (*Send_t)(const void *, size_t, int, int, ncclComm_t, cudaS
 typedef ncclResult_t (*Recv_t)(void *, size_t, int, int, ncclComm_t, cudaStream_t);
 typedef ncclResult_t (*Group_t)(void);
 typedef const char *(*GetErrorString_t)(ncclResult_t);
+typedef ncclResult_t (*CommGetAsyncError_t)(ncclComm_t, ncclResult_t *);
+typedef ncclResult_t (*CommAbort_t)(ncclComm_t);
 struct Api {
     void *h = nullptr;
     GetUniqueId_t getUniqueId;
@@ -96,6 +99,8 @@ struct Api {
     Recv_t recv;
     Group_t groupStart, groupEnd;
     GetErrorString_t getErrorString;
+    CommGetAsyncError_t commGetAsyncError;
+    CommAbort_t commAbort;
 };
 static Api g_api;
 static std::mutex g_mu;
@@ -118,6 +123,8 @@ static hf_status load()
     SYM(groupStart, "ncclGroupStart", Group_t)
     SYM(groupEnd, "ncclGroupEnd", Group_t)
     SYM(getErrorString, "ncclGetErrorString", GetErrorString_t)
+    SYM(commGetAsyncError, "ncclCommGetAsyncError", CommGetAsyncError_t)
+    SYM(commAbort, "ncclCommAbort", CommAbort_t)
 #undef SYM
     g_api.h = h;
     return HF_OK;
@@ -192,6 +199,18 @@ struct Comm {
     // in-place sum of n doubles (device) across ranks
     virtual hf_status allreduce(hf_ctx *c, Sys &s, double *v, int n) = 0;
     virtual bool graph_capturable() const = 0;
+    // the kernels themselves exchange sums and ghost planes (peer memory): no host step between
+    // kernels, the whole solve can run in the step graph
+    virtual bool in_kernel() const { return false; }
+    virtual const PeerSync *peer_dev() const { return nullptr; }
+    virtual bool ready() const { return true; }
+    // host-side health check while waiting for device work (NCCL: asynchronous errors)
+    virtual hf_status poll() { return HF_OK; }
+    // start of a collective call (simulate / cg), after this rank's host-side setup and before
+    // its first kernel that waits for another rank (ranks sharing one process: a barrier, so
+    // that no rank's allocation -- an implicit device synchronisation -- waits for kernels that
+    // themselves wait for this rank)
+    virtual hf_status enter() { return HF_OK; }
 };
 
 struct hf_ctx {
@@ -233,6 +252,9 @@ struct hf_ctx {
     int sys_planes = 0;              // local node planes per system (= nzl for one system)
     int rank = 0, nranks = 1;
     Comm *comm = nullptr;
+    int nsm_share = 0;               // SMs a stencil grid is sized for (< nsm when ranks share a GPU)
+    void *ghost_buf = nullptr;       // peer transport: the two s ghost planes the neighbours write
+    size_t ghost_pb = 0;             // bytes per plane slot of the mailbox buffers
     bool step_flush = false;
     double last_ms_steps = 0.0;      // per-step event total of the last run (step_flush)
     double last_aK = 0.0;            // operator (aK, 1) of the last time loop (hf_time_kernel_a)
@@ -523,11 +545,13 @@ static void tet_matrices(const double h[3], double K[6][16], double *V)
     }
 }
 
-static hf_status node_map(const hf_ctx *c, const double *p, CUtensorMap *m)
+// node tensor map over nplanes planes of plane_bytes each (default: a local node vector)
+static hf_status node_map(const hf_ctx *c, const double *p, CUtensorMap *m, int nplanes = 0, size_t plane_bytes = 0)
 {
     HFCK(get_encode());
-    const cuuint64_t dims[3] = {(cuuint64_t)c->nx1, (cuuint64_t)c->ny1, (cuuint64_t)c->nzl};
-    const cuuint64_t strides[2] = {(cuuint64_t)c->pitch * c->es, (cuuint64_t)c->plane * c->es};
+    const cuuint64_t dims[3] = {(cuuint64_t)c->nx1, (cuuint64_t)c->ny1, (cuuint64_t)(nplanes ? nplanes : c->nzl)};
+    const cuuint64_t strides[2] = {(cuuint64_t)c->pitch * c->es,
+                                   (cuuint64_t)(plane_bytes ? plane_bytes : (size_t)c->plane * c->es)};
     const cuuint32_t bw = c->es == 8 ? StencilShape<2, 8, LD_RAW, double>::BW : StencilShape<2, 8, LD_RAW, float>::BW;
     const cuuint32_t box[3] = {bw, (cuuint32_t)(NW * c->tileR + 1), 1};
     const cuuint32_t es[3] = {1, 1, 1};
@@ -741,7 +765,7 @@ static void stencil_grid(const hf_ctx *c, int z0, int z1, dim3 *grid, int *zchun
     const int ns = c->nsys;
     const int planes = ns > 1 ? c->sys_planes : std::max(1, z1 - z0);
     const long long cols = (long long)tx * ty;
-    const long long slots = (long long)c->nsm * c->occ;
+    const long long slots = (long long)(c->nsm_share ? c->nsm_share : c->nsm) * c->occ;
     long long nch = std::max(1LL, slots / (cols * ns));
     int chunk = (int)std::max(1LL, ((long long)planes + nch - 1) / nch);
     if (c->zchunk_env > 0) chunk = c->zchunk_env;
@@ -763,10 +787,11 @@ static Sync make_sync(hf_ctx *c, Sys &s, int consumes = -1, int produces = -1)
     y.launches = c->launches;
     y.nsys = c->nsys;
     if (consumes >= 0) {
-        if (c->comm) { y.pin = s.sums; y.pin_n = 1; }
+        if (c->comm && !c->comm->in_kernel()) { y.pin = s.sums; y.pin_n = 1; }
         else { y.pin = consumes == 0 ? s.partA : s.partB; y.pin_n = -1; }
     }
     if (produces >= 0) y.pout = produces == 0 ? s.partA : s.partB;
+    y.peer = c->comm ? c->comm->peer_dev() : nullptr;
     return y;
 }
 
@@ -809,6 +834,7 @@ static StencilArgs base_args(hf_ctx *c, double aK, double aM)
     a.z_out1 = c->own_hi;
     a.zs0 = c->own_lo;
     a.zs1 = c->own_hi;
+    a.gz_lo = a.gz_hi = -1000;
     return a;
 }
 
@@ -898,7 +924,8 @@ static int b_blocks(const hf_ctx *c)
 {
     const int per_sm = 3;
     const long long sysn = c->nloc / c->nsys;
-    const int bps = std::max(1, std::min((int)((sysn + 1023) / 1024), c->nsm * per_sm / c->nsys));
+    const int nsm = c->nsm_share ? c->nsm_share : c->nsm;
+    const int bps = std::max(1, std::min((int)((sysn + 1023) / 1024), nsm * per_sm / c->nsys));
     return bps * c->nsys;                  // bps blocks per system, contiguous
 }
 
@@ -967,6 +994,8 @@ static hf_status sys_maps(hf_ctx *c, Sys &s)
     } else HFCK(kc_map(c, s.kc, &s.maps.kc));
     if (s.kcn) HFCK(kcn_map(c, s.kcn, &s.maps.kcn));
     else s.maps.kcn = s.maps.kc;            // unused unless EL_TETV
+    if (c->ghost_buf) HFCK(node_map(c, (const double *)c->ghost_buf, &s.maps.ghost, 2, c->ghost_pb));
+    else s.maps.ghost = s.maps.node[MAP_S];  // unused without the peer transport
     return HF_OK;
 }
 
@@ -1200,6 +1229,10 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
     a.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
     a.dmode = 1;
     a.sy = make_sync(c, s, 1, 0);
+    if (a.sy.peer) {                               // s of the ghost planes: the neighbours' stores
+        a.gz_lo = c->own_lo > 0 ? c->own_lo - 1 : -1000;
+        a.gz_hi = c->own_hi < c->nzl ? c->own_hi : -1000;
+    }
     HFCK(stencil_launch(c, LD_CGD, EP_CGA, false, s.maps, a, 0, &L->A));
     // kernel B: x += alpha d; r -= alpha q; s = P^{-1} r; r^T s, r^T r -> beta   (lines 9-19)
     BArgs b;
@@ -1252,7 +1285,7 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
 // slab mode, after a producer kernel: local sums -> allreduce -> (ghosts of s for the next apply)
 static hf_status comm_after(hf_ctx *c, Sys &s, int which, bool exch)
 {
-    if (!c->comm) return HF_OK;
+    if (!c->comm || c->comm->in_kernel()) return HF_OK;
     Sync sy = make_sync(c, s);
     sy.pin = which == 0 ? s.partA : s.partB;
     k_localsum<<<1, 256, 0, s.stream>>>(sy, which, s.sums);
@@ -1355,6 +1388,25 @@ static hf_status host_cg_iter(hf_ctx *c, Sys &s, CgLaunches &L, int i, int repla
 // k - 1's copy is waited on, so the stream always holds queued work.  Iterations enqueued after
 // convergence exit at their first instruction (the kernels test `active`); every rank of a slab
 // run enqueues the same sequence (the stop decision comes from allreduced sums).
+// wait for an event of the host loop; slab transports are polled for asynchronous errors, and a
+// wait beyond HF_COMM_TIMEOUT_S (default 120 s) fails instead of hanging on a dead peer
+static hf_status wait_event(hf_ctx *c, cudaEvent_t ev)
+{
+    if (!c->comm) { CUCK(cudaEventSynchronize(ev)); return HF_OK; }
+    const char *e = getenv("HF_COMM_TIMEOUT_S");
+    const double limit = e ? atof(e) : 120.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        cudaError_t q = cudaEventQuery(ev);
+        if (q == cudaSuccess) return HF_OK;
+        if (q != cudaErrorNotReady) CUCK(q);
+        HFCK(c->comm->poll());
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit)
+            return fail(HF_E_NCCL, "slab transport: no progress within HF_COMM_TIMEOUT_S");
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
+
 static hf_status host_cg_loop_pipelined(hf_ctx *c, Sys &s, CgLaunches &L, int max_iter, int replace_every,
                                         int check)
 {
@@ -1376,7 +1428,7 @@ static hf_status host_cg_loop_pipelined(hf_ctx *c, Sys &s, CgLaunches &L, int ma
         const int prev = slot ^ 1;
         if (i > max_iter + 2 * check + 2) break;
         if (pending[prev]) {                      // the batch before this one
-            CUCK(cudaEventSynchronize(s.ev_ring[prev]));
+            HFCK(wait_event(c, s.ev_ring[prev]));
             pending[prev] = false;
             if (!s.st_ring[prev].active) break;
         }
@@ -1855,6 +1907,7 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
 {
     if (!c || !b || !x) return fail(HF_E_ARG, "hf_cg: NULL argument");
     if (!c->coef_set) return fail(HF_E_STATE, "hf_cg: coefficients not set");
+    if (c->comm && !c->comm->ready()) return fail(HF_E_STATE, "hf_cg: peer transport not connected (hf_peer_connect)");
     HFCK(check_ptrs(c, "hf_cg", {b, x}));
     CUCK(cudaSetDevice(c->device));
     Sys &s = c->sys0;
@@ -1869,7 +1922,6 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     CUCK(cudaMemcpyAsync(s.b, db, c->nloc * c->es, cudaMemcpyDeviceToDevice, s.stream));
     HFCK(enqueue_diag(c, s, aK, aM, nullptr, s.invd));
     HFCK(enqueue_set_dirichlet(c, s, dx, s.b));           // x_D = b_D
-    if (c->comm) HFCK(c->comm->exchange(c, s, dx));
     Maps xm = s.maps;
     HFCK(node_map(c, dx, &xm.node[MAP_U0]));
     // init: r = b - A x0; s = P^{-1} r; delta; ||b_F||   (Alg. 1 lines 2-4)
@@ -1887,14 +1939,25 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
     StepArgs sa = step_args(c, s, dx, nullptr, -1);
     sa.iters_out = nullptr;
     std::vector<Launch> post = step_launches(c, sa, false);
-    const bool use_graph = c->driver == 0 && !c->comm && !c->prof;
+    const bool use_graph = c->driver == 0 && (!c->comm || c->comm->in_kernel()) && !c->prof;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
     if (use_graph) {
-        cudaGraph_t g;
         HFCK(build_cg_graph(c, {}, init, L, post, o.replace_every, &g));
-        cudaGraphExec_t ge;
         cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
         if (e != cudaSuccess) { cudaGraphDestroy(g); CUCK(e); }
-        e = cudaGraphLaunch(ge, s.stream);
+    }
+    if (c->comm) {                 // collective part: the iterate's ghost planes, then the solve
+        hf_status cs = c->comm->enter();
+        if (cs == HF_OK) cs = c->comm->exchange(c, s, dx);
+        if (cs != HF_OK) {
+            if (ge) cudaGraphExecDestroy(ge);
+            if (g) cudaGraphDestroy(g);
+            return cs;
+        }
+    }
+    if (use_graph) {
+        cudaError_t e = cudaGraphLaunch(ge, s.stream);
         cudaStreamSynchronize(s.stream);
         cudaGraphExecDestroy(ge);
         cudaGraphDestroy(g);
@@ -1926,6 +1989,7 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
 static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int nsteps, const double *dF,
                               bool first, int snap_local, double *snapdev, const hf_cg_opts &o)
 {
+    if (c->comm && c->step_flush && !c->flush) CUCK(cudaMalloc(&c->flush, 512ull << 20));
     const double aK = theta * dt, aM = 1.0;             // A = M + theta dt K
     c->last_aK = aK;
     const double aKL = -(1.0 - theta) * dt, aML = 1.0;  // L = M - (1-theta) dt K   (R8)
@@ -1942,9 +2006,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     if (!first) HFCK(enqueue_set_dirichlet(c, s, s.U[2], nullptr));
     bool lift = false;
     for (int f = 0; f < 6; f++) if ((c->dbits >> f & 1u) && c->gval[f] != 0.0) lift = true;
-    if (nsteps <= 0) return HF_OK;
-
-    const bool use_graph = c->driver == 0 && !c->comm && !c->prof;
+    const bool use_graph = c->driver == 0 && (!c->comm || c->comm->in_kernel()) && !c->prof;
     c->last_ms_steps = 0.0;
     SimKey key;
     std::memset(&key, 0, sizeof(key));
@@ -1998,16 +2060,24 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
         post = step_launches(c, step_args(c, s, nullptr, snapdev, snap_local), true);
     }
 
+    if (use_graph && !cached) {
+        if (s.gexec) { cudaGraphExecDestroy(s.gexec); s.gexec = nullptr; }
+        if (s.graph) { cudaGraphDestroy(s.graph); s.graph = nullptr; }
+        s.key_valid = false;
+        HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph));
+        CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
+        s.key = key;
+        s.key_valid = true;
+    }
+    if (c->comm) {
+        // collective part: every rank's setup is done; make the ghost planes of the input state
+        // consistent (u^n, and u^{n-1} when resuming), then the steps
+        HFCK(c->comm->enter());
+        HFCK(c->comm->exchange(c, s, s.U[0]));
+        if (!first) HFCK(c->comm->exchange(c, s, s.U[2]));
+    }
+    if (nsteps <= 0) return HF_OK;
     if (use_graph) {
-        if (!cached) {
-            if (s.gexec) { cudaGraphExecDestroy(s.gexec); s.gexec = nullptr; }
-            if (s.graph) { cudaGraphDestroy(s.graph); s.graph = nullptr; }
-            s.key_valid = false;
-            HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph));
-            CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
-            s.key = key;
-            s.key_valid = true;
-        }
         if (c->step_flush) {
             // L2 eviction between steps, each step timed alone (no host synchronisation)
             const size_t fb = 512ull << 20;
@@ -2077,6 +2147,7 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
     if (!c || !u || nsteps < 0 || !(dt > 0.0) || !(theta >= 0.0 && theta <= 1.0))
         return fail(HF_E_ARG, "hf_simulate: bad argument");
     if (!c->coef_set) return fail(HF_E_STATE, "hf_simulate: coefficients not set");
+    if (c->comm && !c->comm->ready()) return fail(HF_E_STATE, "hf_simulate: peer transport not connected (hf_peer_connect)");
     if (snap && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "hf_simulate: snap_plane");
     HFCK(check_ptrs(c, "hf_simulate", {F, u, u_prev, snap}));
     CUCK(cudaSetDevice(c->device));
@@ -2092,10 +2163,6 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
     HFCK(copy_in(c, s.U[0], u, c->nzl, s.stream));
     const bool first = step0 <= 0 || !u_prev;
     if (!first) HFCK(copy_in(c, s.U[2], u_prev, c->nzl, s.stream));
-    if (c->comm) {                // make the ghost planes of the input state consistent
-        HFCK(c->comm->exchange(c, s, s.U[0]));
-        if (!first) HFCK(c->comm->exchange(c, s, s.U[2]));
-    }
     int snap_local = -1;
     double *snapdev = nullptr;
     if (snap) {
@@ -2324,8 +2391,19 @@ hf_status hf_nccl_unique_id(uint8_t id[128])
 // ---- NCCL transport ------------------------------------------------------------------------
 struct NcclComm : Comm {
     nccl::ncclComm_t comm = nullptr;
-    ~NcclComm() override { if (comm) nccl::g_api.commDestroy(comm); }
+    bool aborted = false;
+    ~NcclComm() override { if (comm && !aborted) nccl::g_api.commDestroy(comm); }
     bool graph_capturable() const override { return true; }
+    hf_status poll() override
+    {
+        nccl::ncclResult_t ae = 0;
+        if (comm && !aborted && nccl::g_api.commGetAsyncError(comm, &ae) == 0 && ae != 0 && ae != 7 /* inProgress */) {
+            nccl::g_api.commAbort(comm);
+            aborted = true;
+            return fail(HF_E_NCCL, std::string("NCCL asynchronous error: ") + nccl::g_api.getErrorString(ae));
+        }
+        return HF_OK;
+    }
     hf_status exchange(hf_ctx *c, Sys &s, double *v) override
     {
         const long long P = c->plane;
@@ -2350,16 +2428,135 @@ struct NcclComm : Comm {
     }
 };
 
-// ---- in-process transport (all ranks in one process, one host thread each) -----------------
-struct hf_local_group {
+// ---- peer-memory transport (the product path for N > 1; see PeerSync in hf_kernels.cuh) -----
+// Mailbox of a rank (one device allocation, exported by CUDA IPC across processes):
+//   [MailHdr | pad to 4 KB][ghost lo | ghost hi][xbuf lo: 2 parity slots][xbuf hi: 2 parity slots]
+// each plane slot pb bytes (the fp64 plane rounded up to 256 B; the fp32 planes fit too).
+static const size_t MAIL_HDR = 4096;
+
+struct PeerBlob {                     // what a rank tells the others (hf_peer_export)
+    uint32_t magic, version;
+    int32_t pid, rank, nranks, device;
+    char bus[32];                     // PCI bus id of the rank's GPU
+    uint64_t mail_ptr, mail_bytes, pb;
+    cudaIpcMemHandle_t handle;
+};
+static_assert(sizeof(PeerBlob) <= 256, "peer blob");
+static const uint32_t PEER_MAGIC = 0x48465052u;   // "HFPR"
+
+struct hf_local_group;
+static void group_barrier(hf_local_group *g);
+
+struct PeerComm : Comm {
+    int transport = 1;                // 1: ranks in this process, 2: ranks in separate processes (IPC)
+    hf_local_group *grp = nullptr;    // transport 1
+    char *mail = nullptr;
+    size_t mail_bytes = 0, pb = 0;
+    PeerSync host;
+    PeerSync *dev = nullptr;
+    std::vector<void *> opened;       // IPC mappings of the peers' mailboxes
+    bool connected = false;
+    ~PeerComm() override
+    {
+        for (void *p : opened) cudaIpcCloseMemHandle(p);
+        cudaFree(dev);
+        cudaFree(mail);
+    }
+    bool graph_capturable() const override { return true; }
+    bool in_kernel() const override { return true; }
+    bool ready() const override { return connected; }
+    hf_status enter() override
+    {
+        if (grp) group_barrier(grp);
+        return HF_OK;
+    }
+    const PeerSync *peer_dev() const override { return connected ? dev : nullptr; }
+    hf_status allreduce(hf_ctx *, Sys &, double *, int) override { return HF_OK; }   // in the kernels
+    hf_status exchange(hf_ctx *c, Sys &s, double *v) override
+    {
+        const long long P = c->plane;
+        const long long glo = c->own_lo > 0 ? 0 : -1, ghi = c->own_hi < c->nzl ? (long long)c->own_hi * P : -1;
+        const unsigned nb = (unsigned)std::max(1LL, std::min<long long>((P + 255) / 256, 64));
+        if (c->es == 8) {
+            k_xsend<double><<<nb, 256, 0, s.stream>>>(dev, v, c->launches);
+            k_xrecv<double><<<nb, 256, 0, s.stream>>>(dev, v, glo, ghi, c->launches);
+        } else {
+            k_xsend<float><<<nb, 256, 0, s.stream>>>(dev, v, c->launches);
+            k_xrecv<float><<<nb, 256, 0, s.stream>>>(dev, v, glo, ghi, c->launches);
+        }
+        CUCK(cudaGetLastError());
+        return HF_OK;
+    }
+    // device copy of the protocol state for the context's current layout (precision)
+    hf_status refresh(hf_ctx *c)
+    {
+        host.lo0 = (long long)c->own_lo * c->plane;
+        host.hi0 = (long long)(c->own_hi - 1) * c->plane;
+        host.plane = c->plane;
+        host.xslot = (long long)(pb / c->es);
+        if (!dev) CUCK(cudaMalloc(&dev, sizeof(PeerSync)));
+        CUCK(cudaMemcpy(dev, &host, sizeof(PeerSync), cudaMemcpyHostToDevice));
+        return HF_OK;
+    }
+    // every rank's mailbox, mapped in this process: fill the protocol state
+    hf_status connect(hf_ctx *c, const std::vector<char *> &mb, int share)
+    {
+        const int R = c->nranks, r = c->rank;
+        std::memset(&host, 0, sizeof(host));
+        host.nranks = R;
+        host.rank = r;
+        host.mine = (MailHdr *)mb[r];
+        for (int q = 0; q < R; q++) host.peer[q] = (MailHdr *)mb[q];
+        const size_t G0 = MAIL_HDR, X0 = MAIL_HDR + 2 * pb, X1 = MAIL_HDR + 4 * pb;
+        host.gdst_lo = r > 0 ? mb[r - 1] + G0 + pb : nullptr;      // lower neighbour's hi ghost
+        host.gdst_hi = r + 1 < R ? mb[r + 1] + G0 : nullptr;       // upper neighbour's lo ghost
+        host.xdst_lo = r > 0 ? mb[r - 1] + X1 : nullptr;
+        host.xdst_hi = r + 1 < R ? mb[r + 1] + X0 : nullptr;
+        host.xsrc_lo = mb[r] + X0;
+        host.xsrc_hi = mb[r] + X1;
+        HFCK(refresh(c));
+        if (share > 1) {
+            // ranks sharing one GPU (tests): every rank's grids fit on the GPU at once, so a rank
+            // waiting inside a kernel never starves the rank it waits for; no early launches
+            c->nsm_share = std::max(1, c->nsm / share);
+            c->pdl = 0;
+        }
+        connected = true;
+        c->ghost_buf = mail + MAIL_HDR;
+        c->ghost_pb = pb;
+        return sys_maps(c, c->sys0);
+    }
+};
+
+// mailbox of a new slab context (zeroed: flags and counters start at 0)
+static hf_status peer_alloc(hf_ctx *c, PeerComm *pc)
+{
+    const size_t plane64 = (size_t)((c->nx1 + 1) / 2 * 2) * c->ny1 * 8;
+    const size_t plane32 = (size_t)((c->nx1 + 3) / 4 * 4) * c->ny1 * 4;
+    pc->pb = (std::max(plane64, plane32) + 255) / 256 * 256;
+    pc->mail_bytes = MAIL_HDR + 6 * pc->pb;
+    CUCK(cudaMalloc(&pc->mail, pc->mail_bytes));
+    CUCK(cudaMemset(pc->mail, 0, pc->mail_bytes));
+    return HF_OK;
+}
+
+static void bus_id(int device, char out[32])
+{
+    std::memset(out, 0, 32);
+    if (cudaDeviceGetPCIBusId(out, 31, device) != cudaSuccess) {
+        cudaGetLastError();
+        std::snprintf(out, 32, "dev%d", device);
+    }
+}
+
+struct hf_local_group {               // ranks of one process (transport 1)
     int n = 0;
     std::mutex mu;
     std::condition_variable cv;
     int arrived = 0;
     long long gen = 0;
-    std::vector<hf_ctx *> ctx;
-    std::vector<double *> vecs;   // vector each rank published for the current exchange
-    std::vector<double> slots;    // NPART partial sums per rank
+    std::vector<char *> mail;
+    std::vector<int> device;
     void barrier()
     {
         std::unique_lock<std::mutex> lk(mu);
@@ -2369,66 +2566,17 @@ struct hf_local_group {
     }
 };
 
-struct LocalComm : Comm {
-    hf_local_group *grp = nullptr;
-    bool graph_capturable() const override { return false; }
-    hf_status exchange(hf_ctx *c, Sys &s, double *v) override
-    {
-        // publish v, wait until every rank's data is final, then pull the neighbours' owned
-        // boundary planes into our ghost planes (peer copies; same or different device)
-        CUCK(cudaStreamSynchronize(s.stream));
-        {
-            std::lock_guard<std::mutex> lk(grp->mu);
-            grp->vecs[c->rank] = v;
-        }
-        grp->barrier();
-        const long long P = c->plane;
-        if (c->rank > 0) {
-            hf_ctx *o = grp->ctx[c->rank - 1];
-            const double *ov = grp->vecs[c->rank - 1];
-            CUCK(cudaMemcpyPeerAsync(eoff(c, v, (c->own_lo - 1) * P), c->device, eoff(o, ov, (o->own_hi - 1) * P),
-                                     o->device, P * c->es, s.stream));
-        }
-        if (c->rank < c->nranks - 1) {
-            hf_ctx *o = grp->ctx[c->rank + 1];
-            const double *ov = grp->vecs[c->rank + 1];
-            CUCK(cudaMemcpyPeerAsync(eoff(c, v, c->own_hi * P), c->device, eoff(o, ov, o->own_lo * P), o->device,
-                                     P * c->es, s.stream));
-        }
-        CUCK(cudaStreamSynchronize(s.stream));
-        grp->barrier();
-        return HF_OK;
-    }
-    hf_status allreduce(hf_ctx *c, Sys &s, double *v, int n) override
-    {
-        double h[NPART];
-        CUCK(cudaMemcpyAsync(h, v, n * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
-        CUCK(cudaStreamSynchronize(s.stream));
-        {
-            std::lock_guard<std::mutex> lk(grp->mu);
-            for (int j = 0; j < n; j++) grp->slots[(size_t)c->rank * NPART + j] = h[j];
-        }
-        grp->barrier();
-        double tot[NPART] = {0, 0, 0, 0};
-        for (int r = 0; r < grp->n; r++)       // fixed rank order: identical on every rank
-            for (int j = 0; j < n; j++) tot[j] += grp->slots[(size_t)r * NPART + j];
-        grp->barrier();
-        CUCK(cudaMemcpyAsync(v, tot, n * sizeof(double), cudaMemcpyHostToDevice, s.stream));
-        CUCK(cudaStreamSynchronize(s.stream));
-        return HF_OK;
-    }
-};
+static void group_barrier(hf_local_group *g) { g->barrier(); }
 
 extern "C" {
 
 hf_status hf_local_group_create(int32_t nranks, hf_local_group **out)
 {
-    if (nranks < 1 || !out) return fail(HF_E_ARG, "hf_local_group_create: bad argument");
+    if (nranks < 1 || nranks > HF_MAX_RANKS || !out) return fail(HF_E_ARG, "hf_local_group_create: bad argument");
     hf_local_group *g = new hf_local_group();
     g->n = nranks;
-    g->ctx.assign(nranks, nullptr);
-    g->vecs.assign(nranks, nullptr);
-    g->slots.assign((size_t)nranks * NPART, 0.0);
+    g->mail.assign(nranks, nullptr);
+    g->device.assign(nranks, 0);
     *out = g;
     return HF_OK;
 }
@@ -2438,7 +2586,10 @@ void hf_local_group_destroy(hf_local_group *g) { delete g; }
 hf_status hf_create_slab(const hf_grid *g, int32_t rank, int32_t nranks, const uint8_t *id, int32_t transport,
                          int device, void *cuda_stream, hf_ctx **out)
 {
-    if (!g || !out || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(HF_E_ARG, "hf_create_slab: bad argument");
+    if (!g || !out || nranks < 1 || rank < 0 || rank >= nranks) return fail(HF_E_ARG, "hf_create_slab: bad argument");
+    if ((transport == 0 || transport == 1) && !id) return fail(HF_E_ARG, "hf_create_slab: NULL id");
+    if (transport != 0 && nranks > HF_MAX_RANKS)
+        return fail(HF_E_ARG, "hf_create_slab: at most " + std::to_string(HF_MAX_RANKS) + " ranks (one node)");
     hf_ctx *c = new hf_ctx();
     hf_status st = ctx_init(c, g, device, cuda_stream, rank, nranks);
     if (st != HF_OK) { ctx_free(c); delete c; return st; }
@@ -2452,23 +2603,97 @@ hf_status hf_create_slab(const hf_grid *g, int32_t rank, int32_t nranks, const u
             if (r != 0) { st = fail(HF_E_NCCL, std::string("ncclCommInitRank: ") + nccl::g_api.getErrorString(r)); delete nc; }
             else c->comm = nc;
         }
-    } else if (transport == 1) {
-        hf_local_group *grp = (hf_local_group *)id;
-        if (grp->n != nranks) st = fail(HF_E_ARG, "hf_create_slab: group size != nranks");
-        else {
-            LocalComm *lc = new LocalComm();
-            lc->grp = grp;
-            {
-                std::lock_guard<std::mutex> lk(grp->mu);
-                grp->ctx[rank] = c;
+    } else if (transport == 1 || transport == 2) {
+        PeerComm *pc = new PeerComm();
+        pc->transport = transport;
+        c->comm = pc;
+        st = peer_alloc(c, pc);
+        if (st == HF_OK && transport == 1) {
+            // in-process group: publish the mailbox, wait for every rank, connect with plain pointers
+            hf_local_group *grp = (hf_local_group *)id;
+            if (grp->n != nranks) st = fail(HF_E_ARG, "hf_create_slab: group size != nranks");
+            else {
+                {
+                    std::lock_guard<std::mutex> lk(grp->mu);
+                    grp->mail[rank] = pc->mail;
+                    grp->device[rank] = device;
+                }
+                grp->barrier();
+                pc->grp = grp;
+                int share = 0;
+                for (int q = 0; q < nranks; q++) share += grp->device[q] == device;
+                const uintptr_t sh = (uintptr_t)cuda_stream;
+                if (share > 1 && (sh == 1 || sh == 2))
+                    st = fail(HF_E_ARG, "hf_create_slab: ranks sharing a GPU need their own streams (not the legacy or "
+                                        "per-thread default stream): a rank waiting inside a kernel would block the others");
+                for (int q = 0; q < nranks && st == HF_OK; q++)
+                    if (grp->device[q] != device) {
+                        cudaError_t e = cudaDeviceEnablePeerAccess(grp->device[q], 0);
+                        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                            st = fail(HF_E_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+                        cudaGetLastError();
+                    }
+                if (st == HF_OK) st = pc->connect(c, grp->mail, share);
+                grp->barrier();
             }
-            c->comm = lc;
-            grp->barrier();
         }
     } else st = fail(HF_E_ARG, "hf_create_slab: unknown transport");
     if (st != HF_OK) { ctx_free(c); delete c; return st; }
     *out = c;
     return HF_OK;
+}
+
+hf_status hf_peer_export(hf_ctx *c, uint8_t blob[HF_PEER_BLOB_BYTES])
+{
+    PeerComm *pc = c ? dynamic_cast<PeerComm *>(c->comm) : nullptr;
+    if (!pc || !blob) return fail(HF_E_ARG, "hf_peer_export: not a peer-transport slab context");
+    CUCK(cudaSetDevice(c->device));
+    PeerBlob b;
+    std::memset(&b, 0, sizeof(b));
+    b.magic = PEER_MAGIC;
+    b.version = 1;
+    b.pid = (int32_t)getpid();
+    b.rank = c->rank;
+    b.nranks = c->nranks;
+    b.device = c->device;
+    bus_id(c->device, b.bus);
+    b.mail_ptr = (uint64_t)(uintptr_t)pc->mail;
+    b.mail_bytes = pc->mail_bytes;
+    b.pb = pc->pb;
+    CUCK(cudaIpcGetMemHandle(&b.handle, pc->mail));
+    std::memset(blob, 0, HF_PEER_BLOB_BYTES);
+    std::memcpy(blob, &b, sizeof(b));
+    return HF_OK;
+}
+
+hf_status hf_peer_connect(hf_ctx *c, const uint8_t *blobs)
+{
+    PeerComm *pc = c ? dynamic_cast<PeerComm *>(c->comm) : nullptr;
+    if (!pc || !blobs) return fail(HF_E_ARG, "hf_peer_connect: not a peer-transport slab context");
+    if (pc->connected) return fail(HF_E_STATE, "hf_peer_connect: already connected");
+    CUCK(cudaSetDevice(c->device));
+    const int R = c->nranks;
+    char mybus[32];
+    bus_id(c->device, mybus);
+    std::vector<char *> mb(R, nullptr);
+    int share = 0;
+    for (int q = 0; q < R; q++) {
+        PeerBlob b;
+        std::memcpy(&b, blobs + (size_t)q * HF_PEER_BLOB_BYTES, sizeof(b));
+        if (b.magic != PEER_MAGIC || b.version != 1 || b.rank != q || b.nranks != R || b.pb != pc->pb)
+            return fail(HF_E_ARG, "hf_peer_connect: blob " + std::to_string(q) + " does not belong to this group");
+        share += std::strncmp(b.bus, mybus, 32) == 0;
+        if (q == c->rank) { mb[q] = pc->mail; continue; }
+        if (b.pid == (int32_t)getpid()) { mb[q] = (char *)(uintptr_t)b.mail_ptr; continue; }
+        void *p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess)
+            return fail(HF_E_CUDA, "hf_peer_connect: cudaIpcOpenMemHandle(rank " + std::to_string(q) + "): " +
+                                       cudaGetErrorString(e));
+        pc->opened.push_back(p);
+        mb[q] = (char *)p;
+    }
+    return pc->connect(c, mb, share);
 }
 
 hf_status hf_slab_range(const hf_ctx *c, int64_t *z_lo, int64_t *z_hi, int64_t *local_planes, int64_t *local_z0)
@@ -2617,6 +2842,8 @@ hf_status hf_set_precision(hf_ctx *c, int32_t bits)
     c->prec = bits;
     c->es = bits / 8;
     set_layout(c);
+    if (PeerComm *pc = dynamic_cast<PeerComm *>(c->comm))
+        if (pc->connected) HFCK(pc->refresh(c));
     StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
     int occ = 0;

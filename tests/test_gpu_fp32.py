@@ -19,6 +19,13 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_1905_07622_b200 as hf  # noqa: E402
 
 DEV = torch.device("cuda:0")
+
+
+def on_own_stream(fn, r):
+    """Run a slab rank's thread on its own stream: ranks sharing the GPU wait for each other
+    inside kernels, so they must never share (or implicitly synchronise with) a stream."""
+    with torch.cuda.stream(torch.cuda.Stream(device=DEV)):
+        fn(r)
 BAR = 1e-5
 
 
@@ -190,7 +197,7 @@ def test_fp32_slab_local_transport():
         except Exception as e:  # pragma: no cover
             errs.append(e)
 
-    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(nranks)]
+    th = [threading.Thread(target=on_own_stream, args=(rank_main, r)) for r in range(nranks)]
     [t.start() for t in th]
     [t.join(timeout=300) for t in th]
     assert not errs, errs

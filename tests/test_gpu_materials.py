@@ -21,6 +21,13 @@ import paper_1905_07622_b200 as hf  # noqa: E402
 
 DEV = torch.device("cuda:0")
 
+
+def on_own_stream(fn, r):
+    """Run a slab rank's thread on its own stream: ranks sharing the GPU wait for each other
+    inside kernels, so they must never share (or implicitly synchronise with) a stream."""
+    with torch.cuda.stream(torch.cuda.Stream(device=DEV)):
+        fn(r)
+
 GRIDS = {
     "1x1x1": synth.Grid((1, 1, 1), (1.0, 1.0, 1.0)),
     "c1": synth.Grid((8, 8, 8), (0.125, 0.125, 0.125)),
@@ -174,7 +181,7 @@ def test_ids_slabs_match_single():
         except Exception as e:  # pragma: no cover
             errs.append(e)
 
-    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(nranks)]
+    th = [threading.Thread(target=on_own_stream, args=(rank_main, r)) for r in range(nranks)]
     [t.start() for t in th]
     [t.join(timeout=300) for t in th]
     assert not errs, errs

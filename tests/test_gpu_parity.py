@@ -24,6 +24,13 @@ import paper_1905_07622_b200 as hf  # noqa: E402
 DEV = torch.device("cuda:0")
 
 
+def on_own_stream(fn, r):
+    """Run a slab rank's thread on its own stream: ranks sharing the GPU wait for each other
+    inside kernels, so they must never share (or implicitly synchronise with) a stream."""
+    with torch.cuda.stream(torch.cuda.Stream(device=DEV)):
+        fn(r)
+
+
 def T(a):
     return torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device=DEV)
 
@@ -489,7 +496,7 @@ def test_slab_local_transport(nranks):
         except Exception as e:  # pragma: no cover
             errs.append(e)
 
-    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(nranks)]
+    th = [threading.Thread(target=on_own_stream, args=(rank_main, r)) for r in range(nranks)]
     [t.start() for t in th]
     [t.join(timeout=300) for t in th]
     assert not errs, errs
@@ -604,19 +611,25 @@ def test_c5_full_size_stacked_two_steps():
         assert sto == 0 and rel(ub[j], uo) <= 1e-10, j
 
 
-@pytest.mark.parametrize("transport", [0, 1])
+@pytest.mark.parametrize("transport", [0, 1, 2])
 def test_slab_single_rank_nccl_and_local(transport):
-    """A 1-rank slab context runs the slab driver (host loop, k_localsum, transport allreduce,
-    ghost exchange calls) -- through real NCCL for transport 0 -- and must reproduce the plain
-    single-GPU run bit for bit (same kernels, same reduction order)."""
+    """A 1-rank slab context runs the slab driver -- through real NCCL for transport 0 (host loop,
+    k_localsum, allreduce), through the peer-memory protocol for 1 (in-process group) and 2
+    (export / connect handshake with itself; in-kernel publish and wait, step graph) -- and must
+    reproduce the plain single-GPU run bit for bit (same kernels, same reduction order)."""
     p = synth.c1()
     ug, st, _, _ = _gpu_sim(p)
     if transport == 0:
         uid = hf.hf_nccl_unique_id()
         ctx = hf.hf_create_slab(p.grid, 0, 1, uid, transport=0, device=0)
-    else:
+    elif transport == 1:
         grp = hf.hf_local_group_create(1)
         ctx = hf.hf_create_slab(p.grid, 0, 1, grp, transport=1, device=0)
+    else:
+        ctx = hf.hf_create_slab(p.grid, 0, 1, None, transport=2, device=0)
+        with pytest.raises(hf.HfError):          # not connected yet
+            hf.hf_simulate(ctx, p.theta, p.dt, 1, None, T(p.u0))
+        hf.hf_peer_setup(ctx, lambda b: [b])
     hf.hf_set_coefficients(ctx, T(p.k), T(p.c))
     F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
     hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
