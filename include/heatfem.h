@@ -321,6 +321,32 @@ hf_status hf_time_kernel_a(hf_ctx *ctx, int32_t reps, double *ms_per_launch);
  * Profiling (hf_profile) and the NCCL slab transport always use the host loop. */
 hf_status hf_set_driver(hf_ctx *ctx, int32_t driver);
 
+/* On-chip PCG (the default where eligible): hf_simulate* runs each time step's whole PCG solve
+ * (Alg. 1) in ONE cooperative launch whose CTAs (one per SM) keep d (+ a one-node
+ * halo), x, q/s, r and the material ids of their brick of the grid in shared memory and
+ * registers; the Alg. 1 reductions ride on two grid barriers per iteration.  Same operator,
+ * readings (R3-R6) and stop test as the streaming kernels; results agree to rounding order.
+ * Eligible: fp64 Q1 with materials by id (hf_set_material_ids), one system, no slab transport,
+ * graph driver, and a grid whose brick partition fits (<= 31 x 25 x 16 nodes per brick, one brick
+ * per SM: about 1.1M nodes on 148 SMs).  mode 0 = never (streaming kernels), 1 = when eligible.
+ * Errors: HF_E_ARG. */
+hf_status hf_set_resident(hf_ctx *ctx, int32_t mode);
+
+/* The on-chip PCG's plan for the current context: out[0] eligible, out[1..3] bricks per axis,
+ * out[4..6] largest brick (nodes), out[7] plane capacity BZ, out[8] shared memory KB per CTA,
+ * out[9] 1 if the last hf_simulate* used it.  When not eligible hf_last_error() says why.
+ * Errors: HF_E_ARG, HF_E_CUDA. */
+hf_status hf_resident_plan(hf_ctx *ctx, int32_t out[10]);
+
+/* Instrumentation of the on-chip PCG: enable = 1 (re)starts per-phase timers of CTA 0 (the next
+ * hf_simulate* rebuilds its graph with them), 0 stops them.  out (may be NULL) receives the totals
+ * since the last start of CTA 0 in out[0..11] and the largest over the CTAs in out[12..23]: us in
+ * [0] d update, [1] stencil (kernel A), [2] grid reduction of d^T q, [3] kernel B, [4] grid
+ * reduction of r^T s, r^T r (and residual replacements), [5] init, [6] PCG iterations, and inside
+ * the reductions [7] fence + arrival, [8] waiting for the other CTAs, [9] reading the partials.
+ * Errors: HF_E_ARG, HF_E_CUDA. */
+hf_status hf_resident_profile(hf_ctx *ctx, int32_t enable, double out[24]);
+
 /* Enqueue a 512 MiB memset on the context stream (evicts the 126 MB L2; bench timing rule). */
 hf_status hf_flush_l2(hf_ctx *ctx);
 

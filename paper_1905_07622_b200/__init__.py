@@ -81,6 +81,9 @@ _SIGS = {
     "hf_profile": (_i32, [_vp, _i32]),
     "hf_profile_read": (_i32, [_vp, _P(C.c_double * 5), _P(C.c_int64 * 5)]),
     "hf_set_driver": (_i32, [_vp, _i32]),
+    "hf_set_resident": (_i32, [_vp, _i32]),
+    "hf_resident_plan": (_i32, [_vp, _P(C.c_int32)]),
+    "hf_resident_profile": (_i32, [_vp, _i32, _P(C.c_double)]),
     "hf_flush_l2": (_i32, [_vp]),
     "hf_set_step_flush": (_i32, [_vp, _i32]),
     "hf_set_element": (_i32, [_vp, _i32]),
@@ -433,6 +436,30 @@ def hf_profile_read(ctx: Context):
 
 def hf_set_driver(ctx: Context, driver: int):
     _check(_lib.hf_set_driver(ctx.ptr, driver))
+
+
+def hf_set_resident(ctx: Context, mode: int):
+    _check(_lib.hf_set_resident(ctx.ptr, mode))
+
+
+def hf_resident_plan(ctx: Context) -> dict:
+    out = (C.c_int32 * 10)()
+    _check(_lib.hf_resident_plan(ctx.ptr, out))
+    keys = ("eligible", "px", "py", "pz", "bx", "by", "bz", "BZ", "smem_kb", "last_used")
+    d = {k: int(v) for k, v in zip(keys, out)}
+    if not d["eligible"]:
+        d["why"] = _lib.hf_last_error().decode()
+    return d
+
+
+def hf_resident_profile(ctx: Context, enable: int) -> dict:
+    out = (C.c_double * 24)()
+    _check(_lib.hf_resident_profile(ctx.ptr, enable, out))
+    keys = ("d_update_us", "stencil_us", "reduce_dq_us", "kernel_b_us", "reduce_rs_us", "init_us", "iters",
+            "fence_us", "spin_us", "read_us")
+    d = {k: float(v) for k, v in zip(keys, out[:10])}
+    d.update({"max_" + k: float(v) for k, v in zip(keys, out[12:22])})
+    return d
 
 
 def hf_flush_l2(ctx: Context):

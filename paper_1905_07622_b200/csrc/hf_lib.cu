@@ -11,6 +11,7 @@
 #include "heatfem.h"
 #include "hf_kernels.cuh"
 #include "hf_ablate.cuh"
+#include "hf_resident.cuh"
 
 #include <dlfcn.h>
 #include <unistd.h>
@@ -161,7 +162,7 @@ static hf_status get_encode()
 
 struct SimKey {
     double aK = 0, aM = 0, aKL = 0, aML = 0, rtol = 0, dt = 0;
-    int max_iter = 0, replace_every = 0, first = 0, snap_plane = -1, lift = 0, pad = 0;
+    int max_iter = 0, replace_every = 0, first = 0, snap_plane = -1, lift = 0, res = 0;
     const double *F = nullptr;
     double *snap = nullptr;
     bool operator==(const SimKey &o) const { return std::memcmp(this, &o, sizeof(SimKey)) == 0; }
@@ -248,6 +249,11 @@ struct hf_ctx {
     int unroll = 0;                  // PCG iterations per WHILE-body launch (0: by grid size, see build_cg_graph)
     int pdl = 1;                     // programmatic A <-> B edges in the loop body (HF_PDL=0 disables)
     int fuse_ab = 0;                 // A and B of an iteration in one launch (HF_FUSE_AB=1)
+    int tm_fence = 0;                // acquire TMA descriptors in every launch (HF_TM_FENCE=1, see maps_dev)
+    int resident = 0;                // hf_set_resident: 1 = on-chip PCG when eligible, 0 = never (default)
+    int last_resident = 0;           // the last hf_simulate* ran the on-chip PCG
+    ResSync *rsync = nullptr;        // flags + partials of the on-chip PCG's grid reductions
+    unsigned long long *res_prof = nullptr;   // per-phase timer of the on-chip PCG (hf_resident_profile)
     int nsys = 1;                    // systems stacked along z (batched forward simulations, a13)
     int sys_planes = 0;              // local node planes per system (= nzl for one system)
     int rank = 0, nranks = 1;
@@ -663,8 +669,7 @@ struct StencilFn {
 template <int R, int LD, int EP, int FL, int EL, class Real> static StencilFn stencil_fn_t()
 {
     constexpr int NS = ns_of<R, LD>();
-    static const size_t pad = getenv("HF_SMEM_PAD") ? (size_t)atoi(getenv("HF_SMEM_PAD")) : 0;   // tuning / debug
-    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL, Real>, StencilShape<R, NW, LD, Real, EL>::smem_bytes(NS) + pad};
+    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL, Real>, StencilShape<R, NW, LD, Real, EL>::smem_bytes(NS)};
 }
 
 // every (loader, epilogue, flags) variant the library launches, for tile heights R = 2 and 4
@@ -909,8 +914,7 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
     L.block = dim3(32, NW, 1);
     L.smem = f.smem;
     HFCK(maps_dev(c, maps, &a.tm));
-    static const int tm_fence = getenv("HF_TM_FENCE") ? atoi(getenv("HF_TM_FENCE")) : 0;   // see maps_dev
-    a.tm_fence = tm_fence;
+    a.tm_fence = c->tm_fence;
     L.add(a);
     L.cls = cls;
     *out = L;
@@ -1116,6 +1120,8 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     if (const char *e = getenv("HF_PDL")) c->pdl = atoi(e) != 0;
     if (const char *e = getenv("HF_FUSE_AB")) c->fuse_ab = atoi(e) != 0;
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
+    if (const char *e = getenv("HF_TM_FENCE")) c->tm_fence = atoi(e) != 0;
+    if (const char *e = getenv("HF_RESIDENT")) c->resident = atoi(e) != 0;
     // resident CTAs per SM of the CG stencil decide the z split of the grid
     StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
     HFCK(ensure_smem_attr(f.fn, f.smem, device));
@@ -1156,6 +1162,8 @@ static void ctx_free(hf_ctx *c)
     cudaFree(c->ab_A);
     cudaFree(c->ab_contrib);
     cudaFree(c->kid);
+    cudaFree(c->rsync);
+    cudaFree(c->res_prof);
     for (auto &kv : c->stacks) { ctx_free(kv.second); delete kv.second; }
     c->stacks.clear();
     delete c->comm;
@@ -1986,6 +1994,122 @@ hf_status hf_cg(hf_ctx *c, double aK, double aM, const double *b, double *x, con
 
 // One system's time loop; U[0] holds u^0 (and U[2] u^{-1} when resuming) on entry, F (padded)
 // the flux load.
+// ---- on-chip PCG (hf_resident.cuh): eligibility, brick partition, launch ------------------
+struct ResPlan {
+    int ok = 0, px = 0, py = 0, pz = 0, bxm = 0, bym = 0, bzm = 0, BZ = 0, P = 0;
+    size_t smem = 0;
+    const void *fn = nullptr;
+    const char *why = "";
+};
+
+// Eligible: fp64 Q1 with materials by id (hf_set_material_ids), one system, no slab transport,
+// graph driver, and a brick partition that fits one CTA per SM: bricks <= 31 x (RES_NW - 1) x
+// RES_BZ_MAX nodes, px py pz <= SMs, shared memory <= the opt-in limit.
+static ResPlan res_plan(hf_ctx *c)
+{
+    ResPlan p;
+    if (!c->resident) { p.why = "disabled"; return p; }
+    if (!c->pal_on || c->elem != EL_Q1 || c->tetv || c->es != 8) { p.why = "needs fp64 Q1 materials by id"; return p; }
+    if (c->nsys != 1 || c->comm) { p.why = "stacked systems / slabs"; return p; }
+    if (c->driver != 0 || c->prof) { p.why = "host-loop driver / profiling"; return p; }
+    const int RW = 31, RH = RES_ROWS - 1;
+    p.px = (c->nx1 + RW - 1) / RW;
+    p.py = (c->ny1 + RH - 1) / RH;
+    const int cols = p.px * p.py;
+    if (cols > c->nsm) { p.why = "cross-section too large"; return p; }
+    p.pz = std::max(1, std::min(c->nzl, c->nsm / cols));
+    p.bxm = (c->nx1 + p.px - 1) / p.px;
+    p.bym = (c->ny1 + p.py - 1) / p.py;
+    p.bzm = (c->nzl + p.pz - 1) / p.pz;
+    if (p.bzm > RES_BZ_MAX) { p.why = "grid too large for on-chip PCG"; return p; }
+    p.BZ = RES_BZ_MAX;
+    p.fn = (const void *)k_pcg_res;
+    p.smem = res_smem(p.bxm, p.bym, p.bzm, c->npal).total;
+    int optin = 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device) != cudaSuccess ||
+        p.smem > (size_t)optin) { p.why = "shared memory"; return p; }
+    p.P = p.px * p.py * p.pz;
+    if (p.P > RES_PMAX) { p.why = "too many bricks"; return p; }
+    if (ensure_smem_attr(p.fn, p.smem, c->device) != HF_OK) { p.why = "smem attribute"; return p; }
+    int occ = 0;
+    const cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p.fn, RES_NT, p.smem);
+    if (oe != cudaSuccess || occ * c->nsm < p.P) {
+        static thread_local char buf[160];
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, p.fn);
+        snprintf(buf, sizeof(buf), "occupancy: %d CTAs/SM (%s), %d registers, %zu B smem", occ, cudaGetErrorString(oe),
+                 fa.numRegs, p.smem);
+        cudaGetLastError();
+        p.why = buf;
+        return p;
+    }
+    p.ok = 1;
+    return p;
+}
+
+static hf_status res_launch(hf_ctx *c, Sys &s, const ResPlan &p, double aK, double aM, bool first, Launch *out)
+{
+    if (!c->rsync) CUCK(cudaMalloc(&c->rsync, sizeof(ResSync)));
+    ResArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.g = make_geom(c);
+    a.lam = make_lam(c->g.h, aK, aM);
+    a.px = p.px; a.py = p.py; a.pz = p.pz;
+    a.bxm = p.bxm; a.bym = p.bym; a.bzm = p.bzm;
+    a.kid = c->kid;
+    a.kid_pitch = c->kid_pitch;
+    std::memcpy(a.pal, c->pal, sizeof(a.pal));
+    a.npal = c->npal;
+    a.b = s.b;
+    a.invd = s.invd;
+    for (int i = 0; i < 3; i++) a.ring[i] = s.U[i];
+    a.sg = s.s;
+    a.dsave = s.dbuf[0];
+    a.st = s.st;
+    a.rs = c->rsync;
+    a.first = first ? 1 : 0;
+    a.launches = c->launches;
+    a.prof = c->res_prof;
+    Launch L;
+    L.fn = p.fn;
+    L.grid = dim3(p.P, 1, 1);
+    L.block = dim3(RES_NT, 1, 1);
+    L.smem = p.smem;
+    L.add(a);
+    L.cls = 0;
+    *out = L;
+    return HF_OK;
+}
+
+// graph of one time step with the on-chip PCG: [RHS] -> [lift] -> zero the reduction flags ->
+// k_pcg_res (cooperative: every CTA co-resident, or the launch fails) -> step end, commit
+static hf_status build_res_graph(hf_ctx *c, const std::vector<Launch> &pre, const Launch &res,
+                                 const std::vector<Launch> &post, cudaGraph_t *out)
+{
+    cudaGraph_t g;
+    CUCK(cudaGraphCreate(&g, 0));
+    cudaGraphNode_t prev = nullptr, n;
+    for (auto &p : pre) { HFCK(add_node(g, p, prev ? &prev : nullptr, &n)); prev = n; }
+    cudaMemsetParams mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.dst = c->rsync;
+    mp.elementSize = 4;
+    mp.width = sizeof(ResSync) / 4;
+    mp.height = 1;
+    mp.value = 0;
+    CUCK(cudaGraphAddMemsetNode(&n, g, prev ? &prev : nullptr, prev ? 1 : 0, &mp));
+    prev = n;
+    HFCK(add_node(g, res, &prev, &n));
+    cudaKernelNodeAttrValue v;
+    std::memset(&v, 0, sizeof(v));
+    v.cooperative = 1;
+    CUCK(cudaGraphKernelNodeSetAttribute(n, cudaKernelNodeAttributeCooperative, &v));
+    prev = n;
+    for (auto &p : post) { HFCK(add_node(g, p, &prev, &n)); prev = n; }
+    *out = g;
+    return HF_OK;
+}
+
 static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int nsteps, const double *dF,
                               bool first, int snap_local, double *snapdev, const hf_cg_opts &o)
 {
@@ -2013,6 +2137,10 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     key.aK = aK; key.aM = aM; key.aKL = aKL; key.aML = aML; key.rtol = o.rtol; key.dt = dt;
     key.max_iter = o.max_iter; key.replace_every = o.replace_every; key.first = first;
     key.snap_plane = snap_local; key.lift = lift; key.F = dF; key.snap = snapdev;
+    ResPlan rp;
+    if (use_graph && &s == &c->sys0) rp = res_plan(c);
+    key.res = rp.ok;
+    c->last_resident = rp.ok;
     const bool cached = use_graph && s.key_valid && s.key == key && s.gexec;
 
     std::vector<Launch> pre, post;
@@ -2056,7 +2184,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
         ia.zs0 = c->own_lo - (c->own_lo > 0 ? 1 : 0);
         ia.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
         HFCK(stencil_launch(c, LD_X0, EP_RESID_INIT, true, s.maps, ia, 2, &init));
-        HFCK(cg_launches(c, s, aK, aM, nullptr, s.maps, &L));
+        if (!rp.ok) HFCK(cg_launches(c, s, aK, aM, nullptr, s.maps, &L));
         post = step_launches(c, step_args(c, s, nullptr, snapdev, snap_local), true);
     }
 
@@ -2064,7 +2192,12 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
         if (s.gexec) { cudaGraphExecDestroy(s.gexec); s.gexec = nullptr; }
         if (s.graph) { cudaGraphDestroy(s.graph); s.graph = nullptr; }
         s.key_valid = false;
-        HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph));
+        if (rp.ok) {
+            Launch RL;
+            HFCK(res_launch(c, s, rp, aK, aM, first, &RL));
+            HFCK(build_res_graph(c, pre, RL, post, &s.graph));
+        } else
+            HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph));
         CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
         s.key = key;
         s.key_valid = true;
@@ -2850,6 +2983,53 @@ hf_status hf_set_precision(hf_ctx *c, int32_t bits)
     CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
     c->occ = std::max(1, occ);
     HFCK(sys_alloc(c, c->sys0, c->stream));
+    return HF_OK;
+}
+
+hf_status hf_set_resident(hf_ctx *c, int32_t mode)
+{
+    if (!c || mode < 0 || mode > 1) return fail(HF_E_ARG, "hf_set_resident: mode must be 0 or 1");
+    c->resident = mode;
+    c->sys0.key_valid = false;
+    return HF_OK;
+}
+
+hf_status hf_resident_plan(hf_ctx *c, int32_t out[10])
+{
+    if (!c || !out) return fail(HF_E_ARG, "hf_resident_plan: NULL argument");
+    CUCK(cudaSetDevice(c->device));
+    const ResPlan p = res_plan(c);
+    out[0] = p.ok; out[1] = p.px; out[2] = p.py; out[3] = p.pz; out[4] = p.bxm; out[5] = p.bym; out[6] = p.bzm;
+    out[7] = p.BZ; out[8] = (int32_t)(p.smem / 1024); out[9] = c->last_resident;
+    if (!p.ok) g_err = std::string("hf_resident_plan: not eligible: ") + p.why;
+    return HF_OK;
+}
+
+hf_status hf_resident_profile(hf_ctx *c, int32_t enable, double out[24])
+{
+    if (!c) return fail(HF_E_ARG, "hf_resident_profile: NULL");
+    CUCK(cudaSetDevice(c->device));
+    const size_t n = (size_t)RES_PMAX * RES_PROF_N;
+    if (out) {
+        std::vector<unsigned long long> h(n, 0ull);
+        if (c->res_prof) {
+            CUCK(cudaStreamSynchronize(c->stream));
+            CUCK(cudaMemcpy(h.data(), c->res_prof, n * 8, cudaMemcpyDeviceToHost));
+        }
+        // [k]: CTA 0's total of phase k (us); [12 + k]: the largest total over the CTAs
+        for (int k = 0; k < 24; k++) out[k] = 0.0;
+        for (int k = 0; k < RES_PROF_N && k < 12; k++) {
+            const double f = k == RES_PROF_ITERS ? 1.0 : 1e-3;
+            out[k] = h[k] * f;
+            unsigned long long mx = 0;
+            for (int b = 0; b < RES_PMAX; b++) mx = std::max(mx, h[(size_t)b * RES_PROF_N + k]);
+            out[12 + k] = mx * f;
+        }
+    }
+    if (enable && !c->res_prof) CUCK(cudaMalloc(&c->res_prof, n * 8));
+    if (enable) CUCK(cudaMemset(c->res_prof, 0, n * 8));
+    if (!enable && c->res_prof) { cudaFree(c->res_prof); c->res_prof = nullptr; }
+    c->sys0.key_valid = false;
     return HF_OK;
 }
 

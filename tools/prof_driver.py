@@ -28,6 +28,21 @@ if mode == "sim":
     u = torch.zeros(p.grid.n_nodes, dtype=torch.float64, device=dev)
     st = hf.hf_simulate(ctx, p.theta, p.dt, steps, F, u)
     print(st)
+elif mode == "sim512":
+    # C4 grid (512^3 nodes), two materials i.i.d. per element as bench.c4_steps, 1 CN step
+    g = synth.c4_grid(512)
+    gen = torch.Generator(device=dev).manual_seed(3)
+    ox = torch.rand(g.n_elems, device=dev, generator=gen) < 0.2
+    k = torch.where(ox, synth.OXIDE[1], synth.STEEL[1]).to(torch.float64)
+    c = torch.where(ox, synth.OXIDE[0], synth.STEEL[0]).to(torch.float64)
+    del ox
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_coefficients(ctx, k, c)
+    del k, c
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=dev)
+    hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+    u = torch.zeros(g.n_nodes, dtype=torch.float64, device=dev)
+    print(hf.hf_simulate(ctx, 0.5, 0.01, steps, F, u))
 elif mode.startswith("apply"):
     n = int(mode[5:] or 512)
     g = synth.c4_grid(n)
