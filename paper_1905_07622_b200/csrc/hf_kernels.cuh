@@ -707,6 +707,7 @@ enum {
     FL_HB = 4,     // EP_APPLY: y = c A u + s b (else y = c A u)
     FL_DSET = 8,   // EP_APPLY with FL_DIR: y_D = g (else y_D = u_D, identity rows)
     FL_FUSEB = 16, // EP_CGA: kernel B's work follows in the same launch after a grid barrier
+    FL_PEER = 32,  // slab over peer memory: sums / ghost planes through the mailboxes (a.sy.peer)
 };
 
 // ---- PCG kernel B: x += alpha d; r -= alpha q; s = P^{-1} r; r^T s, r^T r ---------------
@@ -723,7 +724,7 @@ enum {
 // directly); glob: also do the loop duties (fused A+B launch, one system).
 // FUSED: d and q were written by other CTAs of the same launch before a grid barrier, so they
 // are read through L2 (ld.cg), never through the non-coherent read-only path.
-template <int NT, class Real, bool FUSED>
+template <int NT, class Real, bool FUSED, bool PEER = false>
 __device__ __forceinline__ void cg_b_work(const BArgs &a, CgState *sst, bool one_sys, long long base, int blk,
                                           int nblk, int pblk, int tid, int it, int re, int step, double delta,
                                           double dq, bool glob)
@@ -797,7 +798,7 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, CgState *sst, bool one
                 acc[1] = fma((double)rv[k].y, (double)rv[k].y, acc[1]);
                 *reinterpret_cast<V2 *>(rv_ + i) = rv[k];
                 *reinterpret_cast<V2 *>(sv_ + i) = sv;
-                if (a.sy.peer) {
+                if (PEER) {
                     peer_ghost<Real>(a.sy.peer, i, sv.x);
                     peer_ghost<Real>(a.sy.peer, i + 1, sv.y);
                 }
@@ -806,7 +807,7 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, CgState *sst, bool one
     }
     pdl_trigger();
     if (!replace) block_reduce_store<NT>(acc, a.sy.pout, pblk);
-    if (!replace && a.sy.peer) peer_publish<NT>(a.sy.peer, a.sy.pout, nblk);
+    if (PEER && !replace) peer_publish<NT>(a.sy.peer, a.sy.pout, nblk);
     if (blk == 0 && tid == 0) {
         sst->alpha = alpha;
         sst->dq = dq;
@@ -820,7 +821,7 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, CgState *sst, bool one
     }
 }
 
-template <int NT, class Real>
+template <int NT, class Real, bool PEER>
 __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
 {
     const int tid = threadIdx.x;
@@ -853,9 +854,9 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     if (hs.h0.x >= 0 || !hs.h0.y) return;          // this system failed earlier / has converged
     // alpha_i = delta_i / (d_i^T q_i)  (Alg. 1 line 8) from kernel A's partials of this system
     double ps[NPART];
-    if (a.sy.peer) peer_sums<NT>(a.sy.peer, ps);
+    if (PEER) peer_sums<NT>(a.sy.peer, ps);
     else prev_sums<NT>(a.sy, hd.h2.x, ps, sj);
-    cg_b_work<NT, Real, false>(a, sst, nsys == 1, (long long)sj * a.sysn, blk, bps, (int)blockIdx.x, tid, it, re,
+    cg_b_work<NT, Real, false, PEER>(a, sst, nsys == 1, (long long)sj * a.sysn, blk, bps, (int)blockIdx.x, tid, it, re,
                                step, sst->delta[it & 1], ps[0], false);
 }
 
@@ -934,7 +935,10 @@ k_stencil(const __grid_constant__ StencilArgs a)
     if (blk == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
     // warm the SM's descriptor cache for every map this launch may use (which node maps it
     // uses depends on the state header, read next): one prefetch per lane of warp 0
-    if (w == 0 && lane < NMAPS + 3) prefetch_map(a.tm + lane);
+    // (only descriptors that exist: kcn for EL_TETV, the ghost map on the peer transport)
+    constexpr bool PEER = (FL & FL_PEER) != 0;
+    if (w == 0 && (lane < NMAPS + 1 || (lane == MAP_KCN && EL == EL_TETV) || (lane == MAP_GHOST && PEER)))
+        prefetch_map(a.tm + lane);
     HF_TR(0);
 #ifdef HF_TRACE
     if (EP == EP_CGA && tid == 0 && blk < 4096) {
@@ -1042,7 +1046,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
         const int p = zb - 1 + it;
         Real *sb = stage + st * SH::STAGE_DBL;
         mbar_expect_tx(&bars[st], SH::STAGE_BYTES);
-        if (LD == LD_CGD && a.sy.peer && (p == a.gz_lo || p == a.gz_hi))   // s of a neighbour's plane
+        if (LD == LD_CGD && PEER && (p == a.gz_lo || p == a.gz_hi))   // s of a neighbour's plane
             tma_load_3d(sb, a.tm + MAP_GHOST, xb, Y0 - 1, p == a.gz_lo ? 0 : 1, &bars[st]);
         else if (NA >= 1) tma_load_3d(sb, a.tm + map0, xb, Y0 - 1, p, &bars[st]);
         if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, a.tm + map1, xb, Y0 - 1, p, &bars[st]);
@@ -1069,7 +1073,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     __syncthreads();
     // slab over peer memory: a CTA whose planes include a ghost plane of s waits for the
     // neighbours' data (and every rank's sums) before its first TMA; the others wait after
-    const PeerSync *const pp = a.sy.peer;
+    const PeerSync *const pp = PEER ? a.sy.peer : nullptr;
     double ps_peer[NPART];
     const bool peer_early = EP == EP_CGA && pp && ((a.gz_lo >= zb - 1 && a.gz_lo <= ze) || (a.gz_hi >= zb - 1 && a.gz_hi <= ze));
     if (peer_early) peer_sums<NT>(pp, ps_peer);

@@ -687,7 +687,15 @@ template <int R, int LD, int EP, int FL, int EL, class Real> static StencilFn st
     X(LD_RAW, EP_RESID_INIT, 0)                                                                 \
     X(LD_RAW, EP_RESID_INIT, FL_MASK | FL_DIR)                                                  \
     X(LD_RAW, EP_RESID, 0)                                                                      \
-    X(LD_RAW, EP_RESID, FL_MASK | FL_DIR)
+    X(LD_RAW, EP_RESID, FL_MASK | FL_DIR)                                                       \
+    X(LD_CGD, EP_CGA, FL_PEER)                                                                  \
+    X(LD_CGD, EP_CGA, FL_DIR | FL_PEER)                                                         \
+    X(LD_X0, EP_RESID_INIT, FL_PEER)                                                            \
+    X(LD_X0, EP_RESID_INIT, FL_MASK | FL_DIR | FL_PEER)                                         \
+    X(LD_RAW, EP_RESID_INIT, FL_PEER)                                                           \
+    X(LD_RAW, EP_RESID_INIT, FL_MASK | FL_DIR | FL_PEER)                                        \
+    X(LD_RAW, EP_RESID, FL_PEER)                                                                \
+    X(LD_RAW, EP_RESID, FL_MASK | FL_DIR | FL_PEER)
 
 template <class Real> static StencilFn stencil_fn_p(int R, int LD, int EP, int FL, int EL)
 {
@@ -846,6 +854,7 @@ static StencilArgs base_args(hf_ctx *c, double aK, double aM)
 static int dir_flags(const hf_ctx *c, int EP, bool has_b, bool dset)
 {
     int fl = has_b && EP == EP_APPLY ? FL_HB : 0;
+    if (EP != EP_APPLY && c->comm && c->comm->in_kernel()) fl |= FL_PEER;   // mailbox sums / ghosts
     if (c->dbits) {
         if (EP == EP_APPLY) { if (dset) fl |= FL_DIR | FL_DSET; }
         else if (EP == EP_CGA) fl |= FL_DIR;
@@ -1259,7 +1268,9 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
     if (rot) for (int i = 0; i < 3; i++) b.rot[i] = s.U[i];
     b.sy = make_sync(c, s, 0, 1);
     L->B = Launch();
-    L->B.fn = c->es == 8 ? (const void *)k_cg_b<256, double> : (const void *)k_cg_b<256, float>;
+    const bool peer = c->comm && c->comm->in_kernel();
+    L->B.fn = c->es == 8 ? (peer ? (const void *)k_cg_b<256, double, true> : (const void *)k_cg_b<256, double, false>)
+                         : (peer ? (const void *)k_cg_b<256, float, true> : (const void *)k_cg_b<256, float, false>);
     L->B.grid = dim3(b_blocks(c));
     L->B.block = dim3(256);
     L->B.add(b);
