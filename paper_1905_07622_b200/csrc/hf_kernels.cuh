@@ -436,7 +436,10 @@ __device__ __forceinline__ void reduce_prev(const double *part, int n, double (&
     // trip for n <= KU * NT); the per-thread order stays b = tid, tid + NT, ... (fixed).  Every
     // block of the grid reads the same partials: through the read-only (L1) path, not L2-only
     // (-0.6 us per C3 iteration); they are written by the previous kernel only.
-    constexpr int KU = 4;
+#ifndef HF_RP_KU
+#define HF_RP_KU 4
+#endif
+    constexpr int KU = HF_RP_KU;
     static_assert(NPART == 4, "partials are read as 2 x double2");
     for (int b0 = tid; b0 < n; b0 += KU * NT) {
         double2 v[KU][2];

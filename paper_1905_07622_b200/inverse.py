@@ -96,30 +96,51 @@ class MHResult:
     forward_calls: int
 
 
+def chain_generators(seed: int, chain_ids: Sequence[int]) -> list:
+    """One random stream per chain (numpy SeedSequence of (seed, chain id)): a chain draws the
+    same proposals and acceptance variates whichever process or batch it runs in."""
+    return [np.random.default_rng([int(seed), int(c)]) for c in chain_ids]
+
+
 def metropolis_hastings(loglik_batch: Callable[[np.ndarray], np.ndarray], theta0: Sequence[float],
                         lo: float, hi: float, n_samples: int, burn_in: int, step: float,
-                        rng: np.random.Generator) -> MHResult:
+                        rng: Optional[np.random.Generator], chain_rngs: Optional[Sequence] = None) -> MHResult:
     """theta_{i+1} = theta_hat with probability min(1, p(D|theta_hat)/p(D|theta_i)), else theta_i
     (P:363-364); uniform prior on [lo, hi]: proposals outside are rejected (their
     likelihood is never used).  loglik_batch evaluates a vector of candidate thetas (one batched
     GPU call) of a FIXED size, one per chain: an outside proposal is evaluated at its clipped
     value and discarded, so every forward batch has the same shape (the same stack grouping and
-    reduction order) whatever the number of proposals inside the prior."""
+    reduction order) whatever the number of proposals inside the prior.
+    Random numbers: one generator for all chains (rng), or one per chain (chain_rngs, see
+    chain_generators) so that chains can be split over processes without changing them."""
     theta = np.asarray(theta0, dtype=np.float64).copy()
     chains = theta.size
+    if chain_rngs is not None and len(chain_rngs) != chains:
+        raise ValueError("chain_rngs: one generator per chain")
+
+    def normals():
+        if chain_rngs is None:
+            return rng.standard_normal(chains)
+        return np.array([g.standard_normal() for g in chain_rngs])
+
+    def uniforms():
+        if chain_rngs is None:
+            return rng.uniform(size=chains)
+        return np.array([g.uniform() for g in chain_rngs])
+
     ll = loglik_batch(theta)
     calls = chains
     out, outll = [], []
     acc = 0
     total = 0
     for it in range(burn_in + n_samples):
-        prop = theta + step * rng.standard_normal(chains)
+        prop = theta + step * normals()
         inside = (prop >= lo) & (prop <= hi)
         llp = np.full(chains, -np.inf)
         if inside.any():
             llp = np.where(inside, loglik_batch(np.clip(prop, lo, hi)), -np.inf)
             calls += chains
-        logu = np.log(rng.uniform(size=chains))
+        logu = np.log(uniforms())
         take = inside & (logu < llp - ll)
         theta = np.where(take, prop, theta)
         ll = np.where(take, llp, ll)
@@ -230,3 +251,53 @@ def invert(forward: CorrosionForward, camera: Camera, data: np.ndarray, chains: 
 
     theta0 = np.full(chains, 0.5 * forward.thickness)      # "middle of the prior"
     return metropolis_hastings(ll, theta0, 0.0, forward.thickness, n_samples, burn_in, step, rng)
+
+
+def chain_range(chains: int, rank: int, world: int) -> range:
+    """The chains of one process: contiguous, sizes differing by at most one."""
+    return range(rank * chains // world, (rank + 1) * chains // world)
+
+
+def mh_distributed(loglik_batch: Callable[[np.ndarray], np.ndarray], chains: int, theta0: float, lo: float,
+                   hi: float, n_samples: int, burn_in: int, step: float, seed: int, group=None) -> MHResult:
+    """Metropolis-Hastings with the chains split over the processes of a torch.distributed group
+    (one GPU per process, each with its own forward model): the chains are independent, so the
+    only communication is the final gather of the samples (all_gather_object, any backend).
+    Every chain uses its own random stream (chain_generators), so the gathered result equals a
+    single-process run of the same chains batched the same way."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    mine = chain_range(chains, rank, world)
+    res = None
+    if len(mine):
+        res = metropolis_hastings(loglik_batch, np.full(len(mine), float(theta0)), lo, hi, n_samples, burn_in,
+                                  step, None, chain_generators(seed, mine))
+    part = None if res is None else (list(mine), res.samples, res.loglik, res.accept_rate, res.forward_calls)
+    parts = [None] * world
+    dist.all_gather_object(parts, part, group=group)
+    samples = np.zeros((n_samples, chains))
+    loglik = np.zeros((n_samples, chains))
+    acc, calls = 0.0, 0
+    for pr in parts:
+        if pr is None:
+            continue
+        ids, smp, ll, rate, nc = pr
+        samples[:, ids] = smp
+        loglik[:, ids] = ll
+        acc += rate * len(ids) * n_samples
+        calls += nc
+    return MHResult(samples, acc / max(chains * n_samples, 1), loglik, calls)
+
+
+def invert_distributed(forward: CorrosionForward, camera: Camera, data: np.ndarray, chains: int = 8,
+                       n_samples: int = 200, burn_in: int = 50, step: float = 0.3, seed: int = 0,
+                       group=None) -> MHResult:
+    """invert() with the chains spread over the ranks of a process group, one GPU each (the
+    rank's forward model lives on its own device): P:362-376 with the chains/ensemble filling
+    the GPUs of one node."""
+    def ll(thetas):
+        fr = forward.fronts(thetas)
+        return np.array([camera.loglik(data, f) for f in fr])
+
+    return mh_distributed(ll, chains, 0.5 * forward.thickness, 0.0, forward.thickness, n_samples, burn_in, step,
+                          seed, group)
