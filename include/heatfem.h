@@ -321,14 +321,30 @@ hf_status hf_time_kernel_a(hf_ctx *ctx, int32_t reps, double *ms_per_launch);
  * Profiling (hf_profile) and the NCCL slab transport always use the host loop. */
 hf_status hf_set_driver(hf_ctx *ctx, int32_t driver);
 
-/* On-chip PCG (the default where eligible): hf_simulate* runs each time step's whole PCG solve
+/* Mixed precision (NEXT row f3 at the fp64 bar): enable = 1 gives this fp64 context an fp32
+ * shadow (same grid, coefficients, Dirichlet faces, element; every later setter is forwarded).
+ * hf_simulate* then solves each time step in two stages on the device: the fp32 PCG (fp32
+ * storage, fp64 reductions) from the extrapolated guess to rtol_lo (or the call's rtol if larger),
+ * and the fp64 PCG from the fp32 iterate to the call's rtol.  The fp64 residual of the fp64
+ * operator decides convergence (defect correction), so results have the fp64 path's accuracy
+ * (reading R18); the fp32 stage carries most of the error reduction at half the bytes.  Call
+ * before the coefficients; enable = 0 removes the shadow.  Graph driver only (the host-loop
+ * driver runs plain fp64).  Errors: HF_E_ARG, HF_E_STATE (fp32 / slab / stacked context, or
+ * coefficients already set), HF_E_CUDA. */
+hf_status hf_set_mixed(hf_ctx *ctx, int32_t enable, double rtol_lo);
+
+/* PCG iterations of the fp32 stage since hf_set_mixed (device counter; synchronises). */
+hf_status hf_mixed_iters(hf_ctx *ctx, int64_t *lo_iters);
+
+/* On-chip PCG (opt-in, hf_set_resident): hf_simulate* runs each time step's whole PCG solve
  * (Alg. 1) in ONE cooperative launch whose CTAs (one per SM) keep d (+ a one-node
- * halo), x, q/s, r and the material ids of their brick of the grid in shared memory and
- * registers; the Alg. 1 reductions ride on two grid barriers per iteration.  Same operator,
+ * halo), r, q/s and the material ids of their brick of the grid in shared memory (x in the
+ * L2-resident output vector); the Alg. 1 reductions ride on two grid barriers per iteration.  Same operator,
  * readings (R3-R6) and stop test as the streaming kernels; results agree to rounding order.
  * Eligible: fp64 Q1 with materials by id (hf_set_material_ids), one system, no slab transport,
  * graph driver, and a grid whose brick partition fits (<= 31 x 25 x 16 nodes per brick, one brick
- * per SM: about 1.1M nodes on 148 SMs).  mode 0 = never (streaming kernels), 1 = when eligible.
+ * per SM: about 1.1M nodes on 148 SMs).  mode 0 = never (streaming kernels, the default), 1 = when
+ * eligible.  Measured slower than the streaming kernels at C3.
  * Errors: HF_E_ARG. */
 hf_status hf_set_resident(hf_ctx *ctx, int32_t mode);
 

@@ -82,6 +82,8 @@ _SIGS = {
     "hf_profile_read": (_i32, [_vp, _P(C.c_double * 5), _P(C.c_int64 * 5)]),
     "hf_set_driver": (_i32, [_vp, _i32]),
     "hf_set_resident": (_i32, [_vp, _i32]),
+    "hf_set_mixed": (_i32, [_vp, _i32, _d]),
+    "hf_mixed_iters": (_i32, [_vp, _P(C.c_int64)]),
     "hf_resident_plan": (_i32, [_vp, _P(C.c_int32)]),
     "hf_resident_profile": (_i32, [_vp, _i32, _P(C.c_double)]),
     "hf_flush_l2": (_i32, [_vp]),
@@ -436,6 +438,16 @@ def hf_profile_read(ctx: Context):
 
 def hf_set_driver(ctx: Context, driver: int):
     _check(_lib.hf_set_driver(ctx.ptr, driver))
+
+
+def hf_set_mixed(ctx: Context, enable: int, rtol_lo: float = 1e-6):
+    _check(_lib.hf_set_mixed(ctx.ptr, enable, rtol_lo))
+
+
+def hf_mixed_iters(ctx: Context) -> int:
+    v = C.c_int64()
+    _check(_lib.hf_mixed_iters(ctx.ptr, C.byref(v)))
+    return int(v.value)
 
 
 def hf_set_resident(ctx: Context, mode: int):

@@ -1878,6 +1878,53 @@ __global__ void k_step_commit(Sync sy, int *iters_out)
     if (j == 0) st0->step = step + 1;
 }
 
+// ---- mixed precision (hf_set_mixed, NEXT row f3): fp32 correction, fp64 finish ---------------
+// The fp64 context (hi) owns an fp32 shadow (lo) with the same grid, coefficients and Dirichlet
+// faces.  Per time step (defect correction): hi's RHS and init kernels give x0 = 2u^n - u^(n-1)
+// (in U[(n+1) % 3]) and its fp64 residual r0 = b - A x0; k_mix_in hands r0 to the fp32 PCG,
+// which solves A e = r0 from e = 0 to rtol_lo; k_mix_out adds e to x0 in fp64; hi's PCG then
+// finishes from x0 + e to rtol with the fp64 residual of the fp64 operator deciding, so the
+// result has the fp64 path's accuracy while most of the error reduction ran on half the bytes.
+struct MixArgs {
+    int nx1, ny1, nzl;
+    int pitch_hi, pitch_lo;          // row pitches of the two layouts
+    long long plane_hi, plane_lo;
+    const double *rhi;               // hi r0 = b - A x0 (after hi's init kernel)
+    double *ring[3];                 // hi time-step ring: x0 in U[(step + 1) % 3]
+    const CgState *st;               // hi state (step counter)
+    float *blo, *xlo;                // lo right-hand side (r0) and iterate (e)
+    const CgState *stlo;             // lo state (iterations of the fp32 solve)
+    unsigned long long *lo_iters;    // accumulated fp32 iterations
+    unsigned long long *launches;
+};
+
+__global__ void k_mix_in(const MixArgs a)
+{
+    const long long n = (long long)a.nx1 * a.ny1 * a.nzl;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && a.launches) atomicAdd(a.launches, 1ull);
+    if (i >= n) return;
+    const int x = (int)(i % a.nx1), y = (int)((i / a.nx1) % a.ny1), z = (int)(i / ((long long)a.nx1 * a.ny1));
+    const long long h = z * a.plane_hi + (long long)y * a.pitch_hi + x, l = z * a.plane_lo + (long long)y * a.pitch_lo + x;
+    a.blo[l] = (float)a.rhi[h];
+    a.xlo[l] = 0.0f;
+}
+
+__global__ void k_mix_out(const MixArgs a)
+{
+    const long long n = (long long)a.nx1 * a.ny1 * a.nzl;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        if (a.launches) atomicAdd(a.launches, 1ull);
+        if (a.lo_iters) atomicAdd(a.lo_iters, (unsigned long long)a.stlo->iter);
+    }
+    if (i >= n) return;
+    const int x = (int)(i % a.nx1), y = (int)((i / a.nx1) % a.ny1), z = (int)(i / ((long long)a.nx1 * a.ny1));
+    const long long h = z * a.plane_hi + (long long)y * a.pitch_hi + x, l = z * a.plane_lo + (long long)y * a.pitch_lo + x;
+    double *xv = a.ring[(a.st->step + 1) % 3];
+    xv[h] += (double)a.xlo[l];
+}
+
 // ---- c lane of the packed (k, c) pairs back to a plain per-element fp64 array ----------------
 template <class Real>
 __global__ void k_extract_c(Geom g, int nz, const void *kcp, double *c, unsigned long long *launches)
@@ -1890,6 +1937,20 @@ __global__ void k_extract_c(Geom g, int nz, const void *kcp, double *c, unsigned
     if (e >= ne) return;
     const int ex = (int)(e % g.nx), ey = (int)((e / g.nx) % g.ny), ez = (int)(e / ((long long)g.nx * g.ny));
     c[e] = (double)kc[((long long)(ez - g.zg0 + 1) * g.ny + ey) * g.kpitch + ex].y;
+}
+
+// both lanes (k and c) of the fp64 pairs back to plain per-element arrays (the mixed-precision
+// shadow of a context whose coefficients came as material ids)
+__global__ void k_extract_kc(Geom g, int nz, const double2 *kc, double *k, double *c, unsigned long long *launches)
+{
+    const long long ne = (long long)g.nx * g.ny * nz;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e == 0 && launches) atomicAdd(launches, 1ull);
+    if (e >= ne) return;
+    const int ex = (int)(e % g.nx), ey = (int)((e / g.nx) % g.ny), ez = (int)(e / ((long long)g.nx * g.ny));
+    const double2 v = kc[((long long)(ez - g.zg0 + 1) * g.ny + ey) * g.kpitch + ex];
+    k[e] = v.x;
+    c[e] = v.y;
 }
 
 // ---- boundary conversions of the fp32 variant: user fp64 (natural pitch) <-> internal Real ----

@@ -254,6 +254,13 @@ struct hf_ctx {
     int last_resident = 0;           // the last hf_simulate* ran the on-chip PCG
     ResSync *rsync = nullptr;        // flags + partials of the on-chip PCG's grid reductions
     unsigned long long *res_prof = nullptr;   // per-phase timer of the on-chip PCG (hf_resident_profile)
+    // mixed precision (hf_set_mixed): the fp32 shadow context, its stop tolerance, its iteration
+    // counter, and the per-step graph of [RHS -> fp32 solve] (the fp64 finish is sys0's graph)
+    hf_ctx *lo = nullptr;
+    double mix_rtol = 1e-6;
+    unsigned long long *mix_iters = nullptr;
+    cudaGraph_t mix_graph = nullptr;
+    cudaGraphExec_t mix_exec = nullptr;
     int nsys = 1;                    // systems stacked along z (batched forward simulations, a13)
     int sys_planes = 0;              // local node planes per system (= nzl for one system)
     int rank = 0, nranks = 1;
@@ -1173,6 +1180,10 @@ static void ctx_free(hf_ctx *c)
     cudaFree(c->kid);
     cudaFree(c->rsync);
     cudaFree(c->res_prof);
+    cudaFree(c->mix_iters);
+    if (c->mix_exec) cudaGraphExecDestroy(c->mix_exec);
+    if (c->mix_graph) cudaGraphDestroy(c->mix_graph);
+    if (c->lo) { ctx_free(c->lo); delete c->lo; c->lo = nullptr; }
     for (auto &kv : c->stacks) { ctx_free(kv.second); delete kv.second; }
     c->stacks.clear();
     delete c->comm;
@@ -1650,6 +1661,7 @@ hf_status hf_set_coefficients(hf_ctx *c, const double *k, const double *cc)
     }
     c->coef_set = true;
     c->ab_ready = false;
+    if (c->lo) HFCK(hf_set_coefficients(c->lo, k, cc));    // mixed precision: the fp32 shadow
     return HF_OK;
 }
 
@@ -1709,6 +1721,17 @@ hf_status hf_set_material_ids(hf_ctx *c, const uint8_t *ids, int32_t nmat, const
     c->sys0.key_valid = false;
     c->coef_set = true;
     c->ab_ready = false;
+    if (c->lo) {                                // mixed precision: the fp32 shadow takes (k, c) pairs
+        const size_t ne = (size_t)(c->g.ne[0] * c->g.ne[1] * c->g.ne[2]);
+        void *kp, *cp;
+        HFCK(scratch_get(c, 55, ne * sizeof(double), &kp));
+        HFCK(scratch_get(c, 56, ne * sizeof(double), &cp));
+        k_extract_kc<<<(unsigned)((ne + 255) / 256), 256, 0, c->stream>>>(make_geom(c), (int)c->g.ne[2],
+            (const double2 *)c->sys0.kc, (double *)kp, (double *)cp, c->launches);
+        CUCK(cudaGetLastError());
+        CUCK(cudaStreamSynchronize(c->stream));
+        HFCK(hf_set_coefficients(c->lo, (const double *)kp, (const double *)cp));
+    }
     return HF_OK;
 }
 
@@ -1748,6 +1771,7 @@ hf_status hf_set_vertex_coefficients(hf_ctx *c, const double *k, const double *c
     s.key_valid = false;
     c->coef_set = true;
     c->ab_ready = false;
+    if (c->lo) HFCK(hf_set_vertex_coefficients(c->lo, k, cc));
     return HF_OK;
 }
 
@@ -1758,6 +1782,7 @@ hf_status hf_set_dirichlet_faces(hf_ctx *c, uint32_t bits, const double values[6
     for (int f = 0; f < 6; f++) c->gval[f] = values ? values[f] : 0.0;
     drop_stacks(c);
     c->sys0.key_valid = false;
+    if (c->lo) HFCK(hf_set_dirichlet_faces(c->lo, bits, values));
     return HF_OK;
 }
 
@@ -2150,9 +2175,17 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     key.snap_plane = snap_local; key.lift = lift; key.F = dF; key.snap = snapdev;
     ResPlan rp;
     if (use_graph && &s == &c->sys0) rp = res_plan(c);
-    key.res = rp.ok;
+    // mixed precision (hf_set_mixed): [RHS -> fp32 solve] graph + the fp64 finish graph
+    const bool mixed = c->lo && use_graph && &s == &c->sys0 && !rp.ok;
+    key.res = rp.ok + 2 * (int)mixed;
     c->last_resident = rp.ok;
-    const bool cached = use_graph && s.key_valid && s.key == key && s.gexec;
+    const bool cached = use_graph && s.key_valid && s.key == key && s.gexec && (!mixed || c->mix_exec);
+    if (mixed) {
+        // the fp32 shadow's solver state and Jacobi diagonal (same operator, fp32 storage)
+        hf_cg_opts lo_o = {std::max(c->mix_rtol, o.rtol), o.max_iter, -1};
+        HFCK(set_solver_opts(c->lo, c->lo->sys0, lo_o));
+        HFCK(enqueue_diag(c->lo, c->lo->sys0, aK, aM, nullptr, c->lo->sys0.invd));
+    }
 
     std::vector<Launch> pre, post;
     Launch init;
@@ -2195,6 +2228,59 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
         ia.zs0 = c->own_lo - (c->own_lo > 0 ? 1 : 0);
         ia.zs1 = c->own_hi + (c->own_hi < c->nzl ? 1 : 0);
         HFCK(stencil_launch(c, LD_X0, EP_RESID_INIT, true, s.maps, ia, 2, &init));
+        if (mixed) {
+            // fp32 stage (defect correction): r0 of the extrapolated guess to fp32 (k_mix_in),
+            // the fp32 PCG for A e = r0 from e = 0, x0 += e in fp64 (k_mix_out)
+            hf_ctx *lo = c->lo;
+            Sys &ls = lo->sys0;
+            MixArgs ma;
+            std::memset(&ma, 0, sizeof(ma));
+            ma.nx1 = c->nx1; ma.ny1 = c->ny1; ma.nzl = c->nzl;
+            ma.pitch_hi = c->pitch; ma.pitch_lo = lo->pitch;
+            ma.plane_hi = c->plane; ma.plane_lo = lo->plane;
+            ma.rhi = s.r;
+            for (int i = 0; i < 3; i++) ma.ring[i] = s.U[i];
+            ma.st = s.st;
+            ma.blo = (float *)ls.b;
+            ma.xlo = (float *)ls.U[0];
+            ma.stlo = ls.st;
+            ma.lo_iters = c->mix_iters;
+            ma.launches = c->launches;
+            const long long nn = (long long)c->nx1 * c->ny1 * c->nzl;
+            Launch Min, Mout;
+            Min.fn = (const void *)k_mix_in;
+            Mout.fn = (const void *)k_mix_out;
+            Min.grid = Mout.grid = dim3((unsigned)((nn + 255) / 256));
+            Min.block = Mout.block = dim3(256);
+            Min.add(ma);
+            Mout.add(ma);
+            std::vector<Launch> mpre = pre;
+            mpre.push_back(init);                     // x0 -> U[(n+1) % 3], r0 = b - A x0 (fp64)
+            mpre.push_back(Min);
+            pre.clear();
+            StencilArgs li = base_args(lo, aK, aM);
+            li.invd = ls.invd;
+            li.bvec = ls.b;
+            li.out0 = ls.r;
+            li.out_s = ls.s;
+            li.xout = ls.U[0];
+            li.sy = make_sync(lo, ls, -1, 1);
+            Launch linit;
+            HFCK(stencil_launch(lo, LD_RAW, EP_RESID_INIT, true, ls.maps, li, 2, &linit));
+            CgLaunches LL;
+            HFCK(cg_launches(lo, ls, aK, aM, ls.U[0], ls.maps, &LL));
+            if (c->mix_exec) { cudaGraphExecDestroy(c->mix_exec); c->mix_exec = nullptr; }
+            if (c->mix_graph) { cudaGraphDestroy(c->mix_graph); c->mix_graph = nullptr; }
+            HFCK(build_cg_graph(lo, mpre, linit, LL, {Mout}, resolved(lo, hf_cg_opts{0.0, 0, -1}).replace_every,
+                                 &c->mix_graph));
+            CUCK(cudaGraphInstantiate(&c->mix_exec, c->mix_graph, 0));
+        }
+        if (mixed) {
+            // the fp64 finish: init from x0 + e, already in U[(n+1) % 3]
+            ia.rot_role = ROT_X;
+            ia.zs0 = ia.zs1 = 0;
+            HFCK(stencil_launch(c, LD_RAW, EP_RESID_INIT, true, s.maps, ia, 2, &init));
+        }
         if (!rp.ok) HFCK(cg_launches(c, s, aK, aM, nullptr, s.maps, &L));
         post = step_launches(c, step_args(c, s, nullptr, snapdev, snap_local), true);
     }
@@ -2231,6 +2317,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             for (int n = 0; n < nsteps; n++) {
                 CUCK(cudaMemsetAsync(c->flush, n & 1, fb, s.stream));
                 CUCK(cudaEventRecord(ev[2 * n], s.stream));
+                if (mixed) CUCK(cudaGraphLaunch(c->mix_exec, s.stream));
                 CUCK(cudaGraphLaunch(s.gexec, s.stream));
                 CUCK(cudaEventRecord(ev[2 * n + 1], s.stream));
             }
@@ -2244,7 +2331,10 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             for (auto &e : ev) cudaEventDestroy(e);
             c->last_ms_steps = tot;
         } else {
-            for (int n = 0; n < nsteps; n++) CUCK(cudaGraphLaunch(s.gexec, s.stream));
+            for (int n = 0; n < nsteps; n++) {
+                if (mixed) CUCK(cudaGraphLaunch(c->mix_exec, s.stream));
+                CUCK(cudaGraphLaunch(s.gexec, s.stream));
+            }
         }
     } else {
         for (int n = 0; n < nsteps; n++) {
@@ -2968,6 +3058,7 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
     }
     HFCK(update_occ(c));
     c->sys0.key_valid = false;
+    if (c->lo) HFCK(hf_set_element(c->lo, type));
     return HF_OK;
 }
 
@@ -3041,6 +3132,49 @@ hf_status hf_resident_profile(hf_ctx *c, int32_t enable, double out[24])
     if (enable) CUCK(cudaMemset(c->res_prof, 0, n * 8));
     if (!enable && c->res_prof) { cudaFree(c->res_prof); c->res_prof = nullptr; }
     c->sys0.key_valid = false;
+    return HF_OK;
+}
+
+hf_status hf_set_mixed(hf_ctx *c, int32_t enable, double rtol_lo)
+{
+    if (!c || (enable && !(rtol_lo > 0.0 && rtol_lo < 1.0))) return fail(HF_E_ARG, "hf_set_mixed: bad argument");
+    CUCK(cudaSetDevice(c->device));
+    CUCK(cudaStreamSynchronize(c->stream));
+    c->sys0.key_valid = false;
+    if (!enable) {
+        if (c->mix_exec) { cudaGraphExecDestroy(c->mix_exec); c->mix_exec = nullptr; }
+        if (c->mix_graph) { cudaGraphDestroy(c->mix_graph); c->mix_graph = nullptr; }
+        if (c->lo) { ctx_free(c->lo); delete c->lo; c->lo = nullptr; }
+        return HF_OK;
+    }
+    if (c->prec != 64 || c->nsys != 1 || c->comm)
+        return fail(HF_E_STATE, "hf_set_mixed: needs a single-GPU fp64 context with one system");
+    if (c->coef_set) return fail(HF_E_STATE, "hf_set_mixed: call before the coefficients are set");
+    c->mix_rtol = rtol_lo;
+    if (!c->lo) {
+        hf_ctx *lo = new hf_ctx();
+        hf_status st = ctx_init(lo, &c->g, c->device, c->stream, 0, 1);
+        if (st == HF_OK) st = hf_set_precision(lo, 32);
+        if (st == HF_OK && c->dbits) st = hf_set_dirichlet_faces(lo, c->dbits, c->gval);
+        if (st == HF_OK && c->elem != EL_Q1) st = hf_set_element(lo, c->elem);
+        if (st != HF_OK) { ctx_free(lo); delete lo; return st; }
+        c->lo = lo;
+    }
+    if (!c->mix_iters) CUCK(cudaMalloc(&c->mix_iters, sizeof(unsigned long long)));
+    CUCK(cudaMemset(c->mix_iters, 0, sizeof(unsigned long long)));
+    return HF_OK;
+}
+
+hf_status hf_mixed_iters(hf_ctx *c, int64_t *lo_iters)
+{
+    if (!c || !lo_iters) return fail(HF_E_ARG, "hf_mixed_iters: NULL argument");
+    *lo_iters = 0;
+    if (!c->mix_iters) return HF_OK;
+    CUCK(cudaSetDevice(c->device));
+    CUCK(cudaStreamSynchronize(c->stream));
+    unsigned long long v = 0;
+    CUCK(cudaMemcpy(&v, c->mix_iters, sizeof(v), cudaMemcpyDeviceToHost));
+    *lo_iters = (int64_t)v;
     return HF_OK;
 }
 

@@ -207,3 +207,74 @@ def test_fp32_slab_local_transport():
     assert rel(full, uo) <= BAR
     del ctxs
     hf.hf_local_group_destroy(grp)
+
+
+# ---- mixed precision (hf_set_mixed): fp32 PCG stage + fp64 finish -------------------------------
+
+def _mixed_run(p, mixed=True, rtol_lo=1e-6, nsteps=None):
+    ctx = hf.hf_create(p.grid, 0)
+    if mixed:
+        hf.hf_set_mixed(ctx, 1, rtol_lo)
+    if p.dirichlet_bits:
+        hf.hf_set_dirichlet_faces(ctx, p.dirichlet_bits, p.dirichlet_values)
+    hf.hf_set_coefficients(ctx, T(p.k), T(p.c))
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
+    u = T(p.u0)
+    n = p.nsteps if nsteps is None else nsteps
+    st = hf.hf_simulate(ctx, p.theta, p.dt, n, F, u, rtol=p.rtol)
+    return u.cpu().numpy(), st, (hf.hf_mixed_iters(ctx) if mixed else 0)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_mixed_meets_the_fp64_bar(cfg):
+    """C1 (kappa ~ 300, where plain fp32 storage stalls at ~4e-5) and C2 (Dirichlet): the fp64
+    finish takes x0 + e (e: the fp32 correction) to rtol 1e-12, so the result meets the fp64 bar
+    (1e-10) and therefore the fp32 one (1e-5, north_star).  (On these small, quickly converging
+    grids the fp32 stage does not save fp64 iterations: the rounding noise it leaves spreads over
+    the whole spectrum, while the extrapolated guess's error is smooth.)"""
+    p = getattr(synth, cfg)()
+    u, st, lo_it = _mixed_run(p)
+    o, F = oracle.problem_oracle(p)
+    uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, F, p.u0, tol=p.rtol)
+    assert rel(u, uo) <= 1e-10, rel(u, uo)
+    assert lo_it > 0
+    u64, st64, _ = _mixed_run(p, mixed=False)
+    print(f"\n[mixed {cfg}] fp32 iterations {lo_it}, fp64 iterations {st['total_iters']} "
+          f"(fp64 alone {st64['total_iters']}), rel-L2 vs oracle {rel(u, uo):.2e}")
+
+
+def test_mixed_c3_two_steps():
+    p = synth.c3(nsteps=2)
+    u, st, lo_it = _mixed_run(p)
+    o, F = oracle.problem_oracle(p)
+    uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, F, p.u0, tol=p.rtol)
+    assert rel(u, uo) <= 1e-10, rel(u, uo)
+    _, st64, _ = _mixed_run(p, mixed=False)
+    print(f"\n[mixed c3] fp32 iterations {lo_it}, fp64 iterations {st['total_iters']} "
+          f"(fp64 alone {st64['total_iters']})")
+
+
+def test_mixed_setter_order_and_forwarding():
+    g = synth.c1().grid
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_coefficients(ctx, T(np.ones(g.n_elems)), T(np.ones(g.n_elems)))
+    with pytest.raises(hf.HfError):
+        hf.hf_set_mixed(ctx, 1, 1e-6)                    # after the coefficients: HF_E_STATE
+    ctx32 = hf.hf_create(g, 0)
+    hf.hf_set_precision(ctx32, 32)
+    with pytest.raises(hf.HfError):
+        hf.hf_set_mixed(ctx32, 1, 1e-6)                  # fp32 context: HF_E_STATE
+    # materials by id are forwarded to the shadow as (k, c) pairs
+    p = synth.c1()
+    kc, inv = np.unique(np.stack([p.k, p.c], 1), axis=0, return_inverse=True)
+    ctx2 = hf.hf_create(p.grid, 0)
+    hf.hf_set_mixed(ctx2, 1, 1e-6)
+    hf.hf_set_material_ids(ctx2, inv.astype(np.uint8).ravel(), kc[:, 0], kc[:, 1])
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx2, p.flux_face, p.flux_const, None, F)
+    u = T(p.u0)
+    hf.hf_simulate(ctx2, p.theta, p.dt, p.nsteps, F, u, rtol=p.rtol)
+    o, Fo = oracle.problem_oracle(p)
+    uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
+    assert rel(u.cpu().numpy(), uo) <= 1e-10
