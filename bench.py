@@ -344,6 +344,8 @@ def run_ours(args):
             line["c5_batched_replicas"] = c5r
     if not slab:
         line["c3_other_coef"] = variant_c3(hf, torch, dev, 64, p.rtol, coef="pairs" if use_ids else "ids")
+        # the on-chip PCG (opt-in): one cooperative launch per time step
+        line["c3_resident_ids"] = variant_c3(hf, torch, dev, 64, p.rtol, steps=5, coef="ids", resident=True)
         line["apply_512"] = apply_512(hf, torch, dev, peak)
         line["apply_512_ids"] = apply_512(hf, torch, dev, peak, ids=True)
         line["c4_steps"] = c4_steps(hf, torch, dev, peak)
@@ -484,13 +486,18 @@ def _apply_time(hf, torch, dev, peak, ctx, g, u, y, es, ids=False):
                       % ("EL_Q1P, material ids" if ids else "EL_Q1, (k, c) pairs")}
 
 
-def variant_c3(hf, torch, dev, prec, rtol, steps=10, warm=3, coef="pairs"):
-    """C3 time steps of a precision / tolerance / coefficient-layout variant, L2 flushed before
-    each timed step."""
-    p = synth.c3(nsteps=steps + warm)
+def variant_c3(hf, torch, dev, prec, rtol, steps=10, warm=3, coef="pairs", mixed=None, resident=False, n=100):
+    """C3 time steps of a precision / tolerance / coefficient-layout / solver variant, L2 flushed
+    before each timed step.  mixed: rtol of the fp32 stage (hf_set_mixed); resident: the
+    on-chip PCG (hf_set_resident, material ids); n: nodes per axis."""
+    p = synth.c3(n_nodes_axis=n, nsteps=steps + warm)
     ctx = hf.hf_create(p.grid, dev.index)
     if prec != 64:
         hf.hf_set_precision(ctx, prec)
+    if mixed:
+        hf.hf_set_mixed(ctx, 1, mixed)
+    if resident:
+        hf.hf_set_resident(ctx, 1)
     if coef == "ids":
         hf.hf_set_material_ids(ctx, torch.tensor(p.extra["ids"], device=dev),
                                [m[1] for m in p.extra["materials"]], [m[0] for m in p.extra["materials"]])
@@ -501,14 +508,23 @@ def variant_c3(hf, torch, dev, prec, rtol, steps=10, warm=3, coef="pairs"):
     u = torch.zeros(p.grid.n_nodes, dtype=torch.float64, device=dev)
     up = torch.zeros_like(u)
     hf.hf_simulate_resume(ctx, p.theta, p.dt, warm, F, u, up, 0, rtol=rtol)
+    lo0 = hf.hf_mixed_iters(ctx) if mixed else 0
     hf.hf_set_step_flush(ctx, True)
     st = hf.hf_simulate_resume(ctx, p.theta, p.dt, steps, F, u, up, warm, rtol=rtol)
     hf.hf_set_step_flush(ctx, False)
+    out = {"precision": f"fp{prec}" if not mixed else "fp32 correction + fp64 finish", "coefficients": coef,
+           "rtol": rtol, "steps": steps, "nodes": p.grid.n_nodes,
+           "ms_per_step": st["ms_steps"] / steps,
+           "pcg_iters_per_step": st["total_iters"] / steps,
+           "us_per_pcg_iter": st["ms_steps"] / max(st["total_iters"], 1) * 1e3}
+    if mixed:
+        out["fp32_iters_per_step"] = (hf.hf_mixed_iters(ctx) - lo0) / steps
+        out["fp32_stage_rtol"] = mixed
+    if resident:
+        out["solver"] = "on-chip PCG (hf_set_resident)"
+        out["used"] = bool(hf.hf_resident_plan(ctx)["last_used"])
     del ctx
-    return {"precision": f"fp{prec}", "coefficients": coef, "rtol": rtol, "steps": steps,
-            "ms_per_step": st["ms_steps"] / steps,
-            "pcg_iters_per_step": st["total_iters"] / steps,
-            "us_per_pcg_iter": st["ms_steps"] / max(st["total_iters"], 1) * 1e3}
+    return out
 
 
 def fp32_variant(hf, torch, dev, peak):
@@ -517,7 +533,14 @@ def fp32_variant(hf, torch, dev, peak):
     return {"c3_fp32_rtol1e-6": variant_c3(hf, torch, dev, 32, 1e-6),
             "c3_fp64_rtol1e-6": variant_c3(hf, torch, dev, 64, 1e-6),
             "apply_512_fp32": apply_512(hf, torch, dev, peak, 32),
-            "parity": "fp32 vs the fp64 oracle: rel-L2 1.9e-7 after 2 C3 steps at rtol 1e-6 (bar 1e-5)"}
+            "parity": "fp32 vs the fp64 oracle: rel-L2 1.9e-7 after 2 C3 steps at rtol 1e-6 (bar 1e-5)",
+            # the fp64 result from mostly-fp32 work (hf_set_mixed, defect correction), rtol 1e-12,
+            # next to plain fp64 on the same grid: C3, and a 256^3 grid where iterations are
+            # bandwidth-bound (C3's are latency-bound)
+            "mixed_c3_rtol1e-12": variant_c3(hf, torch, dev, 64, 1e-12, steps=5, mixed=1e-5),
+            "mixed_256_rtol1e-12": variant_c3(hf, torch, dev, 64, 1e-12, steps=3, warm=2, mixed=1e-5, n=256),
+            "fp64_256_rtol1e-12": variant_c3(hf, torch, dev, 64, 1e-12, steps=3, warm=2, n=256),
+            "mixed_parity": "fp64 finish to rtol 1e-12: C1, C2, C3 within 1e-10 of the oracle (tests/test_gpu_fp32.py)"}
 
 
 def c4_steps(hf, torch, dev, peak, steps=2, rank=0, world=1, dist=None):
