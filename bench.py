@@ -37,20 +37,22 @@ METRIC = "ms per time step at 1M DOF (C3: 100^3-node heterogeneous cube, CN, Jac
 UNIT = "ms/step"
 
 
-def workload_config(p, n_gpus, extra=None):
-    cfg = {
+def workload_config(p):
+    """The workload the line is about (identical in both arms; measured quantities and the
+    implementation's parallelism are top-level keys of the line)."""
+    return {
         "workload": "C3 (BASELINE.json configs[2]): 100^3 nodes = 1,000,000 DoF, 99^3 trilinear voxels, "
                     "h=0.2 mm, 20% spherical Fe2O3 inclusions in steel (P:271), f=1 on z=0, theta=0.5, "
                     "dt=0.01, rtol=1e-12, guess 2u^n-u^(n-1)",
         "nodes": p.grid.n_nodes,
         "elements": p.grid.n_elems,
-        "parallelism": "single GPU" if n_gpus == 1 else f"z-slabs x{n_gpus} ({TRANSPORT_NAME})",
         "l2": "flushed (512 MiB memset) before every timed step; within a step the 104 MB working set "
               "stays L2-resident, as in any real run",
     }
-    if extra:
-        cfg.update(extra)
-    return cfg
+
+
+def parallelism(n_gpus):
+    return "single GPU" if n_gpus == 1 else f"z-slabs x{n_gpus} ({TRANSPORT_NAME})"
 
 
 # ---------------------------------------------------------------------------------------------
@@ -306,8 +308,10 @@ def run_ours(args):
             "data": "synthetic (seeded inclusion field, synth.c3)",
             "coefficients": ("material ids (uint8 per element, 2-entry table: steel / Fe2O3, P:271)" if use_ids
                              else "per-element fp64 (k, c) pairs"),
-            "config": workload_config(p, world, {"pcg_iters_per_step": iters / args.steps,
-                                                 "us_per_pcg_iter": total_ms / max(iters, 1) * 1e3}),
+            "config": workload_config(p),
+            "parallelism": parallelism(world),
+            "pcg_iters_per_step": iters / args.steps,
+            "us_per_pcg_iter": total_ms / max(iters, 1) * 1e3,
             "e2e": e2e,
             # the whole PCG iteration against the same peak: kernel A (48 B/node + coefficients)
             # + kernel B (64 B/node) algorithmic bytes / the measured time per iteration
@@ -698,7 +702,9 @@ def run_reference(args):
     return {"impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded inclusion field, synth.c3)",
-            "config": workload_config(p, 1, {"pcg_iters_per_step": iters / steps}),
+            "config": workload_config(p),
+            "parallelism": f"CPU oracle, OpenMP on {cores} threads",
+            "pcg_iters_per_step": iters / steps,
             "cpu_baseline": {"value": ms, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
