@@ -167,6 +167,41 @@ def test_face_load_beam_total():
     assert abs(F.sum() - exact) > 0  # quadrature, not the closed form
 
 
+def test_face_load_beam_axes_on_a_rectangular_face():
+    """The beam's in-plane axes (R12): on a rectangular face with the beam off centre and cut by
+    one edge, the total is P times the product of the two truncated-normal masses and the load's
+    centroid is the truncated-normal mean along each axis (closed forms); swapping the face axes
+    changes both."""
+    g = synth.Grid((40, 24, 4), (0.5, 0.5, 0.5), (-10.0, -6.0, 0.0))
+    o = oracle.Oracle(g, np.ones(g.n_elems), np.ones(g.n_elems), assemble=False)
+    P, s, cx, cy = 10.0, 1.5, 4.0, -2.5
+    F = o.face_load(synth.FACE_ZM, 0.0, (P, s, cx, cy))
+    r2 = math.sqrt(2.0)
+
+    def mass(a, b, c0):
+        return 0.5 * (math.erf((b - c0) / (s * r2)) - math.erf((a - c0) / (s * r2)))
+
+    def mean(a, b, c0):
+        phi = lambda t: math.exp(-0.5 * t * t) / math.sqrt(2 * math.pi)
+        al, be = (a - c0) / s, (b - c0) / s
+        return c0 + s * (phi(al) - phi(be)) / mass(a, b, c0)
+
+    exact = P * mass(-10, 10, cx) * mass(-6, 6, cy)
+    swapped = P * mass(-10, 10, cy) * mass(-6, 6, cx)
+    assert abs(F.sum() - exact) <= 2e-4 * exact
+    assert abs(swapped - exact) > 1e-2 * exact
+    x, y, _ = g.node_coords()
+    Fz = F.reshape(g.ne[2] + 1, g.ne[1] + 1, g.ne[0] + 1)[0]
+    X, Y = x[0], y[0]
+    # the nodal load's first moments equal the continuous ones for the bilinear face basis up to
+    # quadrature error (sum_i phi_i(x) x_i = x on a Q1 face)
+    mx = float((Fz * X).sum() / Fz.sum())
+    my = float((Fz * Y).sum() / Fz.sum())
+    assert abs(mx - mean(-10, 10, cx)) < 5e-3, (mx, mean(-10, 10, cx))
+    assert abs(my - mean(-6, 6, cy)) < 5e-3, (my, mean(-6, 6, cy))
+    assert np.count_nonzero(F.reshape(g.ne[2] + 1, -1)[1:]) == 0   # all load on the z = 0 face
+
+
 # ---------------------------------------------------------------------------------------------
 # PCG (Alg. 1, P:93-113)
 
