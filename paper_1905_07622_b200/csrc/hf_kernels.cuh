@@ -476,11 +476,21 @@ __device__ __forceinline__ void reduce_prev(const double *part, int n, double (&
         if (lane == 0) redp[wid][j] = v;
     }
     __syncthreads();
+    if constexpr (NT / 32 * NPART == 32) {
+        // every warp adds the warps' values in one xor butterfly over lanes l = NPART w + j (fp
+        // addition commutes, so every lane, warp and block gets the same bits)
+        double v = redp[lane / NPART][lane % NPART];
 #pragma unroll
-    for (int j = 0; j < NPART; j++) {
-        double v = 0.0;
-        for (int w = 0; w < NT / 32; w++) v += redp[w][j];
-        sums[j] = v;
+        for (int o = NPART; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+#pragma unroll
+        for (int j = 0; j < NPART; j++) sums[j] = __shfl_sync(0xffffffffu, v, j);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NPART; j++) {
+            double v = 0.0;
+            for (int w = 0; w < NT / 32; w++) v += redp[w][j];
+            sums[j] = v;
+        }
     }
 }
 

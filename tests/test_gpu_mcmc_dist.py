@@ -42,28 +42,47 @@ def _free_port():
 def _rank_main(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    import traceback
     import torch.distributed as dist
-    dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
         fwd, cam, data = _setup()
         res = inv.invert_distributed(fwd, cam, data, chains=CHAINS, n_samples=NS, burn_in=BURN, step=STEP, seed=SEED)
         if rank == 0:
-            q.put((res.samples, res.forward_calls))
+            q.put(("ok", res.samples, res.forward_calls))
+    except Exception:                      # report instead of leaving the parent waiting
+        q.put(("error", f"rank {rank}: " + traceback.format_exc(), None))
     finally:
-        dist.destroy_process_group()
+        if dist.is_initialized():
+            dist.destroy_process_group()
 
 
 def test_chains_over_two_processes_equal_single_process_groups():
+    import gc
+    import queue
+    gc.collect()                           # earlier tests' contexts and cached blocks
+    torch.cuda.empty_cache()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    samples, calls = q.get(timeout=600)
+    msg = None
+    for _ in range(600):
+        try:
+            msg = q.get(timeout=1)
+            break
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
     for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+        p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+    assert msg is not None, [p.exitcode for p in procs]
+    assert msg[0] == "ok", msg[1]
+    _, samples, calls = msg
     fwd, cam, data = _setup()
 
     def ll(th):
