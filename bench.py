@@ -325,7 +325,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic("stencil_cg_a_c3_ids" if use_ids else "stencil_cg_a_c3"),
+                         "traffic": ncu_traffic("stencil_cg_a_c3_ids" if use_ids else "r02_stencil_cg_a_c3"),
                          "kernel": "k_stencil<LD_CGD,EP_CGA,%s> (PCG kernel A: d = s + beta d; q = A d; d.q)"
                                    % ("EL_Q1P" if use_ids else "EL_Q1"),
                          "bytes_per_launch": a_bytes, "avg_launch_ms": a_avg_ms,

@@ -559,11 +559,15 @@ __device__ __forceinline__ void peer_sums(const PeerSync *pp, double (&sums)[NPA
 // producer side: after every block stored its partials (and ghost planes), the last block of
 // the kernel publishes the fixed-order sums to every rank
 template <int NT>
-__device__ void peer_publish(const PeerSync *pp, const double *part, int nblk)
+__device__ void peer_publish(const PeerSync *pp, const double *part, int nblk, bool remote)
 {
     __shared__ int last_sh;
     const int tid = threadIdx.x + threadIdx.y * blockDim.x;
-    __threadfence_system();               // this thread's remote ghost stores and partials
+    // order this thread's stores before the block's arrival: remote ghost stores (peer memory)
+    // at system scope, the block's partials (tid < NPART, local memory) at GPU scope; the other
+    // threads stored nothing the consumers read
+    if (remote) __threadfence_system();
+    else if (tid < NPART) __threadfence();
     __syncthreads();
     if (tid == 0) last_sh = atomicAdd(&pp->mine->done, 1u) == (unsigned)nblk - 1u;
     __syncthreads();
@@ -578,17 +582,20 @@ __device__ void peer_publish(const PeerSync *pp, const double *part, int nblk)
         m->done = 0u;
         for (int q = 0; q < pp->nranks; q++)
             for (int j = 0; j < NPART; j++) pp->peer[q]->sums[k & 1][pp->rank][j] = s[j];
-        __threadfence_system();
+        // each release store orders this thread's sum stores (and, cumulatively, the blocks'
+        // ghost stores fenced before their arrival) before the flag
         for (int q = 0; q < pp->nranks; q++) st_release_sys(&pp->peer[q]->flags[pp->rank], k);
     }
 }
 
 // my first / last owned plane of s, stored into the neighbours' ghost buffers (slot index i)
 template <class Real>
-__device__ __forceinline__ void peer_ghost(const PeerSync *pp, long long i, Real v)
+__device__ __forceinline__ bool peer_ghost(const PeerSync *pp, long long i, Real v)
 {
-    if (pp->gdst_lo && i >= pp->lo0 && i < pp->lo0 + pp->plane) reinterpret_cast<Real *>(pp->gdst_lo)[i - pp->lo0] = v;
-    if (pp->gdst_hi && i >= pp->hi0 && i < pp->hi0 + pp->plane) reinterpret_cast<Real *>(pp->gdst_hi)[i - pp->hi0] = v;
+    bool st = false;
+    if (pp->gdst_lo && i >= pp->lo0 && i < pp->lo0 + pp->plane) { reinterpret_cast<Real *>(pp->gdst_lo)[i - pp->lo0] = v; st = true; }
+    if (pp->gdst_hi && i >= pp->hi0 && i < pp->hi0 + pp->plane) { reinterpret_cast<Real *>(pp->gdst_hi)[i - pp->hi0] = v; st = true; }
+    return st;
 }
 
 // one-off exchange of a vector's ghost planes (state vectors at the start of a solve): send my
@@ -765,6 +772,7 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, CgState *sst, bool one
     const Real *dvec = reinterpret_cast<const Real *>(a.dbuf[(it & 1) ^ 1]);
     Real *xvec = reinterpret_cast<Real *>(a.rot[0] ? a.rot[(step + 1) % 3] : a.x);
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
+    bool remote = false;                     // this thread stored into a neighbour's memory
     const long long end = base + a.sysn;
     // BP aligned pairs per thread per sweep (slot counts are even: even row pitch), loads issued
     // up front; a pair never straddles the owned range (planes hold an even number of slots)
@@ -812,15 +820,15 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, CgState *sst, bool one
                 *reinterpret_cast<V2 *>(rv_ + i) = rv[k];
                 *reinterpret_cast<V2 *>(sv_ + i) = sv;
                 if (PEER) {
-                    peer_ghost<Real>(a.sy.peer, i, sv.x);
-                    peer_ghost<Real>(a.sy.peer, i + 1, sv.y);
+                    remote |= peer_ghost<Real>(a.sy.peer, i, sv.x);
+                    remote |= peer_ghost<Real>(a.sy.peer, i + 1, sv.y);
                 }
             }
         }
     }
     pdl_trigger();
     if (!replace) block_reduce_store<NT>(acc, a.sy.pout, pblk);
-    if (PEER && !replace) peer_publish<NT>(a.sy.peer, a.sy.pout, nblk);
+    if (PEER && !replace) peer_publish<NT>(a.sy.peer, a.sy.pout, nblk, remote);
     if (blk == 0 && tid == 0) {
         sst->alpha = alpha;
         sst->dq = dq;
@@ -1161,6 +1169,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     V2 PK0[R + 1], PK1[R + 1];    // EL_TETV: node (k, c) pairs of plane p-1 at x and x+1
     Real cen[R];              // raw centre values of plane p-1 (rows 0..R-1)
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
+    bool remote = false;                     // this thread stored into a neighbour's memory
 #pragma unroll
     for (int r = 0; r < R; r++) {
 #pragma unroll
@@ -1437,7 +1446,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
                     const Real sv = r * __ldg(invdv + idx);
                     out0[idx] = r;
                     out_s[idx] = sv;
-                    if (pp) peer_ghost<Real>(pp, idx, sv);
+                    if (pp) remote |= peer_ghost<Real>(pp, idx, sv);
                     acc[0] = fma((double)r, (double)sv, acc[0]);
                     acc[1] = fma((double)r, (double)r, acc[1]);
                     if (EP == EP_RESID_INIT && !isd) acc[2] = fma((double)b, (double)b, acc[2]);
@@ -1453,7 +1462,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     HF_TR(5);
     // per-block partial sums for the next kernel: A -> (d^T q); init, RESID -> (r^T s, r^T r, b^T b)
     block_reduce_store<NT>(acc, a.sy.pout, blk);
-    if (pp) peer_publish<NT>(pp, a.sy.pout, nblocks);
+    if (pp) peer_publish<NT>(pp, a.sy.pout, nblocks, remote);
     HF_TR(6);
     if (EP == EP_RESID_INIT && sys_lead) {      // a new solve of this system starts: A_0 follows
         CgState *stw = sst;

@@ -1,5 +1,6 @@
 """Corrosion inversion with the Metropolis-Hastings chains spread over processes, each with its
-own GPU forward model (NEXT row f2).  Two ranks share the one B200 of the test box
+own GPU forward model (NEXT row f2).  (File name sorts first: the two spawned ranks
+start while the test process is still small, before the full-size tests grow its host memory.)  Two ranks share the one B200 of the test box
 (gloo for the final gather): the gathered chains must equal single-process runs of the same
 chain groups (per-chain random streams, forward batches of the same size)."""
 import os
