@@ -9,10 +9,15 @@ of the theta-scheme: RHS apply + PCG solve (Alg. 1) + guess update, all on the d
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N = 1: one GPU, the C3 problem.  N > 1 (torchrun, one process per GPU; `--gpus N` launches it):
-the same global C3 problem split into z-slabs over N GPUs (strong scaling).  The slabs talk over
-peer memory (CUDA IPC mailboxes over NVLink: the kernels store ghost planes into the neighbours'
-buffers and publish their reduction sums to every rank; the whole solve stays in the step graph);
-`--transport nccl` selects the NCCL send/recv + allreduce baseline instead.
+the headline is weak scaling over N independent C3 problems, one per GPU (the inverse problem's
+forward solves; no collective on the data path): value = the slowest rank's time / all ranks'
+time steps.  Legs: `c3_slabs_strong` (the same C3 problem split into N z-slabs, strong scaling;
+`--strong` makes it the headline), `apply_512_slabs`, `c4_steps_slabs` (BASELINE configs[3]) and
+`c5_batched_replicas`.  The slabs talk over peer memory (CUDA IPC mailboxes over NVLink: the
+kernels store ghost planes into the neighbours' buffers and publish their reduction sums to every
+rank; the whole solve stays in the step graph); `--transport nccl` selects the NCCL send/recv +
+allreduce baseline instead.  HF_BENCH_SHARE_GPU=1 puts every rank on GPU 0 (code-path validation
+on a one-GPU box; its timings mean nothing).
 --impl reference: the CPU oracle (oracle/, plain C, 1 core) on the same workload, a bounded
 sample of steps.  Prints ONE JSON line on rank 0.
 """
@@ -128,6 +133,15 @@ def ncu_traffic(kernel_key):
         return None
 
 
+def _reduce(dist, dev, values, op="max"):
+    """All-reduce a list of floats across ranks (CUDA tensors over NCCL, CPU tensors over gloo)."""
+    import torch
+    where = "cpu" if dist.get_backend() == "gloo" else dev
+    t = torch.tensor([float(v) for v in values], device=where, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return [float(x) for x in t.tolist()]
+
+
 # ---------------------------------------------------------------------------------------------
 # our arm
 
@@ -138,11 +152,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    slab = world > 1 or args.force_slab          # --force-slab: the N > 1 code path on 1 rank
+    if os.environ.get("HF_BENCH_SHARE_GPU"):           # validation only: every rank on GPU 0
+        local_rank = 0
+    # N > 1: the headline is weak scaling over independent C3 problems, one per GPU (the inverse
+    # problem's forward solves, north_star; no collective on the data path); --strong makes it
+    # the same C3 problem split into N z-slabs; --force-slab: the slab code path on one rank
+    slab = args.force_slab or (world > 1 and args.strong)
+    replicas = world > 1 and not slab
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
-    if slab:
+    if world > 1 or args.force_slab:
         # stdout carries exactly one JSON line: NCCL's log (NCCL_DEBUG as the caller set it,
         # e.g. INFO for the communicator lines) goes to stderr unless a log file is given
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
@@ -152,7 +172,10 @@ def run_ours(args):
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-            dist.init_process_group("nccl", device_id=dev)
+            if os.environ.get("HF_BENCH_SHARE_GPU"):   # NCCL refuses two ranks on one GPU
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=dev)
 
     p = synth.c3(nsteps=args.warmup + args.steps)
     g = p.grid
@@ -219,10 +242,12 @@ def run_ours(args):
     launches = hf.hf_get_launch_count(ctx) - lc0
     total_ms = float(sum(times))
     if dist:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = _reduce(dist, dev, [total_ms])[0]
+        if replicas:                                   # every rank's kernels count
+            launches = int(_reduce(dist, dev, [launches], "sum")[0])
     ms_step = total_ms / args.steps
+    # whole-job value: time steps of 1M-DoF problems processed by all ranks / the slowest rank's time
+    value = total_ms / (args.steps * (world if replicas else 1))
 
     # dominant kernel: PCG kernel A (stencil apply), timed per launch with CUDA events on the
     # context stream over the same steps replayed with the profiling driver
@@ -249,6 +274,8 @@ def run_ours(args):
     # and D2H of the front-face plane every step + the final field, inside the timed region
     e2e = None
     if not slab:
+        # (N > 1 replicas: every rank runs this on its own GPU; wall clock max over ranks and the
+        # whole job's step count, as the headline)
         kh = torch.tensor(p.k).pin_memory()
         ch = torch.tensor(p.c).pin_memory()
         idh = torch.tensor(p.extra["ids"]).pin_memory()
@@ -269,6 +296,8 @@ def run_ours(args):
         se = hf.hf_simulate(ctx2, p.theta, p.dt, args.steps, Fe, uh, 0, snap, rtol=p.rtol)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - t0) * 1e3
+        if replicas:
+            wall = _reduce(dist, dev, [wall])[0] / world
         coef_bytes = idh.numel() + 16 * len(kmat) if use_ids else (kh.numel() + ch.numel()) * 8
         e2e = {"value": wall / args.steps, "unit": UNIT,
                "h2d_bytes_per_step": int((coef_bytes + uh.numel() * 8) / args.steps),
@@ -291,9 +320,8 @@ def run_ours(args):
         hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
         se = hf.hf_simulate(ctx, p.theta, p.dt, args.steps, F, uh, rtol=p.rtol)
         torch.cuda.synchronize()
-        wall = torch.tensor([(time.perf_counter() - t0) * 1e3], device=dev, dtype=torch.float64)
-        dist.all_reduce(wall, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(wall.item()) / args.steps, "unit": UNIT,
+        wall = _reduce(dist, dev, [(time.perf_counter() - t0) * 1e3])[0]
+        e2e = {"value": wall / args.steps, "unit": UNIT,
                "h2d_bytes_per_step": int((kh.numel() + ch.numel() + uh.numel()) * 8 / args.steps),
                "d2h_bytes_per_step": int(uh.numel() * 8 / args.steps),
                "how": "per rank: wall clock around hf_set_coefficients + hf_face_load + hf_simulate(K steps) "
@@ -302,14 +330,16 @@ def run_ours(args):
     line = None
     if rank == 0:
         line = {
-            "metric": METRIC, "value": ms_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if replicas else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded inclusion field, synth.c3)",
             "coefficients": ("material ids (uint8 per element, 2-entry table: steel / Fe2O3, P:271)" if use_ids
                              else "per-element fp64 (k, c) pairs"),
             "config": workload_config(p),
-            "parallelism": parallelism(world),
+            "parallelism": (f"{world} independent C3 problems, one per GPU (inverse-problem forward solves, "
+                            "no collective on the data path); value = slowest rank's time / all ranks' steps"
+                            if replicas else parallelism(world)),
             "pcg_iters_per_step": iters / args.steps,
             "us_per_pcg_iter": total_ms / max(iters, 1) * 1e3,
             "e2e": e2e,
@@ -336,9 +366,14 @@ def run_ours(args):
                          "note": "C3 working set (~104 MB) is L2-resident during a step, so achieved can exceed "
                                  "the HBM copy peak; see apply_512 for the HBM-bound apply"},
         }
-    if slab:
-        # the metric's second half at N GPUs: the 512^3 operator apply on N z-slabs (BASELINE
-        # configs[3]), each rank its slab + ghosts, time = max over ranks
+    if world > 1 or args.force_slab:
+        # strong scaling on N z-slabs: C3 itself (peer memory), and the metric's second half --
+        # the 512^3 operator apply and time step on N slabs (BASELINE configs[3]) -- plus the
+        # corrosion sims as independent replicas; times max over ranks
+        if replicas:
+            c3s = c3_slabs(hf, torch, dev, rank, world, dist)
+            if rank == 0:
+                line["c3_slabs_strong"] = c3s
         a512 = apply_512_slabs(hf, torch, dev, peak, rank, world, dist)
         c4s = c4_steps(hf, torch, dev, peak, rank=rank, world=world, dist=dist)
         c5r = c5_batched(hf, torch, dev, world, rank=rank, dist=dist)
@@ -346,7 +381,7 @@ def run_ours(args):
             line["apply_512_slabs"] = a512
             line["c4_steps_slabs"] = c4s
             line["c5_batched_replicas"] = c5r
-    if not slab:
+    if world == 1 and not slab:
         line["c3_other_coef"] = variant_c3(hf, torch, dev, 64, p.rtol, coef="pairs" if use_ids else "ids")
         # the on-chip PCG (opt-in): one cooperative launch per time step
         line["c3_resident_ids"] = variant_c3(hf, torch, dev, 64, p.rtol, steps=5, coef="ids", resident=True)
@@ -360,6 +395,36 @@ def run_ours(args):
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(args)
     return line
+
+
+def c3_slabs(hf, torch, dev, rank, world, dist, steps=5, warm=3):
+    """C3 on N z-slabs over peer memory (strong scaling of the headline problem): ms per time
+    step, max over ranks, L2 flushed before each timed step."""
+    p = synth.c3(nsteps=steps + warm)
+    ctx = make_slab_ctx(hf, p.grid, rank, world, dist, dev.index, _TRANSPORT[0])
+    hf.hf_set_coefficients(ctx, torch.tensor(p.k, device=dev), torch.tensor(p.c, device=dev))
+    F = torch.empty(ctx.n_nodes, dtype=torch.float64, device=dev)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
+    u = torch.zeros(ctx.n_nodes, dtype=torch.float64, device=dev)
+    up = torch.zeros_like(u)
+    hf.hf_simulate_resume(ctx, p.theta, p.dt, warm, F, u, up, 0, rtol=p.rtol)
+    stream = torch.cuda.current_stream(dev)
+    tot, iters = 0.0, 0
+    for n in range(steps):
+        hf.hf_flush_l2(ctx)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st = hf.hf_simulate_resume(ctx, p.theta, p.dt, 1, F, u, up, warm + n, rtol=p.rtol)
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+        iters += st["total_iters"]
+    tot = _reduce(dist, dev, [tot])[0]
+    return {"ranks": world, "steps": steps, "ms_per_step": tot / steps,
+            "pcg_iters_per_step": iters / steps, "transport": TRANSPORT_NAME,
+            "note": "the same 1M-DoF problem split into z-slabs; per-iteration cross-GPU synchronisation "
+                    "(two reductions) dominates at this size (DESIGN.md section 8)"}
 
 
 def make_slab_ctx(hf, g, rank, world, dist, device, transport):
@@ -430,9 +495,7 @@ def apply_512_slabs(hf, torch, dev, peak, rank, world, dist, _unused=None):
         hf.hf_apply(ctx, 0.005, 1.0, u, y)
     e1.record(s)
     e1.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1) / 10], device=dev, dtype=torch.float64)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    ms = _reduce(dist, dev, [e0.elapsed_time(e1) / 10])[0]
     nodes = (g.ne[0] + 1) * (g.ne[1] + 1) * (hi - lo)          # owned output nodes of this rank
     byts_total = 16.0 * g.n_nodes + 16.0 * g.n_elems              # all ranks together
     del ctx
@@ -583,9 +646,7 @@ def c4_steps(hf, torch, dev, peak, steps=2, rank=0, world=1, dist=None):
     e1.synchronize()
     ms = e0.elapsed_time(e1)
     if dist is not None:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _reduce(dist, dev, [ms])[0]
     it = max(st["total_iters"], 1)
     byts = 112.0 * g.n_nodes + 16.0 * g.n_elems          # kernel A 48 B/node + (k, c); kernel B 64 B/node
     del ctx, F, u, up
@@ -629,9 +690,7 @@ def c5_batched(hf, torch, dev, world, nsims=8, nsteps=300, prec=64, rtol=None, r
     torch.cuda.synchronize()
     sec = time.perf_counter() - t0
     if dist is not None:
-        t = torch.tensor([sec], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sec = float(t.item())
+        sec = _reduce(dist, dev, [sec])[0]
     its = sum(st["total_iters"] for st in stats)
     del ctx
     return {"sims": nsims * world, "ranks": world, "sims_per_rank": nsims, "steps_per_sim": nsteps, "seconds": sec,
@@ -723,6 +782,9 @@ def main():
                     help="element coefficients as per-element fp64 (k, c) pairs (default) or material ids "
                          "(the paper's two-material field, 1 B per element; no faster at C3, whose kernel A "
                          "is latency-bound, but 16 %% faster for the HBM-bound 512^3 apply)")
+    ap.add_argument("--strong", action="store_true",
+                    help="N > 1: the headline is the one C3 problem split into N z-slabs (default: one "
+                         "independent C3 problem per GPU, weak scaling)")
     ap.add_argument("--force-slab", action="store_true",
                     help="run the multi-GPU (z-slab) code path even on one rank (validation)")
     ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
@@ -750,7 +812,8 @@ def main():
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "ours":
         import torch
-        if torch.cuda.device_count() < int(os.environ.get("LOCAL_WORLD_SIZE", world)):
+        if torch.cuda.device_count() < int(os.environ.get("LOCAL_WORLD_SIZE", world)) and \
+                not os.environ.get("HF_BENCH_SHARE_GPU"):
             sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {torch.cuda.device_count()}")
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None:
