@@ -79,3 +79,29 @@ def test_c3_300_steps_full_trajectory(c3_oracle_run):
     assert abs(st["total_iters"] - int(ito.sum())) <= 0.02 * ito.sum()
     print(f"[c3 300 steps] worst front-face rel-L2 {worst:.2e}, u150 {r150:.2e}, u300 {r300:.2e} / {r300b:.2e}, "
           f"iterations {st['total_iters']} (oracle {int(ito.sum())})")
+
+
+@pytest.mark.parametrize("variant", ["ids", "mixed"])
+def test_c3_300_steps_variants(c3_oracle_run, variant):
+    """The same 300-step trajectory through material ids (1 B per element, EL_Q1P stencil) and
+    through mixed precision (fp32 correction + fp64 finish, hf_set_mixed): u^300 and the front
+    face after every step within 1e-10 of the fp64 oracle."""
+    p, F, u150o, u300o, snapo, ito = c3_oracle_run
+    ctx = hf.hf_create(p.grid, 0)
+    if variant == "mixed":
+        hf.hf_set_mixed(ctx, 1, 1e-5)
+        hf.hf_set_coefficients(ctx, T(p.k), T(p.c))
+    else:
+        hf.hf_set_material_ids(ctx, torch.tensor(p.extra["ids"], device=DEV),
+                               [m[1] for m in p.extra["materials"]], [m[0] for m in p.extra["materials"]])
+    Fd = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, Fd)
+    u = T(p.u0)
+    snap = torch.empty(p.nsteps * ctx.n_plane, dtype=torch.float64, device=DEV)
+    st = hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, Fd, u, 0, snap, rtol=p.rtol)
+    assert st["steps_done"] == p.nsteps and st["first_failed_step"] == -1
+    sn = snap.cpu().numpy().reshape(p.nsteps, -1)
+    worst = max(rel(sn[n], snapo[n]) for n in range(p.nsteps))
+    r300 = rel(u.cpu().numpy(), u300o)
+    assert worst <= BAR and r300 <= BAR, (worst, r300)
+    print(f"\n[c3 300 steps, {variant}] worst front-face rel-L2 {worst:.2e}, u300 {r300:.2e}")
