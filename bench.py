@@ -658,7 +658,7 @@ def c4_steps(hf, torch, dev, peak, steps=2, rank=0, world=1, dist=None):
             "fields": "two materials, 20 % oxide i.i.d. per element (device RNG, seed 3)"}
 
 
-def c5_batched(hf, torch, dev, world, nsims=8, nsteps=300, prec=64, rtol=None, rank=0, dist=None):
+def c5_batched(hf, torch, dev, world, nsims=10, nsteps=300, prec=64, rtol=None, rank=0, dist=None):
     """C5 (BASELINE configs[4]): corrosion-inverse forward simulations, 99^3 voxels each
     (1M DoF), T_F = 10 s in 300 CN steps, Gaussian beam 10 W sigma 2 mm, per-sim depth and
     log-normal k perturbation; nsims of them through hf_simulate_batched on this GPU.  With dist

@@ -2485,12 +2485,41 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
 // systems per stack: about 8M stacked nodes (a 1M-DoF system alone is latency-bound, a stack of
 // 8 streams at the HBM roofline), at most 256 (kernel B's loop duties scan the systems with one
 // block) and at most B
+// Systems per stack (batched sims, a13).  A stack of G systems runs its stencil kernels on
+// tx * ty * G * nch CTAs, each system's z-range cut into nch chunks (stencil_grid); CTAs are
+// dispatched in waves of (SMs x resident CTAs per SM) slots, and every chunk carries ~4 planes of
+// warm-up / prologue.  The group size is the one that minimises the modelled time of the whole
+// batch: sum over groups of (systems / slot efficiency).  E.g. C5 (100^3 nodes, 28 tile
+// columns, 296 slots): a stack of 8 fills 224 of 296 slots (efficiency 0.72), a stack of 5 with
+// two chunks per system 280 (0.86), a stack of 10 280 (0.91).  Measured C5 sim-steps/s, B = 20:
+// groups of 10: 193, 5: 189, 4: 176, 7: 161, 20: 152; B = 8: 5 + 3: 196, one stack of 8: 185.
 static int stack_group(const hf_ctx *c, int B)
 {
-    const long long nn = (long long)c->nx1 * c->ny1 * c->nz1g;
-    long long G = std::max(1LL, (8LL << 20) / nn);
-    if (const char *e = getenv("HF_BATCH_GROUP")) G = std::max(1, atoi(e));
-    return (int)std::min<long long>(std::min<long long>(G, 256), B);
+    if (const char *e = getenv("HF_BATCH_GROUP")) return std::max(1, std::min(atoi(e), B));
+    const long long nn = (long long)c->pitch * c->ny1 * c->nz1g;     // nodes per system (padded)
+    const int planes = c->nz1g;
+    // stacks stay below the R = 4 tile threshold (default_tile_r): measured at C5, stacks of 16-20
+    // systems on R = 4 tiles ran 20 % slower than stacks of 10 on R = 2 tiles
+    const int gmax = (int)std::min<long long>(std::min<long long>(B, 64), std::max(1LL, ((16LL << 20) - 1) / nn));
+    auto eff = [&](int G) -> double {
+        const int R = 2;
+        const int occ = std::max(1, c->tileR == 2 ? c->occ : 2);
+        const long long tx = (c->nx1 + TILE_X - 1) / TILE_X, ty = (c->ny1 + NW * R - 2) / (NW * R - 1);
+        const long long cols = tx * ty, slots = (long long)c->nsm * occ;
+        long long nch = std::max(1LL, slots / (cols * G));
+        const long long chunk = (planes + nch - 1) / nch;
+        nch = (planes + chunk - 1) / chunk;
+        const long long ctas = cols * G * nch, waves = (ctas + slots - 1) / slots;
+        return (double)(G * (long long)planes * cols) / ((double)waves * slots * (chunk + 4));
+    };
+    int best = 1;
+    double tbest = 1e300;
+    for (int G = 1; G <= gmax; G++) {
+        const int full = B / G, rem = B % G;
+        const double t = full * (G / eff(G)) + (rem ? rem / eff(rem) : 0.0);
+        if (t < tbest * (1.0 - 1e-9)) { tbest = t; best = G; }
+    }
+    return best;
 }
 
 static hf_status batched_stacked(hf_ctx *c, int32_t B, const double *k_batch, const double *c_batch, double theta,
