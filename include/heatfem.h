@@ -232,10 +232,12 @@ hf_status hf_simulate_resume(hf_ctx *ctx, double theta, double dt, int32_t nstep
  * (in u^0, out u^nsteps); front_out: NULL or B x n_plane receiving plane snap_plane of
  * u^nsteps per system (a failed system: its last iterate); stats: B entries (may be NULL).
  * Systems are independent: each has its own PCG (Alg. 1) scalars, its own stop test
- * ||r_j|| <= rtol ||b_j||, iteration counts and failure status.  Groups of up to ~8M stacked
- * nodes (at most 256 systems) run as one grid: the systems are stacked along z with a
+ * ||r_j|| <= rtol ||b_j||, iteration counts and failure status.  Groups of systems (below 16M
+ * stacked nodes, at most 64 systems) run as one grid: the systems are stacked along z with a
  * coefficient-free element layer between them, each kernel block works inside one system and
  * a converged system stops while the others iterate on.  Dirichlet faces apply per system.
+ * Systems are grouped into stacks by a model of the GPU's CTA slots.
+ * B = 0 is a no-op (the arrays may then be NULL).
  * Returns the first failing status (the other systems run on and are returned). */
 hf_status hf_simulate_batched(hf_ctx *ctx, int32_t B, const double *k_batch,
                               const double *c_batch, double theta, double dt, int32_t nsteps,

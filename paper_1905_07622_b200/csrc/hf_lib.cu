@@ -2611,15 +2611,15 @@ hf_status hf_simulate_batched(hf_ctx *c, int32_t B, const double *k_batch, const
                               double dt, int32_t nsteps, const double *F, double *u_batch, int64_t snap_plane,
                               double *front_out, const hf_cg_opts *opts, hf_sim_stats *stats)
 {
-    if (!c || B < 0 || !k_batch || !u_batch || nsteps < 0 || !(dt > 0.0))
-        return fail(HF_E_ARG, "hf_simulate_batched: bad argument");
+    if (!c || B < 0 || nsteps < 0 || !(dt > 0.0)) return fail(HF_E_ARG, "hf_simulate_batched: bad argument");
+    if (B == 0) return HF_OK;                    // an empty batch (its arrays may be NULL)
+    if (!k_batch || !u_batch) return fail(HF_E_ARG, "hf_simulate_batched: NULL k_batch / u_batch");
     if (!c_batch && !c->coef_set) return fail(HF_E_STATE, "hf_simulate_batched: no capacity field");
     if (c->comm) return fail(HF_E_ARG, "hf_simulate_batched: not available on slab contexts");
     if (c->tetv) return fail(HF_E_STATE, "hf_simulate_batched: per-element coefficients only (not vertex materials)");
     if (front_out && (snap_plane < 0 || snap_plane >= c->nz1g)) return fail(HF_E_INDEX, "snap_plane");
     HFCK(check_ptrs(c, "hf_simulate_batched", {k_batch, c_batch, F, u_batch, front_out}));
     CUCK(cudaSetDevice(c->device));
-    if (B == 0) return HF_OK;
     hf_cg_opts o = {1e-12, 10000, -1};
     if (opts) o = *opts;
     o = resolved(c, o);

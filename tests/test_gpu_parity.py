@@ -738,3 +738,23 @@ def test_c4_time_step_properties():
     sm = float(y.sum())
     assert abs(sa - sm) <= 1e-9 * abs(sm), (sa, sm)
     assert abs(sm - dt * float(F.sum())) <= 1e-9 * abs(sm)
+
+
+def test_empty_inputs():
+    """Degenerate calls: 0 time steps leave u unchanged and report 0 steps; a batch of 0 systems
+    is a no-op; a 0-iteration cap on a non-trivial step reports NOCONV at step 0."""
+    p = synth.c1()
+    ctx = make_ctx(p.grid, p.k, p.c)
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
+    u0 = synth.random_vector(p.grid.n_nodes, 5)
+    u = T(u0)
+    st = hf.hf_simulate(ctx, p.theta, p.dt, 0, F, u, rtol=p.rtol)
+    assert st["steps_done"] == 0 and st["total_iters"] == 0
+    assert np.array_equal(N(u), u0)
+    ub = torch.zeros(0, dtype=torch.float64, device=DEV)
+    kb = torch.zeros(0, dtype=torch.float64, device=DEV)
+    hf.hf_simulate_batched(ctx, 0, kb, None, p.theta, p.dt, 3, F, ub)
+    u = T(u0)
+    st = hf.hf_simulate(ctx, p.theta, p.dt, 2, F, u, rtol=p.rtol, max_iter=0, raise_on_noconv=False)
+    assert st["rc"] == hf.HF_E_NOCONV and st["first_failed_step"] == 0
