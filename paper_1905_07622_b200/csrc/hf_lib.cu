@@ -3095,6 +3095,7 @@ hf_status hf_set_precision(hf_ctx *c, int32_t bits)
 {
     if (!c || (bits != 32 && bits != 64)) return fail(HF_E_ARG, "hf_set_precision: bits must be 32 or 64");
     if (c->coef_set) return fail(HF_E_STATE, "hf_set_precision: call before hf_set_coefficients");
+    if (c->lo && bits != 64) return fail(HF_E_STATE, "hf_set_precision: mixed precision is on (hf_set_mixed(ctx, 0) first)");
     if (bits == c->prec) return HF_OK;
     CUCK(cudaSetDevice(c->device));
     CUCK(cudaStreamSynchronize(c->stream));

@@ -265,6 +265,12 @@ def test_mixed_setter_order_and_forwarding():
     hf.hf_set_precision(ctx32, 32)
     with pytest.raises(hf.HfError):
         hf.hf_set_mixed(ctx32, 1, 1e-6)                  # fp32 context: HF_E_STATE
+    ctxm = hf.hf_create(g, 0)
+    hf.hf_set_mixed(ctxm, 1, 1e-6)
+    with pytest.raises(hf.HfError):
+        hf.hf_set_precision(ctxm, 32)                    # mixed on: the context stays fp64
+    hf.hf_set_mixed(ctxm, 0, 1e-6)
+    hf.hf_set_precision(ctxm, 32)
     # materials by id are forwarded to the shadow as (k, c) pairs
     p = synth.c1()
     kc, inv = np.unique(np.stack([p.k, p.c], 1), axis=0, return_inverse=True)
