@@ -392,7 +392,7 @@ def run_ours(args):
         # the paper's settings for the inverse problem: rtol 1e-6, single precision
         line["c5_batched_fp32_rtol1e-6"] = c5_batched(hf, torch, dev, world, prec=32, rtol=1e-6)
         line["fp32_variant"] = fp32_variant(hf, torch, dev, peak)
-    if rank == 0:
+    if rank == 0 and world == 1:                   # the oracle on the host cores: N = 1 only
         line["cpu_baseline"] = cpu_baseline(args)
     return line
 
