@@ -370,7 +370,8 @@ hf_status hf_flush_l2(hf_ctx *ctx);
 
 /* Benchmark mode of hf_simulate*: enable = 1 flushes L2 (as hf_flush_l2) before every time
  * step and times every step alone with CUDA events (hf_sim_stats.ms_steps), all enqueued
- * asynchronously; enable = 0 restores normal operation. */
+ * asynchronously; enable = 2 times every step without the flush; enable = 0 restores normal
+ * operation.  Errors: HF_E_ARG. */
 hf_status hf_set_step_flush(hf_ctx *ctx, int32_t enable);
 
 #ifdef __cplusplus

@@ -268,7 +268,7 @@ struct hf_ctx {
     int nsm_share = 0;               // SMs a stencil grid is sized for (< nsm when ranks share a GPU)
     void *ghost_buf = nullptr;       // peer transport: the two s ghost planes the neighbours write
     size_t ghost_pb = 0;             // bytes per plane slot of the mailbox buffers
-    bool step_flush = false;
+    int step_flush = 0;              // 1: flush L2 + time every step; 2: time every step, no flush
     double last_ms_steps = 0.0;      // per-step event total of the last run (step_flush)
     double last_aK = 0.0;            // operator (aK, 1) of the last time loop (hf_time_kernel_a)
     bool prof = false;
@@ -2315,7 +2315,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             std::vector<cudaEvent_t> ev(2 * (size_t)nsteps);
             for (auto &e : ev) CUCK(cudaEventCreate(&e));
             for (int n = 0; n < nsteps; n++) {
-                CUCK(cudaMemsetAsync(c->flush, n & 1, fb, s.stream));
+                if (c->step_flush == 1) CUCK(cudaMemsetAsync(c->flush, n & 1, fb, s.stream));
                 CUCK(cudaEventRecord(ev[2 * n], s.stream));
                 if (mixed) CUCK(cudaGraphLaunch(c->mix_exec, s.stream));
                 CUCK(cudaGraphLaunch(s.gexec, s.stream));
@@ -3211,7 +3211,8 @@ hf_status hf_mixed_iters(hf_ctx *c, int64_t *lo_iters)
 hf_status hf_set_step_flush(hf_ctx *c, int32_t enable)
 {
     if (!c) return fail(HF_E_ARG, "hf_set_step_flush: NULL");
-    c->step_flush = enable != 0;
+    if (enable < 0 || enable > 2) return fail(HF_E_ARG, "hf_set_step_flush: enable must be 0, 1 or 2");
+    c->step_flush = enable;
     return HF_OK;
 }
 
