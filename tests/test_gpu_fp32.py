@@ -284,3 +284,31 @@ def test_mixed_setter_order_and_forwarding():
     o, Fo = oracle.problem_oracle(p)
     uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
     assert rel(u.cpu().numpy(), uo) <= 1e-10
+
+
+def test_mixed_nonzero_dirichlet_beam_and_resume():
+    """Mixed precision with non-zero Dirichlet faces and a Gaussian beam, run as 3 + 4 steps
+    through hf_simulate_resume (the guess extrapolates across the call boundary): within 1e-10
+    of the oracle's 7-step run."""
+    g = synth.Grid((20, 18, 16), (0.5, 0.5, 0.4), (-5.0, -4.5, 0.0))
+    rng = np.random.default_rng(5)
+    ids = (rng.random(g.n_elems) < 0.25).astype(np.int64)
+    kmat, cmat = np.array([4.9, 0.04]), np.array([3.7, 1.65])
+    p = synth.Problem("dirbeam", g, kmat[ids], cmat[ids], np.zeros(g.n_nodes), theta=0.5, dt=0.05, nsteps=7,
+                      rtol=1e-12, flux_face=synth.FACE_ZM, flux_const=0.0,
+                      beam=(10.0, 2.0, 0.0, 0.0), dirichlet_bits=(1 << synth.FACE_XP) | (1 << synth.FACE_YM),
+                      dirichlet_values=(0.0, 3.0, -1.5, 0.0, 0.0, 0.0))
+    ctx = hf.hf_create(p.grid, 0)
+    hf.hf_set_mixed(ctx, 1, 1e-5)
+    hf.hf_set_dirichlet_faces(ctx, p.dirichlet_bits, p.dirichlet_values)
+    hf.hf_set_coefficients(ctx, T(p.k), T(p.c))
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
+    u = T(p.u0)
+    up = torch.empty_like(u)
+    hf.hf_simulate_resume(ctx, p.theta, p.dt, 3, F, u, up, 0, rtol=p.rtol)
+    hf.hf_simulate_resume(ctx, p.theta, p.dt, 4, F, u, up, 3, rtol=p.rtol)
+    o, Fo = oracle.problem_oracle(p)
+    uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
+    assert rel(N(u), uo) <= 1e-10, rel(N(u), uo)
+    assert hf.hf_mixed_iters(ctx) > 0
