@@ -758,3 +758,59 @@ def test_empty_inputs():
     u = T(u0)
     st = hf.hf_simulate(ctx, p.theta, p.dt, 2, F, u, rtol=p.rtol, max_iter=0, raise_on_noconv=False)
     assert st["rc"] == hf.HF_E_NOCONV and st["first_failed_step"] == 0
+
+
+def test_slab_local_transport_tets_and_mixed_tets():
+    """The paper's 6-tet element (row f1) on 2 in-process z-slabs against one context and the
+    oracle's tet assembly; and the tet element through mixed precision (fp32 correction, fp64
+    finish) against the oracle."""
+    g = synth.Grid((10, 9, 12), (0.3, 0.3, 0.2))
+    k, c = synth.random_fields(g, seed=25)
+    theta, dt, nsteps, nranks = 0.5, 0.05, 4, 2
+    o = oracle.Oracle(g, k, c, elem=1)
+    Fo = o.face_load(synth.FACE_ZM, 1.0)
+    u0 = synth.random_vector(g.n_nodes, 26) * 0.01
+    uo, _, _, _ = o.simulate(theta, dt, nsteps, Fo, u0)
+    # mixed precision, one context
+    ctxm = hf.hf_create(g, 0)
+    hf.hf_set_mixed(ctxm, 1, 1e-5)
+    hf.hf_set_element(ctxm, 1)
+    hf.hf_set_coefficients(ctxm, T(k), T(c))
+    Fm = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctxm, synth.FACE_ZM, 1.0, None, Fm)
+    um = T(u0)
+    hf.hf_simulate(ctxm, theta, dt, nsteps, Fm, um)
+    assert rel(N(um), uo) <= 1e-10
+    # two slabs
+    grp = hf.hf_local_group_create(nranks)
+    plane = (g.ne[0] + 1) * (g.ne[1] + 1)
+    out = [None] * nranks
+    errs = []
+    ctxs = [None] * nranks
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            ctx = hf.hf_create_slab(g, r, nranks, grp, transport=1, device=0)
+            ctxs[r] = ctx
+            lo, hi, lp, z0 = ctx.slab
+            hf.hf_set_element(ctx, 1)
+            hf.hf_set_coefficients(ctx, T(k), T(c))
+            F = torch.empty(ctx.n_nodes, dtype=torch.float64, device=DEV)
+            hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+            u = T(u0[z0 * plane:(z0 + lp) * plane])
+            hf.hf_simulate(ctx, theta, dt, nsteps, F, u)
+            out[r] = (lo, hi, z0, N(u))
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=on_own_stream, args=(rank_main, r)) for r in range(nranks)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not errs, errs
+    full = np.empty(g.n_nodes)
+    for lo, hi, z0, u in out:
+        full[lo * plane:hi * plane] = u[(lo - z0) * plane:(hi - z0) * plane]
+    assert rel(full, uo) <= 1e-10
+    del ctxs
+    hf.hf_local_group_destroy(grp)
