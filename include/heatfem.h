@@ -338,6 +338,22 @@ hf_status hf_set_mixed(hf_ctx *ctx, int32_t enable, double rtol_lo);
 /* PCG iterations of the fp32 stage since hf_set_mixed (device counter; synchronises). */
 hf_status hf_mixed_iters(hf_ctx *ctx, int64_t *lo_iters);
 
+/* PCG arrangement of hf_simulate* (hf_set_cg_variant).  variant 0 (default): Alg. 1 as printed
+ * (P:93-113), two streaming kernels per iteration (A: d = s + beta d, q = A d, d^T q; B: x, r, s
+ * updates, r^T s, r^T r).  variant 1: the single-reduction (Chronopoulos-Gear) arrangement of the
+ * same Jacobi PCG -- w = A u and s = A p are carried by recurrence, so alpha_i and beta_i follow
+ * from one set of sums (r^T u, w^T u) and each iteration is ONE stencil kernel that also performs
+ * the vector updates; identical iterates in exact arithmetic, the same residual replacement every
+ * 50 iterations (Alg. 1 line 10: r = b - A x, then w = A P^-1 r) and the same stop test (R4).
+ * Used when eligible: fp64 Q1 elements ((k, c) pairs or material ids), one system, no slab
+ * transport, not mixed / on-chip; otherwise variant 0 runs.  DESIGN.md section 7b.
+ * Errors: HF_E_ARG. */
+hf_status hf_set_cg_variant(hf_ctx *ctx, int32_t variant);
+
+/* out[0] = the variant set by hf_set_cg_variant, out[1] = 1 if the last hf_simulate* ran the
+ * single-reduction PCG.  Errors: HF_E_ARG. */
+hf_status hf_cg_variant(hf_ctx *ctx, int32_t out[2]);
+
 /* On-chip PCG (opt-in, hf_set_resident): hf_simulate* runs each time step's whole PCG solve
  * (Alg. 1) in ONE cooperative launch whose CTAs (one per SM) keep d (+ a one-node
  * halo), r, q/s and the material ids of their brick of the grid in shared memory (x in the

@@ -82,6 +82,8 @@ _SIGS = {
     "hf_profile_read": (_i32, [_vp, _P(C.c_double * 5), _P(C.c_int64 * 5)]),
     "hf_set_driver": (_i32, [_vp, _i32]),
     "hf_set_resident": (_i32, [_vp, _i32]),
+    "hf_set_cg_variant": (_i32, [_vp, _i32]),
+    "hf_cg_variant": (_i32, [_vp, _P(C.c_int32)]),
     "hf_set_mixed": (_i32, [_vp, _i32, _d]),
     "hf_mixed_iters": (_i32, [_vp, _P(C.c_int64)]),
     "hf_resident_plan": (_i32, [_vp, _P(C.c_int32)]),
@@ -448,6 +450,16 @@ def hf_mixed_iters(ctx: Context) -> int:
     v = C.c_int64()
     _check(_lib.hf_mixed_iters(ctx.ptr, C.byref(v)))
     return int(v.value)
+
+
+def hf_set_cg_variant(ctx: Context, variant: int):
+    _check(_lib.hf_set_cg_variant(ctx.ptr, variant))
+
+
+def hf_cg_variant(ctx: Context) -> dict:
+    out = (C.c_int32 * 2)()
+    _check(_lib.hf_cg_variant(ctx.ptr, out))
+    return {"variant": int(out[0]), "last_used": int(out[1])}
 
 
 def hf_set_resident(ctx: Context, mode: int):

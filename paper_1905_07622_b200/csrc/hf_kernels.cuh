@@ -38,8 +38,8 @@ constexpr int TILE_X = 31;    // owned node columns per CTA
 constexpr int BOXW = 34;      // fp64 node columns in a TMA box (even start <= X0-1, covers X0+31)
 constexpr int NMAPS = 6;      // node tensor maps: ring U[0..2], d[0..1], s
 
-enum { LD_RAW = 0, LD_GT = 1, LD_CGD = 2, LD_X0 = 3 };
-enum { EP_APPLY = 0, EP_CGA = 1, EP_RESID = 2, EP_RESID_INIT = 3 };
+enum { LD_RAW = 0, LD_GT = 1, LD_CGD = 2, LD_X0 = 3, LD_CG1 = 4, LD_CG1W = 5 };
+enum { EP_APPLY = 0, EP_CGA = 1, EP_RESID = 2, EP_RESID_INIT = 3, EP_CG1 = 4, EP_CG1W = 5 };
 enum { ST_OK = 0, ST_NOCONV = -3, ST_BREAKDOWN = -4 };
 enum { ROT_NONE = 0, ROT_RHS = 1, ROT_INIT = 2, ROT_X = 3 };
 enum { MAP_U0 = 0, MAP_D0 = 3, MAP_S = 5 };
@@ -75,6 +75,7 @@ struct CgState {
     double delta[2];        // delta_i = r_i^T s_i in slot i & 1          (written by A_i)
     double thresh, bb, rr;  // rtol^2 ||b_F||^2, ||b_F||^2, last r^T r      (A)
     double alpha, dq;       // last alpha, d^T q                          (B)
+    double alf[2];          // single-reduction PCG: alpha_i in slot i & 1 (CG1 kernel i)
 };
 static_assert(offsetof(CgState, a_iter) == 16 && offsetof(CgState, npart_a) == 32, "CgState header layout");
 
@@ -230,6 +231,20 @@ struct BArgs {
     Sync sy;
 };
 
+// Single-reduction PCG (Chronopoulos-Gear form of Alg. 1): one
+// stencil kernel per iteration.  Kernel i (iteration parity par = i & 1, fixed per graph node)
+// streams r_i, w_i = A u_i, s_{i-1} = A p_{i-1} and P^{-1} (TMA maps 0..3) and forms, on every
+// node of its box, s_i = w_i + beta_i s_{i-1}, r_{i+1} = r_i - alpha_i s_i, u_{i+1} = P^{-1} r_{i+1};
+// on its owned nodes it also writes s_i, r_{i+1}, p_i = u_i + beta_i p_{i-1}, x_{i+1} = x_i +
+// alpha_i p_i; the stencil gives w_{i+1} = A u_{i+1}.  Partials: (r u, r r, b b (forwarded), w u).
+// r, w, s are ping-pong buffers (read at halo nodes by other CTAs); p, x are pointwise.
+struct CgOne {
+    double *rout, *sout, *wout;   // r_{i+1}, s_i, w_{i+1} (slot par ^ 1; EP_CG1W: wout = w slot of its r)
+    double *p;                    // p (in place)
+    double *x;                    // the iterate; NULL: the time-step ring slot U[(step + 1) % 3]
+    int par;                      // parity of the iteration (kernel i reads counter slot par)
+};
+
 struct StencilArgs {
     Geom g;
     Lam lam;
@@ -259,6 +274,7 @@ struct StencilArgs {
     int npal;                     // EL_Q1P: table entries in use (materials + 1)
     BArgs fb;                     // FL_FUSEB: kernel B's arguments
     unsigned long long *gbar;     // FL_FUSEB: grid-barrier counter (monotonic)
+    CgOne c1;                     // EP_CG1 / EP_CG1W: the single-reduction PCG's vectors
 };
 // Node-vector pointers of StencilArgs / BArgs / StepArgs are declared double* but address
 // vectors of the context's storage type; kernels instantiated for Real = float reinterpret them.
@@ -693,13 +709,60 @@ __device__ __forceinline__ IterStart iter_start(const CgState *st, int i, const 
     return r;
 }
 
+// Start of iteration i of the single-reduction PCG (EP_CG1) from the previous kernel's sums
+// s = (gamma_i = r_i^T u_i, r_i^T r_i, ||b_F||^2 (i = 0 only), delta_i = w_i^T u_i):
+//   beta_0 = 0, alpha_0 = gamma_0 / delta_0;
+//   beta_i = gamma_i / gamma_{i-1},  alpha_i = gamma_i / (delta_i - beta_i gamma_i / alpha_{i-1})
+// (Chronopoulos & Gear; in exact arithmetic the alpha_i, beta_i of Alg. 1 lines 8 and 17, since
+// delta_i - beta_i gamma_i / alpha_{i-1} = d_i^T A d_i).  The stop test is Alg. 1's (R4).
+struct IterStart1 {
+    bool go;
+    double alpha, beta, gamma, rr, thresh, bb;
+    int status, zero_x;
+};
+
+__device__ __forceinline__ IterStart1 iter_start_cg1(const CgState *st, int i, const double *s, int max_iter)
+{
+    IterStart1 r;
+    r.gamma = s[0];
+    r.rr = s[1];
+    r.status = ST_OK;
+    r.zero_x = 0;
+    r.beta = 0.0;
+    r.alpha = 0.0;
+    double den = s[3];
+    if (i == 0) {
+        r.bb = s[2];
+        r.thresh = st->rtol2 * s[2];
+    } else {
+        r.bb = st->bb;
+        r.thresh = st->thresh;
+        r.beta = s[0] / st->delta[(i - 1) & 1];
+        den = s[3] - r.beta * s[0] / st->alf[(i - 1) & 1];
+    }
+    if (!isfinite(s[0]) || !isfinite(s[1]) || !isfinite(s[3]) || !isfinite(r.bb)) {
+        r.status = ST_BREAKDOWN;
+        r.go = false;
+        return r;
+    }
+    if (i == 0 && r.bb == 0.0) { r.zero_x = 1; r.go = false; return r; }   // b_F = 0 -> x_F = 0
+    const bool need = r.rr > r.thresh;                                      // R4: ||r|| > tol ||b||
+    r.go = need && i < max_iter;
+    if (need && i >= max_iter) r.status = ST_NOCONV;
+    if (r.go) {
+        r.alpha = r.gamma / den;
+        if (!(den > 0.0) || !isfinite(r.alpha)) { r.status = ST_BREAKDOWN; r.go = false; }   // d^T A d <= 0
+    }
+    return r;
+}
+
 // ---- the stencil kernel (operator apply with fused prologue/epilogue) ---------------------
 
 template <int R, int NW, int LD, class Real = double, int EL = EL_Q1>
 struct StencilShape {
     static constexpr int ES = (int)sizeof(Real);
     static constexpr int H = NW * R + 1;                                     // node rows per box
-    static constexpr int NA = LD == LD_RAW ? 1 : (LD == LD_GT ? 0 : 2);      // node arrays per plane
+    static constexpr int NA = LD == LD_RAW ? 1 : (LD == LD_GT ? 0 : (LD == LD_CG1 ? 4 : 2));   // node arrays per plane
     // box widths: the x origin must be 16-B aligned, so it starts up to 16/ES - 1 columns early
     static constexpr int BW = ES == 8 ? BOXW : 36;                           // node columns per box
     static constexpr int KW = ES == 8 ? 64 : 68;                             // kc values per box row
@@ -713,10 +776,11 @@ struct StencilShape {
     static constexpr int STAGE_DBL = (NA * NODE_DBL + KC_DBL + AL - 1) / AL * AL;
     static constexpr unsigned STAGE_BYTES = NA * NODE_BOX * (unsigned)ES + KC_BYTES;   // TMA bytes
     static constexpr int PAL_BYTES = EL == EL_Q1P ? PAL_MAX * 8 * 8 : 0;    // (a, b) x 4 channels per material
+    static constexpr int UB_BYTES = LD == LD_CG1 ? NODE_DBL * ES : 0;       // LD_CG1: the u plane (one node box)
     // rounded to 1 KB so that CTAs of different variants sharing an SM get aligned windows
     static size_t smem_bytes(int ns)
     {
-        return HF_SMEM_ROUND((size_t)ns * STAGE_DBL * ES + 16 * ns + 2 * NW * 32 * ES + PAL_BYTES);
+        return HF_SMEM_ROUND((size_t)ns * STAGE_DBL * ES + 16 * ns + 2 * NW * 32 * ES + PAL_BYTES + UB_BYTES);
     }
 };
 
@@ -915,8 +979,11 @@ __device__ __forceinline__ unsigned long long gtime()
 #define HF_TR(k) do { } while (0)
 #endif
 
+// (the single-reduction PCG kernel at R = 2 is held to 128 registers: two CTAs per SM; a
+// minimum of 0 leaves the other kernels to the same register heuristic as no minimum, which an
+// explicit 1 does not: it raised the apply from 72 to 104 registers)
 template <int R, int NW, int NS, int LD, int EP, int FL, int EL, class Real>
-__global__ void __launch_bounds__(32 * NW)
+__global__ void __launch_bounds__(32 * NW, (EP == EP_CG1 && R == 2) ? 2 : 0)
 k_stencil(const __grid_constant__ StencilArgs a)
 {
     using SH = StencilShape<R, NW, LD, Real, EL>;
@@ -972,7 +1039,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     extern __shared__ __align__(128) double smem_d[];
     Real *stage = reinterpret_cast<Real *>(smem_d);
     uint64_t *bars = reinterpret_cast<uint64_t *>(stage + NS * SH::STAGE_DBL);
-    if constexpr (EP == EP_CGA) {
+    if constexpr (EP == EP_CGA || EP == EP_CG1) {
         // independent of the previous kernel: may overlap its tail under a programmatic edge
         if (tid == 0) {
             for (int i = 0; i < NS; i++) mbar_init(&bars[i], 1);
@@ -997,6 +1064,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
         max_iter = hd.h2.y;
         re_ = hd.h1.y;
         step_ = hd.h0.w;
+        if (EP == EP_CG1) it_i = a.c1.par ? hd.h1.x : b_iter;   // iteration counter slot of this parity
         if (glob_lead) {
             // shared loop fields, written before any early exit (no block of this kernel reads them)
             CgState *st0 = a.sy.st;
@@ -1005,10 +1073,10 @@ k_stencil(const __grid_constant__ StencilArgs a)
             else if (EP == EP_RESID && hd.h1.z) st0->npart_b = bps;
         }
         if (first_failed >= 0) {                 // an earlier time step of this system failed
-            if (EP == EP_CGA && nsys == 1 && sys_lead) { set_while(a.sy, 0); set_if(a.sy, 0); }
+            if ((EP == EP_CGA || EP == EP_CG1) && nsys == 1 && sys_lead) { set_while(a.sy, 0); set_if(a.sy, 0); }
             return;
         }
-        if (EP == EP_CGA || EP == EP_RESID) {
+        if (EP == EP_CGA || EP == EP_RESID || EP == EP_CG1 || EP == EP_CG1W) {
             if (!active) return;                 // converged / stopped: nothing to do
             if (EP == EP_RESID && !hd.h1.z) return;
         }
@@ -1039,6 +1107,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     // EL_Q1P: per material the (a, b) coefficients of the fused z butterfly, as the pair path
     // computes them from (k, c) (bit-identical): palt[m] = {a0, b0, a1, b1, a2, b2, a3, b3}
     double(*palt)[8] = reinterpret_cast<double(*)[8]>(seam + 2);
+    Real *const ubuf = reinterpret_cast<Real *>(reinterpret_cast<char *>(palt) + SH::PAL_BYTES);   // LD_CG1
 
     const int X0 = blockIdx.x * TILE_X;
     const int Y0 = blockIdx.y * (NW * R - 1);
@@ -1067,10 +1136,13 @@ k_stencil(const __grid_constant__ StencilArgs a)
         const int p = zb - 1 + it;
         Real *sb = stage + st * SH::STAGE_DBL;
         mbar_expect_tx(&bars[st], SH::STAGE_BYTES);
-        if (LD == LD_CGD && PEER && (p == a.gz_lo || p == a.gz_hi))   // s of a neighbour's plane
+        if (LD == LD_CG1 || LD == LD_CG1W) {   // single-reduction PCG: node maps 0 .. NA-1
+#pragma unroll
+            for (int k = 0; k < NA; k++) tma_load_3d(sb + k * SH::NODE_DBL, a.tm + k, xb, Y0 - 1, p, &bars[st]);
+        } else if (LD == LD_CGD && PEER && (p == a.gz_lo || p == a.gz_hi))   // s of a neighbour's plane
             tma_load_3d(sb, a.tm + MAP_GHOST, xb, Y0 - 1, p == a.gz_lo ? 0 : 1, &bars[st]);
         else if (NA >= 1) tma_load_3d(sb, a.tm + map0, xb, Y0 - 1, p, &bars[st]);
-        if (NA >= 2) tma_load_3d(sb + SH::NODE_DBL, a.tm + map1, xb, Y0 - 1, p, &bars[st]);
+        if (NA >= 2 && LD != LD_CG1 && LD != LD_CG1W) tma_load_3d(sb + SH::NODE_DBL, a.tm + map1, xb, Y0 - 1, p, &bars[st]);
         if (EL == EL_TETV)   // per-node (k, c) pairs of plane p, same rows as the node box
             tma_load_3d(sb + NA * SH::NODE_DBL, a.tm + MAP_KCN, 2 * xb, Y0 - 1, p, &bars[st]);
         else if (EL == EL_Q1P)   // material ids of element layer p - 1 (16-B aligned x origin)
@@ -1081,13 +1153,14 @@ k_stencil(const __grid_constant__ StencilArgs a)
 
     if (tid == 0) {
         if (smem_u32(stage) & 127u) __trap();     // TMA destinations need 128-B alignment
-        if (EP != EP_CGA) {                       // (kernel A initialised them before its wait)
+        if (EP != EP_CGA && EP != EP_CG1) {       // (kernel A initialised them before its wait)
             for (int i = 0; i < NS; i++) mbar_init(&bars[i], 1);
             fence_mbar_init();
         }
         if (a.tm_fence) {
-            if (NA >= 1) tensormap_acquire(a.tm + map0);
-            if (NA >= 2) tensormap_acquire(a.tm + map1);
+            if (LD == LD_CG1 || LD == LD_CG1W) for (int k = 0; k < NA; k++) tensormap_acquire(a.tm + k);
+            else if (NA >= 1) tensormap_acquire(a.tm + map0);
+            if (NA >= 2 && LD != LD_CG1 && LD != LD_CG1W) tensormap_acquire(a.tm + map1);
             tensormap_acquire(a.tm + KMAP);
         }
     }
@@ -1112,6 +1185,48 @@ k_stencil(const __grid_constant__ StencilArgs a)
         __syncthreads();
     }
 
+    double alpha1 = 0.0, bb_fwd = 0.0;      // EP_CG1: alpha_i; EP_CG1W: ||b_F||^2 forwarded by block 0
+    if (EP == EP_CG1) {
+        // start of iteration i of the single-reduction PCG from the previous kernel's sums
+        double ps[NPART];
+        prev_sums<NT>(a.sy, npart_b, ps, sj);
+        const IterStart1 is = iter_start_cg1(sst, it_i, ps, max_iter);
+        if (sys_lead) {
+            CgState *stw = sst;
+            stw->rr = is.rr;
+            if (it_i == 0) { stw->bb = is.bb; stw->thresh = is.thresh; }
+            stw->delta[it_i & 1] = is.gamma;
+            stw->alf[it_i & 1] = is.alpha;
+            if (!is.go) {
+                stw->active = 0;
+                stw->status = is.status;
+                stw->zero_x = is.zero_x;
+                stw->iter = it_i;
+                set_while(a.sy, 0);
+                set_if(a.sy, 0);
+            } else {
+                // loop duties: the next iteration's counter (the other parity's slot) and the
+                // residual replacement after this iteration (Alg. 1 line 10, R6)
+                const bool replace = it_i > 0 && re_ > 0 && (it_i % re_) == 0;
+                if (a.c1.par) stw->b_iter = it_i + 1;
+                else stw->a_iter = it_i + 1;
+                stw->replace = replace;
+                set_if(a.sy, replace ? 1 : 0);
+            }
+        }
+        if (!is.go) {
+            for (int i = 0; i < NS && i < nplanes; i++) mbar_wait(&bars[i], 0);   // drain the TMA
+            return;
+        }
+        beta = is.beta;
+        alpha1 = is.alpha;
+    }
+    if (EP == EP_CG1W && blk == 0) {
+        // ||b_F||^2 of the init kernel (slot 2 of its sums) rides along in block 0's partial
+        double ps[NPART];
+        prev_sums<NT>(a.sy, npart_b, ps, sj);
+        bb_fwd = ps[2];
+    }
     if (EP == EP_CGA) {
         // start of PCG iteration i from the previous kernel's partial sums (overlaps the TMA)
         double ps[NPART];
@@ -1162,6 +1277,56 @@ k_stencil(const __grid_constant__ StencilArgs a)
     }
 
     const Real betar = (Real)beta;
+    const Real alphar = (Real)alpha1;
+    const bool first_it = it_i == 0;
+    // planes whose owned nodes this CTA updates / stores (each plane of the run belongs to one chunk)
+    auto own_plane = [&](int pl) -> bool {
+        return (pl >= a.zs0 && pl < a.zs1) &&
+               ((pl >= zb && pl < ze) || (pl == zb - 1 && zb == a.z_out0) || (pl == ze && ze == a.z_out1));
+    };
+    // LD_CG1 pre-pass: the CTA's threads form u_{i+1} once per box node (rows 0..NW R, columns
+    // xoff .. xoff + TILE_X + 1) into the shared u plane; thread t takes the owned nodes
+    // n = t + k NT (k < KOWN) of the tile (box rows 1..NW R - 1, columns xoff+1 .. xoff+TILE_X) and
+    // t < NHALO one halo node.  p_{i-1} and x_i of its owned nodes are prefetched one plane ahead.
+    constexpr int OWNR = NW * R - 1, NOWN = TILE_X * OWNR, KOWN = (NOWN + NT - 1) / NT;
+    constexpr int NHALO = 2 * (TILE_X + 2) + 2 * OWNR;
+    static_assert(LD != LD_CG1 || NHALO <= NT, "halo pass: one node per thread");
+    Real *const c1x = EP == EP_CG1 ? reinterpret_cast<Real *>(a.c1.x ? a.c1.x : a.ring[(step_ + 1) % 3]) : nullptr;
+    Real *const c1p = reinterpret_cast<Real *>(a.c1.p);
+    int c1o[KOWN], c1h = 0;
+    long long c1g[KOWN];
+    unsigned c1own = 0;
+    Real pfp[KOWN], pfx[KOWN];
+    if constexpr (LD == LD_CG1) {
+        constexpr int BW = SH::BW;
+#pragma unroll
+        for (int k = 0; k < KOWN; k++) {
+            const int n = tid + k * NT;
+            const int row = 1 + n / TILE_X, col = 1 + n % TILE_X;
+            const int x = X0 - 1 + col, y = Y0 - 1 + row;
+            c1o[k] = n < NOWN ? row * BW + xoff + col : -1;
+            c1g[k] = (long long)y * g.pitch + x;
+            if (n < NOWN && x < g.nx1 && y < g.ny1) c1own |= 1u << k;
+        }
+        int hr, hc;
+        const int t = tid;
+        if (t < TILE_X + 2) { hr = 0; hc = t; }
+        else if (t < 2 * (TILE_X + 2)) { hr = NW * R; hc = t - (TILE_X + 2); }
+        else if (t < 2 * (TILE_X + 2) + OWNR) { hr = 1 + t - 2 * (TILE_X + 2); hc = 0; }
+        else { hr = 1 + t - 2 * (TILE_X + 2) - OWNR; hc = TILE_X + 1; }
+        c1h = hr * BW + xoff + hc;
+    }
+    auto c1_prefetch = [&](int pl) {
+        if (EP == EP_CG1 && own_plane(pl)) {
+            const long long b0 = (long long)pl * g.plane;
+#pragma unroll
+            for (int k = 0; k < KOWN; k++)
+                if ((c1own >> k) & 1u) {
+                    pfx[k] = c1x[b0 + c1g[k]];
+                    if (!first_it) pfp[k] = c1p[b0 + c1g[k]];
+                }
+        }
+    };
     Real Fp[R][4];            // Q1: face transforms of the lower plane p-1
     Real Cy[R][4];            // contributions carried from the layer below (face / node space)
     float2 Fp2[R][2], Cy2[R][2];  // fp32 Q1: the same per channel pair (0,2), (1,3), packed math
@@ -1169,7 +1334,9 @@ k_stencil(const __grid_constant__ StencilArgs a)
     V2 PK0[R + 1], PK1[R + 1];    // EL_TETV: node (k, c) pairs of plane p-1 at x and x+1
     Real cen[R];              // raw centre values of plane p-1 (rows 0..R-1)
     double acc[NPART] = {0.0, 0.0, 0.0, 0.0};
+    if (EP == EP_CG1W && blk == 0 && tid == 0) acc[2] = bb_fwd;
     bool remote = false;                     // this thread stored into a neighbour's memory
+    c1_prefetch(zb - 1);
 #pragma unroll
     for (int r = 0; r < R; r++) {
 #pragma unroll
@@ -1195,7 +1362,44 @@ k_stencil(const __grid_constant__ StencilArgs a)
 #endif
         if (it == 0) HF_TR(4);
         const Real *sb = stage + st * SH::STAGE_DBL;
-        const Real *n0 = sb + w * R * SH::BW + lane + xoff;                 // row 0 of this warp
+        if constexpr (LD == LD_CG1) {
+            // ---- pre-pass: s_i = w_i + beta s_{i-1}; r_{i+1} = r_i - alpha s_i; u_{i+1} = P^{-1} r_{i+1}
+            const Real *sr = sb, *sw = sb + SH::NODE_DBL, *ss = sb + 2 * SH::NODE_DBL, *si = sb + 3 * SH::NODE_DBL;
+            const bool ownp = own_plane(p);
+            const long long pb = (long long)p * g.plane;
+            Real *const sout = reinterpret_cast<Real *>(a.c1.sout);
+            Real *const rout = reinterpret_cast<Real *>(a.c1.rout);
+#pragma unroll
+            for (int k = 0; k < KOWN; k++) {
+                const int o = c1o[k];
+                if (o < 0) continue;
+                const Real rv = sr[o], wv = sw[o], sv = ss[o], iv = si[o];
+                const Real sn = first_it ? wv : fma(betar, sv, wv);
+                const Real rn = fma(-alphar, sn, rv);
+                const Real u = iv * rn;
+                ubuf[o] = u;
+                if (ownp && ((c1own >> k) & 1u)) {
+                    // owned node: s_i, r_{i+1}; p_i = u_i + beta p_{i-1}; x_{i+1} = x_i + alpha p_i
+                    const long long idx = pb + c1g[k];
+                    sout[idx] = sn;
+                    rout[idx] = rn;
+                    const Real uo = iv * rv;
+                    const Real pn = first_it ? uo : fma(betar, pfp[k], uo);
+                    c1p[idx] = pn;
+                    c1x[idx] = fma(alphar, pn, pfx[k]);
+                    acc[0] = fma((double)rn, (double)u, acc[0]);
+                    acc[1] = fma((double)rn, (double)rn, acc[1]);
+                }
+            }
+            if (tid < NHALO) {
+                const int o = c1h;
+                const Real sn = first_it ? sw[o] : fma(betar, ss[o], sw[o]);
+                ubuf[o] = si[o] * fma(-alphar, sn, sr[o]);
+            }
+            c1_prefetch(p + 1);
+            __syncthreads();                            // u plane complete ((k, c) still read below)
+        }
+        const Real *n0 = (LD == LD_CG1 ? ubuf : sb) + w * R * SH::BW + lane + xoff;   // row 0 of this warp
         const Real *n1 = sb + SH::NODE_DBL + w * R * SH::BW + lane + xoff;
         const Real *kcs = sb + NA * SH::NODE_DBL + w * R * SH::KW + koff + 2 * lane;
         const unsigned char *kis = reinterpret_cast<const unsigned char *>(sb + NA * SH::NODE_DBL) + w * R * PAL_BW +
@@ -1217,18 +1421,26 @@ k_stencil(const __grid_constant__ StencilArgs a)
                 for (int ch = 0; ch < 4; ch++) pabr[r][ch] = pe[ch];
             }
         }
-        const bool store_p = (EP == EP_CGA || EP == EP_RESID_INIT) && (p >= a.zs0 && p < a.zs1) &&
-                             ((p >= zb && p < ze) || (p == zb - 1 && zb == a.z_out0) ||
-                              (p == ze && ze == a.z_out1));
+        const bool store_p = (EP == EP_CGA || EP == EP_RESID_INIT || EP == EP_CG1 || EP == EP_CG1W) && own_plane(p);
         Real *cst = store_p ? cstore + (long long)p * g.plane + rowbase : nullptr;
 #pragma unroll
         for (int r = 0; r <= R; r++) {
             Real v, v1;
             constexpr int BW = SH::BW;
-            if (LD == LD_RAW) { v = n0[r * BW]; v1 = n0[r * BW + 1]; }
+            if (LD == LD_RAW || LD == LD_CG1) { v = n0[r * BW]; v1 = n0[r * BW + 1]; }
             else if (LD == LD_CGD) {
                 v = fma(betar, n1[r * BW], n0[r * BW]);
                 v1 = fma(betar, n1[r * BW + 1], n0[r * BW + 1]);
+            } else if (LD == LD_CG1W) {
+                // u = P^{-1} r (map 0: r, map 1: P^{-1}); owned nodes: r^T u, r^T r
+                const int o = r * BW;
+                const Real r0v = n0[o];
+                v = n1[o] * r0v;
+                v1 = n1[o + 1] * n0[o + 1];
+                if (r < R && store_p && ((own >> r) & 1u)) {
+                    acc[0] = fma((double)r0v, (double)v, acc[0]);
+                    acc[1] = fma((double)r0v, (double)r0v, acc[1]);
+                }
             } else if (LD == LD_X0) {
                 v = n0[r * BW];
                 v1 = n0[r * BW + 1];
@@ -1245,7 +1457,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
             if (r < R) {
                 craw[r] = v;
                 // d_new (CG kernel A) or the guess x0 (init) is stored once, raw, by its owner
-                if (store_p && ((own >> r) & 1u)) cst[r * g.pitch] = v;
+                if ((EP == EP_CGA || EP == EP_RESID_INIT) && store_p && ((own >> r) & 1u)) cst[r * g.pitch] = v;
             }
             if (MASK) {
                 double gv;
@@ -1435,6 +1647,11 @@ k_stencil(const __grid_constant__ StencilArgs a)
                     if (HB) y = fma((Real)a.s, bvec[idx], y);
                     if (DIR && DSET && isd) y = (Real)gv;
                     out0[idx] = y;
+                } else if (EP == EP_CG1 || EP == EP_CG1W) {
+                    const Real u = cen[e];
+                    const Real wv = isd ? u : yv[e];        // identity rows (R3)
+                    reinterpret_cast<Real *>(a.c1.wout)[idx] = wv;
+                    acc[3] = fma((double)u, (double)wv, acc[3]);
                 } else if (EP == EP_CGA) {
                     const Real d = cen[e];
                     const Real q = isd ? d : yv[e];         // identity rows (R3)
@@ -1458,7 +1675,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     }
 
     if (EP == EP_APPLY) return;
-    if (EP == EP_CGA) pdl_trigger();
+    if (EP == EP_CGA || EP == EP_CG1) pdl_trigger();
     HF_TR(5);
     // per-block partial sums for the next kernel: A -> (d^T q); init, RESID -> (r^T s, r^T r, b^T b)
     block_reduce_store<NT>(acc, a.sy.pout, blk);

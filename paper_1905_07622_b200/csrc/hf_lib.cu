@@ -162,7 +162,7 @@ static hf_status get_encode()
 
 struct SimKey {
     double aK = 0, aM = 0, aKL = 0, aML = 0, rtol = 0, dt = 0;
-    int max_iter = 0, replace_every = 0, first = 0, snap_plane = -1, lift = 0, res = 0;
+    int max_iter = 0, replace_every = 0, first = 0, snap_plane = -1, lift = 0, res = 0, cg1 = 0;
     const double *F = nullptr;
     double *snap = nullptr;
     bool operator==(const SimKey &o) const { return std::memcmp(this, &o, sizeof(SimKey)) == 0; }
@@ -182,6 +182,12 @@ struct Sys {                         // one system's PCG workspace (Table 3 buff
     unsigned long long *gbar = nullptr;          // grid-barrier counter of the fused A+B launch
     CgState *st_ring = nullptr;                  // pinned state copies of the pipelined host loop
     cudaEvent_t ev_ring[2] = {nullptr, nullptr};
+    // single-reduction PCG (hf_set_cg_variant 1): r, w = A u, s = A p ping-pong by iteration
+    // parity, p; node maps of the CG1 kernel of parity k (r[k], w[k], s[k], P^-1) and of the
+    // w = A P^-1 r kernel reading r[k] (r[k], P^-1)
+    double *c1r[2] = {nullptr, nullptr}, *c1w[2] = {nullptr, nullptr}, *c1s[2] = {nullptr, nullptr};
+    double *c1p = nullptr;
+    Maps c1maps[2], c1wmaps[2];
 
     int *iters = nullptr;
     int iters_cap = 0;
@@ -249,6 +255,8 @@ struct hf_ctx {
     int unroll = 0;                  // PCG iterations per WHILE-body launch (0: by grid size, see build_cg_graph)
     int pdl = 1;                     // programmatic A <-> B edges in the loop body (HF_PDL=0 disables)
     int fuse_ab = 0;                 // A and B of an iteration in one launch (HF_FUSE_AB=1)
+    int cg1 = 0;                     // hf_set_cg_variant: 1 = single-reduction PCG (one kernel per iteration)
+    int last_cg1 = 0;                // the last hf_simulate* ran the single-reduction PCG
     int tm_fence = 0;                // acquire TMA descriptors in every launch (HF_TM_FENCE=1, see maps_dev)
     int resident = 0;                // hf_set_resident: 1 = on-chip PCG when eligible, 0 = never (default)
     int last_resident = 0;           // the last hf_simulate* ran the on-chip PCG
@@ -665,18 +673,19 @@ struct Launch {
 #endif
 template <int R, int LD> constexpr int ns_of()
 {
-    return (R >= 4 && StencilShape<R, NW, LD>::NA == 2) ? 3 : (R == 2 ? HF_NS_R2 : 4);
+    return (LD == LD_CG1 || (R >= 4 && StencilShape<R, NW, LD>::NA >= 2)) ? 3 : (R == 2 ? HF_NS_R2 : 4);
 }
 
 struct StencilFn {
     const void *fn;
     size_t smem;
+    int nw = NW;             // warps per CTA
 };
 
 template <int R, int LD, int EP, int FL, int EL, class Real> static StencilFn stencil_fn_t()
 {
     constexpr int NS = ns_of<R, LD>();
-    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL, Real>, StencilShape<R, NW, LD, Real, EL>::smem_bytes(NS)};
+    return {(const void *)k_stencil<R, NW, NS, LD, EP, FL, EL, Real>, StencilShape<R, NW, LD, Real, EL>::smem_bytes(NS), NW};
 }
 
 // every (loader, epilogue, flags) variant the library launches, for tile heights R = 2 and 4
@@ -717,6 +726,20 @@ template <class Real> static StencilFn stencil_fn_p(int R, int LD, int EP, int F
     }
     HF_STENCIL_VARIANTS(X)
 #undef X
+    // single-reduction PCG kernels: fp64, Q1 elements ((k, c) pairs or material ids)
+    if constexpr (sizeof(Real) == 8) {
+#define Y(ld, ep, fl)                                                                           \
+        if (LD == (ld) && EP == (ep) && FL == (fl) && (EL == EL_Q1 || EL == EL_Q1P)) {          \
+            if (EL == EL_Q1P)                                                                   \
+                return R >= 4 ? stencil_fn_t<4, ld, ep, fl, EL_Q1P, Real>() : stencil_fn_t<2, ld, ep, fl, EL_Q1P, Real>(); \
+            return R >= 4 ? stencil_fn_t<4, ld, ep, fl, EL_Q1, Real>() : stencil_fn_t<2, ld, ep, fl, EL_Q1, Real>(); \
+        }
+        Y(LD_CG1, EP_CG1, 0)
+        Y(LD_CG1, EP_CG1, FL_DIR)
+        Y(LD_CG1W, EP_CG1W, 0)
+        Y(LD_CG1W, EP_CG1W, FL_DIR)
+#undef Y
+    }
     return {nullptr, 0};
 }
 
@@ -756,7 +779,7 @@ static hf_status update_occ(hf_ctx *c)
     StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, el, c->es);
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
     int occ = 0;
-    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
+    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * f.nw, f.smem));
     c->occ = std::max(1, occ);
     return HF_OK;
 }
@@ -864,7 +887,7 @@ static int dir_flags(const hf_ctx *c, int EP, bool has_b, bool dset)
     if (EP != EP_APPLY && c->comm && c->comm->in_kernel()) fl |= FL_PEER;   // mailbox sums / ghosts
     if (c->dbits) {
         if (EP == EP_APPLY) { if (dset) fl |= FL_DIR | FL_DSET; }
-        else if (EP == EP_CGA) fl |= FL_DIR;
+        else if (EP == EP_CGA || EP == EP_CG1 || EP == EP_CG1W) fl |= FL_DIR;
         else fl |= FL_MASK | FL_DIR;
     }
     return fl;
@@ -927,7 +950,7 @@ static hf_status stencil_launch(hf_ctx *c, int LD, int EP, bool dset, const Maps
     Launch L;
     L.fn = f.fn;
     L.grid = grid;
-    L.block = dim3(32, NW, 1);
+    L.block = dim3(32, f.nw, 1);
     L.smem = f.smem;
     HFCK(maps_dev(c, maps, &a.tm));
     a.tm_fence = c->tm_fence;
@@ -1050,6 +1073,8 @@ static void sys_free(Sys &s)
     for (int i = 0; i < 3; i++) cudaFree(s.U[i]);
     cudaFree(s.b); cudaFree(s.r); cudaFree(s.s); cudaFree(s.q); cudaFree(s.invd);
     cudaFree(s.dbuf[0]); cudaFree(s.dbuf[1]);
+    for (int k = 0; k < 2; k++) { cudaFree(s.c1r[k]); cudaFree(s.c1w[k]); cudaFree(s.c1s[k]); }
+    cudaFree(s.c1p);
     cudaFree(s.st); cudaFreeHost(s.st_host);
     cudaFree(s.partA); cudaFree(s.partB); cudaFree(s.sums); cudaFree(s.iters); cudaFree(s.gbar);
     if (s.st_ring) cudaFreeHost(s.st_ring);
@@ -1135,6 +1160,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     if (const char *e = getenv("HF_UNROLL")) c->unroll = std::min(50, std::max(1, atoi(e)));
     if (const char *e = getenv("HF_PDL")) c->pdl = atoi(e) != 0;
     if (const char *e = getenv("HF_FUSE_AB")) c->fuse_ab = atoi(e) != 0;
+    if (const char *e = getenv("HF_CG1")) c->cg1 = atoi(e) != 0;
     if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
     if (const char *e = getenv("HF_TM_FENCE")) c->tm_fence = atoi(e) != 0;
     if (const char *e = getenv("HF_RESIDENT")) c->resident = atoi(e) != 0;
@@ -1142,7 +1168,7 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
     StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
     HFCK(ensure_smem_attr(f.fn, f.smem, device));
     int occ = 0;
-    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
+    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * f.nw, f.smem));
     c->occ = std::max(1, occ);
     // partial-sum buffers sized for any tile height / z split (upper bound: one plane per CTA)
     {
@@ -1296,7 +1322,7 @@ static hf_status cg_launches(hf_ctx *c, Sys &s, double aK, double aM, double *x,
         f.gbar = s.gbar;
         HFCK(stencil_launch(c, LD_CGD, EP_CGA, false, s.maps, f, 0, &L->AB, FL_FUSEB));
         int occ = 0;
-        CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->AB.fn, 32 * NW, L->AB.smem));
+        CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->AB.fn, 32 * L->AB.block.y, L->AB.smem));
         const long long grid = (long long)L->AB.grid.x * L->AB.grid.y * L->AB.grid.z;
         L->has_ab = (long long)occ * c->nsm >= grid;
     }
@@ -1609,6 +1635,180 @@ static hf_status build_cg_graph(hf_ctx *c, std::vector<Launch> pre, Launch init,
     prev = wnode;
     for (auto &p : post) { HFCK(add_node(g, p, &prev, &n)); prev = n; }
     *out = g;
+    return HF_OK;
+}
+
+// ---- single-reduction PCG (hf_set_cg_variant 1) -----------------------
+// One stencil kernel per iteration (EP_CG1): the Chronopoulos-Gear arrangement of Alg. 1 keeps
+// w = A u and s = A p by recurrence, so alpha_i and beta_i both follow from ONE set of sums
+// (r^T u, w^T u) of the previous kernel, and the vector updates of Alg. 1 lines 9, 13, 15, 18 run
+// inside the stencil kernel that computes the next w.  Kernel i has the parity k = i & 1, fixed
+// per graph node (every WHILE body starts at an even iteration and holds an even number of
+// copies), so its TMA maps, output buffers and partial-sum slots are bound at build time:
+//   CG1(k): reads r[k], w[k], s[k] (+ P^-1) and partials P[k^1]; writes r[k^1], w[k^1], s[k^1], p,
+//           x and partials P[k]
+//   RES(k): r[k] = b - A x (replacement, Alg. 1 line 10); partials P[k]
+//   W(k):   w[k] = A P^-1 r[k]; reads partials P[k], writes P[k^1]
+// Solve: init (r[0], partials P[0]) -> W(0) -> WHILE{ CG1(0) -> [IF: RES(1) -> W(1)] -> CG1(1) -> ... }.
+static bool cg1_eligible(const hf_ctx *c, const Sys &s)
+{
+    return c->cg1 && c->es == 8 && c->elem == EL_Q1 && c->nsys == 1 && !c->comm && &s == &c->sys0;
+}
+
+static hf_status c1_alloc(hf_ctx *c, Sys &s)
+{
+    if (s.c1p) return HF_OK;
+    const size_t vb = (size_t)c->nloc * c->es;
+    double **vecs[] = {&s.c1r[0], &s.c1r[1], &s.c1w[0], &s.c1w[1], &s.c1s[0], &s.c1s[1], &s.c1p};
+    for (double **v : vecs) {
+        CUCK(cudaMalloc(v, vb));
+        CUCK(cudaMemsetAsync(*v, 0, vb, s.stream));   // pitch padding must stay zero
+    }
+    return HF_OK;
+}
+
+struct Cg1Launches {
+    Launch C[2];      // iteration of parity k
+    Launch W[2];      // w[k] = A P^-1 r[k]
+    Launch RES[2];    // r[k] = b - A x
+};
+
+static hf_status cg1_launches(hf_ctx *c, Sys &s, double aK, double aM, Cg1Launches *L)
+{
+    HFCK(c1_alloc(c, s));
+    dim3 grid;
+    int chunk, zper;
+    stencil_grid(c, c->own_lo, c->own_hi, &grid, &chunk, &zper);
+    const int nb = (int)(grid.x * grid.y * grid.z);     // partials per stencil launch (same grid for all)
+    double *P[2] = {s.partA, s.partB};
+    for (int k = 0; k < 2; k++) {
+        Maps m = s.maps, mw = s.maps;
+        HFCK(node_map(c, s.c1r[k], &m.node[0]));
+        HFCK(node_map(c, s.c1w[k], &m.node[1]));
+        HFCK(node_map(c, s.c1s[k], &m.node[2]));
+        HFCK(node_map(c, s.invd, &m.node[3]));
+        for (int j = 4; j < NMAPS; j++) m.node[j] = m.node[0];    // unused (valid for the prefetch)
+        mw.node[0] = m.node[0];
+        mw.node[1] = m.node[3];
+        for (int j = 2; j < NMAPS; j++) mw.node[j] = m.node[0];
+        StencilArgs a = base_args(c, aK, aM);
+        a.c1.rout = s.c1r[k ^ 1];
+        a.c1.sout = s.c1s[k ^ 1];
+        a.c1.wout = s.c1w[k ^ 1];
+        a.c1.p = s.c1p;
+        a.c1.x = nullptr;                                  // the time-step ring slot
+        a.c1.par = k;
+        for (int i = 0; i < 3; i++) a.ring[i] = s.U[i];
+        a.sy = make_sync(c, s);
+        a.sy.pin = P[k ^ 1];
+        a.sy.pin_n = nb;
+        a.sy.pout = P[k];
+        HFCK(stencil_launch(c, LD_CG1, EP_CG1, false, m, a, 0, &L->C[k]));
+        StencilArgs w = base_args(c, aK, aM);
+        w.c1.wout = s.c1w[k];
+        w.sy = make_sync(c, s);
+        w.sy.pin = P[k];
+        w.sy.pin_n = nb;
+        w.sy.pout = P[k ^ 1];
+        HFCK(stencil_launch(c, LD_CG1W, EP_CG1W, false, mw, w, 2, &L->W[k]));
+        StencilArgs rr = base_args(c, aK, aM);
+        rr.invd = s.invd;
+        rr.bvec = s.b;
+        rr.out0 = s.c1r[k];
+        rr.out_s = s.s;                                    // (s = P^-1 r: not used by this variant)
+        rr.sy = make_sync(c, s, -1, 0);
+        rr.sy.pout = P[k];
+        rr.rot_role = ROT_X;
+        HFCK(stencil_launch(c, LD_RAW, EP_RESID, true, s.maps, rr, 2, &L->RES[k]));
+    }
+    return HF_OK;
+}
+
+// root: [pre...] -> init -> W(0) -> WHILE(active){ CG1(0) -> IF(replace){ RES(1) -> W(1) } -> CG1(1) -> ... }
+static hf_status build_cg1_graph(hf_ctx *c, const std::vector<Launch> &pre, const Launch &init, const Cg1Launches &L,
+                                 const std::vector<Launch> &post, int replace_every, cudaGraph_t *out)
+{
+    cudaGraph_t g;
+    CUCK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hw, hi = 0;
+    CUCK(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t prev = nullptr, n;
+    for (auto &p : pre) { HFCK(add_node(g, p, prev ? &prev : nullptr, &n)); prev = n; }
+    HFCK(add_node(g, init, prev ? &prev : nullptr, &n));
+    prev = n;
+    HFCK(add_node(g, L.W[0], &prev, &n));
+    prev = n;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hw;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CUCK(cudaGraphAddNode(&wnode, g, &prev, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    // an even number of copies per body (static parities), a divisor of the replacement period
+    // when one exists (then only the first copy can meet a replacement iteration: one IF node)
+    int U = c->unroll > 0 ? c->unroll : (c->nloc >= 500000 ? 50 : 10);
+    U = std::max(2, U & ~1);
+    if (replace_every > 0)
+        while (U > 2 && replace_every % U != 0) U -= 2;
+    const bool if_first_only = replace_every > 0 && replace_every % U == 0;
+    cudaGraphNode_t bprev = nullptr;
+    bool bprev_is_k = false;
+    for (int u = 0; u < U; u++) {
+        const int k = u & 1;
+        const bool with_if = replace_every > 0 && !(u > 0 && if_first_only);
+        if (with_if) CUCK(cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault));
+        Launch C = L.C[k];
+        StencilArgs ca = C.get<StencilArgs>(0);
+        ca.sy.h_while = hw; ca.sy.h_if = hi; ca.sy.use_handles = 1; ca.sy.use_if = with_if;
+        C.put(0, ca);
+        cudaGraphNode_t nc;
+        if (c->pdl && bprev && bprev_is_k) {
+            HFCK(add_node(body, C, nullptr, &nc));
+            HFCK(add_pdl_edge(body, bprev, nc));
+        } else
+            HFCK(add_node(body, C, bprev ? &bprev : nullptr, &nc));
+        bprev = nc;
+        bprev_is_k = true;
+        if (!with_if) continue;
+        cudaGraphNodeParams ip = {};
+        ip.type = cudaGraphNodeTypeConditional;
+        ip.conditional.handle = hi;
+        ip.conditional.type = cudaGraphCondTypeIf;
+        ip.conditional.size = 1;
+        cudaGraphNode_t inode;
+        CUCK(cudaGraphAddNode(&inode, body, &nc, 1, &ip));
+        cudaGraphNode_t nr, nw;
+        HFCK(add_node(ip.conditional.phGraph_out[0], L.RES[k ^ 1], nullptr, &nr));
+        HFCK(add_node(ip.conditional.phGraph_out[0], L.W[k ^ 1], &nr, &nw));
+        bprev = inode;
+        bprev_is_k = false;
+    }
+    prev = wnode;
+    for (auto &p : post) { HFCK(add_node(g, p, &prev, &n)); prev = n; }
+    *out = g;
+    return HF_OK;
+}
+
+// host-loop driver of the same sequence (profiling, sanitizers)
+static hf_status host_cg1_loop(hf_ctx *c, Sys &s, const Cg1Launches &L, int max_iter, int replace_every)
+{
+    HFCK(read_state(c, s));
+    if (!s.st_host->active) return HF_OK;
+    for (int i = 0;;) {
+        const int k = i & 1;
+        HFCK(run(c, L.C[k], s.stream));
+        if (i > 0 && replace_every > 0 && i % replace_every == 0) {
+            HFCK(run(c, L.RES[k ^ 1], s.stream));
+            HFCK(run(c, L.W[k ^ 1], s.stream));
+        }
+        i++;
+        if (i % c->check_every == 0 || i > max_iter) {
+            HFCK(read_state(c, s));
+            if (!s.st_host->active) break;
+        }
+    }
     return HF_OK;
 }
 
@@ -2179,6 +2379,9 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     const bool mixed = c->lo && use_graph && &s == &c->sys0 && !rp.ok;
     key.res = rp.ok + 2 * (int)mixed;
     c->last_resident = rp.ok;
+    const bool use_cg1 = cg1_eligible(c, s) && !mixed && !rp.ok;
+    key.cg1 = use_cg1;
+    c->last_cg1 = use_cg1;
     const bool cached = use_graph && s.key_valid && s.key == key && s.gexec && (!mixed || c->mix_exec);
     if (mixed) {
         // the fp32 shadow's solver state and Jacobi diagonal (same operator, fp32 storage)
@@ -2190,6 +2393,7 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
     std::vector<Launch> pre, post;
     Launch init;
     CgLaunches L;
+    Cg1Launches L1;
     if (!cached) {
         Sync sy = make_sync(c, s);
         // b = L u^n + dt F  (knl_RHS_A/B P:678-681), b_D = g
@@ -2281,7 +2485,13 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             ia.zs0 = ia.zs1 = 0;
             HFCK(stencil_launch(c, LD_RAW, EP_RESID_INIT, true, s.maps, ia, 2, &init));
         }
-        if (!rp.ok) HFCK(cg_launches(c, s, aK, aM, nullptr, s.maps, &L));
+        if (use_cg1) {
+            // single-reduction PCG: the init kernel writes r[0] and its partials into P[0] (partA)
+            HFCK(cg1_launches(c, s, aK, aM, &L1));
+            ia.out0 = s.c1r[0];
+            ia.sy = make_sync(c, s, -1, 0);
+            HFCK(stencil_launch(c, LD_X0, EP_RESID_INIT, true, s.maps, ia, 2, &init));
+        } else if (!rp.ok) HFCK(cg_launches(c, s, aK, aM, nullptr, s.maps, &L));
         post = step_launches(c, step_args(c, s, nullptr, snapdev, snap_local), true);
     }
 
@@ -2293,7 +2503,9 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             Launch RL;
             HFCK(res_launch(c, s, rp, aK, aM, first, &RL));
             HFCK(build_res_graph(c, pre, RL, post, &s.graph));
-        } else
+        } else if (use_cg1)
+            HFCK(build_cg1_graph(c, pre, init, L1, post, resolved(c, o).replace_every, &s.graph));
+        else
             HFCK(build_cg_graph(c, pre, init, L, post, o.replace_every, &s.graph));
         CUCK(cudaGraphInstantiate(&s.gexec, s.graph, 0));
         s.key = key;
@@ -2340,8 +2552,13 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
         for (int n = 0; n < nsteps; n++) {
             for (auto &p : pre) HFCK(run(c, p, s.stream));
             HFCK(run(c, init, s.stream));
-            HFCK(comm_after(c, s, 1, true));
-            HFCK(host_cg_loop(c, s, L, o.max_iter, o.replace_every));
+            if (use_cg1) {
+                HFCK(run(c, L1.W[0], s.stream));
+                HFCK(host_cg1_loop(c, s, L1, o.max_iter, resolved(c, o).replace_every));
+            } else {
+                HFCK(comm_after(c, s, 1, true));
+                HFCK(host_cg_loop(c, s, L, o.max_iter, o.replace_every));
+            }
             for (auto &p : post) HFCK(run(c, p, s.stream));
             if (c->comm) {
                 // the next RHS reads u^{n+1} ghosts: kernel B keeps the iterate's ghost planes
@@ -3112,9 +3329,25 @@ hf_status hf_set_precision(hf_ctx *c, int32_t bits)
     StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
     HFCK(ensure_smem_attr(f.fn, f.smem, c->device));
     int occ = 0;
-    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * NW, f.smem));
+    CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * f.nw, f.smem));
     c->occ = std::max(1, occ);
     HFCK(sys_alloc(c, c->sys0, c->stream));
+    return HF_OK;
+}
+
+hf_status hf_set_cg_variant(hf_ctx *c, int32_t variant)
+{
+    if (!c || variant < 0 || variant > 1) return fail(HF_E_ARG, "hf_set_cg_variant: variant must be 0 or 1");
+    c->cg1 = variant;
+    c->sys0.key_valid = false;
+    return HF_OK;
+}
+
+hf_status hf_cg_variant(hf_ctx *c, int32_t out[2])
+{
+    if (!c || !out) return fail(HF_E_ARG, "hf_cg_variant: NULL argument");
+    out[0] = c->cg1;
+    out[1] = c->last_cg1;
     return HF_OK;
 }
 
