@@ -338,6 +338,30 @@ hf_status hf_set_mixed(hf_ctx *ctx, int32_t enable, double rtol_lo);
 /* PCG iterations of the fp32 stage since hf_set_mixed (device counter; synchronises). */
 hf_status hf_mixed_iters(hf_ctx *ctx, int64_t *lo_iters);
 
+/* Tuning knobs of a context (performance only: every setting computes the same operator and
+ * PCG; results agree to rounding order).  Keys and values:
+ *   "tile_r"         0 = default (R = 2 below 16M local nodes, else 4; tets always 2), 2 or 4:
+ *                    node rows per thread of the stencil tiles (a CTA owns 31 x (8 R - 1) nodes)
+ *   "zchunk"         0 = sized to fill the SMs, else z planes per stencil CTA
+ *   "unroll"         0 = by grid size, else 1..50 PCG iterations per WHILE-body launch
+ *   "pdl"            1 (default) / 0: programmatic-launch edges between the loop kernels
+ *   "fuse_ab"        0 (default) / 1: kernels A and B of an iteration in one launch (grid barrier)
+ *   "check_every"    host-loop driver: iterations per asynchronous state check (default 8)
+ *   "tm_fence"       0 (default) / 1: acquire the TMA descriptors in every launch
+ *   "batch_group"    0 = modelled, else systems per stack of hf_simulate_batched
+ *   "comm_timeout_s" host-loop slab transports: fail (HF_E_NCCL) after this many seconds
+ *                    without progress (default 120)
+ * Changing a knob rebuilds the context's cached graphs at the next call.  The environment
+ * variables HF_TILE_R, HF_ZCHUNK, HF_UNROLL, HF_PDL, HF_FUSE_AB, HF_CHECK_EVERY, HF_TM_FENCE,
+ * HF_BATCH_GROUP, HF_COMM_TIMEOUT_S (and HF_DRIVER, HF_RESIDENT: hf_set_driver,
+ * hf_set_resident) give the defaults of a context when it is created; nothing reads them later.
+ * Errors: HF_E_ARG (NULL, unknown key, value out of range), HF_E_CUDA. */
+hf_status hf_set_tuning(hf_ctx *ctx, const char *key, int64_t value);
+
+/* The current value of a tuning knob ("tile_r" reports the tile height in use).
+ * Errors: HF_E_ARG. */
+hf_status hf_get_tuning(const hf_ctx *ctx, const char *key, int64_t *value);
+
 /* PCG arrangement of hf_simulate* (hf_set_cg_variant).  variant 0 (default): Alg. 1 as printed
  * (P:93-113), two streaming kernels per iteration (A: d = s + beta d, q = A d, d^T q; B: x, r, s
  * updates, r^T s, r^T r).  variant 1: the single-reduction (Chronopoulos-Gear) arrangement of the

@@ -83,6 +83,8 @@ _SIGS = {
     "hf_set_driver": (_i32, [_vp, _i32]),
     "hf_set_resident": (_i32, [_vp, _i32]),
     "hf_set_cg_variant": (_i32, [_vp, _i32]),
+    "hf_set_tuning": (_i32, [_vp, C.c_char_p, C.c_int64]),
+    "hf_get_tuning": (_i32, [_vp, C.c_char_p, _P(C.c_int64)]),
     "hf_cg_variant": (_i32, [_vp, _P(C.c_int32)]),
     "hf_set_mixed": (_i32, [_vp, _i32, _d]),
     "hf_mixed_iters": (_i32, [_vp, _P(C.c_int64)]),
@@ -449,6 +451,18 @@ def hf_set_mixed(ctx: Context, enable: int, rtol_lo: float = 1e-6):
 def hf_mixed_iters(ctx: Context) -> int:
     v = C.c_int64()
     _check(_lib.hf_mixed_iters(ctx.ptr, C.byref(v)))
+    return int(v.value)
+
+
+def hf_set_tuning(ctx: Context, key: str, value: int):
+    """Performance knob of the context (see heatfem.h: tile_r, zchunk, unroll, pdl, fuse_ab,
+    check_every, tm_fence, batch_group, comm_timeout_s)."""
+    _check(_lib.hf_set_tuning(ctx.ptr, key.encode(), int(value)))
+
+
+def hf_get_tuning(ctx: Context, key: str) -> int:
+    v = C.c_int64()
+    _check(_lib.hf_get_tuning(ctx.ptr, key.encode(), C.byref(v)))
     return int(v.value)
 
 

@@ -248,7 +248,10 @@ struct hf_ctx {
     double *flush = nullptr;
     int driver = 0;                  // 0 graph, 1 host loop
     int tileR = 4;
-    int zchunk_env = 0;
+    int zchunk = 0;                  // z planes per stencil CTA (0: sized to fill the SMs)
+    int tile_r_set = 0;              // tile height set by hf_set_tuning / HF_TILE_R (0: default_tile_r)
+    int batch_group = 0;             // systems per stack of hf_simulate_batched (0: stack_group's model)
+    double comm_timeout_s = 120.0;   // host-loop slab transports: fail instead of waiting longer
     int check_every = 8;
     int max_blocks = 0;
     int occ = 2;                     // resident CTAs/SM of the CG stencil (occupancy API)
@@ -811,7 +814,7 @@ static void stencil_grid(const hf_ctx *c, int z0, int z1, dim3 *grid, int *zchun
     const long long slots = (long long)(c->nsm_share ? c->nsm_share : c->nsm) * c->occ;
     long long nch = std::max(1LL, slots / (cols * ns));
     int chunk = (int)std::max(1LL, ((long long)planes + nch - 1) / nch);
-    if (c->zchunk_env > 0) chunk = c->zchunk_env;
+    if (c->zchunk > 0) chunk = c->zchunk;
     chunk = std::min(chunk, planes);
     nch = (planes + chunk - 1) / chunk;
     *grid = dim3(tx, ty, (unsigned)(nch * ns));
@@ -1099,6 +1102,24 @@ static void set_layout(hf_ctx *c)
     c->kc_elems = (long long)c->kpitch * c->g.ne[1] * (c->nzl + 1);
 }
 
+// The library's only reads of the environment: defaults of the tuning knobs for tools and
+// experiments, read once when a context is created (hf_set_tuning / hf_set_driver /
+// hf_set_resident override them per context; see heatfem.h).
+static void tuning_from_env(hf_ctx *c)
+{
+    if (const char *e = getenv("HF_TILE_R")) c->tile_r_set = atoi(e) >= 4 ? 4 : 2;
+    if (const char *e = getenv("HF_ZCHUNK")) c->zchunk = std::max(0, atoi(e));
+    if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e) != 0;
+    if (const char *e = getenv("HF_UNROLL")) c->unroll = std::min(50, std::max(1, atoi(e)));
+    if (const char *e = getenv("HF_PDL")) c->pdl = atoi(e) != 0;
+    if (const char *e = getenv("HF_FUSE_AB")) c->fuse_ab = atoi(e) != 0;
+    if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
+    if (const char *e = getenv("HF_TM_FENCE")) c->tm_fence = atoi(e) != 0;
+    if (const char *e = getenv("HF_RESIDENT")) c->resident = atoi(e) != 0;
+    if (const char *e = getenv("HF_BATCH_GROUP")) c->batch_group = std::max(0, atoi(e));
+    if (const char *e = getenv("HF_COMM_TIMEOUT_S")) c->comm_timeout_s = atof(e);
+}
+
 static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream, int rank, int nranks, int nsys = 1)
 {
     for (int d = 0; d < 3; d++)
@@ -1153,17 +1174,8 @@ static hf_status ctx_init(hf_ctx *c, const hf_grid *g, int device, void *stream,
         c->dg.Kd[l] = (hy * hz / hx + hx * hz / hy + hx * hy / hz) / 9.0;
         c->dg.Md[l] = hx * hy * hz / 27.0;
     }
-    c->tileR = default_tile_r(c, EL_Q1);
-    if (const char *e = getenv("HF_TILE_R")) c->tileR = atoi(e) >= 4 ? 4 : 2;
-    if (const char *e = getenv("HF_ZCHUNK")) c->zchunk_env = std::max(0, atoi(e));
-    if (const char *e = getenv("HF_DRIVER")) c->driver = atoi(e);
-    if (const char *e = getenv("HF_UNROLL")) c->unroll = std::min(50, std::max(1, atoi(e)));
-    if (const char *e = getenv("HF_PDL")) c->pdl = atoi(e) != 0;
-    if (const char *e = getenv("HF_FUSE_AB")) c->fuse_ab = atoi(e) != 0;
-    if (const char *e = getenv("HF_CG1")) c->cg1 = atoi(e) != 0;
-    if (const char *e = getenv("HF_CHECK_EVERY")) c->check_every = std::max(1, atoi(e));
-    if (const char *e = getenv("HF_TM_FENCE")) c->tm_fence = atoi(e) != 0;
-    if (const char *e = getenv("HF_RESIDENT")) c->resident = atoi(e) != 0;
+    tuning_from_env(c);
+    c->tileR = c->tile_r_set ? c->tile_r_set : default_tile_r(c, EL_Q1);
     // resident CTAs per SM of the CG stencil decide the z split of the grid
     StencilFn f = stencil_fn(c->tileR, LD_CGD, EP_CGA, 0, c->elem, c->es);
     HFCK(ensure_smem_attr(f.fn, f.smem, device));
@@ -1449,8 +1461,7 @@ static hf_status host_cg_iter(hf_ctx *c, Sys &s, CgLaunches &L, int i, int repla
 static hf_status wait_event(hf_ctx *c, cudaEvent_t ev)
 {
     if (!c->comm) { CUCK(cudaEventSynchronize(ev)); return HF_OK; }
-    const char *e = getenv("HF_COMM_TIMEOUT_S");
-    const double limit = e ? atof(e) : 120.0;
+    const double limit = c->comm_timeout_s;
     const auto t0 = std::chrono::steady_clock::now();
     for (;;) {
         cudaError_t q = cudaEventQuery(ev);
@@ -2690,6 +2701,10 @@ static hf_status stack_ctx(hf_ctx *c, int G, hf_ctx **out)
     for (int f = 0; f < 6; f++) s->gval[f] = c->gval[f];
     s->driver = c->driver;
     s->unroll = c->unroll;
+    s->zchunk = c->zchunk;
+    s->pdl = c->pdl;
+    s->check_every = c->check_every;
+    s->tm_fence = c->tm_fence;
     c->stacks[G] = s;
     *out = s;
     return HF_OK;
@@ -2712,7 +2727,7 @@ static hf_status simulate_common(hf_ctx *c, double theta, double dt, int32_t nst
 // groups of 10: 193, 5: 189, 4: 176, 7: 161, 20: 152; B = 8: 5 + 3: 196, one stack of 8: 185.
 static int stack_group(const hf_ctx *c, int B)
 {
-    if (const char *e = getenv("HF_BATCH_GROUP")) return std::max(1, std::min(atoi(e), B));
+    if (c->batch_group > 0) return std::min(c->batch_group, B);
     const long long nn = (long long)c->pitch * c->ny1 * c->nz1g;     // nodes per system (padded)
     const int planes = c->nz1g;
     // stacks stay below the R = 4 tile threshold (default_tile_r): measured at C5, stacks of 16-20
@@ -3288,7 +3303,7 @@ hf_status hf_set_element(hf_ctx *c, int32_t type)
     const double *h = c->g.h;
     // the dense (tet) element keeps R = 2 tiles (R = 4 spills); TMA boxes follow the tile height
     int want_r = default_tile_r(c, type);
-    if (type != EL_DENSE && getenv("HF_TILE_R")) want_r = atoi(getenv("HF_TILE_R")) >= 4 ? 4 : 2;
+    if (type != EL_DENSE && c->tile_r_set) want_r = c->tile_r_set;
     CUCK(cudaStreamSynchronize(c->stream));
     if (want_r != c->tileR) c->tileR = want_r;
     HFCK(sys_maps(c, c->sys0));              // also selects the material-id map (Q1 only)
@@ -3332,6 +3347,48 @@ hf_status hf_set_precision(hf_ctx *c, int32_t bits)
     CUCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f.fn, 32 * f.nw, f.smem));
     c->occ = std::max(1, occ);
     HFCK(sys_alloc(c, c->sys0, c->stream));
+    return HF_OK;
+}
+
+hf_status hf_set_tuning(hf_ctx *c, const char *key, int64_t value)
+{
+    if (!c || !key) return fail(HF_E_ARG, "hf_set_tuning: NULL argument");
+    const std::string k(key);
+    const long long v = value;
+    if (k == "tile_r") {
+        if (v != 0 && v != 2 && v != 4) return fail(HF_E_ARG, "hf_set_tuning: tile_r must be 0 (default), 2 or 4");
+        c->tile_r_set = (int)v;
+        if (c->lo) c->lo->tile_r_set = (int)v;  // the mixed-precision shadow follows
+        return hf_set_element(c, c->elem);      // re-derives the tile height, TMA maps, grid occupancy
+    }
+    if (k == "zchunk") { if (v < 0) return fail(HF_E_ARG, "hf_set_tuning: zchunk >= 0"); c->zchunk = (int)v; }
+    else if (k == "unroll") { if (v < 0 || v > 50) return fail(HF_E_ARG, "hf_set_tuning: unroll in 0..50"); c->unroll = (int)v; }
+    else if (k == "pdl") { if (v < 0 || v > 1) return fail(HF_E_ARG, "hf_set_tuning: pdl 0 or 1"); c->pdl = (int)v; }
+    else if (k == "fuse_ab") { if (v < 0 || v > 1) return fail(HF_E_ARG, "hf_set_tuning: fuse_ab 0 or 1"); c->fuse_ab = (int)v; }
+    else if (k == "check_every") { if (v < 1) return fail(HF_E_ARG, "hf_set_tuning: check_every >= 1"); c->check_every = (int)v; }
+    else if (k == "tm_fence") { if (v < 0 || v > 1) return fail(HF_E_ARG, "hf_set_tuning: tm_fence 0 or 1"); c->tm_fence = (int)v; }
+    else if (k == "batch_group") { if (v < 0) return fail(HF_E_ARG, "hf_set_tuning: batch_group >= 0"); c->batch_group = (int)v; }
+    else if (k == "comm_timeout_s") { if (v < 1) return fail(HF_E_ARG, "hf_set_tuning: comm_timeout_s >= 1"); c->comm_timeout_s = (double)v; }
+    else return fail(HF_E_ARG, "hf_set_tuning: unknown key '" + k + "'");
+    c->sys0.key_valid = false;                   // graphs are rebuilt with the new setting
+    drop_stacks(c);
+    return HF_OK;
+}
+
+hf_status hf_get_tuning(const hf_ctx *c, const char *key, int64_t *value)
+{
+    if (!c || !key || !value) return fail(HF_E_ARG, "hf_get_tuning: NULL argument");
+    const std::string k(key);
+    if (k == "tile_r") *value = c->tileR;
+    else if (k == "zchunk") *value = c->zchunk;
+    else if (k == "unroll") *value = c->unroll;
+    else if (k == "pdl") *value = c->pdl;
+    else if (k == "fuse_ab") *value = c->fuse_ab;
+    else if (k == "check_every") *value = c->check_every;
+    else if (k == "tm_fence") *value = c->tm_fence;
+    else if (k == "batch_group") *value = c->batch_group;
+    else if (k == "comm_timeout_s") *value = (int64_t)c->comm_timeout_s;
+    else return fail(HF_E_ARG, "hf_get_tuning: unknown key '" + k + "'");
     return HF_OK;
 }
 

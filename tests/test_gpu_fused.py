@@ -1,8 +1,7 @@
-"""The fused PCG iteration (HF_FUSE_AB=1: kernel A, a grid barrier and kernel B's work in one
+"""The fused PCG iteration (hf_set_tuning(ctx, "fuse_ab", 1): kernel A, a grid barrier and kernel B's work in one
 launch inside the graph loop body) against the oracle: the same bars as the two-kernel path
 (rel-L2 <= 1e-10 at rtol 1e-12).  The grouping of kernel B's partial sums differs, so iteration
 counts may differ by rounding, not results."""
-import os
 
 import numpy as np
 import pytest
@@ -35,11 +34,8 @@ def rel(a, b):
 
 
 def fused_ctx(g, prec=64):
-    os.environ["HF_FUSE_AB"] = "1"
-    try:
-        ctx = hf.hf_create(g, 0)
-    finally:
-        os.environ.pop("HF_FUSE_AB", None)
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_tuning(ctx, "fuse_ab", 1)
     if prec != 64:
         hf.hf_set_precision(ctx, prec)
     return ctx

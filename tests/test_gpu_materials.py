@@ -2,7 +2,6 @@
 P:345-357) streamed as one uint8 id per element (stencil variant EL_Q1P).  The operator must be
 bit-identical to the per-element pair path (hf_set_coefficients with k_e = k_mat[id_e]) and
 match the oracle with the apply / solution bars."""
-import os
 import threading
 
 import numpy as np
@@ -60,12 +59,10 @@ def materials(n, seed):
 
 
 def ctx_pair(g, ids, km, cm, tile_r=None):
+    a, b = hf.hf_create(g, 0), hf.hf_create(g, 0)
     if tile_r is not None:
-        os.environ["HF_TILE_R"] = str(tile_r)
-    try:
-        a, b = hf.hf_create(g, 0), hf.hf_create(g, 0)
-    finally:
-        os.environ.pop("HF_TILE_R", None)
+        hf.hf_set_tuning(a, "tile_r", tile_r)
+        hf.hf_set_tuning(b, "tile_r", tile_r)
     hf.hf_set_material_ids(a, ids, km, cm)
     hf.hf_set_coefficients(b, T(km[ids]), T(cm[ids]))
     return a, b

@@ -4,7 +4,6 @@ Bars: operator apply / diagonal / load max-abs error <= 1e-
 output scale (rounding-order differences only); PCG and time-step solutions rel-L2 <= 1e-10
 (BASELINE.json north_star) at rtol 1e-12.
 """
-import os
 import threading
 
 import numpy as np
@@ -48,13 +47,12 @@ def maxerr(a, b):
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
 
 
-def make_ctx(grid, k, c, tile_r=None):
+def make_ctx(grid, k, c, tile_r=None, **tuning):
+    ctx = hf.hf_create(grid, 0)
     if tile_r is not None:
-        os.environ["HF_TILE_R"] = str(tile_r)
-    try:
-        ctx = hf.hf_create(grid, 0)
-    finally:
-        os.environ.pop("HF_TILE_R", None)
+        hf.hf_set_tuning(ctx, "tile_r", tile_r)
+    for key, v in tuning.items():
+        hf.hf_set_tuning(ctx, key, v)
     hf.hf_set_coefficients(ctx, T(k), T(c))
     return ctx
 
@@ -72,7 +70,7 @@ GRIDS = {
 # ---------------------------------------------------------------------------------------------
 # operator apply (Eq. (1))
 
-@pytest.mark.parametrize("tile_r", [1, 2, 4])
+@pytest.mark.parametrize("tile_r", [0, 2, 4])
 @pytest.mark.parametrize("gname", list(GRIDS))
 def test_apply_matches_assembled(gname, tile_r):
     g = GRIDS[gname]
@@ -209,8 +207,8 @@ def test_cg_dirichlet_zero_rhs_and_breakdown():
 # ---------------------------------------------------------------------------------------------
 # time stepping
 
-def _gpu_sim(p, driver=0, snap_plane=-1, tile_r=None):
-    ctx = make_ctx(p.grid, p.k, p.c, tile_r)
+def _gpu_sim(p, driver=0, snap_plane=-1, tile_r=None, **tuning):
+    ctx = make_ctx(p.grid, p.k, p.c, tile_r, **tuning)
     hf.hf_set_driver(ctx, driver)
     if p.dirichlet_bits:
         hf.hf_set_dirichlet_faces(ctx, p.dirichlet_bits, p.dirichlet_values)
@@ -224,7 +222,7 @@ def _gpu_sim(p, driver=0, snap_plane=-1, tile_r=None):
     return N(u), st, (None if snap is None else N(snap)), ctx
 
 
-@pytest.mark.parametrize("tile_r", [1, 2, 4])
+@pytest.mark.parametrize("tile_r", [0, 2, 4])
 def test_simulate_c1(tile_r):
     p = synth.c1()
     ug, st, _, _ = _gpu_sim(p, tile_r=tile_r)
@@ -249,11 +247,7 @@ def test_failed_step_stops_the_run(driver, unroll):
     same call are skipped on the device (no host check between graph launches), the call returns
     NOCONV with the failing step, and the graph WHILE loops of the skipped steps terminate."""
     p = synth.c1()
-    os.environ["HF_UNROLL"] = str(unroll)
-    try:
-        ctx = make_ctx(p.grid, p.k, p.c)
-    finally:
-        os.environ.pop("HF_UNROLL", None)
+    ctx = make_ctx(p.grid, p.k, p.c, unroll=unroll)
     hf.hf_set_driver(ctx, driver)
     F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
     hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
@@ -287,11 +281,7 @@ def test_time_kernel_a_replay_then_simulate():
 def test_unrolled_loop_body_bitwise_equal(unroll):
     p = synth.c1()
     ug, st0, _, _ = _gpu_sim(p, driver=0)
-    os.environ["HF_UNROLL"] = str(unroll)
-    try:
-        uu, st1, _, _ = _gpu_sim(p, driver=0)
-    finally:
-        os.environ.pop("HF_UNROLL", None)
+    uu, st1, _, _ = _gpu_sim(p, driver=0, unroll=unroll)
     assert np.array_equal(ug, uu) and st0["total_iters"] == st1["total_iters"]
 
 
@@ -339,11 +329,9 @@ def test_resume_equals_one_run():
 
 
 @pytest.mark.parametrize("group", [None, 2, 1])
-def test_batched_matches_individual(group, monkeypatch):
+def test_batched_matches_individual(group):
     """Batched sims: systems stacked along z with per-system PCG (default group; groups of 2, the
     last group smaller; one system per group) against the oracle."""
-    if group:
-        monkeypatch.setenv("HF_BATCH_GROUP", str(group))
     g = synth.Grid((12, 10, 9), (0.3, 0.3, 0.2))
     B = 3
     base_k, base_c = synth.random_fields(g, seed=14)
@@ -351,7 +339,7 @@ def test_batched_matches_individual(group, monkeypatch):
     cs = np.stack([base_c * (1.0 + 0.1 * j) for j in range(B)])
     u0 = np.zeros((B, g.n_nodes))
     for shared_c in (False, True):
-        ctx = make_ctx(g, base_k, base_c)
+        ctx = make_ctx(g, base_k, base_c, batch_group=group or 0)
         F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
         hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
         ub = T(u0.ravel())
@@ -687,17 +675,12 @@ def test_tet_simulate_matches_oracle(driver):
 
 
 def test_pdl_edges_do_not_change_results():
-    """The programmatic-launch edges of the PCG loop body (HF_PDL, default on) only let the next
-    kernel start early: the solution is bit-identical to fully serialised edges."""
+    """The programmatic-launch edges of the PCG loop body (tuning "pdl", default on) only let the
+    next kernel start early: the solution is bit-identical to fully serialised edges."""
     p = synth.c1()
     outs = []
-    for pdl in ("0", "1"):
-        os.environ["HF_PDL"] = pdl
-        try:
-            ctx = hf.hf_create(p.grid, 0)
-        finally:
-            os.environ.pop("HF_PDL", None)
-        hf.hf_set_coefficients(ctx, T(p.k), T(p.c))
+    for pdl in (0, 1):
+        ctx = make_ctx(p.grid, p.k, p.c, pdl=pdl)
         F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
         hf.hf_face_load(ctx, p.flux_face, p.flux_const, None, F)
         u = T(p.u0)
@@ -814,3 +797,29 @@ def test_slab_local_transport_tets_and_mixed_tets():
     assert rel(full, uo) <= 1e-10
     del ctxs
     hf.hf_local_group_destroy(grp)
+
+
+def test_tuning_api_and_environment_defaults(monkeypatch):
+    """hf_set_tuning / hf_get_tuning: values, range checks, unknown keys; HF_* environment
+    variables only give the defaults of a context at its creation."""
+    p = synth.c1()
+    monkeypatch.setenv("HF_UNROLL", "3")
+    monkeypatch.setenv("HF_ZCHUNK", "4")
+    ctx = make_ctx(p.grid, p.k, p.c)
+    monkeypatch.delenv("HF_UNROLL")
+    monkeypatch.delenv("HF_ZCHUNK")
+    assert hf.hf_get_tuning(ctx, "unroll") == 3 and hf.hf_get_tuning(ctx, "zchunk") == 4
+    assert hf.hf_get_tuning(ctx, "tile_r") == 2                   # default below 16M nodes
+    hf.hf_set_tuning(ctx, "tile_r", 4)
+    assert hf.hf_get_tuning(ctx, "tile_r") == 4
+    for key, bad in (("tile_r", 3), ("unroll", 51), ("pdl", 2), ("check_every", 0), ("nope", 1)):
+        with pytest.raises(hf.HfError):
+            hf.hf_set_tuning(ctx, key, bad)
+    # the tuned context (R = 4 tiles, 4-plane chunks, 3 iterations per body) still matches
+    F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
+    u = T(p.u0)
+    hf.hf_simulate(ctx, p.theta, p.dt, p.nsteps, F, u, rtol=p.rtol)
+    o, Fo = oracle.problem_oracle(p)
+    uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
+    assert rel(N(u), uo) <= 1e-10

@@ -18,6 +18,8 @@ if mode == "sim":
     ctx = hf.hf_create(p.grid, 0)
     if os.environ.get("HF_PREC"):
         hf.hf_set_precision(ctx, int(os.environ["HF_PREC"]))
+    if os.environ.get("CG_VARIANT"):    # single-reduction PCG (hf_set_cg_variant)
+        hf.hf_set_cg_variant(ctx, int(os.environ["CG_VARIANT"]))
     if os.environ.get("HF_IDS"):        # materials by id (stencil variant EL_Q1P)
         hf.hf_set_material_ids(ctx, torch.tensor(p.extra["ids"], device=dev),
                                [m[1] for m in p.extra["materials"]], [m[0] for m in p.extra["materials"]])
