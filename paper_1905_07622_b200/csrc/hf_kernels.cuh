@@ -200,7 +200,10 @@ struct PeerSync {                     // device copy per slab context
 struct Sync {               // per-system reduction plumbing
     CgState *st;
     const double *pin;      // partial sums of the previous kernel (NPART per block)
-    int pin_n;              // their count; -1: taken from the state (npart_a / npart_b)
+    int pin_n;              // their count; -1: taken from the state (npart_a / npart_b); > 0: fixed
+                            // (every producer of pin writes exactly pin_n entries, see pout_pad)
+    int pout_pad;           // > nblocks: block 0 zero-fills partial entries [nblocks, pout_pad) so
+                            // that a consumer can always sum pout_pad entries (adding 0 is exact)
     double *pout;           // this kernel's partial sums (NPART per block)
     unsigned long long *launches;
     cudaGraphConditionalHandle h_while, h_if;
@@ -440,8 +443,43 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NPART], double 
 // Grid-wide sums of the PREVIOUS kernel's per-block partials, computed redundantly by every
 // block in one fixed order (deterministic, no atomics, no fences: the kernel boundary orders
 // the producer's writes before these reads).  All threads return the same sums.
+// The first round of the partial-sum loads (KU blocks per thread, all issued before any add):
+// a kernel whose partial count is fixed (Sync::pin_n > 0) issues them right after
+// griddepcontrol.wait, in parallel with its state header (prev_finish adds them later).
+#ifndef HF_RP_KU
+#define HF_RP_KU 4
+#endif
+struct PrevPre {
+    double2 v[HF_RP_KU][2];
+};
+
 template <int NT, bool CG = false>
-__device__ __forceinline__ void reduce_prev(const double *part, int n, double (&sums)[NPART])
+__device__ __forceinline__ void prev_load(const double *part, int n, int b0, PrevPre &pre)
+{
+    constexpr int KU = HF_RP_KU;
+    static_assert(NPART == 4, "partials are read as 2 x double2");
+#pragma unroll
+    for (int k = 0; k < KU; k++) {
+        const int b = b0 + k * NT;
+        if (b < n) {
+            const double2 *q = reinterpret_cast<const double2 *>(part + (long long)b * NPART);
+            // CG: partials written by other CTAs of the SAME kernel (fused A+B, after the grid
+            // barrier): through L2, never the non-coherent read-only path
+            pre.v[k][0] = CG ? __ldcg(q) : __ldg(q);
+            pre.v[k][1] = CG ? __ldcg(q + 1) : __ldg(q + 1);
+        } else {
+            pre.v[k][0] = make_double2(0.0, 0.0);
+            pre.v[k][1] = make_double2(0.0, 0.0);
+        }
+    }
+}
+
+// Grid-wide sums of the PREVIOUS kernel's per-block partials, computed redundantly by every
+// block in one fixed order (deterministic, no atomics, no fences: the kernel boundary orders
+// the producer's writes before these reads).  All threads return the same sums.  pre: the first
+// round's loads (prev_load at b0 = tid).
+template <int NT, bool CG = false>
+__device__ __forceinline__ void prev_finish(const PrevPre &pre0, const double *part, int n, double (&sums)[NPART])
 {
     __shared__ double redp[NT / 32][NPART];
     const int tid = threadIdx.x + threadIdx.y * blockDim.x;
@@ -452,34 +490,17 @@ __device__ __forceinline__ void reduce_prev(const double *part, int n, double (&
     // trip for n <= KU * NT); the per-thread order stays b = tid, tid + NT, ... (fixed).  Every
     // block of the grid reads the same partials: through the read-only (L1) path, not L2-only
     // (-0.6 us per C3 iteration); they are written by the previous kernel only.
-#ifndef HF_RP_KU
-#define HF_RP_KU 4
-#endif
     constexpr int KU = HF_RP_KU;
-    static_assert(NPART == 4, "partials are read as 2 x double2");
+    PrevPre pre = pre0;
     for (int b0 = tid; b0 < n; b0 += KU * NT) {
-        double2 v[KU][2];
-#pragma unroll
-        for (int k = 0; k < KU; k++) {
-            const int b = b0 + k * NT;
-            if (b < n) {
-                const double2 *q = reinterpret_cast<const double2 *>(part + (long long)b * NPART);
-                // CG: partials written by other CTAs of the SAME kernel (fused A+B, after the
-                // grid barrier): through L2, never the non-coherent read-only path
-                v[k][0] = CG ? __ldcg(q) : __ldg(q);
-                v[k][1] = CG ? __ldcg(q + 1) : __ldg(q + 1);
-            } else {
-                v[k][0] = make_double2(0.0, 0.0);
-                v[k][1] = make_double2(0.0, 0.0);
-            }
-        }
+        if (b0 != tid) prev_load<NT, CG>(part, n, b0, pre);
 #pragma unroll
         for (int k = 0; k < KU; k++) {
             if (b0 + k * NT < n) {
-                acc[0] += v[k][0].x;
-                acc[1] += v[k][0].y;
-                acc[2] += v[k][1].x;
-                acc[3] += v[k][1].y;
+                acc[0] += pre.v[k][0].x;
+                acc[1] += pre.v[k][0].y;
+                acc[2] += pre.v[k][1].x;
+                acc[3] += pre.v[k][1].y;
             }
         }
     }
@@ -508,6 +529,22 @@ __device__ __forceinline__ void reduce_prev(const double *part, int n, double (&
             sums[j] = v;
         }
     }
+}
+
+template <int NT, bool CG = false>
+__device__ __forceinline__ void reduce_prev(const double *part, int n, double (&sums)[NPART])
+{
+    PrevPre pre;
+    prev_load<NT, CG>(part, n, threadIdx.x + threadIdx.y * blockDim.x, pre);
+    prev_finish<NT, CG>(pre, part, n, sums);
+}
+
+// zero-fill of the partial entries [nblk, sy.pout_pad) by block 0 (fixed consumer counts)
+template <int NT>
+__device__ __forceinline__ void pad_partials(const Sync &sy, int nblk, int blk, int tid)
+{
+    if (blk != 0 || sy.pout_pad <= nblk) return;
+    for (int i = nblk * NPART + tid; i < sy.pout_pad * NPART; i += NT) sy.pout[i] = 0.0;
 }
 
 // sums of system sj's partials (the previous kernel's blocks of system sj are contiguous)
@@ -891,7 +928,10 @@ __device__ __forceinline__ void cg_b_work(const BArgs &a, CgState *sst, bool one
         }
     }
     pdl_trigger();
-    if (!replace) block_reduce_store<NT>(acc, a.sy.pout, pblk);
+    if (!replace) {
+        block_reduce_store<NT>(acc, a.sy.pout, pblk);
+        pad_partials<NT>(a.sy, nblk, pblk, tid);
+    }
     if (PEER && !replace) peer_publish<NT>(a.sy.peer, a.sy.pout, nblk, remote);
     if (blk == 0 && tid == 0) {
         sst->alpha = alpha;
@@ -915,6 +955,11 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     const int sj = (int)blockIdx.x / bps, blk = (int)blockIdx.x - sj * bps;
     if (blockIdx.x == 0 && tid == 0 && a.sy.launches) atomicAdd(a.sy.launches, 1ull);
     pdl_wait();
+    // a fixed partial count (one system, no peer transport): kernel A's partials are requested
+    // before the state header
+    const bool pre_ok = !PEER && nsys == 1 && a.sy.pin_n > 0;
+    PrevPre pre;
+    if (pre_ok) prev_load<NT>(a.sy.pin, a.sy.pin_n, tid, pre);
     CgState *st0 = a.sy.st, *sst = st0 + sj;
     const CgHdr hd = load_hdr(st0);
     const CgHdr hs = sj ? load_hdr(sst) : hd;
@@ -940,7 +985,12 @@ __global__ void __launch_bounds__(NT) k_cg_b(const BArgs a)
     // alpha_i = delta_i / (d_i^T q_i)  (Alg. 1 line 8) from kernel A's partials of this system
     double ps[NPART];
     if (PEER) peer_sums<NT>(a.sy.peer, ps);
-    else prev_sums<NT>(a.sy, hd.h2.x, ps, sj);
+    else {
+        const int n = pre_ok ? a.sy.pin_n : (a.sy.pin_n >= 0 ? a.sy.pin_n : hd.h2.x);
+        const double *pin = a.sy.pin + (long long)sj * n * NPART;
+        if (!pre_ok) prev_load<NT>(pin, n, tid, pre);
+        prev_finish<NT>(pre, pin, n, ps);
+    }
     cg_b_work<NT, Real, false, PEER>(a, sst, nsys == 1, (long long)sj * a.sysn, blk, bps, (int)blockIdx.x, tid, it, re,
                                step, sst->delta[it & 1], ps[0], false);
 }
@@ -1047,6 +1097,11 @@ k_stencil(const __grid_constant__ StencilArgs a)
         }
         pdl_wait();
     }
+    // kernel A with a fixed partial count (one system, no peer transport): the previous kernel's
+    // partials are requested before the state header
+    const bool pre_ok = EP == EP_CGA && !PEER && nsys == 1 && a.sy.pin_n > 0;
+    PrevPre pre;
+    if (pre_ok) prev_load<NT>(a.sy.pin, a.sy.pin_n, tid, pre);
 
     // ---- state checks and per-launch resolution of buffers ---------------------------------
     double beta = 0.0, delta_i = 0.0;
@@ -1232,7 +1287,12 @@ k_stencil(const __grid_constant__ StencilArgs a)
         double ps[NPART];
         if (peer_early) for (int j = 0; j < NPART; j++) ps[j] = ps_peer[j];
         else if (pp) peer_sums<NT>(pp, ps);
-        else prev_sums<NT>(a.sy, npart_b, ps, sj);
+        else {
+            const int n = pre_ok ? a.sy.pin_n : (a.sy.pin_n >= 0 ? a.sy.pin_n : npart_b);
+            const double *pin = a.sy.pin + (long long)sj * n * NPART;
+            if (!pre_ok) prev_load<NT>(pin, n, tid, pre);
+            prev_finish<NT>(pre, pin, n, ps);
+        }
         const IterStart is = iter_start(sst, it_i, ps, max_iter);
         if (!is.go) {
             if (sys_lead) {
@@ -1679,6 +1739,7 @@ k_stencil(const __grid_constant__ StencilArgs a)
     HF_TR(5);
     // per-block partial sums for the next kernel: A -> (d^T q); init, RESID -> (r^T s, r^T r, b^T b)
     block_reduce_store<NT>(acc, a.sy.pout, blk);
+    if (nsys == 1) pad_partials<NT>(a.sy, nblocks, blk, tid);
     if (pp) peer_publish<NT>(pp, a.sy.pout, nblocks, remote);
     HF_TR(6);
     if (EP == EP_RESID_INIT && sys_lead) {      // a new solve of this system starts: A_0 follows

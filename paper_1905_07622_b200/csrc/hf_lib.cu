@@ -825,6 +825,21 @@ static void stencil_grid(const hf_ctx *c, int z0, int z1, dim3 *grid, int *zchun
 // which = 0: consumes kernel A's partials, 1: consumes init/B/RESID partials, -1: none.
 // pout = 0: writes A partials, 1: writes init/B/RESID partials, -1: none.  In slab mode the
 // consumer reads the allreduced sums instead (count 1).
+static int b_blocks(const hf_ctx *c);
+
+// CTAs of this context's stencil launches over its owned planes (every stencil launch of a
+// context has this grid)
+static int stencil_blocks(const hf_ctx *c)
+{
+    dim3 grid;
+    int chunk, zper;
+    stencil_grid(c, c->own_lo, c->own_hi, &grid, &chunk, &zper);
+    return (int)(grid.x * grid.y * grid.z);
+}
+
+// Fixed partial counts (one system, no slab transport): every producer of the init / B / RESID
+// buffer writes max(B blocks, stencil blocks) entries (zero-padded), the A buffer holds the
+// stencil grid's, so consumers know the count before they read the state header.
 static Sync make_sync(hf_ctx *c, Sys &s, int consumes = -1, int produces = -1)
 {
     Sync y;
@@ -832,11 +847,17 @@ static Sync make_sync(hf_ctx *c, Sys &s, int consumes = -1, int produces = -1)
     y.st = s.st;
     y.launches = c->launches;
     y.nsys = c->nsys;
+    const bool fixed = c->nsys == 1 && !c->comm;
+    const int nb_st = fixed ? stencil_blocks(c) : 0;
+    const int nb_b = fixed ? std::max(b_blocks(c), nb_st) : 0;
     if (consumes >= 0) {
         if (c->comm && !c->comm->in_kernel()) { y.pin = s.sums; y.pin_n = 1; }
-        else { y.pin = consumes == 0 ? s.partA : s.partB; y.pin_n = -1; }
+        else { y.pin = consumes == 0 ? s.partA : s.partB; y.pin_n = fixed ? (consumes == 0 ? nb_st : nb_b) : -1; }
     }
-    if (produces >= 0) y.pout = produces == 0 ? s.partA : s.partB;
+    if (produces >= 0) {
+        y.pout = produces == 0 ? s.partA : s.partB;
+        if (fixed && produces == 1) y.pout_pad = nb_b;
+    }
     y.peer = c->comm ? c->comm->peer_dev() : nullptr;
     return y;
 }
