@@ -237,6 +237,7 @@ hf_status hf_simulate_resume(hf_ctx *ctx, double theta, double dt, int32_t nstep
  * coefficient-free element layer between them, each kernel block works inside one system and
  * a converged system stops while the others iterate on.  Dirichlet faces apply per system.
  * Systems are grouped into stacks by a model of the GPU's CTA slots.
+ * With hf_set_mixed on, each step's solves run as fp32 correction + fp64 finish per stack.
  * B = 0 is a no-op (the arrays may then be NULL).
  * Returns the first failing status (the other systems run on and are returned). */
 hf_status hf_simulate_batched(hf_ctx *ctx, int32_t B, const double *k_batch,
@@ -331,7 +332,9 @@ hf_status hf_set_driver(hf_ctx *ctx, int32_t driver);
  * operator decides convergence (defect correction), so results have the fp64 path's accuracy
  * (reading R18); the fp32 stage carries most of the error reduction at half the bytes.  Call
  * before the coefficients; enable = 0 removes the shadow.  Graph driver only (the host-loop
- * driver runs plain fp64).  Errors: HF_E_ARG, HF_E_STATE (fp32 / slab / stacked context, or
+ * driver runs plain fp64).  hf_simulate_batched on a mixed context runs every stack the same
+ * way (each stack gets its own fp32 shadow with per-system fp32 PCG; a system that failed in an
+ * earlier step gets no correction).  Errors: HF_E_ARG, HF_E_STATE (fp32 / slab context, or
  * coefficients already set), HF_E_CUDA. */
 hf_status hf_set_mixed(hf_ctx *ctx, int32_t enable, double rtol_lo);
 

@@ -2193,7 +2193,15 @@ struct MixArgs {
     const CgState *stlo;             // lo state (iterations of the fp32 solve)
     unsigned long long *lo_iters;    // accumulated fp32 iterations
     unsigned long long *launches;
+    int nsys, sys_planes;            // stacked systems (batched sims): planes per system
 };
+
+// a system of a stack that failed in an earlier step keeps its result: no correction
+__device__ __forceinline__ bool mix_failed(const MixArgs &a, int z)
+{
+    const int sj = a.nsys > 1 ? z / a.sys_planes : 0;
+    return a.st[sj].first_failed >= 0;
+}
 
 __global__ void k_mix_in(const MixArgs a)
 {
@@ -2203,7 +2211,7 @@ __global__ void k_mix_in(const MixArgs a)
     if (i >= n) return;
     const int x = (int)(i % a.nx1), y = (int)((i / a.nx1) % a.ny1), z = (int)(i / ((long long)a.nx1 * a.ny1));
     const long long h = z * a.plane_hi + (long long)y * a.pitch_hi + x, l = z * a.plane_lo + (long long)y * a.pitch_lo + x;
-    a.blo[l] = (float)a.rhi[h];
+    a.blo[l] = mix_failed(a, z) ? 0.0f : (float)a.rhi[h];
     a.xlo[l] = 0.0f;
 }
 
@@ -2218,6 +2226,7 @@ __global__ void k_mix_out(const MixArgs a)
     if (i >= n) return;
     const int x = (int)(i % a.nx1), y = (int)((i / a.nx1) % a.ny1), z = (int)(i / ((long long)a.nx1 * a.ny1));
     const long long h = z * a.plane_hi + (long long)y * a.pitch_hi + x, l = z * a.plane_lo + (long long)y * a.pitch_lo + x;
+    if (mix_failed(a, z)) return;
     double *xv = a.ring[(a.st->step + 1) % 3];
     xv[h] += (double)a.xlo[l];
 }

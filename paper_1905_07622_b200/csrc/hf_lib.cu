@@ -2482,6 +2482,8 @@ static hf_status simulate_sys(hf_ctx *c, Sys &s, double theta, double dt, int ns
             ma.stlo = ls.st;
             ma.lo_iters = c->mix_iters;
             ma.launches = c->launches;
+            ma.nsys = c->nsys;
+            ma.sys_planes = c->sys_planes;
             const long long nn = (long long)c->nx1 * c->ny1 * c->nzl;
             Launch Min, Mout;
             Min.fn = (const void *)k_mix_in;
@@ -2726,6 +2728,10 @@ static hf_status stack_ctx(hf_ctx *c, int G, hf_ctx **out)
     s->pdl = c->pdl;
     s->check_every = c->check_every;
     s->tm_fence = c->tm_fence;
+    if (c->lo) {                            // mixed precision: the stack gets its own fp32 shadow
+        const hf_status sm = hf_set_mixed(s, 1, c->mix_rtol);
+        if (sm != HF_OK) { ctx_free(s); delete s; return sm; }
+    }
     c->stacks[G] = s;
     *out = s;
     return HF_OK;
@@ -3483,18 +3489,20 @@ hf_status hf_set_mixed(hf_ctx *c, int32_t enable, double rtol_lo)
     CUCK(cudaStreamSynchronize(c->stream));
     c->sys0.key_valid = false;
     if (!enable) {
+        drop_stacks(c);
         if (c->mix_exec) { cudaGraphExecDestroy(c->mix_exec); c->mix_exec = nullptr; }
         if (c->mix_graph) { cudaGraphDestroy(c->mix_graph); c->mix_graph = nullptr; }
         if (c->lo) { ctx_free(c->lo); delete c->lo; c->lo = nullptr; }
         return HF_OK;
     }
-    if (c->prec != 64 || c->nsys != 1 || c->comm)
-        return fail(HF_E_STATE, "hf_set_mixed: needs a single-GPU fp64 context with one system");
+    if (c->prec != 64 || c->comm)
+        return fail(HF_E_STATE, "hf_set_mixed: needs a single-GPU fp64 context");
     if (c->coef_set) return fail(HF_E_STATE, "hf_set_mixed: call before the coefficients are set");
     c->mix_rtol = rtol_lo;
+    drop_stacks(c);                         // batched stacks are rebuilt with (or without) the shadow
     if (!c->lo) {
         hf_ctx *lo = new hf_ctx();
-        hf_status st = ctx_init(lo, &c->g, c->device, c->stream, 0, 1);
+        hf_status st = ctx_init(lo, &c->g, c->device, c->stream, 0, 1, c->nsys);   // same system stack
         if (st == HF_OK) st = hf_set_precision(lo, 32);
         if (st == HF_OK && c->dbits) st = hf_set_dirichlet_faces(lo, c->dbits, c->gval);
         if (st == HF_OK && c->elem != EL_Q1) st = hf_set_element(lo, c->elem);

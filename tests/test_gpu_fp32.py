@@ -312,3 +312,34 @@ def test_mixed_nonzero_dirichlet_beam_and_resume():
     uo, _, _, _ = o.simulate(p.theta, p.dt, p.nsteps, Fo, p.u0, tol=p.rtol)
     assert rel(N(u), uo) <= 1e-10, rel(N(u), uo)
     assert hf.hf_mixed_iters(ctx) > 0
+
+
+@pytest.mark.parametrize("group", [0, 2])
+def test_mixed_batched_meets_the_fp64_bar(group):
+    """Batched sims on a mixed-precision context (every stack gets its own fp32 shadow, per-system
+    fp32 PCG, then the per-system fp64 finish): each system against its own oracle run at the
+    fp64 bar, with non-zero Dirichlet faces; group 2 splits B = 3 into stacks of 2 and 1."""
+    g = synth.Grid((12, 10, 9), (0.3, 0.3, 0.2))
+    B = 3
+    base_k, base_c = synth.random_fields(g, seed=31)
+    ks = np.stack([base_k * synth.lognormal_perturbation(g.n_elems, seed=40 + j) for j in range(B)])
+    bits = (1 << synth.FACE_XM) | (1 << synth.FACE_ZP)
+    vals = [0.5, 0, 0, 0, 0, -0.25]
+    ctx = hf.hf_create(g, 0)
+    hf.hf_set_mixed(ctx, 1, 1e-6)
+    if group:
+        hf.hf_set_tuning(ctx, "batch_group", group)
+    hf.hf_set_coefficients(ctx, T(base_k), T(base_c))
+    hf.hf_set_dirichlet_faces(ctx, bits, vals)
+    F = torch.empty(g.n_nodes, dtype=torch.float64, device=DEV)
+    hf.hf_face_load(ctx, synth.FACE_ZM, 1.0, None, F)
+    u0 = np.zeros((B, g.n_nodes))
+    ub = T(u0.ravel())
+    stats = hf.hf_simulate_batched(ctx, B, T(ks.ravel()), None, 0.5, 0.05, 6, F, ub, 0, None)
+    ub = N(ub).reshape(B, -1)
+    for j in range(B):
+        o = oracle.Oracle(g, ks[j], base_c)
+        o.set_dirichlet(bits, tuple(vals))
+        uo, _, _, _ = o.simulate(0.5, 0.05, 6, o.face_load(synth.FACE_ZM, 1.0), u0[j])
+        assert rel(ub[j], uo) <= 1e-10, (j, rel(ub[j], uo))
+        assert stats[j]["steps_done"] == 6 and stats[j]["first_failed_step"] == -1
