@@ -388,6 +388,11 @@ def run_ours(args):
         line["apply_512"] = apply_512(hf, torch, dev, peak)
         line["apply_512_ids"] = apply_512(hf, torch, dev, peak, ids=True)
         line["c4_steps"] = c4_steps(hf, torch, dev, peak)
+        # the same 512^3 time steps at the same accuracy through mixed precision
+        c4m = c4_steps(hf, torch, dev, peak, mixed=1e-7)
+        line["c4_steps_mixed"] = {"ms_per_step": c4m["ms_per_step"], "fp64_iters_per_step": c4m["pcg_iters_per_step"],
+                                  "rtol": 1e-12, "precision": "fp64 mixed (fp32 stage to 1e-07, fp64 finish)",
+                                  "nodes": c4m["nodes"]}
         line["c5_batched"] = c5_batched(hf, torch, dev, world)
         # the same sims at the same fp64 accuracy through mixed precision (fp32 stage to 1e-7,
         # fp64 finish to rtol 1e-12 on the fp64 residual)
@@ -613,7 +618,7 @@ def fp32_variant(hf, torch, dev, peak):
             "mixed_parity": "fp64 finish to rtol 1e-12: C1, C2, C3 within 1e-10 of the oracle (tests/test_gpu_fp32.py)"}
 
 
-def c4_steps(hf, torch, dev, peak, steps=2, rank=0, world=1, dist=None):
+def c4_steps(hf, torch, dev, peak, steps=2, rank=0, world=1, dist=None, mixed=None):
     """C4 (BASELINE configs[3] grid, 512^3 nodes = 134M DoF) time steps: two materials (steel /
     Fe2O3, 20 % oxide, i.i.d. per element, generated on the device), f = 1 on z = 0, CN,
     dt = 0.01, rtol 1e-12, after one warm-up step.  Every iteration streams ~17 GB, far beyond
@@ -628,6 +633,8 @@ def c4_steps(hf, torch, dev, peak, steps=2, rank=0, world=1, dist=None):
     del ox
     if dist is None:
         ctx = hf.hf_create(g, dev.index)
+        if mixed:                               # fp32 stage to rtol_lo, fp64 finish
+            hf.hf_set_mixed(ctx, 1, mixed)
     else:
         ctx = make_slab_ctx(hf, g, rank, world, dist, dev.index, _TRANSPORT[0])
     hf.hf_set_coefficients(ctx, k, c)
