@@ -690,11 +690,13 @@ def test_pdl_edges_do_not_change_results():
 
 
 @pytest.mark.slow
-def test_c4_time_step_properties():
-    """C4 (512^3 nodes, 134M DoF) in the configuration bench.py's c4_steps times: one backward-
-    free CN step from u0 = 0 must leave a true residual ||dt F - A u1|| <= 1e-10 ||dt F|| (the
-    solve met rtol 1e-12 on the recurrence residual; Alg. 1 replaces it every 50 iterations), and
-    the stiffness part must carry no heat: sum(A u1) = sum(M u1) (K 1 = 0, K symmetric)."""
+@pytest.mark.parametrize("mixed", [None, 1e-7])
+def test_c4_time_step_properties(mixed):
+    """C4 (512^3 nodes, 134M DoF) in the configuration bench.py's c4_steps / c4_steps_mixed
+    times: one backward-free CN step from u0 = 0 must leave a true residual ||dt F - A u1|| <=
+    1e-10 ||dt F|| (the solve met rtol 1e-12 on the recurrence residual; Alg. 1 replaces it every
+    50 iterations; mixed: the fp64 finish after the fp32 stage), and the stiffness part must
+    carry no heat: sum(A u1) = sum(M u1) (K 1 = 0, K symmetric)."""
     g = synth.c4_grid()
     gen = torch.Generator(device=DEV).manual_seed(3)
     ox = torch.rand(g.n_elems, device=DEV, generator=gen) < 0.2
@@ -702,6 +704,8 @@ def test_c4_time_step_properties():
     c = torch.where(ox, synth.OXIDE[0], synth.STEEL[0]).to(torch.float64)
     del ox
     ctx = hf.hf_create(g, 0)
+    if mixed:
+        hf.hf_set_mixed(ctx, 1, mixed)
     hf.hf_set_coefficients(ctx, k, c)
     del k, c
     torch.cuda.empty_cache()
