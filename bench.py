@@ -377,10 +377,12 @@ def run_ours(args):
         a512 = apply_512_slabs(hf, torch, dev, peak, rank, world, dist)
         c4s = c4_steps(hf, torch, dev, peak, rank=rank, world=world, dist=dist)
         c5r = c5_batched(hf, torch, dev, world, rank=rank, dist=dist)
+        c5m = c5_batched(hf, torch, dev, world, rank=rank, dist=dist, mixed=1e-7)   # same fp64 bar
         if rank == 0:
             line["apply_512_slabs"] = a512
             line["c4_steps_slabs"] = c4s
             line["c5_batched_replicas"] = c5r
+            line["c5_batched_replicas_mixed"] = c5m
     if world == 1 and not slab:
         line["c3_other_coef"] = variant_c3(hf, torch, dev, 64, p.rtol, coef="pairs" if use_ids else "ids")
         # the on-chip PCG (opt-in): one cooperative launch per time step
