@@ -137,8 +137,11 @@ template <> struct Vec2<float> { using type = float2; };
 // stencil streams one uint8 id per element instead of a 16-B (k, c) pair and looks the
 // element's z-butterfly coefficients up in a per-CTA shared-memory table
 enum { EL_Q1 = 0, EL_DENSE = 1, EL_TETV = 2, EL_Q1P = 3 };
+// z-plane loop of the Q1 kernels unrolled by 2: the loop-carried face transforms and centre values alternate
+// between two register sets instead of being copied every plane (8.6 % of kernel A's executed
+// instructions were such moves); C3 22.84 vs 23.19 us per PCG iteration (R = 2 tiles only, see PU)
 #ifndef HF_PLANE_UNROLL
-#define HF_PLANE_UNROLL 1
+#define HF_PLANE_UNROLL 2
 #endif
 constexpr int kPlaneUnroll = HF_PLANE_UNROLL;   // unroll of the stencil's z-plane loop
 constexpr int PAL_MAX = 64;        // material table entries; entry 0 = (0, 0) (outside the domain)
@@ -1411,7 +1414,11 @@ k_stencil(const __grid_constant__ StencilArgs a)
         PK0[r].x = PK0[r].y = PK1[r].x = PK1[r].y = Real(0);
     }
 
-#pragma unroll kPlaneUnroll
+    // R = 2 Q1 kernels without the peer protocol only (< 16M nodes, latency-bound): the tet and
+    // slab variants would spill, and at R = 4 (512^3) the unrolled apply ran 9 % slower (0.805 vs
+    // 0.739 ms; with material ids 0.780 vs 0.613)
+    constexpr int PU = (R == 2 && (EL == EL_Q1 || EL == EL_Q1P) && !PEER) ? kPlaneUnroll : 1;
+#pragma unroll PU
     for (int it = 0; it < nplanes; ++it) {
         const int p = zb - 1 + it;
         const int st = it % NS;
