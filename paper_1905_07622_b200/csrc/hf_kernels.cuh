@@ -1414,10 +1414,11 @@ k_stencil(const __grid_constant__ StencilArgs a)
         PK0[r].x = PK0[r].y = PK1[r].x = PK1[r].y = Real(0);
     }
 
-    // R = 2 Q1 kernels without the peer protocol only (< 16M nodes, latency-bound): the tet and
-    // slab variants would spill, and at R = 4 (512^3) the unrolled apply ran 9 % slower (0.805 vs
-    // 0.739 ms; with material ids 0.780 vs 0.613)
-    constexpr int PU = (R == 2 && (EL == EL_Q1 || EL == EL_Q1P) && !PEER) ? kPlaneUnroll : 1;
+    // Q1 kernels without the peer protocol, at R = 2 (< 16M nodes, latency-bound) and PCG kernel
+    // A at R = 4 (512^3: 2.512 vs 2.550 ms per PCG iteration): the tet and slab variants would
+    // spill, and the unrolled R = 4 apply ran 9 % slower (0.805 vs 0.739 ms; with material ids
+    // 0.780 vs 0.613)
+    constexpr int PU = ((R == 2 || EP == EP_CGA) && (EL == EL_Q1 || EL == EL_Q1P) && !PEER) ? kPlaneUnroll : 1;
 #pragma unroll PU
     for (int it = 0; it < nplanes; ++it) {
         const int p = zb - 1 + it;
