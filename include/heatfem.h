@@ -320,6 +320,12 @@ hf_status hf_profile_read(hf_ctx *ctx, double ms[5], int64_t n[5]);
  * hf_cg / hf_simulate* call resets it).  Errors: HF_E_STATE (no previous simulation). */
 hf_status hf_time_kernel_a(hf_ctx *ctx, int32_t reps, double *ms_per_launch);
 
+/* The same kernel A launch replayed as a CUDA graph of `reps` nodes joined by the PCG loop
+ * body's programmatic edges (each launch's prologue overlaps the previous one's tail, as behind
+ * kernel B in the loop); ms per launch from one timed graph launch after a warm-up launch.
+ * Errors: HF_E_ARG, HF_E_STATE (no previous simulation), HF_E_CUDA. */
+hf_status hf_time_kernel_a_graph(hf_ctx *ctx, int32_t reps, double *ms_per_launch);
+
 /* Loop driver: 0 = CUDA graph with device-side WHILE loop (default), 1 = host loop.
  * Profiling (hf_profile) and the NCCL slab transport always use the host loop. */
 hf_status hf_set_driver(hf_ctx *ctx, int32_t driver);

@@ -84,6 +84,7 @@ _SIGS = {
     "hf_set_resident": (_i32, [_vp, _i32]),
     "hf_set_cg_variant": (_i32, [_vp, _i32]),
     "hf_set_tuning": (_i32, [_vp, C.c_char_p, C.c_int64]),
+    "hf_time_kernel_a_graph": (_i32, [_vp, _i32, _P(C.c_double)]),
     "hf_get_tuning": (_i32, [_vp, C.c_char_p, _P(C.c_int64)]),
     "hf_cg_variant": (_i32, [_vp, _P(C.c_int32)]),
     "hf_set_mixed": (_i32, [_vp, _i32, _d]),
@@ -508,6 +509,13 @@ def hf_time_kernel_a(ctx: Context, reps: int = 200) -> float:
     """ms per launch of PCG kernel A replayed back to back (instrumentation, see heatfem.h)."""
     ms = C.c_double()
     _check(_lib.hf_time_kernel_a(ctx.ptr, reps, C.byref(ms)))
+    return ms.value
+
+
+def hf_time_kernel_a_graph(ctx: Context, reps: int = 200) -> float:
+    """ms per launch of PCG kernel A replayed as a graph chain with the loop's programmatic edges."""
+    ms = C.c_double()
+    _check(_lib.hf_time_kernel_a_graph(ctx.ptr, reps, C.byref(ms)))
     return ms.value
 
 

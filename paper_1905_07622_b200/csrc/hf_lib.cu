@@ -3302,6 +3302,69 @@ hf_status hf_time_kernel_a(hf_ctx *c, int32_t reps, double *ms_per_launch)
     return HF_OK;
 }
 
+// Kernel A replayed as a CUDA graph of `reps` kernel-A nodes joined by the programmatic edges of
+// the PCG loop body (each launch's prologue overlaps the previous launch's tail, as behind
+// kernel B in the loop), timed as one graph launch after a warm-up launch.
+hf_status hf_time_kernel_a_graph(hf_ctx *c, int32_t reps, double *ms_per_launch)
+{
+    if (!c || reps < 1 || !ms_per_launch) return fail(HF_E_ARG, "hf_time_kernel_a_graph: bad argument");
+    if (!(c->last_aK > 0.0)) return fail(HF_E_STATE, "hf_time_kernel_a_graph: no previous simulation");
+    CUCK(cudaSetDevice(c->device));
+    Sys &s = c->sys0;
+    hf_cg_opts o = resolved(c, {1e-12, 10000, -1});
+    o.max_iter = 1 << 30;                       // every launch runs (no stop test)
+    o.rtol = 0.0;
+    HFCK(set_solver_opts(c, s, o));
+    StencilArgs ia = base_args(c, c->last_aK, 1.0);
+    ia.invd = s.invd;
+    ia.bvec = s.b;
+    ia.out0 = s.r;
+    ia.out_s = s.s;
+    ia.first = 1;
+    ia.rot_role = ROT_INIT;
+    for (int i = 0; i < 3; i++) ia.ring[i] = s.U[i];
+    ia.sy = make_sync(c, s, -1, 1);
+    ia.zs0 = c->own_lo;
+    ia.zs1 = c->own_hi;
+    Launch init;
+    HFCK(stencil_launch(c, LD_X0, EP_RESID_INIT, true, s.maps, ia, 2, &init));
+    CgLaunches L;
+    HFCK(cg_launches(c, s, c->last_aK, 1.0, nullptr, s.maps, &L));
+    const bool prof = c->prof;
+    c->prof = false;
+    HFCK(run(c, init, s.stream));
+    cudaGraph_t g;
+    CUCK(cudaGraphCreate(&g, 0));
+    cudaGraphNode_t prev = nullptr, n;
+    for (int i = 0; i < reps; i++) {
+        if (prev && c->pdl) {
+            HFCK(add_node(g, L.A, nullptr, &n));
+            HFCK(add_pdl_edge(g, prev, n));
+        } else
+            HFCK(add_node(g, L.A, prev ? &prev : nullptr, &n));
+        prev = n;
+    }
+    cudaGraphExec_t ge;
+    CUCK(cudaGraphInstantiate(&ge, g, 0));
+    CUCK(cudaGraphLaunch(ge, s.stream));            // warm
+    cudaEvent_t e0, e1;
+    CUCK(cudaEventCreate(&e0));
+    CUCK(cudaEventCreate(&e1));
+    CUCK(cudaEventRecord(e0, s.stream));
+    CUCK(cudaGraphLaunch(ge, s.stream));
+    CUCK(cudaEventRecord(e1, s.stream));
+    CUCK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    c->prof = prof;
+    *ms_per_launch = ms / reps;
+    return HF_OK;
+}
+
 #ifdef HF_TRACE
 // debug builds only (not part of the ABI): kernel-A timestamps of the last traced launch
 hf_status hf_trace_read(unsigned long long *out, int32_t nblocks)

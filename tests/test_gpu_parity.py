@@ -270,6 +270,8 @@ def test_time_kernel_a_replay_then_simulate():
         hf.hf_time_kernel_a(make_ctx(p.grid, p.k, p.c), 5)      # no simulation yet: HF_E_STATE
     ms = hf.hf_time_kernel_a(ctx, 20)
     assert 0.0 < ms < 10.0
+    msg = hf.hf_time_kernel_a_graph(ctx, 20)             # graph chain with programmatic edges
+    assert 0.0 < msg < 10.0
     F = torch.empty(p.grid.n_nodes, dtype=torch.float64, device=DEV)
     hf.hf_face_load(ctx, p.flux_face, p.flux_const, p.beam, F)
     u = T(p.u0)
